@@ -1,0 +1,176 @@
+/*
+ * nimbus_cop.h -- C ABI of libnimbus_cop.so, the B200 (sm_100a) hot path of
+ * Nimbus' client-side outer-product (COP) homomorphic matmul
+ * (arXiv 2411.15707, Alg. 1).
+ *
+ * Citations: PAPER.md:<line> = /root/reference/PAPER.md (section / algorithm);
+ * SURVEY.md §8(c) #<n> = the reading taken where the paper is silent or
+ * ambiguous (repeated in DESIGN.md "Readings").
+ *
+ * Conventions for every entry point
+ *  - Return value: nimbus_status, 0 = NIMBUS_OK.  Shape / parameter / noise
+ *    budget errors are detected on the host BEFORE any launch, and nothing is
+ *    written.  Asynchronous CUDA faults surface as NIMBUS_ECUDA on the next
+ *    call that synchronises; nimbus_last_error() has the text.
+ *  - d_* pointers are DEVICE pointers owned by the caller (e.g. torch tensor
+ *    data_ptr()), contiguous, 16-byte aligned, with the sizes annotated.
+ *    h_* pointers are HOST pointers (pinned memory recommended).
+ *  - stream is a cudaStream_t (NULL = legacy default stream).  All device work
+ *    is enqueued on it; functions return without synchronising unless noted.
+ *  - Residues are little-endian uint32 in [0, p_i).  Prime order is
+ *    p_0 > p_1 > ....
+ *  - Opaque handles are allocated by the library and released by *_destroy.
+ *    A context is not thread-safe; distinct contexts are independent.
+ */
+#ifndef NIMBUS_COP_H
+#define NIMBUS_COP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NIMBUS_OK = 0,
+    NIMBUS_EINVAL = -1,  /* null pointer, zero dimension, unsupported N/L/ell */
+    NIMBUS_ESHAPE = -2,  /* n > N (PAPER.md:232 assumes n < N), dims mismatch, buffer too small */
+    NIMBUS_ERANGE = -3,  /* an input entry >= t (only when NIMBUS_FLAG_CHECK_RANGE) */
+    NIMBUS_ENOISE = -4,  /* parameters fail the worst-case decryption bound */
+    NIMBUS_ECUDA = -5,   /* CUDA runtime error, text in nimbus_last_error */
+    NIMBUS_ENOMEM = -6,  /* device allocation failed */
+    NIMBUS_EARCH = -8    /* device is not sm_100 (B200) */
+} nimbus_status;
+
+enum { NIMBUS_IMPL_TCGEN05 = 0, NIMBUS_IMPL_CUDACORE = 1 };
+enum { NIMBUS_FLAG_CHECK_RANGE = 1 };
+
+/* RLWE / workload parameters (App. B.1 {N, q, t}).
+ *  N      ring degree, power of two, 64 <= N <= 8192
+ *  L      number of 31-bit NTT primes in q (1..4); q = p_0 ... p_{L-1}
+ *  ell    plaintext bits, t = 2^ell, 1 <= ell <= 32
+ *  L_out  limbs kept by the mod-switch of the output (1..L)
+ *  impl   NIMBUS_IMPL_TCGEN05 (tcgen05 int8 tensor cores) or
+ *         NIMBUS_IMPL_CUDACORE (lazy-reduction CUDA-core ablation)
+ *  flags  NIMBUS_FLAG_* */
+typedef struct {
+    uint32_t N, L, ell, L_out, impl, flags;
+} nimbus_params;
+
+typedef struct nimbus_ctx nimbus_ctx;
+typedef struct nimbus_sk nimbus_sk;
+typedef struct nimbus_encw nimbus_encw;
+
+/* Context: validates params, derives the primes (the L largest p < 2^31 with
+ * p = 1 mod 2N), uploads NTT twiddles and RNS constants to
+ * `device`.  Fails with NIMBUS_EARCH off sm_100. */
+nimbus_status nimbus_ctx_create(const nimbus_params* params, int device, nimbus_ctx** out);
+void nimbus_ctx_destroy(nimbus_ctx* ctx);
+/* Writes the L primes to out_primes[L] (host). */
+nimbus_status nimbus_ctx_primes(const nimbus_ctx* ctx, uint32_t* out_primes);
+/* Last error text of this context ("" if none).  Valid until the next call. */
+const char* nimbus_last_error(const nimbus_ctx* ctx);
+/* Blocks until `stream` drains; reports async faults (NIMBUS_ECUDA) and, if
+ * range checking is on, NIMBUS_ERANGE for any input seen >= t since the last call. */
+nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream);
+
+/* ---------------------------------------------------------------- setup ---- */
+/* KeyGen: ternary secret s in {-1,0,1}^N (SURVEY.md §8(c) #7,
+ * symmetric key per #8), drawn from the PRG with domain 1,
+ * kept on the device together with its per-limb NTT form. */
+nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus_sk** out);
+void nimbus_sk_destroy(nimbus_sk* sk);
+/* Copies s (N int8 values in {-1,0,1}) to d_s. */
+nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream);
+
+/* Alg. 1 step 1, server side: row-wise encode each weight row
+ * (Eq. 2: w_hat[j] = W[beta][j] for j < n, 0 beyond) and
+ * encrypt it: b = a*s + Emb_q(w_hat) + e mod p_i, a uniform mod p_i (domain 2),
+ * e CBD(21) (domain 3), Emb_q(w) = floor((q w + t/2)/t) (SURVEY.md §8(c) #4,#6).
+ *  d_W   m x n uint32, row-major, entries < t
+ * The handle keeps Enc(W) resident in HBM in the kernel layout (DESIGN.md
+ * "Data layout").  Errors: n > N -> ESHAPE; m or n == 0 -> EINVAL;
+ * noise bound violated for this (m, n) -> ENOISE. */
+nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W,
+                                     uint32_t m, uint32_t n, uint64_t seed, void* stream,
+                                     nimbus_encw** out);
+void nimbus_encw_destroy(nimbus_encw* encw);
+/* Bytes of device memory held by the handle. */
+size_t nimbus_encw_bytes(const nimbus_encw* encw);
+/* Canonical layout export / import: d_buf is m x 2 x L x N uint32,
+ * [beta][comp b=0,a=1][limb][j] (the store format). */
+nimbus_status nimbus_encw_export(const nimbus_encw* encw, uint32_t* d_out, void* stream);
+nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t m, uint32_t n,
+                                 void* stream, nimbus_encw** out);
+
+/* ---------------------------------------------------------------- online --- */
+/* Number of packed output ciphertexts per query, ceil(k_q / floor(N/n))
+ * (Table 1, "Pad with zeros"). */
+nimbus_status nimbus_cop_out_count(const nimbus_ctx* ctx, uint32_t k_per_query, uint32_t n,
+                                   uint32_t* n_cts);
+/* Device workspace bytes needed by nimbus_cop_matmul / nimbus_cop_accumulate
+ * for k = n_queries * k_per_query rows. */
+nimbus_status nimbus_cop_workspace_size(const nimbus_ctx* ctx, const nimbus_encw* encw, uint32_t k,
+                                        size_t* bytes);
+
+/* Alg. 1 steps 2-4, client side, the timed hot path:
+ *   step 2  c[alpha] = sum_beta X[alpha][beta] (x) Enc(W_beta)
+ *   step 3  ct~[theta] = sum_r RShift(c[theta R + r], r n), R = floor(N/n)
+ *           (stride n per SURVEY.md §8(c) #11)
+ *   mod-switch to L_out limbs, iterated round(c/p_last)
+ *   step 4  b -= Emb_{q'}(r_theta), r uniform in Z_t for all N slots (domain 6,
+ *           index theta_global*N + J)
+ *  d_X     k x m uint32 (k = n_queries * k_per_query; query-major), entries < t
+ *          (unsigned representative)
+ *  d_cts   n_queries x n_cts x 2 x L_out x N uint32  [query][theta][comp][limb][J]
+ *  d_R     k x n uint32: the client's output share Y_c = R
+ *  d_ws    workspace of at least nimbus_cop_workspace_size bytes (16-byte aligned)
+ * No allocation, no host synchronisation. */
+nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* d_X,
+                                uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
+                                uint32_t* d_cts, uint32_t* d_R, void* d_ws, size_t ws_bytes,
+                                void* stream);
+
+/* Same computation with HOST buffers: copies h_X in, runs nimbus_cop_matmul,
+ * copies h_cts and h_R out, and synchronises `stream` before returning. */
+nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* h_X,
+                                     uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
+                                     uint32_t* h_cts, uint32_t* h_R, void* d_ws, size_t ws_bytes,
+                                     void* stream);
+
+/* Step 2 alone (verification of the contraction): d_C is k x 2 x L x N uint32,
+ * [alpha][comp][limb][j], the unpacked ciphertexts c[alpha] reduced mod p_i. */
+nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* d_X,
+                                    uint32_t k, uint32_t* d_C, void* d_ws, size_t ws_bytes,
+                                    void* stream);
+
+/* Steps 3-4 alone on an unpacked d_C (k x 2 x L x N, as produced above). */
+nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t k_per_query,
+                              uint32_t n_queries, uint32_t n, uint64_t mask_seed, uint32_t* d_cts,
+                              uint32_t* d_R, void* stream);
+
+/* Server step 5 decryption: u = b - a*s mod q'
+ * (NTT), m = floor((2 t u + q')/(2 q')) mod t, unpacked
+ * Z[alpha][j] = m_theta[(alpha mod R) n + j]; Z = (X.W - R) mod t.
+ *  d_cts  as written by nimbus_cop_matmul;  d_Z  k x n uint32.
+ *  d_M    optional (may be NULL): n_queries x n_cts x N full decrypted slots. */
+nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts,
+                             uint32_t k_per_query, uint32_t n_queries, uint32_t n, uint32_t* d_Z,
+                             uint32_t* d_M, void* stream);
+
+/* ---------------------------------------------------------- test helpers --- */
+/* PRG words word(seed, dom, start + i), i < count. */
+nimbus_status nimbus_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count,
+                               uint64_t* d_out, void* stream);
+/* Negacyclic products c = a*b mod (X^N+1, p_i) through the library's NTT
+ * (PAPER.md:606, 180).  d_a, d_b, d_c: count x L x N uint32. */
+nimbus_status nimbus_negacyclic_mul(nimbus_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b,
+                                    uint32_t count, uint32_t* d_c, void* stream);
+/* Number of library kernels launched through this context since creation. */
+uint64_t nimbus_launch_count(const nimbus_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NIMBUS_COP_H */

@@ -1,0 +1,420 @@
+// capi.cu -- the C ABI of libnimbus_cop.so (include/nimbus_cop.h): parameter
+// validation, RNS constant / twiddle derivation, handle management, and the
+// launch sequence of each entry point.  All arithmetic runs in the kernels.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.h"
+
+using namespace nimbus;
+
+// ---------------------------------------------------------------- host number theory
+static uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t p) { return (uint64_t)((u128)a * b % p); }
+static uint64_t h_pow(uint64_t a, uint64_t e, uint64_t p) {
+    uint64_t r = 1 % p;
+    a %= p;
+    while (e) { if (e & 1) r = h_mulmod(r, a, p); a = h_mulmod(a, a, p); e >>= 1; }
+    return r;
+}
+static uint64_t h_inv(uint64_t a, uint64_t p) { return h_pow(a % p, p - 2, p); }
+
+// deterministic Miller-Rabin for n < 2^32 (bases 2, 3, 5, 7)
+static bool h_is_prime(uint64_t n) {
+    if (n < 2) return false;
+    for (uint64_t sp : {2ull, 3ull, 5ull, 7ull}) if (n % sp == 0) return n == sp;
+    uint64_t d = n - 1; int s = 0;
+    while ((d & 1) == 0) { d >>= 1; s++; }
+    for (uint64_t a : {2ull, 3ull, 5ull, 7ull}) {
+        uint64_t x = h_pow(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int r = 1; r < s; r++) { x = h_mulmod(x, x, n); if (x == n - 1) { comp = false; break; } }
+        if (comp) return false;
+    }
+    return true;
+}
+
+static uint32_t bitrev(uint32_t x, uint32_t bits) {
+    uint32_t r = 0;
+    for (uint32_t i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+
+static nimbus_status set_err(nimbus_ctx* c, nimbus_status st, const char* msg) {
+    if (c) c->err = msg;
+    return st;
+}
+static nimbus_status cuda_err(nimbus_ctx* c, cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return NIMBUS_OK;
+    if (c) { c->err = std::string(where) + ": " + cudaGetErrorString(e); }
+    return e == cudaErrorMemoryAllocation ? NIMBUS_ENOMEM : NIMBUS_ECUDA;
+}
+#define CK(call, where) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) return cuda_err(ctx, e_, where); } while (0)
+
+static inline uint64_t ncols(const nimbus_ctx* c) { return 2ull * c->rns.L * c->rns.N; }
+
+// Worst-case decryption bound (SURVEY.md §8(c) "Worst-case noise guarantee"),
+// in integer upper bounds on 2|v|:  fresh+COP+packing 2v <= R m (t-1)(2 eta + 1);
+// each limb drop v -> v/p + (1+N)/2; the mask adds 1/2.  Requires 2|v| t < q.
+static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff) {
+    const uint32_t ell = c->rns.ell, N = c->rns.N;
+    const u128 t = (u128)1 << ell;
+    u128 B = (u128)R_eff * m * (t - 1) * 43u;  // 2 eta + 1 = 43 for CBD(21)
+    if (B * t >= c->q) return false;
+    for (uint32_t l = c->rns.L; l > c->rns.L_out; l--) {
+        const uint64_t p = c->rns.p[l - 1];
+        B = (B + p - 1) / p + 1 + N;
+    }
+    B += 1;
+    return B * t < c->qout;
+}
+
+extern "C" {
+
+nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx** out) {
+    if (!prm || !out) return NIMBUS_EINVAL;
+    *out = nullptr;
+    const uint32_t N = prm->N, L = prm->L, ell = prm->ell, Lo = prm->L_out;
+    if (N < 64 || N > 8192 || (N & (N - 1))) return NIMBUS_EINVAL;
+    if (L < 1 || L > NIMBUS_MAXL || Lo < 1 || Lo > L || ell < 1 || ell > 32) return NIMBUS_EINVAL;
+    if (prm->impl > 1) return NIMBUS_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return NIMBUS_ECUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return NIMBUS_ECUDA;
+    if (prop.major != 10 || prop.minor != 0) return NIMBUS_EARCH;
+
+    nimbus_ctx* ctx = new (std::nothrow) nimbus_ctx();
+    if (!ctx) return NIMBUS_ENOMEM;
+    ctx->prm = *prm;
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    Rns& R = ctx->rns;
+    R.N = N; R.L = L; R.L_out = Lo; R.ell = ell;
+    R.logN = 0; while ((1u << R.logN) < N) R.logN++;
+    // primes: the L largest p < 2^31 with p = 1 mod 2N, descending
+    {
+        const uint64_t step = 2ull * N;
+        uint64_t cnd = ((((1ull << 31) - 2)) / step) * step + 1;
+        uint32_t f = 0;
+        while (f < L && cnd > (1ull << 30)) { if (h_is_prime(cnd)) R.p[f++] = (uint32_t)cnd; cnd -= step; }
+        if (f < L) { delete ctx; return NIMBUS_EINVAL; }
+    }
+    ctx->q = 1;
+    for (uint32_t i = 0; i < L; i++) ctx->q *= R.p[i];
+    ctx->qout = 1;
+    for (uint32_t i = 0; i < Lo; i++) ctx->qout *= R.p[i];
+    // decrypt arithmetic: 2 t u + q' must fit in 127 bits
+    {
+        int qb = 0; u128 x = ctx->qout; while (x) { qb++; x >>= 1; }
+        if (qb + (int)ell + 2 > 127) { delete ctx; return NIMBUS_EINVAL; }
+    }
+    const u128 t = (u128)1 << ell;
+    R.q_mod_t = (uint32_t)(ctx->q % t);
+    R.qout_mod_t = (uint32_t)(ctx->qout % t);
+    for (uint32_t i = 0; i < L; i++) {
+        const uint64_t p = R.p[i];
+        R.mu[i] = (uint64_t)((((u128)1) << 64) / p);
+        R.t_inv[i] = (uint32_t)h_inv((uint64_t)(t % p), p);
+        for (uint32_t s = 0; s < 8; s++) R.pow8[i][s] = (uint32_t)h_pow(2, 8 * s, p);
+        for (uint32_t l = 0; l < L; l++) R.inv_p[l][i] = (l == i) ? 0 : (uint32_t)h_inv(R.p[l], p);
+        R.ninv[i] = (uint32_t)h_inv(N, p);
+        R.ninv_sh[i] = (uint32_t)(((uint64_t)R.ninv[i] << 32) / p);
+    }
+    // twiddles: psi a primitive 2N-th root (psi^N = -1), bit-reversed powers
+    std::vector<uint32_t> tw((size_t)L * 4 * N);
+    for (uint32_t i = 0; i < L; i++) {
+        const uint64_t p = R.p[i];
+        uint64_t psi = 0;
+        for (uint64_t x = 3; x < p; x++) {
+            uint64_t c = h_pow(x, (p - 1) / (2ull * N), p);
+            if (h_pow(c, N, p) == p - 1) { psi = c; break; }
+        }
+        const uint64_t ipsi = h_inv(psi, p);
+        uint32_t* b = tw.data() + (size_t)i * 4 * N;
+        for (uint32_t kk = 0; kk < N; kk++) {
+            const uint32_t e = bitrev(kk, R.logN);
+            const uint32_t w = (uint32_t)h_pow(psi, e, p), iw = (uint32_t)h_pow(ipsi, e, p);
+            b[kk] = w;
+            b[N + kk] = (uint32_t)(((uint64_t)w << 32) / p);
+            b[2 * N + kk] = iw;
+            b[3 * N + kk] = (uint32_t)(((uint64_t)iw << 32) / p);
+        }
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_tw, tw.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_flag, 16);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_flag, 0, 16);
+    if (e != cudaSuccess) { nimbus_ctx_destroy(ctx); return e == cudaErrorMemoryAllocation ? NIMBUS_ENOMEM : NIMBUS_ECUDA; }
+    *out = ctx;
+    return NIMBUS_OK;
+}
+
+void nimbus_ctx_destroy(nimbus_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->d_tw) cudaFree(ctx->d_tw);
+    if (ctx->d_flag) cudaFree(ctx->d_flag);
+    delete ctx;
+}
+
+nimbus_status nimbus_ctx_primes(const nimbus_ctx* ctx, uint32_t* out) {
+    if (!ctx || !out) return NIMBUS_EINVAL;
+    for (uint32_t i = 0; i < ctx->rns.L; i++) out[i] = ctx->rns.p[i];
+    return NIMBUS_OK;
+}
+
+const char* nimbus_last_error(const nimbus_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+uint64_t nimbus_launch_count(const nimbus_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
+    if (!ctx) return NIMBUS_EINVAL;
+    CK(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+    uint32_t flag = 0;
+    CK(cudaMemcpy(&flag, ctx->d_flag, 4, cudaMemcpyDeviceToHost), "sync flag");
+    if (flag) {
+        CK(cudaMemset(ctx->d_flag, 0, 4), "sync flag reset");
+        return set_err(ctx, NIMBUS_ERANGE, "an input entry was >= t");
+    }
+    return NIMBUS_OK;
+}
+
+// ---------------------------------------------------------------- keys
+nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus_sk** out) {
+    if (!ctx || !out) return NIMBUS_EINVAL;
+    *out = nullptr;
+    nimbus_sk* sk = new (std::nothrow) nimbus_sk();
+    if (!sk) return NIMBUS_ENOMEM;
+    sk->ctx = ctx;
+    const uint32_t N = ctx->rns.N, L = ctx->rns.L;
+    cudaError_t e = cudaMalloc(&sk->d_s, N);
+    if (e == cudaSuccess) e = cudaMalloc(&sk->d_s_ntt, (size_t)L * N * 4);
+    if (e == cudaSuccess) e = launch_keygen(ctx, seed, sk->d_s, sk->d_s_ntt, (cudaStream_t)stream);
+    if (e != cudaSuccess) { nimbus_sk_destroy(sk); return cuda_err(ctx, e, "keygen"); }
+    *out = sk;
+    return NIMBUS_OK;
+}
+
+void nimbus_sk_destroy(nimbus_sk* sk) {
+    if (!sk) return;
+    if (sk->d_s) cudaFree(sk->d_s);
+    if (sk->d_s_ntt) cudaFree(sk->d_s_ntt);
+    delete sk;
+}
+
+nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream) {
+    if (!sk || !d_s) return NIMBUS_EINVAL;
+    nimbus_ctx* ctx = sk->ctx;
+    CK(cudaMemcpyAsync(d_s, sk->d_s, ctx->rns.N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "sk export");
+    return NIMBUS_OK;
+}
+
+// ---------------------------------------------------------------- Enc(W)
+static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_encw** out) {
+    if (m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "m and n must be positive");
+    if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N (PAPER.md:232 needs n < N)");
+    if (m > 8192) return set_err(ctx, NIMBUS_ESHAPE, "m > 8192 exceeds the int32 slice-accumulator bound");
+    if (!noise_ok(ctx, m, 1)) return set_err(ctx, NIMBUS_ENOISE, "parameters fail the decryption noise bound");
+    nimbus_encw* w = new (std::nothrow) nimbus_encw();
+    if (!w) return NIMBUS_ENOMEM;
+    w->ctx = ctx; w->m = m; w->n = n; w->KB = (m + kBK - 1) / kBK;
+    w->bytes = (size_t)w->KB * kBK * ncols(ctx) * 4;
+    cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
+    if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "encw alloc"); }
+    *out = w;
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint32_t m,
+                                     uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
+    if (!ctx || !sk || !d_W || !out || sk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    *out = nullptr;
+    nimbus_encw* w = nullptr;
+    nimbus_status st = new_encw(ctx, m, n, &w);
+    if (st != NIMBUS_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t* canon = nullptr;
+    cudaError_t e = cudaMallocAsync(&canon, (size_t)m * ncols(ctx) * 4, s);
+    if (e == cudaSuccess) e = launch_encrypt(ctx, sk->d_s_ntt, d_W, m, n, seed, canon, s);
+    if (e == cudaSuccess) e = launch_tile_encw(ctx, canon, m, w->KB, w->d_Et, s);
+    if (canon) cudaFreeAsync(canon, s);
+    if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encrypt_weights"); }
+    *out = w;
+    return NIMBUS_OK;
+}
+
+void nimbus_encw_destroy(nimbus_encw* w) {
+    if (!w) return;
+    if (w->d_Et) cudaFree(w->d_Et);
+    delete w;
+}
+
+size_t nimbus_encw_bytes(const nimbus_encw* w) { return w ? w->bytes : 0; }
+
+nimbus_status nimbus_encw_export(const nimbus_encw* w, uint32_t* d_out, void* stream) {
+    if (!w || !d_out) return NIMBUS_EINVAL;
+    nimbus_ctx* ctx = w->ctx;
+    CK(launch_untile_encw(ctx, w->d_Et, w->m, w->KB, d_out, (cudaStream_t)stream), "encw export");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t m, uint32_t n, void* stream,
+                                 nimbus_encw** out) {
+    if (!ctx || !d_in || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    *out = nullptr;
+    nimbus_encw* w = nullptr;
+    nimbus_status st = new_encw(ctx, m, n, &w);
+    if (st != NIMBUS_OK) return st;
+    cudaError_t e = launch_tile_encw(ctx, d_in, m, w->KB, w->d_Et, (cudaStream_t)stream);
+    if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encw import"); }
+    *out = w;
+    return NIMBUS_OK;
+}
+
+// ---------------------------------------------------------------- online path
+nimbus_status nimbus_cop_out_count(const nimbus_ctx* ctx, uint32_t kq, uint32_t n, uint32_t* n_cts) {
+    if (!ctx || !n_cts || kq == 0 || n == 0) return NIMBUS_EINVAL;
+    if (n > ctx->rns.N) return NIMBUS_ESHAPE;
+    const uint32_t R = ctx->rns.N / n;
+    *n_cts = (kq + R - 1) / R;
+    return NIMBUS_OK;
+}
+
+struct WsLayout {
+    size_t xt = 0, c = 0, stage_x = 0, stage_cts = 0, stage_r = 0, total = 0;
+};
+static WsLayout ws_layout(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t k) {
+    auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+    WsLayout L;
+    const size_t Mt = (k + kBM - 1) / kBM;
+    const size_t xt_bytes = sx_of(ctx->rns.ell) * Mt * kBM * (size_t)w->KB * kBK;
+    const size_t c_bytes = (size_t)k * ncols(ctx) * 4;
+    L.xt = 0;
+    L.c = al(xt_bytes);
+    L.stage_x = L.c + al(c_bytes);
+    L.stage_cts = L.stage_x + al((size_t)k * w->m * 4);
+    L.stage_r = L.stage_cts + al((size_t)k * 2 * ctx->rns.L_out * ctx->rns.N * 4);
+    L.total = L.stage_r + al((size_t)k * w->n * 4);
+    return L;
+}
+
+nimbus_status nimbus_cop_workspace_size(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t k, size_t* bytes) {
+    if (!ctx || !w || !bytes || k == 0) return NIMBUS_EINVAL;
+    *bytes = ws_layout(ctx, w, k).total;
+    return NIMBUS_OK;
+}
+
+static nimbus_status check_online(nimbus_ctx* ctx, const nimbus_encw* w, uint32_t kq, uint32_t nq) {
+    if (!ctx || !w || w->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "bad context / encw");
+    if (kq == 0 || nq == 0) return set_err(ctx, NIMBUS_EINVAL, "k must be positive");
+    if ((uint64_t)kq * nq > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
+    const uint32_t R = ctx->rns.N / w->n;
+    if (!noise_ok(ctx, w->m, kq < R ? kq : R)) return set_err(ctx, NIMBUS_ENOISE, "noise bound violated");
+    return NIMBUS_OK;
+}
+
+static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
+                                    uint32_t* d_C, uint8_t* ws, cudaStream_t s) {
+    if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
+        uint8_t* xt = ws + ws_layout(ctx, w, k).xt;
+        CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, xt, s), "slice X");
+        CK(launch_cop_tcgen05(ctx, w, xt, k, d_C, s), "cop tcgen05");
+    } else {
+        CK(launch_cop_cudacore(ctx, w, d_X, k, d_C, s), "cop cudacore");
+    }
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
+                                    uint32_t* d_C, void* d_ws, size_t ws_bytes, void* stream) {
+    nimbus_status st = check_online(ctx, w, k, 1);
+    if (st != NIMBUS_OK && st != NIMBUS_ENOISE) return st;
+    if (!d_X || !d_C || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
+    if (ws_bytes < ws_layout(ctx, w, k).total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    return run_accumulate(ctx, w, d_X, k, d_C, (uint8_t*)d_ws, (cudaStream_t)stream);
+}
+
+nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
+                              uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* stream) {
+    if (!ctx || !d_C || !d_cts || !d_R || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
+    CK(launch_pack(ctx, d_C, kq, nq, n, seed, d_cts, d_R, (cudaStream_t)stream), "pack");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t kq,
+                                uint32_t nq, uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+    nimbus_status st = check_online(ctx, w, kq, nq);
+    if (st != NIMBUS_OK) return st;
+    if (!d_X || !d_cts || !d_R || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
+    const uint32_t k = kq * nq;
+    const WsLayout L = ws_layout(ctx, w, k);
+    if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t* C = reinterpret_cast<uint32_t*>((uint8_t*)d_ws + L.c);
+    st = run_accumulate(ctx, w, d_X, k, C, (uint8_t*)d_ws, s);
+    if (st != NIMBUS_OK) return st;
+    CK(launch_pack(ctx, C, kq, nq, w->n, seed, d_cts, d_R, s), "pack");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* h_X, uint32_t kq,
+                                     uint32_t nq, uint64_t seed, uint32_t* h_cts, uint32_t* h_R, void* d_ws,
+                                     size_t ws_bytes, void* stream) {
+    nimbus_status st = check_online(ctx, w, kq, nq);
+    if (st != NIMBUS_OK) return st;
+    if (!h_X || !h_cts || !h_R || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
+    const uint32_t k = kq * nq;
+    const WsLayout L = ws_layout(ctx, w, k);
+    if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* ws = (uint8_t*)d_ws;
+    uint32_t* dX = reinterpret_cast<uint32_t*>(ws + L.stage_x);
+    uint32_t* dcts = reinterpret_cast<uint32_t*>(ws + L.stage_cts);
+    uint32_t* dR = reinterpret_cast<uint32_t*>(ws + L.stage_r);
+    uint32_t nct = 0;
+    nimbus_cop_out_count(ctx, kq, w->n, &nct);
+    const size_t cts_bytes = (size_t)nq * nct * 2 * ctx->rns.L_out * ctx->rns.N * 4;
+    CK(cudaMemcpyAsync(dX, h_X, (size_t)k * w->m * 4, cudaMemcpyHostToDevice, s), "h2d X");
+    st = nimbus_cop_matmul(ctx, w, dX, kq, nq, seed, dcts, dR, d_ws, ws_bytes, stream);
+    if (st != NIMBUS_OK) return st;
+    CK(cudaMemcpyAsync(h_cts, dcts, cts_bytes, cudaMemcpyDeviceToHost, s), "d2h cts");
+    CK(cudaMemcpyAsync(h_R, dR, (size_t)k * w->n * 4, cudaMemcpyDeviceToHost, s), "d2h R");
+    CK(cudaStreamSynchronize(s), "host matmul sync");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
+                             uint32_t n, uint32_t* d_Z, uint32_t* d_M, void* stream) {
+    if (!ctx || !sk || !d_cts || !d_Z || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t nct = 0;
+    nimbus_cop_out_count(ctx, kq, n, &nct);
+    uint32_t* U = nullptr;
+    CK(cudaMallocAsync(&U, (size_t)nq * nct * ctx->rns.L_out * ctx->rns.N * 4, s), "decrypt alloc");
+    cudaError_t e = launch_decrypt(ctx, sk->d_s_ntt, d_cts, nq * nct, nct, kq, n, U, d_Z, d_M, s);
+    cudaFreeAsync(U, s);
+    CK(e, "decrypt");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* d_out,
+                               void* stream) {
+    if (!d_out) return NIMBUS_EINVAL;
+    return launch_prg_words(seed, dom, start, count, d_out, (cudaStream_t)stream) == cudaSuccess ? NIMBUS_OK
+                                                                                                : NIMBUS_ECUDA;
+}
+
+nimbus_status nimbus_negacyclic_mul(nimbus_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t count,
+                                    uint32_t* c, void* stream) {
+    if (!ctx || !a || !b || !c || count == 0) return NIMBUS_EINVAL;
+    CK(launch_negacyclic_mul(ctx, a, b, count, c, (cudaStream_t)stream), "negacyclic_mul");
+    return NIMBUS_OK;
+}
+
+}  // extern "C"

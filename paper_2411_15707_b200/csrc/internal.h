@@ -1,0 +1,75 @@
+// internal.h -- host-side structures shared by the translation units of
+// libnimbus_cop.so.  Not part of the public ABI (see include/nimbus_cop.h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <cuda_runtime.h>
+
+#include "../../include/nimbus_cop.h"
+#include "common.cuh"
+
+typedef unsigned __int128 u128;
+
+// Kernel-layout geometry of Enc(W) and of the sliced X.
+constexpr uint32_t kBK = 128;      // beta (contraction) bytes per k-block = one 128-B swizzle row
+constexpr uint32_t kBNT = 64;      // coefficient columns per Enc(W) tile
+constexpr uint32_t kBM = 128;      // rows (alpha) per X tile = tcgen05 M
+constexpr uint32_t kSW = 4;        // 8-bit slices of a 31-bit residue (S_w)
+
+struct nimbus_ctx {
+    nimbus_params prm{};
+    int device = 0;
+    nimbus::Rns rns{};
+    u128 q = 0, qout = 0;
+    uint32_t* d_tw = nullptr;      // per limb 4 x N: psi_rev, psi_rev_shoup, ipsi_rev, ipsi_rev_shoup
+    uint32_t* d_flag = nullptr;    // device error flags (bit 0: input >= t)
+    std::string err;
+    uint64_t launches = 0;
+    int num_sms = 148;
+};
+
+struct nimbus_sk {
+    nimbus_ctx* ctx = nullptr;
+    int8_t* d_s = nullptr;         // N ternary coefficients
+    uint32_t* d_s_ntt = nullptr;   // L x N, NTT domain (bit-reversed order)
+};
+
+struct nimbus_encw {
+    nimbus_ctx* ctx = nullptr;
+    uint32_t m = 0, n = 0, KB = 0; // KB = ceil(m / 128) k-blocks
+    uint8_t* d_Et = nullptr;       // tiled byte planes [ct][kb][s][64][128 swizzled]
+    size_t bytes = 0;
+};
+
+// number of 8-bit slices of an ell-bit X entry (S_x)
+inline uint32_t sx_of(uint32_t ell) { return ell <= 8 ? 1 : ell <= 16 ? 2 : 4; }
+
+// ---------------------------------------------------------------- launchers
+namespace nimbus {
+// ntt.cu
+cudaError_t launch_keygen(nimbus_ctx* c, uint64_t seed, int8_t* d_s, uint32_t* d_s_ntt, cudaStream_t st);
+cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* d_W, uint32_t m,
+                           uint32_t n, uint64_t seed, uint32_t* d_encW, cudaStream_t st);
+cudaError_t launch_negacyclic_mul(nimbus_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t count,
+                                  uint32_t* out, cudaStream_t st);
+cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* cts, uint32_t nct_total,
+                           uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, uint32_t* d_Z,
+                           uint32_t* d_M, cudaStream_t st);
+cudaError_t launch_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* out,
+                             cudaStream_t st);
+// layout.cu
+cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m, uint32_t KB, uint8_t* d_Et,
+                             cudaStream_t st);
+cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t* d_canon,
+                               cudaStream_t st);
+cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB,
+                           uint8_t* d_Xt, cudaStream_t st);
+cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
+                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st);
+// cop_cc.cu
+cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
+                                uint32_t* d_C, cudaStream_t st);
+// cop_tc.cu
+cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
+                               uint32_t* d_C, cudaStream_t st);
+}  // namespace nimbus

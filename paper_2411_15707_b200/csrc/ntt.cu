@@ -1,0 +1,259 @@
+// ntt.cu -- negacyclic NTT over Z_p[X]/(X^N+1) (§3.1; used only
+// for KeyGen/Encrypt at setup and for the verification decrypt
+// "the NTT is only applied when the server decrypts"), plus the KeyGen (K1),
+// fused Encrypt-rows (K3) and Decrypt (K8) kernels.
+//
+// One CTA per (polynomial, limb); the N residues are staged in shared memory
+// and transformed in place: Cooley-Tukey forward (natural -> bit-reversed) and
+// Gentleman-Sande inverse (bit-reversed -> natural) with the negacyclic twist
+// psi^i folded into the twiddles, Shoup modular multiplication.
+#include "internal.h"
+
+namespace nimbus {
+
+// psi_rev[k] = psi^bitrev(k), k in [1, N) used by stage (m, i) as psi_rev[m + i]
+__device__ void ntt_fwd_smem(uint32_t* a, const uint32_t* tw, const uint32_t* tw_sh, uint32_t N,
+                             uint32_t logN, uint32_t p) {
+    uint32_t lt = logN - 1;  // log2(t)
+    for (uint32_t m = 1; m < N; m <<= 1, lt--) {
+        const uint32_t t = 1u << lt;
+        for (uint32_t idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
+            const uint32_t i = idx >> lt, j = idx & (t - 1);
+            const uint32_t j1 = (i << (lt + 1)) + j;
+            const uint32_t S = tw[m + i], Ssh = tw_sh[m + i];
+            const uint32_t U = a[j1];
+            const uint32_t V = mulmod_shoup(a[j1 + t], S, Ssh, p);
+            a[j1] = addmod(U, V, p);
+            a[j1 + t] = submod(U, V, p);
+        }
+        __syncthreads();
+    }
+}
+
+__device__ void ntt_inv_smem(uint32_t* a, const uint32_t* itw, const uint32_t* itw_sh, uint32_t N,
+                             uint32_t logN, uint32_t p, uint32_t ninv, uint32_t ninv_sh) {
+    uint32_t lt = 0;
+    for (uint32_t m = N; m > 1; m >>= 1, lt++) {
+        const uint32_t t = 1u << lt, h = m >> 1;
+        for (uint32_t idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
+            const uint32_t i = idx >> lt, j = idx & (t - 1);
+            const uint32_t j1 = (i << (lt + 1)) + j;
+            const uint32_t S = itw[h + i], Ssh = itw_sh[h + i];
+            const uint32_t U = a[j1], V = a[j1 + t];
+            a[j1] = addmod(U, V, p);
+            a[j1 + t] = mulmod_shoup(submod(U, V, p), S, Ssh, p);
+        }
+        __syncthreads();
+    }
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) a[j] = mulmod_shoup(a[j], ninv, ninv_sh, p);
+    __syncthreads();
+}
+
+struct TwLimb {
+    const uint32_t *fw, *fw_sh, *iv, *iv_sh;
+};
+__device__ __forceinline__ TwLimb tw_limb(const uint32_t* d_tw, uint32_t N, uint32_t i) {
+    const uint32_t* b = d_tw + (size_t)i * 4 * N;
+    return {b, b + N, b + 2 * N, b + 3 * N};
+}
+
+// ---------------------------------------------------------------- KeyGen (A1)
+// s[j] = floor(word(seed,1,j) * 3 / 2^64) - 1; s_ntt[i] = NTT_{p_i}(s mod p_i)
+__global__ void k_keygen(Rns R, const uint32_t* d_tw, uint64_t seed, int8_t* s, uint32_t* s_ntt) {
+    extern __shared__ uint32_t sa[];
+    const uint32_t N = R.N, i = blockIdx.x, p = R.p[i];
+    const uint64_t key = prg_key(seed, 1);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+        int32_t v = samp_ternary(prg_word(key, j));
+        if (i == 0) s[j] = (int8_t)v;
+        sa[j] = v < 0 ? p - 1 : (uint32_t)v;
+    }
+    __syncthreads();
+    TwLimb tw = tw_limb(d_tw, N, i);
+    ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) s_ntt[(size_t)i * N + j] = sa[j];
+}
+
+// ---------------------------------------------------------------- Encrypt (A2)
+// Alg. 1 step 1 for row beta = blockIdx.x, limb i = blockIdx.y:
+//   a = uniform mod p_i (domain 2, index (beta L + i) N + j)
+//   b = a*s + Emb_q(w_hat) + e mod p_i, e = CBD(21) (domain 3, index beta N + j),
+//   w_hat[j] = W[beta][j] for j < n else 0 (Eq. 2).
+// Writes the canonical layout encW[beta][comp][limb][j].
+__global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, const uint32_t* W,
+                          uint32_t n, uint64_t seed, uint32_t* encW) {
+    extern __shared__ uint32_t sa[];
+    const uint32_t N = R.N, L = R.L, beta = blockIdx.x, i = blockIdx.y, p = R.p[i];
+    const uint64_t mu = R.mu[i];
+    const uint64_t ka = prg_key(seed, 2), ke = prg_key(seed, 3);
+    uint32_t* bo = encW + (((size_t)beta * 2 + 0) * L + i) * N;
+    uint32_t* ao = encW + (((size_t)beta * 2 + 1) * L + i) * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+        uint32_t a = samp_uniform_mod(prg_word(ka, ((uint64_t)beta * L + i) * N + j), p);
+        sa[j] = a;
+        ao[j] = a;
+    }
+    __syncthreads();
+    TwLimb tw = tw_limb(d_tw, N, i);
+    ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
+    const uint32_t* sn = s_ntt + (size_t)i * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sn[j], p, mu);
+    __syncthreads();
+    ntt_inv_smem(sa, tw.iv, tw.iv_sh, N, R.logN, p, R.ninv[i], R.ninv_sh[i]);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+        uint32_t w = j < n ? W[(size_t)beta * n + j] : 0u;
+        int32_t e = samp_cbd21(prg_word(ke, (uint64_t)beta * N + j));
+        uint32_t em = emb_mod(w, R.q_mod_t, R.ell, p, mu, R.t_inv[i]);
+        uint32_t er = e < 0 ? p - (uint32_t)(-e) : (uint32_t)e;
+        bo[j] = addmod(addmod(sa[j], em, p), er, p);
+    }
+}
+
+// ---------------------------------------------------------------- test helper
+__global__ void k_negacyclic_mul(Rns R, const uint32_t* d_tw, const uint32_t* A, const uint32_t* B,
+                                 uint32_t* Cout) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t N = R.N, i = blockIdx.y, p = R.p[i];
+    uint32_t *sa = sm, *sb = sm + N;
+    const size_t off = ((size_t)blockIdx.x * R.L + i) * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) { sa[j] = A[off + j]; sb[j] = B[off + j]; }
+    __syncthreads();
+    TwLimb tw = tw_limb(d_tw, N, i);
+    ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
+    ntt_fwd_smem(sb, tw.fw, tw.fw_sh, N, R.logN, p);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sb[j], p, R.mu[i]);
+    __syncthreads();
+    ntt_inv_smem(sa, tw.iv, tw.iv_sh, N, R.logN, p, R.ninv[i], R.ninv_sh[i]);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) Cout[off + j] = sa[j];
+}
+
+// ---------------------------------------------------------------- Decrypt (A7)
+// Per packed ciphertext tg and limb i < L_out: u_i = b_i - a_i * s mod p_i.
+__global__ void k_decrypt_phase(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, const uint32_t* cts,
+                                uint32_t* U) {
+    extern __shared__ uint32_t sa[];
+    const uint32_t N = R.N, Lo = R.L_out, tg = blockIdx.x, i = blockIdx.y, p = R.p[i];
+    const uint32_t* b = cts + (((size_t)tg * 2 + 0) * Lo + i) * N;
+    const uint32_t* a = cts + (((size_t)tg * 2 + 1) * Lo + i) * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = a[j];
+    __syncthreads();
+    TwLimb tw = tw_limb(d_tw, N, i);
+    ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
+    const uint32_t* sn = s_ntt + (size_t)i * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sn[j], p, R.mu[i]);
+    __syncthreads();
+    ntt_inv_smem(sa, tw.iv, tw.iv_sh, N, R.logN, p, R.ninv[i], R.ninv_sh[i]);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) U[((size_t)tg * Lo + i) * N + j] = submod(b[j], sa[j], p);
+}
+
+// CRT (Garner) of u_0..u_{Lo-1} and m = floor((2 t u + q') / (2 q')) mod t
+// (SURVEY.md §8(c) #5); unpack Z[alpha][j] = m_theta[(alpha mod R) n + j].
+__global__ void k_decrypt_round(Rns R, const uint32_t* U, uint32_t nct, uint32_t kq, uint32_t n,
+                                uint32_t* Z, uint32_t* M, u128 qout, uint32_t garner0, uint32_t garner1,
+                                uint32_t garner2) {
+    const uint32_t N = R.N, Lo = R.L_out, tg = blockIdx.y;
+    const uint32_t J = blockIdx.x * blockDim.x + threadIdx.x;
+    if (J >= N) return;
+    // Garner: u = v0 + p0 (v1 + p1 v2), v_i in [0, p_i)
+    uint32_t u0 = U[((size_t)tg * Lo + 0) * N + J];
+    u128 u = u0;
+    if (Lo >= 2) {
+        uint32_t p1 = R.p[1];
+        uint32_t u1 = U[((size_t)tg * Lo + 1) * N + J];
+        // v1 = (u1 - u0) * p0^-1 mod p1
+        uint32_t v1 = mulmod(submod(u1, u0 % p1, p1), garner0, p1, R.mu[1]);
+        u += (u128)R.p[0] * v1;
+        if (Lo >= 3) {
+            uint32_t p2 = R.p[2];
+            uint32_t u2 = U[((size_t)tg * Lo + 2) * N + J];
+            // v2 = (u2 - (u0 + p0 v1)) * (p0 p1)^-1 mod p2
+            uint64_t x = (uint64_t)u0 + (uint64_t)R.p[0] * v1;  // < 2^62
+            uint32_t xm = mod64(x, p2, R.mu[2]);
+            uint32_t v2 = mulmod(submod(u2, xm, p2), garner1, p2, R.mu[2]);
+            u += (u128)R.p[0] * R.p[1] * v2;
+        }
+    }
+    (void)garner2;
+    const uint32_t ell = R.ell;
+    // m~ = floor((2 t u + q') / (2 q')): estimate in double, then correct exactly
+    const u128 num = (u << (ell + 1)) + qout;
+    const u128 den = qout << 1;
+    double est = ((double)(uint64_t)(u >> 64) * 18446744073709551616.0 + (double)(uint64_t)u) *
+                 (double)(1ULL << ell) / ((double)(uint64_t)(qout >> 64) * 18446744073709551616.0 +
+                                          (double)(uint64_t)qout);
+    uint64_t mt = (uint64_t)(est + 0.5);
+    while ((u128)mt * den > num) mt--;
+    while ((u128)(mt + 1) * den <= num) mt++;
+    const uint32_t m = (uint32_t)(mt & ((1ULL << ell) - 1));
+    if (M) M[(size_t)tg * N + J] = m;
+    const uint32_t Rr = N / n, theta = tg % nct, query = tg / nct;
+    const uint32_t rows = min(Rr, kq - theta * Rr);
+    if (J < rows * n) Z[((size_t)query * kq + theta * Rr) * n + J] = m;
+}
+
+__global__ void k_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* out) {
+    const uint64_t key = prg_key(seed, dom);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = prg_word(key, start + i);
+}
+
+// ---------------------------------------------------------------- launchers
+static uint32_t ntt_threads(uint32_t N) { return N >= 1024 ? 512 : N / 2; }
+
+cudaError_t launch_keygen(nimbus_ctx* c, uint64_t seed, int8_t* d_s, uint32_t* d_s_ntt, cudaStream_t st) {
+    const uint32_t N = c->rns.N;
+    k_keygen<<<c->rns.L, ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, seed, d_s, d_s_ntt);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* d_W, uint32_t m,
+                           uint32_t n, uint64_t seed, uint32_t* d_encW, cudaStream_t st) {
+    const uint32_t N = c->rns.N;
+    k_encrypt<<<dim3(m, c->rns.L), ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, d_s_ntt, d_W, n, seed, d_encW);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_negacyclic_mul(nimbus_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t count,
+                                  uint32_t* out, cudaStream_t st) {
+    const uint32_t N = c->rns.N;
+    size_t smem = (size_t)N * 8;
+    cudaFuncSetAttribute(k_negacyclic_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_negacyclic_mul<<<dim3(count, c->rns.L), ntt_threads(N), smem, st>>>(c->rns, c->d_tw, a, b, out);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* cts, uint32_t nct_total,
+                           uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, uint32_t* d_Z,
+                           uint32_t* d_M, cudaStream_t st) {
+    const uint32_t N = c->rns.N;
+    k_decrypt_phase<<<dim3(nct_total, c->rns.L_out), ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, d_s_ntt,
+                                                                                  cts, d_u_tmp);
+    c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // Garner constants
+    const nimbus::Rns& R = c->rns;
+    auto inv = [](uint64_t a, uint64_t p) {
+        uint64_t r = 1, e2 = p - 2; a %= p;
+        while (e2) { if (e2 & 1) r = (uint64_t)((u128)r * a % p); a = (uint64_t)((u128)a * a % p); e2 >>= 1; }
+        return (uint32_t)r;
+    };
+    uint32_t g0 = R.L_out >= 2 ? inv(R.p[0], R.p[1]) : 0;
+    uint32_t g1 = R.L_out >= 3 ? inv((uint64_t)R.p[0] * R.p[1] % R.p[2], R.p[2]) : 0;
+    k_decrypt_round<<<dim3((N + 255) / 256, nct_total), 256, 0, st>>>(c->rns, d_u_tmp, nct, kq, n, d_Z, d_M,
+                                                                     c->qout, g0, g1, 0);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* out,
+                             cudaStream_t st) {
+    k_prg_words<<<592, 256, 0, st>>>(seed, dom, start, count, out);
+    return cudaGetLastError();
+}
+
+}  // namespace nimbus

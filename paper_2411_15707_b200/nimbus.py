@@ -1,0 +1,335 @@
+"""Thin ctypes binding of libnimbus_cop.so (include/nimbus_cop.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  Functions carry the C names; tensors are torch CUDA tensors
+(contiguous, the dtype the header states), passed as data_ptr(); the stream
+defaults to torch's current stream.  There is no CPU fallback: if the library
+is missing or no sm_100 device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libnimbus_cop.so")
+
+STATUS = {0: "NIMBUS_OK", -1: "NIMBUS_EINVAL", -2: "NIMBUS_ESHAPE", -3: "NIMBUS_ERANGE",
+          -4: "NIMBUS_ENOISE", -5: "NIMBUS_ECUDA", -6: "NIMBUS_ENOMEM", -8: "NIMBUS_EARCH"}
+IMPL_TCGEN05, IMPL_CUDACORE = 0, 1
+FLAG_CHECK_RANGE = 1
+
+
+class NimbusError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+
+
+class nimbus_params(C.Structure):
+    _fields_ = [("N", C.c_uint32), ("L", C.c_uint32), ("ell", C.c_uint32),
+                ("L_out", C.c_uint32), ("impl", C.c_uint32), ("flags", C.c_uint32)]
+
+
+_lib = None
+_vp, _u32, _u64, _sz = C.c_void_p, C.c_uint32, C.c_uint64, C.c_size_t
+_SIGS = {
+    "nimbus_ctx_create": (C.c_int, [C.POINTER(nimbus_params), C.c_int, C.POINTER(_vp)]),
+    "nimbus_ctx_destroy": (None, [_vp]),
+    "nimbus_ctx_primes": (C.c_int, [_vp, C.POINTER(_u32)]),
+    "nimbus_last_error": (C.c_char_p, [_vp]),
+    "nimbus_sync": (C.c_int, [_vp, _vp]),
+    "nimbus_keygen": (C.c_int, [_vp, _u64, _vp, C.POINTER(_vp)]),
+    "nimbus_sk_destroy": (None, [_vp]),
+    "nimbus_sk_export": (C.c_int, [_vp, _vp, _vp]),
+    "nimbus_encrypt_weights": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, C.POINTER(_vp)]),
+    "nimbus_encw_destroy": (None, [_vp]),
+    "nimbus_encw_bytes": (_sz, [_vp]),
+    "nimbus_encw_export": (C.c_int, [_vp, _vp, _vp]),
+    "nimbus_encw_import": (C.c_int, [_vp, _vp, _u32, _u32, _vp, C.POINTER(_vp)]),
+    "nimbus_cop_out_count": (C.c_int, [_vp, _u32, _u32, C.POINTER(_u32)]),
+    "nimbus_cop_workspace_size": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
+    "nimbus_cop_matmul": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_cop_matmul_host": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_cop_accumulate": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp, _sz, _vp]),
+    "nimbus_cop_pack": (C.c_int, [_vp, _vp, _u32, _u32, _u32, _u64, _vp, _vp, _vp]),
+    "nimbus_decrypt": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _vp]),
+    "nimbus_prg_words": (C.c_int, [_u64, _u32, _u64, _u64, _vp, _vp]),
+    "nimbus_negacyclic_mul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp]),
+    "nimbus_launch_count": (_u64, [_vp]),
+}
+EXPORTED = tuple(_SIGS)
+
+
+def lib():
+    """Load the in-tree library (built by __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _stream(stream):
+    if stream is None:
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, torch.cuda.Stream):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+def _ptr(t: torch.Tensor, dtype=None, what=""):
+    if t is None:
+        return None
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{what}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+class _Handle:
+    _destroy = None
+
+    def __init__(self, ptr, owner=None):
+        self.ptr = ptr
+        self.owner = owner
+
+    def close(self):
+        if self.ptr:
+            getattr(lib(), self._destroy)(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context(_Handle):
+    _destroy = "nimbus_ctx_destroy"
+
+    def __init__(self, ptr, params: nimbus_params, device: int):
+        super().__init__(ptr)
+        self.params = params
+        self.device = device
+
+    @property
+    def N(self):
+        return self.params.N
+
+    @property
+    def L(self):
+        return self.params.L
+
+    @property
+    def L_out(self):
+        return self.params.L_out
+
+    @property
+    def ell(self):
+        return self.params.ell
+
+
+class SecretKey(_Handle):
+    _destroy = "nimbus_sk_destroy"
+
+
+class EncW(_Handle):
+    _destroy = "nimbus_encw_destroy"
+
+    def __init__(self, ptr, ctx, m, n):
+        super().__init__(ptr, ctx)
+        self.m, self.n = m, n
+
+
+def _check(st: int, ctx=None):
+    if st != 0:
+        msg = lib().nimbus_last_error(ctx.ptr if ctx is not None else None)
+        raise NimbusError(st, msg.decode() if msg else "")
+
+
+# ------------------------------------------------------------------ C-named API
+def nimbus_ctx_create(N, L, ell, L_out, impl=IMPL_TCGEN05, flags=0, device=0) -> Context:
+    prm = nimbus_params(N, L, ell, L_out, impl, flags)
+    out = C.c_void_p()
+    _check(lib().nimbus_ctx_create(C.byref(prm), device, C.byref(out)))
+    return Context(out, prm, device)
+
+
+def nimbus_ctx_primes(ctx: Context):
+    arr = (_u32 * ctx.L)()
+    _check(lib().nimbus_ctx_primes(ctx.ptr, arr), ctx)
+    return [int(x) for x in arr]
+
+
+def nimbus_sync(ctx: Context, stream=None):
+    _check(lib().nimbus_sync(ctx.ptr, _stream(stream)), ctx)
+
+
+def nimbus_keygen(ctx: Context, seed: int, stream=None) -> SecretKey:
+    out = C.c_void_p()
+    _check(lib().nimbus_keygen(ctx.ptr, seed, _stream(stream), C.byref(out)), ctx)
+    return SecretKey(out, ctx)
+
+
+def nimbus_sk_export(sk: SecretKey, stream=None) -> torch.Tensor:
+    ctx = sk.owner
+    s = torch.empty(ctx.N, dtype=torch.int8, device=f"cuda:{ctx.device}")
+    _check(lib().nimbus_sk_export(sk.ptr, _ptr(s), _stream(stream)), ctx)
+    return s
+
+
+def nimbus_encrypt_weights(ctx: Context, sk: SecretKey, W: torch.Tensor, seed: int, stream=None) -> EncW:
+    m, n = W.shape
+    out = C.c_void_p()
+    _check(lib().nimbus_encrypt_weights(ctx.ptr, sk.ptr, _ptr(W, torch.int32, "W"), m, n, seed,
+                                        _stream(stream), C.byref(out)), ctx)
+    return EncW(out, ctx, m, n)
+
+
+def nimbus_encw_bytes(w: EncW) -> int:
+    return int(lib().nimbus_encw_bytes(w.ptr))
+
+
+def nimbus_encw_export(w: EncW, stream=None) -> torch.Tensor:
+    ctx = w.owner
+    out = torch.empty((w.m, 2, ctx.L, ctx.N), dtype=torch.int32, device=f"cuda:{ctx.device}")
+    _check(lib().nimbus_encw_export(w.ptr, _ptr(out), _stream(stream)), ctx)
+    return out
+
+
+def nimbus_encw_import(ctx: Context, canon: torch.Tensor, n: int, stream=None) -> EncW:
+    m = canon.shape[0]
+    out = C.c_void_p()
+    _check(lib().nimbus_encw_import(ctx.ptr, _ptr(canon, torch.int32, "canon"), m, n, _stream(stream),
+                                    C.byref(out)), ctx)
+    return EncW(out, ctx, m, n)
+
+
+def nimbus_cop_out_count(ctx: Context, k_per_query: int, n: int) -> int:
+    out = _u32()
+    _check(lib().nimbus_cop_out_count(ctx.ptr, k_per_query, n, C.byref(out)), ctx)
+    return int(out.value)
+
+
+def nimbus_cop_workspace_size(ctx: Context, w: EncW, k: int) -> int:
+    out = _sz()
+    _check(lib().nimbus_cop_workspace_size(ctx.ptr, w.ptr, k, C.byref(out)), ctx)
+    return int(out.value)
+
+
+def alloc_workspace(ctx: Context, w: EncW, k: int) -> torch.Tensor:
+    return torch.empty(nimbus_cop_workspace_size(ctx, w, k), dtype=torch.uint8, device=f"cuda:{ctx.device}")
+
+
+def alloc_outputs(ctx: Context, w: EncW, k_per_query: int, n_queries: int, pin: bool = False,
+                  device=None):
+    nct = nimbus_cop_out_count(ctx, k_per_query, w.n)
+    dev = device if device is not None else f"cuda:{ctx.device}"
+    kw = dict(dtype=torch.int32, device=dev)
+    if pin:
+        kw["pin_memory"] = True
+    cts = torch.empty((n_queries, nct, 2, ctx.L_out, ctx.N), **kw)
+    R = torch.empty((n_queries * k_per_query, w.n), **kw)
+    return cts, R
+
+
+def nimbus_cop_matmul(ctx: Context, w: EncW, X: torch.Tensor, k_per_query: int, n_queries: int,
+                      mask_seed: int, cts: torch.Tensor, R: torch.Tensor, ws: torch.Tensor,
+                      stream=None):
+    _check(lib().nimbus_cop_matmul(ctx.ptr, w.ptr, _ptr(X, torch.int32, "X"), k_per_query, n_queries,
+                                   mask_seed, _ptr(cts, torch.int32, "cts"), _ptr(R, torch.int32, "R"),
+                                   _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return cts, R
+
+
+def nimbus_cop_matmul_host(ctx: Context, w: EncW, X_host: torch.Tensor, k_per_query: int,
+                           n_queries: int, mask_seed: int, cts_host: torch.Tensor,
+                           R_host: torch.Tensor, ws: torch.Tensor, stream=None):
+    for t, nm in ((X_host, "X"), (cts_host, "cts"), (R_host, "R")):
+        if t.is_cuda:
+            raise ValueError(f"{nm} must be a host tensor")
+    _check(lib().nimbus_cop_matmul_host(ctx.ptr, w.ptr, _ptr(X_host, torch.int32, "X"), k_per_query,
+                                        n_queries, mask_seed, _ptr(cts_host, torch.int32, "cts"),
+                                        _ptr(R_host, torch.int32, "R"), _ptr(ws), ws.numel(),
+                                        _stream(stream)), ctx)
+    return cts_host, R_host
+
+
+def nimbus_cop_accumulate(ctx: Context, w: EncW, X: torch.Tensor, ws: torch.Tensor, C_out=None,
+                          stream=None) -> torch.Tensor:
+    k = X.shape[0]
+    if C_out is None:
+        C_out = torch.empty((k, 2, ctx.L, ctx.N), dtype=torch.int32, device=X.device)
+    _check(lib().nimbus_cop_accumulate(ctx.ptr, w.ptr, _ptr(X, torch.int32, "X"), k,
+                                       _ptr(C_out, torch.int32, "C"), _ptr(ws), ws.numel(),
+                                       _stream(stream)), ctx)
+    return C_out
+
+
+def nimbus_cop_pack(ctx: Context, C_in: torch.Tensor, k_per_query: int, n_queries: int, n: int,
+                    mask_seed: int, stream=None):
+    nct = nimbus_cop_out_count(ctx, k_per_query, n)
+    cts = torch.empty((n_queries, nct, 2, ctx.L_out, ctx.N), dtype=torch.int32, device=C_in.device)
+    R = torch.empty((n_queries * k_per_query, n), dtype=torch.int32, device=C_in.device)
+    _check(lib().nimbus_cop_pack(ctx.ptr, _ptr(C_in, torch.int32, "C"), k_per_query, n_queries, n,
+                                 mask_seed, _ptr(cts), _ptr(R), _stream(stream)), ctx)
+    return cts, R
+
+
+def nimbus_decrypt(ctx: Context, sk: SecretKey, cts: torch.Tensor, k_per_query: int, n_queries: int,
+                   n: int, want_full: bool = False, stream=None):
+    Z = torch.zeros((n_queries * k_per_query, n), dtype=torch.int32, device=cts.device)
+    M = None
+    if want_full:
+        nct = nimbus_cop_out_count(ctx, k_per_query, n)
+        M = torch.empty((n_queries * nct, ctx.N), dtype=torch.int32, device=cts.device)
+    _check(lib().nimbus_decrypt(ctx.ptr, sk.ptr, _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
+                                n, _ptr(Z), _ptr(M) if M is not None else None, _stream(stream)), ctx)
+    return Z, M
+
+
+def nimbus_prg_words(seed: int, dom: int, start: int, count: int, device="cuda:0", stream=None):
+    out = torch.empty(count, dtype=torch.int64, device=device)
+    st = lib().nimbus_prg_words(seed, dom, start, count, _ptr(out), _stream(stream))
+    if st != 0:
+        raise NimbusError(st, "prg_words")
+    return out
+
+
+def nimbus_negacyclic_mul(ctx: Context, a: torch.Tensor, b: torch.Tensor, stream=None) -> torch.Tensor:
+    count = a.shape[0]
+    c = torch.empty_like(a)
+    _check(lib().nimbus_negacyclic_mul(ctx.ptr, _ptr(a, torch.int32, "a"), _ptr(b, torch.int32, "b"),
+                                       count, _ptr(c), _stream(stream)), ctx)
+    return c
+
+
+def nimbus_launch_count(ctx: Context) -> int:
+    return int(lib().nimbus_launch_count(ctx.ptr))
+
+
+# ------------------------------------------------------------------ helpers
+def as_u32(t: torch.Tensor) -> torch.Tensor:
+    """View a uint32-valued int32 tensor as int64 with values in [0, 2^32)."""
+    return t.to(torch.int64) & 0xFFFFFFFF
+
+
+def from_numpy_u32(a, device) -> torch.Tensor:
+    import numpy as np
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).to(device)
+
+
+def to_numpy_u32(t: torch.Tensor):
+    import numpy as np
+    return t.detach().cpu().contiguous().numpy().view(np.uint32)

@@ -1,0 +1,308 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle,
+element by element on the same seeded inputs, plus properties that hold at any
+size (decryption of every packed ciphertext equals X.W - R mod t, invalid slots
+equal -r).  Bit-exact is the bar everywhere: the whole path is integer arithmetic
+(SURVEY.md §8(c) "Plain definition of the result").
+
+Sizes: full oracle comparison where the oracle finishes in seconds (toy, C1,
+C2, C3, ragged multi-tile shapes); at C4/C5 sizes, full Enc(W) comparison plus
+sampled output coefficients from the oracle, plus the exact decryption property
+over every output.
+"""
+import numpy as np
+import pytest
+import torch
+
+import nimbus_inputs as ni
+
+pytestmark = pytest.mark.gpu
+
+P4096 = [2147377153, 2147352577]
+P8192 = [2147352577, 2147205121, 2147074049]
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def nb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2411_15707_b200 import nimbus
+    nimbus.lib()
+    return nimbus
+
+
+def u32(t):
+    from paper_2411_15707_b200 import nimbus
+    return nimbus.to_numpy_u32(t)
+
+
+def dev_u32(a):
+    from paper_2411_15707_b200 import nimbus
+    return nimbus.from_numpy_u32(a, DEV)
+
+
+def matmul_mod_t(X, W, ell):
+    """X.W mod 2^ell with uint64 wrap-around arithmetic (exact mod 2^64)."""
+    with np.errstate(over="ignore"):
+        Y = X.astype(np.uint64) @ W.astype(np.uint64)
+    return Y & np.uint64((1 << ell) - 1)
+
+
+class Case:
+    def __init__(self, nb, oracle, N, L, ell, L_out, m, n, kq, nq=1, impl=0, seed=0x5EED, W=None, X=None,
+                 oracle_full=True):
+        self.nb, self.O = nb, oracle
+        self.N, self.L, self.ell, self.L_out = N, L, ell, L_out
+        self.m, self.n, self.kq, self.nq, self.k = m, n, kq, nq, kq * nq
+        self.seed = seed
+        self.ctx = nb.nimbus_ctx_create(N, L, ell, L_out, impl)
+        self.pr = np.array(nb.nimbus_ctx_primes(self.ctx), np.uint32)
+        self.W = ni.gen_W(seed, m, n, ell) if W is None else W
+        self.X = ni.gen_X(seed ^ 0xA5, self.k, m, ell) if X is None else X
+        self.sk = nb.nimbus_keygen(self.ctx, seed)
+        self.encw = nb.nimbus_encrypt_weights(self.ctx, self.sk, dev_u32(self.W), seed)
+        self.s_oracle = oracle.keygen(N, seed)
+        self.E_oracle = oracle.encrypt_rows(N, L, self.pr, ell, self.s_oracle, self.W, seed) if oracle_full else None
+
+    def run(self, mask_seed=None):
+        nb = self.nb
+        mask_seed = self.seed if mask_seed is None else mask_seed
+        ws = nb.alloc_workspace(self.ctx, self.encw, self.k)
+        cts, R = nb.alloc_outputs(self.ctx, self.encw, self.kq, self.nq)
+        nb.nimbus_cop_matmul(self.ctx, self.encw, dev_u32(self.X), self.kq, self.nq, mask_seed, cts, R, ws)
+        nb.nimbus_sync(self.ctx)
+        return cts, R
+
+    def oracle_out(self, mask_seed=None):
+        mask_seed = self.seed if mask_seed is None else mask_seed
+        return self.O.cop_matmul(self.N, self.L, self.L_out, self.pr, self.ell, self.E_oracle, self.X, self.n,
+                                 self.kq, self.nq, mask_seed)
+
+    def check_decrypt(self, cts, R):
+        """Server step 5: Dec - mask = X.W mod t; invalid slots = -r."""
+        nb = self.nb
+        Z, M = nb.nimbus_decrypt(self.ctx, self.sk, cts, self.kq, self.nq, self.n, want_full=True)
+        t = 1 << self.ell
+        Y = matmul_mod_t(self.X, self.W, self.ell)
+        Rn = u32(R).astype(np.uint64)
+        assert (u32(Z).astype(np.uint64) == (Y + t - Rn) % t).all()
+        Mn = u32(M)
+        Rr = self.N // self.n
+        nct = Mn.shape[0] // self.nq
+        for tg in range(Mn.shape[0]):
+            th = tg % nct
+            rows = min(Rr, self.kq - th * Rr)
+            mask = ni.uniform_mod_t(self.seed, 6, self.N, self.ell, start=tg * self.N).astype(np.uint64)
+            inval = np.ones(self.N, bool)
+            inval[: rows * self.n] = False
+            assert (Mn[tg][inval] == (t - mask[inval]) % t).all()
+        return Z
+
+
+# ------------------------------------------------------------------ primitives
+def test_prg_words(nb, oracle):
+    for seed, dom, start in ((ni.seed_cfg(1), 1, 0), (ni.seed_cfg(4), 2, 12345), (7, 6, 1 << 33)):
+        got = nb.nimbus_prg_words(seed, dom, start, 4096).cpu().numpy().view(np.uint64)
+        assert (got == oracle.words(seed, dom, start, 4096)).all()
+
+
+@pytest.mark.parametrize("N,L", [(64, 2), (4096, 2), (8192, 3)])
+def test_keygen_and_primes(nb, oracle, N, L):
+    ctx = nb.nimbus_ctx_create(N, L, 16, 1)
+    assert nb.nimbus_ctx_primes(ctx) == [int(p) for p in oracle.primes(N, L)]
+    sk = nb.nimbus_keygen(ctx, ni.seed_cfg(2) + N)
+    s = nb.nimbus_sk_export(sk).cpu().numpy()
+    assert (s == oracle.keygen(N, ni.seed_cfg(2) + N)).all()
+
+
+@pytest.mark.parametrize("N,L", [(64, 2), (1024, 3), (4096, 2), (8192, 3)])
+def test_ntt_negacyclic_product(nb, oracle, N, L):
+    """K2 through the library's NTT vs the oracle's negacyclic product."""
+    ctx = nb.nimbus_ctx_create(N, L, 16, 1)
+    pr = nb.nimbus_ctx_primes(ctx)
+    rng = np.random.default_rng(N)
+    cnt = 2
+    a = np.stack([np.stack([rng.integers(0, p, N, dtype=np.uint64) for p in pr]) for _ in range(cnt)]).astype(np.uint32)
+    b = np.stack([np.stack([rng.integers(0, p, N, dtype=np.uint64) for p in pr]) for _ in range(cnt)]).astype(np.uint32)
+    b[0, :, :] = 0
+    b[0, :, 0] = 1          # identity
+    c = u32(nb.nimbus_negacyclic_mul(ctx, dev_u32(a), dev_u32(b)))
+    assert (c[0] == a[0]).all()
+    for i in range(cnt):
+        for l, p in enumerate(pr):
+            want = oracle.negacyclic_schoolbook(N, p, a[i, l], b[i, l]) if N <= 64 else \
+                oracle.negacyclic_ntt(N, p, a[i, l], b[i, l])
+            assert (c[i, l] == want).all()
+
+
+# ------------------------------------------------------------------ Enc(W)
+@pytest.mark.parametrize("N,L,ell,m,n", [(64, 2, 16, 16, 20), (4096, 2, 16, 64, 64), (4096, 2, 16, 200, 4096),
+                                         (8192, 3, 32, 130, 768)])
+def test_encrypt_weights_parity(nb, oracle, N, L, ell, m, n):
+    c = Case(nb, oracle, N, L, ell, 2 if ell == 32 else 1, m, n, kq=1)
+    E = u32(nb.nimbus_encw_export(c.encw))
+    assert E.shape == c.E_oracle.shape
+    assert (E == c.E_oracle).all()
+    # import(export) round trip reproduces the resident layout
+    w2 = nb.nimbus_encw_import(c.ctx, dev_u32(E), n)
+    assert (u32(nb.nimbus_encw_export(w2)) == E).all()
+
+
+# ------------------------------------------------------------------ contraction (step 2)
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("N,L,ell,k,m,n", [
+    (64, 2, 16, 12, 16, 20),          # toy
+    (4096, 2, 16, 16, 64, 64),        # C1
+    (4096, 2, 16, 200, 300, 700),     # two M tiles, ragged k and m (3 k-blocks, last partial)
+    (8192, 3, 32, 130, 200, 768),     # ell=32: 4 X slices, 7 accumulators, ragged
+    (1024, 2, 8, 129, 257, 100),      # ell=8: 1 X slice
+    (1024, 2, 16, 1, 1, 1),           # degenerate k = m = n = 1
+])
+def test_cop_accumulate_parity(nb, oracle, impl, N, L, ell, k, m, n):
+    c = Case(nb, oracle, N, L, ell, 2 if ell == 32 else 1, m, n, kq=k, impl=impl)
+    ws = nb.alloc_workspace(c.ctx, c.encw, k)
+    Cg = u32(nb.nimbus_cop_accumulate(c.ctx, c.encw, dev_u32(c.X), ws))
+    nb.nimbus_sync(c.ctx)
+    Co = oracle.cop_accumulate(N, L, c.pr, c.E_oracle, c.X)
+    assert (Cg == Co).all()
+
+
+def test_cop_onehot_selects_row_ciphertext(nb, oracle):
+    """x = e_beta gives c[alpha] = Enc(W_beta) bit for bit."""
+    N, L, m = 4096, 2, 300
+    X = np.zeros((160, m), np.uint32)
+    for a in range(160):
+        X[a, (a * 7) % m] = 1
+    c = Case(nb, oracle, N, L, 16, 1, m, 500, kq=160, X=X, oracle_full=False)
+    ws = nb.alloc_workspace(c.ctx, c.encw, 160)
+    Cg = u32(nb.nimbus_cop_accumulate(c.ctx, c.encw, dev_u32(X), ws))
+    E = u32(nb.nimbus_encw_export(c.encw))
+    for a in range(160):
+        assert (Cg[a] == E[(a * 7) % m]).all()
+
+
+# ------------------------------------------------------------------ end to end (steps 2-4)
+E2E = [
+    # name, N, L, ell, L_out, m, n, kq, nq, impl
+    ("toy_l16", 64, 2, 16, 1, 16, 20, 12, 1, 0),
+    ("toy_l32", 64, 3, 32, 2, 16, 20, 12, 1, 0),
+    ("C1", 4096, 2, 16, 1, 64, 64, 16, 1, 0),
+    ("C1_cc", 4096, 2, 16, 1, 64, 64, 16, 1, 1),
+    ("C2", 4096, 2, 16, 1, 768, 768, 128, 1, 0),
+    ("C3", 4096, 2, 16, 1, 768, 3072, 128, 1, 0),
+    ("C2_cc", 4096, 2, 16, 1, 768, 768, 128, 1, 1),
+    ("multiquery_ragged", 4096, 2, 16, 1, 200, 700, 23, 3, 0),
+    ("l32_multiquery", 8192, 3, 32, 2, 300, 768, 25, 2, 0),
+    ("l32_to1limb", 8192, 3, 16, 1, 100, 1000, 17, 1, 0),
+    ("n_equals_N", 1024, 2, 16, 1, 100, 1024, 5, 1, 0),
+    ("n_half_plus_1", 1024, 2, 16, 1, 70, 513, 4, 1, 0),
+    ("k_one", 4096, 2, 16, 1, 128, 64, 1, 1, 0),
+    ("m_one", 4096, 2, 16, 1, 1, 64, 64, 1, 0),
+    ("R_gt_k", 8192, 3, 32, 2, 64, 64, 7, 2, 0),
+]
+
+
+@pytest.mark.parametrize("case", E2E, ids=[c[0] for c in E2E])
+def test_cop_matmul_parity(nb, oracle, case):
+    name, N, L, ell, L_out, m, n, kq, nq, impl = case
+    c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, impl, seed=ni.seed_mm(2, 0, len(name)))
+    cts, R = c.run()
+    cts_o, R_o = c.oracle_out()
+    assert cts.shape == cts_o.shape
+    assert (u32(cts) == cts_o).all(), "output ciphertexts differ"
+    assert (u32(R) == R_o).all(), "client share R differs"
+    c.check_decrypt(cts, R)
+
+
+def test_host_buffer_api_matches_device(nb, oracle):
+    c = Case(nb, oracle, 4096, 2, 16, 1, 768, 768, 128, oracle_full=False)
+    cts_d, R_d = c.run()
+    ws = nb.alloc_workspace(c.ctx, c.encw, c.k)
+    cts_h, R_h = nb.alloc_outputs(c.ctx, c.encw, c.kq, c.nq, pin=True, device="cpu")
+    Xh = torch.from_numpy(c.X.view(np.int32)).pin_memory()
+    nb.nimbus_cop_matmul_host(c.ctx, c.encw, Xh, c.kq, c.nq, c.seed, cts_h, R_h, ws)
+    assert torch.equal(cts_h, cts_d.cpu()) and torch.equal(R_h, R_d.cpu())
+
+
+# ------------------------------------------------------------------ full-size configs (sampled)
+def _sampled_check(c, cts, n_samples=600, rng_seed=0):
+    nct = cts.shape[1]
+    rng = np.random.default_rng(rng_seed)
+    sq = rng.integers(0, c.nq, n_samples).astype(np.uint32)
+    st = rng.integers(0, nct, n_samples).astype(np.uint32)
+    sJ = rng.integers(0, c.N, n_samples).astype(np.uint32)
+    sJ[:8] = [0, 1, c.n - 1, c.n, c.N - 1, c.N - c.n, (c.N // c.n) * c.n - 1, c.N // 2]
+    want = c.O.cop_matmul_sampled(c.N, c.L, c.L_out, c.pr, c.ell, c.E_oracle, c.X, c.n, c.kq, c.nq, c.seed,
+                                  sq, st, sJ)
+    g = u32(cts)
+    got = np.stack([g[sq[i], st[i], :, :, sJ[i]] for i in range(n_samples)])
+    assert (got == want).all()
+
+
+@pytest.mark.parametrize("ell,L_out", [(32, 2), (16, 1)])
+def test_c4_full_size(nb, oracle, ell, L_out):
+    """C4: X 128x3072, W 3072x768, N=8192, 3 limbs (BASELINE.json configs[3]) at the
+    launch configuration bench.py times; Enc(W) compared in full, outputs sampled,
+    every slot checked through decryption."""
+    cfg = ni.CONFIGS[4]
+    lay = cfg.layers[0][2]
+    seed = ni.seed_mm(4)
+    c = Case(nb, oracle, cfg.N, cfg.L, ell, L_out, lay.m, lay.n, lay.k_per_query, seed=seed,
+             W=ni.gen_W(seed, lay.m, lay.n, ell), X=ni.gen_X(seed, lay.k, lay.m, ell))
+    assert (u32(nb.nimbus_encw_export(c.encw)) == c.E_oracle).all()
+    cts, R = c.run()
+    _sampled_check(c, cts)
+    c.check_decrypt(cts, R)
+
+
+@pytest.mark.parametrize("proj", [0, 4, 5])
+def test_c5_layer_matmuls(nb, oracle, proj):
+    """C5: seq 512 x 4 queries (k=2048) on the Q (768x768), FFN-up (768x3072) and
+    FFN-down (3072x768) shapes of layer 0, same launch as bench --config 5."""
+    cfg = ni.CONFIGS[5]
+    li, pj, lay = cfg.layers[proj]
+    seed = ni.seed_mm(5, li, pj)
+    c = Case(nb, oracle, cfg.N, cfg.L, cfg.ell, cfg.L_out, lay.m, lay.n, lay.k_per_query, lay.n_queries,
+             seed=seed, W=ni.gen_W(seed, lay.m, lay.n, cfg.ell), X=ni.gen_X(seed, lay.k, lay.m, cfg.ell))
+    assert (u32(nb.nimbus_encw_export(c.encw)) == c.E_oracle).all()
+    cts, R = c.run()
+    _sampled_check(c, cts, n_samples=300)
+    c.check_decrypt(cts, R)
+
+
+# ------------------------------------------------------------------ errors
+def test_error_codes(nb, oracle):
+    ctx = nb.nimbus_ctx_create(1024, 2, 16, 1)
+    sk = nb.nimbus_keygen(ctx, 1)
+    W = dev_u32(ni.gen_W(1, 4, 1025, 16))
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_encrypt_weights(ctx, sk, W, 1)     # n > N
+    assert e.value.status == -2
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_ctx_create(1000, 2, 16, 1)          # N not a power of two
+    assert e.value.status == -1
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_ctx_create(1024, 2, 16, 3)          # L_out > L
+    assert e.value.status == -1
+    # ell=32 cannot be switched down to one 31-bit limb: the noise bound refuses it
+    ctx32 = nb.nimbus_ctx_create(8192, 3, 32, 1)
+    sk32 = nb.nimbus_keygen(ctx32, 1)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_encrypt_weights(ctx32, sk32, dev_u32(ni.gen_W(1, 8, 8, 32)), 1)
+    assert e.value.status == -4
+    # range check: an entry >= t is reported at the next sync
+    ctxr = nb.nimbus_ctx_create(1024, 2, 16, 1, flags=nb.FLAG_CHECK_RANGE)
+    skr = nb.nimbus_keygen(ctxr, 1)
+    wr = nb.nimbus_encrypt_weights(ctxr, skr, dev_u32(ni.gen_W(1, 8, 8, 16)), 1)
+    ws = nb.alloc_workspace(ctxr, wr, 4)
+    cts, R = nb.alloc_outputs(ctxr, wr, 4, 1)
+    Xbad = ni.gen_X(1, 4, 8, 16)
+    Xbad[2, 3] = 1 << 16
+    nb.nimbus_cop_matmul(ctxr, wr, dev_u32(Xbad), 4, 1, 1, cts, R, ws)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_sync(ctxr)
+    assert e.value.status == -3
+    # workspace too small
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_cop_matmul(ctxr, wr, dev_u32(ni.gen_X(1, 4, 8, 16)), 4, 1, 1, cts, R, ws[:16])
+    assert e.value.status == -2
