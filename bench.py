@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the Nimbus COP hot path (Alg. 1 steps 2-4)
+on B200: one `step` = one nimbus_cop_matmul (slice X -> tcgen05 contraction ->
+RShift packing + mod-switch + mask) over one batch of synthetic inputs with
+Enc(W) resident in HBM.
+
+Default workload = BASELINE.json configs[1] (C2, BERT-base attention
+projection X 128x768 . W 768x768, N=4096, 2 limbs, ell=16).  `--config`
+selects another BASELINE config (1..5; 4l16 / 5l16 = the ell=16 secondary
+lines).  For C5 a step is the full 12-layer x 6-matmul pass.
+
+Prints ONE JSON line (rank 0).  Multi-GPU (torchrun): every rank runs its own
+independent queries against its own copy of Enc(W) (weak scaling, no
+data-path collective); timing is the max over ranks.
+
+--impl reference runs the CPU oracle (oracle/, the reference arm of this
+tier) on the same config, each step a bounded row sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import nimbus_inputs as ni  # noqa: E402
+
+METRIC = "COP matmul ms/layer and modular MAC/s (BERT-base shapes) vs int8 TC roofline"
+UNIT = "modMAC/s"
+L2_FLUSH_BYTES = 512 << 20     # > 126 MB L2, written between timed steps
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="2")
+    ap.add_argument("--impl", default="tcgen05", choices=["tcgen05", "cudacore", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def get_config(key: str):
+    if key.endswith("l16"):
+        return ni.CONFIGS_L16[int(key[0])]
+    return ni.CONFIGS[int(key)]
+
+
+def workload_name(cfg):
+    lays = [l for _, _, l in cfg.layers]
+    if len(lays) == 1:
+        l = lays[0]
+        return (f"{cfg.name} {l.name}: X {l.k}x{l.m} . W {l.m}x{l.n}, N={cfg.N}, L={cfg.L}, "
+                f"ell={cfg.ell}, L_out={cfg.L_out}")
+    return (f"{cfg.name} BERT-base linear stack: 12 layers x (4x768x768 + 768x3072 + 3072x768), "
+            f"k={lays[0].k} (seq {lays[0].k_per_query} x {lays[0].n_queries} queries), N={cfg.N}, "
+            f"L={cfg.L}, ell={cfg.ell}, L_out={cfg.L_out}")
+
+
+def sx_of(ell):
+    return 1 if ell <= 8 else 2 if ell <= 16 else 4
+
+
+def measured_peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        p.update({k: d[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in d})
+        p["src"] = "MEASURED_PEAKS.json"
+    return p
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_gpu(args, cfg, rank, world, local_rank):
+    import torch
+    from paper_2411_15707_b200 import nimbus as nb
+
+    torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
+    impl = nb.IMPL_TCGEN05 if args.impl == "tcgen05" else nb.IMPL_CUDACORE
+    ctx = nb.nimbus_ctx_create(cfg.N, cfg.L, cfg.ell, cfg.L_out, impl, device=local_rank)
+    sk = nb.nimbus_keygen(ctx, cfg.seed_cfg)
+    # setup (untimed, reported separately): encrypt every weight matrix of the workload
+    mats = []
+    t_setup = 0.0
+    enc_bytes = 0
+    for li, pj, lay in cfg.layers:
+        seed = ni.seed_mm(cfg.cid, li, pj)
+        W = nb.from_numpy_u32(ni.gen_W(seed, lay.m, lay.n, cfg.ell), dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        encw = nb.nimbus_encrypt_weights(ctx, sk, W, seed)
+        torch.cuda.synchronize()
+        t_setup += time.perf_counter() - t0
+        del W
+        enc_bytes += nb.nimbus_encw_bytes(encw)
+        # per-rank independent queries (weak scaling): X seeded by rank
+        xseed = seed ^ (rank << 40)
+        X = nb.from_numpy_u32(ni.gen_X(xseed, lay.k, lay.m, cfg.ell), dev)
+        cts, R = nb.alloc_outputs(ctx, encw, lay.k_per_query, lay.n_queries)
+        mats.append(dict(lay=lay, seed=seed, encw=encw, X=X, cts=cts, R=R,
+                         ws_bytes=nb.nimbus_cop_workspace_size(ctx, encw, lay.k)))
+    # one workspace shared by every matmul of the step (they run in stream order)
+    ws = torch.empty(max(mt["ws_bytes"] for mt in mats), dtype=torch.uint8, device=dev)
+    for mt in mats:
+        mt["ws"] = ws
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for mt in mats:
+            lay = mt["lay"]
+            nb.nimbus_cop_matmul(ctx, mt["encw"], mt["X"], lay.k_per_query, lay.n_queries, mt["seed"],
+                                 mt["cts"], mt["R"], mt["ws"])
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    # clock spin-up outside the workload (memory writes only)
+    t0 = time.time()
+    while time.time() - t0 < 0.3:
+        flush.zero_()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    nb.nimbus_profile_enable(ctx, True)
+    nb.nimbus_profile_read(ctx, reset=True)
+    launches0 = nb.nimbus_launch_count(ctx)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()                       # evict Enc(W) from L2 between timed steps
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = nb.nimbus_launch_count(ctx) - launches0
+    stage_ms, calls = nb.nimbus_profile_read(ctx, reset=True)
+    nb.nimbus_profile_enable(ctx, False)
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # ---------------- e2e through the host-buffer C-ABI call (H2D X + D2H cts,R inside)
+    e2e = None
+    if not args.no_e2e:
+        hosts = []
+        for mt in mats:
+            lay = mt["lay"]
+            Xh = mt["X"].cpu().pin_memory()
+            ch, Rh = nb.alloc_outputs(ctx, mt["encw"], lay.k_per_query, lay.n_queries, pin=True, device="cpu")
+            hosts.append((Xh, ch, Rh))
+        h2d = sum(h[0].numel() * 4 for h in hosts)
+        d2h = sum(h[1].numel() * 4 + h[2].numel() * 4 for h in hosts)
+
+        def step_host():
+            for mt, (Xh, ch, Rh) in zip(mats, hosts):
+                lay = mt["lay"]
+                nb.nimbus_cop_matmul_host(ctx, mt["encw"], Xh, lay.k_per_query, lay.n_queries, mt["seed"],
+                                          ch, Rh, mt["ws"])
+        for _ in range(max(3, args.warmup)):
+            step_host()
+        ke = max(3, min(args.steps, 50))
+        e2e_ms = []
+        for _ in range(ke):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            step_host()                      # synchronises the stream before returning
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_step = statistics.median(e2e_ms)
+        if world > 1:
+            t = torch.tensor([e2e_step], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_step = float(t.item())
+        e2e = dict(step_ms=e2e_step, h2d=h2d, d2h=d2h)
+    return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=stage_ms, calls=calls, launches=launches,
+                clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e)
+
+
+# ----------------------------------------------------------------- CPU oracle
+def oracle_sample(cfg, budget_s, rows_cap=None):
+    """Time the oracle (as it stands) on a bounded row sample of the workload:
+    the first matrix of the config, steps 2-4 on `rows` rows (whole packed
+    groups), grown until ~budget_s of CPU work.  Returns (modMAC/s, desc, cores)."""
+    from oracle import oracle as O
+    li, pj, lay = cfg.layers[0]
+    seed = ni.seed_mm(cfg.cid, li, pj)
+    pr = O.primes(cfg.N, cfg.L)
+    s = O.keygen(cfg.N, cfg.seed_cfg)
+    W = ni.gen_W(seed, lay.m, lay.n, cfg.ell)
+    t0 = time.perf_counter()
+    E = O.encrypt_rows(cfg.N, cfg.L, pr, cfg.ell, s, W, seed)
+    t_enc = time.perf_counter() - t0
+    R = cfg.N // lay.n
+    rows = min(lay.k_per_query, R)
+    done_macs, done_t, reps = 0, 0.0, 0
+    while True:
+        X = ni.gen_X(seed, rows, lay.m, cfg.ell)
+        t0 = time.perf_counter()
+        O.cop_matmul(cfg.N, cfg.L, cfg.L_out, pr, cfg.ell, E, X, lay.n, rows, 1, seed)
+        dt = time.perf_counter() - t0
+        done_macs += ni.modmacs(rows, lay.m, cfg.N, cfg.L)
+        done_t += dt
+        reps += 1
+        if done_t >= budget_s or (rows_cap and rows >= rows_cap):
+            break
+        if rows < lay.k_per_query:
+            rows = min(lay.k_per_query, rows * 2)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    desc = (f"{cfg.name} matrix {lay.name} (m={lay.m}, n={lay.n}): oracle steps 2-4 on up to {rows} rows "
+            f"x {reps} runs, {done_t:.1f} s CPU wall; Enc(W) setup {t_enc:.1f} s untimed")
+    return done_macs / done_t, desc, cores
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    li, pj, lay = cfg.layers[0]
+    seed = ni.seed_mm(cfg.cid, li, pj)
+    pr = O.primes(cfg.N, cfg.L)
+    s = O.keygen(cfg.N, cfg.seed_cfg)
+    W = ni.gen_W(seed, lay.m, lay.n, cfg.ell)
+    E = O.encrypt_rows(cfg.N, cfg.L, pr, cfg.ell, s, W, seed)
+    R = cfg.N // lay.n
+    # calibrate one packed group, then size each step so the run stays ~ within 120 s
+    rows = min(R, lay.k_per_query)
+    X = ni.gen_X(seed, rows, lay.m, cfg.ell)
+    t0 = time.perf_counter()
+    O.cop_matmul(cfg.N, cfg.L, cfg.L_out, pr, cfg.ell, E, X, lay.n, rows, 1, seed)
+    t1 = time.perf_counter() - t0
+    per_row = t1 / rows
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    rows = int(max(1, min(lay.k_per_query, budget / per_row)))
+    X = ni.gen_X(seed, rows, lay.m, cfg.ell)
+    for _ in range(args.warmup):
+        O.cop_matmul(cfg.N, cfg.L, cfg.L_out, pr, cfg.ell, E, X, lay.n, rows, 1, seed)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.cop_matmul(cfg.N, cfg.L, cfg.L_out, pr, cfg.ell, E, X, lay.n, rows, 1, seed)
+        times.append(time.perf_counter() - t0)
+    macs = ni.modmacs(rows, lay.m, cfg.N, cfg.L)
+    value = macs * len(times) / sum(times)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = (f"{rows} of {lay.k} rows of {cfg.name} matrix {lay.name} per step (oracle steps 2-4: "
+              f"contraction + packing + mod-switch + mask)")
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u128", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "sample_rows": rows},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ----------------------------------------------------------------- main
+def main():
+    args = parse()
+    cfg = get_config(args.config)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        out = run_reference(args, cfg, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    res = run_gpu(args, cfg, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    lays = [l for _, _, l in cfg.layers]
+    macs_step = sum(ni.modmacs(l.k, l.m, cfg.N, cfg.L) for l in lays)
+    ms_step = res["total_ms"] / args.steps
+    value = macs_step * world / (ms_step / 1e3)
+    # roofline of the dominant kernel (the contraction, stage 1)
+    SX, SW = sx_of(cfg.ell), 4
+    contract_ms = res["stage_ms"][1] / max(1, res["calls"])           # per launch
+    per_launch_macs = macs_step / len(lays)
+    ops = 2 * per_launch_macs * SX * SW                                  # int8 tensor ops
+    hbm_bytes = sum(4 * l.m * 2 * cfg.L * cfg.N + SX * l.k * l.m + 4 * l.k * 2 * cfg.L * cfg.N
+                    for l in lays) / len(lays)                           # Enc(W) + X slices + C
+    i8_peak = 2.0 * (peaks["bf16_tflops"] if ms_step < 50 else peaks["bf16_tflops_sustained"])
+    t_i8 = ops / (i8_peak * 1e12)
+    t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
+    tens = {"bound": "tensor", "achieved": ops / (contract_ms / 1e3) / 1e12, "peak": i8_peak,
+            "unit": "TFLOP/s"}
+    tens["frac"] = tens["achieved"] / tens["peak"]
+    hbm = {"bound": "hbm", "achieved": hbm_bytes / (contract_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
+           "unit": "GB/s"}
+    hbm["frac"] = hbm["achieved"] / hbm["peak"]
+    prim, alt = (tens, hbm) if t_i8 >= t_hbm else (hbm, tens)
+    prim = dict(prim)
+    prim["traffic"] = None
+    prim["kernel"] = "k_cop_tc (tcgen05 kind::i8 contraction)" if args.impl == "tcgen05" else "k_cop_cc"
+    prim["peak_src"] = (f"{peaks['src']}: int8 = 2 x bf16 {'burst' if ms_step < 50 else 'sustained'}"
+                        if prim["bound"] == "tensor" else f"{peaks['src']} hbm_gbs")
+    prim["ops_per_launch"] = ops if prim["bound"] == "tensor" else hbm_bytes
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": workload_name(cfg), "config": cfg.name, "k": lays[0].k, "matmuls_per_step": len(lays),
+                   "impl": args.impl, "l2": f"flushed by a {L2_FLUSH_BYTES >> 20} MiB write before every timed step",
+                   "enc_w_bytes_resident": res["enc_bytes"]},
+        "roofline": prim,
+        "roofline_other": alt,
+        "stages_ms_per_step": {"slice_x": res["stage_ms"][0] / args.steps,
+                               "contraction": res["stage_ms"][1] / args.steps,
+                               "pack_moddown_mask": res["stage_ms"][2] / args.steps},
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+        "setup_encrypt_s": res["t_setup"],
+    }
+    if res["e2e"] is not None:
+        e = res["e2e"]
+        out["e2e"] = {"value": macs_step * world / (e["step_ms"] / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"], "ms_per_step": e["step_ms"]}
+    if world == 1 and not args.no_cpu_baseline:
+        v, desc, cores = oracle_sample(cfg, args.cpu_budget_s)
+        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

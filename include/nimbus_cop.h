@@ -170,6 +170,15 @@ nimbus_status nimbus_negacyclic_mul(nimbus_ctx* ctx, const uint32_t* d_a, const 
 /* Number of library kernels launched through this context since creation. */
 uint64_t nimbus_launch_count(const nimbus_ctx* ctx);
 
+/* Per-stage CUDA-event timing of nimbus_cop_matmul (for the bench's live
+ * roofline numbers).  When enabled, each stage -- [0] slice X (K4),
+ * [1] contraction (K5/K6), [2] pack + mod-switch + mask (K7) -- is bracketed by
+ * events recorded on the caller's stream.  nimbus_profile_read synchronises
+ * those events and returns the accumulated milliseconds per stage in ms[3]
+ * and the number of profiled calls; reset != 0 clears the totals. */
+nimbus_status nimbus_profile_enable(nimbus_ctx* ctx, int on);
+nimbus_status nimbus_profile_read(nimbus_ctx* ctx, double* ms, uint64_t* calls, int reset);
+
 #ifdef __cplusplus
 }
 #endif

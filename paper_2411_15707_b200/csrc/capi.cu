@@ -2,6 +2,7 @@
 // validation, RNS constant / twiddle derivation, handle management, and the
 // launch sequence of each entry point.  All arithmetic runs in the kernels.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -91,6 +92,7 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
     ctx->prm = *prm;
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
+    if (const char* cl = getenv("NIMBUS_CLUSTER")) ctx->cluster = atoi(cl) == 1 ? 1 : 2;
     Rns& R = ctx->rns;
     R.N = N; R.L = L; R.L_out = Lo; R.ell = ell;
     R.logN = 0; while ((1u << R.logN) < N) R.logN++;
@@ -119,7 +121,13 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
         R.mu[i] = (uint64_t)((((u128)1) << 64) / p);
         R.t_inv[i] = (uint32_t)h_inv((uint64_t)(t % p), p);
         for (uint32_t s = 0; s < 8; s++) R.pow8[i][s] = (uint32_t)h_pow(2, 8 * s, p);
-        for (uint32_t l = 0; l < L; l++) R.inv_p[l][i] = (l == i) ? 0 : (uint32_t)h_inv(R.p[l], p);
+        R.c32[i] = (uint32_t)(((u128)1 << 32) % p);
+        if (R.c32[i] >= (1u << 21)) { delete ctx; return NIMBUS_EINVAL; }   // reduce64_pm precondition
+        R.t_inv_sh[i] = (uint32_t)(((uint64_t)R.t_inv[i] << 32) / p);
+        for (uint32_t l = 0; l < L; l++) {
+            R.inv_p[l][i] = (l == i) ? 0 : (uint32_t)h_inv(R.p[l], p);
+            R.inv_p_sh[l][i] = (uint32_t)(((uint64_t)R.inv_p[l][i] << 32) / p);
+        }
         R.ninv[i] = (uint32_t)h_inv(N, p);
         R.ninv_sh[i] = (uint32_t)(((uint64_t)R.ninv[i] << 32) / p);
     }
@@ -157,6 +165,8 @@ void nimbus_ctx_destroy(nimbus_ctx* ctx) {
     if (!ctx) return;
     if (ctx->d_tw) cudaFree(ctx->d_tw);
     if (ctx->d_flag) cudaFree(ctx->d_flag);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->ev_pending) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -221,7 +231,7 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     nimbus_encw* w = new (std::nothrow) nimbus_encw();
     if (!w) return NIMBUS_ENOMEM;
     w->ctx = ctx; w->m = m; w->n = n; w->KB = (m + kBK - 1) / kBK;
-    w->bytes = (size_t)w->KB * kBK * ncols(ctx) * 4;
+    w->bytes = (size_t)w->KB * kBK * col_tiles(ctx) * kBNT * 4;
     cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
     if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "encw alloc"); }
     *out = w;
@@ -316,13 +326,27 @@ static nimbus_status check_online(nimbus_ctx* ctx, const nimbus_encw* w, uint32_
     return NIMBUS_OK;
 }
 
+// stage events: ev[0] before slice, ev[1] after slice, ev[2] after contraction, ev[3] after pack
+static cudaEvent_t prof_event(nimbus_ctx* ctx) {
+    cudaEvent_t e;
+    if (!ctx->ev_pool.empty()) { e = ctx->ev_pool.back(); ctx->ev_pool.pop_back(); }
+    else cudaEventCreate(&e);
+    ctx->ev_pending.push_back(e);
+    return e;
+}
+static void prof_mark(nimbus_ctx* ctx, cudaStream_t s) {
+    if (ctx->profile) cudaEventRecord(prof_event(ctx), s);
+}
+
 static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                     uint32_t* d_C, uint8_t* ws, cudaStream_t s) {
     if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
         uint8_t* xt = ws + ws_layout(ctx, w, k).xt;
         CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, xt, s), "slice X");
+        prof_mark(ctx, s);
         CK(launch_cop_tcgen05(ctx, w, xt, k, d_C, s), "cop tcgen05");
     } else {
+        prof_mark(ctx, s);
         CK(launch_cop_cudacore(ctx, w, d_X, k, d_C, s), "cop cudacore");
     }
     return NIMBUS_OK;
@@ -334,7 +358,11 @@ nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
     if (st != NIMBUS_OK && st != NIMBUS_ENOISE) return st;
     if (!d_X || !d_C || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
     if (ws_bytes < ws_layout(ctx, w, k).total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
-    return run_accumulate(ctx, w, d_X, k, d_C, (uint8_t*)d_ws, (cudaStream_t)stream);
+    const bool pf = ctx->profile;
+    ctx->profile = false;
+    st = run_accumulate(ctx, w, d_X, k, d_C, (uint8_t*)d_ws, (cudaStream_t)stream);
+    ctx->profile = pf;
+    return st;
 }
 
 nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
@@ -356,9 +384,38 @@ nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uin
     if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t* C = reinterpret_cast<uint32_t*>((uint8_t*)d_ws + L.c);
+    prof_mark(ctx, s);
     st = run_accumulate(ctx, w, d_X, k, C, (uint8_t*)d_ws, s);
     if (st != NIMBUS_OK) return st;
+    prof_mark(ctx, s);
     CK(launch_pack(ctx, C, kq, nq, w->n, seed, d_cts, d_R, s), "pack");
+    prof_mark(ctx, s);
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_profile_enable(nimbus_ctx* ctx, int on) {
+    if (!ctx) return NIMBUS_EINVAL;
+    ctx->profile = on != 0;
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_profile_read(nimbus_ctx* ctx, double* ms, uint64_t* calls, int reset) {
+    if (!ctx) return NIMBUS_EINVAL;
+    auto& P = ctx->ev_pending;
+    for (size_t i = 0; i + 4 <= P.size(); i += 4) {
+        CK(cudaEventSynchronize(P[i + 3]), "profile sync");
+        float a = 0, b = 0, c = 0;
+        cudaEventElapsedTime(&a, P[i], P[i + 1]);
+        cudaEventElapsedTime(&b, P[i + 1], P[i + 2]);
+        cudaEventElapsedTime(&c, P[i + 2], P[i + 3]);
+        ctx->prof_ms[0] += a; ctx->prof_ms[1] += b; ctx->prof_ms[2] += c;
+        ctx->prof_calls++;
+    }
+    for (cudaEvent_t e : P) ctx->ev_pool.push_back(e);
+    P.clear();
+    if (ms) for (int i = 0; i < 3; i++) ms[i] = ctx->prof_ms[i];
+    if (calls) *calls = ctx->prof_calls;
+    if (reset) { ctx->prof_ms[0] = ctx->prof_ms[1] = ctx->prof_ms[2] = 0; ctx->prof_calls = 0; }
     return NIMBUS_OK;
 }
 

@@ -16,10 +16,13 @@ struct Rns {
     uint32_t p[NIMBUS_MAXL];
     uint64_t mu[NIMBUS_MAXL];            // floor(2^64 / p_i)            (Barrett)
     uint32_t inv_p[NIMBUS_MAXL][NIMBUS_MAXL];  // inv_p[l][i] = p_l^-1 mod p_i (mod-switch)
+    uint32_t inv_p_sh[NIMBUS_MAXL][NIMBUS_MAXL];  // Shoup companions floor(inv_p * 2^32 / p_i)
     uint32_t t_inv[NIMBUS_MAXL];         // t^-1 mod p_i                 (embedding)
+    uint32_t t_inv_sh[NIMBUS_MAXL];      // floor(t_inv * 2^32 / p_i)
     uint32_t q_mod_t;                    // q mod t, q = prod of all L primes
     uint32_t qout_mod_t;                 // q' mod t, q' = prod of the first L_out primes
     uint32_t pow8[NIMBUS_MAXL][8];       // 2^(8s) mod p_i                (slice recombination)
+    uint32_t c32[NIMBUS_MAXL];           // 2^32 mod p_i (< 2^21 required by reduce64_pm)
     uint32_t ninv[NIMBUS_MAXL], ninv_sh[NIMBUS_MAXL];  // N^-1 mod p_i and its Shoup companion
 };
 
@@ -74,6 +77,22 @@ __device__ __forceinline__ uint32_t mulmod_shoup(uint32_t a, uint32_t w, uint32_
     return r >= p ? r - p : r;
 }
 
+// a * b + c with a 32x32 -> 64-bit multiply-add (one IMAD.WIDE.U32)
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) { return (uint64_t)a * b + c; }
+
+// x mod p for any 64-bit x when c32 = 2^32 mod p < 2^21 (true for the primes
+// within 2^20 of 2^31 that the context derives): fold x = hi 2^32 + lo ->
+// hi c32 + lo five times (64 -> 54 -> 44 -> 34 -> 33 -> 32 bits), then at most
+// two conditional subtractions (2^32 < 3p).
+__device__ __forceinline__ uint32_t reduce64_pm(uint64_t x, uint32_t p, uint32_t c32) {
+#pragma unroll
+    for (int f = 0; f < 5; f++) x = mad_wide((uint32_t)(x >> 32), c32, (uint32_t)x);
+    uint32_t r = (uint32_t)x;
+    r = r >= p ? r - p : r;
+    r = r >= p ? r - p : r;
+    return r;
+}
+
 // Emb(w) mod p_i for w in [0,t): floor((Q w + t/2)/t) = (Q w + t/2 - f)/t with
 // f = (Q w + t/2) mod t; since p_i | Q this is (t/2 - f) * t^-1 mod p_i.
 // (SURVEY.md §8(c) #4.)  qmodt = Q mod t.
@@ -125,6 +144,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
         :: "r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// Same, multicast to every CTA of the cluster in cta_mask (same smem offset, and
+// complete_tx on the mbarrier at the same offset in each destination CTA).
+__device__ __forceinline__ void bulk_g2s_mc(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
+                                            uint32_t cta_mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4, %5;"
+        :: "r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "h"((uint16_t)cta_mask),
+           "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -135,6 +173,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+
+// ------------------------------------------------------------------ PDL
+// Programmatic dependent launch: wait for the preceding kernel of the stream
+// (complete, memory visible) / allow the next one to be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ------------------------------------------------------------------ PTX: tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
@@ -164,6 +208,11 @@ __device__ __forceinline__ void mma_i8_ss(uint32_t tmem_d, uint64_t adesc, uint6
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                  :: "r"(smem_u32(bar)) : "memory");
+}
+// arrive on the mbarrier at this offset in every CTA of cta_mask when all prior MMAs complete
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint32_t cta_mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 :: "r"(smem_u32(bar)), "h"((uint16_t)cta_mask) : "memory");
 }
 // 32 lanes x 32b, 16 consecutive columns per thread
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {

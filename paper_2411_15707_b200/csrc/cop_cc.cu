@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kCcCols) k_cop_cc(Rns R, const uint8_t* __rest
 cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                 uint32_t* d_C, cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    dim3 g(ncol / kCcCols, (k + kCcRows - 1) / kCcRows);
+    dim3 g((ncol + kCcCols - 1) / kCcCols, (k + kCcRows - 1) / kCcRows);
     if (c->rns.ell <= 16) k_cop_cc<false><<<g, kCcCols, 0, st>>>(c->rns, w->d_Et, d_X, k, w->m, w->KB, ncol, d_C);
     else k_cop_cc<true><<<g, kCcCols, 0, st>>>(c->rns, w->d_Et, d_X, k, w->m, w->KB, ncol, d_C);
     c->launches++;

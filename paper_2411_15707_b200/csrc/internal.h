@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../../include/nimbus_cop.h"
@@ -12,7 +13,7 @@ typedef unsigned __int128 u128;
 
 // Kernel-layout geometry of Enc(W) and of the sliced X.
 constexpr uint32_t kBK = 128;      // beta (contraction) bytes per k-block = one 128-B swizzle row
-constexpr uint32_t kBNT = 64;      // coefficient columns per Enc(W) tile
+constexpr uint32_t kBNT = 48;      // coefficient columns per Enc(W) tile (4 planes -> MMA N = 192)
 constexpr uint32_t kBM = 128;      // rows (alpha) per X tile = tcgen05 M
 constexpr uint32_t kSW = 4;        // 8-bit slices of a 31-bit residue (S_w)
 
@@ -26,6 +27,12 @@ struct nimbus_ctx {
     std::string err;
     uint64_t launches = 0;
     int num_sms = 148;
+    int cluster = 2;               // CTAs per cluster of the tcgen05 contraction (A multicast); env NIMBUS_CLUSTER
+    // stage profiling (nimbus_profile_*): pending event quadruples, accumulated ms
+    bool profile = false;
+    std::vector<cudaEvent_t> ev_pool, ev_pending;
+    double prof_ms[3] = {0, 0, 0};
+    uint64_t prof_calls = 0;
 };
 
 struct nimbus_sk {
@@ -43,6 +50,9 @@ struct nimbus_encw {
 
 // number of 8-bit slices of an ell-bit X entry (S_x)
 inline uint32_t sx_of(uint32_t ell) { return ell <= 8 ? 1 : ell <= 16 ? 2 : 4; }
+// number of 48-column Enc(W) tiles covering the 2 L N coefficient columns (last one zero padded)
+// (rounded up to an even count so column tiles pair up in 2-CTA clusters)
+inline uint32_t col_tiles(const nimbus_ctx* c) { return (((2 * c->rns.L * c->rns.N + kBNT - 1) / kBNT) + 1) & ~1u; }
 
 // ---------------------------------------------------------------- launchers
 namespace nimbus {
@@ -73,3 +83,21 @@ cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint3
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st);
 }  // namespace nimbus
+
+// Launch with programmatic dependent launch (PDL) allowed: the kernel may be
+// scheduled while its stream predecessor is still running; it must call
+// nimbus::pdl_wait() before touching data that predecessor produces.
+template <typename K, typename... Args>
+static inline cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}

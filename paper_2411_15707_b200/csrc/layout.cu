@@ -2,7 +2,7 @@
 //   K4  slice X into 8-bit planes in the tcgen05 operand layout (A3)
 //   tile / untile Enc(W) between the canonical [beta][comp][limb][j] layout
 //       and the resident byte-plane kernel layout (setup / export)
-//   K7  RShift packing + mod-switch + mask (A5, A6; Alg. 1 steps 3-4)
+//   (K7, packing + mod-switch + mask, is in pack.cu)
 //
 // Kernel layout of a byte-plane tile: a 2-D block of
 // R rows x 128 bytes, row r at offset r*128, the 16-byte chunk c of row r
@@ -23,6 +23,8 @@ __device__ __forceinline__ uint32_t swz_off(uint32_t r, uint32_t chunk) {
 template <int SX>
 __global__ void k_slice_x(const uint32_t* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB, uint32_t ell,
                           uint8_t* __restrict__ Xt, uint32_t total, uint32_t* flag, int check) {
+    pdl_trigger();
+    pdl_wait();          // Xt may still be read by the previous contraction in the stream
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= total) return;
     const uint32_t alpha = idx / (KB * 8), ch = idx % (KB * 8);
@@ -62,14 +64,16 @@ __global__ void k_slice_x(const uint32_t* __restrict__ X, uint32_t k, uint32_t m
 
 // ---------------------------------------------------------------- tile Enc(W)
 // CTA (ct, kb): canonical E[beta][col] for beta in the k-block, col in the
-// 64-column tile -> 4 byte planes Et[ct][kb][s][64][128 B swizzled].
+// 48-column tile -> 4 byte planes Et[ct][kb][s][48][128 B swizzled]; rows
+// beta >= m and columns >= 2LN (last tile) are zero.
 __global__ void __launch_bounds__(256) k_tile_encw(const uint32_t* __restrict__ canon, uint32_t m,
                                                    uint32_t ncol, uint32_t KB, uint8_t* __restrict__ Et) {
     __shared__ uint32_t sE[kBK][kBNT + 1];
     const uint32_t ct = blockIdx.x, kb = blockIdx.y;
     for (uint32_t idx = threadIdx.x; idx < kBK * kBNT; idx += blockDim.x) {
         const uint32_t b = idx / kBNT, c = idx % kBNT, beta = kb * kBK + b;
-        sE[b][c] = beta < m ? canon[(size_t)beta * ncol + (size_t)ct * kBNT + c] : 0u;
+        const size_t col = (size_t)ct * kBNT + c;
+        sE[b][c] = (beta < m && col < ncol) ? canon[(size_t)beta * ncol + col] : 0u;
     }
     __syncthreads();
     uint8_t* base = Et + ((size_t)ct * KB + kb) * kSW * kBNT * kBK;
@@ -102,65 +106,9 @@ __global__ void __launch_bounds__(256) k_untile_encw(const uint8_t* __restrict__
     __syncthreads();
     for (uint32_t idx = threadIdx.x; idx < kBK * kBNT; idx += blockDim.x) {
         const uint32_t b = idx / kBNT, c = idx % kBNT, beta = kb * kBK + b;
-        if (beta < m) canon[(size_t)beta * ncol + (size_t)ct * kBNT + c] = sE[b][c];
+        const size_t col = (size_t)ct * kBNT + c;
+        if (beta < m && col < ncol) canon[(size_t)beta * ncol + col] = sE[b][c];
     }
-}
-
-// ---------------------------------------------------------------- K7 pack/moddown/mask
-// Thread per output coefficient J of packed ciphertext tg = query*nct + theta.
-//  step 3: s_i = sum_{r<rows} X^{r n} c[theta R + r] at J
-//        = sum_r (J >= r n ? C_r[J - r n] : -C_r[J - r n + N])
-//  mod-switch: drop p_{L-1}, ..., p_{L_out}:
-//        c_i <- (c_i - rho) * p_l^-1 mod p_i, rho = centered c_l  ( = round(c / p_l) )
-//  step 4: b_i -= Emb_{q'}(r_theta[J]) mod p_i; R rows = r at valid slots.
-__global__ void __launch_bounds__(256) k_pack(Rns Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
-                                              uint32_t nct, uint64_t key_mask, uint32_t* __restrict__ cts,
-                                              uint32_t* __restrict__ Rout) {
-    const uint32_t N = Rn.N, L = Rn.L, Lo = Rn.L_out;
-    const uint32_t J = blockIdx.x * blockDim.x + threadIdx.x, tg = blockIdx.y;
-    if (J >= N) return;
-    const uint32_t query = tg / nct, theta = tg % nct, Rr = N / n;
-    const uint32_t rows = min(Rr, kq - theta * Rr);
-    const size_t ncol = (size_t)2 * L * N;
-    const size_t row0 = (size_t)query * kq + (size_t)theta * Rr;
-    const uint32_t rmask = samp_mod_t(prg_word(key_mask, (uint64_t)tg * N + J), Rn.ell);
-#pragma unroll 1
-    for (uint32_t comp = 0; comp < 2; comp++) {
-        uint32_t res[NIMBUS_MAXL];
-        for (uint32_t i = 0; i < L; i++) {
-            const uint32_t p = Rn.p[i];
-            uint64_t acc = 0;
-            const uint32_t* base = C + row0 * ncol + ((size_t)comp * L + i) * N;
-            for (uint32_t r = 0; r < rows; r++) {
-                const uint32_t s = r * n;
-                if (J >= s) acc += __ldg(base + r * ncol + (J - s));
-                else        acc += p - __ldg(base + r * ncol + (J + N - s));
-            }
-            res[i] = mod64(acc, p, Rn.mu[i]);
-        }
-        for (uint32_t l = L - 1; l >= Lo; l--) {
-            const uint32_t pl = Rn.p[l];
-            const uint32_t cl = res[l];
-            const bool neg = cl > (pl >> 1);                  // centered rho = cl - pl < 0
-            const uint32_t mag = neg ? pl - cl : cl;          // |rho| < p_l / 2
-            for (uint32_t i = 0; i < l; i++) {
-                const uint32_t p = Rn.p[i];
-                const uint32_t mm = mag >= p ? mag - p : mag;
-                const uint32_t d = neg ? addmod(res[i], mm, p) : submod(res[i], mm, p);
-                res[i] = mulmod(d, Rn.inv_p[l][i], p, Rn.mu[i]);
-            }
-            if (l == 0) break;
-        }
-        for (uint32_t i = 0; i < Lo; i++) {
-            uint32_t v = res[i];
-            if (comp == 0) {
-                const uint32_t p = Rn.p[i];
-                v = submod(v, emb_mod(rmask, Rn.qout_mod_t, Rn.ell, p, Rn.mu[i], Rn.t_inv[i]), p);
-            }
-            cts[(((size_t)tg * 2 + comp) * Lo + i) * N + J] = v;
-        }
-    }
-    if (J < rows * n) Rout[row0 * n + J] = rmask;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -171,17 +119,18 @@ cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint3
     const uint32_t SX = sx_of(c->rns.ell);
     const int check = (c->prm.flags & NIMBUS_FLAG_CHECK_RANGE) && c->rns.ell < 32;
     dim3 g((total + 255) / 256);
-    if (SX == 1) k_slice_x<1><<<g, 256, 0, st>>>(d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
-    else if (SX == 2) k_slice_x<2><<<g, 256, 0, st>>>(d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
-    else k_slice_x<4><<<g, 256, 0, st>>>(d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
+    cudaError_t e;
+    if (SX == 1) e = launch_pdl(k_slice_x<1>, g, 256, 0, st, d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
+    else if (SX == 2) e = launch_pdl(k_slice_x<2>, g, 256, 0, st, d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
+    else e = launch_pdl(k_slice_x<4>, g, 256, 0, st, d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
     c->launches++;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m, uint32_t KB, uint8_t* d_Et,
                              cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    k_tile_encw<<<dim3(ncol / kBNT, KB), 256, 0, st>>>(d_canon, m, ncol, KB, d_Et);
+    k_tile_encw<<<dim3(col_tiles(c), KB), 256, 0, st>>>(d_canon, m, ncol, KB, d_Et);
     c->launches++;
     return cudaGetLastError();
 }
@@ -189,15 +138,7 @@ cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m,
 cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t* d_canon,
                                cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    k_untile_encw<<<dim3(ncol / kBNT, KB), 256, 0, st>>>(d_Et, m, ncol, KB, d_canon);
-    c->launches++;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
-                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st) {
-    const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
-    k_pack<<<dim3((N + 255) / 256, nq * nct), 256, 0, st>>>(c->rns, d_C, kq, n, nct, prg_key(seed, 6), d_cts, d_R);
+    k_untile_encw<<<dim3(col_tiles(c), KB), 256, 0, st>>>(d_Et, m, ncol, KB, d_canon);
     c->launches++;
     return cudaGetLastError();
 }

@@ -59,6 +59,8 @@ _SIGS = {
     "nimbus_prg_words": (C.c_int, [_u64, _u32, _u64, _u64, _vp, _vp]),
     "nimbus_negacyclic_mul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp]),
     "nimbus_launch_count": (_u64, [_vp]),
+    "nimbus_profile_enable": (C.c_int, [_vp, C.c_int]),
+    "nimbus_profile_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(_u64), C.c_int]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -317,6 +319,18 @@ def nimbus_negacyclic_mul(ctx: Context, a: torch.Tensor, b: torch.Tensor, stream
 
 def nimbus_launch_count(ctx: Context) -> int:
     return int(lib().nimbus_launch_count(ctx.ptr))
+
+
+def nimbus_profile_enable(ctx: Context, on: bool = True):
+    _check(lib().nimbus_profile_enable(ctx.ptr, int(on)), ctx)
+
+
+def nimbus_profile_read(ctx: Context, reset: bool = True):
+    """-> (ms[slice, contraction, pack] accumulated, number of profiled calls)."""
+    ms = (C.c_double * 3)()
+    calls = _u64()
+    _check(lib().nimbus_profile_read(ctx.ptr, ms, C.byref(calls), int(reset)), ctx)
+    return [float(x) for x in ms], int(calls.value)
 
 
 # ------------------------------------------------------------------ helpers

@@ -1,0 +1,52 @@
+"""Timeline of the tcgen05 contraction kernel from the debug trace build
+(NIMBUS_TRACE=1 python paper_2411_15707_b200/_build.py): per-CTA setup,
+PDL wait, per-tile MMA and epilogue intervals (globaltimer ns)."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import nimbus_inputs as ni
+from paper_2411_15707_b200 import nimbus as nb
+
+_var = os.environ.get("NIMBUS_VARIANT", "")
+nb.LIB_PATH = os.path.join(os.path.dirname(nb.LIB_PATH), "libnimbus_cop_trace" + (f"_{_var}" if _var else "") + ".so")
+lib = nb.lib()
+cfg = ni.get = None
+N, L, ell, Lo, m, n, k = (int(x) for x in sys.argv[1:8])
+ctx = nb.nimbus_ctx_create(N, L, ell, Lo)
+sk = nb.nimbus_keygen(ctx, 1)
+w = nb.nimbus_encrypt_weights(ctx, sk, nb.from_numpy_u32(ni.gen_W(1, m, n, ell), "cuda"), 1)
+X = nb.from_numpy_u32(ni.gen_X(2, k, m, ell), "cuda")
+ws = nb.alloc_workspace(ctx, w, k)
+cts, R = nb.alloc_outputs(ctx, w, k, 1)
+tr = torch.zeros(148 * 64, dtype=torch.int64, device="cuda")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+for _ in range(3):
+    nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
+lib.nimbus_trace_set(ctypes.c_void_p(tr.data_ptr()))
+flush.zero_()
+torch.cuda.synchronize()
+nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
+torch.cuda.synchronize()
+lib.nimbus_trace_set(ctypes.c_void_p(0))
+t = tr.cpu().numpy().reshape(148, 64).astype(np.int64)
+t0 = t[:, 0][t[:, 0] > 0].min()
+us = lambda x: (x - t0) / 1e3 if x > 0 else float("nan")
+print(f"N={N} L={L} ell={ell} m={m} n={n} k={k}")
+ends = []
+for c in (0, 1, 2, 50, 100, 147):
+    row = t[c]
+    s = f"cta {c:3d}: start {us(row[0]):6.2f} setup {us(row[1]):6.2f} pdl {us(row[2]):6.2f} end {us(row[3]):6.2f} |"
+    for ti in range(15):
+        if row[4 + 4 * ti] == 0:
+            break
+        s += f" t{ti}: mma {us(row[4+4*ti]):.1f}-{us(row[5+4*ti]):.1f} epi {us(row[6+4*ti]):.1f}-{us(row[7+4*ti]):.1f} |"
+    print(s)
+e = np.array([us(x) for x in t[:, 3] if x > 0])
+print(f"CTA end: min {e.min():.2f} median {np.median(e):.2f} max {e.max():.2f} us")
+st = np.array([us(x) for x in t[:, 0] if x > 0])
+print(f"CTA start: min {st.min():.2f} max {st.max():.2f}")
