@@ -92,7 +92,7 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
     ctx->prm = *prm;
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
-    if (const char* cl = getenv("NIMBUS_CLUSTER")) ctx->cluster = atoi(cl) == 1 ? 1 : 2;
+    if (const char* cl = getenv("NIMBUS_CLUSTER")) ctx->cluster = atoi(cl) == 2 ? 2 : 1;
     Rns& R = ctx->rns;
     R.N = N; R.L = L; R.L_out = Lo; R.ell = ell;
     R.logN = 0; while ((1u << R.logN) < N) R.logN++;
@@ -231,7 +231,9 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     nimbus_encw* w = new (std::nothrow) nimbus_encw();
     if (!w) return NIMBUS_ENOMEM;
     w->ctx = ctx; w->m = m; w->n = n; w->KB = (m + kBK - 1) / kBK;
-    w->bytes = (size_t)w->KB * kBK * col_tiles(ctx) * kBNT * 4;
+    // resident-X kernel (tcgen05, ell <= 16, m <= 768) uses 32-column tiles, the streaming kernel 48
+    w->bn = (ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && sx_of(ctx->rns.ell) == 2 && w->KB <= kResMaxKB && !getenv("NIMBUS_NO_RESIDENT")) ? kBNR : kBNT;
+    w->bytes = (size_t)w->KB * kBK * col_tiles(ctx, w->bn) * w->bn * 4;
     cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
     if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "encw alloc"); }
     *out = w;
@@ -249,7 +251,7 @@ nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const
     uint32_t* canon = nullptr;
     cudaError_t e = cudaMallocAsync(&canon, (size_t)m * ncols(ctx) * 4, s);
     if (e == cudaSuccess) e = launch_encrypt(ctx, sk->d_s_ntt, d_W, m, n, seed, canon, s);
-    if (e == cudaSuccess) e = launch_tile_encw(ctx, canon, m, w->KB, w->d_Et, s);
+    if (e == cudaSuccess) e = launch_tile_encw(ctx, canon, m, w->KB, w->bn, w->d_Et, s);
     if (canon) cudaFreeAsync(canon, s);
     if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encrypt_weights"); }
     *out = w;
@@ -267,7 +269,7 @@ size_t nimbus_encw_bytes(const nimbus_encw* w) { return w ? w->bytes : 0; }
 nimbus_status nimbus_encw_export(const nimbus_encw* w, uint32_t* d_out, void* stream) {
     if (!w || !d_out) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
-    CK(launch_untile_encw(ctx, w->d_Et, w->m, w->KB, d_out, (cudaStream_t)stream), "encw export");
+    CK(launch_untile_encw(ctx, w->d_Et, w->m, w->KB, w->bn, d_out, (cudaStream_t)stream), "encw export");
     return NIMBUS_OK;
 }
 
@@ -278,7 +280,7 @@ nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t
     nimbus_encw* w = nullptr;
     nimbus_status st = new_encw(ctx, m, n, &w);
     if (st != NIMBUS_OK) return st;
-    cudaError_t e = launch_tile_encw(ctx, d_in, m, w->KB, w->d_Et, (cudaStream_t)stream);
+    cudaError_t e = launch_tile_encw(ctx, d_in, m, w->KB, w->bn, w->d_Et, (cudaStream_t)stream);
     if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encw import"); }
     *out = w;
     return NIMBUS_OK;

@@ -23,12 +23,14 @@ __device__ __forceinline__ uint32_t assemble(uint32_t p0, uint32_t p1, uint32_t 
 template <bool WIDE>
 __global__ void __launch_bounds__(kCcCols) k_cop_cc(Rns R, const uint8_t* __restrict__ Et,
                                                     const uint32_t* __restrict__ X, uint32_t k, uint32_t m,
-                                                    uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
+                                                    uint32_t KB, uint32_t bn, uint32_t ncol,
+                                                    uint32_t* __restrict__ C) {
     __shared__ uint32_t sX[kCcRows][kBK];
-    const uint32_t col = blockIdx.x * kCcCols + threadIdx.x;
-    const uint32_t ct = col / kBNT, r = col % kBNT;
+    const uint32_t col = blockIdx.x * kCcCols + threadIdx.x;   // ncol is a multiple of 128
+    const uint32_t ct = col / bn, r = col % bn;
     const uint32_t alpha0 = blockIdx.y * kCcRows;
     const uint32_t limb = (col / R.N) % R.L, p = R.p[limb];
+    const size_t plane = (size_t)bn * kBK;
     uint64_t acc[kCcRows];
     uint32_t carry[kCcRows];
 #pragma unroll
@@ -41,14 +43,14 @@ __global__ void __launch_bounds__(kCcCols) k_cop_cc(Rns R, const uint8_t* __rest
             sX[rr][b] = (alpha < k && beta < m) ? X[(size_t)alpha * m + beta] : 0u;
         }
         __syncthreads();
-        const uint8_t* tb = Et + ((size_t)ct * KB + kb) * kSW * kBNT * kBK;
+        const uint8_t* tb = Et + ((size_t)ct * KB + kb) * kSW * plane;
 #pragma unroll 1
         for (uint32_t c16 = 0; c16 < 8; c16++) {
             const uint32_t off = r * 128u + ((c16 ^ (r & 7u)) << 4);
-            const uint4 P0 = __ldg(reinterpret_cast<const uint4*>(tb + 0 * kBNT * kBK + off));
-            const uint4 P1 = __ldg(reinterpret_cast<const uint4*>(tb + 1 * kBNT * kBK + off));
-            const uint4 P2 = __ldg(reinterpret_cast<const uint4*>(tb + 2 * kBNT * kBK + off));
-            const uint4 P3 = __ldg(reinterpret_cast<const uint4*>(tb + 3 * kBNT * kBK + off));
+            const uint4 P0 = __ldg(reinterpret_cast<const uint4*>(tb + 0 * plane + off));
+            const uint4 P1 = __ldg(reinterpret_cast<const uint4*>(tb + 1 * plane + off));
+            const uint4 P2 = __ldg(reinterpret_cast<const uint4*>(tb + 2 * plane + off));
+            const uint4 P3 = __ldg(reinterpret_cast<const uint4*>(tb + 3 * plane + off));
             const uint32_t w0[4] = {P0.x, P0.y, P0.z, P0.w}, w1[4] = {P1.x, P1.y, P1.z, P1.w};
             const uint32_t w2[4] = {P2.x, P2.y, P2.z, P2.w}, w3[4] = {P3.x, P3.y, P3.z, P3.w};
 #pragma unroll
@@ -82,9 +84,11 @@ __global__ void __launch_bounds__(kCcCols) k_cop_cc(Rns R, const uint8_t* __rest
 cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                 uint32_t* d_C, cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    dim3 g((ncol + kCcCols - 1) / kCcCols, (k + kCcRows - 1) / kCcRows);
-    if (c->rns.ell <= 16) k_cop_cc<false><<<g, kCcCols, 0, st>>>(c->rns, w->d_Et, d_X, k, w->m, w->KB, ncol, d_C);
-    else k_cop_cc<true><<<g, kCcCols, 0, st>>>(c->rns, w->d_Et, d_X, k, w->m, w->KB, ncol, d_C);
+    dim3 g(ncol / kCcCols, (k + kCcRows - 1) / kCcRows);
+    if (c->rns.ell <= 16)
+        k_cop_cc<false><<<g, kCcCols, 0, st>>>(c->rns, w->d_Et, d_X, k, w->m, w->KB, w->bn, ncol, d_C);
+    else
+        k_cop_cc<true><<<g, kCcCols, 0, st>>>(c->rns, w->d_Et, d_X, k, w->m, w->KB, w->bn, ncol, d_C);
     c->launches++;
     return cudaGetLastError();
 }

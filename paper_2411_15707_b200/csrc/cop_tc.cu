@@ -8,52 +8,46 @@
 //     acc_s = sum_{i+j=s} sum_beta x_i[alpha][beta] e_j[beta][col]
 // accumulated in int32 TMEM by tcgen05.mma kind::i8 (u8 x u8 -> s32); the
 // epilogue recombines v = sum_s acc_s 2^(8s) in 64-bit (terms s >= 4 folded as
-// acc_s * (2^(8s) mod p)) and Barrett-reduces it.  Bounds (host-checked):
+// acc_s * (2^(8s) mod p)) and reduces it mod p.  Bounds (host-checked):
 // acc_s < 4 * m * 255^2 < 2^31 for m <= 8192.
 //
-// Structure (persistent, warp-specialised, one CTA per SM):
-//   warp 0      producer: 1-D bulk async copies of the pre-swizzled operand
-//               tiles (X slices of the M tile, the 4 E planes of the N tile)
-//               into a STAGES-deep shared-memory ring (mbarrier full/empty)
-//   warp 1      MMA issuer: per 32-byte k-step, S_x MMAs of 128 x 4*BN x 32 --
-//               the 4 E planes are stacked along N, so one MMA whose D starts
-//               at TMEM column BN*i writes x_i*e_j into acc_{i+j} for all j
-//   warp 2      TMEM allocator
-//   warps 4-11  epilogue: tcgen05.ld -> exact recombination -> mod p -> C,
-//               overlapped with the next tile's MMAs when the accumulators
-//               fit twice in TMEM (ell <= 16)
-// Tiles are walked M-fastest so concurrently running CTAs share the E tile in L2.
+// The 4 byte planes of an Enc(W) tile are stacked along N in shared memory
+// (plane j = rows [BN j, BN j + BN)), so ONE MMA of N = 4 BN whose D starts at
+// TMEM column BN*i writes x_i*e_j into acc_{i+j} for all four j at once.
+//
+// Two kernels, both persistent and warp-specialised (one CTA per SM):
+//  k_cop_tc      streaming: every k-block brings its X slices and its E planes
+//                through a shared-memory ring (bulk async copies).
+//  k_cop_tc_res  resident X (ell <= 16, one 128-row M tile, m <= 768): the X
+//                slices are fetched once per CTA -- slice 0 into TMEM (read by
+//                the MMA as its A operand), slice 1 kept in shared memory --
+//                and only Enc(W) streams.  The L2->SM traffic per tile drops
+//                from (X + E) to E, which is what bounds the k = 128 layers.
+// Roles: warp 0 producer, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-11
+// epilogue (tcgen05.ld -> recombination -> mod p -> C), double-buffered TMEM
+// accumulators when two sets fit so the epilogue overlaps the next tile.
 #include "internal.h"
 
 namespace nimbus {
-
-template <int SX>
-struct TcCfg {
-    static constexpr uint32_t BM = kBM, BN = kBNT, BK = kBK;
-    static constexpr uint32_t A_BYTES = SX * BM * BK;          // 16 KB per X slice
-    static constexpr uint32_t B_BYTES = kSW * BN * BK;         // 24 KB (4 planes x 48 rows)
-    static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
-    static constexpr uint32_t STAGES = (SX == 4) ? 2 : (SX == 2 ? 3 : 4);
-    static constexpr uint32_t NACC = SX + kSW - 1;
-    static constexpr uint32_t ACC_COLS = NACC * BN;            // one accumulator set
-    static constexpr uint32_t ACC_BUFS = (2 * 256 >= 2 * ACC_COLS && ACC_COLS <= 256) ? 2 : 1;
-    static constexpr uint32_t BUF_STRIDE = 256;                // TMEM column offset of buffer 1
-    static constexpr uint32_t TMEM_COLS = 512;
-    static constexpr uint32_t EPI_WARPS = 8;
-    static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
-    static constexpr uint32_t CHUNK = 8;                       // columns per tcgen05.ld
-    static constexpr uint32_t NCHUNK = BN / CHUNK;             // 6
-    static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
-    static_assert(ACC_COLS <= TMEM_COLS, "accumulators exceed TMEM");
-    static_assert(SMEM <= 232448, "shared memory");
-    static_assert(NCHUNK % 2 == 0, "epilogue split");
-};
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
                    "=r"(v[7])
                  : "r"(taddr));
+}
+// D[tmem] (+)= A[tmem] * B[smem], kind::i8
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+        :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// smem (SWIZZLE_128B K-major, 128 rows x 32 B) -> TMEM 128 lanes x 8 columns
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" :: "r"(taddr), "l"(sdesc) : "memory");
 }
 
 #ifdef NIMBUS_TRACE
@@ -68,15 +62,88 @@ extern "C" int nimbus_trace_set(void* p) { return (int)cudaMemcpyToSymbol(g_trac
 #define TRACE(slot) do { } while (0)
 #endif
 
-template <int SX, int CL>
-__global__ void __launch_bounds__(TcCfg<SX>::THREADS, 1)
+// ------------------------------------------------------------------ epilogue
+// Warp (sub, half) drains rows [32 sub, 32 sub + 32) and half of the BN
+// columns of one accumulator set: CPW chunks of 8 columns, BATCH chunks of
+// tcgen05.ld per wait.  tacc = TMEM address of acc_0 for lane 32 sub.
+template <uint32_t NACC, uint32_t BN>
+__device__ __forceinline__ void epilogue_tile(const Rns& R, uint32_t tacc, uint32_t half, uint32_t row, uint32_t k,
+                                              uint32_t col_base, uint32_t ncol, uint32_t* __restrict__ C) {
+    constexpr uint32_t CPW = BN / 8 / 2;
+    constexpr uint32_t BATCH = (NACC * 8 * CPW <= 128) ? CPW : 1;
+#pragma unroll 1
+    for (uint32_t c0 = 0; c0 < CPW; c0 += BATCH) {
+        uint32_t v[BATCH][NACC][8];
+#pragma unroll
+        for (uint32_t b = 0; b < BATCH; b++)
+#pragma unroll
+            for (uint32_t s = 0; s < NACC; s++) tmem_ld8(tacc + s * BN + (half * CPW + c0 + b) * 8, v[b][s]);
+        tmem_ld_wait();
+#pragma unroll
+        for (uint32_t b = 0; b < BATCH; b++) {
+            const uint32_t col0 = col_base + (half * CPW + c0 + b) * 8;
+            if (col0 >= ncol || row >= k) continue;
+            const uint32_t limb = (col0 / R.N) % R.L;
+            const uint32_t p = R.p[limb], c32 = R.c32[limb];
+            uint32_t out[8];
+#ifdef NIMBUS_NOMATH
+#pragma unroll
+            for (uint32_t u = 0; u < 8; u++) {
+                uint32_t x = 0;
+#pragma unroll
+                for (uint32_t s = 0; s < NACC; s++) x ^= v[b][s][u];
+                out[u] = x;
+            }
+#else
+#pragma unroll
+            for (uint32_t u = 0; u < 8; u++) {
+                // v = sum_s acc_s 2^(8s): s < 4 exact, s >= 4 as acc_s (2^(8s) mod p)  (< 2^64)
+                uint64_t x = v[b][0][u];
+                if (NACC > 1) x = mad_wide(v[b][1][u], 1u << 8, x);
+                if (NACC > 2) x = mad_wide(v[b][2][u], 1u << 16, x);
+                if (NACC > 3) x = mad_wide(v[b][3][u], 1u << 24, x);
+#pragma unroll
+                for (uint32_t s = 4; s < NACC; s++) x = mad_wide(v[b][s][u], R.pow8[limb][s], x);
+                out[u] = reduce64_pm(x, p, c32);
+            }
+#endif
+            uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ncol + col0);
+            dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+            dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ streaming kernel
+template <int SX, int BN_>
+struct TcCfg {
+    static constexpr uint32_t BM = kBM, BN = BN_, BK = kBK;
+    static constexpr uint32_t A_BYTES = SX * BM * BK;          // 16 KB per X slice
+    static constexpr uint32_t B_BYTES = kSW * BN * BK;         // 4 planes x BN rows x 128 B
+    static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+    static constexpr uint32_t STAGES = (220u * 1024u) / STAGE > 6 ? 6 : (220u * 1024u) / STAGE;
+    static constexpr uint32_t NACC = SX + kSW - 1;
+    static constexpr uint32_t ACC_COLS = NACC * BN;            // one accumulator set
+    static constexpr uint32_t ACC_BUFS = ACC_COLS <= 256 ? 2 : 1;
+    static constexpr uint32_t BUF_STRIDE = 256;                // TMEM column offset of buffer 1
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t EPI_WARPS = 8;
+    static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
+    static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+    static_assert(ACC_COLS <= TMEM_COLS, "accumulators exceed TMEM");
+    static_assert(SMEM <= 232448, "shared memory");
+    static_assert((BN / 8) % 2 == 0, "epilogue split");
+};
+
+template <int SX, int CL, int BN_>
+__global__ void __launch_bounds__(TcCfg<SX, BN_>::THREADS, 1)
 k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t Mt,
          uint32_t CT, uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
     // CL = cluster size along the column-tile dimension.  With CL = 2 the two
     // CTAs of a cluster work on column tiles (2q, 2q+1) of the same M tile in
     // lockstep; each fetches half of every X-slice block and multicasts it into
-    // both CTAs' shared memory, halving the L2->SM traffic of the A operand.
-    using Cfg = TcCfg<SX>;
+    // both CTAs' shared memory (halves the L2 reads of the A operand).
+    using Cfg = TcCfg<SX, BN_>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
@@ -102,7 +169,9 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) TRACE(1);
-    pdl_trigger();   // let the pack kernel's CTAs get resident early (they wait on us)
+#ifndef NIMBUS_LATE_TRIGGER
+    pdl_trigger();   // let the pack kernel CTAs get resident early (they wait on us)
+#endif
 
     if (warp == 0) {
         if (lane == 0) {
@@ -133,9 +202,9 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
     } else if (warp == 1) {
         if (lane == 0) {
             // ---------------- MMA issuer
-            constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 192
-            constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 144
-            constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = 48
+            constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 4 BN
+            constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 3 BN
+            constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = BN
             uint32_t it = 0, ti = 0;
             for (uint32_t u = cid; u < nunits; u += ncl, ti++) {
                 const uint32_t buf = Cfg::ACC_BUFS == 2 ? (ti & 1) : 0;
@@ -187,58 +256,8 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
             mbar_wait(&tfull[buf], use & 1);
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
             tc_fence_after();
-            const uint32_t row = mt * Cfg::BM + sub * 32 + lane;
-            const uint32_t tbase = tmem + ((sub * 32) << 16) + buf * Cfg::BUF_STRIDE;
-            // Each warp drains CPW chunks of 8 columns for its 32 rows; BATCH chunks of
-            // tcgen05.ld are issued before one wait (all of them when they fit in registers).
-            constexpr uint32_t CPW = Cfg::NCHUNK / 2;
-            constexpr uint32_t BATCH = (Cfg::NACC * 8 * CPW <= 128) ? CPW : 1;
-#pragma unroll 1
-            for (uint32_t c0 = 0; c0 < CPW; c0 += BATCH) {
-                uint32_t v[BATCH][Cfg::NACC][8];
-#pragma unroll
-                for (uint32_t b = 0; b < BATCH; b++)
-#pragma unroll
-                    for (uint32_t s = 0; s < Cfg::NACC; s++)
-                        tmem_ld8(tbase + s * Cfg::BN + (half * CPW + c0 + b) * Cfg::CHUNK, v[b][s]);
-                tmem_ld_wait();
-#pragma unroll
-                for (uint32_t b = 0; b < BATCH; b++) {
-                    const uint32_t col0 = ct * Cfg::BN + (half * CPW + c0 + b) * Cfg::CHUNK;
-                    if (col0 >= ncol || row >= k) continue;
-                    const uint32_t limb = (col0 / R.N) % R.L;
-                    const uint32_t p = R.p[limb], c32 = R.c32[limb];
-                    uint32_t out[8];
-#ifdef NIMBUS_NOMATH
-#pragma unroll
-                    for (uint32_t u = 0; u < 8; u++) {
-                        uint32_t x = 0;
-#pragma unroll
-                        for (uint32_t s = 0; s < Cfg::NACC; s++) x ^= v[b][s][u];
-                        out[u] = x;
-                    }
-#else
-#pragma unroll
-                    for (uint32_t u = 0; u < 8; u++) {
-                        // v = sum_s acc_s 2^(8s): s < 4 exact, s >= 4 as acc_s (2^(8s) mod p)  (< 2^64)
-                        uint64_t x = mad_wide(v[b][1][u], 1u << 8, v[b][0][u]);
-                        x = mad_wide(v[b][2][u], 1u << 16, x);
-                        x = mad_wide(v[b][3][u], 1u << 24, x);
-#pragma unroll
-                        for (uint32_t s = 4; s < Cfg::NACC; s++) x = mad_wide(v[b][s][u], R.pow8[limb][s], x);
-                        out[u] = reduce64_pm(x, p, c32);
-                    }
-#endif
-#ifdef NIMBUS_NOSTORE
-                    if (out[0] == 0x12345678u && out[7] == 0x9abcdef0u)
-#endif
-                    {
-                        uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ncol + col0);
-                        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
-                        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
-                    }
-                }
-            }
+            epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + buf * Cfg::BUF_STRIDE, half,
+                                             mt * Cfg::BM + sub * 32 + lane, k, ct * Cfg::BN, ncol, C);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -254,19 +273,173 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
     }
 }
 
-template <int SX, int CL>
+// ------------------------------------------------------------------ resident-X kernel
+struct ResCfg {
+    static constexpr uint32_t BM = kBM, BN = kBNR, BK = kBK, SX = 2;
+    static constexpr uint32_t SLICE = BM * BK;                 // one X slice, one k-block: 16 KB
+    static constexpr uint32_t B_BYTES = kSW * BN * BK;         // 16 KB
+    static constexpr uint32_t STAGES = 5;
+    static constexpr uint32_t NACC = SX + kSW - 1;             // 5
+    static constexpr uint32_t ACC_COLS = NACC * BN;            // 160
+    static constexpr uint32_t A0_COLS = kResMaxKB * (BK / 4);  // slice 0 in TMEM: 32 columns per k-block
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t EPI_WARPS = 8;
+    static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
+    // smem: slice 1 resident [KB][16 KB] | slice 0 staging [2][16 KB] | B ring [STAGES][16 KB]
+    static constexpr uint32_t OFF_A1 = 0, OFF_STG = kResMaxKB * SLICE, OFF_B = OFF_STG + 2 * SLICE;
+    static constexpr size_t SMEM = (size_t)OFF_B + STAGES * B_BYTES + 1024 + 256;
+    static_assert(A0_COLS + 2 * ACC_COLS <= TMEM_COLS, "TMEM budget");
+    static_assert(SMEM <= 232448, "shared memory");
+};
+
+__global__ void __launch_bounds__(ResCfg::THREADS, 1)
+k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t CT,
+             uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
+    using Cfg = ResCfg;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::B_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* sfree = tempty + 2;                 // slice-0 staging slot free (tcgen05.cp done)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) TRACE(0);
+    if (warp == 0 && lane == 0) {
+        for (uint32_t s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (uint32_t b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); mbar_init(&sfree[b], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) TRACE(1);
+#ifndef NIMBUS_LATE_TRIGGER
+    pdl_trigger();
+#endif
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- producer: E every tile; X slices during the first tile only
+            const uint64_t pol_a = policy_evict_last();
+            const uint64_t pol_b = policy_evict_first();
+            uint32_t it = 0, ti = 0;
+            for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+                const uint8_t* b_src = Et + (size_t)ct * KB * Cfg::B_BYTES;
+                for (uint32_t kb = 0; kb < KB; kb++, it++) {
+                    const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
+                    if (it >= Cfg::STAGES) mbar_wait(&empty[s], ph ^ 1);
+                    if (ti == 1 && kb < 8) TRACE(52 + kb);
+                    const bool first = ti == 0;
+                    mbar_arrive_expect_tx(&full[s], Cfg::B_BYTES + (first ? 2 * Cfg::SLICE : 0));
+                    bulk_g2s(smem + Cfg::OFF_B + s * Cfg::B_BYTES, b_src + (size_t)kb * Cfg::B_BYTES, Cfg::B_BYTES,
+                             &full[s], pol_b);
+                    if (first) {
+                        if (kb == 0) { pdl_wait(); TRACE(2); }
+                        const uint8_t* xsrc = Xt + (size_t)kb * 2 * Cfg::SLICE;   // Xt[0][kb][slice][128][128]
+                        if (kb >= 2) mbar_wait(&sfree[kb & 1], ((kb >> 1) - 1) & 1);
+                        bulk_g2s(smem + Cfg::OFF_STG + (kb & 1) * Cfg::SLICE, xsrc, Cfg::SLICE, &full[s], pol_a);
+                        bulk_g2s(smem + Cfg::OFF_A1 + kb * Cfg::SLICE, xsrc + Cfg::SLICE, Cfg::SLICE, &full[s], pol_a);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer
+            constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 128
+            constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 96
+            constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = 32
+            uint32_t it = 0, ti = 0;
+            for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+                const uint32_t buf = ti & 1, use = ti >> 1;
+                if (ti >= 2) mbar_wait(&tempty[buf], (use & 1) ^ 1);
+                TRACE(4 + 4 * ti);
+                tc_fence_after();
+                const uint32_t dacc = tmem + Cfg::A0_COLS + buf * Cfg::ACC_COLS;
+                for (uint32_t kb = 0; kb < KB; kb++, it++) {
+                    const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    if (ti == 1 && kb < 8) TRACE(40 + kb);
+                    tc_fence_after();
+                    const uint32_t a0t = tmem + kb * (Cfg::BK / 4);                      // slice 0, TMEM
+                    const uint32_t a1 = smem_u32(smem + Cfg::OFF_A1 + kb * Cfg::SLICE);  // slice 1, smem
+                    const uint32_t b0 = smem_u32(smem + Cfg::OFF_B + s * Cfg::B_BYTES);
+                    if (ti == 0) {
+                        // first tile: move this k-block of slice 0 into TMEM (in issue order with the MMAs)
+                        const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + (kb & 1) * Cfg::SLICE);
+#pragma unroll
+                        for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
+                            tmem_cp_128x256b(a0t + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
+                        mma_commit(&sfree[kb & 1]);
+                    }
+#pragma unroll
+                    for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
+                        const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
+                        const uint32_t first = (kb | kk) == 0;
+                        mma_i8_ts(dacc, a0t + kk * 8, bd, idesc_full, !first);          // x_0 e_j -> acc_j
+                        const uint64_t ad1 = sdesc_kmajor_sw128(a1 + kk * 32);
+                        if (!first) {
+                            mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_full, 1u);          // x_1 e_j -> acc_{j+1}
+                        } else {
+                            mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_lo, 1u);
+                            const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (kSW - 1) * Cfg::BN * Cfg::BK + kk * 32);
+                            mma_i8_ss(dacc + kSW * Cfg::BN, ad1, bd3, idesc_one, 0u);
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[buf]);
+                TRACE(5 + 4 * ti);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue
+        const uint32_t ew = warp - 4;
+        const uint32_t sub = ew & 3, half = ew >> 2;
+        uint32_t ti = 0;
+        for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+            const uint32_t buf = ti & 1, use = ti >> 1;
+            mbar_wait(&tfull[buf], use & 1);
+            if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
+            tc_fence_after();
+            epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS, half,
+                                             sub * 32 + lane, k, ct * Cfg::BN, ncol, C);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) TRACE(3);
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, Cfg::TMEM_COLS);
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+template <int SX, int CL, int BN>
 static cudaError_t launch_sx(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                              cudaStream_t st) {
-    using Cfg = TcCfg<SX>;
+    using Cfg = TcCfg<SX, BN>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_cop_tc<SX, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_cop_tc<SX, CL, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)Cfg::SMEM);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    const uint32_t CT = col_tiles(c), Mt = (k + kBM - 1) / kBM;
+    const uint32_t CT = col_tiles(c, BN), Mt = (k + kBM - 1) / kBM;
     const uint32_t nunits = Mt * (CT / CL);
     uint32_t nclusters = (uint32_t)c->num_sms / CL;
     if (nunits < nclusters) nclusters = nunits;
@@ -284,18 +457,51 @@ static cudaError_t launch_sx(nimbus_ctx* c, const nimbus_encw* w, const uint8_t*
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_cop_tc<SX, CL>, c->rns, d_Xt, (const uint8_t*)w->d_Et, k, Mt, CT,
-                                       w->KB, ncol, d_C);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_cop_tc<SX, CL, BN>, c->rns, d_Xt, (const uint8_t*)w->d_Et, k, Mt,
+                                       CT, w->KB, ncol, d_C);
     c->launches++;
     return e;
 }
 
+static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
+                              cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_cop_tc_res, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)ResCfg::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const uint32_t ncol = 2 * c->rns.L * c->rns.N;
+    const uint32_t CT = col_tiles(c, kBNR);
+    const uint32_t grid = CT < (uint32_t)c->num_sms ? CT : (uint32_t)c->num_sms;
+    cudaError_t e = launch_pdl(k_cop_tc_res, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt,
+                               (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, d_C);
+    c->launches++;
+    return e;
+}
+
+template <int SX, int BN>
+static cudaError_t launch_cl(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
+                             cudaStream_t st) {
+    return c->cluster == 2 ? launch_sx<SX, 2, BN>(c, w, d_Xt, k, d_C, st) : launch_sx<SX, 1, BN>(c, w, d_Xt, k, d_C, st);
+}
+
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st) {
-    switch (sx_of(c->rns.ell)) {
-        case 1: return c->cluster == 2 ? launch_sx<1, 2>(c, w, d_Xt, k, d_C, st) : launch_sx<1, 1>(c, w, d_Xt, k, d_C, st);
-        case 2: return c->cluster == 2 ? launch_sx<2, 2>(c, w, d_Xt, k, d_C, st) : launch_sx<2, 1>(c, w, d_Xt, k, d_C, st);
-        default: return c->cluster == 2 ? launch_sx<4, 2>(c, w, d_Xt, k, d_C, st) : launch_sx<4, 1>(c, w, d_Xt, k, d_C, st);
+    const uint32_t SX = sx_of(c->rns.ell);
+    if (w->bn == kBNR) {
+        if (SX == 2 && k <= kBM && w->KB <= kResMaxKB) return launch_res(c, w, d_Xt, k, d_C, st);
+        switch (SX) {
+            case 1: return launch_cl<1, kBNR>(c, w, d_Xt, k, d_C, st);
+            case 2: return launch_cl<2, kBNR>(c, w, d_Xt, k, d_C, st);
+            default: return launch_cl<4, kBNR>(c, w, d_Xt, k, d_C, st);
+        }
+    }
+    switch (SX) {
+        case 1: return launch_cl<1, kBNT>(c, w, d_Xt, k, d_C, st);
+        case 2: return launch_cl<2, kBNT>(c, w, d_Xt, k, d_C, st);
+        default: return launch_cl<4, kBNT>(c, w, d_Xt, k, d_C, st);
     }
 }
 

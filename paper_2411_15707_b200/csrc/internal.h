@@ -13,7 +13,9 @@ typedef unsigned __int128 u128;
 
 // Kernel-layout geometry of Enc(W) and of the sliced X.
 constexpr uint32_t kBK = 128;      // beta (contraction) bytes per k-block = one 128-B swizzle row
-constexpr uint32_t kBNT = 48;      // coefficient columns per Enc(W) tile (4 planes -> MMA N = 192)
+constexpr uint32_t kBNT = 48;      // coefficient columns per Enc(W) tile, streaming kernel (4 planes -> MMA N = 192)
+constexpr uint32_t kBNR = 32;      // tile width of the resident-X kernel (ell <= 16, m <= 768; MMA N = 128)
+constexpr uint32_t kResMaxKB = 6;  // resident-X kernel: at most 6 k-blocks (m <= 768) of X in TMEM + smem
 constexpr uint32_t kBM = 128;      // rows (alpha) per X tile = tcgen05 M
 constexpr uint32_t kSW = 4;        // 8-bit slices of a 31-bit residue (S_w)
 
@@ -27,7 +29,7 @@ struct nimbus_ctx {
     std::string err;
     uint64_t launches = 0;
     int num_sms = 148;
-    int cluster = 2;               // CTAs per cluster of the tcgen05 contraction (A multicast); env NIMBUS_CLUSTER
+    int cluster = 1;               // CTAs per cluster of the streaming contraction (2 = X multicast); env NIMBUS_CLUSTER
     // stage profiling (nimbus_profile_*): pending event quadruples, accumulated ms
     bool profile = false;
     std::vector<cudaEvent_t> ev_pool, ev_pending;
@@ -44,7 +46,8 @@ struct nimbus_sk {
 struct nimbus_encw {
     nimbus_ctx* ctx = nullptr;
     uint32_t m = 0, n = 0, KB = 0; // KB = ceil(m / 128) k-blocks
-    uint8_t* d_Et = nullptr;       // tiled byte planes [ct][kb][s][64][128 swizzled]
+    uint32_t bn = kBNT;            // tile width (columns) of the resident layout
+    uint8_t* d_Et = nullptr;       // tiled byte planes [ct][kb][s][bn][128 swizzled]
     size_t bytes = 0;
 };
 
@@ -52,7 +55,7 @@ struct nimbus_encw {
 inline uint32_t sx_of(uint32_t ell) { return ell <= 8 ? 1 : ell <= 16 ? 2 : 4; }
 // number of 48-column Enc(W) tiles covering the 2 L N coefficient columns (last one zero padded)
 // (rounded up to an even count so column tiles pair up in 2-CTA clusters)
-inline uint32_t col_tiles(const nimbus_ctx* c) { return (((2 * c->rns.L * c->rns.N + kBNT - 1) / kBNT) + 1) & ~1u; }
+inline uint32_t col_tiles(const nimbus_ctx* c, uint32_t bn) { return (((2 * c->rns.L * c->rns.N + bn - 1) / bn) + 1) & ~1u; }
 
 // ---------------------------------------------------------------- launchers
 namespace nimbus {
@@ -68,10 +71,10 @@ cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_
 cudaError_t launch_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* out,
                              cudaStream_t st);
 // layout.cu
-cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m, uint32_t KB, uint8_t* d_Et,
-                             cudaStream_t st);
-cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t* d_canon,
-                               cudaStream_t st);
+cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m, uint32_t KB, uint32_t bn,
+                             uint8_t* d_Et, cudaStream_t st);
+cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t bn,
+                               uint32_t* d_canon, cudaStream_t st);
 cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB,
                            uint8_t* d_Xt, cudaStream_t st);
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,

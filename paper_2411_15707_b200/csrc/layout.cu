@@ -1,4 +1,4 @@
-// layout.cu -- data-layout and epilogue kernels of the COP hot path:
+// layout.cu -- data-layout kernels of the COP hot path:
 //   K4  slice X into 8-bit planes in the tcgen05 operand layout (A3)
 //   tile / untile Enc(W) between the canonical [beta][comp][limb][j] layout
 //       and the resident byte-plane kernel layout (setup / export)
@@ -64,21 +64,22 @@ __global__ void k_slice_x(const uint32_t* __restrict__ X, uint32_t k, uint32_t m
 
 // ---------------------------------------------------------------- tile Enc(W)
 // CTA (ct, kb): canonical E[beta][col] for beta in the k-block, col in the
-// 48-column tile -> 4 byte planes Et[ct][kb][s][48][128 B swizzled]; rows
-// beta >= m and columns >= 2LN (last tile) are zero.
+// BN-column tile -> 4 byte planes Et[ct][kb][s][BN][128 B swizzled]; rows
+// beta >= m and columns >= 2LN (padding tiles) are zero.
+template <int BN>
 __global__ void __launch_bounds__(256) k_tile_encw(const uint32_t* __restrict__ canon, uint32_t m,
                                                    uint32_t ncol, uint32_t KB, uint8_t* __restrict__ Et) {
-    __shared__ uint32_t sE[kBK][kBNT + 1];
+    __shared__ uint32_t sE[kBK][BN + 1];
     const uint32_t ct = blockIdx.x, kb = blockIdx.y;
-    for (uint32_t idx = threadIdx.x; idx < kBK * kBNT; idx += blockDim.x) {
-        const uint32_t b = idx / kBNT, c = idx % kBNT, beta = kb * kBK + b;
-        const size_t col = (size_t)ct * kBNT + c;
+    for (uint32_t idx = threadIdx.x; idx < kBK * BN; idx += blockDim.x) {
+        const uint32_t b = idx / BN, c = idx % BN, beta = kb * kBK + b;
+        const size_t col = (size_t)ct * BN + c;
         sE[b][c] = (beta < m && col < ncol) ? canon[(size_t)beta * ncol + col] : 0u;
     }
     __syncthreads();
-    uint8_t* base = Et + ((size_t)ct * KB + kb) * kSW * kBNT * kBK;
-    for (uint32_t idx = threadIdx.x; idx < kSW * kBNT * 8; idx += blockDim.x) {
-        const uint32_t s = idx / (kBNT * 8), r = (idx / 8) % kBNT, c16 = idx % 8;
+    uint8_t* base = Et + ((size_t)ct * KB + kb) * kSW * BN * kBK;
+    for (uint32_t idx = threadIdx.x; idx < kSW * BN * 8; idx += blockDim.x) {
+        const uint32_t s = idx / (BN * 8), r = (idx / 8) % BN, c16 = idx % 8;
         uint32_t w[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) {
@@ -87,26 +88,27 @@ __global__ void __launch_bounds__(256) k_tile_encw(const uint32_t* __restrict__ 
             for (int u = 0; u < 4; u++) acc |= ((sE[c16 * 16 + 4 * q + u][r] >> (8 * s)) & 0xFF) << (8 * u);
             w[q] = acc;
         }
-        *reinterpret_cast<uint4*>(base + (size_t)s * kBNT * kBK + swz_off(r, c16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(base + (size_t)s * BN * kBK + swz_off(r, c16)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
+template <int BN>
 __global__ void __launch_bounds__(256) k_untile_encw(const uint8_t* __restrict__ Et, uint32_t m, uint32_t ncol,
                                                      uint32_t KB, uint32_t* __restrict__ canon) {
-    __shared__ uint32_t sE[kBK][kBNT + 1];
+    __shared__ uint32_t sE[kBK][BN + 1];
     const uint32_t ct = blockIdx.x, kb = blockIdx.y;
-    for (uint32_t idx = threadIdx.x; idx < kBK * kBNT; idx += blockDim.x) sE[idx / kBNT][idx % kBNT] = 0;
+    for (uint32_t idx = threadIdx.x; idx < kBK * BN; idx += blockDim.x) sE[idx / BN][idx % BN] = 0;
     __syncthreads();
-    const uint8_t* base = Et + ((size_t)ct * KB + kb) * kSW * kBNT * kBK;
-    for (uint32_t idx = threadIdx.x; idx < kSW * kBNT * kBK; idx += blockDim.x) {
-        const uint32_t s = idx / (kBNT * kBK), r = (idx / kBK) % kBNT, b = idx % kBK;
-        uint32_t byte = base[(size_t)s * kBNT * kBK + swz_off(r, b >> 4) + (b & 15)];
+    const uint8_t* base = Et + ((size_t)ct * KB + kb) * kSW * BN * kBK;
+    for (uint32_t idx = threadIdx.x; idx < kSW * BN * kBK; idx += blockDim.x) {
+        const uint32_t s = idx / (BN * kBK), r = (idx / kBK) % BN, b = idx % kBK;
+        uint32_t byte = base[(size_t)s * BN * kBK + swz_off(r, b >> 4) + (b & 15)];
         atomicOr(&sE[b][r], byte << (8 * s));
     }
     __syncthreads();
-    for (uint32_t idx = threadIdx.x; idx < kBK * kBNT; idx += blockDim.x) {
-        const uint32_t b = idx / kBNT, c = idx % kBNT, beta = kb * kBK + b;
-        const size_t col = (size_t)ct * kBNT + c;
+    for (uint32_t idx = threadIdx.x; idx < kBK * BN; idx += blockDim.x) {
+        const uint32_t b = idx / BN, c = idx % BN, beta = kb * kBK + b;
+        const size_t col = (size_t)ct * BN + c;
         if (beta < m && col < ncol) canon[(size_t)beta * ncol + col] = sE[b][c];
     }
 }
@@ -127,18 +129,22 @@ cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint3
     return e;
 }
 
-cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m, uint32_t KB, uint8_t* d_Et,
-                             cudaStream_t st) {
+cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m, uint32_t KB, uint32_t bn,
+                             uint8_t* d_Et, cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    k_tile_encw<<<dim3(col_tiles(c), KB), 256, 0, st>>>(d_canon, m, ncol, KB, d_Et);
+    const dim3 g(col_tiles(c, bn), KB);
+    if (bn == kBNR) k_tile_encw<kBNR><<<g, 256, 0, st>>>(d_canon, m, ncol, KB, d_Et);
+    else k_tile_encw<kBNT><<<g, 256, 0, st>>>(d_canon, m, ncol, KB, d_Et);
     c->launches++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t* d_canon,
-                               cudaStream_t st) {
+cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t bn,
+                               uint32_t* d_canon, cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    k_untile_encw<<<dim3(col_tiles(c), KB), 256, 0, st>>>(d_Et, m, ncol, KB, d_canon);
+    const dim3 g(col_tiles(c, bn), KB);
+    if (bn == kBNR) k_untile_encw<kBNR><<<g, 256, 0, st>>>(d_Et, m, ncol, KB, d_canon);
+    else k_untile_encw<kBNT><<<g, 256, 0, st>>>(d_Et, m, ncol, KB, d_canon);
     c->launches++;
     return cudaGetLastError();
 }

@@ -3,17 +3,17 @@
 // unpacked C (k x 2LN residues, L2-resident right after the contraction)
 // once, writes the compact ciphertexts and the client share R.
 //
-// Thread = V consecutive output coefficients J of packed ciphertext
-// tg = query*nct + theta, both components, all limbs:
+// Thread = V consecutive output coefficients J of one component of packed
+// ciphertext tg = query*nct + theta, all limbs (the mod-switch mixes limbs):
 //   step 3:  s_i[J] = sum_{r < rows} (X^{r n} c[theta R + r])_i[J]
 //                   = sum_r (J >= r n ? C_r[J - r n] : p_i - C_r[J - r n + N])  (RShift)
-//            summed lazily in 64 bits, one Barrett reduction per coefficient;
+//            summed lazily in 64 bits, one reduction per coefficient;
 //   switch:  for l = L-1 .. L_out:  c_i <- (c_i - rho) * p_l^-1 mod p_i,
 //            rho = centered c_l  (= round(c / p_l));
 //   step 4:  b_i -= Emb_{q'}(r_theta[J]),  r_theta[J] = word(seed, 6, tg*N + J) >> (64-ell)
 //            (SURVEY.md §8(c) #13); R[alpha][j] = r_theta[(alpha mod R) n + j].
-// V = 4 (uint4 loads/stores) when n % 4 == 0: a group of 4 J never straddles a
-// wrap point because J and r n are then multiples of 4.
+// V = 4 (uint4 loads/stores) when n % 4 == 0 and the grid stays large; a group
+// of 4 J never straddles a wrap point because J and r n are multiples of 4.
 #include "internal.h"
 
 namespace nimbus {
@@ -53,100 +53,92 @@ template <int V, int L>
 __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                               uint32_t Rr, uint32_t nct, uint64_t key_mask,
                                               uint32_t* __restrict__ cts, uint32_t* __restrict__ Rout) {
-    constexpr int RB = 4;  // rows of loads in flight per batch
+    constexpr int RB = 8;  // rows of loads in flight per batch
     pdl_trigger();
     const uint32_t N = Rn.N, Lo = Rn.L_out;
-    const uint32_t tg = blockIdx.y;
+    const uint32_t tg = blockIdx.y, comp = blockIdx.z;
     const uint32_t J = (blockIdx.x * blockDim.x + threadIdx.x) * V;
     if (J >= N) return;
     const uint32_t query = tg / nct, theta = tg - query * nct;
     const uint32_t rows = min(Rr, kq - theta * Rr);
     const size_t ncol = (size_t)2 * L * N;
     const size_t row0 = (size_t)query * kq + (size_t)theta * Rr;
-    const uint32_t* Cq = C + row0 * ncol;
+    const uint32_t* Cq = C + row0 * ncol + (size_t)comp * L * N;
     pdl_wait();  // C is produced by the contraction kernel
 
+    uint64_t acc[L][V];
+#pragma unroll
+    for (int i = 0; i < L; i++)
+#pragma unroll
+        for (int u = 0; u < V; u++) acc[i][u] = 0;
+#pragma unroll 1
+    for (uint32_t r0 = 0; r0 < rows; r0 += RB) {
+        uint32_t v[RB][L][V];
+        bool wrap[RB];
+#pragma unroll
+        for (int b = 0; b < RB; b++) {
+            const uint32_t r = r0 + b, s = r * n;
+            wrap[b] = J < s;
+            const uint32_t idx = wrap[b] ? J + N - s : J - s;
+#pragma unroll
+            for (int i = 0; i < L; i++) {
+                if (r < rows) VecU32<V>::load(Cq + r * ncol + (size_t)i * N + idx, v[b][i]);
+                else {
+#pragma unroll
+                    for (int u = 0; u < V; u++) v[b][i][u] = 0;
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < RB; b++) {
+            if (r0 + b < rows) {
+#pragma unroll
+                for (int i = 0; i < L; i++)
+#pragma unroll
+                    for (int u = 0; u < V; u++) acc[i][u] += wrap[b] ? Rn.p[i] - v[b][i][u] : v[b][i][u];
+            }
+        }
+    }
     uint32_t rmask[V];
-    {
+    if (comp == 0) {
         const uint64_t i0 = (uint64_t)tg * N + J;
 #pragma unroll
         for (int u = 0; u < V; u++) rmask[u] = samp_mod_t(prg_word(key_mask, i0 + u), Rn.ell);
     }
+    uint32_t out[L][V];
 #pragma unroll
-    for (int comp = 0; comp < 2; comp++) {
-        uint64_t acc[L][V];
+    for (int u = 0; u < V; u++) {
+        uint32_t res[L];
 #pragma unroll
-        for (int i = 0; i < L; i++)
+        for (int i = 0; i < L; i++) res[i] = reduce64_pm(acc[i][u], Rn.p[i], Rn.c32[i]);
 #pragma unroll
-            for (int u = 0; u < V; u++) acc[i][u] = 0;
-#pragma unroll 1
-        for (uint32_t r0 = 0; r0 < rows; r0 += RB) {
-            uint32_t v[RB][L][V];
-            bool wrap[RB];
+        for (int l = L - 1; l >= 1; l--) {
+            if ((uint32_t)l >= Lo) {
+                const uint32_t pl = Rn.p[l], c = res[l];
+                const bool neg = c > (pl >> 1);          // centered rho = c - p_l < 0
+                const uint32_t mag = neg ? pl - c : c;   // |rho| < p_l / 2 < p_i
 #pragma unroll
-            for (int b = 0; b < RB; b++) {
-                const uint32_t r = r0 + b, s = r * n;
-                wrap[b] = J < s;
-                const uint32_t idx = wrap[b] ? J + N - s : J - s;
-#pragma unroll
-                for (int i = 0; i < L; i++) {
-                    if (r < rows) VecU32<V>::load(Cq + r * ncol + (size_t)(comp * L + i) * N + idx, v[b][i]);
-                    else {
-#pragma unroll
-                        for (int u = 0; u < V; u++) v[b][i][u] = 0;
-                    }
-                }
-            }
-#pragma unroll
-            for (int b = 0; b < RB; b++) {
-                if (r0 + b < rows) {
-#pragma unroll
-                    for (int i = 0; i < L; i++)
-#pragma unroll
-                        for (int u = 0; u < V; u++) acc[i][u] += wrap[b] ? Rn.p[i] - v[b][i][u] : v[b][i][u];
+                for (int i = 0; i < l; i++) {
+                    const uint32_t p = Rn.p[i];
+                    const uint32_t d = neg ? addmod(res[i], mag, p) : submod(res[i], mag, p);
+                    res[i] = mulmod_shoup(d, Rn.inv_p[l][i], Rn.inv_p_sh[l][i], p);
                 }
             }
         }
+        if (comp == 0) {
 #pragma unroll
-        for (int u = 0; u < V; u++) {
-            uint32_t res[L];
-#pragma unroll
-            for (int i = 0; i < L; i++) res[i] = mod64(acc[i][u], Rn.p[i], Rn.mu[i]);
-#pragma unroll
-            for (int l = L - 1; l >= 1; l--) {
-                if ((uint32_t)l >= Lo) {
-                    const uint32_t pl = Rn.p[l], c = res[l];
-                    const bool neg = c > (pl >> 1);          // centered rho = c - p_l < 0
-                    const uint32_t mag = neg ? pl - c : c;   // |rho| < p_l / 2 < p_i
-#pragma unroll
-                    for (int i = 0; i < l; i++) {
-                        const uint32_t p = Rn.p[i];
-                        const uint32_t d = neg ? addmod(res[i], mag, p) : submod(res[i], mag, p);
-                        res[i] = mulmod_shoup(d, Rn.inv_p[l][i], Rn.inv_p_sh[l][i], p);
-                    }
-                }
-            }
-            if (comp == 0) {
-#pragma unroll
-                for (int i = 0; i < L; i++)
-                    if ((uint32_t)i < Lo)
-                        res[i] = submod(res[i], emb_fast(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
-                                                         Rn.t_inv_sh[i]), Rn.p[i]);
-            }
-#pragma unroll
-            for (int i = 0; i < L; i++) acc[i][u] = res[i];   // reuse registers for the store
+            for (int i = 0; i < L; i++)
+                if ((uint32_t)i < Lo)
+                    res[i] = submod(res[i], emb_fast(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
+                                                     Rn.t_inv_sh[i]), Rn.p[i]);
         }
 #pragma unroll
-        for (int i = 0; i < L; i++) {
-            if ((uint32_t)i < Lo) {
-                uint32_t o[V];
-#pragma unroll
-                for (int u = 0; u < V; u++) o[u] = (uint32_t)acc[i][u];
-                VecU32<V>::store(cts + (((size_t)tg * 2 + comp) * Lo + i) * N + J, o);
-            }
-        }
+        for (int i = 0; i < L; i++) out[i][u] = res[i];
     }
-    if (J < rows * n) VecU32<V>::store(Rout + row0 * n + J, rmask);
+#pragma unroll
+    for (int i = 0; i < L; i++)
+        if ((uint32_t)i < Lo) VecU32<V>::store(cts + (((size_t)tg * 2 + comp) * Lo + i) * N + J, out[i]);
+    if (comp == 0 && J < rows * n) VecU32<V>::store(Rout + row0 * n + J, rmask);
 }
 
 template <int V>
@@ -154,7 +146,7 @@ static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uin
                             uint32_t* d_cts, uint32_t* d_R, cudaStream_t st) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     const uint32_t per_block = 128 * V;
-    dim3 grid((N + per_block - 1) / per_block, nq * nct);
+    dim3 grid((N + per_block - 1) / per_block, nq * nct, 2);
     const uint64_t key = prg_key(seed, 6);
     switch (c->rns.L) {
         case 1: return launch_pdl(k_pack<V, 1>, grid, dim3(128), 0, st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
@@ -166,8 +158,11 @@ static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uin
 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                         uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st) {
-    cudaError_t e = (n % 4 == 0) ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st)
-                                 : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st);
+    const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
+    const uint64_t threads_v1 = 2ull * nq * nct * N;      // one thread per (comp, J)
+    const bool vec = (n % 4 == 0) && threads_v1 / 4 >= 8ull * 128 * (uint64_t)c->num_sms;
+    cudaError_t e = vec ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st)
+                        : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st);
     c->launches++;
     return e;
 }

@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(uint32_t iters, unsigned long lo
 // A operand from TMEM (columns [256, 288)), B from shared memory; optional
 // concurrent bulk-copy fill traffic into a separate shared-memory buffer
 // (fill_kb KB per 4 MMAs) to see whether TMA writes compete with MMA reads.
-template <uint32_t N, bool TMEM_A>
+template <uint32_t N, bool TMEM_A, bool MIX = false, bool LD = false>
 __global__ void __launch_bounds__(128, 1) k_mma2(uint32_t iters, uint32_t fill_bytes, const uint8_t* gsrc,
                                                  unsigned long long* cycles) {
     extern __shared__ uint8_t smem_raw[];
@@ -84,7 +84,13 @@ __global__ void __launch_bounds__(128, 1) k_mma2(uint32_t iters, uint32_t fill_b
         for (uint32_t it = 0; it < iters; it++) {
 #pragma unroll
             for (uint32_t kk = 0; kk < 4; kk++) {
-                if (TMEM_A) {
+                if (MIX) {
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+                                 :: "r"(tmem), "r"(tmem + 256 + kk * 8), "l"(sdesc_kmajor_sw128(b0 + kk * 32)),
+                                    "r"(idesc), "r"(it | kk) : "memory");
+                    mma_i8_ss(tmem + 32, sdesc_kmajor_sw128(a0 + kk * 32), sdesc_kmajor_sw128(b0 + kk * 32), idesc, 1);
+                } else if (TMEM_A) {
                     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
                                  :: "r"(tmem), "r"(tmem + 256 + kk * 8), "l"(sdesc_kmajor_sw128(b0 + kk * 32)),
@@ -99,6 +105,22 @@ __global__ void __launch_bounds__(128, 1) k_mma2(uint32_t iters, uint32_t fill_b
         long long t1 = clock64();
         cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
         stop = 1;
+    } else if (LD && threadIdx.x >= 32) {
+        // warps 1-3: continuous TMEM reads (lanes of their subpartition) of columns 384..447
+        const uint32_t sub = (threadIdx.x >> 5) & 3;
+        uint32_t x = 0;
+        while (!stop) {
+            uint32_t v[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                               "=r"(v[7]) : "r"(tmem + ((sub * 32) << 16) + 384 + c * 8));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                x ^= v[0] ^ v[7];
+            }
+        }
+        if (x == 0x1234567) cycles[blockIdx.x] = 0;
     } else if (threadIdx.x == 32 && fill_bytes) {
         uint32_t ph = 0;
         const uint64_t pol = policy_evict_last();
@@ -114,18 +136,18 @@ __global__ void __launch_bounds__(128, 1) k_mma2(uint32_t iters, uint32_t fill_b
     if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 
-template <uint32_t N, bool TMEM_A>
+template <uint32_t N, bool TMEM_A, bool MIX = false, bool LD = false>
 void run2(int sms, uint32_t fill, const uint8_t* g) {
     unsigned long long* d;
     cudaMalloc(&d, sizeof(unsigned long long) * sms);
     const size_t smem = 16384 + 32768 + 65536 + 1024;
-    cudaFuncSetAttribute(k_mma2<N, TMEM_A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_mma2<N, TMEM_A, MIX, LD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint32_t iters = 4096;
-    k_mma2<N, TMEM_A><<<sms, 128, smem>>>(64, fill, g, d);
+    k_mma2<N, TMEM_A, MIX, LD><<<sms, 128, smem>>>(64, fill, g, d);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k_mma2<N, TMEM_A><<<sms, 128, smem>>>(iters, fill, g, d);
+    k_mma2<N, TMEM_A, MIX, LD><<<sms, 128, smem>>>(iters, fill, g, d);
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     float ms = 0;
@@ -135,8 +157,8 @@ void run2(int sms, uint32_t fill, const uint8_t* g) {
     double cyc = 0;
     for (int i = 0; i < sms; i++) cyc += h[i];
     cyc /= sms;
-    const double mmas = 4.0 * iters;
-    printf("%s N=%3u fill=%5u B: %6.1f cycles/MMA (floor %5.1f)  %s\n", TMEM_A ? "TMEM-A" : "SMEM-A", N, fill,
+    const double mmas = 4.0 * iters * (MIX ? 2 : 1);
+    printf("%s N=%3u fill=%5u B: %6.1f cycles/MMA (floor %5.1f)  %s\n", MIX ? (LD ? "MIX+LDTM" : "MIX TS+SS") : (TMEM_A ? (LD ? "TMEM-A+LDTM" : "TMEM-A") : (LD ? "SMEM-A+LDTM" : "SMEM-A")), N, fill,
            cyc / mmas, 128.0 * N / 256.0, cudaGetErrorString(err));
     cudaFree(d);
 }
@@ -179,6 +201,15 @@ int main() {
     uint8_t* g;
     cudaMalloc(&g, 1 << 20);
     cudaMemset(g, 1, 1 << 20);
+    run2<128, true, true, true>(sms, 0, g);
+    run2<128, false, false, true>(sms, 0, g);
+    run2<192, false, false, true>(sms, 0, g);
+    run2<128, true, false, true>(sms, 0, g);
+    for (uint32_t f : {0u, 16384u, 65536u}) {
+        run2<128, true, true>(sms, f, g);
+        run2<128, false>(sms, f, g);
+        run2<128, true>(sms, f, g);
+    }
     run2<32, true>(sms, 0, g);
     run2<64, true>(sms, 0, g);
     run2<128, true>(sms, 0, g);

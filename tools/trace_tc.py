@@ -25,10 +25,14 @@ ws = nb.alloc_workspace(ctx, w, k)
 cts, R = nb.alloc_outputs(ctx, w, k, 1)
 tr = torch.zeros(148 * 64, dtype=torch.int64, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+rflush = torch.ones(64 << 20, dtype=torch.int32, device="cuda")   # 256 MB read: leaves L2 clean
+MODE = os.environ.get("FLUSH", "write")
 for _ in range(3):
     nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
 lib.nimbus_trace_set(ctypes.c_void_p(tr.data_ptr()))
 flush.zero_()
+if MODE == "writeread":
+    rflush.sum()
 torch.cuda.synchronize()
 nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
 torch.cuda.synchronize()
@@ -46,6 +50,10 @@ for c in (0, 1, 2, 50, 100, 147):
             break
         s += f" t{ti}: mma {us(row[4+4*ti]):.1f}-{us(row[5+4*ti]):.1f} epi {us(row[6+4*ti]):.1f}-{us(row[7+4*ti]):.1f} |"
     print(s)
+for c in (0, 100):
+    row = t[c]
+    print(f"cta {c} tile1 producer B issue:", " ".join(f"{us(row[52+i]):.2f}" for i in range(8) if row[52+i] > 0))
+    print(f"cta {c} tile1 MMA full ready :", " ".join(f"{us(row[40+i]):.2f}" for i in range(8) if row[40+i] > 0))
 e = np.array([us(x) for x in t[:, 3] if x > 0])
 print(f"CTA end: min {e.min():.2f} median {np.median(e):.2f} max {e.max():.2f} us")
 st = np.array([us(x) for x in t[:, 0] if x > 0])
