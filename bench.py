@@ -190,10 +190,20 @@ def run_gpu(args, cfg, rank, world, local_rank):
     ws = torch.empty(max(mt["ws_bytes"] for mt in mats), dtype=torch.uint8, device=dev)
     for mt in mats:
         mt["ws"] = ws
+    # multi-matmul steps (C5) go through the batched call: the pack of matmul i
+    # overlaps the contraction of matmul i+1 on the library's side stream
+    jobs = [dict(encw=mt["encw"], X=mt["X"], k_per_query=mt["lay"].k_per_query, n_queries=mt["lay"].n_queries,
+                 mask_seed=mt["seed"], cts=mt["cts"], R=mt["R"]) for mt in mats]
+    ws_batch = None
+    if len(mats) > 1:
+        ws_batch = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs), dtype=torch.uint8, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
     def step():
+        if ws_batch is not None:
+            nb.nimbus_cop_matmul_batch(ctx, jobs, ws_batch)
+            return
         for mt in mats:
             lay = mt["lay"]
             nb.nimbus_cop_matmul(ctx, mt["encw"], mt["X"], lay.k_per_query, lay.n_queries, mt["seed"],

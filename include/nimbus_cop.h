@@ -132,6 +132,27 @@ nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* encw, const 
                                 uint32_t* d_cts, uint32_t* d_R, void* d_ws, size_t ws_bytes,
                                 void* stream);
 
+/* A sequence of COP matmuls (e.g. all linear layers of a model pass, SURVEY.md
+ * config C5): equivalent to nimbus_cop_matmul for jobs[0..count-1] in order,
+ * with identical outputs, but the memory-bound pack/mod-switch/mask of job i
+ * runs on a library-owned side stream concurrently with the tensor-bound
+ * contraction of job i+1 (two C buffers in the workspace, event-ordered).
+ * Everything is complete in `stream` order when the call's work on `stream` is.
+ * Workspace: nimbus_cop_workspace_size_batch.  Each job's buffers as in
+ * nimbus_cop_matmul.  Errors are checked for all jobs before any launch. */
+typedef struct {
+    const nimbus_encw* encw;
+    const uint32_t* d_X;          /* k x m, k = n_queries * k_per_query */
+    uint32_t k_per_query, n_queries;
+    uint64_t mask_seed;
+    uint32_t* d_cts;              /* n_queries x n_cts x 2 x L_out x N */
+    uint32_t* d_R;                /* k x n */
+} nimbus_cop_job;
+nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
+                                              size_t* bytes);
+nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+                                      size_t ws_bytes, void* stream);
+
 /* Same computation with HOST buffers: copies h_X in, runs nimbus_cop_matmul,
  * copies h_cts and h_R out, and synchronises `stream` before returning. */
 nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* h_X,

@@ -167,6 +167,8 @@ void nimbus_ctx_destroy(nimbus_ctx* ctx) {
     if (ctx->d_flag) cudaFree(ctx->d_flag);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->ev_pending) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->sync_ev) cudaEventDestroy(e);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     delete ctx;
 }
 
@@ -371,7 +373,7 @@ nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq,
                               uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* stream) {
     if (!ctx || !d_C || !d_cts || !d_R || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
-    CK(launch_pack(ctx, d_C, kq, nq, n, seed, d_cts, d_R, (cudaStream_t)stream), "pack");
+    CK(launch_pack(ctx, d_C, kq, nq, n, seed, d_cts, d_R, (cudaStream_t)stream, true), "pack");
     return NIMBUS_OK;
 }
 
@@ -390,8 +392,84 @@ nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uin
     st = run_accumulate(ctx, w, d_X, k, C, (uint8_t*)d_ws, s);
     if (st != NIMBUS_OK) return st;
     prof_mark(ctx, s);
-    CK(launch_pack(ctx, C, kq, nq, w->n, seed, d_cts, d_R, s), "pack");
     prof_mark(ctx, s);
+    CK(launch_pack(ctx, C, kq, nq, w->n, seed, d_cts, d_R, s, true), "pack");
+    prof_mark(ctx, s);
+    return NIMBUS_OK;
+}
+
+// ---------------------------------------------------------------- batched online path
+static size_t al1k(size_t x) { return (x + 1023) & ~size_t(1023); }
+
+nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
+                                              size_t* bytes) {
+    if (!ctx || !jobs || !bytes || count == 0) return NIMBUS_EINVAL;
+    size_t xt = 0, c = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        if (!jobs[i].encw) return NIMBUS_EINVAL;
+        const uint32_t k = jobs[i].k_per_query * jobs[i].n_queries;
+        const WsLayout L = ws_layout(ctx, jobs[i].encw, k);
+        xt = xt > L.c ? xt : L.c;                                   // X planes (1 KB aligned)
+        const size_t cb = al1k((size_t)k * ncols(ctx) * 4);
+        c = c > cb ? c : cb;
+    }
+    *bytes = xt + 2 * c;
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+                                      size_t ws_bytes, void* stream) {
+    if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    for (uint32_t i = 0; i < count; i++) {
+        nimbus_status st = check_online(ctx, jobs[i].encw, jobs[i].k_per_query, jobs[i].n_queries);
+        if (st != NIMBUS_OK) return st;
+        if (!jobs[i].d_X || !jobs[i].d_cts || !jobs[i].d_R) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
+    }
+    size_t need = 0;
+    nimbus_cop_workspace_size_batch(ctx, jobs, count, &need);
+    if (ws_bytes < need) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    size_t xt = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        const WsLayout L = ws_layout(ctx, jobs[i].encw, jobs[i].k_per_query * jobs[i].n_queries);
+        xt = xt > L.c ? xt : L.c;
+    }
+    const size_t cbytes = (need - xt) / 2;
+    uint8_t* ws = (uint8_t*)d_ws;
+    uint32_t* Cbuf[2] = {reinterpret_cast<uint32_t*>(ws + xt), reinterpret_cast<uint32_t*>(ws + xt + cbytes)};
+    cudaStream_t a = (cudaStream_t)stream;
+    if (!ctx->side) CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
+    cudaStream_t b = ctx->side;
+    while (ctx->sync_ev.size() < 2 * (size_t)count + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        ctx->sync_ev.push_back(e);
+    }
+    cudaEvent_t* done_c = ctx->sync_ev.data();             // contraction i finished (stream a)
+    cudaEvent_t* done_p = ctx->sync_ev.data() + count;     // pack i finished (stream b)
+    cudaEvent_t start = ctx->sync_ev[2 * count];
+    // the side stream must not start before earlier work on `stream`
+    CK(cudaEventRecord(start, a), "record");
+    CK(cudaStreamWaitEvent(b, start, 0), "wait");
+    for (uint32_t i = 0; i < count; i++) {
+        const nimbus_cop_job& J = jobs[i];
+        const uint32_t k = J.k_per_query * J.n_queries;
+        uint32_t* C = Cbuf[i & 1];
+        // C[i%2] is free once the pack of job i-2 has read it
+        if (i >= 2) CK(cudaStreamWaitEvent(a, done_p[i - 2], 0), "wait pack");
+        prof_mark(ctx, a);
+        nimbus_status st = run_accumulate(ctx, J.encw, J.d_X, k, C, ws, a);
+        if (st != NIMBUS_OK) return st;
+        prof_mark(ctx, a);
+        CK(cudaEventRecord(done_c[i], a), "record");
+        // pack of job i overlaps the contraction of job i+1 (memory- vs tensor-bound)
+        CK(cudaStreamWaitEvent(b, done_c[i], 0), "wait contraction");
+        prof_mark(ctx, b);
+        CK(launch_pack(ctx, C, J.k_per_query, J.n_queries, J.encw->n, J.mask_seed, J.d_cts, J.d_R, b, false),
+           "pack");
+        prof_mark(ctx, b);
+        CK(cudaEventRecord(done_p[i], b), "record");
+    }
+    CK(cudaStreamWaitEvent(a, done_p[count - 1], 0), "join");   // everything complete in `stream` order
     return NIMBUS_OK;
 }
 
@@ -404,12 +482,14 @@ nimbus_status nimbus_profile_enable(nimbus_ctx* ctx, int on) {
 nimbus_status nimbus_profile_read(nimbus_ctx* ctx, double* ms, uint64_t* calls, int reset) {
     if (!ctx) return NIMBUS_EINVAL;
     auto& P = ctx->ev_pending;
-    for (size_t i = 0; i + 4 <= P.size(); i += 4) {
-        CK(cudaEventSynchronize(P[i + 3]), "profile sync");
+    // groups of 5: before slice, after slice, after contraction, before pack, after pack
+    for (size_t i = 0; i + 5 <= P.size(); i += 5) {
+        CK(cudaEventSynchronize(P[i + 4]), "profile sync");
+        CK(cudaEventSynchronize(P[i + 2]), "profile sync");
         float a = 0, b = 0, c = 0;
         cudaEventElapsedTime(&a, P[i], P[i + 1]);
         cudaEventElapsedTime(&b, P[i + 1], P[i + 2]);
-        cudaEventElapsedTime(&c, P[i + 2], P[i + 3]);
+        cudaEventElapsedTime(&c, P[i + 3], P[i + 4]);
         ctx->prof_ms[0] += a; ctx->prof_ms[1] += b; ctx->prof_ms[2] += c;
         ctx->prof_calls++;
     }

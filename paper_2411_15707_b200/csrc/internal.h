@@ -35,6 +35,9 @@ struct nimbus_ctx {
     std::vector<cudaEvent_t> ev_pool, ev_pending;
     double prof_ms[3] = {0, 0, 0};
     uint64_t prof_calls = 0;
+    // batched path (nimbus_cop_matmul_batch): side stream for the pack kernels + sync events
+    cudaStream_t side = nullptr;
+    std::vector<cudaEvent_t> sync_ev;
 };
 
 struct nimbus_sk {
@@ -78,7 +81,7 @@ cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, u
 cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB,
                            uint8_t* d_Xt, cudaStream_t st);
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
-                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st);
+                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl);
 // cop_cc.cu
 cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                 uint32_t* d_C, cudaStream_t st);

@@ -141,28 +141,35 @@ __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict
     if (comp == 0 && J < rows * n) VecU32<V>::store(Rout + row0 * n + J, rmask);
 }
 
+template <typename K, typename... Args>
+static cudaError_t launch_maybe_pdl(bool pdl, K kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    if (pdl) return launch_pdl(kernel, grid, block, 0, st, args...);
+    kernel<<<grid, block, 0, st>>>(args...);
+    return cudaGetLastError();
+}
+
 template <int V>
 static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                            uint32_t* d_cts, uint32_t* d_R, cudaStream_t st) {
+                            uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     const uint32_t per_block = 128 * V;
     dim3 grid((N + per_block - 1) / per_block, nq * nct, 2);
     const uint64_t key = prg_key(seed, 6);
     switch (c->rns.L) {
-        case 1: return launch_pdl(k_pack<V, 1>, grid, dim3(128), 0, st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 2: return launch_pdl(k_pack<V, 2>, grid, dim3(128), 0, st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 3: return launch_pdl(k_pack<V, 3>, grid, dim3(128), 0, st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        default: return launch_pdl(k_pack<V, 4>, grid, dim3(128), 0, st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 1: return launch_maybe_pdl(pdl, k_pack<V, 1>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 2: return launch_maybe_pdl(pdl, k_pack<V, 2>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 3: return launch_maybe_pdl(pdl, k_pack<V, 3>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        default: return launch_maybe_pdl(pdl, k_pack<V, 4>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
     }
 }
 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
-                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st) {
+                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     const uint64_t threads_v1 = 2ull * nq * nct * N;      // one thread per (comp, J)
     const bool vec = (n % 4 == 0) && threads_v1 / 4 >= 8ull * 128 * (uint64_t)c->num_sms;
-    cudaError_t e = vec ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st)
-                        : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st);
+    cudaError_t e = vec ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl)
+                        : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
     c->launches++;
     return e;
 }

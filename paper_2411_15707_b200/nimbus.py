@@ -59,6 +59,8 @@ _SIGS = {
     "nimbus_prg_words": (C.c_int, [_u64, _u32, _u64, _u64, _vp, _vp]),
     "nimbus_negacyclic_mul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp]),
     "nimbus_launch_count": (_u64, [_vp]),
+    "nimbus_cop_workspace_size_batch": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
+    "nimbus_cop_matmul_batch": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_profile_enable": (C.c_int, [_vp, C.c_int]),
     "nimbus_profile_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(_u64), C.c_int]),
 }
@@ -253,6 +255,31 @@ def nimbus_cop_matmul(ctx: Context, w: EncW, X: torch.Tensor, k_per_query: int, 
                                    mask_seed, _ptr(cts, torch.int32, "cts"), _ptr(R, torch.int32, "R"),
                                    _ptr(ws), ws.numel(), _stream(stream)), ctx)
     return cts, R
+
+
+class nimbus_cop_job(C.Structure):
+    _fields_ = [("encw", _vp), ("d_X", _vp), ("k_per_query", _u32), ("n_queries", _u32),
+                ("mask_seed", _u64), ("d_cts", _vp), ("d_R", _vp)]
+
+
+def _jobs(jobs):
+    """jobs: sequence of dicts with encw, X, k_per_query, n_queries, mask_seed, cts, R."""
+    arr = (nimbus_cop_job * len(jobs))()
+    for i, j in enumerate(jobs):
+        arr[i] = nimbus_cop_job(j["encw"].ptr, _ptr(j["X"], torch.int32, "X"), j["k_per_query"], j["n_queries"],
+                                j["mask_seed"], _ptr(j["cts"], torch.int32, "cts"), _ptr(j["R"], torch.int32, "R"))
+    return arr
+
+
+def nimbus_cop_workspace_size_batch(ctx: Context, jobs) -> int:
+    out = _sz()
+    _check(lib().nimbus_cop_workspace_size_batch(ctx.ptr, _jobs(jobs), len(jobs), C.byref(out)), ctx)
+    return int(out.value)
+
+
+def nimbus_cop_matmul_batch(ctx: Context, jobs, ws: torch.Tensor, stream=None):
+    arr = _jobs(jobs)
+    _check(lib().nimbus_cop_matmul_batch(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(), _stream(stream)), ctx)
 
 
 def nimbus_cop_matmul_host(ctx: Context, w: EncW, X_host: torch.Tensor, k_per_query: int,

@@ -306,3 +306,53 @@ def test_error_codes(nb, oracle):
     with pytest.raises(nb.NimbusError) as e:
         nb.nimbus_cop_matmul(ctxr, wr, dev_u32(ni.gen_X(1, 4, 8, 16)), 4, 1, 1, cts, R, ws[:16])
     assert e.value.status == -2
+
+
+def test_batch_matches_sequential_and_oracle(nb, oracle):
+    """nimbus_cop_matmul_batch (pack of job i overlapped with the contraction of
+    job i+1 on a side stream) gives the same bytes as job-by-job calls, and the
+    oracle's, for a mixed sequence of shapes sharing one context."""
+    N, L, ell, L_out = 4096, 2, 16, 1
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
+    sk = nb.nimbus_keygen(ctx, 91)
+    shapes = [(128, 768, 768, 1), (64, 300, 700, 2), (128, 768, 3072, 1), (100, 1000, 500, 1), (20, 64, 64, 3)]
+    jobs, seq = [], []
+    for i, (kq, m, n, nq) in enumerate(shapes):
+        W = ni.gen_W(100 + i, m, n, ell)
+        X = ni.gen_X(200 + i, kq * nq, m, ell)
+        w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W), 100 + i)
+        cts, R = nb.alloc_outputs(ctx, w, kq, nq)
+        jobs.append(dict(encw=w, X=dev_u32(X), k_per_query=kq, n_queries=nq, mask_seed=300 + i, cts=cts, R=R,
+                         W=W, Xh=X))
+    ws = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs), dtype=torch.uint8, device=DEV)
+    nb.nimbus_cop_matmul_batch(ctx, jobs, ws)
+    nb.nimbus_sync(ctx)
+    for j in jobs:
+        kq, nq = j["k_per_query"], j["n_queries"]
+        ws1 = nb.alloc_workspace(ctx, j["encw"], kq * nq)
+        c2, R2 = nb.alloc_outputs(ctx, j["encw"], kq, nq)
+        nb.nimbus_cop_matmul(ctx, j["encw"], j["X"], kq, nq, j["mask_seed"], c2, R2, ws1)
+        nb.nimbus_sync(ctx)
+        assert torch.equal(c2, j["cts"]) and torch.equal(R2, j["R"])
+    j = jobs[1]
+    s = oracle.keygen(N, 91)
+    E = oracle.encrypt_rows(N, L, pr, ell, s, j["W"], 101)
+    cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E, j["Xh"], j["W"].shape[1], j["k_per_query"],
+                                   j["n_queries"], j["mask_seed"])
+    assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all()
+
+
+@pytest.mark.parametrize("env", [{"NIMBUS_NO_RESIDENT": "1"}, {"NIMBUS_CLUSTER": "2"},
+                                 {"NIMBUS_NO_RESIDENT": "1", "NIMBUS_CLUSTER": "2"}])
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [(4096, 2, 16, 1, 768, 768, 128, 1),
+                                                     (8192, 3, 32, 2, 300, 1000, 70, 3)])
+def test_kernel_variants_parity(nb, oracle, monkeypatch, env, N, L, ell, L_out, m, n, kq, nq):
+    """The non-default kernel variants (48-column streaming kernel for ell=16,
+    2-CTA clusters with X multicast) give the same bytes as the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=777 + m)
+    cts, R = c.run()
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()

@@ -34,6 +34,6 @@ sust = 2 * M * N * K * n / (s.elapsed_time(e) / 1e3) / 1e12
 out = {"int8_tops_burst": round(burst, 1), "int8_tops_sustained": round(sust, 1),
        "how": "torch._int_mm int8 8192^3 (2*N^3 ops): best of 10 (burst); back to back for 4 s (sustained)",
        "gpu": torch.cuda.get_device_name()}
-os.makedirs("profiles", exist_ok=True)
-json.dump(out, open("profiles/int8_peak.json", "w"), indent=1)
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump(out, open("gpurun_out/int8_peak.json", "w"), indent=1)
 print(json.dumps(out))
