@@ -234,7 +234,11 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     if (!w) return NIMBUS_ENOMEM;
     w->ctx = ctx; w->m = m; w->n = n; w->KB = (m + kBK - 1) / kBK;
     // resident-X kernel (tcgen05, ell <= 16, m <= 768) uses 32-column tiles, the streaming kernel 48
-    w->bn = (ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && sx_of(ctx->rns.ell) == 2 && w->KB <= kResMaxKB && !getenv("NIMBUS_NO_RESIDENT")) ? kBNR : kBNT;
+    w->bn = kBNT;
+    if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
+        if (sx_of(ctx->rns.ell) == 2 && w->KB <= kResMaxKB && !getenv("NIMBUS_NO_RESIDENT")) w->bn = kBNR;
+        else if (sx_of(ctx->rns.ell) == 4 && ctx->rns.N >= kBNW && !getenv("NIMBUS_NO_TRANSPOSED")) w->bn = kBNW;
+    }
     w->bytes = (size_t)w->KB * kBK * col_tiles(ctx, w->bn) * w->bn * 4;
     cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
     if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "encw alloc"); }
@@ -346,7 +350,7 @@ static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
                                     uint32_t* d_C, uint8_t* ws, cudaStream_t s) {
     if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
         uint8_t* xt = ws + ws_layout(ctx, w, k).xt;
-        CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, xt, s), "slice X");
+        CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, w->bn == kBNW ? kRTT : kBM, xt, s), "slice X");
         prof_mark(ctx, s);
         CK(launch_cop_tcgen05(ctx, w, xt, k, d_C, s), "cop tcgen05");
     } else {

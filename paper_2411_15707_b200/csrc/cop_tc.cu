@@ -277,17 +277,19 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
 struct ResCfg {
     static constexpr uint32_t BM = kBM, BN = kBNR, BK = kBK, SX = 2;
     static constexpr uint32_t SLICE = BM * BK;                 // one X slice, one k-block: 16 KB
-    static constexpr uint32_t B_BYTES = kSW * BN * BK;         // 16 KB
-    static constexpr uint32_t STAGES = 5;
+    static constexpr uint32_t B_BYTES = kSW * BN * BK;         // Enc(W) per k-block: 16 KB
+    static constexpr uint32_t KPS = 2;                         // k-blocks per ring slot: one 32 KB bulk copy
+    static constexpr uint32_t SLOT = KPS * B_BYTES;
+    static constexpr uint32_t STAGES = 3;
     static constexpr uint32_t NACC = SX + kSW - 1;             // 5
     static constexpr uint32_t ACC_COLS = NACC * BN;            // 160
     static constexpr uint32_t A0_COLS = kResMaxKB * (BK / 4);  // slice 0 in TMEM: 32 columns per k-block
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t EPI_WARPS = 8;
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
-    // smem: slice 1 resident [KB][16 KB] | slice 0 staging [2][16 KB] | B ring [STAGES][16 KB]
-    static constexpr uint32_t OFF_A1 = 0, OFF_STG = kResMaxKB * SLICE, OFF_B = OFF_STG + 2 * SLICE;
-    static constexpr size_t SMEM = (size_t)OFF_B + STAGES * B_BYTES + 1024 + 256;
+    // smem: slice 1 resident [KB][16 KB] | slice 0 staging [KPS][16 KB] | E ring [STAGES][32 KB]
+    static constexpr uint32_t OFF_A1 = 0, OFF_STG = kResMaxKB * SLICE, OFF_B = OFF_STG + KPS * SLICE;
+    static constexpr size_t SMEM = (size_t)OFF_B + STAGES * SLOT + 1024 + 256;
     static_assert(A0_COLS + 2 * ACC_COLS <= TMEM_COLS, "TMEM budget");
     static_assert(SMEM <= 232448, "shared memory");
 };
@@ -298,7 +300,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
     using Cfg = ResCfg;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::B_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::SLOT);
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;
     uint64_t* tempty = tfull + 2;
@@ -326,26 +328,31 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- producer: E every tile; X slices during the first tile only
+            // ---------------- producer: E every tile (32 KB copies = 2 k-blocks); X slices in the first tile
             const uint64_t pol_a = policy_evict_last();
             const uint64_t pol_b = policy_evict_first();
+            const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
             uint32_t it = 0, ti = 0;
             for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
                 const uint8_t* b_src = Et + (size_t)ct * KB * Cfg::B_BYTES;
-                for (uint32_t kb = 0; kb < KB; kb++, it++) {
+                for (uint32_t kp = 0; kp < KP; kp++, it++) {
                     const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
+                    const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
                     if (it >= Cfg::STAGES) mbar_wait(&empty[s], ph ^ 1);
-                    if (ti == 1 && kb < 8) TRACE(52 + kb);
+                    if (ti == 1 && kp < 8) TRACE(52 + kp);
                     const bool first = ti == 0;
-                    mbar_arrive_expect_tx(&full[s], Cfg::B_BYTES + (first ? 2 * Cfg::SLICE : 0));
-                    bulk_g2s(smem + Cfg::OFF_B + s * Cfg::B_BYTES, b_src + (size_t)kb * Cfg::B_BYTES, Cfg::B_BYTES,
+                    mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES + (first ? nkb * 2 * Cfg::SLICE : 0));
+                    bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES,
                              &full[s], pol_b);
                     if (first) {
-                        if (kb == 0) { pdl_wait(); TRACE(2); }
-                        const uint8_t* xsrc = Xt + (size_t)kb * 2 * Cfg::SLICE;   // Xt[0][kb][slice][128][128]
-                        if (kb >= 2) mbar_wait(&sfree[kb & 1], ((kb >> 1) - 1) & 1);
-                        bulk_g2s(smem + Cfg::OFF_STG + (kb & 1) * Cfg::SLICE, xsrc, Cfg::SLICE, &full[s], pol_a);
-                        bulk_g2s(smem + Cfg::OFF_A1 + kb * Cfg::SLICE, xsrc + Cfg::SLICE, Cfg::SLICE, &full[s], pol_a);
+                        if (kp == 0) { pdl_wait(); TRACE(2); }
+                        else mbar_wait(&sfree[0], (kp - 1) & 1);       // staging copied into TMEM
+                        for (uint32_t q = 0; q < nkb; q++) {
+                            const uint8_t* xsrc = Xt + (size_t)(kb0 + q) * 2 * Cfg::SLICE;   // Xt[0][kb][slice]
+                            bulk_g2s(smem + Cfg::OFF_STG + q * Cfg::SLICE, xsrc, Cfg::SLICE, &full[s], pol_a);
+                            bulk_g2s(smem + Cfg::OFF_A1 + (kb0 + q) * Cfg::SLICE, xsrc + Cfg::SLICE, Cfg::SLICE,
+                                     &full[s], pol_a);
+                        }
                     }
                 }
             }
@@ -356,6 +363,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 128
             constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 96
             constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = 32
+            const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
             uint32_t it = 0, ti = 0;
             for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
                 const uint32_t buf = ti & 1, use = ti >> 1;
@@ -363,34 +371,40 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                 TRACE(4 + 4 * ti);
                 tc_fence_after();
                 const uint32_t dacc = tmem + Cfg::A0_COLS + buf * Cfg::ACC_COLS;
-                for (uint32_t kb = 0; kb < KB; kb++, it++) {
+                for (uint32_t kp = 0; kp < KP; kp++, it++) {
                     const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
+                    const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
                     mbar_wait(&full[s], ph);
-                    if (ti == 1 && kb < 8) TRACE(40 + kb);
+                    if (ti == 1 && kp < 8) TRACE(40 + kp);
                     tc_fence_after();
-                    const uint32_t a0t = tmem + kb * (Cfg::BK / 4);                      // slice 0, TMEM
-                    const uint32_t a1 = smem_u32(smem + Cfg::OFF_A1 + kb * Cfg::SLICE);  // slice 1, smem
-                    const uint32_t b0 = smem_u32(smem + Cfg::OFF_B + s * Cfg::B_BYTES);
                     if (ti == 0) {
-                        // first tile: move this k-block of slice 0 into TMEM (in issue order with the MMAs)
-                        const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + (kb & 1) * Cfg::SLICE);
+                        // first tile: move these k-blocks of slice 0 into TMEM (in issue order with the MMAs)
+                        for (uint32_t q = 0; q < nkb; q++) {
+                            const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + q * Cfg::SLICE);
 #pragma unroll
-                        for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
-                            tmem_cp_128x256b(a0t + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
-                        mma_commit(&sfree[kb & 1]);
+                            for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
+                                tmem_cp_128x256b(tmem + (kb0 + q) * (Cfg::BK / 4) + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
+                        }
+                        mma_commit(&sfree[0]);
                     }
+                    for (uint32_t q = 0; q < nkb; q++) {
+                        const uint32_t kb = kb0 + q;
+                        const uint32_t a0t = tmem + kb * (Cfg::BK / 4);                      // slice 0, TMEM
+                        const uint32_t a1 = smem_u32(smem + Cfg::OFF_A1 + kb * Cfg::SLICE);  // slice 1, smem
+                        const uint32_t b0 = smem_u32(smem + Cfg::OFF_B + s * Cfg::SLOT + q * Cfg::B_BYTES);
 #pragma unroll
-                    for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
-                        const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
-                        const uint32_t first = (kb | kk) == 0;
-                        mma_i8_ts(dacc, a0t + kk * 8, bd, idesc_full, !first);          // x_0 e_j -> acc_j
-                        const uint64_t ad1 = sdesc_kmajor_sw128(a1 + kk * 32);
-                        if (!first) {
-                            mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_full, 1u);          // x_1 e_j -> acc_{j+1}
-                        } else {
-                            mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_lo, 1u);
-                            const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (kSW - 1) * Cfg::BN * Cfg::BK + kk * 32);
-                            mma_i8_ss(dacc + kSW * Cfg::BN, ad1, bd3, idesc_one, 0u);
+                        for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
+                            const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
+                            const uint32_t first = (kb | kk) == 0;
+                            mma_i8_ts(dacc, a0t + kk * 8, bd, idesc_full, !first);          // x_0 e_j -> acc_j
+                            const uint64_t ad1 = sdesc_kmajor_sw128(a1 + kk * 32);
+                            if (!first) {
+                                mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_full, 1u);          // x_1 e_j -> acc_{j+1}
+                            } else {
+                                mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_lo, 1u);
+                                const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (kSW - 1) * Cfg::BN * Cfg::BK + kk * 32);
+                                mma_i8_ss(dacc + kSW * Cfg::BN, ad1, bd3, idesc_one, 0u);
+                            }
                         }
                     }
                     mma_commit(&empty[s]);
@@ -414,6 +428,170 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) TRACE(3);
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, Cfg::TMEM_COLS);
+    }
+}
+
+// ------------------------------------------------------------------ transposed kernel (ell = 32)
+// D[coefficient column][row]: the 4 Enc(W) byte planes are the MMA A operand
+// (M = 128 coefficient columns per plane) and the 4 X slices of a 64-row tile
+// are stacked along N = 256, so one MMA per (plane j, 32-byte k-step) with D at
+// TMEM column 64 j writes x_i e_j into acc_{i+j} (columns [64(i+j), +64)).  Per
+// k-block it moves 64 KB of E + 32 KB of X into shared memory for 8192
+// outputs, against 64 KB of X + 24 KB of E for 6144 in the streaming kernel:
+// the L2->SM delivery rate is what bounds ell = 32.  The epilogue thread owns
+// one coefficient column and writes rows, so stores are coalesced across lanes.
+struct TCfgT {
+    static constexpr uint32_t BM = kBNW, RT = kRTT, BK = kBK, SX = 4;
+    static constexpr uint32_t A_BYTES = kSW * BM * BK;     // 64 KB: 4 planes x 128 columns x 128 B
+    static constexpr uint32_t B_BYTES = SX * RT * BK;      // 32 KB: 4 slices x 64 rows x 128 B
+    static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+    static constexpr uint32_t STAGES = 2;
+    static constexpr uint32_t NACC = SX + kSW - 1;         // 7 accumulators x 64 columns = 448
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t EPI_WARPS = 8;
+    static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
+    static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
+    static_assert(NACC * RT <= TMEM_COLS, "TMEM");
+    static_assert(SMEM <= 232448, "shared memory");
+};
+
+__global__ void __launch_bounds__(TCfgT::THREADS, 1)
+k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t RTt,
+           uint32_t CT, uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
+    using Cfg = TCfgT;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nunits = RTt * CT;
+    if (threadIdx.x == 0) TRACE(0);
+    if (warp == 0 && lane == 0) {
+        for (uint32_t s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, Cfg::EPI_WARPS);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) TRACE(1);
+    pdl_trigger();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- producer
+            const uint64_t pol_x = policy_evict_last();
+            const uint64_t pol_e = policy_evict_last();   // an E tile is reused by every row tile (L2)
+            uint32_t it = 0;
+            bool waited = false;
+            for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const uint32_t rt = u % RTt, ct = u / RTt;
+                for (uint32_t kb = 0; kb < KB; kb++, it++) {
+                    const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
+                    if (it >= Cfg::STAGES) mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* sa = smem + s * Cfg::STAGE;
+                    mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
+                    bulk_g2s(sa, Et + ((size_t)ct * KB + kb) * Cfg::A_BYTES, Cfg::A_BYTES, &full[s], pol_e);
+                    if (!waited) { pdl_wait(); waited = true; TRACE(2); }
+                    bulk_g2s(sa + Cfg::A_BYTES, Xt + ((size_t)rt * KB + kb) * Cfg::B_BYTES, Cfg::B_BYTES, &full[s],
+                             pol_x);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer
+            constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, Cfg::SX * Cfg::RT);         // N = 256
+            constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (Cfg::SX - 1) * Cfg::RT);     // N = 192
+            constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::RT);                    // N = 64
+            uint32_t it = 0, ti = 0;
+            for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
+                if (ti >= 1) mbar_wait(tempty, (ti - 1) & 1);
+                TRACE(4 + 4 * ti);
+                tc_fence_after();
+                for (uint32_t kb = 0; kb < KB; kb++, it++) {
+                    const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + s * Cfg::STAGE);
+                    const uint32_t b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+                    for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
+                        const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
+#pragma unroll
+                        for (uint32_t j = 0; j < kSW; j++) {
+                            const uint64_t ad = sdesc_kmajor_sw128(a0 + j * Cfg::BM * Cfg::BK + kk * 32);
+                            if ((kb | kk) != 0 || j == 0) {
+                                mma_i8_ss(tmem + j * Cfg::RT, ad, bd, idesc_full, (kb | kk) != 0);
+                            } else {
+                                // first k-step, j >= 1: acc_j..acc_{j+2} exist, acc_{j+3} is new
+                                mma_i8_ss(tmem + j * Cfg::RT, ad, bd, idesc_lo, 1u);
+                                const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (Cfg::SX - 1) * Cfg::RT * Cfg::BK + kk * 32);
+                                mma_i8_ss(tmem + (j + Cfg::SX - 1) * Cfg::RT, ad, bd3, idesc_one, 0u);
+                            }
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(tfull);
+                TRACE(5 + 4 * ti);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: lane = coefficient column, 8 rows per tcgen05.ld
+        const uint32_t ew = warp - 4;
+        const uint32_t sub = ew & 3, half = ew >> 2;
+        uint32_t ti = 0;
+        for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
+            const uint32_t rt = u % RTt, ct = u / RTt;
+            mbar_wait(tfull, ti & 1);
+            if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
+            tc_fence_after();
+            const uint32_t col = ct * Cfg::BM + sub * 32 + lane;
+            const uint32_t limb = (col / R.N) % R.L;
+            const uint32_t p = R.p[limb], c32 = R.c32[limb];
+            const uint32_t tbase = tmem + ((sub * 32) << 16) + half * 32;
+#pragma unroll 1
+            for (uint32_t c0 = 0; c0 < 4; c0 += 2) {
+                uint32_t v[2][Cfg::NACC][8];
+#pragma unroll
+                for (uint32_t b = 0; b < 2; b++)
+#pragma unroll
+                    for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld8(tbase + s * Cfg::RT + (c0 + b) * 8, v[b][s]);
+                tmem_ld_wait();
+#pragma unroll
+                for (uint32_t b = 0; b < 2; b++) {
+#pragma unroll
+                    for (uint32_t q = 0; q < 8; q++) {
+                        const uint32_t row = rt * Cfg::RT + half * 32 + (c0 + b) * 8 + q;
+                        uint64_t x = mad_wide(v[b][1][q], 1u << 8, v[b][0][q]);
+                        x = mad_wide(v[b][2][q], 1u << 16, x);
+                        x = mad_wide(v[b][3][q], 1u << 24, x);
+#pragma unroll
+                        for (uint32_t s = 4; s < Cfg::NACC; s++) x = mad_wide(v[b][s][q], R.pow8[limb][s], x);
+                        if (row < k && col < ncol) C[(size_t)row * ncol + col] = reduce64_pm(x, p, c32);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
             if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
         }
     }
@@ -481,6 +659,24 @@ static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t
     return e;
 }
 
+static cudaError_t launch_t(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
+                            cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_cop_tc_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TCfgT::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const uint32_t ncol = 2 * c->rns.L * c->rns.N;
+    const uint32_t CT = col_tiles(c, kBNW), RTt = (k + kRTT - 1) / kRTT;
+    const uint32_t nunits = CT * RTt;
+    const uint32_t grid = nunits < (uint32_t)c->num_sms ? nunits : (uint32_t)c->num_sms;
+    cudaError_t e = launch_pdl(k_cop_tc_t, dim3(grid), dim3(TCfgT::THREADS), TCfgT::SMEM, st, c->rns, d_Xt,
+                               (const uint8_t*)w->d_Et, k, RTt, CT, w->KB, ncol, d_C);
+    c->launches++;
+    return e;
+}
+
 template <int SX, int BN>
 static cudaError_t launch_cl(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                              cudaStream_t st) {
@@ -490,6 +686,10 @@ static cudaError_t launch_cl(nimbus_ctx* c, const nimbus_encw* w, const uint8_t*
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st) {
     const uint32_t SX = sx_of(c->rns.ell);
+    if (w->bn == kBNW) {
+        if (SX != 4) return cudaErrorInvalidValue;
+        return launch_t(c, w, d_Xt, k, d_C, st);
+    }
     if (w->bn == kBNR) {
         if (SX == 2 && k <= kBM && w->KB <= kResMaxKB) return launch_res(c, w, d_Xt, k, d_C, st);
         switch (SX) {

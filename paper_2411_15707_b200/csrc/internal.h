@@ -15,6 +15,8 @@ typedef unsigned __int128 u128;
 constexpr uint32_t kBK = 128;      // beta (contraction) bytes per k-block = one 128-B swizzle row
 constexpr uint32_t kBNT = 48;      // coefficient columns per Enc(W) tile, streaming kernel (4 planes -> MMA N = 192)
 constexpr uint32_t kBNR = 32;      // tile width of the resident-X kernel (ell <= 16, m <= 768; MMA N = 128)
+constexpr uint32_t kBNW = 128;     // tile width of the transposed ell = 32 kernel (E planes are the MMA A operand)
+constexpr uint32_t kRTT = 64;      // X rows per tile of the transposed kernel (4 slices x 64 rows -> MMA N = 256)
 constexpr uint32_t kResMaxKB = 6;  // resident-X kernel: at most 6 k-blocks (m <= 768) of X in TMEM + smem
 constexpr uint32_t kBM = 128;      // rows (alpha) per X tile = tcgen05 M
 constexpr uint32_t kSW = 4;        // 8-bit slices of a 31-bit residue (S_w)
@@ -78,7 +80,7 @@ cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m,
                              uint8_t* d_Et, cudaStream_t st);
 cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t bn,
                                uint32_t* d_canon, cudaStream_t st);
-cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB,
+cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st);
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                         uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl);

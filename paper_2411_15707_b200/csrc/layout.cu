@@ -9,57 +9,18 @@
 // stored at chunk position c ^ (r & 7) -- the 128-byte swizzle that the
 // tcgen05 shared-memory descriptor (SWIZZLE_128B, K-major) expects, applied
 // once at rest so that one linear bulk copy lands a ready-to-use operand tile.
-#include "internal.h"
+#include "slice_dev.cuh"
 
 namespace nimbus {
 
-__device__ __forceinline__ uint32_t swz_off(uint32_t r, uint32_t chunk) {
-    return r * 128u + ((chunk ^ (r & 7u)) << 4);
-}
-
-// ---------------------------------------------------------------- K4 slice X
-// X[alpha][beta] = sum_i x_i 2^(8i) (unsigned representative)
-// Xt[mt][kb][i][128 rows][128 B], zero padded to whole tiles.
-template <int SX>
+template <int SX, int RT>
 __global__ void k_slice_x(const uint32_t* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB, uint32_t ell,
                           uint8_t* __restrict__ Xt, uint32_t total, uint32_t* flag, int check) {
     pdl_trigger();
     pdl_wait();          // Xt may still be read by the previous contraction in the stream
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= total) return;
-    const uint32_t alpha = idx / (KB * 8), ch = idx % (KB * 8);
-    const uint32_t kb = ch >> 3, c16 = ch & 7;
-    const uint32_t beta0 = kb * kBK + c16 * 16;
-    uint32_t v[16];
-    if (alpha < k && beta0 + 16 <= m && (m & 3) == 0) {
-        const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)alpha * m + beta0);
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            uint4 w = __ldg(src + q);
-            v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
-        }
-    } else {
-#pragma unroll
-        for (int u = 0; u < 16; u++)
-            v[u] = (alpha < k && beta0 + u < m) ? X[(size_t)alpha * m + beta0 + u] : 0u;
-    }
-    if (check) {
-        uint32_t bad = 0;
-#pragma unroll
-        for (int u = 0; u < 16; u++) bad |= (v[u] >> ell);
-        if (bad) atomicOr(flag, 1u);
-    }
-    const uint32_t mt = alpha / kBM, r = alpha % kBM;
-#pragma unroll
-    for (int i = 0; i < SX; i++) {
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-            w[q] = ((v[4 * q] >> (8 * i)) & 0xFF) | (((v[4 * q + 1] >> (8 * i)) & 0xFF) << 8) |
-                   (((v[4 * q + 2] >> (8 * i)) & 0xFF) << 16) | (((v[4 * q + 3] >> (8 * i)) & 0xFF) << 24);
-        uint8_t* dst = Xt + ((((size_t)mt * KB + kb) * SX + i) * kBM) * kBK + swz_off(r, c16);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-    }
+    slice_item<SX, RT>(X, k, m, KB, ell, Xt, idx, flag, check);
 }
 
 // ---------------------------------------------------------------- tile Enc(W)
@@ -69,7 +30,8 @@ __global__ void k_slice_x(const uint32_t* __restrict__ X, uint32_t k, uint32_t m
 template <int BN>
 __global__ void __launch_bounds__(256) k_tile_encw(const uint32_t* __restrict__ canon, uint32_t m,
                                                    uint32_t ncol, uint32_t KB, uint8_t* __restrict__ Et) {
-    __shared__ uint32_t sE[kBK][BN + 1];
+    extern __shared__ uint32_t sE_raw[];
+    uint32_t (*sE)[BN + 1] = reinterpret_cast<uint32_t (*)[BN + 1]>(sE_raw);
     const uint32_t ct = blockIdx.x, kb = blockIdx.y;
     for (uint32_t idx = threadIdx.x; idx < kBK * BN; idx += blockDim.x) {
         const uint32_t b = idx / BN, c = idx % BN, beta = kb * kBK + b;
@@ -95,7 +57,8 @@ __global__ void __launch_bounds__(256) k_tile_encw(const uint32_t* __restrict__ 
 template <int BN>
 __global__ void __launch_bounds__(256) k_untile_encw(const uint8_t* __restrict__ Et, uint32_t m, uint32_t ncol,
                                                      uint32_t KB, uint32_t* __restrict__ canon) {
-    __shared__ uint32_t sE[kBK][BN + 1];
+    extern __shared__ uint32_t sE_raw[];
+    uint32_t (*sE)[BN + 1] = reinterpret_cast<uint32_t (*)[BN + 1]>(sE_raw);
     const uint32_t ct = blockIdx.x, kb = blockIdx.y;
     for (uint32_t idx = threadIdx.x; idx < kBK * BN; idx += blockDim.x) sE[idx / BN][idx % BN] = 0;
     __syncthreads();
@@ -114,17 +77,19 @@ __global__ void __launch_bounds__(256) k_untile_encw(const uint8_t* __restrict__
 }
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB,
+cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st) {
-    const uint32_t Mt = (k + kBM - 1) / kBM;
-    const uint32_t total = Mt * kBM * KB * 8;
+    const uint32_t Mt = (k + rt - 1) / rt;
+    const uint32_t total = Mt * rt * KB * 8;
     const uint32_t SX = sx_of(c->rns.ell);
     const int check = (c->prm.flags & NIMBUS_FLAG_CHECK_RANGE) && c->rns.ell < 32;
     dim3 g((total + 255) / 256);
     cudaError_t e;
-    if (SX == 1) e = launch_pdl(k_slice_x<1>, g, 256, 0, st, d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
-    else if (SX == 2) e = launch_pdl(k_slice_x<2>, g, 256, 0, st, d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
-    else e = launch_pdl(k_slice_x<4>, g, 256, 0, st, d_X, k, m, KB, c->rns.ell, d_Xt, total, c->d_flag, check);
+    const uint32_t ell = c->rns.ell;
+    if (rt == 64) e = launch_pdl(k_slice_x<4, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
+    else if (SX == 1) e = launch_pdl(k_slice_x<1, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
+    else if (SX == 2) e = launch_pdl(k_slice_x<2, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
+    else e = launch_pdl(k_slice_x<4, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
     c->launches++;
     return e;
 }
@@ -133,8 +98,17 @@ cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m,
                              uint8_t* d_Et, cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
     const dim3 g(col_tiles(c, bn), KB);
-    if (bn == kBNR) k_tile_encw<kBNR><<<g, 256, 0, st>>>(d_canon, m, ncol, KB, d_Et);
-    else k_tile_encw<kBNT><<<g, 256, 0, st>>>(d_canon, m, ncol, KB, d_Et);
+    const size_t smem = (size_t)kBK * (bn + 1) * 4;
+    cudaError_t e;
+    if (bn == kBNR) {
+        k_tile_encw<kBNR><<<g, 256, smem, st>>>(d_canon, m, ncol, KB, d_Et);
+    } else if (bn == kBNW) {
+        e = cudaFuncSetAttribute(k_tile_encw<kBNW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_tile_encw<kBNW><<<g, 256, smem, st>>>(d_canon, m, ncol, KB, d_Et);
+    } else {
+        k_tile_encw<kBNT><<<g, 256, smem, st>>>(d_canon, m, ncol, KB, d_Et);
+    }
     c->launches++;
     return cudaGetLastError();
 }
@@ -143,8 +117,17 @@ cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, u
                                uint32_t* d_canon, cudaStream_t st) {
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
     const dim3 g(col_tiles(c, bn), KB);
-    if (bn == kBNR) k_untile_encw<kBNR><<<g, 256, 0, st>>>(d_Et, m, ncol, KB, d_canon);
-    else k_untile_encw<kBNT><<<g, 256, 0, st>>>(d_Et, m, ncol, KB, d_canon);
+    const size_t smem = (size_t)kBK * (bn + 1) * 4;
+    cudaError_t e;
+    if (bn == kBNR) {
+        k_untile_encw<kBNR><<<g, 256, smem, st>>>(d_Et, m, ncol, KB, d_canon);
+    } else if (bn == kBNW) {
+        e = cudaFuncSetAttribute(k_untile_encw<kBNW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_untile_encw<kBNW><<<g, 256, smem, st>>>(d_Et, m, ncol, KB, d_canon);
+    } else {
+        k_untile_encw<kBNT><<<g, 256, smem, st>>>(d_Et, m, ncol, KB, d_canon);
+    }
     c->launches++;
     return cudaGetLastError();
 }

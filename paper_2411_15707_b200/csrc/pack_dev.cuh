@@ -1,0 +1,138 @@
+// pack_dev.cuh -- device code of K7 (RShift packing + mod-switch + mask), shared
+// by the stand-alone pack kernel (pack.cu) and the fused single-kernel path
+// (cop_tc.cu).  See pack.cu for the math and the citations.
+#pragma once
+#include "internal.h"
+
+namespace nimbus {
+
+// Emb_{Q}(w) mod p with 32-bit Shoup multiplication:
+// (t/2 - f) * t^-1 mod p,  f = (Q w + t/2) mod t,  |t/2 - f| <= t/2 < 2p.
+__device__ __forceinline__ uint32_t emb_fast(uint32_t w, uint32_t qmodt, uint32_t ell, uint32_t p, uint32_t tinv,
+                                             uint32_t tinv_sh) {
+    const uint64_t t = 1ULL << ell;
+    const uint64_t f = ((uint64_t)qmodt * w + (t >> 1)) & (t - 1);
+    int64_t d = (int64_t)(t >> 1) - (int64_t)f;
+    if (d < 0) d += p;
+    if (d < 0) d += p;
+    if (d >= (int64_t)p) d -= p;
+    return mulmod_shoup((uint32_t)d, tinv, tinv_sh, p);
+}
+
+template <int V>
+struct VecU32;
+template <>
+struct VecU32<1> {
+    __device__ static void load(const uint32_t* p, uint32_t (&v)[1]) { v[0] = __ldg(p); }
+    __device__ static void load_cg(const uint32_t* p, uint32_t (&v)[1]) { v[0] = __ldcg(p); }
+    __device__ static void store(uint32_t* p, const uint32_t (&v)[1]) { p[0] = v[0]; }
+};
+template <>
+struct VecU32<4> {
+    __device__ static void load(const uint32_t* p, uint32_t (&v)[4]) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+    __device__ static void load_cg(const uint32_t* p, uint32_t (&v)[4]) {
+        const uint4 x = __ldcg(reinterpret_cast<const uint4*>(p));
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+    __device__ static void store(uint32_t* p, const uint32_t (&v)[4]) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+};
+
+// One work item of K7: coefficients J..J+V-1 of component `comp` of packed
+// ciphertext tg (all limbs).  Used by k_pack and by the fused single-kernel path
+// (COHERENT: C was written by other CTAs of the same kernel -> L2-coherent loads).
+template <int V, int L, bool COHERENT = false>
+__device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
+                                          uint32_t Rr, uint32_t nct, uint64_t key_mask, uint32_t* __restrict__ cts,
+                                          uint32_t* __restrict__ Rout, uint32_t tg, uint32_t comp, uint32_t J) {
+    constexpr int RB = 8;  // rows of loads in flight per batch
+    const uint32_t N = Rn.N, Lo = Rn.L_out;
+    const uint32_t query = tg / nct, theta = tg - query * nct;
+    const uint32_t rows = min(Rr, kq - theta * Rr);
+    const size_t ncol = (size_t)2 * L * N;
+    const size_t row0 = (size_t)query * kq + (size_t)theta * Rr;
+    const uint32_t* Cq = C + row0 * ncol + (size_t)comp * L * N;
+
+    uint64_t acc[L][V];
+#pragma unroll
+    for (int i = 0; i < L; i++)
+#pragma unroll
+        for (int u = 0; u < V; u++) acc[i][u] = 0;
+#pragma unroll 1
+    for (uint32_t r0 = 0; r0 < rows; r0 += RB) {
+        uint32_t v[RB][L][V];
+        bool wrap[RB];
+#pragma unroll
+        for (int b = 0; b < RB; b++) {
+            const uint32_t r = r0 + b, s = r * n;
+            wrap[b] = J < s;
+            const uint32_t idx = wrap[b] ? J + N - s : J - s;
+#pragma unroll
+            for (int i = 0; i < L; i++) {
+                if (r < rows) {
+                    if (COHERENT) VecU32<V>::load_cg(Cq + r * ncol + (size_t)i * N + idx, v[b][i]);
+                    else VecU32<V>::load(Cq + r * ncol + (size_t)i * N + idx, v[b][i]);
+                }
+                else {
+#pragma unroll
+                    for (int u = 0; u < V; u++) v[b][i][u] = 0;
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < RB; b++) {
+            if (r0 + b < rows) {
+#pragma unroll
+                for (int i = 0; i < L; i++)
+#pragma unroll
+                    for (int u = 0; u < V; u++) acc[i][u] += wrap[b] ? Rn.p[i] - v[b][i][u] : v[b][i][u];
+            }
+        }
+    }
+    uint32_t rmask[V];
+    if (comp == 0) {
+        const uint64_t i0 = (uint64_t)tg * N + J;
+#pragma unroll
+        for (int u = 0; u < V; u++) rmask[u] = samp_mod_t(prg_word(key_mask, i0 + u), Rn.ell);
+    }
+    uint32_t out[L][V];
+#pragma unroll
+    for (int u = 0; u < V; u++) {
+        uint32_t res[L];
+#pragma unroll
+        for (int i = 0; i < L; i++) res[i] = reduce64_pm(acc[i][u], Rn.p[i], Rn.c32[i]);
+#pragma unroll
+        for (int l = L - 1; l >= 1; l--) {
+            if ((uint32_t)l >= Lo) {
+                const uint32_t pl = Rn.p[l], c = res[l];
+                const bool neg = c > (pl >> 1);          // centered rho = c - p_l < 0
+                const uint32_t mag = neg ? pl - c : c;   // |rho| < p_l / 2 < p_i
+#pragma unroll
+                for (int i = 0; i < l; i++) {
+                    const uint32_t p = Rn.p[i];
+                    const uint32_t d = neg ? addmod(res[i], mag, p) : submod(res[i], mag, p);
+                    res[i] = mulmod_shoup(d, Rn.inv_p[l][i], Rn.inv_p_sh[l][i], p);
+                }
+            }
+        }
+        if (comp == 0) {
+#pragma unroll
+            for (int i = 0; i < L; i++)
+                if ((uint32_t)i < Lo)
+                    res[i] = submod(res[i], emb_fast(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
+                                                     Rn.t_inv_sh[i]), Rn.p[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < L; i++) out[i][u] = res[i];
+    }
+#pragma unroll
+    for (int i = 0; i < L; i++)
+        if ((uint32_t)i < Lo) VecU32<V>::store(cts + (((size_t)tg * 2 + comp) * Lo + i) * N + J, out[i]);
+    if (comp == 0 && J < rows * n) VecU32<V>::store(Rout + row0 * n + J, rmask);
+}
+
+}  // namespace nimbus
