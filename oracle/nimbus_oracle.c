@@ -180,8 +180,11 @@ void orc_keygen(uint32_t N, uint64_t seed, int8_t* s) {
 /* Emb_q(w) = floor((q*w + t/2) / t)  (reduces to the
  * Delta*w of an exact q/t when t | q). */
 static u128 emb(u128 q, uint64_t w, uint32_t ell) {
+    /* floor((q w + t/2) / t) evaluated without forming q w (which exceeds
+     * 128 bits for 4 limbs): q = a t + b  =>  a w + floor((b w + t/2) / t). */
     u128 t = (u128)1 << ell;
-    return (q * w + t / 2) / t;
+    u128 a = q >> ell, b = q & (t - 1);
+    return a * w + (b * w + t / 2) / t;
 }
 
 /* Encrypt the row-wise encoded weight rows (Alg. 1 step 1, PAPER.md:663;

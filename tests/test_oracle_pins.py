@@ -188,7 +188,8 @@ def test_embedding(oracle):
     and the defining inequality |t Emb - q w| <= t/2 via CRT of the residues."""
     for w, want in KAT["emb_N4096_l16"].items():
         assert list(oracle.emb(np.array(P4096, np.uint32), 16, int(w))) == want
-    for pr, ell in ((P4096, 16), (P8192, 32), (P8192, 16)):
+    P8192_4 = [int(v) for v in oracle.primes(8192, 4)]      # 4 limbs: q w exceeds 128 bits
+    for pr, ell in ((P4096, 16), (P8192, 32), (P8192, 16), (P8192_4, 16), (P8192_4, 32)):
         q = 1
         for p in pr:
             q *= p
