@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-stage-profile", action="store_true", help="no per-stage events inside the step")
+    ap.add_argument("--l2", default="rotate", choices=["rotate", "write"],
+                    help="cold-L2 method: rotate through input copies totalling >= 3x L2 (default), "
+                         "or write a 512 MiB buffer before every timed step")
     return ap.parse_args()
 
 
@@ -178,39 +181,62 @@ def run_gpu(args, cfg, rank, world, local_rank):
         encw = nb.nimbus_encrypt_weights(ctx, sk, W, seed)
         torch.cuda.synchronize()
         t_setup += time.perf_counter() - t0
-        del W
         enc_bytes += nb.nimbus_encw_bytes(encw)
         # per-rank independent queries (weak scaling): X seeded by rank
         xseed = rank_x_seed(seed, rank)
         X = nb.from_numpy_u32(ni.gen_X(xseed, lay.k, lay.m, cfg.ell), dev)
         cts, R = nb.alloc_outputs(ctx, encw, lay.k_per_query, lay.n_queries)
-        mats.append(dict(lay=lay, seed=seed, encw=encw, X=X, cts=cts, R=R,
+        mats.append(dict(lay=lay, seed=seed, encw=[encw], X=[X], W=W, cts=cts, R=R,
                          ws_bytes=nb.nimbus_cop_workspace_size(ctx, encw, lay.k)))
+    # cold L2 without a flush write (whose dirty lines would be written back during
+    # the next step): rotate through copies of every input whose total is >= 3x L2,
+    # so each step reads Enc(W) and X that were evicted by the steps in between
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    n_copies = 1
+    if args.l2 == "rotate":
+        n_copies = max(1, -(-3 * l2_bytes // enc_bytes))
+        for mt in mats:
+            lay = mt["lay"]
+            for _ in range(n_copies - 1):
+                mt["encw"].append(nb.nimbus_encrypt_weights(ctx, sk, mt["W"], mt["seed"]))
+                mt["X"].append(mt["X"][0].clone())
+    for mt in mats:
+        del mt["W"]
+    torch.cuda.synchronize()
     # one workspace shared by every matmul of the step (they run in stream order)
     ws = torch.empty(max(mt["ws_bytes"] for mt in mats), dtype=torch.uint8, device=dev)
     for mt in mats:
         mt["ws"] = ws
     # multi-matmul steps (C5) go through the batched call: the pack of matmul i
     # overlaps the contraction of matmul i+1 on the library's side stream
-    jobs = [dict(encw=mt["encw"], X=mt["X"], k_per_query=mt["lay"].k_per_query, n_queries=mt["lay"].n_queries,
-                 mask_seed=mt["seed"], cts=mt["cts"], R=mt["R"]) for mt in mats]
+    jobs = [[dict(encw=mt["encw"][c], X=mt["X"][c], k_per_query=mt["lay"].k_per_query,
+                  n_queries=mt["lay"].n_queries, mask_seed=mt["seed"], cts=mt["cts"], R=mt["R"]) for mt in mats]
+            for c in range(n_copies)]
     ws_batch = None
     if len(mats) > 1:
-        ws_batch = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs), dtype=torch.uint8, device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+        ws_batch = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs[0]), dtype=torch.uint8, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES if args.l2 == "write" else 64 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    step_no = [0]
+
+    def cold():
+        """Between timed steps: next input copy (rotate) or an L2 flush write."""
+        if args.l2 == "write":
+            flush.zero_()
+        step_no[0] += 1
 
     def step():
+        c = step_no[0] % n_copies
         if ws_batch is not None:
-            nb.nimbus_cop_matmul_batch(ctx, jobs, ws_batch)
+            nb.nimbus_cop_matmul_batch(ctx, jobs[c], ws_batch)
             return
         for mt in mats:
             lay = mt["lay"]
-            nb.nimbus_cop_matmul(ctx, mt["encw"], mt["X"], lay.k_per_query, lay.n_queries, mt["seed"],
+            nb.nimbus_cop_matmul(ctx, mt["encw"][c], mt["X"][c], lay.k_per_query, lay.n_queries, mt["seed"],
                                  mt["cts"], mt["R"], mt["ws"])
 
-    for _ in range(args.warmup):
-        flush.zero_()
+    for _ in range(max(args.warmup, n_copies)):
+        cold()
         step()
     torch.cuda.synchronize()
     # clock spin-up outside the workload (memory writes only)
@@ -218,6 +244,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     while time.time() - t0 < 0.3:
         flush.zero_()
     torch.cuda.synchronize()
+    if args.l2 == "rotate":      # leave the L2 holding other copies' inputs, as in steady state
+        for _ in range(n_copies):
+            cold()
+            step()
+        torch.cuda.synchronize()
 
     def timed(profile: bool):
         """K steps, each preceded (outside the timed window) by an L2 flush."""
@@ -230,7 +261,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             torch.distributed.barrier()
         torch.cuda.synchronize()
         for i in range(args.steps):
-            flush.zero_()                       # evict Enc(W) from L2 between timed steps
+            cold()                              # Enc(W), X of this step are not in L2
             starts[i].record(stream)
             step()
             ends[i].record(stream)
@@ -264,23 +295,25 @@ def run_gpu(args, cfg, rank, world, local_rank):
         hosts = []
         for mt in mats:
             lay = mt["lay"]
-            Xh = mt["X"].cpu().pin_memory()
-            ch, Rh = nb.alloc_outputs(ctx, mt["encw"], lay.k_per_query, lay.n_queries, pin=True, device="cpu")
+            Xh = mt["X"][0].cpu().pin_memory()
+            ch, Rh = nb.alloc_outputs(ctx, mt["encw"][0], lay.k_per_query, lay.n_queries, pin=True, device="cpu")
             hosts.append((Xh, ch, Rh))
         h2d = sum(h[0].numel() * 4 for h in hosts)
         d2h = sum(h[1].numel() * 4 + h[2].numel() * 4 for h in hosts)
 
         def step_host():
+            c = step_no[0] % n_copies
             for mt, (Xh, ch, Rh) in zip(mats, hosts):
                 lay = mt["lay"]
-                nb.nimbus_cop_matmul_host(ctx, mt["encw"], Xh, lay.k_per_query, lay.n_queries, mt["seed"],
+                nb.nimbus_cop_matmul_host(ctx, mt["encw"][c], Xh, lay.k_per_query, lay.n_queries, mt["seed"],
                                           ch, Rh, mt["ws"])
         for _ in range(max(3, args.warmup)):
+            cold()
             step_host()
         ke = max(3, min(args.steps, 50))
         e2e_ms = []
         for _ in range(ke):
-            flush.zero_()
+            cold()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             step_host()                      # synchronises the stream before returning
@@ -288,8 +321,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
         e2e_step = statistics.median(e2e_ms)
         e2e_step = max_over_ranks(e2e_step, world, dev)
         e2e = dict(step_ms=e2e_step, h2d=h2d, d2h=d2h)
+    l2_desc = (f"cold: {n_copies} rotating copies of Enc(W)+X ({n_copies * enc_bytes >> 20} MiB >= 3x the "
+               f"{l2_bytes >> 20} MiB L2), step i reads copy i mod {n_copies}" if args.l2 == "rotate" else
+               f"flushed by a {L2_FLUSH_BYTES >> 20} MiB write before every timed step")
     return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=stage_ms, calls=calls, launches=launches,
-                clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e)
+                clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e, l2_desc=l2_desc)
 
 
 # ----------------------------------------------------------------- CPU oracle
@@ -437,7 +473,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": workload_name(cfg), "config": cfg.name, "k": lays[0].k, "matmuls_per_step": len(lays),
-                   "impl": args.impl, "l2": f"flushed by a {L2_FLUSH_BYTES >> 20} MiB write before every timed step",
+                   "impl": args.impl, "l2": res["l2_desc"],
                    "enc_w_bytes_resident": res["enc_bytes"]},
         "roofline": prim,
         "roofline_other": alt,

@@ -1,6 +1,5 @@
-// pack_dev.cuh -- device code of K7 (RShift packing + mod-switch + mask), shared
-// by the stand-alone pack kernel (pack.cu) and the fused single-kernel path
-// (cop_tc.cu).  See pack.cu for the math and the citations.
+// pack_dev.cuh -- device code of K7 (RShift packing + mod-switch + mask), the
+// per-item body of k_pack (pack.cu).  See pack.cu for the math and the citations.
 #pragma once
 #include "internal.h"
 
@@ -24,7 +23,6 @@ struct VecU32;
 template <>
 struct VecU32<1> {
     __device__ static void load(const uint32_t* p, uint32_t (&v)[1]) { v[0] = __ldg(p); }
-    __device__ static void load_cg(const uint32_t* p, uint32_t (&v)[1]) { v[0] = __ldcg(p); }
     __device__ static void store(uint32_t* p, const uint32_t (&v)[1]) { p[0] = v[0]; }
 };
 template <>
@@ -33,19 +31,14 @@ struct VecU32<4> {
         const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
         v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
     }
-    __device__ static void load_cg(const uint32_t* p, uint32_t (&v)[4]) {
-        const uint4 x = __ldcg(reinterpret_cast<const uint4*>(p));
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    }
     __device__ static void store(uint32_t* p, const uint32_t (&v)[4]) {
         *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
     }
 };
 
 // One work item of K7: coefficients J..J+V-1 of component `comp` of packed
-// ciphertext tg (all limbs).  Used by k_pack and by the fused single-kernel path
-// (COHERENT: C was written by other CTAs of the same kernel -> L2-coherent loads).
-template <int V, int L, bool COHERENT = false>
+// ciphertext tg (all limbs).
+template <int V, int L>
 __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                           uint32_t Rr, uint32_t nct, uint64_t key_mask, uint32_t* __restrict__ cts,
                                           uint32_t* __restrict__ Rout, uint32_t tg, uint32_t comp, uint32_t J) {
@@ -74,10 +67,8 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
 #pragma unroll
             for (int i = 0; i < L; i++) {
                 if (r < rows) {
-                    if (COHERENT) VecU32<V>::load_cg(Cq + r * ncol + (size_t)i * N + idx, v[b][i]);
-                    else VecU32<V>::load(Cq + r * ncol + (size_t)i * N + idx, v[b][i]);
-                }
-                else {
+                    VecU32<V>::load(Cq + r * ncol + (size_t)i * N + idx, v[b][i]);
+                } else {
 #pragma unroll
                     for (int u = 0; u < V; u++) v[b][i][u] = 0;
                 }

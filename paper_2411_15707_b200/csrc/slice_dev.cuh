@@ -1,5 +1,5 @@
 // slice_dev.cuh -- device code of K4 (X -> 8-bit planes in the swizzled tcgen05
-// operand layout), shared by k_slice_x (layout.cu) and the fused kernel.
+// operand layout), the per-item body of k_slice_x (layout.cu).
 #pragma once
 #include "internal.h"
 

@@ -14,7 +14,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnimbus_cop.so")
+# NIMBUS_LIB selects an experiment build of the same library (e.g. libnimbus_cop_<variant>.so)
+LIB_PATH = os.path.join(_PKG, os.environ.get("NIMBUS_LIB", "libnimbus_cop.so"))
 
 STATUS = {0: "NIMBUS_OK", -1: "NIMBUS_EINVAL", -2: "NIMBUS_ESHAPE", -3: "NIMBUS_ERANGE",
           -4: "NIMBUS_ENOISE", -5: "NIMBUS_ECUDA", -6: "NIMBUS_ENOMEM", -8: "NIMBUS_EARCH"}

@@ -29,8 +29,16 @@ rflush = torch.ones(64 << 20, dtype=torch.int32, device="cuda")   # 256 MB read:
 MODE = os.environ.get("FLUSH", "write")
 for _ in range(3):
     nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
+others = []
+if MODE == "rotate":   # as bench --l2 rotate: other copies' inputs fill the L2 (clean lines)
+    Wd = nb.from_numpy_u32(ni.gen_W(1, m, n, ell), "cuda")
+    others = [(nb.nimbus_encrypt_weights(ctx, sk, Wd, 1), X.clone()) for _ in range(7)]
+    flush.zero_()
+    for wo, Xo in others:
+        nb.nimbus_cop_matmul(ctx, wo, Xo, k, 1, 3, cts, R, ws)
 lib.nimbus_trace_set(ctypes.c_void_p(tr.data_ptr()))
-flush.zero_()
+if MODE in ("write", "writeread"):
+    flush.zero_()
 if MODE == "writeread":
     rflush.sum()
 torch.cuda.synchronize()
@@ -50,6 +58,11 @@ for c in (0, 1, 2, 50, 100, 147):
             break
         s += f" t{ti}: mma {us(row[4+4*ti]):.1f}-{us(row[5+4*ti]):.1f} epi {us(row[6+4*ti]):.1f}-{us(row[7+4*ti]):.1f} |"
     print(s)
+if (t[:, 61] > 0).any():
+    for c in (0, 1, 100, 147):
+        row = t[c]
+        print(f"cta {c}: 3rd E copy issued {us(row[63]):.2f} first E landed {us(row[60]):.2f} "
+              f"X: past PDL wait {us(row[61]):.2f} rows written {us(row[62]):.2f}")
 for c in (0, 100):
     row = t[c]
     print(f"cta {c} tile1 producer B issue:", " ".join(f"{us(row[52+i]):.2f}" for i in range(8) if row[52+i] > 0))
