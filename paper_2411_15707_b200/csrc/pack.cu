@@ -18,7 +18,7 @@
 
 namespace nimbus {
 
-template <int V, int L>
+template <int V, int L, int RB>
 __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                               uint32_t Rr, uint32_t nct, uint64_t key_mask,
                                               uint32_t* __restrict__ cts, uint32_t* __restrict__ Rout) {
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict
     const uint32_t J = (blockIdx.x * blockDim.x + threadIdx.x) * V;
     if (J >= Rn.N) return;
     pdl_wait();  // C is produced by the contraction kernel
-    pack_item<V, L>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, blockIdx.y, blockIdx.z, J);
+    pack_item<V, L, RB>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, blockIdx.y, blockIdx.z, J);
 }
 
 template <typename K, typename... Args>
@@ -36,24 +36,49 @@ static cudaError_t launch_maybe_pdl(bool pdl, K kernel, dim3 grid, dim3 block, c
     return cudaGetLastError();
 }
 
-template <int V>
-static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                            uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
+template <int V, int RB>
+static cudaError_t launch_vr(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
+                             uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     const uint32_t per_block = 128 * V;
     dim3 grid((N + per_block - 1) / per_block, nq * nct, 2);
     const uint64_t key = prg_key(seed, 6);
     switch (c->rns.L) {
-        case 1: return launch_maybe_pdl(pdl, k_pack<V, 1>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 2: return launch_maybe_pdl(pdl, k_pack<V, 2>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 3: return launch_maybe_pdl(pdl, k_pack<V, 3>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        default: return launch_maybe_pdl(pdl, k_pack<V, 4>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 1: return launch_maybe_pdl(pdl, k_pack<V, 1, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 2: return launch_maybe_pdl(pdl, k_pack<V, 2, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 3: return launch_maybe_pdl(pdl, k_pack<V, 3, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        default: return launch_maybe_pdl(pdl, k_pack<V, 4, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+    }
+}
+
+// rows per load batch: R itself when R is 1, 2, 4 or 5 (or a multiple of 5), else a power of two
+static uint32_t rows_per_batch(uint32_t Rr, uint32_t kq) {
+    const uint32_t r = Rr < kq ? Rr : kq;         // rows of the fullest packed ciphertext
+    if (r <= 2) return r;
+    if (r <= 4) return 4;
+    if (r % 5 == 0) return 5;
+    return 8;
+}
+
+template <int V>
+static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
+                            uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
+    switch (rows_per_batch(c->rns.N / n, kq)) {
+        case 1: return launch_vr<V, 1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 2: return launch_vr<V, 2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 4: return launch_vr<V, 4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 5: return launch_vr<V, 5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        default: return launch_vr<V, 8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
     }
 }
 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                         uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
+    // 4 coefficients per thread when the RShift stride allows it and the grid stays
+    // at >= 8 blocks of 128 per SM: in the PDL chain the pack runs alone after the
+    // contraction and is latency-bound, so thread count beats per-thread efficiency
+    // (C2: V = 1 26.1 us/step vs V = 4 28.2; C3: V = 4)
     const uint64_t threads_v1 = 2ull * nq * nct * N;      // one thread per (comp, J)
     const bool vec = (n % 4 == 0) && threads_v1 / 4 >= 8ull * 128 * (uint64_t)c->num_sms;
     cudaError_t e = vec ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl)

@@ -18,6 +18,28 @@ __device__ __forceinline__ uint32_t emb_fast(uint32_t w, uint32_t qmodt, uint32_
     return mulmod_shoup((uint32_t)d, tinv, tinv_sh, p);
 }
 
+// Emb_{Q}(w) mod p for ell <= 16, all in 32 bits: Q w + t/2 < 2^32 when Q < t = 2^ell.
+__device__ __forceinline__ uint32_t emb_fast16(uint32_t w, uint32_t qmodt, uint32_t ell, uint32_t p, uint32_t tinv,
+                                               uint32_t tinv_sh) {
+    const uint32_t t = 1u << ell;
+    const uint32_t f = (qmodt * w + (t >> 1)) & (t - 1);
+    const uint32_t h = t >> 1;
+    const uint32_t d = h >= f ? h - f : p - (f - h);     // (t/2 - f) mod p, |t/2 - f| <= t/2 < p
+    return mulmod_shoup(d, tinv, tinv_sh, p);
+}
+
+// x mod p for a sum of at most 2^13 residues (x < 2^44, rows <= N <= 8192) when c32 = 2^32 mod p < 2^21:
+// three folds x = hi 2^32 + lo -> hi c32 + lo (< 3*2^32, < 2^32 + 2^22, < 2^32),
+// then two conditional subtractions (2^32 < 3p).
+__device__ __forceinline__ uint32_t reduce44_pm(uint64_t x, uint32_t p, uint32_t c32) {
+#pragma unroll
+    for (int f = 0; f < 3; f++) x = mad_wide((uint32_t)(x >> 32), c32, (uint32_t)x);
+    uint32_t r = (uint32_t)x;
+    r = r >= p ? r - p : r;
+    r = r >= p ? r - p : r;
+    return r;
+}
+
 template <int V>
 struct VecU32;
 template <>
@@ -37,18 +59,19 @@ struct VecU32<4> {
 };
 
 // One work item of K7: coefficients J..J+V-1 of component `comp` of packed
-// ciphertext tg (all limbs).
-template <int V, int L>
+// ciphertext tg (all limbs).  RB rows of loads are in flight per batch; the host
+// picks RB to fit R = floor(N/n) (1 for C3, 5 for C2, ...) so that few load slots
+// are predicated off -- the kernel is issue-bound, not bandwidth-bound.
+template <int V, int L, int RB>
 __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                           uint32_t Rr, uint32_t nct, uint64_t key_mask, uint32_t* __restrict__ cts,
                                           uint32_t* __restrict__ Rout, uint32_t tg, uint32_t comp, uint32_t J) {
-    constexpr int RB = 8;  // rows of loads in flight per batch
     const uint32_t N = Rn.N, Lo = Rn.L_out;
     const uint32_t query = tg / nct, theta = tg - query * nct;
     const uint32_t rows = min(Rr, kq - theta * Rr);
-    const size_t ncol = (size_t)2 * L * N;
+    const uint32_t ncol = 2u * L * N;          // row offsets below stay in 32 bits (rows * ncol < 2^30)
     const size_t row0 = (size_t)query * kq + (size_t)theta * Rr;
-    const uint32_t* Cq = C + row0 * ncol + (size_t)comp * L * N;
+    const uint32_t* Cq = C + row0 * ncol + comp * L * N;
 
     uint64_t acc[L][V];
 #pragma unroll
@@ -67,7 +90,7 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
 #pragma unroll
             for (int i = 0; i < L; i++) {
                 if (r < rows) {
-                    VecU32<V>::load(Cq + r * ncol + (size_t)i * N + idx, v[b][i]);
+                    VecU32<V>::load(Cq + (r * ncol + i * N + idx), v[b][i]);
                 } else {
 #pragma unroll
                     for (int u = 0; u < V; u++) v[b][i][u] = 0;
@@ -86,16 +109,21 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
     }
     uint32_t rmask[V];
     if (comp == 0) {
-        const uint64_t i0 = (uint64_t)tg * N + J;
+        // word(seed, 6, i) = mix64(key + golden (i + 1)) for i = tg N + J + u: one multiply, then steps
+        uint64_t z = key_mask + 0x9E3779B97F4A7C15ULL * ((uint64_t)tg * N + J + 1);
 #pragma unroll
-        for (int u = 0; u < V; u++) rmask[u] = samp_mod_t(prg_word(key_mask, i0 + u), Rn.ell);
+        for (int u = 0; u < V; u++, z += 0x9E3779B97F4A7C15ULL) rmask[u] = samp_mod_t(mix64(z), Rn.ell);
     }
     uint32_t out[L][V];
 #pragma unroll
     for (int u = 0; u < V; u++) {
         uint32_t res[L];
 #pragma unroll
-        for (int i = 0; i < L; i++) res[i] = reduce64_pm(acc[i][u], Rn.p[i], Rn.c32[i]);
+        for (int i = 0; i < L; i++) {
+            // RB == 1: a single unwrapped row (R = 1), already a residue
+            if (RB == 1) res[i] = (uint32_t)acc[i][u];
+            else res[i] = reduce44_pm(acc[i][u], Rn.p[i], Rn.c32[i]);
+        }
 #pragma unroll
         for (int l = L - 1; l >= 1; l--) {
             if ((uint32_t)l >= Lo) {
@@ -114,8 +142,11 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
 #pragma unroll
             for (int i = 0; i < L; i++)
                 if ((uint32_t)i < Lo)
-                    res[i] = submod(res[i], emb_fast(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
-                                                     Rn.t_inv_sh[i]), Rn.p[i]);
+                    res[i] = submod(res[i], Rn.ell <= 16
+                                                ? emb_fast16(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
+                                                             Rn.t_inv_sh[i])
+                                                : emb_fast(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
+                                                           Rn.t_inv_sh[i]), Rn.p[i]);
         }
 #pragma unroll
         for (int i = 0; i < L; i++) out[i][u] = res[i];

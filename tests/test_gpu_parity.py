@@ -203,6 +203,8 @@ E2E = [
     ("res_L3_v4", 8192, 3, 16, 1, 768, 1024, 128, 1, 0),
     ("res_L4_v4", 8192, 4, 16, 2, 200, 2048, 128, 1, 0),
     ("res_small_grid", 1024, 2, 16, 1, 130, 96, 100, 1, 0),
+    # n = 1: R = N rows per packed ciphertext (the largest lazy sum in the pack)
+    ("n_one", 1024, 2, 16, 1, 50, 1, 1031, 1, 0),
 ]
 
 
