@@ -61,6 +61,7 @@ typedef struct {
 typedef struct nimbus_ctx nimbus_ctx;
 typedef struct nimbus_sk nimbus_sk;
 typedef struct nimbus_encw nimbus_encw;
+typedef struct nimbus_plainw nimbus_plainw;
 
 /* Context: validates params, derives the primes (the L largest p < 2^31 with
  * p = 1 mod 2N), uploads NTT twiddles and RNS constants to
@@ -179,6 +180,36 @@ nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t k_p
 nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts,
                              uint32_t k_per_query, uint32_t n_queries, uint32_t n, uint32_t* d_Z,
                              uint32_t* d_M, void* stream);
+
+/* ------------------------------------------------------ server, step 5 --- */
+/* Alg. 1 step 5: the server computes W<X>_s locally and outputs
+ * <Y>_s = W<X>_s + (W<X>_c - R), the second term being its decryption of the
+ * client's masked ciphertexts; the client's share is <Y>_c = R.  Orientation
+ * Y = X.W.  Plaintext products are exact mod t = 2^ell
+ * (int8 slices on the tensor cores, the same slicing as the contraction).
+ *
+ * Server plaintext weights in the tensor-core layout (the server owns W).
+ *  d_W  m x n uint32 row-major; entries are taken mod 2^(8 S_x) >= t, so the
+ *       products are exact mod t for any input. */
+nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_t m, uint32_t n,
+                                   void* stream, nimbus_plainw** out);
+void nimbus_plainw_destroy(nimbus_plainw* w);
+/* Workspace bytes for nimbus_plain_matmul (n_queries = 0) or nimbus_server_output
+ * with k = k_per_query * n_queries rows. */
+nimbus_status nimbus_server_workspace_size(const nimbus_ctx* ctx, const nimbus_plainw* w,
+                                           uint32_t k_per_query, uint32_t n_queries, size_t* bytes);
+/* d_Y = (d_X . W + d_add) mod t.  d_X k x m uint32, d_add k x n uint32 or NULL,
+ * d_Y k x n uint32 (may alias d_add). */
+nimbus_status nimbus_plain_matmul(nimbus_ctx* ctx, const nimbus_plainw* w, const uint32_t* d_X, uint32_t k,
+                                  const uint32_t* d_add, uint32_t* d_Y, void* d_ws, size_t ws_bytes,
+                                  void* stream);
+/* d_Ys = (d_Xs . W + unpack(Dec(d_cts))) mod t, k = k_per_query * n_queries rows of
+ * n = w's n columns; d_cts as written by nimbus_cop_matmul for the same n.
+ * Decryption as nimbus_decrypt (L_out limbs, NTT, exact rounding). */
+nimbus_status nimbus_server_output(nimbus_ctx* ctx, const nimbus_sk* sk, const nimbus_plainw* w,
+                                   const uint32_t* d_Xs, const uint32_t* d_cts, uint32_t k_per_query,
+                                   uint32_t n_queries, uint32_t* d_Ys, void* d_ws, size_t ws_bytes,
+                                   void* stream);
 
 /* ---------------------------------------------------------- test helpers --- */
 /* PRG words word(seed, dom, start + i), i < count. */

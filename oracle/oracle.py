@@ -3,7 +3,9 @@
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
 bench.py's cpu_baseline / --impl reference leg.  Never imported by the product
 package paper_2411_15707_b200/.  Numpy in, numpy out; all arithmetic happens
-in the C file, whose functions cite the paper passages they implement.
+in the C file, whose functions cite the paper passages they implement -- except
+the server's plaintext product X.W mod 2^ell (plain_matmul), a textbook numpy
+integer matmul.
 """
 from __future__ import annotations
 
@@ -196,6 +198,23 @@ def decrypt_unpack(N, L_out, pr, ell, s, cts, kq, n_queries, n, want_full=False)
                              full.ctypes.data_as(C.c_void_p) if full is not None else None,
                              C.byref(tv))
     return Z, full, tv.value
+
+
+def plain_matmul(X, W, ell) -> np.ndarray:
+    """X.W mod 2^ell (Alg. 1 step 5's W<X>_s; orientation SURVEY.md
+    §8(c) #10): the textbook product in uint64 -- exact mod 2^64, hence mod 2^ell
+    for ell <= 32 -- then reduced mod t."""
+    t_mask = np.uint64((1 << ell) - 1)
+    Y = _u32(X).astype(np.uint64) @ _u32(W).astype(np.uint64)
+    return (Y & t_mask).astype(np.uint32)
+
+
+def server_output(N, L_out, pr, ell, s, cts, Xs, W, kq, n_queries):
+    """Alg. 1 step 5: <Y>_s = W<X>_s + (W<X>_c - R) mod 2^ell, the
+    second term being the server's decryption + unpack of the client's ciphertexts."""
+    Z, _, _ = decrypt_unpack(N, L_out, pr, ell, s, cts, kq, n_queries, _u32(W).shape[1])
+    t_mask = np.uint64((1 << ell) - 1)
+    return ((plain_matmul(Xs, W, ell).astype(np.uint64) + Z.astype(np.uint64)) & t_mask).astype(np.uint32)
 
 
 def emb(pr, ell, w) -> np.ndarray:

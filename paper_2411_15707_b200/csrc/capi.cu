@@ -546,6 +546,92 @@ nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_
     return NIMBUS_OK;
 }
 
+// ---------------------------------------------------------------- server, step 5
+nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_t m, uint32_t n, void* stream,
+                                   nimbus_plainw** out) {
+    if (!ctx || !d_W || !out || m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    nimbus_plainw* w = new (std::nothrow) nimbus_plainw();
+    if (!w) return set_err(ctx, NIMBUS_ENOMEM, "host alloc");
+    w->ctx = ctx;
+    w->m = m;
+    w->n = n;
+    w->KB = (m + kBK - 1) / kBK;
+    w->bytes = (size_t)plain_col_tiles(n) * w->KB * sx_of(ctx->rns.ell) * 64 * kBK;
+    cudaError_t e = cudaMalloc(&w->d_Wt, w->bytes);
+    if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "plain weights alloc"); }
+    e = launch_tile_plainw(ctx, d_W, m, n, w->KB, w->d_Wt, (cudaStream_t)stream);
+    if (e != cudaSuccess) { cudaFree(w->d_Wt); delete w; return cuda_err(ctx, e, "tile plain weights"); }
+    *out = w;
+    return NIMBUS_OK;
+}
+
+void nimbus_plainw_destroy(nimbus_plainw* w) {
+    if (!w) return;
+    if (w->d_Wt) cudaFree(w->d_Wt);
+    delete w;
+}
+
+struct ServerWs {
+    size_t xt = 0, z = 0, u = 0, total = 0;
+};
+static ServerWs server_ws(const nimbus_ctx* ctx, const nimbus_plainw* w, uint32_t kq, uint32_t nq) {
+    auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+    ServerWs L;
+    const size_t k = (size_t)kq * (nq ? nq : 1);
+    const size_t Mt = (k + kBM - 1) / kBM;
+    L.xt = 0;
+    L.z = al(sx_of(ctx->rns.ell) * Mt * kBM * (size_t)w->KB * kBK);
+    L.u = L.z + (nq ? al(k * w->n * 4) : 0);
+    size_t ubytes = 0;
+    if (nq) {
+        const uint32_t R = ctx->rns.N / w->n, nct = (kq + R - 1) / R;
+        ubytes = al((size_t)nq * nct * ctx->rns.L_out * ctx->rns.N * 4);
+    }
+    L.total = L.u + ubytes;
+    return L;
+}
+
+nimbus_status nimbus_server_workspace_size(const nimbus_ctx* ctx, const nimbus_plainw* w, uint32_t kq, uint32_t nq,
+                                           size_t* bytes) {
+    if (!ctx || !w || !bytes || kq == 0) return NIMBUS_EINVAL;
+    if (nq && w->n > ctx->rns.N) return NIMBUS_ESHAPE;
+    *bytes = server_ws(ctx, w, kq, nq).total;
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_plain_matmul(nimbus_ctx* ctx, const nimbus_plainw* w, const uint32_t* d_X, uint32_t k,
+                                  const uint32_t* d_add, uint32_t* d_Y, void* d_ws, size_t ws_bytes, void* stream) {
+    if (!ctx || !w || w->ctx != ctx || !d_X || !d_Y || !d_ws || k == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (k > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
+    const ServerWs L = server_ws(ctx, w, k, 0);
+    if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* xt = (uint8_t*)d_ws + L.xt;
+    CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, kBM, xt, s), "slice X");
+    CK(launch_plain_matmul(ctx, xt, w->d_Wt, k, w->n, w->KB, d_add, d_Y, s), "plain matmul");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_server_output(nimbus_ctx* ctx, const nimbus_sk* sk, const nimbus_plainw* w,
+                                   const uint32_t* d_Xs, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
+                                   uint32_t* d_Ys, void* d_ws, size_t ws_bytes, void* stream) {
+    if (!ctx || !sk || !w || w->ctx != ctx || !d_Xs || !d_cts || !d_Ys || !d_ws || kq == 0 || nq == 0)
+        return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (w->n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
+    if ((uint64_t)kq * nq > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
+    const ServerWs L = server_ws(ctx, w, kq, nq);
+    if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t k = kq * nq, R = ctx->rns.N / w->n, nct = (kq + R - 1) / R;
+    uint8_t* ws = (uint8_t*)d_ws;
+    uint32_t* Z = reinterpret_cast<uint32_t*>(ws + L.z);
+    uint32_t* U = reinterpret_cast<uint32_t*>(ws + L.u);
+    CK(launch_decrypt(ctx, sk->d_s_ntt, d_cts, nq * nct, nct, kq, w->n, U, Z, nullptr, s), "decrypt");
+    CK(launch_slice_x(ctx, d_Xs, k, w->m, w->KB, kBM, ws + L.xt, s), "slice X_s");
+    CK(launch_plain_matmul(ctx, ws + L.xt, w->d_Wt, k, w->n, w->KB, Z, d_Ys, s), "plain matmul");
+    return NIMBUS_OK;
+}
+
 nimbus_status nimbus_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* d_out,
                                void* stream) {
     if (!d_out) return NIMBUS_EINVAL;

@@ -56,6 +56,13 @@ struct nimbus_encw {
     size_t bytes = 0;
 };
 
+struct nimbus_plainw {
+    nimbus_ctx* ctx = nullptr;
+    uint32_t m = 0, n = 0, KB = 0;
+    uint8_t* d_Wt = nullptr;       // S_x byte planes [ct][kb][j][64][128 swizzled] (plain.cu)
+    size_t bytes = 0;
+};
+
 // number of 8-bit slices of an ell-bit X entry (S_x)
 inline uint32_t sx_of(uint32_t ell) { return ell <= 8 ? 1 : ell <= 16 ? 2 : 4; }
 // number of 48-column Enc(W) tiles covering the 2 L N coefficient columns (last one zero padded)
@@ -87,6 +94,12 @@ cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_
 // cop_cc.cu
 cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                 uint32_t* d_C, cudaStream_t st);
+// plain.cu (server step 5)
+uint32_t plain_col_tiles(uint32_t n);
+cudaError_t launch_tile_plainw(nimbus_ctx* c, const uint32_t* d_W, uint32_t m, uint32_t n, uint32_t KB,
+                               uint8_t* d_Wt, cudaStream_t st);
+cudaError_t launch_plain_matmul(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_t* d_Wt, uint32_t k, uint32_t n,
+                                uint32_t KB, const uint32_t* d_add, uint32_t* d_Y, cudaStream_t st);
 // cop_tc.cu
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st);

@@ -64,6 +64,11 @@ _SIGS = {
     "nimbus_cop_matmul_batch": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_profile_enable": (C.c_int, [_vp, C.c_int]),
     "nimbus_profile_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(_u64), C.c_int]),
+    "nimbus_plain_weights": (C.c_int, [_vp, _vp, _u32, _u32, _vp, C.POINTER(_vp)]),
+    "nimbus_plainw_destroy": (None, [_vp]),
+    "nimbus_server_workspace_size": (C.c_int, [_vp, _vp, _u32, _u32, C.POINTER(_sz)]),
+    "nimbus_plain_matmul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_server_output": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _sz, _vp]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -151,6 +156,14 @@ class SecretKey(_Handle):
 
 class EncW(_Handle):
     _destroy = "nimbus_encw_destroy"
+
+    def __init__(self, ptr, ctx, m, n):
+        super().__init__(ptr, ctx)
+        self.m, self.n = m, n
+
+
+class PlainW(_Handle):
+    _destroy = "nimbus_plainw_destroy"
 
     def __init__(self, ptr, ctx, m, n):
         super().__init__(ptr, ctx)
@@ -359,6 +372,47 @@ def nimbus_profile_read(ctx: Context, reset: bool = True):
     calls = _u64()
     _check(lib().nimbus_profile_read(ctx.ptr, ms, C.byref(calls), int(reset)), ctx)
     return [float(x) for x in ms], int(calls.value)
+
+
+# ------------------------------------------------------------------ server, Alg. 1 step 5
+def nimbus_plain_weights(ctx: Context, W: torch.Tensor, stream=None) -> PlainW:
+    m, n = W.shape
+    out = C.c_void_p()
+    _check(lib().nimbus_plain_weights(ctx.ptr, _ptr(W, torch.int32, "W"), m, n, _stream(stream), C.byref(out)), ctx)
+    return PlainW(out, ctx, m, n)
+
+
+def nimbus_server_workspace_size(ctx: Context, w: PlainW, k_per_query: int, n_queries: int) -> int:
+    out = _sz()
+    _check(lib().nimbus_server_workspace_size(ctx.ptr, w.ptr, k_per_query, n_queries, C.byref(out)), ctx)
+    return int(out.value)
+
+
+def nimbus_plain_matmul(ctx: Context, w: PlainW, X: torch.Tensor, add: torch.Tensor = None, Y=None, ws=None,
+                        stream=None) -> torch.Tensor:
+    k = X.shape[0]
+    if Y is None:
+        Y = torch.empty((k, w.n), dtype=torch.int32, device=X.device)
+    if ws is None:
+        ws = torch.empty(nimbus_server_workspace_size(ctx, w, k, 0), dtype=torch.uint8, device=X.device)
+    _check(lib().nimbus_plain_matmul(ctx.ptr, w.ptr, _ptr(X, torch.int32, "X"), k,
+                                     _ptr(add, torch.int32, "add") if add is not None else None,
+                                     _ptr(Y, torch.int32, "Y"), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return Y
+
+
+def nimbus_server_output(ctx: Context, sk: SecretKey, w: PlainW, Xs: torch.Tensor, cts: torch.Tensor,
+                         k_per_query: int, n_queries: int, Ys=None, ws=None, stream=None) -> torch.Tensor:
+    k = k_per_query * n_queries
+    if Ys is None:
+        Ys = torch.empty((k, w.n), dtype=torch.int32, device=Xs.device)
+    if ws is None:
+        ws = torch.empty(nimbus_server_workspace_size(ctx, w, k_per_query, n_queries), dtype=torch.uint8,
+                         device=Xs.device)
+    _check(lib().nimbus_server_output(ctx.ptr, sk.ptr, w.ptr, _ptr(Xs, torch.int32, "Xs"),
+                                      _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
+                                      _ptr(Ys, torch.int32, "Ys"), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return Ys
 
 
 # ------------------------------------------------------------------ helpers

@@ -364,3 +364,45 @@ def test_kernel_variants_parity(nb, oracle, monkeypatch, env, N, L, ell, L_out, 
     cts, R = c.run()
     cts_o, R_o = c.oracle_out()
     assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+
+
+# ------------------------------------------------------------------ server, Alg. 1 step 5
+@pytest.mark.parametrize("ell", [8, 12, 16, 32])
+@pytest.mark.parametrize("k,m,n", [(1, 1, 1), (200, 300, 100), (128, 768, 768), (130, 129, 65)])
+def test_plain_matmul_parity(nb, oracle, ell, k, m, n):
+    """nimbus_plain_matmul (int8-sliced tcgen05 GEMM mod 2^ell) == oracle.plain_matmul,
+    bit for bit, with and without the added term; ragged k, m, n tails."""
+    N = 4096 if ell <= 16 else 8192
+    ctx = nb.nimbus_ctx_create(N, 2 if ell <= 16 else 3, ell, 1 if ell <= 16 else 2)
+    W = ni.gen_W(11 + m, m, n, ell)
+    X = ni.gen_X(12 + k, k, m, ell)
+    w = nb.nimbus_plain_weights(ctx, dev_u32(W))
+    Y = nb.nimbus_plain_matmul(ctx, w, dev_u32(X))
+    want = oracle.plain_matmul(X, W, ell)
+    assert (u32(Y) == want).all()
+    A = ni.gen_X(13, k, n, ell)
+    Y2 = nb.nimbus_plain_matmul(ctx, w, dev_u32(X), add=dev_u32(A))
+    t = np.uint64((1 << ell) - 1)
+    assert (u32(Y2) == ((want.astype(np.uint64) + A) & t)).all()
+
+
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [(4096, 2, 16, 1, 768, 768, 128, 1),
+                                                     (4096, 2, 16, 1, 200, 700, 23, 3),
+                                                     (8192, 3, 32, 2, 300, 768, 25, 2),
+                                                     (4096, 2, 16, 1, 768, 3072, 128, 1)])
+def test_server_output_parity_and_shares(nb, oracle, N, L, ell, L_out, m, n, kq, nq):
+    """Alg. 1 end to end on the GPU: client COP (nimbus_cop_matmul) + server step 5
+    (nimbus_server_output).  <Y>_s equals the oracle's bit for bit, and
+    <Y>_s + <Y>_c (= R) reconstructs X.W mod t for X = <X>_s + <X>_c."""
+    c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=4242 + m, oracle_full=False)
+    cts, R = c.run()
+    Xs = ni.gen_X(c.seed + 7, c.k, m, ell)
+    w = nb.nimbus_plain_weights(c.ctx, dev_u32(c.W))
+    Ys = nb.nimbus_server_output(c.ctx, c.sk, w, dev_u32(Xs), cts, kq, nq)
+    nb.nimbus_sync(c.ctx)
+    want = oracle.server_output(N, L_out, c.pr[:L_out], ell, c.s_oracle, u32(cts), Xs, c.W, kq, nq)
+    assert (u32(Ys) == want).all()
+    t = (1 << ell)
+    X = (c.X.astype(np.uint64) + Xs) % t
+    Y = matmul_mod_t(X, c.W, ell)
+    assert ((u32(Ys).astype(np.uint64) + u32(R)) % t == Y).all()

@@ -415,6 +415,44 @@ def test_e2e_identity_weights(oracle):
     assert (((Z.astype(np.uint64) + d["R"]) % (1 << ell)) == X).all()
 
 
+# ----------------------------------------------------------------- server, Alg. 1 step 5
+@pytest.mark.parametrize("ell", [4, 8, 12, 16, 32])
+def test_plain_matmul_bruteforce(oracle, ell):
+    """The server's W<X>_s mod 2^ell against Python integers, at
+    full-range entries (t-1 everywhere exercises every carry) and random ones."""
+    t = 1 << ell
+    for k, m, n, seed in ((3, 5, 4, 1), (7, 33, 9, 2)):
+        X = ni.gen_X(seed, k, m, ell)
+        W = ni.gen_W(seed, m, n, ell)
+        assert (oracle.plain_matmul(X, W, ell) == py_matmul_mod(X, W, t)).all()
+    X = np.full((2, 40), t - 1, np.uint32)
+    W = np.full((40, 3), t - 1, np.uint32)
+    assert (oracle.plain_matmul(X, W, ell) == py_matmul_mod(X, W, t)).all()
+
+
+@pytest.mark.parametrize("case", [
+    dict(N=64, pr=P4096, ell=16, L_out=1, k=12, m=16, n=20, nq=1),
+    dict(N=64, pr=P8192, ell=32, L_out=2, k=12, m=16, n=20, nq=2),
+    dict(N=128, pr=P8192, ell=16, L_out=1, k=9, m=30, n=128, nq=1),
+])
+def test_protocol_shares_reconstruct(oracle, case):
+    """Alg. 1 end to end: with X = <X>_s + <X>_c mod t, the
+    server's <Y>_s = W<X>_s + Dec(...) and the client's <Y>_c = R satisfy
+    <Y>_s + <Y>_c = X.W mod t (brute force with Python integers)."""
+    c = case
+    t = 1 << c["ell"]
+    seed = 0xABC + c["N"] + c["k"]
+    d = toy_pipeline(oracle, c["N"], c["pr"], c["ell"], c["L_out"], c["k"], c["m"], c["n"], seed, nq=c["nq"])
+    Xc = d["X"]
+    Xs = ni.gen_X(seed + 1, Xc.shape[0], c["m"], c["ell"])
+    Ys = oracle.server_output(c["N"], c["L_out"], np.array(c["pr"][:c["L_out"]], np.uint32), c["ell"], d["s"],
+                              d["cts"], Xs, d["W"], c["k"], c["nq"])
+    X = (Xc.astype(np.uint64) + Xs) % t
+    want = py_matmul_mod(X, d["W"], t)
+    assert ((Ys.astype(np.uint64) + d["R"]) % t == want).all()
+    assert not (Ys == want).all()          # the server's share alone is not the product
+
+
 def test_toy_known_answer_digests(oracle):
     """Survey's independent reading of the whole contract, toy shape."""
     toy = KAT["toy"]
