@@ -11,42 +11,89 @@
 
 namespace nimbus {
 
-// psi_rev[k] = psi^bitrev(k), k in [1, N) used by stage (m, i) as psi_rev[m + i]
+// psi_rev[k] = psi^bitrev(k), k in [1, N) used by stage (m, i) as psi_rev[m + i].
+// Two butterfly stages per pass (radix 4 in registers): a thread loads the four
+// elements a pair of consecutive stages couples, so a transform takes
+// ceil(log N / 2) barriers instead of log N.
+__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t S, uint32_t Ssh, uint32_t p) {
+    const uint32_t V = mulmod_shoup(y, S, Ssh, p);
+    y = submod(x, V, p);
+    x = addmod(x, V, p);
+}
+__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint32_t S, uint32_t Ssh, uint32_t p) {
+    const uint32_t U = x;
+    x = addmod(U, y, p);
+    y = mulmod_shoup(submod(U, y, p), S, Ssh, p);
+}
+
+// Cooley-Tukey forward, natural -> bit-reversed order
 __device__ void ntt_fwd_smem(uint32_t* a, const uint32_t* tw, const uint32_t* tw_sh, uint32_t N,
                              uint32_t logN, uint32_t p) {
-    uint32_t lt = logN - 1;  // log2(t)
-    for (uint32_t m = 1; m < N; m <<= 1, lt--) {
-        const uint32_t t = 1u << lt;
-        for (uint32_t idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
-            const uint32_t i = idx >> lt, j = idx & (t - 1);
-            const uint32_t j1 = (i << (lt + 1)) + j;
+    uint32_t m = 1, lt = logN - 1;            // stage (m, t = 2^lt): pairs (j, j + t) in blocks of 2t
+    for (; lt >= 1; m <<= 2, lt -= 2) {       // stages (m, t) and (2m, t/2)
+        const uint32_t t = 1u << lt, h = t >> 1;
+        for (uint32_t idx = threadIdx.x; idx < N / 4; idx += blockDim.x) {
+            const uint32_t i = idx >> (lt - 1), j = idx & (h - 1);
+            const uint32_t base = (i << (lt + 1)) + j;
+            uint32_t x0 = a[base], x1 = a[base + h], x2 = a[base + t], x3 = a[base + t + h];
             const uint32_t S = tw[m + i], Ssh = tw_sh[m + i];
-            const uint32_t U = a[j1];
-            const uint32_t V = mulmod_shoup(a[j1 + t], S, Ssh, p);
-            a[j1] = addmod(U, V, p);
-            a[j1 + t] = submod(U, V, p);
+            ct_bfly(x0, x2, S, Ssh, p);
+            ct_bfly(x1, x3, S, Ssh, p);
+            const uint32_t k0 = 2 * m + 2 * i;
+            ct_bfly(x0, x1, tw[k0], tw_sh[k0], p);
+            ct_bfly(x2, x3, tw[k0 + 1], tw_sh[k0 + 1], p);
+            a[base] = x0; a[base + h] = x1; a[base + t] = x2; a[base + t + h] = x3;
+        }
+        __syncthreads();
+        if (lt == 1) { m <<= 2; lt = 0; break; }
+    }
+    if (m < N) {                               // odd log N: last radix-2 stage, t = 1
+        for (uint32_t idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
+            const uint32_t j1 = idx << 1;
+            uint32_t x = a[j1], y = a[j1 + 1];
+            ct_bfly(x, y, tw[m + idx], tw_sh[m + idx], p);
+            a[j1] = x; a[j1 + 1] = y;
         }
         __syncthreads();
     }
 }
 
+// Gentleman-Sande inverse, bit-reversed -> natural order, times N^-1
 __device__ void ntt_inv_smem(uint32_t* a, const uint32_t* itw, const uint32_t* itw_sh, uint32_t N,
                              uint32_t logN, uint32_t p, uint32_t ninv, uint32_t ninv_sh) {
-    uint32_t lt = 0;
-    for (uint32_t m = N; m > 1; m >>= 1, lt++) {
-        const uint32_t t = 1u << lt, h = m >> 1;
+    uint32_t lt = 0, hh = N >> 1;             // stage (t = 2^lt, h = N / 2^(lt+1)): twiddle itw[h + i]
+    if (logN & 1) {                            // odd log N: first radix-2 stage, t = 1
         for (uint32_t idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
-            const uint32_t i = idx >> lt, j = idx & (t - 1);
-            const uint32_t j1 = (i << (lt + 1)) + j;
-            const uint32_t S = itw[h + i], Ssh = itw_sh[h + i];
-            const uint32_t U = a[j1], V = a[j1 + t];
-            a[j1] = addmod(U, V, p);
-            a[j1 + t] = mulmod_shoup(submod(U, V, p), S, Ssh, p);
+            const uint32_t j1 = idx << 1;
+            uint32_t x = a[j1], y = a[j1 + 1];
+            gs_bfly(x, y, itw[hh + idx], itw_sh[hh + idx], p);
+            a[j1] = x; a[j1 + 1] = y;
+        }
+        __syncthreads();
+        lt = 1; hh >>= 1;
+    }
+    for (; (1u << lt) < N; lt += 2, hh >>= 2) {     // stages (t, h) and (2t, h/2)
+        const uint32_t t = 1u << lt;
+        for (uint32_t idx = threadIdx.x; idx < N / 4; idx += blockDim.x) {
+            const uint32_t i = idx >> lt, j = idx & (t - 1);     // block of 4t
+            const uint32_t base = (i << (lt + 2)) + j;
+            uint32_t y0 = a[base], y1 = a[base + t], y2 = a[base + 2 * t], y3 = a[base + 3 * t];
+            const uint32_t k0 = hh + 2 * i;
+            gs_bfly(y0, y1, itw[k0], itw_sh[k0], p);
+            gs_bfly(y2, y3, itw[k0 + 1], itw_sh[k0 + 1], p);
+            const uint32_t k1 = (hh >> 1) + i;
+            gs_bfly(y0, y2, itw[k1], itw_sh[k1], p);
+            gs_bfly(y1, y3, itw[k1], itw_sh[k1], p);
+            if ((4u << lt) == N) {                // last pass: scale by N^-1 here
+                y0 = mulmod_shoup(y0, ninv, ninv_sh, p);
+                y1 = mulmod_shoup(y1, ninv, ninv_sh, p);
+                y2 = mulmod_shoup(y2, ninv, ninv_sh, p);
+                y3 = mulmod_shoup(y3, ninv, ninv_sh, p);
+            }
+            a[base] = y0; a[base + t] = y1; a[base + 2 * t] = y2; a[base + 3 * t] = y3;
         }
         __syncthreads();
     }
-    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) a[j] = mulmod_shoup(a[j], ninv, ninv_sh, p);
-    __syncthreads();
 }
 
 struct TwLimb {
@@ -55,6 +102,16 @@ struct TwLimb {
 __device__ __forceinline__ TwLimb tw_limb(const uint32_t* d_tw, uint32_t N, uint32_t i) {
     const uint32_t* b = d_tw + (size_t)i * 4 * N;
     return {b, b + N, b + 2 * N, b + 3 * N};
+}
+// Stage a limb's twiddle tables (forward pair, and the inverse pair if `inv`) in
+// shared memory at `dst`: every butterfly stage then reads them without a global
+// round trip (a transform is 2 log N dependent stages).  Returns the smem view.
+__device__ __forceinline__ TwLimb tw_stage(const uint32_t* d_tw, uint32_t N, uint32_t i, uint32_t* dst, bool inv) {
+    const uint4* src = reinterpret_cast<const uint4*>(d_tw + (size_t)i * 4 * N);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint32_t n4 = (inv ? 4 * N : 2 * N) / 4;
+    for (uint32_t j = threadIdx.x; j < n4; j += blockDim.x) d[j] = __ldg(src + j);
+    return {dst, dst + N, dst + 2 * N, dst + 3 * N};
 }
 
 // ---------------------------------------------------------------- KeyGen (A1)
@@ -68,8 +125,8 @@ __global__ void k_keygen(Rns R, const uint32_t* d_tw, uint64_t seed, int8_t* s, 
         if (i == 0) s[j] = (int8_t)v;
         sa[j] = v < 0 ? p - 1 : (uint32_t)v;
     }
+    TwLimb tw = tw_stage(d_tw, N, i, sa + N, false);
     __syncthreads();
-    TwLimb tw = tw_limb(d_tw, N, i);
     ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) s_ntt[(size_t)i * N + j] = sa[j];
 }
@@ -93,8 +150,10 @@ __global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, co
         sa[j] = a;
         ao[j] = a;
     }
-    __syncthreads();
+    // twiddles straight from global memory (L1/L2 resident): setup runs m x L CTAs,
+    // and occupancy hides their latency better than staging them in shared memory
     TwLimb tw = tw_limb(d_tw, N, i);
+    __syncthreads();
     ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
     const uint32_t* sn = s_ntt + (size_t)i * N;
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sn[j], p, mu);
@@ -117,8 +176,8 @@ __global__ void k_negacyclic_mul(Rns R, const uint32_t* d_tw, const uint32_t* A,
     uint32_t *sa = sm, *sb = sm + N;
     const size_t off = ((size_t)blockIdx.x * R.L + i) * N;
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) { sa[j] = A[off + j]; sb[j] = B[off + j]; }
+    TwLimb tw = tw_stage(d_tw, N, i, sm + 2 * N, true);
     __syncthreads();
-    TwLimb tw = tw_limb(d_tw, N, i);
     ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
     ntt_fwd_smem(sb, tw.fw, tw.fw_sh, N, R.logN, p);
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sb[j], p, R.mu[i]);
@@ -136,8 +195,8 @@ __global__ void k_decrypt_phase(Rns R, const uint32_t* d_tw, const uint32_t* s_n
     const uint32_t* b = cts + (((size_t)tg * 2 + 0) * Lo + i) * N;
     const uint32_t* a = cts + (((size_t)tg * 2 + 1) * Lo + i) * N;
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = a[j];
+    TwLimb tw = tw_stage(d_tw, N, i, sa + N, true);
     __syncthreads();
-    TwLimb tw = tw_limb(d_tw, N, i);
     ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
     const uint32_t* sn = s_ntt + (size_t)i * N;
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sn[j], p, R.mu[i]);
@@ -201,9 +260,17 @@ __global__ void k_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_
 // ---------------------------------------------------------------- launchers
 static uint32_t ntt_threads(uint32_t N) { return N >= 1024 ? 512 : N / 2; }
 
+// dynamic shared memory of the NTT kernels: `words` 32-bit words (data + staged twiddles)
+template <typename K>
+static cudaError_t ntt_smem(K kernel, size_t words) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(words * 4));
+}
+
 cudaError_t launch_keygen(nimbus_ctx* c, uint64_t seed, int8_t* d_s, uint32_t* d_s_ntt, cudaStream_t st) {
     const uint32_t N = c->rns.N;
-    k_keygen<<<c->rns.L, ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, seed, d_s, d_s_ntt);
+    cudaError_t e = ntt_smem(k_keygen, 3 * N);
+    if (e != cudaSuccess) return e;
+    k_keygen<<<c->rns.L, ntt_threads(N), 3 * N * 4, st>>>(c->rns, c->d_tw, seed, d_s, d_s_ntt);
     c->launches++;
     return cudaGetLastError();
 }
@@ -219,8 +286,9 @@ cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_
 cudaError_t launch_negacyclic_mul(nimbus_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t count,
                                   uint32_t* out, cudaStream_t st) {
     const uint32_t N = c->rns.N;
-    size_t smem = (size_t)N * 8;
-    cudaFuncSetAttribute(k_negacyclic_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = (size_t)N * 6 * 4;
+    cudaError_t e = ntt_smem(k_negacyclic_mul, 6 * N);
+    if (e != cudaSuccess) return e;
     k_negacyclic_mul<<<dim3(count, c->rns.L), ntt_threads(N), smem, st>>>(c->rns, c->d_tw, a, b, out);
     c->launches++;
     return cudaGetLastError();
@@ -230,8 +298,14 @@ cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_
                            uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, uint32_t* d_Z,
                            uint32_t* d_M, cudaStream_t st) {
     const uint32_t N = c->rns.N;
-    k_decrypt_phase<<<dim3(nct_total, c->rns.L_out), ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, d_s_ntt,
-                                                                                  cts, d_u_tmp);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e0 = ntt_smem(k_decrypt_phase, 5 * 8192);
+        if (e0 != cudaSuccess) return e0;
+        attr_set = true;
+    }
+    k_decrypt_phase<<<dim3(nct_total, c->rns.L_out), ntt_threads(N), 5 * N * 4, st>>>(c->rns, c->d_tw, d_s_ntt,
+                                                                                      cts, d_u_tmp);
     c->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -81,6 +81,8 @@ def lib():
             raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if "NIMBUS_LIB" in os.environ and not hasattr(L, name):
+                continue          # an older experiment build may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -1,0 +1,40 @@
+"""Time setup (Alg. 1 step 1: encrypt + tile Enc(W)) for one config's first
+matrix after a warm-up call; reports ms and GB/s of resident Enc(W) written.
+
+  NIMBUS_LIB=libnimbus_cop.so python tools/bench_setup.py --config 2
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import nimbus_inputs as ni
+from paper_2411_15707_b200 import nimbus as nb
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="2")
+ap.add_argument("--reps", type=int, default=5)
+args = ap.parse_args()
+cfg = ni.CONFIGS[int(args.config)]
+li, pj, lay = cfg.layers[0]
+seed = ni.seed_mm(cfg.cid, li, pj)
+ctx = nb.nimbus_ctx_create(cfg.N, cfg.L, cfg.ell, cfg.L_out)
+sk = nb.nimbus_keygen(ctx, cfg.seed_cfg)
+W = nb.from_numpy_u32(ni.gen_W(seed, lay.m, lay.n, cfg.ell), "cuda:0")
+w = nb.nimbus_encrypt_weights(ctx, sk, W, seed)
+torch.cuda.synchronize()
+ts = []
+for _ in range(args.reps):
+    del w
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    w = nb.nimbus_encrypt_weights(ctx, sk, W, seed)
+    torch.cuda.synchronize()
+    ts.append(time.perf_counter() - t0)
+t = min(ts)
+print(json.dumps({"config": cfg.name, "m": lay.m, "encrypt_ms": t * 1e3,
+                  "encw_gb_per_s": nb.nimbus_encw_bytes(w) / t / 1e9, "lib": nb.LIB_PATH.split("/")[-1]}))
