@@ -58,9 +58,9 @@ __device__ void ntt_fwd_smem(uint32_t* a, const uint32_t* tw, const uint32_t* tw
     }
 }
 
-// Gentleman-Sande inverse, bit-reversed -> natural order, times N^-1
+// Gentleman-Sande inverse, bit-reversed -> natural order, times N^-1 if `scale`
 __device__ void ntt_inv_smem(uint32_t* a, const uint32_t* itw, const uint32_t* itw_sh, uint32_t N,
-                             uint32_t logN, uint32_t p, uint32_t ninv, uint32_t ninv_sh) {
+                             uint32_t logN, uint32_t p, uint32_t ninv, uint32_t ninv_sh, bool scale = true) {
     uint32_t lt = 0, hh = N >> 1;             // stage (t = 2^lt, h = N / 2^(lt+1)): twiddle itw[h + i]
     if (logN & 1) {                            // odd log N: first radix-2 stage, t = 1
         for (uint32_t idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
@@ -84,7 +84,7 @@ __device__ void ntt_inv_smem(uint32_t* a, const uint32_t* itw, const uint32_t* i
             const uint32_t k1 = (hh >> 1) + i;
             gs_bfly(y0, y2, itw[k1], itw_sh[k1], p);
             gs_bfly(y1, y3, itw[k1], itw_sh[k1], p);
-            if ((4u << lt) == N) {                // last pass: scale by N^-1 here
+            if (scale && (4u << lt) == N) {       // last pass: scale by N^-1 here
                 y0 = mulmod_shoup(y0, ninv, ninv_sh, p);
                 y1 = mulmod_shoup(y1, ninv, ninv_sh, p);
                 y2 = mulmod_shoup(y2, ninv, ninv_sh, p);
@@ -205,6 +205,94 @@ __global__ void k_decrypt_phase(Rns R, const uint32_t* d_tw, const uint32_t* s_n
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) U[((size_t)tg * Lo + i) * N + j] = submod(b[j], sa[j], p);
 }
 
+// Same, one polynomial per 4-CTA cluster: CTA r holds coefficients [r Q, (r+1) Q),
+// Q = N/4, in shared memory.  The two forward stages and the two inverse stages
+// whose butterflies span the quarters run as one radix-4 pass over distributed
+// shared memory (each CTA takes a quarter of the Q four-element groups); every
+// other stage is CTA-local.  4x the SMs per polynomial: a few dozen packed
+// ciphertexts (C2: 26) no longer leave most of the GPU idle.
+constexpr uint32_t kDecCl = 4;
+
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_dsmem(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_dsmem(uint32_t a, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_decrypt_cl(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt,
+                                                   const uint32_t* cts, uint32_t* U) {
+    extern __shared__ uint32_t sa[];
+    const uint32_t N = R.N, Q = N / kDecCl, logQ = R.logN - 2, Lo = R.L_out;
+    const uint32_t r = cluster_ctarank(), tg = blockIdx.x / kDecCl, i = blockIdx.y, p = R.p[i];
+    const uint32_t* b = cts + (((size_t)tg * 2 + 0) * Lo + i) * N + r * Q;
+    const uint32_t* a = cts + (((size_t)tg * 2 + 1) * Lo + i) * N + r * Q;
+    for (uint32_t j = threadIdx.x; j < Q; j += blockDim.x) sa[j] = a[j];
+    const TwLimb tw = tw_limb(d_tw, N, i);
+    // this CTA's local-stage twiddles, re-indexed as a length-Q table: its stage-m
+    // block i is block r m + i of the global stage 4m, whose twiddle is entry
+    // 4m + r m + i; stored at m + i, the local stages run as a plain length-Q NTT
+    uint32_t* st = sa + Q;                        // [fw | fw_sh | iv | iv_sh], Q words each
+    for (uint32_t e = threadIdx.x; e < Q; e += blockDim.x) {
+        if (e == 0) continue;
+        const uint32_t m = 1u << (31 - __clz(e)), g = m * (kDecCl + r) + (e - m);
+        st[e] = tw.fw[g]; st[Q + e] = tw.fw_sh[g]; st[2 * Q + e] = tw.iv[g]; st[3 * Q + e] = tw.iv_sh[g];
+    }
+    uint32_t rem[kDecCl];
+#pragma unroll
+    for (uint32_t c = 0; c < kDecCl; c++) rem[c] = dsmem_addr(sa, c);
+    cluster_sync();
+    // forward stages (m = 1, t = N/2) and (m = 2, t = N/4): group j = {j, j+Q, j+2Q, j+3Q}
+    {
+        const uint32_t S1 = tw.fw[1], S1s = tw.fw_sh[1], S2 = tw.fw[2], S2s = tw.fw_sh[2];
+        const uint32_t S3 = tw.fw[3], S3s = tw.fw_sh[3];
+        for (uint32_t j = r * (Q / kDecCl) + threadIdx.x; j < (r + 1) * (Q / kDecCl); j += blockDim.x) {
+            uint32_t x0 = ld_dsmem(rem[0] + 4 * j), x1 = ld_dsmem(rem[1] + 4 * j);
+            uint32_t x2 = ld_dsmem(rem[2] + 4 * j), x3 = ld_dsmem(rem[3] + 4 * j);
+            ct_bfly(x0, x2, S1, S1s, p);
+            ct_bfly(x1, x3, S1, S1s, p);
+            ct_bfly(x0, x1, S2, S2s, p);
+            ct_bfly(x2, x3, S3, S3s, p);
+            st_dsmem(rem[0] + 4 * j, x0); st_dsmem(rem[1] + 4 * j, x1);
+            st_dsmem(rem[2] + 4 * j, x2); st_dsmem(rem[3] + 4 * j, x3);
+        }
+    }
+    cluster_sync();
+    ntt_fwd_smem(sa, st, st + Q, Q, logQ, p);
+    const uint32_t* sn = s_ntt + (size_t)i * N + r * Q;
+    for (uint32_t j = threadIdx.x; j < Q; j += blockDim.x) sa[j] = mulmod(sa[j], sn[j], p, R.mu[i]);
+    __syncthreads();
+    ntt_inv_smem(sa, st + 2 * Q, st + 3 * Q, Q, logQ, p, 0, 0, false);
+    cluster_sync();
+    // inverse stages (t = N/4, h = 2) and (t = N/2, h = 1), then N^-1
+    {
+        const uint32_t S1 = tw.iv[1], S1s = tw.iv_sh[1], S2 = tw.iv[2], S2s = tw.iv_sh[2];
+        const uint32_t S3 = tw.iv[3], S3s = tw.iv_sh[3], ni = R.ninv[i], nis = R.ninv_sh[i];
+        for (uint32_t j = r * (Q / kDecCl) + threadIdx.x; j < (r + 1) * (Q / kDecCl); j += blockDim.x) {
+            uint32_t y0 = ld_dsmem(rem[0] + 4 * j), y1 = ld_dsmem(rem[1] + 4 * j);
+            uint32_t y2 = ld_dsmem(rem[2] + 4 * j), y3 = ld_dsmem(rem[3] + 4 * j);
+            gs_bfly(y0, y1, S2, S2s, p);
+            gs_bfly(y2, y3, S3, S3s, p);
+            gs_bfly(y0, y2, S1, S1s, p);
+            gs_bfly(y1, y3, S1, S1s, p);
+            st_dsmem(rem[0] + 4 * j, mulmod_shoup(y0, ni, nis, p));
+            st_dsmem(rem[1] + 4 * j, mulmod_shoup(y1, ni, nis, p));
+            st_dsmem(rem[2] + 4 * j, mulmod_shoup(y2, ni, nis, p));
+            st_dsmem(rem[3] + 4 * j, mulmod_shoup(y3, ni, nis, p));
+        }
+    }
+    cluster_sync();
+    uint32_t* u = U + ((size_t)tg * Lo + i) * N + r * Q;
+    for (uint32_t j = threadIdx.x; j < Q; j += blockDim.x) u[j] = submod(b[j], sa[j], p);
+}
+
 // CRT (Garner) of u_0..u_{Lo-1} and m = floor((2 t u + q') / (2 q')) mod t
 // (SURVEY.md §8(c) #5); unpack Z[alpha][j] = m_theta[(alpha mod R) n + j].
 __global__ void k_decrypt_round(Rns R, const uint32_t* U, uint32_t nct, uint32_t kq, uint32_t n,
@@ -298,14 +386,24 @@ cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_
                            uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, uint32_t* d_Z,
                            uint32_t* d_M, cudaStream_t st) {
     const uint32_t N = c->rns.N;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e0 = ntt_smem(k_decrypt_phase, 5 * 8192);
+    {
+        // one 4-CTA cluster per (ciphertext, limb), a quarter of the coefficients each
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nct_total * kDecCl, c->rns.L_out);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = (size_t)N / kDecCl * 5 * 4;     // quarter + its 4 twiddle tables
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kDecCl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e0 = cudaLaunchKernelEx(&cfg, k_decrypt_cl, c->rns, (const uint32_t*)c->d_tw, d_s_ntt, cts,
+                                            d_u_tmp);
         if (e0 != cudaSuccess) return e0;
-        attr_set = true;
     }
-    k_decrypt_phase<<<dim3(nct_total, c->rns.L_out), ntt_threads(N), 5 * N * 4, st>>>(c->rns, c->d_tw, d_s_ntt,
-                                                                                      cts, d_u_tmp);
     c->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
