@@ -349,15 +349,15 @@ def test_batch_matches_sequential_and_oracle(nb, oracle):
     assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all()
 
 
-@pytest.mark.parametrize("env", [{"NIMBUS_NO_TRANSPOSED": "1"},
+@pytest.mark.parametrize("env", [{"NIMBUS_TRANSPOSED": "1"},
                                  {"NIMBUS_NO_RESIDENT": "1"}, {"NIMBUS_CLUSTER": "2"},
                                  {"NIMBUS_NO_RESIDENT": "1", "NIMBUS_CLUSTER": "2"}])
 @pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [(4096, 2, 16, 1, 768, 768, 128, 1),
                                                      (8192, 3, 32, 2, 300, 1000, 70, 3)])
 def test_kernel_variants_parity(nb, oracle, monkeypatch, env, N, L, ell, L_out, m, n, kq, nq):
-    """The non-default kernel variants (streaming instead of transposed for
-    ell=32, 48-column streaming kernel for ell=16, 2-CTA clusters with X
-    multicast) give the same bytes as the oracle."""
+    """The non-default kernel variants (transposed kernel for ell=32, 48-column
+    streaming kernel for ell=16, 2-CTA clusters with X multicast) give the same
+    bytes as the oracle."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=777 + m)
