@@ -3,6 +3,9 @@
 // copies in flight per CTA and CTAs per SM: what does the resident contraction's
 // E stream (3 x 32 KB in flight, one CTA per SM, ~17 us for 50 MB) leave on the
 // table?  L2 is made cold by reading (not writing) 512 MB before every run.
+// Result on B200 (TILE_KB=384, all copy sizes dividing the tile): ~13.2 us
+// (~3.97 TB/s) for 32 KB x 4, 64 KB x 2 or 96 KB x 2 alike -- no copy size or
+// depth beats the 3 x 32 KB ring for a cold 50 MB stream.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/stream_cold tools/stream_cold.cu
 #include <cstdio>
 #include <cstdlib>
@@ -71,7 +74,7 @@ int main() {
                     {131072, 1, 1}, {49152, 2, 1}, {49152, 4, 1}, {98304, 1, 1}, {98304, 2, 1}, {16384, 12, 1}};
     for (const V& v : vs) {
         const size_t smem = (size_t)v.stages * v.bytes + 1024;
-        if (smem * v.ctas_per_sm > 228 * 1024) continue;
+        if (smem * v.ctas_per_sm > 228 * 1024 || tile % v.bytes) continue;   // copies must tile the tile
         cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const uint32_t grid = sms * v.ctas_per_sm;
         float best = 1e9, sum = 0;
