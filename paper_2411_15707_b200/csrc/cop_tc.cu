@@ -274,7 +274,7 @@ struct ResCfg {
     static constexpr uint32_t B_BYTES = kSW * BN * BK;         // Enc(W) per k-block: 16 KB
     static constexpr uint32_t KPS = 2;                         // k-blocks per ring slot: one 32 KB bulk copy
     static constexpr uint32_t SLOT = KPS * B_BYTES;
-    static constexpr uint32_t STAGES = 3;
+    static constexpr uint32_t STAGES = 96 * 1024 / SLOT;       // 96 KB ring
     static constexpr uint32_t NACC = SX + kSW - 1;             // 5
     static constexpr uint32_t ACC_COLS = NACC * BN;            // 160
     static constexpr uint32_t A0_COLS = kResMaxKB * (BK / 4);  // slice 0 in TMEM: 32 columns per k-block
