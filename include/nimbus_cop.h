@@ -154,6 +154,28 @@ nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbu
 nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                       size_t ws_bytes, void* stream);
 
+/* Asynchronous weight loading: keep
+ * Enc(W) in pinned host memory and stage each matrix into HBM right before its
+ * matmul, overlapping the copy with the previous matmul's compute.
+ *  nimbus_encw_offload  moves the handle's Enc(W) to pinned host memory (synchronous
+ *                       on `stream`) and frees the device copy; nimbus_cop_matmul
+ *                       then returns EINVAL for it;
+ *  nimbus_encw_reload   copies it back into a fresh device allocation (async on `stream`);
+ *  nimbus_cop_stage_size  bytes of the device staging buffer for a job list
+ *                       (2 x the largest host-resident Enc(W); 0 if none);
+ *  nimbus_cop_matmul_streamed  runs the jobs in order on `stream` exactly as
+ *                       nimbus_cop_matmul would (same outputs, bit for bit); the
+ *                       host-resident ones are copied into alternating halves of
+ *                       d_stage on the context's copy stream, job j+2's copy
+ *                       overlapping job j+1's compute.  d_ws as for the largest job. */
+nimbus_status nimbus_encw_offload(nimbus_encw* encw, void* stream);
+nimbus_status nimbus_encw_reload(nimbus_encw* encw, void* stream);
+int nimbus_encw_is_resident(const nimbus_encw* encw);
+nimbus_status nimbus_cop_stage_size(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
+                                    size_t* bytes);
+nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+                                         size_t ws_bytes, void* d_stage, size_t stage_bytes, void* stream);
+
 /* Same computation with HOST buffers: copies h_X in, runs nimbus_cop_matmul,
  * copies h_cts and h_R out, and synchronises `stream` before returning. */
 nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* h_X,

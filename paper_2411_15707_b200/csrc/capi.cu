@@ -169,6 +169,8 @@ void nimbus_ctx_destroy(nimbus_ctx* ctx) {
     for (cudaEvent_t e : ctx->ev_pending) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->sync_ev) cudaEventDestroy(e);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    for (cudaEvent_t e : ctx->stream_ev) cudaEventDestroy(e);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
     delete ctx;
 }
 
@@ -271,14 +273,40 @@ nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const
 void nimbus_encw_destroy(nimbus_encw* w) {
     if (!w) return;
     if (w->d_Et) cudaFree(w->d_Et);
+    if (w->h_Et) cudaFreeHost(w->h_Et);
     delete w;
 }
+
+nimbus_status nimbus_encw_offload(nimbus_encw* w, void* stream) {
+    if (!w) return NIMBUS_EINVAL;
+    nimbus_ctx* ctx = w->ctx;
+    if (!w->d_Et) return NIMBUS_OK;                       // already host-resident
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!w->h_Et) CK(cudaMallocHost(&w->h_Et, w->bytes), "pinned host alloc");
+    CK(cudaMemcpyAsync(w->h_Et, w->d_Et, w->bytes, cudaMemcpyDeviceToHost, s), "offload copy");
+    CK(cudaStreamSynchronize(s), "offload sync");
+    CK(cudaFree(w->d_Et), "offload free");
+    w->d_Et = nullptr;
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_encw_reload(nimbus_encw* w, void* stream) {
+    if (!w) return NIMBUS_EINVAL;
+    nimbus_ctx* ctx = w->ctx;
+    if (w->d_Et) return NIMBUS_OK;
+    CK(cudaMalloc(&w->d_Et, w->bytes), "reload alloc");
+    CK(cudaMemcpyAsync(w->d_Et, w->h_Et, w->bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream), "reload copy");
+    return NIMBUS_OK;
+}
+
+int nimbus_encw_is_resident(const nimbus_encw* w) { return w && w->d_Et ? 1 : 0; }
 
 size_t nimbus_encw_bytes(const nimbus_encw* w) { return w ? w->bytes : 0; }
 
 nimbus_status nimbus_encw_export(const nimbus_encw* w, uint32_t* d_out, void* stream) {
     if (!w || !d_out) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
+    if (!w->d_Et) return set_err(ctx, NIMBUS_EINVAL, "Enc(W) is host-resident (nimbus_encw_reload first)");
     CK(launch_untile_encw(ctx, w->d_Et, w->m, w->KB, w->bn, d_out, (cudaStream_t)stream), "encw export");
     return NIMBUS_OK;
 }
@@ -329,12 +357,18 @@ nimbus_status nimbus_cop_workspace_size(const nimbus_ctx* ctx, const nimbus_encw
     return NIMBUS_OK;
 }
 
-static nimbus_status check_online(nimbus_ctx* ctx, const nimbus_encw* w, uint32_t kq, uint32_t nq) {
+static nimbus_status check_shape(nimbus_ctx* ctx, const nimbus_encw* w, uint32_t kq, uint32_t nq) {
     if (!ctx || !w || w->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "bad context / encw");
     if (kq == 0 || nq == 0) return set_err(ctx, NIMBUS_EINVAL, "k must be positive");
     if ((uint64_t)kq * nq > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
     const uint32_t R = ctx->rns.N / w->n;
     if (!noise_ok(ctx, w->m, kq < R ? kq : R)) return set_err(ctx, NIMBUS_ENOISE, "noise bound violated");
+    return NIMBUS_OK;
+}
+static nimbus_status check_online(nimbus_ctx* ctx, const nimbus_encw* w, uint32_t kq, uint32_t nq) {
+    nimbus_status st = check_shape(ctx, w, kq, nq);
+    if (st != NIMBUS_OK) return st;
+    if (!w->d_Et) return set_err(ctx, NIMBUS_EINVAL, "Enc(W) is host-resident: use nimbus_cop_matmul_streamed");
     return NIMBUS_OK;
 }
 
@@ -478,6 +512,96 @@ nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* job
         CK(cudaEventRecord(done_p[i], b), "record");
     }
     CK(cudaStreamWaitEvent(a, done_p[count - 1], 0), "join");   // everything complete in `stream` order
+    return NIMBUS_OK;
+}
+
+// ---------------------------------------------------------------- streamed path (Enc(W) in host memory)
+nimbus_status nimbus_cop_stage_size(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
+                                    size_t* bytes) {
+    if (!ctx || !jobs || !bytes || count == 0) return NIMBUS_EINVAL;
+    size_t mx = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        if (!jobs[i].encw) return NIMBUS_EINVAL;
+        if (!jobs[i].encw->d_Et) mx = mx > jobs[i].encw->bytes ? mx : jobs[i].encw->bytes;
+    }
+    *bytes = 2 * al1k(mx);
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+                                         size_t ws_bytes, void* d_stage, size_t stage_bytes, void* stream) {
+    if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    size_t need = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        nimbus_status st = check_shape(ctx, jobs[i].encw, jobs[i].k_per_query, jobs[i].n_queries);
+        if (st != NIMBUS_OK) return st;
+        if (!jobs[i].d_X || !jobs[i].d_cts || !jobs[i].d_R) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
+        const size_t w = ws_layout(ctx, jobs[i].encw, jobs[i].k_per_query * jobs[i].n_queries).total;
+        need = need > w ? need : w;
+    }
+    if (ws_bytes < need) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    size_t stage_need = 0;
+    nimbus_cop_stage_size(ctx, jobs, count, &stage_need);
+    if (stage_need && (!d_stage || stage_bytes < stage_need)) return set_err(ctx, NIMBUS_ESHAPE, "stage too small");
+    const size_t slot = stage_need / 2;
+    cudaStream_t a = (cudaStream_t)stream;
+    if (!ctx->copy) CK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "copy stream");
+    cudaStream_t b = ctx->copy;
+    while (ctx->stream_ev.size() < 2 * (size_t)count + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        ctx->stream_ev.push_back(e);
+    }
+    cudaEvent_t* loaded = ctx->stream_ev.data();           // Enc(W) of job i is in its slot (stream b)
+    cudaEvent_t* used = ctx->stream_ev.data() + count;     // job i's kernels are done with its slot (stream a)
+    // copies must not start before earlier work on `stream` that may still read the slots
+    CK(cudaEventRecord(ctx->stream_ev[2 * count], a), "record");
+    CK(cudaStreamWaitEvent(b, ctx->stream_ev[2 * count], 0), "wait");
+    // host-resident jobs alternate between the two slots; job j's copy waits until the
+    // job that last used its slot has finished, so copy j+1 overlaps the compute of job j
+    std::vector<int> slot_of(count, -1), prev_user(count, -1);
+    int last_user[2] = {-1, -1}, nh = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        if (jobs[i].encw->d_Et) continue;
+        const int sl = nh++ & 1;
+        slot_of[i] = sl;
+        prev_user[i] = last_user[sl];
+        last_user[sl] = (int)i;
+    }
+    uint8_t* stage = (uint8_t*)d_stage;
+    auto issue_copy = [&](uint32_t j) -> nimbus_status {
+        if (prev_user[j] >= 0) CK(cudaStreamWaitEvent(b, used[prev_user[j]], 0), "wait slot");
+        CK(cudaMemcpyAsync(stage + (size_t)slot_of[j] * slot, jobs[j].encw->h_Et, jobs[j].encw->bytes,
+                           cudaMemcpyHostToDevice, b), "stage copy");
+        CK(cudaEventRecord(loaded[j], b), "record");
+        return NIMBUS_OK;
+    };
+    // prefetch the first two host-resident jobs (both slots are free)
+    uint32_t issued = 0, n_issue = 0;
+    for (uint32_t j = 0; j < count && n_issue < 2; j++)
+        if (slot_of[j] >= 0) { nimbus_status st = issue_copy(j); if (st != NIMBUS_OK) return st; issued = j + 1; n_issue++; }
+    if (n_issue < 2) issued = count;
+    for (uint32_t i = 0; i < count; i++) {
+        const nimbus_cop_job& J = jobs[i];
+        nimbus_encw view = *J.encw;                        // same shape/layout, Enc(W) in its slot
+        view.h_Et = nullptr;
+        if (slot_of[i] >= 0) {
+            view.d_Et = stage + (size_t)slot_of[i] * slot;
+            CK(cudaStreamWaitEvent(a, loaded[i], 0), "wait load");
+        }
+        nimbus_status st = nimbus_cop_matmul(ctx, &view, J.d_X, J.k_per_query, J.n_queries, J.mask_seed, J.d_cts,
+                                             J.d_R, d_ws, ws_bytes, a);
+        view.d_Et = nullptr;                               // the view owns nothing
+        if (st != NIMBUS_OK) return st;
+        CK(cudaEventRecord(used[i], a), "record");
+        // next host-resident job not yet in flight: its slot frees when job i (or earlier) is done
+        while (issued < count && slot_of[issued] < 0) issued++;
+        if (issued < count && slot_of[i] >= 0) {
+            nimbus_status st2 = issue_copy(issued);
+            if (st2 != NIMBUS_OK) return st2;
+            issued++;
+        }
+    }
     return NIMBUS_OK;
 }
 

@@ -40,6 +40,9 @@ struct nimbus_ctx {
     // batched path (nimbus_cop_matmul_batch): side stream for the pack kernels + sync events
     cudaStream_t side = nullptr;
     std::vector<cudaEvent_t> sync_ev;
+    // streamed path (nimbus_cop_matmul_streamed): host -> device copy stream + events
+    cudaStream_t copy = nullptr;
+    std::vector<cudaEvent_t> stream_ev;
 };
 
 struct nimbus_sk {
@@ -52,7 +55,8 @@ struct nimbus_encw {
     nimbus_ctx* ctx = nullptr;
     uint32_t m = 0, n = 0, KB = 0; // KB = ceil(m / 128) k-blocks
     uint32_t bn = kBNT;            // tile width (columns) of the resident layout
-    uint8_t* d_Et = nullptr;       // tiled byte planes [ct][kb][s][bn][128 swizzled]
+    uint8_t* d_Et = nullptr;       // tiled byte planes [ct][kb][s][bn][128 swizzled]; null when offloaded
+    uint8_t* h_Et = nullptr;       // pinned host copy of the same bytes (nimbus_encw_offload)
     size_t bytes = 0;
 };
 

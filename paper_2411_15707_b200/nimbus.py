@@ -64,6 +64,11 @@ _SIGS = {
     "nimbus_cop_matmul_batch": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_profile_enable": (C.c_int, [_vp, C.c_int]),
     "nimbus_profile_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(_u64), C.c_int]),
+    "nimbus_encw_offload": (C.c_int, [_vp, _vp]),
+    "nimbus_encw_reload": (C.c_int, [_vp, _vp]),
+    "nimbus_encw_is_resident": (C.c_int, [_vp]),
+    "nimbus_cop_stage_size": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
+    "nimbus_cop_matmul_streamed": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp, _sz, _vp]),
     "nimbus_plain_weights": (C.c_int, [_vp, _vp, _u32, _u32, _vp, C.POINTER(_vp)]),
     "nimbus_plainw_destroy": (None, [_vp]),
     "nimbus_server_workspace_size": (C.c_int, [_vp, _vp, _u32, _u32, C.POINTER(_sz)]),
@@ -296,6 +301,31 @@ def nimbus_cop_workspace_size_batch(ctx: Context, jobs) -> int:
 def nimbus_cop_matmul_batch(ctx: Context, jobs, ws: torch.Tensor, stream=None):
     arr = _jobs(jobs)
     _check(lib().nimbus_cop_matmul_batch(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+
+
+def nimbus_encw_offload(w: EncW, stream=None):
+    _check(lib().nimbus_encw_offload(w.ptr, _stream(stream)), w.owner)
+
+
+def nimbus_encw_reload(w: EncW, stream=None):
+    _check(lib().nimbus_encw_reload(w.ptr, _stream(stream)), w.owner)
+
+
+def nimbus_encw_is_resident(w: EncW) -> bool:
+    return bool(lib().nimbus_encw_is_resident(w.ptr))
+
+
+def nimbus_cop_stage_size(ctx: Context, jobs) -> int:
+    out = _sz()
+    _check(lib().nimbus_cop_stage_size(ctx.ptr, _jobs(jobs), len(jobs), C.byref(out)), ctx)
+    return int(out.value)
+
+
+def nimbus_cop_matmul_streamed(ctx: Context, jobs, ws: torch.Tensor, stage: torch.Tensor = None, stream=None):
+    arr = _jobs(jobs)
+    _check(lib().nimbus_cop_matmul_streamed(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(),
+                                            _ptr(stage) if stage is not None else None,
+                                            stage.numel() if stage is not None else 0, _stream(stream)), ctx)
 
 
 def nimbus_cop_matmul_host(ctx: Context, w: EncW, X_host: torch.Tensor, k_per_query: int,

@@ -406,3 +406,44 @@ def test_server_output_parity_and_shares(nb, oracle, N, L, ell, L_out, m, n, kq,
     X = (c.X.astype(np.uint64) + Xs) % t
     Y = matmul_mod_t(X, c.W, ell)
     assert ((u32(Ys).astype(np.uint64) + u32(R)) % t == Y).all()
+
+
+# ------------------------------------------------------------------ streamed Enc(W) (host-resident)
+def test_streamed_matches_resident(nb, oracle):
+    """nimbus_cop_matmul_streamed (Enc(W) offloaded to pinned host memory and
+    staged into alternating device slots, copy j+2 overlapping compute j+1) gives
+    the bytes nimbus_cop_matmul gives with Enc(W) resident, for a job list mixing
+    host-resident and resident matrices of different shapes; offloaded handles
+    are refused by nimbus_cop_matmul and work again after nimbus_encw_reload."""
+    N, L, ell, L_out = 4096, 2, 16, 1
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, 5)
+    shapes = [(128, 768, 768, 1), (64, 300, 700, 2), (128, 768, 3072, 1), (100, 1000, 500, 1), (128, 768, 768, 1)]
+    jobs, ref = [], []
+    ws = torch.empty(max(nb.nimbus_cop_workspace_size(ctx, nb.nimbus_encrypt_weights(ctx, sk, dev_u32(
+        ni.gen_W(1, m, n, ell)), 1), kq * nq) for kq, m, n, nq in shapes), dtype=torch.uint8, device=DEV)
+    for i, (kq, m, n, nq) in enumerate(shapes):
+        w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(ni.gen_W(40 + i, m, n, ell)), 40 + i)
+        X = dev_u32(ni.gen_X(50 + i, kq * nq, m, ell))
+        c0, R0 = nb.alloc_outputs(ctx, w, kq, nq)
+        nb.nimbus_cop_matmul(ctx, w, X, kq, nq, 60 + i, c0, R0, ws)
+        ref.append((c0, R0))
+        cts, R = nb.alloc_outputs(ctx, w, kq, nq)
+        jobs.append(dict(encw=w, X=X, k_per_query=kq, n_queries=nq, mask_seed=60 + i, cts=cts, R=R))
+    nb.nimbus_sync(ctx)
+    for i in (0, 2, 3, 4):                      # job 1 stays resident
+        nb.nimbus_encw_offload(jobs[i]["encw"])
+        assert not nb.nimbus_encw_is_resident(jobs[i]["encw"])
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_cop_matmul(ctx, jobs[0]["encw"], jobs[0]["X"], 128, 1, 60, jobs[0]["cts"], jobs[0]["R"], ws)
+    assert e.value.status == -1
+    stage = torch.empty(nb.nimbus_cop_stage_size(ctx, jobs), dtype=torch.uint8, device=DEV)
+    nb.nimbus_cop_matmul_streamed(ctx, jobs, ws, stage)
+    nb.nimbus_sync(ctx)
+    for j, (c0, R0) in zip(jobs, ref):
+        assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+    nb.nimbus_encw_reload(jobs[0]["encw"])
+    c1, R1 = nb.alloc_outputs(ctx, jobs[0]["encw"], 128, 1)
+    nb.nimbus_cop_matmul(ctx, jobs[0]["encw"], jobs[0]["X"], 128, 1, 60, c1, R1, ws)
+    nb.nimbus_sync(ctx)
+    assert torch.equal(c1, ref[0][0]) and torch.equal(R1, ref[0][1])
