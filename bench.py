@@ -59,6 +59,8 @@ def parse():
 def get_config(key: str):
     if key.endswith("l16"):
         return ni.CONFIGS_L16[int(key[0])]
+    if key.endswith("l64"):
+        return ni.CONFIGS_L64[int(key[0])]
     return ni.CONFIGS[int(key)]
 
 
@@ -94,7 +96,7 @@ def weak_value(macs_per_rank_step: float, world: int, ms_per_step: float) -> flo
 
 
 def sx_of(ell):
-    return 1 if ell <= 8 else 2 if ell <= 16 else 4
+    return 1 if ell <= 8 else 2 if ell <= 16 else 4 if ell <= 32 else 8
 
 
 def measured_peaks():
@@ -173,19 +175,24 @@ def run_gpu(args, cfg, rank, world, local_rank):
     mats = []
     t_setup = 0.0
     enc_bytes = 0
+    wide = cfg.ell > 32                      # X, W, R as uint64: the _u64 entry points
+    to_dev = nb.from_numpy_u64 if wide else nb.from_numpy_u32
+    encrypt = nb.nimbus_encrypt_weights_u64 if wide else nb.nimbus_encrypt_weights
+    outputs = nb.alloc_outputs_u64 if wide else nb.alloc_outputs
+    matmul = nb.nimbus_cop_matmul_u64 if wide else nb.nimbus_cop_matmul
     for li, pj, lay in cfg.layers:
         seed = ni.seed_mm(cfg.cid, li, pj)
-        W = nb.from_numpy_u32(ni.gen_W(seed, lay.m, lay.n, cfg.ell), dev)
+        W = to_dev(ni.gen_W(seed, lay.m, lay.n, cfg.ell), dev)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        encw = nb.nimbus_encrypt_weights(ctx, sk, W, seed)
+        encw = encrypt(ctx, sk, W, seed)
         torch.cuda.synchronize()
         t_setup += time.perf_counter() - t0
         enc_bytes += nb.nimbus_encw_bytes(encw)
         # per-rank independent queries (weak scaling): X seeded by rank
         xseed = rank_x_seed(seed, rank)
-        X = nb.from_numpy_u32(ni.gen_X(xseed, lay.k, lay.m, cfg.ell), dev)
-        cts, R = nb.alloc_outputs(ctx, encw, lay.k_per_query, lay.n_queries)
+        X = to_dev(ni.gen_X(xseed, lay.k, lay.m, cfg.ell), dev)
+        cts, R = outputs(ctx, encw, lay.k_per_query, lay.n_queries)
         mats.append(dict(lay=lay, seed=seed, encw=[encw], X=[X], W=W, cts=cts, R=R,
                          ws_bytes=nb.nimbus_cop_workspace_size(ctx, encw, lay.k)))
     # cold L2 without a flush write (whose dirty lines would be written back during
@@ -198,7 +205,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         for mt in mats:
             lay = mt["lay"]
             for _ in range(n_copies - 1):
-                mt["encw"].append(nb.nimbus_encrypt_weights(ctx, sk, mt["W"], mt["seed"]))
+                mt["encw"].append(encrypt(ctx, sk, mt["W"], mt["seed"]))
                 mt["X"].append(mt["X"][0].clone())
     for mt in mats:
         del mt["W"]
@@ -213,7 +220,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                   n_queries=mt["lay"].n_queries, mask_seed=mt["seed"], cts=mt["cts"], R=mt["R"]) for mt in mats]
             for c in range(n_copies)]
     ws_batch = None
-    if len(mats) > 1:
+    if len(mats) > 1 and not wide:           # the batched call is 32-bit only
         ws_batch = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs[0]), dtype=torch.uint8, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES if args.l2 == "write" else 64 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -232,8 +239,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
             return
         for mt in mats:
             lay = mt["lay"]
-            nb.nimbus_cop_matmul(ctx, mt["encw"][c], mt["X"][c], lay.k_per_query, lay.n_queries, mt["seed"],
-                                 mt["cts"], mt["R"], mt["ws"])
+            matmul(ctx, mt["encw"][c], mt["X"][c], lay.k_per_query, lay.n_queries, mt["seed"],
+                   mt["cts"], mt["R"], mt["ws"])
 
     for _ in range(max(args.warmup, n_copies)):
         cold()
@@ -296,17 +303,23 @@ def run_gpu(args, cfg, rank, world, local_rank):
         for mt in mats:
             lay = mt["lay"]
             Xh = mt["X"][0].cpu().pin_memory()
-            ch, Rh = nb.alloc_outputs(ctx, mt["encw"][0], lay.k_per_query, lay.n_queries, pin=True, device="cpu")
+            if wide:
+                c_, R_ = nb.alloc_outputs_u64(ctx, mt["encw"][0], lay.k_per_query, lay.n_queries)
+                ch, Rh = c_.cpu().pin_memory(), R_.cpu().pin_memory()
+            else:
+                ch, Rh = nb.alloc_outputs(ctx, mt["encw"][0], lay.k_per_query, lay.n_queries, pin=True,
+                                          device="cpu")
             hosts.append((Xh, ch, Rh))
-        h2d = sum(h[0].numel() * 4 for h in hosts)
-        d2h = sum(h[1].numel() * 4 + h[2].numel() * 4 for h in hosts)
+        h2d = sum(h[0].numel() * h[0].element_size() for h in hosts)
+        d2h = sum(h[1].numel() * h[1].element_size() + h[2].numel() * h[2].element_size() for h in hosts)
+        host_matmul = nb.nimbus_cop_matmul_host_u64 if wide else nb.nimbus_cop_matmul_host
 
         def step_host():
             c = step_no[0] % n_copies
             for mt, (Xh, ch, Rh) in zip(mats, hosts):
                 lay = mt["lay"]
-                nb.nimbus_cop_matmul_host(ctx, mt["encw"][c], Xh, lay.k_per_query, lay.n_queries, mt["seed"],
-                                          ch, Rh, mt["ws"])
+                host_matmul(ctx, mt["encw"][c], Xh, lay.k_per_query, lay.n_queries, mt["seed"],
+                            ch, Rh, mt["ws"])
         for _ in range(max(3, args.warmup)):
             cold()
             step_host()
@@ -489,8 +502,14 @@ def main():
         out["e2e"] = {"value": weak_value(macs_step, world, e["step_ms"]), "unit": UNIT,
                       "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"], "ms_per_step": e["step_ms"]}
     if world == 1 and not args.no_cpu_baseline:
-        v, desc, cores = oracle_sample(cfg, args.cpu_budget_s)
-        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        if cfg.ell > 32:
+            # q > 2^128: only the Python-integer oracle (oracle/wide.py) covers ell = 64, far too slow
+            # to time on a workload-sized sample
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
+                                   "sample": "not timed: the ell > 32 oracle is Python integers (oracle/wide.py)"}
+        else:
+            v, desc, cores = oracle_sample(cfg, args.cpu_budget_s)
+            out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
     print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

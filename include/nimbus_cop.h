@@ -48,9 +48,10 @@ enum { NIMBUS_FLAG_CHECK_RANGE = 1 };
 
 /* RLWE / workload parameters (App. B.1 {N, q, t}).
  *  N      ring degree, power of two, 64 <= N <= 8192
- *  L      number of 31-bit NTT primes in q (1..4); q = p_0 ... p_{L-1}
- *  ell    plaintext bits, t = 2^ell, 1 <= ell <= 32
- *  L_out  limbs kept by the mod-switch of the output (1..L)
+ *  L      number of 31-bit NTT primes in q (1..6, each with 2^32 mod p < 2^21);
+ *         q = p_0 ... p_{L-1}
+ *  ell    plaintext bits, t = 2^ell, 1 <= ell <= 64 (> 32: the _u64 entry points)
+ *  L_out  limbs kept by the mod-switch of the output (1..min(L, 3))
  *  impl   NIMBUS_IMPL_TCGEN05 (tcgen05 int8 tensor cores) or
  *         NIMBUS_IMPL_CUDACORE (lazy-reduction CUDA-core ablation)
  *  flags  NIMBUS_FLAG_* */
@@ -96,6 +97,16 @@ nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream);
 nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W,
                                      uint32_t m, uint32_t n, uint64_t seed, void* stream,
                                      nimbus_encw** out);
+/* ell > 32 (up to the paper's ell = 64): X, W, R and Z
+ * are uint64 arrays, through the _u64 entry points below; the 32-bit entry
+ * points return NIMBUS_EINVAL for such a context and the _u64 ones for ell <= 32.
+ * ell > 32 needs L >= 4 limbs for the noise bound (5 at N = 8192), uses S_x = 8
+ * X slices (11 shifted accumulators, the transposed kernel) and m <= 4096; the
+ * CUDA-core ablation, the batched / streamed / host-buffer / server-side calls
+ * and nimbus_cop_accumulate / nimbus_cop_pack are 32-bit only. */
+nimbus_status nimbus_encrypt_weights_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W,
+                                         uint32_t m, uint32_t n, uint64_t seed, void* stream,
+                                         nimbus_encw** out);
 void nimbus_encw_destroy(nimbus_encw* encw);
 /* Bytes of device memory held by the handle. */
 size_t nimbus_encw_bytes(const nimbus_encw* encw);
@@ -132,6 +143,11 @@ nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* encw, const 
                                 uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
                                 uint32_t* d_cts, uint32_t* d_R, void* d_ws, size_t ws_bytes,
                                 void* stream);
+/* ell > 32: d_X k x m uint64, d_R k x n uint64 (see nimbus_encrypt_weights_u64). */
+nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* encw, const uint64_t* d_X,
+                                    uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
+                                    uint32_t* d_cts, uint64_t* d_R, void* d_ws, size_t ws_bytes,
+                                    void* stream);
 
 /* A sequence of COP matmuls (e.g. all linear layers of a model pass, SURVEY.md
  * config C5): equivalent to nimbus_cop_matmul for jobs[0..count-1] in order,
@@ -182,6 +198,10 @@ nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* encw, c
                                      uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
                                      uint32_t* h_cts, uint32_t* h_R, void* d_ws, size_t ws_bytes,
                                      void* stream);
+nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* encw, const uint64_t* h_X,
+                                         uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
+                                         uint32_t* h_cts, uint64_t* h_R, void* d_ws, size_t ws_bytes,
+                                         void* stream);
 
 /* Step 2 alone (verification of the contraction): d_C is k x 2 x L x N uint32,
  * [alpha][comp][limb][j], the unpacked ciphertexts c[alpha] reduced mod p_i. */
@@ -202,6 +222,10 @@ nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t k_p
 nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts,
                              uint32_t k_per_query, uint32_t n_queries, uint32_t n, uint32_t* d_Z,
                              uint32_t* d_M, void* stream);
+/* ell > 32: d_Z k x n uint64, d_M (optional) n_queries x n_cts x N uint64. */
+nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts,
+                                 uint32_t k_per_query, uint32_t n_queries, uint32_t n, uint64_t* d_Z,
+                                 uint64_t* d_M, void* stream);
 
 /* ------------------------------------------------------ server, step 5 --- */
 /* Alg. 1 step 5: the server computes W<X>_s locally and outputs

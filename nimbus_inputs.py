@@ -58,9 +58,9 @@ def prg_words(seed: int, dom: int, start: int, count: int) -> np.ndarray:
 
 
 def uniform_mod_t(seed: int, dom: int, count: int, ell: int, start: int = 0) -> np.ndarray:
-    """uniform in Z_t, t = 2^ell: word >> (64 - ell)."""
+    """uniform in Z_t, t = 2^ell: word >> (64 - ell); uint32 for ell <= 32, uint64 beyond."""
     w = prg_words(seed, dom, start, count)
-    return (w >> np.uint64(64 - ell)).astype(np.uint32)
+    return (w >> np.uint64(64 - ell)).astype(np.uint32 if ell <= 32 else np.uint64)
 
 
 @dataclasses.dataclass(frozen=True)
@@ -132,6 +132,14 @@ CONFIGS = {
 CONFIGS_L16 = {
     4: dataclasses.replace(CONFIGS[4], ell=16, L_out=1, name="C4@l16"),
     5: dataclasses.replace(CONFIGS[5], ell=16, L_out=1, name="C5@l16"),
+}
+
+
+# The paper's own t (ell = 64): q = 5 x 31-bit primes,
+# 3-limb output (the noise bound at m = 3072, R = 10 needs q > 2^148 and q' > 2^86).
+CONFIGS_L64 = {
+    4: dataclasses.replace(CONFIGS[4], L=5, ell=64, L_out=3, name="C4@l64"),
+    5: dataclasses.replace(CONFIGS[5], L=5, ell=64, L_out=3, name="C5@l64"),
 }
 
 

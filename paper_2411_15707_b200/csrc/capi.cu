@@ -56,20 +56,52 @@ static nimbus_status cuda_err(nimbus_ctx* c, cudaError_t e, const char* where) {
 
 static inline uint64_t ncols(const nimbus_ctx* c) { return 2ull * c->rns.L * c->rns.N; }
 
+// Big (internal.h) arithmetic for q = prod p_i beyond 128 bits (ell = 64 needs q > 2^150)
+// and the noise bound products.
+static Big big_of(u128 x) { Big b; b.w[0] = (uint64_t)x; b.w[1] = (uint64_t)(x >> 64); return b; }
+static void big_mul(Big& a, uint64_t m) {
+    u128 c = 0;
+    for (int i = 0; i < 6; i++) { c += (u128)a.w[i] * m; a.w[i] = (uint64_t)c; c >>= 64; }
+}
+static void big_add(Big& a, uint64_t v) {
+    u128 c = v;
+    for (int i = 0; i < 6 && c; i++) { c += a.w[i]; a.w[i] = (uint64_t)c; c >>= 64; }
+}
+static void big_shl(Big& a, uint32_t sh) {       // a <<= sh, sh <= 64
+    if (sh == 64) { for (int i = 5; i > 0; i--) a.w[i] = a.w[i - 1]; a.w[0] = 0; return; }
+    if (sh == 0) return;
+    for (int i = 5; i > 0; i--) a.w[i] = (a.w[i] << sh) | (a.w[i - 1] >> (64 - sh));
+    a.w[0] <<= sh;
+}
+static uint64_t big_divmod(Big& a, uint64_t d) {  // a /= d, returns a mod d
+    u128 r = 0;
+    for (int i = 5; i >= 0; i--) { r = (r << 64) | a.w[i]; a.w[i] = (uint64_t)(r / d); r %= d; }
+    return (uint64_t)r;
+}
+static int big_cmp(const Big& a, const Big& b) {
+    for (int i = 5; i >= 0; i--) if (a.w[i] != b.w[i]) return a.w[i] < b.w[i] ? -1 : 1;
+    return 0;
+}
+
 // Worst-case decryption bound (SURVEY.md §8(c) "Worst-case noise guarantee"),
 // in integer upper bounds on 2|v|:  fresh+COP+packing 2v <= R m (t-1)(2 eta + 1);
 // each limb drop v -> v/p + (1+N)/2; the mask adds 1/2.  Requires 2|v| t < q.
 static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff) {
     const uint32_t ell = c->rns.ell, N = c->rns.N;
-    const u128 t = (u128)1 << ell;
-    u128 B = (u128)R_eff * m * (t - 1) * 43u;  // 2 eta + 1 = 43 for CBD(21)
-    if (B * t >= c->q) return false;
+    const uint64_t tm1 = ell >= 64 ? ~0ULL : (1ULL << ell) - 1;
+    Big B = big_of((u128)R_eff * m * 43u);      // 2 eta + 1 = 43 for CBD(21)
+    big_mul(B, tm1);
+    Big Bt = B;
+    big_shl(Bt, ell);
+    if (big_cmp(Bt, c->q) >= 0) return false;
     for (uint32_t l = c->rns.L; l > c->rns.L_out; l--) {
         const uint64_t p = c->rns.p[l - 1];
-        B = (B + p - 1) / p + 1 + N;
+        const uint64_t r = big_divmod(B, p);      // ceil(B / p) + 1 + N
+        big_add(B, (r ? 1 : 0) + 1 + N);
     }
-    B += 1;
-    return B * t < c->qout;
+    big_add(B, 1);
+    big_shl(B, ell);
+    return big_cmp(B, big_of(c->qout)) < 0;
 }
 
 extern "C" {
@@ -79,7 +111,8 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
     *out = nullptr;
     const uint32_t N = prm->N, L = prm->L, ell = prm->ell, Lo = prm->L_out;
     if (N < 64 || N > 8192 || (N & (N - 1))) return NIMBUS_EINVAL;
-    if (L < 1 || L > NIMBUS_MAXL || Lo < 1 || Lo > L || ell < 1 || ell > 32) return NIMBUS_EINVAL;
+    if (L < 1 || L > NIMBUS_MAXL || Lo < 1 || Lo > L || ell < 1 || ell > 64) return NIMBUS_EINVAL;
+    if (ell > 32 && prm->impl != NIMBUS_IMPL_TCGEN05) return NIMBUS_EINVAL;   // CUDA-core ablation: ell <= 32
     if (prm->impl > 1) return NIMBUS_EINVAL;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return NIMBUS_ECUDA;
@@ -104,23 +137,25 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
         while (f < L && cnd > (1ull << 30)) { if (h_is_prime(cnd)) R.p[f++] = (uint32_t)cnd; cnd -= step; }
         if (f < L) { delete ctx; return NIMBUS_EINVAL; }
     }
-    ctx->q = 1;
-    for (uint32_t i = 0; i < L; i++) ctx->q *= R.p[i];
+    ctx->q = Big();
+    ctx->q.w[0] = 1;
+    for (uint32_t i = 0; i < L; i++) big_mul(ctx->q, R.p[i]);
     ctx->qout = 1;
     for (uint32_t i = 0; i < Lo; i++) ctx->qout *= R.p[i];
-    // decrypt arithmetic: 2 t u + q' must fit in 127 bits
+    // decrypt arithmetic: the remainder of the long division by 2q' is shifted 32 bits
+    // at a time in 128 bits, so q' < 2^95 (at most 3 limbs)
     {
         int qb = 0; u128 x = ctx->qout; while (x) { qb++; x >>= 1; }
-        if (qb + (int)ell + 2 > 127) { delete ctx; return NIMBUS_EINVAL; }
+        if (Lo > 3 || qb > 95) { delete ctx; return NIMBUS_EINVAL; }
     }
-    const u128 t = (u128)1 << ell;
-    R.q_mod_t = (uint32_t)(ctx->q % t);
-    R.qout_mod_t = (uint32_t)(ctx->qout % t);
+    const uint64_t tmask = ell >= 64 ? ~0ULL : (1ULL << ell) - 1;
+    R.q_mod_t = ctx->q.w[0] & tmask;                 // q mod 2^ell = low bits
+    R.qout_mod_t = (uint64_t)ctx->qout & tmask;
     for (uint32_t i = 0; i < L; i++) {
         const uint64_t p = R.p[i];
         R.mu[i] = (uint64_t)((((u128)1) << 64) / p);
-        R.t_inv[i] = (uint32_t)h_inv((uint64_t)(t % p), p);
-        for (uint32_t s = 0; s < 8; s++) R.pow8[i][s] = (uint32_t)h_pow(2, 8 * s, p);
+        R.t_inv[i] = (uint32_t)h_inv(h_pow(2, ell, p), p);
+        for (uint32_t s = 0; s < 12; s++) R.pow8[i][s] = (uint32_t)h_pow(2, 8 * s, p);
         R.c32[i] = (uint32_t)(((u128)1 << 32) % p);
         if (R.c32[i] >= (1u << 21)) { delete ctx; return NIMBUS_EINVAL; }   // reduce64_pm precondition
         R.t_inv_sh[i] = (uint32_t)(((uint64_t)R.t_inv[i] << 32) / p);
@@ -231,6 +266,8 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     if (m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "m and n must be positive");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N (PAPER.md:232 needs n < N)");
     if (m > 8192) return set_err(ctx, NIMBUS_ESHAPE, "m > 8192 exceeds the int32 slice-accumulator bound");
+    // ell > 32: the 11 shifted accumulators, 7 of them scaled by 2^(8s) mod p, must sum below 2^64
+    if (ctx->rns.ell > 32 && m > 4096) return set_err(ctx, NIMBUS_ESHAPE, "m > 4096 at ell > 32 (64-bit recombination)");
     if (!noise_ok(ctx, m, 1)) return set_err(ctx, NIMBUS_ENOISE, "parameters fail the decryption noise bound");
     nimbus_encw* w = new (std::nothrow) nimbus_encw();
     if (!w) return NIMBUS_ENOMEM;
@@ -244,6 +281,7 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
         const char* tr = getenv("NIMBUS_TRANSPOSED");
         if (sx_of(ctx->rns.ell) == 2 && w->KB <= kResMaxKB && !getenv("NIMBUS_NO_RESIDENT")) w->bn = kBNR;
         else if (sx_of(ctx->rns.ell) == 4 && ctx->rns.N >= kBNW && tr && atoi(tr) == 1) w->bn = kBNW;
+        else if (sx_of(ctx->rns.ell) == 8) w->bn = kBNW;      // 8 X slices: transposed kernel only
     }
     w->bytes = (size_t)w->KB * kBK * col_tiles(ctx, w->bn) * w->bn * 4;
     cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
@@ -252,7 +290,7 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     return NIMBUS_OK;
 }
 
-nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint32_t m,
+static nimbus_status encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const void* d_W, uint32_t m,
                                      uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
     if (!ctx || !sk || !d_W || !out || sk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     *out = nullptr;
@@ -268,6 +306,27 @@ nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const
     if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encrypt_weights"); }
     *out = w;
     return NIMBUS_OK;
+}
+
+// the element width at the boundary follows ell: uint32 up to 32 bits, uint64 beyond
+static nimbus_status want_width(nimbus_ctx* ctx, uint32_t bytes) {
+    if (!ctx) return NIMBUS_EINVAL;
+    if (elem_bytes(ctx->rns.ell) != bytes)
+        return set_err(ctx, NIMBUS_EINVAL, bytes == 4 ? "ell > 32: use the _u64 entry point"
+                                                      : "ell <= 32: use the 32-bit entry point");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint32_t m,
+                                     uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : encrypt_weights(ctx, sk, d_W, m, n, seed, stream, out);
+}
+
+nimbus_status nimbus_encrypt_weights_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W, uint32_t m,
+                                         uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
+    nimbus_status st = want_width(ctx, 8);
+    return st != NIMBUS_OK ? st : encrypt_weights(ctx, sk, d_W, m, n, seed, stream, out);
 }
 
 void nimbus_encw_destroy(nimbus_encw* w) {
@@ -345,9 +404,10 @@ static WsLayout ws_layout(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t 
     L.xt = 0;
     L.c = al(xt_bytes);
     L.stage_x = L.c + al(c_bytes);
-    L.stage_cts = L.stage_x + al((size_t)k * w->m * 4);
+    const size_t es = elem_bytes(ctx->rns.ell);
+    L.stage_cts = L.stage_x + al((size_t)k * w->m * es);
     L.stage_r = L.stage_cts + al((size_t)k * 2 * ctx->rns.L_out * ctx->rns.N * 4);
-    L.total = L.stage_r + al((size_t)k * w->n * 4);
+    L.total = L.stage_r + al((size_t)k * w->n * es);
     return L;
 }
 
@@ -384,23 +444,27 @@ static void prof_mark(nimbus_ctx* ctx, cudaStream_t s) {
     if (ctx->profile) cudaEventRecord(prof_event(ctx), s);
 }
 
-static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
+static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const void* d_X, uint32_t k,
                                     uint32_t* d_C, uint8_t* ws, cudaStream_t s) {
     if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
         uint8_t* xt = ws + ws_layout(ctx, w, k).xt;
-        CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, w->bn == kBNW ? kRTT : kBM, xt, s), "slice X");
+        // X rows per tile: 128, or 256 / S_x in the transposed orientation
+        const uint32_t rt = w->bn == kBNW ? 256 / sx_of(ctx->rns.ell) : kBM;
+        CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, rt, xt, s), "slice X");
         prof_mark(ctx, s);
         CK(launch_cop_tcgen05(ctx, w, xt, k, d_C, s), "cop tcgen05");
     } else {
         prof_mark(ctx, s);
-        CK(launch_cop_cudacore(ctx, w, d_X, k, d_C, s), "cop cudacore");
+        CK(launch_cop_cudacore(ctx, w, static_cast<const uint32_t*>(d_X), k, d_C, s), "cop cudacore");
     }
     return NIMBUS_OK;
 }
 
 nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                     uint32_t* d_C, void* d_ws, size_t ws_bytes, void* stream) {
-    nimbus_status st = check_online(ctx, w, k, 1);
+    nimbus_status st = want_width(ctx, 4);
+    if (st != NIMBUS_OK) return st;
+    st = check_online(ctx, w, k, 1);
     if (st != NIMBUS_OK && st != NIMBUS_ENOISE) return st;
     if (!d_X || !d_C || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
     if (ws_bytes < ws_layout(ctx, w, k).total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
@@ -413,14 +477,15 @@ nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
 
 nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                               uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* stream) {
+    if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;
     if (!ctx || !d_C || !d_cts || !d_R || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
     CK(launch_pack(ctx, d_C, kq, nq, n, seed, d_cts, d_R, (cudaStream_t)stream, true), "pack");
     return NIMBUS_OK;
 }
 
-nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t kq,
-                                uint32_t nq, uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* d_ws,
+static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const void* d_X, uint32_t kq,
+                                uint32_t nq, uint64_t seed, uint32_t* d_cts, void* d_R, void* d_ws,
                                 size_t ws_bytes, void* stream) {
     nimbus_status st = check_online(ctx, w, kq, nq);
     if (st != NIMBUS_OK) return st;
@@ -438,6 +503,20 @@ nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uin
     CK(launch_pack(ctx, C, kq, nq, w->n, seed, d_cts, d_R, s, true), "pack");
     prof_mark(ctx, s);
     return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t kq,
+                                uint32_t nq, uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* d_ws,
+                                size_t ws_bytes, void* stream) {
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream);
+}
+
+nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* d_X, uint32_t kq,
+                                    uint32_t nq, uint64_t seed, uint32_t* d_cts, uint64_t* d_R, void* d_ws,
+                                    size_t ws_bytes, void* stream) {
+    nimbus_status st = want_width(ctx, 8);
+    return st != NIMBUS_OK ? st : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream);
 }
 
 // ---------------------------------------------------------------- batched online path
@@ -462,6 +541,7 @@ nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbu
 nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                       size_t ws_bytes, void* stream) {
     if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;
     for (uint32_t i = 0; i < count; i++) {
         nimbus_status st = check_online(ctx, jobs[i].encw, jobs[i].k_per_query, jobs[i].n_queries);
         if (st != NIMBUS_OK) return st;
@@ -633,34 +713,49 @@ nimbus_status nimbus_profile_read(nimbus_ctx* ctx, double* ms, uint64_t* calls, 
     return NIMBUS_OK;
 }
 
-nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* h_X, uint32_t kq,
-                                     uint32_t nq, uint64_t seed, uint32_t* h_cts, uint32_t* h_R, void* d_ws,
+static nimbus_status cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, const void* h_X, uint32_t kq,
+                                     uint32_t nq, uint64_t seed, uint32_t* h_cts, void* h_R, void* d_ws,
                                      size_t ws_bytes, void* stream) {
     nimbus_status st = check_online(ctx, w, kq, nq);
     if (st != NIMBUS_OK) return st;
     if (!h_X || !h_cts || !h_R || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
     const uint32_t k = kq * nq;
+    const size_t es = elem_bytes(ctx->rns.ell);
     const WsLayout L = ws_layout(ctx, w, k);
     if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t* ws = (uint8_t*)d_ws;
-    uint32_t* dX = reinterpret_cast<uint32_t*>(ws + L.stage_x);
+    void* dX = ws + L.stage_x;
     uint32_t* dcts = reinterpret_cast<uint32_t*>(ws + L.stage_cts);
-    uint32_t* dR = reinterpret_cast<uint32_t*>(ws + L.stage_r);
+    void* dR = ws + L.stage_r;
     uint32_t nct = 0;
     nimbus_cop_out_count(ctx, kq, w->n, &nct);
     const size_t cts_bytes = (size_t)nq * nct * 2 * ctx->rns.L_out * ctx->rns.N * 4;
-    CK(cudaMemcpyAsync(dX, h_X, (size_t)k * w->m * 4, cudaMemcpyHostToDevice, s), "h2d X");
-    st = nimbus_cop_matmul(ctx, w, dX, kq, nq, seed, dcts, dR, d_ws, ws_bytes, stream);
+    CK(cudaMemcpyAsync(dX, h_X, (size_t)k * w->m * es, cudaMemcpyHostToDevice, s), "h2d X");
+    st = cop_matmul(ctx, w, dX, kq, nq, seed, dcts, dR, d_ws, ws_bytes, stream);
     if (st != NIMBUS_OK) return st;
     CK(cudaMemcpyAsync(h_cts, dcts, cts_bytes, cudaMemcpyDeviceToHost, s), "d2h cts");
-    CK(cudaMemcpyAsync(h_R, dR, (size_t)k * w->n * 4, cudaMemcpyDeviceToHost, s), "d2h R");
+    CK(cudaMemcpyAsync(h_R, dR, (size_t)k * w->n * es, cudaMemcpyDeviceToHost, s), "d2h R");
     CK(cudaStreamSynchronize(s), "host matmul sync");
     return NIMBUS_OK;
 }
 
-nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
-                             uint32_t n, uint32_t* d_Z, uint32_t* d_M, void* stream) {
+nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* h_X, uint32_t kq,
+                                     uint32_t nq, uint64_t seed, uint32_t* h_cts, uint32_t* h_R, void* d_ws,
+                                     size_t ws_bytes, void* stream) {
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
+}
+
+nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* h_X, uint32_t kq,
+                                         uint32_t nq, uint64_t seed, uint32_t* h_cts, uint64_t* h_R, void* d_ws,
+                                         size_t ws_bytes, void* stream) {
+    nimbus_status st = want_width(ctx, 8);
+    return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
+}
+
+static nimbus_status decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
+                             uint32_t n, void* d_Z, void* d_M, void* stream) {
     if (!ctx || !sk || !d_cts || !d_Z || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
     cudaStream_t s = (cudaStream_t)stream;
@@ -674,9 +769,22 @@ nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_
     return NIMBUS_OK;
 }
 
+nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
+                             uint32_t n, uint32_t* d_Z, uint32_t* d_M, void* stream) {
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, nq, n, d_Z, d_M, stream);
+}
+
+nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq,
+                                 uint32_t nq, uint32_t n, uint64_t* d_Z, uint64_t* d_M, void* stream) {
+    nimbus_status st = want_width(ctx, 8);
+    return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, nq, n, d_Z, d_M, stream);
+}
+
 // ---------------------------------------------------------------- server, step 5
 nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_t m, uint32_t n, void* stream,
                                    nimbus_plainw** out) {
+    if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;          // server GEMM: ell <= 32
     if (!ctx || !d_W || !out || m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     nimbus_plainw* w = new (std::nothrow) nimbus_plainw();
     if (!w) return set_err(ctx, NIMBUS_ENOMEM, "host alloc");

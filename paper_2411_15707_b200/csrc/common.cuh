@@ -5,7 +5,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#define NIMBUS_MAXL 4
+#define NIMBUS_MAXL 6
 
 namespace nimbus {
 
@@ -19,9 +19,9 @@ struct Rns {
     uint32_t inv_p_sh[NIMBUS_MAXL][NIMBUS_MAXL];  // Shoup companions floor(inv_p * 2^32 / p_i)
     uint32_t t_inv[NIMBUS_MAXL];         // t^-1 mod p_i                 (embedding)
     uint32_t t_inv_sh[NIMBUS_MAXL];      // floor(t_inv * 2^32 / p_i)
-    uint32_t q_mod_t;                    // q mod t, q = prod of all L primes
-    uint32_t qout_mod_t;                 // q' mod t, q' = prod of the first L_out primes
-    uint32_t pow8[NIMBUS_MAXL][8];       // 2^(8s) mod p_i                (slice recombination)
+    uint64_t q_mod_t;                    // q mod t, q = prod of all L primes (t = 2^ell <= 2^64)
+    uint64_t qout_mod_t;                 // q' mod t, q' = prod of the first L_out primes
+    uint32_t pow8[NIMBUS_MAXL][12];      // 2^(8s) mod p_i, s < S_x + 3   (slice recombination)
     uint32_t c32[NIMBUS_MAXL];           // 2^32 mod p_i (< 2^21 required by reduce64_pm)
     uint32_t ninv[NIMBUS_MAXL], ninv_sh[NIMBUS_MAXL];  // N^-1 mod p_i and its Shoup companion
 };
@@ -95,14 +95,15 @@ __device__ __forceinline__ uint32_t reduce64_pm(uint64_t x, uint32_t p, uint32_t
 
 // Emb(w) mod p_i for w in [0,t): floor((Q w + t/2)/t) = (Q w + t/2 - f)/t with
 // f = (Q w + t/2) mod t; since p_i | Q this is (t/2 - f) * t^-1 mod p_i.
-// (SURVEY.md §8(c) #4.)  qmodt = Q mod t.
-__device__ __forceinline__ uint32_t emb_mod(uint32_t w, uint32_t qmodt, uint32_t ell, uint32_t p,
+// (SURVEY.md §8(c) #4.)  qmodt = Q mod t.  All arithmetic mod 2^64, so ell = 64
+// (the paper's t) is the same formula with the mask omitted.
+__device__ __forceinline__ uint32_t emb_mod(uint64_t w, uint64_t qmodt, uint32_t ell, uint32_t p,
                                             uint64_t mu, uint32_t tinv) {
-    const uint64_t t = 1ULL << ell;
-    uint64_t f = ((uint64_t)qmodt * w + (t >> 1)) & (t - 1);
-    int64_t d = (int64_t)(t >> 1) - (int64_t)f;        // in (-t/2, t/2]
-    uint64_t dm = (uint64_t)(d + 2 * (int64_t)p);        // p > 2^30 >= |d|/2 ... d + 2p > 0
-    uint32_t dr = mod64(dm, p, mu);
+    const uint64_t half = 1ULL << (ell - 1);
+    const uint64_t tmask = ell >= 64 ? ~0ULL : (half << 1) - 1;
+    const uint64_t f = (qmodt * w + half) & tmask;
+    // (t/2 - f) mod p, |t/2 - f| <= t/2
+    const uint32_t dr = f <= half ? mod64(half - f, p, mu) : (p - mod64(f - half, p, mu)) % p;
     return mulmod(dr, tinv, p, mu);
 }
 

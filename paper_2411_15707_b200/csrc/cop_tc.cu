@@ -443,13 +443,15 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
 // outputs, against 64 KB of X + 24 KB of E for 6144 in the streaming kernel:
 // the L2->SM delivery rate is what bounds ell = 32.  The epilogue thread owns
 // one coefficient column and writes rows, so stores are coalesced across lanes.
+template <int SX_>
 struct TCfgT {
-    static constexpr uint32_t BM = kBNW, RT = kRTT, BK = kBK, SX = 4;
+    static constexpr uint32_t BM = kBNW, RT = 256 / SX_, BK = kBK, SX = SX_;   // ell = 32: 64 rows; ell = 64: 32
     static constexpr uint32_t A_BYTES = kSW * BM * BK;     // 64 KB: 4 planes x 128 columns x 128 B
     static constexpr uint32_t B_BYTES = SX * RT * BK;      // 32 KB: 4 slices x 64 rows x 128 B
     static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
     static constexpr uint32_t STAGES = 2;
-    static constexpr uint32_t NACC = SX + kSW - 1;         // 7 accumulators x 64 columns = 448
+    static constexpr uint32_t NACC = SX + kSW - 1;         // 7 x 64 or 11 x 32 TMEM columns
+    static constexpr uint32_t EPI_BATCH = NACC <= 7 ? 2 : 1;   // 8-row chunks per tcgen05.ld wait (registers)
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t EPI_WARPS = 8;
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
@@ -458,10 +460,11 @@ struct TCfgT {
     static_assert(SMEM <= 232448, "shared memory");
 };
 
-__global__ void __launch_bounds__(TCfgT::THREADS, 1)
+template <int SX>
+__global__ void __launch_bounds__(TCfgT<SX>::THREADS, 1)
 k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t RTt,
            uint32_t CT, uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
-    using Cfg = TCfgT;
+    using Cfg = TCfgT<SX>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
@@ -534,7 +537,7 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
                             if ((kb | kk) != 0 || j == 0) {
                                 mma_i8_ss(tmem + j * Cfg::RT, ad, bd, idesc_full, (kb | kk) != 0);
                             } else {
-                                // first k-step, j >= 1: acc_j..acc_{j+2} exist, acc_{j+3} is new
+                                // first k-step, j >= 1: acc_j..acc_{j+SX-2} exist, acc_{j+SX-1} is new
                                 mma_i8_ss(tmem + j * Cfg::RT, ad, bd, idesc_lo, 1u);
                                 const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (Cfg::SX - 1) * Cfg::RT * Cfg::BK + kk * 32);
                                 mma_i8_ss(tmem + (j + Cfg::SX - 1) * Cfg::RT, ad, bd3, idesc_one, 0u);
@@ -551,6 +554,7 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
         // ---------------- epilogue: lane = coefficient column, 8 rows per tcgen05.ld
         const uint32_t ew = warp - 4;
         const uint32_t sub = ew & 3, half = ew >> 2;
+        constexpr uint32_t HR = Cfg::RT / 2, CH = HR / 8, B = Cfg::EPI_BATCH;   // rows per half, chunks
         uint32_t ti = 0;
         for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
             const uint32_t rt = u % RTt, ct = u / RTt;
@@ -560,20 +564,21 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
             const uint32_t col = ct * Cfg::BM + sub * 32 + lane;
             const uint32_t limb = (col / R.N) % R.L;
             const uint32_t p = R.p[limb], c32 = R.c32[limb];
-            const uint32_t tbase = tmem + ((sub * 32) << 16) + half * 32;
+            const uint32_t tbase = tmem + ((sub * 32) << 16) + half * HR;
 #pragma unroll 1
-            for (uint32_t c0 = 0; c0 < 4; c0 += 2) {
-                uint32_t v[2][Cfg::NACC][8];
+            for (uint32_t c0 = 0; c0 < CH; c0 += B) {
+                uint32_t v[B][Cfg::NACC][8];
 #pragma unroll
-                for (uint32_t b = 0; b < 2; b++)
+                for (uint32_t b = 0; b < B; b++)
 #pragma unroll
                     for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld8(tbase + s * Cfg::RT + (c0 + b) * 8, v[b][s]);
                 tmem_ld_wait();
 #pragma unroll
-                for (uint32_t b = 0; b < 2; b++) {
+                for (uint32_t b = 0; b < B; b++) {
 #pragma unroll
                     for (uint32_t q = 0; q < 8; q++) {
-                        const uint32_t row = rt * Cfg::RT + half * 32 + (c0 + b) * 8 + q;
+                        const uint32_t row = rt * Cfg::RT + half * HR + (c0 + b) * 8 + q;
+                        // s < 4 exact (< 2^55), s >= 4 as acc_s (2^(8s) mod p): the sum stays < 2^64
                         uint64_t x = mad_wide(v[b][1][q], 1u << 8, v[b][0][q]);
                         x = mad_wide(v[b][2][q], 1u << 16, x);
                         x = mad_wide(v[b][3][q], 1u << 24, x);
@@ -653,19 +658,22 @@ static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t
     return e;
 }
 
+template <int SX>
 static cudaError_t launch_t(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                             cudaStream_t st) {
+    using Cfg = TCfgT<SX>;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_cop_tc_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TCfgT::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_cop_tc_t<SX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)Cfg::SMEM);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    const uint32_t CT = col_tiles(c, kBNW), RTt = (k + kRTT - 1) / kRTT;
+    const uint32_t CT = col_tiles(c, kBNW), RTt = (k + Cfg::RT - 1) / Cfg::RT;
     const uint32_t nunits = CT * RTt;
     const uint32_t grid = nunits < (uint32_t)c->num_sms ? nunits : (uint32_t)c->num_sms;
-    cudaError_t e = launch_pdl(k_cop_tc_t, dim3(grid), dim3(TCfgT::THREADS), TCfgT::SMEM, st, c->rns, d_Xt,
+    cudaError_t e = launch_pdl(k_cop_tc_t<SX>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, c->rns, d_Xt,
                                (const uint8_t*)w->d_Et, k, RTt, CT, w->KB, ncol, d_C);
     c->launches++;
     return e;
@@ -681,9 +689,11 @@ cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_
                                uint32_t* d_C, cudaStream_t st) {
     const uint32_t SX = sx_of(c->rns.ell);
     if (w->bn == kBNW) {
-        if (SX != 4) return cudaErrorInvalidValue;
-        return launch_t(c, w, d_Xt, k, d_C, st);
+        if (SX == 4) return launch_t<4>(c, w, d_Xt, k, d_C, st);
+        if (SX == 8) return launch_t<8>(c, w, d_Xt, k, d_C, st);
+        return cudaErrorInvalidValue;
     }
+    if (SX == 8) return cudaErrorInvalidValue;    // 8 slices only in the transposed orientation
     if (w->bn == kBNR) {
         if (SX == 2 && k <= kBM && w->KB <= kResMaxKB) return launch_res(c, w, d_Xt, k, d_C, st);
         switch (SX) {

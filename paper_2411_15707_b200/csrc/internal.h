@@ -21,11 +21,17 @@ constexpr uint32_t kResMaxKB = 6;  // resident-X kernel: at most 6 k-blocks (m <
 constexpr uint32_t kBM = 128;      // rows (alpha) per X tile = tcgen05 M
 constexpr uint32_t kSW = 4;        // 8-bit slices of a 31-bit residue (S_w)
 
+// unsigned big integer (6 x 64 bits, little-endian): q beyond 128 bits for ell = 64
+struct Big {
+    uint64_t w[6] = {0, 0, 0, 0, 0, 0};
+};
+
 struct nimbus_ctx {
     nimbus_params prm{};
     int device = 0;
     nimbus::Rns rns{};
-    u128 q = 0, qout = 0;
+    Big q;                         // q = prod of all L primes (up to 6 x 31 bits)
+    u128 qout = 0;                 // q' = prod of the first L_out primes (< 2^95)
     uint32_t* d_tw = nullptr;      // per limb 4 x N: psi_rev, psi_rev_shoup, ipsi_rev, ipsi_rev_shoup
     uint32_t* d_flag = nullptr;    // device error flags (bit 0: input >= t)
     std::string err;
@@ -68,7 +74,9 @@ struct nimbus_plainw {
 };
 
 // number of 8-bit slices of an ell-bit X entry (S_x)
-inline uint32_t sx_of(uint32_t ell) { return ell <= 8 ? 1 : ell <= 16 ? 2 : 4; }
+inline uint32_t sx_of(uint32_t ell) { return ell <= 8 ? 1 : ell <= 16 ? 2 : ell <= 32 ? 4 : 8; }
+// bytes of one X / W / R / Z element at the boundary: uint32 up to ell = 32, uint64 beyond
+inline uint32_t elem_bytes(uint32_t ell) { return ell <= 32 ? 4u : 8u; }
 // number of 48-column Enc(W) tiles covering the 2 L N coefficient columns (last one zero padded)
 // (rounded up to an even count so column tiles pair up in 2-CTA clusters)
 inline uint32_t col_tiles(const nimbus_ctx* c, uint32_t bn) { return (((2 * c->rns.L * c->rns.N + bn - 1) / bn) + 1) & ~1u; }
@@ -77,13 +85,13 @@ inline uint32_t col_tiles(const nimbus_ctx* c, uint32_t bn) { return (((2 * c->r
 namespace nimbus {
 // ntt.cu
 cudaError_t launch_keygen(nimbus_ctx* c, uint64_t seed, int8_t* d_s, uint32_t* d_s_ntt, cudaStream_t st);
-cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* d_W, uint32_t m,
+cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const void* d_W, uint32_t m,
                            uint32_t n, uint64_t seed, uint32_t* d_encW, cudaStream_t st);
 cudaError_t launch_negacyclic_mul(nimbus_ctx* c, const uint32_t* a, const uint32_t* b, uint32_t count,
                                   uint32_t* out, cudaStream_t st);
 cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* cts, uint32_t nct_total,
-                           uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, uint32_t* d_Z,
-                           uint32_t* d_M, cudaStream_t st);
+                           uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, void* d_Z,
+                           void* d_M, cudaStream_t st);
 cudaError_t launch_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* out,
                              cudaStream_t st);
 // layout.cu
@@ -91,10 +99,10 @@ cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m,
                              uint8_t* d_Et, cudaStream_t st);
 cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t bn,
                                uint32_t* d_canon, cudaStream_t st);
-cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
+cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st);
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
-                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl);
+                        uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl);
 // cop_cc.cu
 cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                 uint32_t* d_C, cudaStream_t st);

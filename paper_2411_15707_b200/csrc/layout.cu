@@ -13,14 +13,14 @@
 
 namespace nimbus {
 
-template <int SX, int RT>
-__global__ void k_slice_x(const uint32_t* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB, uint32_t ell,
+template <int SX, int RT, typename T = uint32_t>
+__global__ void k_slice_x(const T* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB, uint32_t ell,
                           uint8_t* __restrict__ Xt, uint32_t total, uint32_t* flag, int check) {
     pdl_trigger();
     pdl_wait();          // Xt may still be read by the previous contraction in the stream
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= total) return;
-    slice_item<SX, RT>(X, k, m, KB, ell, Xt, idx, flag, check);
+    slice_item<SX, RT, T>(X, k, m, KB, ell, Xt, idx, flag, check);
 }
 
 // ---------------------------------------------------------------- tile Enc(W)
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) k_untile_encw(const uint8_t* __restrict__
 }
 
 // ---------------------------------------------------------------- launchers
-cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
+cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_Xv, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st) {
     const uint32_t Mt = (k + rt - 1) / rt;
     const uint32_t total = Mt * rt * KB * 8;
@@ -86,7 +86,12 @@ cudaError_t launch_slice_x(nimbus_ctx* c, const uint32_t* d_X, uint32_t k, uint3
     dim3 g((total + 255) / 256);
     cudaError_t e;
     const uint32_t ell = c->rns.ell;
-    if (rt == 64) e = launch_pdl(k_slice_x<4, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
+    const uint32_t* d_X = static_cast<const uint32_t*>(d_Xv);
+    if (SX == 8) {
+        const int check64 = (c->prm.flags & NIMBUS_FLAG_CHECK_RANGE) && ell < 64;
+        e = launch_pdl(k_slice_x<8, 32, uint64_t>, g, 256, 0, st, static_cast<const uint64_t*>(d_Xv), k, m, KB, ell,
+                       d_Xt, total, c->d_flag, check64);
+    } else if (rt == 64) e = launch_pdl(k_slice_x<4, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
     else if (SX == 1) e = launch_pdl(k_slice_x<1, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
     else if (SX == 2) e = launch_pdl(k_slice_x<2, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
     else e = launch_pdl(k_slice_x<4, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);

@@ -137,7 +137,8 @@ __global__ void k_keygen(Rns R, const uint32_t* d_tw, uint64_t seed, int8_t* s, 
 //   b = a*s + Emb_q(w_hat) + e mod p_i, e = CBD(21) (domain 3, index beta N + j),
 //   w_hat[j] = W[beta][j] for j < n else 0 (Eq. 2).
 // Writes the canonical layout encW[beta][comp][limb][j].
-__global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, const uint32_t* W,
+template <typename T>
+__global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, const T* W,
                           uint32_t n, uint64_t seed, uint32_t* encW) {
     extern __shared__ uint32_t sa[];
     const uint32_t N = R.N, L = R.L, beta = blockIdx.x, i = blockIdx.y, p = R.p[i];
@@ -160,7 +161,7 @@ __global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, co
     __syncthreads();
     ntt_inv_smem(sa, tw.iv, tw.iv_sh, N, R.logN, p, R.ninv[i], R.ninv_sh[i]);
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
-        uint32_t w = j < n ? W[(size_t)beta * n + j] : 0u;
+        const uint64_t w = j < n ? (uint64_t)W[(size_t)beta * n + j] : 0u;
         int32_t e = samp_cbd21(prg_word(ke, (uint64_t)beta * N + j));
         uint32_t em = emb_mod(w, R.q_mod_t, R.ell, p, mu, R.t_inv[i]);
         uint32_t er = e < 0 ? p - (uint32_t)(-e) : (uint32_t)e;
@@ -295,9 +296,12 @@ __global__ void __launch_bounds__(256) k_decrypt_cl(Rns R, const uint32_t* d_tw,
 
 // CRT (Garner) of u_0..u_{Lo-1} and m = floor((2 t u + q') / (2 q')) mod t
 // (SURVEY.md §8(c) #5); unpack Z[alpha][j] = m_theta[(alpha mod R) n + j].
+// The division is exact long division in 32-bit steps on 128-bit words
+// (u < q' < 2^95, t <= 2^64: 2 t u alone can exceed 128 bits).  T = uint32_t,
+// or uint64_t for ell > 32.
+template <typename T>
 __global__ void k_decrypt_round(Rns R, const uint32_t* U, uint32_t nct, uint32_t kq, uint32_t n,
-                                uint32_t* Z, uint32_t* M, u128 qout, uint32_t garner0, uint32_t garner1,
-                                uint32_t garner2) {
+                                T* Z, T* M, u128 qout, uint32_t garner0, uint32_t garner1) {
     const uint32_t N = R.N, Lo = R.L_out, tg = blockIdx.y;
     const uint32_t J = blockIdx.x * blockDim.x + threadIdx.x;
     if (J >= N) return;
@@ -320,18 +324,20 @@ __global__ void k_decrypt_round(Rns R, const uint32_t* U, uint32_t nct, uint32_t
             u += (u128)R.p[0] * R.p[1] * v2;
         }
     }
-    (void)garner2;
     const uint32_t ell = R.ell;
-    // m~ = floor((2 t u + q') / (2 q')): estimate in double, then correct exactly
-    const u128 num = (u << (ell + 1)) + qout;
+    // u 2^(ell+1) = Q (2 q') + r by shifting the remainder 32 bits at a time (r < 2q' < 2^96)
     const u128 den = qout << 1;
-    double est = ((double)(uint64_t)(u >> 64) * 18446744073709551616.0 + (double)(uint64_t)u) *
-                 (double)(1ULL << ell) / ((double)(uint64_t)(qout >> 64) * 18446744073709551616.0 +
-                                          (double)(uint64_t)qout);
-    uint64_t mt = (uint64_t)(est + 0.5);
-    while ((u128)mt * den > num) mt--;
-    while ((u128)(mt + 1) * den <= num) mt++;
-    const uint32_t m = (uint32_t)(mt & ((1ULL << ell) - 1));
+    u128 Q = 0, r = u;
+    for (uint32_t S = ell + 1; S > 0;) {
+        const uint32_t sh = S < 32 ? S : 32;
+        r <<= sh;
+        Q = (Q << sh) + r / den;
+        r %= den;
+        S -= sh;
+    }
+    Q += (r + qout) / den;                                  // + q', then floor
+    const uint64_t tmask = ell >= 64 ? ~0ULL : ((1ULL << ell) - 1);
+    const T m = (T)((uint64_t)Q & tmask);
     if (M) M[(size_t)tg * N + J] = m;
     const uint32_t Rr = N / n, theta = tg % nct, query = tg / nct;
     const uint32_t rows = min(Rr, kq - theta * Rr);
@@ -363,10 +369,15 @@ cudaError_t launch_keygen(nimbus_ctx* c, uint64_t seed, int8_t* d_s, uint32_t* d
     return cudaGetLastError();
 }
 
-cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* d_W, uint32_t m,
+cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const void* d_W, uint32_t m,
                            uint32_t n, uint64_t seed, uint32_t* d_encW, cudaStream_t st) {
     const uint32_t N = c->rns.N;
-    k_encrypt<<<dim3(m, c->rns.L), ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, d_s_ntt, d_W, n, seed, d_encW);
+    if (elem_bytes(c->rns.ell) == 8)
+        k_encrypt<uint64_t><<<dim3(m, c->rns.L), ntt_threads(N), N * 4, st>>>(
+            c->rns, c->d_tw, d_s_ntt, static_cast<const uint64_t*>(d_W), n, seed, d_encW);
+    else
+        k_encrypt<uint32_t><<<dim3(m, c->rns.L), ntt_threads(N), N * 4, st>>>(
+            c->rns, c->d_tw, d_s_ntt, static_cast<const uint32_t*>(d_W), n, seed, d_encW);
     c->launches++;
     return cudaGetLastError();
 }
@@ -383,8 +394,8 @@ cudaError_t launch_negacyclic_mul(nimbus_ctx* c, const uint32_t* a, const uint32
 }
 
 cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* cts, uint32_t nct_total,
-                           uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, uint32_t* d_Z,
-                           uint32_t* d_M, cudaStream_t st) {
+                           uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, void* d_Z,
+                           void* d_M, cudaStream_t st) {
     const uint32_t N = c->rns.N;
     {
         // one 4-CTA cluster per (ciphertext, limb), a quarter of the coefficients each
@@ -416,8 +427,13 @@ cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_
     };
     uint32_t g0 = R.L_out >= 2 ? inv(R.p[0], R.p[1]) : 0;
     uint32_t g1 = R.L_out >= 3 ? inv((uint64_t)R.p[0] * R.p[1] % R.p[2], R.p[2]) : 0;
-    k_decrypt_round<<<dim3((N + 255) / 256, nct_total), 256, 0, st>>>(c->rns, d_u_tmp, nct, kq, n, d_Z, d_M,
-                                                                     c->qout, g0, g1, 0);
+    const dim3 gr((N + 255) / 256, nct_total);
+    if (elem_bytes(c->rns.ell) == 8)
+        k_decrypt_round<uint64_t><<<gr, 256, 0, st>>>(c->rns, d_u_tmp, nct, kq, n, static_cast<uint64_t*>(d_Z),
+                                                      static_cast<uint64_t*>(d_M), c->qout, g0, g1);
+    else
+        k_decrypt_round<uint32_t><<<gr, 256, 0, st>>>(c->rns, d_u_tmp, nct, kq, n, static_cast<uint32_t*>(d_Z),
+                                                      static_cast<uint32_t*>(d_M), c->qout, g0, g1);
     c->launches++;
     return cudaGetLastError();
 }

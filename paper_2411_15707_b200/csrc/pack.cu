@@ -18,15 +18,15 @@
 
 namespace nimbus {
 
-template <int V, int L, int RB>
+template <int V, int L, int RB, typename MT = uint32_t>
 __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                               uint32_t Rr, uint32_t nct, uint64_t key_mask,
-                                              uint32_t* __restrict__ cts, uint32_t* __restrict__ Rout) {
+                                              uint32_t* __restrict__ cts, MT* __restrict__ Rout) {
     pdl_trigger();
     const uint32_t J = (blockIdx.x * blockDim.x + threadIdx.x) * V;
     if (J >= Rn.N) return;
     pdl_wait();  // C is produced by the contraction kernel
-    pack_item<V, L, RB>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, blockIdx.y, blockIdx.z, J);
+    pack_item<V, L, RB, MT>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, blockIdx.y, blockIdx.z, J);
 }
 
 template <typename K, typename... Args>
@@ -38,16 +38,35 @@ static cudaError_t launch_maybe_pdl(bool pdl, K kernel, dim3 grid, dim3 block, c
 
 template <int V, int RB>
 static cudaError_t launch_vr(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                             uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
+                             uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     const uint32_t per_block = 128 * V;
     dim3 grid((N + per_block - 1) / per_block, nq * nct, 2);
     const uint64_t key = prg_key(seed, 6);
+    uint32_t* d_R = static_cast<uint32_t*>(d_Rv);
     switch (c->rns.L) {
         case 1: return launch_maybe_pdl(pdl, k_pack<V, 1, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
         case 2: return launch_maybe_pdl(pdl, k_pack<V, 2, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
         case 3: return launch_maybe_pdl(pdl, k_pack<V, 3, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        default: return launch_maybe_pdl(pdl, k_pack<V, 4, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 4: return launch_maybe_pdl(pdl, k_pack<V, 4, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 5: return launch_maybe_pdl(pdl, k_pack<V, 5, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        default: return launch_maybe_pdl(pdl, k_pack<V, 6, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+    }
+}
+
+// ell > 32: 64-bit masks and R, one coefficient per thread, L in {4, 5, 6}
+template <int RB>
+static cudaError_t launch_r64(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
+                              uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl) {
+    const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
+    dim3 grid((N + 127) / 128, nq * nct, 2);
+    const uint64_t key = prg_key(seed, 6);
+    uint64_t* d_R = static_cast<uint64_t*>(d_Rv);
+    switch (c->rns.L) {
+        case 4: return launch_maybe_pdl(pdl, k_pack<1, 4, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 5: return launch_maybe_pdl(pdl, k_pack<1, 5, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 6: return launch_maybe_pdl(pdl, k_pack<1, 6, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        default: return cudaErrorInvalidValue;
     }
 }
 
@@ -60,9 +79,20 @@ static uint32_t rows_per_batch(uint32_t Rr, uint32_t kq) {
     return 8;
 }
 
+static cudaError_t launch_64(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
+                             uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl) {
+    switch (rows_per_batch(c->rns.N / n, kq)) {
+        case 1: return launch_r64<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 2: return launch_r64<2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 4: return launch_r64<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 5: return launch_r64<5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        default: return launch_r64<8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+    }
+}
+
 template <int V>
 static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                            uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
+                            uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl) {
     switch (rows_per_batch(c->rns.N / n, kq)) {
         case 1: return launch_vr<V, 1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
         case 2: return launch_vr<V, 2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
@@ -73,7 +103,12 @@ static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uin
 }
 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
-                        uint64_t seed, uint32_t* d_cts, uint32_t* d_R, cudaStream_t st, bool pdl) {
+                        uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl) {
+    if (elem_bytes(c->rns.ell) == 8) {
+        cudaError_t e = launch_64(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        c->launches++;
+        return e;
+    }
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     // 4 coefficients per thread when the RShift stride allows it and the grid stays
     // at >= 8 blocks of 128 per SM: in the PDL chain the pack runs alone after the

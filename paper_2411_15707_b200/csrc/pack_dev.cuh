@@ -62,10 +62,12 @@ struct VecU32<4> {
 // ciphertext tg (all limbs).  RB rows of loads are in flight per batch; the host
 // picks RB to fit R = floor(N/n) (1 for C3, 5 for C2, ...) so that few load slots
 // are predicated off -- the kernel is issue-bound, not bandwidth-bound.
-template <int V, int L, int RB>
+// MT: element type of the mask / R (uint64_t for ell > 32, then V = 1).
+template <int V, int L, int RB, typename MT = uint32_t>
 __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                           uint32_t Rr, uint32_t nct, uint64_t key_mask, uint32_t* __restrict__ cts,
-                                          uint32_t* __restrict__ Rout, uint32_t tg, uint32_t comp, uint32_t J) {
+                                          MT* __restrict__ Rout, uint32_t tg, uint32_t comp, uint32_t J) {
+    static_assert(sizeof(MT) == 4 || V == 1, "64-bit masks: one coefficient per thread");
     const uint32_t N = Rn.N, Lo = Rn.L_out;
     const uint32_t query = tg / nct, theta = tg - query * nct;
     const uint32_t rows = min(Rr, kq - theta * Rr);
@@ -107,12 +109,16 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
             }
         }
     }
-    uint32_t rmask[V];
+    MT rmask[V];
     if (comp == 0) {
-        // word(seed, 6, i) = mix64(key + golden (i + 1)) for i = tg N + J + u: one multiply, then steps
+        // word(seed, 6, i) = mix64(key + golden (i + 1)) for i = tg N + J + u: one multiply, then steps;
+        // r = word >> (64 - ell)
         uint64_t z = key_mask + 0x9E3779B97F4A7C15ULL * ((uint64_t)tg * N + J + 1);
 #pragma unroll
-        for (int u = 0; u < V; u++, z += 0x9E3779B97F4A7C15ULL) rmask[u] = samp_mod_t(mix64(z), Rn.ell);
+        for (int u = 0; u < V; u++, z += 0x9E3779B97F4A7C15ULL) {
+            const uint64_t w = mix64(z);
+            rmask[u] = (MT)(Rn.ell >= 64 ? w : w >> (64 - Rn.ell));
+        }
     }
     uint32_t out[L][V];
 #pragma unroll
@@ -142,11 +148,14 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
 #pragma unroll
             for (int i = 0; i < L; i++)
                 if ((uint32_t)i < Lo)
-                    res[i] = submod(res[i], Rn.ell <= 16
-                                                ? emb_fast16(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
-                                                             Rn.t_inv_sh[i])
-                                                : emb_fast(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.t_inv[i],
-                                                           Rn.t_inv_sh[i]), Rn.p[i]);
+                    res[i] = submod(res[i], sizeof(MT) == 8
+                                                ? emb_mod(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.mu[i],
+                                                          Rn.t_inv[i])
+                                                : Rn.ell <= 16
+                                                ? emb_fast16((uint32_t)rmask[u], (uint32_t)Rn.qout_mod_t, Rn.ell,
+                                                             Rn.p[i], Rn.t_inv[i], Rn.t_inv_sh[i])
+                                                : emb_fast((uint32_t)rmask[u], (uint32_t)Rn.qout_mod_t, Rn.ell,
+                                                           Rn.p[i], Rn.t_inv[i], Rn.t_inv_sh[i]), Rn.p[i]);
         }
 #pragma unroll
         for (int i = 0; i < L; i++) out[i][u] = res[i];
@@ -154,7 +163,11 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
 #pragma unroll
     for (int i = 0; i < L; i++)
         if ((uint32_t)i < Lo) VecU32<V>::store(cts + (((size_t)tg * 2 + comp) * Lo + i) * N + J, out[i]);
-    if (comp == 0 && J < rows * n) VecU32<V>::store(Rout + row0 * n + J, rmask);
+    if (comp == 0 && J < rows * n) {
+        if (sizeof(MT) == 8) Rout[row0 * n + J] = rmask[0];
+        else VecU32<V>::store(reinterpret_cast<uint32_t*>(Rout) + row0 * n + J,
+                              reinterpret_cast<const uint32_t(&)[V]>(rmask));
+    }
 }
 
 }  // namespace nimbus

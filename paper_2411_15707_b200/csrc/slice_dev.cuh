@@ -11,17 +11,18 @@ __device__ __forceinline__ uint32_t swz_off(uint32_t r, uint32_t chunk) {
 
 // ---------------------------------------------------------------- K4 slice X
 // X[alpha][beta] = sum_i x_i 2^(8i) (unsigned representative)
-// Xt[mt][kb][i][RT rows][128 B] (RT = 128, or 64 for the transposed ell = 32
-// kernel), zero padded to whole tiles.
-template <int SX, int RT>
-__device__ __forceinline__ void slice_item(const uint32_t* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB,
+// Xt[mt][kb][i][RT rows][128 B] (RT = 128; 64 / 32 for the transposed ell = 32 /
+// ell = 64 kernel), zero padded to whole tiles.  T = uint32_t, or uint64_t for
+// ell > 32 (S_x = 8 slices).
+template <int SX, int RT, typename T = uint32_t>
+__device__ __forceinline__ void slice_item(const T* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB,
                                            uint32_t ell, uint8_t* __restrict__ Xt, uint32_t idx, uint32_t* flag,
                                            int check) {
     const uint32_t alpha = idx / (KB * 8), ch = idx % (KB * 8);
     const uint32_t kb = ch >> 3, c16 = ch & 7;
     const uint32_t beta0 = kb * kBK + c16 * 16;
-    uint32_t v[16];
-    if (alpha < k && beta0 + 16 <= m && (m & 3) == 0) {
+    T v[16];
+    if (sizeof(T) == 4 && alpha < k && beta0 + 16 <= m && (m & 3) == 0) {
         const uint4* src = reinterpret_cast<const uint4*>(X + (size_t)alpha * m + beta0);
 #pragma unroll
         for (int q = 0; q < 4; q++) {
@@ -31,10 +32,10 @@ __device__ __forceinline__ void slice_item(const uint32_t* __restrict__ X, uint3
     } else {
 #pragma unroll
         for (int u = 0; u < 16; u++)
-            v[u] = (alpha < k && beta0 + u < m) ? X[(size_t)alpha * m + beta0 + u] : 0u;
+            v[u] = (alpha < k && beta0 + u < m) ? X[(size_t)alpha * m + beta0 + u] : (T)0;
     }
-    if (check) {
-        uint32_t bad = 0;
+    if (check && ell < 8 * sizeof(T)) {
+        T bad = 0;
 #pragma unroll
         for (int u = 0; u < 16; u++) bad |= (v[u] >> ell);
         if (bad) atomicOr(flag, 1u);

@@ -64,6 +64,10 @@ _SIGS = {
     "nimbus_cop_matmul_batch": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_profile_enable": (C.c_int, [_vp, C.c_int]),
     "nimbus_profile_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(_u64), C.c_int]),
+    "nimbus_encrypt_weights_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, C.POINTER(_vp)]),
+    "nimbus_cop_matmul_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_decrypt_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _vp]),
+    "nimbus_cop_matmul_host_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
     "nimbus_encw_offload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_reload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_is_resident": (C.c_int, [_vp]),
@@ -222,6 +226,15 @@ def nimbus_encrypt_weights(ctx: Context, sk: SecretKey, W: torch.Tensor, seed: i
     return EncW(out, ctx, m, n)
 
 
+def nimbus_encrypt_weights_u64(ctx: Context, sk: SecretKey, W: torch.Tensor, seed: int, stream=None) -> EncW:
+    """ell > 32: W is an int64 tensor holding uint64 values."""
+    m, n = W.shape
+    out = C.c_void_p()
+    _check(lib().nimbus_encrypt_weights_u64(ctx.ptr, sk.ptr, _ptr(W, torch.int64, "W"), m, n, seed,
+                                            _stream(stream), C.byref(out)), ctx)
+    return EncW(out, ctx, m, n)
+
+
 def nimbus_encw_bytes(w: EncW) -> int:
     return int(lib().nimbus_encw_bytes(w.ptr))
 
@@ -275,6 +288,23 @@ def nimbus_cop_matmul(ctx: Context, w: EncW, X: torch.Tensor, k_per_query: int, 
     _check(lib().nimbus_cop_matmul(ctx.ptr, w.ptr, _ptr(X, torch.int32, "X"), k_per_query, n_queries,
                                    mask_seed, _ptr(cts, torch.int32, "cts"), _ptr(R, torch.int32, "R"),
                                    _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return cts, R
+
+
+def alloc_outputs_u64(ctx: Context, w: EncW, k_per_query: int, n_queries: int):
+    nct = nimbus_cop_out_count(ctx, k_per_query, w.n)
+    dev = f"cuda:{ctx.device}"
+    cts = torch.empty((n_queries, nct, 2, ctx.L_out, ctx.N), dtype=torch.int32, device=dev)
+    R = torch.empty((n_queries * k_per_query, w.n), dtype=torch.int64, device=dev)
+    return cts, R
+
+
+def nimbus_cop_matmul_u64(ctx: Context, w: EncW, X: torch.Tensor, k_per_query: int, n_queries: int,
+                          mask_seed: int, cts: torch.Tensor, R: torch.Tensor, ws: torch.Tensor, stream=None):
+    """ell > 32: X and R are int64 tensors holding uint64 values."""
+    _check(lib().nimbus_cop_matmul_u64(ctx.ptr, w.ptr, _ptr(X, torch.int64, "X"), k_per_query, n_queries,
+                                       mask_seed, _ptr(cts, torch.int32, "cts"), _ptr(R, torch.int64, "R"),
+                                       _ptr(ws), ws.numel(), _stream(stream)), ctx)
     return cts, R
 
 
@@ -341,6 +371,19 @@ def nimbus_cop_matmul_host(ctx: Context, w: EncW, X_host: torch.Tensor, k_per_qu
     return cts_host, R_host
 
 
+def nimbus_cop_matmul_host_u64(ctx: Context, w: EncW, X_host: torch.Tensor, k_per_query: int,
+                               n_queries: int, mask_seed: int, cts_host: torch.Tensor,
+                               R_host: torch.Tensor, ws: torch.Tensor, stream=None):
+    for t, nm in ((X_host, "X"), (cts_host, "cts"), (R_host, "R")):
+        if t.is_cuda:
+            raise ValueError(f"{nm} must be a host tensor")
+    _check(lib().nimbus_cop_matmul_host_u64(ctx.ptr, w.ptr, _ptr(X_host, torch.int64, "X"), k_per_query,
+                                            n_queries, mask_seed, _ptr(cts_host, torch.int32, "cts"),
+                                            _ptr(R_host, torch.int64, "R"), _ptr(ws), ws.numel(),
+                                            _stream(stream)), ctx)
+    return cts_host, R_host
+
+
 def nimbus_cop_accumulate(ctx: Context, w: EncW, X: torch.Tensor, ws: torch.Tensor, C_out=None,
                           stream=None) -> torch.Tensor:
     k = X.shape[0]
@@ -372,6 +415,28 @@ def nimbus_decrypt(ctx: Context, sk: SecretKey, cts: torch.Tensor, k_per_query: 
     _check(lib().nimbus_decrypt(ctx.ptr, sk.ptr, _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
                                 n, _ptr(Z), _ptr(M) if M is not None else None, _stream(stream)), ctx)
     return Z, M
+
+
+def nimbus_decrypt_u64(ctx: Context, sk: SecretKey, cts: torch.Tensor, k_per_query: int, n_queries: int,
+                       n: int, want_full: bool = False, stream=None):
+    Z = torch.zeros((n_queries * k_per_query, n), dtype=torch.int64, device=cts.device)
+    M = None
+    if want_full:
+        nct = nimbus_cop_out_count(ctx, k_per_query, n)
+        M = torch.empty((n_queries * nct, ctx.N), dtype=torch.int64, device=cts.device)
+    _check(lib().nimbus_decrypt_u64(ctx.ptr, sk.ptr, _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
+                                    n, _ptr(Z), _ptr(M) if M is not None else None, _stream(stream)), ctx)
+    return Z, M
+
+
+def from_numpy_u64(a, device) -> torch.Tensor:
+    import numpy as np
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).to(device)
+
+
+def to_numpy_u64(t: torch.Tensor):
+    import numpy as np
+    return t.detach().cpu().contiguous().numpy().view(np.uint64)
 
 
 def nimbus_prg_words(seed: int, dom: int, start: int, count: int, device="cuda:0", stream=None):

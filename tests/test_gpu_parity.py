@@ -447,3 +447,90 @@ def test_streamed_matches_resident(nb, oracle):
     nb.nimbus_cop_matmul(ctx, jobs[0]["encw"], jobs[0]["X"], 128, 1, 60, c1, R1, ws)
     nb.nimbus_sync(ctx)
     assert torch.equal(c1, ref[0][0]) and torch.equal(R1, ref[0][1])
+
+
+# ------------------------------------------------------------------ ell = 64 (the paper's t, 5 limbs)
+def _u64(t):
+    from paper_2411_15707_b200 import nimbus
+    return nimbus.to_numpy_u64(t)
+
+
+def _dev_u64(a):
+    from paper_2411_15707_b200 import nimbus
+    return nimbus.from_numpy_u64(a, DEV)
+
+
+@pytest.mark.parametrize("N,m,n,kq,nq", [(64, 16, 20, 12, 1), (256, 130, 100, 33, 2), (128, 300, 128, 7, 1)])
+def test_ell64_parity(nb, oracle, N, m, n, kq, nq):
+    """ell = 64, q = 5 x 31-bit primes, 3-limb output: Enc(W), the
+    output ciphertexts and R bit-exact against the Python-integer oracle
+    (oracle/wide.py); decryption gives X.W - R mod 2^64 in every slot."""
+    from oracle import wide
+    L, ell, L_out = 5, 64, 3
+    seed = 0x6464 + N + m
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    pr = [int(p) for p in nb.nimbus_ctx_primes(ctx)]
+    assert pr == [int(p) for p in oracle.primes(N, L)]
+    sk = nb.nimbus_keygen(ctx, seed)
+    s = oracle.keygen(N, seed)
+    W = ni.gen_W(seed, m, n, ell)
+    X = ni.gen_X(seed ^ 0xA5, kq * nq, m, ell)
+    w = nb.nimbus_encrypt_weights_u64(ctx, sk, _dev_u64(W), seed)
+    E = wide.encrypt_rows(N, L, pr, ell, s, W, seed)
+    assert (u32(nb.nimbus_encw_export(w)) == E).all()
+    ws = nb.alloc_workspace(ctx, w, kq * nq)
+    cts, R = nb.alloc_outputs_u64(ctx, w, kq, nq)
+    nb.nimbus_cop_matmul_u64(ctx, w, _dev_u64(X), kq, nq, seed, cts, R, ws)
+    nb.nimbus_sync(ctx)
+    cts_o, R_o = wide.cop_matmul(N, L, L_out, pr, ell, E, X, n, kq, nq, seed)
+    assert (u32(cts) == cts_o).all()
+    assert (_u64(R) == R_o).all()
+    Z, _ = nb.nimbus_decrypt_u64(ctx, sk, cts, kq, nq, n)
+    Y = matmul_mod_t(X, W, ell)
+    with np.errstate(over="ignore"):
+        assert (_u64(Z) == Y - R_o).all()
+
+
+def test_ell64_full_size_decrypts(nb, oracle):
+    """C4's FFN-down shape at the paper's ell = 64 (N = 8192, 5 limbs, m = 3072,
+    k = 128): every output slot decrypts to X.W - R mod 2^64 (valid slots) or
+    -r (invalid ones)."""
+    N, L, ell, L_out, m, n, kq = 8192, 5, 64, 3, 3072, 768, 128
+    seed = ni.seed_mm(4)
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, seed)
+    W = ni.gen_W(seed, m, n, ell)
+    X = ni.gen_X(seed, kq, m, ell)
+    w = nb.nimbus_encrypt_weights_u64(ctx, sk, _dev_u64(W), seed)
+    ws = nb.alloc_workspace(ctx, w, kq)
+    cts, R = nb.alloc_outputs_u64(ctx, w, kq, 1)
+    nb.nimbus_cop_matmul_u64(ctx, w, _dev_u64(X), kq, 1, seed, cts, R, ws)
+    Z, M = nb.nimbus_decrypt_u64(ctx, sk, cts, kq, 1, n, want_full=True)
+    Y = matmul_mod_t(X, W, ell)
+    Rn = _u64(R)
+    with np.errstate(over="ignore"):
+        assert (_u64(Z) == Y - Rn).all()
+    Mn = _u64(M)
+    Rr = N // n
+    for tg in range(Mn.shape[0]):
+        rows = min(Rr, kq - tg * Rr)
+        mask = ni.prg_words(seed, 6, tg * N, N)
+        with np.errstate(over="ignore"):
+            assert (Mn[tg][rows * n:] == (np.uint64(0) - mask[rows * n:])).all()
+
+
+def test_width_guards(nb):
+    """32-bit entry points refuse ell > 32 contexts and the _u64 ones ell <= 32."""
+    c64 = nb.nimbus_ctx_create(256, 5, 64, 3)
+    sk = nb.nimbus_keygen(c64, 1)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_encrypt_weights(c64, sk, dev_u32(ni.gen_W(1, 4, 4, 16)), 1)
+    assert e.value.status == -1
+    c16 = nb.nimbus_ctx_create(256, 2, 16, 1)
+    sk16 = nb.nimbus_keygen(c16, 1)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_encrypt_weights_u64(c16, sk16, _dev_u64(ni.gen_W(1, 4, 4, 64)), 1)
+    assert e.value.status == -1
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_ctx_create(256, 5, 64, 4)          # q' would exceed 2^95
+    assert e.value.status == -1

@@ -512,3 +512,58 @@ def test_pack_is_rshift_product(oracle, N, n, k, pr):
                     emb = [int(oracle.emb(pra, ell, int(w))[l]) for w in mask]
                     acc = [(x - e) % p for x, e in zip(acc, emb)]
                 assert list(cts[0, th, comp, l]) == acc
+
+
+# ----------------------------------------------------------------- wide oracle (ell = 64, q > 2^128)
+def test_wide_oracle_equals_c_oracle(oracle):
+    """The Python-integer oracle (oracle/wide.py) follows the same steps as the C
+    oracle; where both apply (ell = 16, 2 limbs) they give the same bytes for
+    Enc(W), the output ciphertexts, R and the decrypted Z."""
+    from oracle import wide
+    N, pr, ell, L_out, k, m, n = 64, P4096, 16, 1, 7, 9, 20
+    seed = 0xBEEF
+    d = toy_pipeline(oracle, N, pr, ell, L_out, k, m, n, seed)
+    Ew = wide.encrypt_rows(N, 2, np.array(pr, np.uint32), ell, d["s"], d["W"], seed)
+    assert (Ew == d["E"]).all()
+    cts, R = wide.cop_matmul(N, 2, L_out, pr, ell, d["E"], d["X"], n, k, 1, seed)
+    assert (cts == d["cts"]).all() and (R == d["R"]).all()
+    Zw, _ = wide.decrypt_unpack(N, L_out, pr, ell, d["s"], cts, k, 1, n)
+    Zc, _, _ = oracle.decrypt_unpack(N, L_out, np.array(pr[:L_out], np.uint32), ell, d["s"], d["cts"], k, 1, n)
+    assert (Zw == Zc).all()
+
+
+@pytest.mark.parametrize("case", [dict(N=64, L=5, L_out=3, k=6, m=5, n=20, nq=1),
+                                  dict(N=128, L=5, L_out=3, k=5, m=12, n=50, nq=2)])
+def test_wide_e2e_ell64(oracle, case):
+    """The paper's ell = 64 with 5 limbs (q ~ 2^155) and a 3-limb
+    output: Dec - mask = X.W mod 2^64 by Python-integer brute force, round trip of
+    Enc(W) rows (Eq. 2), invalid slots = -r."""
+    from oracle import wide
+    c = case
+    N, L, L_out, ell = c["N"], c["L"], c["L_out"], 64
+    pr = [int(p) for p in oracle.primes(N, L)]
+    t = 1 << ell
+    seed = 0x64 + N
+    s = oracle.keygen(N, seed)
+    W = ni.gen_W(seed, c["m"], c["n"], ell)
+    X = ni.gen_X(seed, c["k"] * c["nq"], c["m"], ell)
+    assert W.dtype == np.uint64 and int(W.max()) >= (1 << 62)    # full-width entries
+    E = wide.encrypt_rows(N, L, pr, ell, s, W, seed)
+    # Dec(Enc(w_hat_beta)) = W[beta] then zeros (row-wise encoding, PAPER.md:228)
+    for beta in range(c["m"]):
+        ct = E[beta][None, None]                                  # as one packed ct with all L limbs
+        Zr, full = wide.decrypt_unpack(N, L, pr, ell, s, ct, 1, 1, N)
+        assert [int(v) for v in full[0][:c["n"]]] == [int(v) for v in W[beta]]
+        assert not full[0][c["n"]:].any()
+    cts, R = wide.cop_matmul(N, L, L_out, pr, ell, E, X, c["n"], c["k"], c["nq"], seed)
+    Z, full = wide.decrypt_unpack(N, L_out, pr, ell, s, cts, c["k"], c["nq"], c["n"])
+    Y = py_matmul_mod(X, W, t)
+    assert all(int(Z[a, j]) == (int(Y[a, j]) - int(R[a, j])) % t for a in range(Z.shape[0]) for j in range(c["n"]))
+    R_ = N // c["n"]
+    nct = -(-c["k"] // R_)
+    for tg in range(c["nq"] * nct):
+        th = tg % nct
+        rows = min(R_, c["k"] - th * R_)
+        mask = oracle.words(seed, 6, tg * N, N)
+        for J in range(rows * c["n"], N):
+            assert int(full[tg, J]) == (t - int(mask[J])) % t
