@@ -534,3 +534,40 @@ def test_width_guards(nb):
     with pytest.raises(nb.NimbusError) as e:
         nb.nimbus_ctx_create(256, 5, 64, 4)          # q' would exceed 2^95
     assert e.value.status == -1
+
+
+# ------------------------------------------------------------------ seeded random shapes
+def _fuzz_cases(count=24, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        N = int(rng.choice([64, 128, 256, 512, 1024]))
+        ell = int(rng.choice([4, 8, 12, 16, 24, 32]))
+        L = 2 if ell <= 16 else 3
+        L_out = 1 if ell <= 16 else 2
+        n = int(rng.integers(1, N + 1))
+        m = int(rng.integers(1, 400))
+        kq = int(rng.integers(1, 140))
+        nq = int(rng.integers(1, 3))
+        out.append((N, L, ell, L_out, m, n, kq, nq))
+    return out
+
+
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", _fuzz_cases())
+def test_random_shapes_parity(nb, oracle, N, L, ell, L_out, m, n, kq, nq):
+    """Seeded random (N, ell, m, n, k, queries): output ciphertexts and R bit-exact
+    vs the oracle, every slot decrypting to X.W - R mod t.  Shapes the noise bound
+    refuses must be refused with NIMBUS_ENOISE, consistently at encrypt or matmul."""
+    try:
+        c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=0xF00 + m * 7 + n)
+    except nb.NimbusError as e:
+        assert e.status == -4
+        return
+    try:
+        cts, R = c.run()
+    except nb.NimbusError as e:
+        assert e.status == -4
+        return
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+    c.check_decrypt(cts, R)
