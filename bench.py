@@ -169,7 +169,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = f"cuda:{local_rank}"
     impl = nb.IMPL_TCGEN05 if args.impl == "tcgen05" else nb.IMPL_CUDACORE
-    ctx = nb.nimbus_ctx_create(cfg.N, cfg.L, cfg.ell, cfg.L_out, impl, device=local_rank)
+    # layout hint: matmuls of >= 512 rows (C5) favour the transposed ell = 32 contraction
+    flags = nb.FLAG_LARGE_K if min(l.k for _, _, l in cfg.layers) >= 512 else 0
+    ctx = nb.nimbus_ctx_create(cfg.N, cfg.L, cfg.ell, cfg.L_out, impl, flags=flags, device=local_rank)
     sk = nb.nimbus_keygen(ctx, cfg.seed_cfg)
     # setup (untimed, reported separately): encrypt every weight matrix of the workload
     mats = []

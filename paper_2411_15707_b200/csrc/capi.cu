@@ -273,14 +273,15 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     if (!w) return NIMBUS_ENOMEM;
     w->ctx = ctx; w->m = m; w->n = n; w->KB = (m + kBK - 1) / kBK;
     // resident-X kernel (tcgen05, ell <= 16, m <= 768) uses 32-column tiles, the streaming kernel 48.
-    // The transposed ell = 32 kernel (128-column tiles) is opt-in (NIMBUS_TRANSPOSED=1): it is 2.7%
-    // faster at C5 (k = 2048) but 7% slower at C4 (k = 128: 768 work units = 5.19 waves on 148 SMs),
-    // and the layout is fixed before k is known.
+    // The transposed ell = 32 kernel (128-column tiles) is chosen by NIMBUS_FLAG_LARGE_K (or
+    // NIMBUS_TRANSPOSED=1): 2.7% faster at C5 (k = 2048) but 7% slower at C4 (k = 128: 768 work
+    // units = 5.19 waves on 148 SMs), and the layout is fixed before k is known.
     w->bn = kBNT;
     if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
         const char* tr = getenv("NIMBUS_TRANSPOSED");
+        const bool large_k = (ctx->prm.flags & NIMBUS_FLAG_LARGE_K) || (tr && atoi(tr) == 1);
         if (sx_of(ctx->rns.ell) == 2 && w->KB <= kResMaxKB && !getenv("NIMBUS_NO_RESIDENT")) w->bn = kBNR;
-        else if (sx_of(ctx->rns.ell) == 4 && ctx->rns.N >= kBNW && tr && atoi(tr) == 1) w->bn = kBNW;
+        else if (sx_of(ctx->rns.ell) == 4 && ctx->rns.N >= kBNW && large_k) w->bn = kBNW;
         else if (sx_of(ctx->rns.ell) == 8) w->bn = kBNW;      // 8 X slices: transposed kernel only
     }
     w->bytes = (size_t)w->KB * kBK * col_tiles(ctx, w->bn) * w->bn * 4;

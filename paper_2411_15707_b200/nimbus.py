@@ -21,6 +21,7 @@ STATUS = {0: "NIMBUS_OK", -1: "NIMBUS_EINVAL", -2: "NIMBUS_ESHAPE", -3: "NIMBUS_
           -4: "NIMBUS_ENOISE", -5: "NIMBUS_ECUDA", -6: "NIMBUS_ENOMEM", -8: "NIMBUS_EARCH"}
 IMPL_TCGEN05, IMPL_CUDACORE = 0, 1
 FLAG_CHECK_RANGE = 1
+FLAG_LARGE_K = 2
 
 
 class NimbusError(RuntimeError):

@@ -50,12 +50,12 @@ def matmul_mod_t(X, W, ell):
 
 class Case:
     def __init__(self, nb, oracle, N, L, ell, L_out, m, n, kq, nq=1, impl=0, seed=0x5EED, W=None, X=None,
-                 oracle_full=True):
+                 oracle_full=True, flags=0):
         self.nb, self.O = nb, oracle
         self.N, self.L, self.ell, self.L_out = N, L, ell, L_out
         self.m, self.n, self.kq, self.nq, self.k = m, n, kq, nq, kq * nq
         self.seed = seed
-        self.ctx = nb.nimbus_ctx_create(N, L, ell, L_out, impl)
+        self.ctx = nb.nimbus_ctx_create(N, L, ell, L_out, impl, flags=flags)
         self.pr = np.array(nb.nimbus_ctx_primes(self.ctx), np.uint32)
         self.W = ni.gen_W(seed, m, n, ell) if W is None else W
         self.X = ni.gen_X(seed ^ 0xA5, self.k, m, ell) if X is None else X
@@ -269,7 +269,8 @@ def test_c5_layer_matmuls(nb, oracle, proj):
     li, pj, lay = cfg.layers[proj]
     seed = ni.seed_mm(5, li, pj)
     c = Case(nb, oracle, cfg.N, cfg.L, cfg.ell, cfg.L_out, lay.m, lay.n, lay.k_per_query, lay.n_queries,
-             seed=seed, W=ni.gen_W(seed, lay.m, lay.n, cfg.ell), X=ni.gen_X(seed, lay.k, lay.m, cfg.ell))
+             seed=seed, W=ni.gen_W(seed, lay.m, lay.n, cfg.ell), X=ni.gen_X(seed, lay.k, lay.m, cfg.ell),
+             flags=nb.FLAG_LARGE_K)                      # bench --config 5 sets the k >= 512 layout hint
     assert (u32(nb.nimbus_encw_export(c.encw)) == c.E_oracle).all()
     cts, R = c.run()
     _sampled_check(c, cts, n_samples=300)
