@@ -135,6 +135,16 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_samples(self, n, timeout_s=3.0, busy=None):
+        """Block until `n` samples in total have arrived (nvidia-smi needs ~0.1-0.3 s to
+        start and samples every 100 ms); `busy()` keeps the GPU under the same load."""
+        t0 = time.time()
+        while self.proc is not None and len(self.lines) < n and time.time() - t0 < timeout_s:
+            if busy is not None:
+                busy()
+            else:
+                time.sleep(0.01)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -286,9 +296,22 @@ def run_gpu(args, cfg, rank, world, local_rank):
         return total, step_ms, stage_ms, calls, launches
 
     # pass A (the reported number): the step exactly as a user runs it, no events inside
+    # clocks: the sampler is already polling when the timed region starts; a region
+    # shorter than its 100 ms period is followed by identical untimed steps until two
+    # more samples have landed, so the reported clocks are those of this load
     clocks = ClockSampler(local_rank)
     clocks.start()
+
+    def busy():
+        for _ in range(4):
+            cold()
+            step()
+        torch.cuda.synchronize()
+
+    clocks.wait_samples(1, busy=busy)
+    n0 = len(clocks.lines)
     total_ms, step_ms, _, _, launches = timed(profile=False)
+    clocks.wait_samples(n0 + 2, busy=busy)
     clk = clocks.stop()
     # pass B (roofline evidence): same K steps with CUDA events around each kernel of the
     # step on its stream; the events serialise the PDL-overlapped launches, so the step
