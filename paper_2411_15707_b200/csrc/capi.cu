@@ -104,6 +104,19 @@ static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff) {
     return big_cmp(B, big_of(c->qout)) < 0;
 }
 
+
+// Every entry point that touches the GPU runs on its context's device and restores the
+// caller's current device on return (a process may drive several devices).
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    explicit DevGuard(const nimbus_ctx* c) : DevGuard(c ? c->device : -1) {}
+    ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
 extern "C" {
 
 nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx** out) {
@@ -186,8 +199,8 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
             b[3 * N + kk] = (uint32_t)(((uint64_t)iw << 32) / p);
         }
     }
-    cudaError_t e = cudaSetDevice(device);
-    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_tw, tw.size() * 4);
+    DevGuard dg_(device);
+    cudaError_t e = cudaMalloc(&ctx->d_tw, tw.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_flag, 16);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_flag, 0, 16);
@@ -197,6 +210,7 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
 }
 
 void nimbus_ctx_destroy(nimbus_ctx* ctx) {
+    DevGuard dg_(ctx);
     if (!ctx) return;
     if (ctx->d_tw) cudaFree(ctx->d_tw);
     if (ctx->d_flag) cudaFree(ctx->d_flag);
@@ -220,6 +234,7 @@ const char* nimbus_last_error(const nimbus_ctx* ctx) { return ctx ? ctx->err.c_s
 uint64_t nimbus_launch_count(const nimbus_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
+    DevGuard dg_(ctx);
     if (!ctx) return NIMBUS_EINVAL;
     CK(cudaStreamSynchronize((cudaStream_t)stream), "sync");
     uint32_t flag = 0;
@@ -233,6 +248,7 @@ nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
 
 // ---------------------------------------------------------------- keys
 nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus_sk** out) {
+    DevGuard dg_(ctx);
     if (!ctx || !out) return NIMBUS_EINVAL;
     *out = nullptr;
     nimbus_sk* sk = new (std::nothrow) nimbus_sk();
@@ -248,6 +264,7 @@ nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus
 }
 
 void nimbus_sk_destroy(nimbus_sk* sk) {
+    DevGuard dg_(sk ? sk->ctx : nullptr);
     if (!sk) return;
     if (sk->d_s) cudaFree(sk->d_s);
     if (sk->d_s_ntt) cudaFree(sk->d_s_ntt);
@@ -255,6 +272,7 @@ void nimbus_sk_destroy(nimbus_sk* sk) {
 }
 
 nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream) {
+    DevGuard dg_(sk ? sk->ctx : nullptr);
     if (!sk || !d_s) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = sk->ctx;
     CK(cudaMemcpyAsync(d_s, sk->d_s, ctx->rns.N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "sk export");
@@ -320,17 +338,20 @@ static nimbus_status want_width(nimbus_ctx* ctx, uint32_t bytes) {
 
 nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint32_t m,
                                      uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : encrypt_weights(ctx, sk, d_W, m, n, seed, stream, out);
 }
 
 nimbus_status nimbus_encrypt_weights_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W, uint32_t m,
                                          uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : encrypt_weights(ctx, sk, d_W, m, n, seed, stream, out);
 }
 
 void nimbus_encw_destroy(nimbus_encw* w) {
+    DevGuard dg_(w ? w->ctx : nullptr);
     if (!w) return;
     if (w->d_Et) cudaFree(w->d_Et);
     if (w->h_Et) cudaFreeHost(w->h_Et);
@@ -338,6 +359,7 @@ void nimbus_encw_destroy(nimbus_encw* w) {
 }
 
 nimbus_status nimbus_encw_offload(nimbus_encw* w, void* stream) {
+    DevGuard dg_(w ? w->ctx : nullptr);
     if (!w) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
     if (!w->d_Et) return NIMBUS_OK;                       // already host-resident
@@ -351,6 +373,7 @@ nimbus_status nimbus_encw_offload(nimbus_encw* w, void* stream) {
 }
 
 nimbus_status nimbus_encw_reload(nimbus_encw* w, void* stream) {
+    DevGuard dg_(w ? w->ctx : nullptr);
     if (!w) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
     if (w->d_Et) return NIMBUS_OK;
@@ -364,6 +387,7 @@ int nimbus_encw_is_resident(const nimbus_encw* w) { return w && w->d_Et ? 1 : 0;
 size_t nimbus_encw_bytes(const nimbus_encw* w) { return w ? w->bytes : 0; }
 
 nimbus_status nimbus_encw_export(const nimbus_encw* w, uint32_t* d_out, void* stream) {
+    DevGuard dg_(w ? w->ctx : nullptr);
     if (!w || !d_out) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
     if (!w->d_Et) return set_err(ctx, NIMBUS_EINVAL, "Enc(W) is host-resident (nimbus_encw_reload first)");
@@ -373,6 +397,7 @@ nimbus_status nimbus_encw_export(const nimbus_encw* w, uint32_t* d_out, void* st
 
 nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t m, uint32_t n, void* stream,
                                  nimbus_encw** out) {
+    DevGuard dg_(ctx);
     if (!ctx || !d_in || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     *out = nullptr;
     nimbus_encw* w = nullptr;
@@ -463,6 +488,7 @@ static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
 
 nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                     uint32_t* d_C, void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 4);
     if (st != NIMBUS_OK) return st;
     st = check_online(ctx, w, k, 1);
@@ -478,6 +504,7 @@ nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
 
 nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                               uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* stream) {
+    DevGuard dg_(ctx);
     if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;
     if (!ctx || !d_C || !d_cts || !d_R || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
@@ -509,6 +536,7 @@ static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const voi
 nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t kq,
                                 uint32_t nq, uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* d_ws,
                                 size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream);
 }
@@ -516,6 +544,7 @@ nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uin
 nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* d_X, uint32_t kq,
                                     uint32_t nq, uint64_t seed, uint32_t* d_cts, uint64_t* d_R, void* d_ws,
                                     size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream);
 }
@@ -541,6 +570,7 @@ nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbu
 
 nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                       size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;
     for (uint32_t i = 0; i < count; i++) {
@@ -611,6 +641,7 @@ nimbus_status nimbus_cop_stage_size(const nimbus_ctx* ctx, const nimbus_cop_job*
 
 nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                          size_t ws_bytes, void* d_stage, size_t stage_bytes, void* stream) {
+    DevGuard dg_(ctx);
     if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     size_t need = 0;
     for (uint32_t i = 0; i < count; i++) {
@@ -693,6 +724,7 @@ nimbus_status nimbus_profile_enable(nimbus_ctx* ctx, int on) {
 }
 
 nimbus_status nimbus_profile_read(nimbus_ctx* ctx, double* ms, uint64_t* calls, int reset) {
+    DevGuard dg_(ctx);
     if (!ctx) return NIMBUS_EINVAL;
     auto& P = ctx->ev_pending;
     // groups of 5: before slice, after slice, after contraction, before pack, after pack
@@ -744,6 +776,7 @@ static nimbus_status cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, cons
 nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* h_X, uint32_t kq,
                                      uint32_t nq, uint64_t seed, uint32_t* h_cts, uint32_t* h_R, void* d_ws,
                                      size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
 }
@@ -751,6 +784,7 @@ nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, cons
 nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* h_X, uint32_t kq,
                                          uint32_t nq, uint64_t seed, uint32_t* h_cts, uint64_t* h_R, void* d_ws,
                                          size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
 }
@@ -772,12 +806,14 @@ static nimbus_status decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_
 
 nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
                              uint32_t n, uint32_t* d_Z, uint32_t* d_M, void* stream) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, nq, n, d_Z, d_M, stream);
 }
 
 nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq,
                                  uint32_t nq, uint32_t n, uint64_t* d_Z, uint64_t* d_M, void* stream) {
+    DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, nq, n, d_Z, d_M, stream);
 }
@@ -785,6 +821,7 @@ nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uin
 // ---------------------------------------------------------------- server, step 5
 nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_t m, uint32_t n, void* stream,
                                    nimbus_plainw** out) {
+    DevGuard dg_(ctx);
     if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;          // server GEMM: ell <= 32
     if (!ctx || !d_W || !out || m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     nimbus_plainw* w = new (std::nothrow) nimbus_plainw();
@@ -803,6 +840,7 @@ nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_
 }
 
 void nimbus_plainw_destroy(nimbus_plainw* w) {
+    DevGuard dg_(w ? w->ctx : nullptr);
     if (!w) return;
     if (w->d_Wt) cudaFree(w->d_Wt);
     delete w;
@@ -838,6 +876,7 @@ nimbus_status nimbus_server_workspace_size(const nimbus_ctx* ctx, const nimbus_p
 
 nimbus_status nimbus_plain_matmul(nimbus_ctx* ctx, const nimbus_plainw* w, const uint32_t* d_X, uint32_t k,
                                   const uint32_t* d_add, uint32_t* d_Y, void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     if (!ctx || !w || w->ctx != ctx || !d_X || !d_Y || !d_ws || k == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (k > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
     const ServerWs L = server_ws(ctx, w, k, 0);
@@ -852,6 +891,7 @@ nimbus_status nimbus_plain_matmul(nimbus_ctx* ctx, const nimbus_plainw* w, const
 nimbus_status nimbus_server_output(nimbus_ctx* ctx, const nimbus_sk* sk, const nimbus_plainw* w,
                                    const uint32_t* d_Xs, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
                                    uint32_t* d_Ys, void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
     if (!ctx || !sk || !w || w->ctx != ctx || !d_Xs || !d_cts || !d_Ys || !d_ws || kq == 0 || nq == 0)
         return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (w->n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
@@ -878,6 +918,7 @@ nimbus_status nimbus_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint
 
 nimbus_status nimbus_negacyclic_mul(nimbus_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t count,
                                     uint32_t* c, void* stream) {
+    DevGuard dg_(ctx);
     if (!ctx || !a || !b || !c || count == 0) return NIMBUS_EINVAL;
     CK(launch_negacyclic_mul(ctx, a, b, count, c, (cudaStream_t)stream), "negacyclic_mul");
     return NIMBUS_OK;

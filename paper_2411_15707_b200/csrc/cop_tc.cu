@@ -608,12 +608,9 @@ template <int SX, int CL, int BN>
 static cudaError_t launch_sx(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                              cudaStream_t st) {
     using Cfg = TcCfg<SX, BN>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_cop_tc<SX, CL, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)Cfg::SMEM);
+    {
+        cudaError_t e = ensure_smem(c, k_cop_tc<SX, CL, BN>, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
     const uint32_t CT = col_tiles(c, BN), Mt = (k + kBM - 1) / kBM;
@@ -642,12 +639,9 @@ static cudaError_t launch_sx(nimbus_ctx* c, const nimbus_encw* w, const uint8_t*
 
 static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                               cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_cop_tc_res, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)ResCfg::SMEM);
+    {
+        cudaError_t e = ensure_smem(c, k_cop_tc_res, ResCfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
     const uint32_t CT = col_tiles(c, kBNR);
@@ -662,12 +656,9 @@ template <int SX>
 static cudaError_t launch_t(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                             cudaStream_t st) {
     using Cfg = TCfgT<SX>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_cop_tc_t<SX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)Cfg::SMEM);
+    {
+        cudaError_t e = ensure_smem(c, k_cop_tc_t<SX>, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
     const uint32_t CT = col_tiles(c, kBNW), RTt = (k + Cfg::RT - 1) / Cfg::RT;

@@ -49,6 +49,8 @@ struct nimbus_ctx {
     // streamed path (nimbus_cop_matmul_streamed): host -> device copy stream + events
     cudaStream_t copy = nullptr;
     std::vector<cudaEvent_t> stream_ev;
+    // kernels already opted into their dynamic shared memory on this context's device
+    std::vector<const void*> smem_ok;
 };
 
 struct nimbus_sk {
@@ -116,6 +118,18 @@ cudaError_t launch_plain_matmul(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st);
 }  // namespace nimbus
+
+// Opt `kernel` into `bytes` of dynamic shared memory on the context's device, once
+// (the attribute is per device; a process may hold contexts on several devices).
+template <typename K>
+static inline cudaError_t ensure_smem(nimbus_ctx* c, K kernel, size_t bytes) {
+    const void* key = reinterpret_cast<const void*>(kernel);
+    for (const void* k : c->smem_ok)
+        if (k == key) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c->smem_ok.push_back(key);
+    return e;
+}
 
 // Launch with programmatic dependent launch (PDL) allowed: the kernel may be
 // scheduled while its stream predecessor is still running; it must call

@@ -225,12 +225,9 @@ template <int S>
 static cudaError_t launch_plain_s(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_t* d_Wt, uint32_t k, uint32_t n,
                                   uint32_t KB, const uint32_t* d_add, uint32_t* d_Y, cudaStream_t st) {
     using Cfg = PlainCfg<S>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_plain_tc<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)Cfg::SMEM);
+    {
+        cudaError_t e = ensure_smem(c, k_plain_tc<S>, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const uint32_t Mt = (k + kBM - 1) / kBM, CT = plain_col_tiles(n);
     const uint32_t units = Mt * CT;
