@@ -20,7 +20,9 @@
  *  - Residues are little-endian uint32 in [0, p_i).  Prime order is
  *    p_0 > p_1 > ....
  *  - Opaque handles are allocated by the library and released by *_destroy.
- *    A context is not thread-safe; distinct contexts are independent.
+ *    A context is not thread-safe; distinct contexts are independent.  Every call
+ *    runs on its context's device and leaves the caller's current device as it was;
+ *    streams passed in must belong to that device.
  */
 #ifndef NIMBUS_COP_H
 #define NIMBUS_COP_H
