@@ -232,8 +232,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
                   n_queries=mt["lay"].n_queries, mask_seed=mt["seed"], cts=mt["cts"], R=mt["R"]) for mt in mats]
             for c in range(n_copies)]
     ws_batch = None
-    if len(mats) > 1 and not wide:           # the batched call is 32-bit only
-        ws_batch = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs[0]), dtype=torch.uint8, device=dev)
+    batch = nb.nimbus_cop_matmul_batch_u64 if wide else nb.nimbus_cop_matmul_batch
+    if len(mats) > 1:
+        size_fn = nb.nimbus_cop_workspace_size_batch_u64 if wide else nb.nimbus_cop_workspace_size_batch
+        ws_batch = torch.empty(size_fn(ctx, jobs[0]), dtype=torch.uint8, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES if args.l2 == "write" else 64 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     step_no = [0]
@@ -247,7 +249,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     def step():
         c = step_no[0] % n_copies
         if ws_batch is not None:
-            nb.nimbus_cop_matmul_batch(ctx, jobs[c], ws_batch)
+            batch(ctx, jobs[c], ws_batch)
             return
         for mt in mats:
             lay = mt["lay"]

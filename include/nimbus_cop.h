@@ -108,8 +108,8 @@ nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const
  * points return NIMBUS_EINVAL for such a context and the _u64 ones for ell <= 32.
  * ell > 32 needs L >= 4 limbs for the noise bound (5 at N = 8192), uses S_x = 8
  * X slices (11 shifted accumulators, the transposed kernel) and m <= 4096; the
- * CUDA-core ablation, the batched / streamed / host-buffer / server-side calls
- * and nimbus_cop_accumulate / nimbus_cop_pack are 32-bit only. */
+ * CUDA-core ablation, the server-side calls and nimbus_cop_accumulate /
+ * nimbus_cop_pack are 32-bit only. */
 nimbus_status nimbus_encrypt_weights_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W,
                                          uint32_t m, uint32_t n, uint64_t seed, void* stream,
                                          nimbus_encw** out);
@@ -175,6 +175,19 @@ nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbu
                                               size_t* bytes);
 nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                       size_t ws_bytes, void* stream);
+/* ell > 32: the same with uint64 X and R. */
+typedef struct {
+    const nimbus_encw* encw;
+    const uint64_t* d_X;          /* k x m uint64 */
+    uint32_t k_per_query, n_queries;
+    uint64_t mask_seed;
+    uint32_t* d_cts;
+    uint64_t* d_R;                /* k x n uint64 */
+} nimbus_cop_job_u64;
+nimbus_status nimbus_cop_workspace_size_batch_u64(const nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs,
+                                                  uint32_t count, size_t* bytes);
+nimbus_status nimbus_cop_matmul_batch_u64(nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
+                                          void* d_ws, size_t ws_bytes, void* stream);
 
 /* Asynchronous weight loading: keep
  * Enc(W) in pinned host memory and stage each matrix into HBM right before its
@@ -197,6 +210,11 @@ nimbus_status nimbus_cop_stage_size(const nimbus_ctx* ctx, const nimbus_cop_job*
                                     size_t* bytes);
 nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                          size_t ws_bytes, void* d_stage, size_t stage_bytes, void* stream);
+nimbus_status nimbus_cop_stage_size_u64(const nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
+                                        size_t* bytes);
+nimbus_status nimbus_cop_matmul_streamed_u64(nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
+                                             void* d_ws, size_t ws_bytes, void* d_stage, size_t stage_bytes,
+                                             void* stream);
 
 /* Same computation with HOST buffers: copies h_X in, runs nimbus_cop_matmul,
  * copies h_cts and h_R out, and synchronises `stream` before returning. */

@@ -568,11 +568,10 @@ nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbu
     return NIMBUS_OK;
 }
 
-nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+// element-width-agnostic: d_X / d_R are passed through untouched (uint64 when ell > 32)
+static nimbus_status cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                       size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
     if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
-    if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;
     for (uint32_t i = 0; i < count; i++) {
         nimbus_status st = check_online(ctx, jobs[i].encw, jobs[i].k_per_query, jobs[i].n_queries);
         if (st != NIMBUS_OK) return st;
@@ -626,6 +625,39 @@ nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* job
     return NIMBUS_OK;
 }
 
+// the _u64 job list viewed as the 32-bit one (same layout; the pointers are passed through)
+static std::vector<nimbus_cop_job> jobs_of(const nimbus_cop_job_u64* jobs, uint32_t count) {
+    std::vector<nimbus_cop_job> v(count);
+    for (uint32_t i = 0; i < count; i++)
+        v[i] = {jobs[i].encw, reinterpret_cast<const uint32_t*>(jobs[i].d_X), jobs[i].k_per_query,
+                jobs[i].n_queries, jobs[i].mask_seed, jobs[i].d_cts, reinterpret_cast<uint32_t*>(jobs[i].d_R)};
+    return v;
+}
+
+nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+                                      size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : cop_matmul_batch(ctx, jobs, count, d_ws, ws_bytes, stream);
+}
+
+nimbus_status nimbus_cop_workspace_size_batch_u64(const nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs,
+                                                  uint32_t count, size_t* bytes) {
+    if (!ctx || !jobs || !bytes || count == 0) return NIMBUS_EINVAL;
+    const std::vector<nimbus_cop_job> v = jobs_of(jobs, count);
+    return nimbus_cop_workspace_size_batch(ctx, v.data(), count, bytes);
+}
+
+nimbus_status nimbus_cop_matmul_batch_u64(nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
+                                          void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 8);
+    if (st != NIMBUS_OK) return st;
+    if (!jobs || count == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    const std::vector<nimbus_cop_job> v = jobs_of(jobs, count);
+    return cop_matmul_batch(ctx, v.data(), count, d_ws, ws_bytes, stream);
+}
+
 // ---------------------------------------------------------------- streamed path (Enc(W) in host memory)
 nimbus_status nimbus_cop_stage_size(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
                                     size_t* bytes) {
@@ -639,9 +671,8 @@ nimbus_status nimbus_cop_stage_size(const nimbus_ctx* ctx, const nimbus_cop_job*
     return NIMBUS_OK;
 }
 
-nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+static nimbus_status cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                          size_t ws_bytes, void* d_stage, size_t stage_bytes, void* stream) {
-    DevGuard dg_(ctx);
     if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     size_t need = 0;
     for (uint32_t i = 0; i < count; i++) {
@@ -701,8 +732,8 @@ nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* 
             view.d_Et = stage + (size_t)slot_of[i] * slot;
             CK(cudaStreamWaitEvent(a, loaded[i], 0), "wait load");
         }
-        nimbus_status st = nimbus_cop_matmul(ctx, &view, J.d_X, J.k_per_query, J.n_queries, J.mask_seed, J.d_cts,
-                                             J.d_R, d_ws, ws_bytes, a);
+        nimbus_status st = cop_matmul(ctx, &view, J.d_X, J.k_per_query, J.n_queries, J.mask_seed, J.d_cts,
+                                      J.d_R, d_ws, ws_bytes, a);
         view.d_Et = nullptr;                               // the view owns nothing
         if (st != NIMBUS_OK) return st;
         CK(cudaEventRecord(used[i], a), "record");
@@ -715,6 +746,31 @@ nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* 
         }
     }
     return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
+                                         size_t ws_bytes, void* d_stage, size_t stage_bytes, void* stream) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : cop_matmul_streamed(ctx, jobs, count, d_ws, ws_bytes, d_stage, stage_bytes, stream);
+}
+
+nimbus_status nimbus_cop_stage_size_u64(const nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
+                                        size_t* bytes) {
+    if (!ctx || !jobs || !bytes || count == 0) return NIMBUS_EINVAL;
+    const std::vector<nimbus_cop_job> v = jobs_of(jobs, count);
+    return nimbus_cop_stage_size(ctx, v.data(), count, bytes);
+}
+
+nimbus_status nimbus_cop_matmul_streamed_u64(nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
+                                             void* d_ws, size_t ws_bytes, void* d_stage, size_t stage_bytes,
+                                             void* stream) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 8);
+    if (st != NIMBUS_OK) return st;
+    if (!jobs || count == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    const std::vector<nimbus_cop_job> v = jobs_of(jobs, count);
+    return cop_matmul_streamed(ctx, v.data(), count, d_ws, ws_bytes, d_stage, stage_bytes, stream);
 }
 
 nimbus_status nimbus_profile_enable(nimbus_ctx* ctx, int on) {

@@ -69,6 +69,10 @@ _SIGS = {
     "nimbus_cop_matmul_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
     "nimbus_decrypt_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _vp]),
     "nimbus_cop_matmul_host_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_cop_workspace_size_batch_u64": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
+    "nimbus_cop_matmul_batch_u64": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
+    "nimbus_cop_stage_size_u64": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
+    "nimbus_cop_matmul_streamed_u64": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp, _sz, _vp]),
     "nimbus_encw_offload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_reload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_is_resident": (C.c_int, [_vp]),
@@ -314,12 +318,14 @@ class nimbus_cop_job(C.Structure):
                 ("mask_seed", _u64), ("d_cts", _vp), ("d_R", _vp)]
 
 
-def _jobs(jobs):
-    """jobs: sequence of dicts with encw, X, k_per_query, n_queries, mask_seed, cts, R."""
+def _jobs(jobs, wide=False):
+    """jobs: sequence of dicts with encw, X, k_per_query, n_queries, mask_seed, cts, R
+    (X and R int64 holding uint64 when wide, i.e. ell > 32: nimbus_cop_job_u64, same layout)."""
+    dt = torch.int64 if wide else torch.int32
     arr = (nimbus_cop_job * len(jobs))()
     for i, j in enumerate(jobs):
-        arr[i] = nimbus_cop_job(j["encw"].ptr, _ptr(j["X"], torch.int32, "X"), j["k_per_query"], j["n_queries"],
-                                j["mask_seed"], _ptr(j["cts"], torch.int32, "cts"), _ptr(j["R"], torch.int32, "R"))
+        arr[i] = nimbus_cop_job(j["encw"].ptr, _ptr(j["X"], dt, "X"), j["k_per_query"], j["n_queries"],
+                                j["mask_seed"], _ptr(j["cts"], torch.int32, "cts"), _ptr(j["R"], dt, "R"))
     return arr
 
 
@@ -357,6 +363,30 @@ def nimbus_cop_matmul_streamed(ctx: Context, jobs, ws: torch.Tensor, stage: torc
     _check(lib().nimbus_cop_matmul_streamed(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(),
                                             _ptr(stage) if stage is not None else None,
                                             stage.numel() if stage is not None else 0, _stream(stream)), ctx)
+
+
+def nimbus_cop_workspace_size_batch_u64(ctx: Context, jobs) -> int:
+    out = _sz()
+    _check(lib().nimbus_cop_workspace_size_batch_u64(ctx.ptr, _jobs(jobs, True), len(jobs), C.byref(out)), ctx)
+    return int(out.value)
+
+
+def nimbus_cop_matmul_batch_u64(ctx: Context, jobs, ws: torch.Tensor, stream=None):
+    arr = _jobs(jobs, True)
+    _check(lib().nimbus_cop_matmul_batch_u64(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+
+
+def nimbus_cop_stage_size_u64(ctx: Context, jobs) -> int:
+    out = _sz()
+    _check(lib().nimbus_cop_stage_size_u64(ctx.ptr, _jobs(jobs, True), len(jobs), C.byref(out)), ctx)
+    return int(out.value)
+
+
+def nimbus_cop_matmul_streamed_u64(ctx: Context, jobs, ws: torch.Tensor, stage: torch.Tensor = None, stream=None):
+    arr = _jobs(jobs, True)
+    _check(lib().nimbus_cop_matmul_streamed_u64(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(),
+                                                _ptr(stage) if stage is not None else None,
+                                                stage.numel() if stage is not None else 0, _stream(stream)), ctx)
 
 
 def nimbus_cop_matmul_host(ctx: Context, w: EncW, X_host: torch.Tensor, k_per_query: int,

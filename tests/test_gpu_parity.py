@@ -572,3 +572,39 @@ def test_random_shapes_parity(nb, oracle, N, L, ell, L_out, m, n, kq, nq):
     cts_o, R_o = c.oracle_out()
     assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
     c.check_decrypt(cts, R)
+
+
+def test_ell64_batch_and_streamed_match_single(nb, oracle):
+    """ell = 64 through the batched (pack on the side stream) and the streamed
+    (Enc(W) from pinned host memory) calls: the same bytes as job-by-job
+    nimbus_cop_matmul_u64."""
+    N, L, ell, L_out = 256, 5, 64, 3
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, 9)
+    shapes = [(33, 130, 100, 2), (7, 300, 128, 1), (64, 64, 256, 1)]
+    jobs, ref = [], []
+    for i, (kq, m, n, nq) in enumerate(shapes):
+        w = nb.nimbus_encrypt_weights_u64(ctx, sk, _dev_u64(ni.gen_W(70 + i, m, n, ell)), 70 + i)
+        X = _dev_u64(ni.gen_X(80 + i, kq * nq, m, ell))
+        ws = nb.alloc_workspace(ctx, w, kq * nq)
+        c0, R0 = nb.alloc_outputs_u64(ctx, w, kq, nq)
+        nb.nimbus_cop_matmul_u64(ctx, w, X, kq, nq, 90 + i, c0, R0, ws)
+        ref.append((c0, R0))
+        cts, R = nb.alloc_outputs_u64(ctx, w, kq, nq)
+        jobs.append(dict(encw=w, X=X, k_per_query=kq, n_queries=nq, mask_seed=90 + i, cts=cts, R=R))
+    wsb = torch.empty(nb.nimbus_cop_workspace_size_batch_u64(ctx, jobs), dtype=torch.uint8, device=DEV)
+    nb.nimbus_cop_matmul_batch_u64(ctx, jobs, wsb)
+    nb.nimbus_sync(ctx)
+    for j, (c0, R0) in zip(jobs, ref):
+        assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+        j["cts"].zero_()
+        j["R"].zero_()
+    for j in jobs:
+        nb.nimbus_encw_offload(j["encw"])
+    ws = torch.empty(max(nb.nimbus_cop_workspace_size(ctx, j["encw"], j["k_per_query"] * j["n_queries"])
+                         for j in jobs), dtype=torch.uint8, device=DEV)
+    stage = torch.empty(nb.nimbus_cop_stage_size_u64(ctx, jobs), dtype=torch.uint8, device=DEV)
+    nb.nimbus_cop_matmul_streamed_u64(ctx, jobs, ws, stage)
+    nb.nimbus_sync(ctx)
+    for j, (c0, R0) in zip(jobs, ref):
+        assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
