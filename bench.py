@@ -406,6 +406,9 @@ def oracle_sample(cfg, budget_s, rows_cap=None):
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return None
+    if cfg.ell > 32:
+        return {"impl": "reference", "unavailable": "ell > 32 needs the Python-integer oracle (oracle/wide.py), "
+                                                    "not timed as a reference arm"}
     from oracle import oracle as O
     li, pj, lay = cfg.layers[0]
     seed = ni.seed_mm(cfg.cid, li, pj)
@@ -439,7 +442,9 @@ def run_reference(args, cfg, rank, world):
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u128", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "sample_rows": rows},
+            "config": {"workload": workload_name(cfg), "config": cfg.name, "k": lay.k,
+                       "matmuls_per_step": 1, "impl": "reference (oracle/, CPU)", "sample_rows": rows,
+                       "l2": "n/a (host)"},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
