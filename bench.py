@@ -219,6 +219,21 @@ def run_gpu(args, cfg, rank, world, local_rank):
             for _ in range(n_copies - 1):
                 mt["encw"].append(encrypt(ctx, sk, mt["W"], mt["seed"]))
                 mt["X"].append(mt["X"][0].clone())
+    # setup on the device, steady state (allocations excluded): re-encrypt the first
+    # matrix into a fresh handle, CUDA events around the kernels' stream work
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mt0 = mats[0]
+    tmp = encrypt(ctx, sk, mt0["W"], mt0["seed"])       # allocate once, then time a second pass
+    torch.cuda.synchronize()
+    t_h0 = time.perf_counter()
+    e0.record()
+    tmp2 = encrypt(ctx, sk, mt0["W"], mt0["seed"])
+    e1.record()
+    torch.cuda.synchronize()
+    setup_host_s = time.perf_counter() - t_h0
+    setup_gpu_ms = e0.elapsed_time(e1)
+    setup_bytes = nb.nimbus_encw_bytes(tmp2)
+    del tmp, tmp2
     for mt in mats:
         del mt["W"]
     torch.cuda.synchronize()
@@ -365,7 +380,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                f"{l2_bytes >> 20} MiB L2), step i reads copy i mod {n_copies}" if args.l2 == "rotate" else
                f"flushed by a {L2_FLUSH_BYTES >> 20} MiB write before every timed step")
     return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=stage_ms, calls=calls, launches=launches,
-                clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e, l2_desc=l2_desc)
+                clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e, l2_desc=l2_desc,
+                setup=dict(gpu_ms=setup_gpu_ms, host_s=setup_host_s, bytes=setup_bytes))
 
 
 # ----------------------------------------------------------------- CPU oracle
@@ -528,6 +544,11 @@ def main():
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
         "setup_encrypt_s": res["t_setup"],
+        # Alg. 1 step 1 for the first matrix, steady state: Enc(W) bytes written / GPU time
+        "setup": {"matrix": f"{lays[0].m}x{lays[0].n}", "enc_w_bytes": res["setup"]["bytes"],
+                  "gpu_ms": res["setup"]["gpu_ms"], "host_ms": res["setup"]["host_s"] * 1e3,
+                  "gb_per_s": res["setup"]["bytes"] / (res["setup"]["gpu_ms"] * 1e-3) / 1e9,
+                  "hbm_frac": res["setup"]["bytes"] / (res["setup"]["gpu_ms"] * 1e-3) / 1e9 / peaks["hbm_gbs"]},
     }
     if res["e2e"] is not None:
         e = res["e2e"]
