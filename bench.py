@@ -519,8 +519,8 @@ def main():
     prim, alt = (tens, hbm) if t_i8 >= t_hbm else (hbm, tens)
     prim = dict(prim)
     prim["traffic"] = None
-    ncu_json = os.path.join(ROOT, "profiles", f"ncu_{cfg.name}.json")
-    if os.path.exists(ncu_json):   # dram__bytes_read.sum + dram__bytes_write.sum of one captured launch
+    ncu_json = os.path.join(ROOT, "profiles", f"ncu_{cfg.name.replace('@', '')}.json")
+    if args.impl == "tcgen05" and os.path.exists(ncu_json):   # dram bytes read + written of one captured launch
         cap = json.load(open(ncu_json)).get("kernel_capture", {})
         if cap.get("dram_traffic_bytes") is not None:
             prim["traffic"] = cap["dram_traffic_bytes"]
