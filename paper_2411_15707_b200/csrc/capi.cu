@@ -512,12 +512,13 @@ nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq,
     return NIMBUS_OK;
 }
 
+// allow_no_R: d_R may be null (the host-buffer call produces R separately)
 static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const void* d_X, uint32_t kq,
                                 uint32_t nq, uint64_t seed, uint32_t* d_cts, void* d_R, void* d_ws,
-                                size_t ws_bytes, void* stream) {
+                                size_t ws_bytes, void* stream, bool allow_no_R = false) {
     nimbus_status st = check_online(ctx, w, kq, nq);
     if (st != NIMBUS_OK) return st;
-    if (!d_X || !d_cts || !d_R || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
+    if (!d_X || !d_cts || (!d_R && !allow_no_R) || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
     const uint32_t k = kq * nq;
     const WsLayout L = ws_layout(ctx, w, k);
     if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
@@ -820,11 +821,25 @@ static nimbus_status cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, cons
     uint32_t nct = 0;
     nimbus_cop_out_count(ctx, kq, w->n, &nct);
     const size_t cts_bytes = (size_t)nq * nct * 2 * ctx->rns.L_out * ctx->rns.N * 4;
+    // R depends only on the mask seed: generate and download it on the side stream while
+    // `stream` uploads X and runs the matmul (whose pack then skips R)
+    if (!ctx->side) CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
+    cudaStream_t b = ctx->side;
+    while (ctx->sync_ev.size() < 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        ctx->sync_ev.push_back(e);
+    }
+    CK(cudaEventRecord(ctx->sync_ev[0], s), "record");
+    CK(cudaStreamWaitEvent(b, ctx->sync_ev[0], 0), "wait");          // after earlier work on `stream`
+    CK(launch_mask_R(ctx, kq, nq, w->n, seed, dR, b), "mask R");
+    CK(cudaMemcpyAsync(h_R, dR, (size_t)k * w->n * es, cudaMemcpyDeviceToHost, b), "d2h R");
+    CK(cudaEventRecord(ctx->sync_ev[1], b), "record");
     CK(cudaMemcpyAsync(dX, h_X, (size_t)k * w->m * es, cudaMemcpyHostToDevice, s), "h2d X");
-    st = cop_matmul(ctx, w, dX, kq, nq, seed, dcts, dR, d_ws, ws_bytes, stream);
+    st = cop_matmul(ctx, w, dX, kq, nq, seed, dcts, nullptr, d_ws, ws_bytes, stream, true);
     if (st != NIMBUS_OK) return st;
     CK(cudaMemcpyAsync(h_cts, dcts, cts_bytes, cudaMemcpyDeviceToHost, s), "d2h cts");
-    CK(cudaMemcpyAsync(h_R, dR, (size_t)k * w->n * es, cudaMemcpyDeviceToHost, s), "d2h R");
+    CK(cudaStreamWaitEvent(s, ctx->sync_ev[1], 0), "join");
     CK(cudaStreamSynchronize(s), "host matmul sync");
     return NIMBUS_OK;
 }

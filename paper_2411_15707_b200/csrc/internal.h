@@ -103,8 +103,11 @@ cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, u
                                uint32_t* d_canon, cudaStream_t st);
 cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st);
+// d_R may be null: then the pack writes only the ciphertexts (R comes from launch_mask_R)
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                         uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl);
+cudaError_t launch_mask_R(nimbus_ctx* c, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed, void* d_R,
+                          cudaStream_t st);
 // cop_cc.cu
 cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                 uint32_t* d_C, cudaStream_t st);

@@ -14,6 +14,7 @@
 //            (SURVEY.md §8(c) #13); R[alpha][j] = r_theta[(alpha mod R) n + j].
 // V = 4 (uint4 loads/stores) when n % 4 == 0 and the grid stays large; a group
 // of 4 J never straddles a wrap point because J and r n are multiples of 4.
+#include <algorithm>
 #include "pack_dev.cuh"
 
 namespace nimbus {
@@ -100,6 +101,37 @@ static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uin
         case 5: return launch_vr<V, 5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
         default: return launch_vr<V, 8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
     }
+}
+
+// R alone (the client's share Y_c = the mask at the valid slots):
+// R[alpha][j] = r_theta[rho n + j], alpha = query kq + theta R + rho.  It depends only on
+// the mask seed, so the host-buffer call computes and downloads it while the
+// contraction runs (the pack then skips R).
+template <typename MT>
+__global__ void k_mask_R(uint32_t N, uint32_t ell, uint32_t kq, uint32_t nq, uint32_t n, uint32_t Rr, uint32_t nct,
+                         uint64_t key, MT* __restrict__ R) {
+    const uint64_t total = (uint64_t)kq * nq * n;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t alpha = (uint32_t)(i / n), j = (uint32_t)(i % n);
+        const uint32_t query = alpha / kq, a = alpha % kq, theta = a / Rr, rho = a % Rr;
+        const uint64_t w = prg_word(key, (uint64_t)(query * nct + theta) * N + rho * n + j);
+        R[i] = (MT)(ell >= 64 ? w : w >> (64 - ell));
+    }
+}
+
+cudaError_t launch_mask_R(nimbus_ctx* c, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed, void* d_R,
+                          cudaStream_t st) {
+    const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
+    const uint64_t key = prg_key(seed, 6);
+    const uint64_t total = (uint64_t)kq * nq * n;
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((total + 255) / 256, 4ull * c->num_sms);
+    if (elem_bytes(c->rns.ell) == 8)
+        k_mask_R<uint64_t><<<blocks, 256, 0, st>>>(N, c->rns.ell, kq, nq, n, Rr, nct, key, static_cast<uint64_t*>(d_R));
+    else
+        k_mask_R<uint32_t><<<blocks, 256, 0, st>>>(N, c->rns.ell, kq, nq, n, Rr, nct, key, static_cast<uint32_t*>(d_R));
+    c->launches++;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,

@@ -163,7 +163,7 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
 #pragma unroll
     for (int i = 0; i < L; i++)
         if ((uint32_t)i < Lo) VecU32<V>::store(cts + (((size_t)tg * 2 + comp) * Lo + i) * N + J, out[i]);
-    if (comp == 0 && J < rows * n) {
+    if (comp == 0 && Rout && J < rows * n) {          // Rout null: R written by k_mask_R instead
         if (sizeof(MT) == 8) Rout[row0 * n + J] = rmask[0];
         else VecU32<V>::store(reinterpret_cast<uint32_t*>(Rout) + row0 * n + J,
                               reinterpret_cast<const uint32_t(&)[V]>(rmask));
