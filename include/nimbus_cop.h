@@ -42,6 +42,7 @@ typedef enum {
     NIMBUS_ENOISE = -4,  /* parameters fail the worst-case decryption bound */
     NIMBUS_ECUDA = -5,   /* CUDA runtime error, text in nimbus_last_error */
     NIMBUS_ENOMEM = -6,  /* device allocation failed */
+    NIMBUS_EIO = -7,     /* store file unreadable, corrupt, or made for other parameters */
     NIMBUS_EARCH = -8    /* device is not sm_100 (B200) */
 } nimbus_status;
 
@@ -121,6 +122,14 @@ size_t nimbus_encw_bytes(const nimbus_encw* encw);
 nimbus_status nimbus_encw_export(const nimbus_encw* encw, uint32_t* d_out, void* stream);
 nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t m, uint32_t n,
                                  void* stream, nimbus_encw** out);
+
+/* Store file (the client keeps Enc(W) on disk between sessions, PAPER.md:300;
+ * SPEC.md:470).  Little-endian: "NIMBUSEW", u32 version (1), N, L, ell, m, n, the
+ * L primes (u32 each), u64 payload bytes, then Enc(W) in the canonical layout of
+ * nimbus_encw_export, then a u64 FNV-1a checksum of the payload.  Loading checks
+ * every header field against the context and the checksum: NIMBUS_EIO otherwise. */
+nimbus_status nimbus_encw_save(const nimbus_encw* encw, const char* path);
+nimbus_status nimbus_encw_load(nimbus_ctx* ctx, const char* path, nimbus_encw** out);
 
 /* ---------------------------------------------------------------- online --- */
 /* Number of packed output ciphertexts per query, ceil(k_q / floor(N/n))

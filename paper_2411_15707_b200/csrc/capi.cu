@@ -409,6 +409,72 @@ nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t
     return NIMBUS_OK;
 }
 
+// ---------------------------------------------------------------- store file
+static uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h = 0xcbf29ce484222325ULL) {
+    for (size_t i = 0; i < n; i++) { h ^= p[i]; h *= 0x100000001b3ULL; }
+    return h;
+}
+
+nimbus_status nimbus_encw_save(const nimbus_encw* w, const char* path) {
+    if (!w || !path) return NIMBUS_EINVAL;
+    nimbus_ctx* ctx = w->ctx;
+    DevGuard dg_(ctx);
+    if (!w->d_Et) return set_err(ctx, NIMBUS_EINVAL, "Enc(W) is host-resident (nimbus_encw_reload first)");
+    const size_t bytes = (size_t)w->m * ncols(ctx) * 4;
+    uint32_t* d_canon = nullptr;
+    CK(cudaMalloc(&d_canon, bytes), "save alloc");
+    std::vector<uint8_t> host(bytes);
+    cudaError_t e = launch_untile_encw(ctx, w->d_Et, w->m, w->KB, w->bn, d_canon, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(host.data(), d_canon, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d_canon);
+    CK(e, "save export");
+    FILE* f = fopen(path, "wb");
+    if (!f) return set_err(ctx, NIMBUS_EIO, "cannot open store file for writing");
+    const uint32_t hdr[6] = {1u, ctx->rns.N, ctx->rns.L, ctx->rns.ell, w->m, w->n};
+    const uint64_t nbytes = bytes, sum = fnv1a(host.data(), bytes);
+    bool ok = fwrite("NIMBUSEW", 1, 8, f) == 8 && fwrite(hdr, 4, 6, f) == 6 &&
+              fwrite(ctx->rns.p, 4, ctx->rns.L, f) == ctx->rns.L && fwrite(&nbytes, 8, 1, f) == 1 &&
+              fwrite(host.data(), 1, bytes, f) == bytes && fwrite(&sum, 8, 1, f) == 1;
+    ok = (fclose(f) == 0) && ok;
+    return ok ? NIMBUS_OK : set_err(ctx, NIMBUS_EIO, "store file write failed");
+}
+
+nimbus_status nimbus_encw_load(nimbus_ctx* ctx, const char* path, nimbus_encw** out) {
+    DevGuard dg_(ctx);
+    if (!ctx || !path || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    *out = nullptr;
+    FILE* f = fopen(path, "rb");
+    if (!f) return set_err(ctx, NIMBUS_EIO, "cannot open store file");
+    char magic[8];
+    uint32_t hdr[6], pr[NIMBUS_MAXL];
+    uint64_t nbytes = 0, sum = 0;
+    bool ok = fread(magic, 1, 8, f) == 8 && memcmp(magic, "NIMBUSEW", 8) == 0 && fread(hdr, 4, 6, f) == 6 &&
+              hdr[0] == 1u && hdr[1] == ctx->rns.N && hdr[2] == ctx->rns.L && hdr[3] == ctx->rns.ell &&
+              fread(pr, 4, ctx->rns.L, f) == ctx->rns.L && memcmp(pr, ctx->rns.p, 4 * ctx->rns.L) == 0 &&
+              fread(&nbytes, 8, 1, f) == 1 && hdr[4] > 0 && hdr[5] > 0 &&
+              nbytes == (uint64_t)hdr[4] * ncols(ctx) * 4;
+    std::vector<uint8_t> host;
+    if (ok) {
+        host.resize(nbytes);
+        ok = fread(host.data(), 1, nbytes, f) == nbytes && fread(&sum, 8, 1, f) == 1 &&
+             sum == fnv1a(host.data(), nbytes);
+    }
+    fclose(f);
+    if (!ok) return set_err(ctx, NIMBUS_EIO, "store file corrupt or made for other parameters");
+    uint32_t* d_canon = nullptr;
+    CK(cudaMalloc(&d_canon, nbytes), "load alloc");
+    cudaError_t e = cudaMemcpy(d_canon, host.data(), nbytes, cudaMemcpyHostToDevice);
+    nimbus_status st = NIMBUS_OK;
+    if (e == cudaSuccess) st = nimbus_encw_import(ctx, d_canon, hdr[4], hdr[5], nullptr, out);
+    if (e == cudaSuccess && st == NIMBUS_OK) e = cudaDeviceSynchronize();
+    cudaFree(d_canon);
+    if (e != cudaSuccess) {
+        if (*out) { nimbus_encw_destroy(*out); *out = nullptr; }
+        return cuda_err(ctx, e, "load import");
+    }
+    return st;
+}
+
 // ---------------------------------------------------------------- online path
 nimbus_status nimbus_cop_out_count(const nimbus_ctx* ctx, uint32_t kq, uint32_t n, uint32_t* n_cts) {
     if (!ctx || !n_cts || kq == 0 || n == 0) return NIMBUS_EINVAL;

@@ -18,7 +18,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, os.environ.get("NIMBUS_LIB", "libnimbus_cop.so"))
 
 STATUS = {0: "NIMBUS_OK", -1: "NIMBUS_EINVAL", -2: "NIMBUS_ESHAPE", -3: "NIMBUS_ERANGE",
-          -4: "NIMBUS_ENOISE", -5: "NIMBUS_ECUDA", -6: "NIMBUS_ENOMEM", -8: "NIMBUS_EARCH"}
+          -4: "NIMBUS_ENOISE", -5: "NIMBUS_ECUDA", -6: "NIMBUS_ENOMEM", -7: "NIMBUS_EIO", -8: "NIMBUS_EARCH"}
 IMPL_TCGEN05, IMPL_CUDACORE = 0, 1
 FLAG_CHECK_RANGE = 1
 FLAG_LARGE_K = 2
@@ -73,6 +73,8 @@ _SIGS = {
     "nimbus_cop_matmul_batch_u64": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_cop_stage_size_u64": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
     "nimbus_cop_matmul_streamed_u64": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp, _sz, _vp]),
+    "nimbus_encw_save": (C.c_int, [_vp, C.c_char_p]),
+    "nimbus_encw_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
     "nimbus_encw_offload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_reload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_is_resident": (C.c_int, [_vp]),
@@ -338,6 +340,20 @@ def nimbus_cop_workspace_size_batch(ctx: Context, jobs) -> int:
 def nimbus_cop_matmul_batch(ctx: Context, jobs, ws: torch.Tensor, stream=None):
     arr = _jobs(jobs)
     _check(lib().nimbus_cop_matmul_batch(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+
+
+def nimbus_encw_save(w: EncW, path: str):
+    _check(lib().nimbus_encw_save(w.ptr, path.encode()), w.owner)
+
+
+def nimbus_encw_load(ctx: Context, path: str, m: int = None, n: int = None) -> EncW:
+    """Enc(W) from a store file; m, n are read from the file (the arguments only label the handle)."""
+    out = C.c_void_p()
+    _check(lib().nimbus_encw_load(ctx.ptr, path.encode(), C.byref(out)), ctx)
+    import struct
+    with open(path, "rb") as f:
+        hdr = struct.unpack("<8s6I", f.read(32))
+    return EncW(out, ctx, hdr[5], hdr[6])
 
 
 def nimbus_encw_offload(w: EncW, stream=None):

@@ -608,3 +608,39 @@ def test_ell64_batch_and_streamed_match_single(nb, oracle):
     nb.nimbus_sync(ctx)
     for j, (c0, R0) in zip(jobs, ref):
         assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+
+
+def test_store_file_roundtrip_and_corruption(nb, oracle, tmp_path):
+    """Enc(W) store file: save -> load gives the same
+    canonical Enc(W) and the same matmul outputs; a flipped payload byte, a
+    truncated file or a context with other parameters are refused with NIMBUS_EIO."""
+    ctx = nb.nimbus_ctx_create(1024, 2, 16, 1)
+    sk = nb.nimbus_keygen(ctx, 3)
+    W = ni.gen_W(5, 200, 300, 16)
+    w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W), 5)
+    path = str(tmp_path / "encw.nimbus")
+    nb.nimbus_encw_save(w, path)
+    w2 = nb.nimbus_encw_load(ctx, path)
+    assert (w2.m, w2.n) == (200, 300)
+    assert torch.equal(nb.nimbus_encw_export(w2), nb.nimbus_encw_export(w))
+    X = dev_u32(ni.gen_X(6, 20, 200, 16))
+    ws = nb.alloc_workspace(ctx, w, 20)
+    c1, R1 = nb.alloc_outputs(ctx, w, 20, 1)
+    c2, R2 = nb.alloc_outputs(ctx, w2, 20, 1)
+    nb.nimbus_cop_matmul(ctx, w, X, 20, 1, 7, c1, R1, ws)
+    nb.nimbus_cop_matmul(ctx, w2, X, 20, 1, 7, c2, R2, ws)
+    nb.nimbus_sync(ctx)
+    assert torch.equal(c1, c2) and torch.equal(R1, R2)
+    raw = open(path, "rb").read()
+    bad = bytearray(raw)
+    bad[100] ^= 1
+    open(str(tmp_path / "flip"), "wb").write(bytes(bad))
+    open(str(tmp_path / "trunc"), "wb").write(raw[:-9])
+    for p in ("flip", "trunc", "missing"):
+        with pytest.raises(nb.NimbusError) as e:
+            nb.nimbus_encw_load(ctx, str(tmp_path / p))
+        assert e.value.status == -7
+    other = nb.nimbus_ctx_create(1024, 3, 16, 1)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_encw_load(other, path)
+    assert e.value.status == -7
