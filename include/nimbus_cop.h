@@ -132,10 +132,10 @@ nimbus_status nimbus_encw_save(const nimbus_encw* encw, const char* path);
 nimbus_status nimbus_encw_load(nimbus_ctx* ctx, const char* path, nimbus_encw** out);
 
 /* ---------------------------------------------------------------- online --- */
-/* Number of packed output ciphertexts per query, ceil(k_q / floor(N/n))
- * (Table 1, "Pad with zeros"). */
+/* Number of packed output ciphertexts of a call, n_queries * ceil(k_q / floor(N/n))
+ * (Table 1, "Pad with zeros"; each query packed apart). */
 nimbus_status nimbus_cop_out_count(const nimbus_ctx* ctx, uint32_t k_per_query, uint32_t n,
-                                   uint32_t* n_cts);
+                                   uint32_t n_queries, uint32_t* n_cts);
 /* Device workspace bytes needed by nimbus_cop_matmul / nimbus_cop_accumulate
  * for k = n_queries * k_per_query rows. */
 nimbus_status nimbus_cop_workspace_size(const nimbus_ctx* ctx, const nimbus_encw* encw, uint32_t k,
@@ -253,11 +253,11 @@ nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t k_p
  *  d_cts  as written by nimbus_cop_matmul;  d_Z  k x n uint32.
  *  d_M    optional (may be NULL): n_queries x n_cts x N full decrypted slots. */
 nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts,
-                             uint32_t k_per_query, uint32_t n_queries, uint32_t n, uint32_t* d_Z,
+                             uint32_t k_per_query, uint32_t n, uint32_t n_queries, uint32_t* d_Z,
                              uint32_t* d_M, void* stream);
 /* ell > 32: d_Z k x n uint64, d_M (optional) n_queries x n_cts x N uint64. */
 nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts,
-                                 uint32_t k_per_query, uint32_t n_queries, uint32_t n, uint64_t* d_Z,
+                                 uint32_t k_per_query, uint32_t n, uint32_t n_queries, uint64_t* d_Z,
                                  uint64_t* d_M, void* stream);
 
 /* ------------------------------------------------------ server, step 5 --- */

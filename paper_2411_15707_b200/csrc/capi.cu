@@ -476,11 +476,16 @@ nimbus_status nimbus_encw_load(nimbus_ctx* ctx, const char* path, nimbus_encw** 
 }
 
 // ---------------------------------------------------------------- online path
-nimbus_status nimbus_cop_out_count(const nimbus_ctx* ctx, uint32_t kq, uint32_t n, uint32_t* n_cts) {
-    if (!ctx || !n_cts || kq == 0 || n == 0) return NIMBUS_EINVAL;
-    if (n > ctx->rns.N) return NIMBUS_ESHAPE;
+// packed ciphertexts per query: ceil(k_q / floor(N/n))
+static uint32_t cts_per_query(const nimbus_ctx* ctx, uint32_t kq, uint32_t n) {
     const uint32_t R = ctx->rns.N / n;
-    *n_cts = (kq + R - 1) / R;
+    return (kq + R - 1) / R;
+}
+
+nimbus_status nimbus_cop_out_count(const nimbus_ctx* ctx, uint32_t kq, uint32_t n, uint32_t nq, uint32_t* n_cts) {
+    if (!ctx || !n_cts || kq == 0 || n == 0 || nq == 0) return NIMBUS_EINVAL;
+    if (n > ctx->rns.N) return NIMBUS_ESHAPE;
+    *n_cts = nq * cts_per_query(ctx, kq, n);
     return NIMBUS_OK;
 }
 
@@ -884,8 +889,7 @@ static nimbus_status cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, cons
     void* dX = ws + L.stage_x;
     uint32_t* dcts = reinterpret_cast<uint32_t*>(ws + L.stage_cts);
     void* dR = ws + L.stage_r;
-    uint32_t nct = 0;
-    nimbus_cop_out_count(ctx, kq, w->n, &nct);
+    const uint32_t nct = cts_per_query(ctx, kq, w->n);
     const size_t cts_bytes = (size_t)nq * nct * 2 * ctx->rns.L_out * ctx->rns.N * 4;
     // R depends only on the mask seed: generate and download it on the side stream while
     // `stream` uploads X and runs the matmul (whose pack then skips R)
@@ -926,13 +930,12 @@ nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* w, 
     return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
 }
 
-static nimbus_status decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
-                             uint32_t n, void* d_Z, void* d_M, void* stream) {
+static nimbus_status decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t n,
+                             uint32_t nq, void* d_Z, void* d_M, void* stream) {
     if (!ctx || !sk || !d_cts || !d_Z || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
     cudaStream_t s = (cudaStream_t)stream;
-    uint32_t nct = 0;
-    nimbus_cop_out_count(ctx, kq, n, &nct);
+    const uint32_t nct = cts_per_query(ctx, kq, n);
     uint32_t* U = nullptr;
     CK(cudaMallocAsync(&U, (size_t)nq * nct * ctx->rns.L_out * ctx->rns.N * 4, s), "decrypt alloc");
     cudaError_t e = launch_decrypt(ctx, sk->d_s_ntt, d_cts, nq * nct, nct, kq, n, U, d_Z, d_M, s);
@@ -941,18 +944,18 @@ static nimbus_status decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_
     return NIMBUS_OK;
 }
 
-nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
-                             uint32_t n, uint32_t* d_Z, uint32_t* d_M, void* stream) {
+nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t n,
+                             uint32_t nq, uint32_t* d_Z, uint32_t* d_M, void* stream) {
     DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 4);
-    return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, nq, n, d_Z, d_M, stream);
+    return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, n, nq, d_Z, d_M, stream);
 }
 
 nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq,
-                                 uint32_t nq, uint32_t n, uint64_t* d_Z, uint64_t* d_M, void* stream) {
+                                 uint32_t n, uint32_t nq, uint64_t* d_Z, uint64_t* d_M, void* stream) {
     DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 8);
-    return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, nq, n, d_Z, d_M, stream);
+    return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, n, nq, d_Z, d_M, stream);
 }
 
 // ---------------------------------------------------------------- server, step 5

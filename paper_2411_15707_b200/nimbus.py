@@ -51,7 +51,7 @@ _SIGS = {
     "nimbus_encw_bytes": (_sz, [_vp]),
     "nimbus_encw_export": (C.c_int, [_vp, _vp, _vp]),
     "nimbus_encw_import": (C.c_int, [_vp, _vp, _u32, _u32, _vp, C.POINTER(_vp)]),
-    "nimbus_cop_out_count": (C.c_int, [_vp, _u32, _u32, C.POINTER(_u32)]),
+    "nimbus_cop_out_count": (C.c_int, [_vp, _u32, _u32, _u32, C.POINTER(_u32)]),
     "nimbus_cop_workspace_size": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
     "nimbus_cop_matmul": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
     "nimbus_cop_matmul_host": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
@@ -261,9 +261,10 @@ def nimbus_encw_import(ctx: Context, canon: torch.Tensor, n: int, stream=None) -
     return EncW(out, ctx, m, n)
 
 
-def nimbus_cop_out_count(ctx: Context, k_per_query: int, n: int) -> int:
+def nimbus_cop_out_count(ctx: Context, k_per_query: int, n: int, n_queries: int = 1) -> int:
+    """Packed output ciphertexts of a call (per query with the default n_queries = 1)."""
     out = _u32()
-    _check(lib().nimbus_cop_out_count(ctx.ptr, k_per_query, n, C.byref(out)), ctx)
+    _check(lib().nimbus_cop_out_count(ctx.ptr, k_per_query, n, n_queries, C.byref(out)), ctx)
     return int(out.value)
 
 
@@ -459,8 +460,8 @@ def nimbus_decrypt(ctx: Context, sk: SecretKey, cts: torch.Tensor, k_per_query: 
     if want_full:
         nct = nimbus_cop_out_count(ctx, k_per_query, n)
         M = torch.empty((n_queries * nct, ctx.N), dtype=torch.int32, device=cts.device)
-    _check(lib().nimbus_decrypt(ctx.ptr, sk.ptr, _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
-                                n, _ptr(Z), _ptr(M) if M is not None else None, _stream(stream)), ctx)
+    _check(lib().nimbus_decrypt(ctx.ptr, sk.ptr, _ptr(cts, torch.int32, "cts"), k_per_query, n,
+                                n_queries, _ptr(Z), _ptr(M) if M is not None else None, _stream(stream)), ctx)
     return Z, M
 
 
@@ -471,8 +472,8 @@ def nimbus_decrypt_u64(ctx: Context, sk: SecretKey, cts: torch.Tensor, k_per_que
     if want_full:
         nct = nimbus_cop_out_count(ctx, k_per_query, n)
         M = torch.empty((n_queries * nct, ctx.N), dtype=torch.int64, device=cts.device)
-    _check(lib().nimbus_decrypt_u64(ctx.ptr, sk.ptr, _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
-                                    n, _ptr(Z), _ptr(M) if M is not None else None, _stream(stream)), ctx)
+    _check(lib().nimbus_decrypt_u64(ctx.ptr, sk.ptr, _ptr(cts, torch.int32, "cts"), k_per_query, n,
+                                    n_queries, _ptr(Z), _ptr(M) if M is not None else None, _stream(stream)), ctx)
     return Z, M
 
 
