@@ -228,8 +228,12 @@ __device__ __forceinline__ void st_dsmem(uint32_t a, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
 }
 
+// With one output limb (L_out = 1, ell <= 32) the rounding and unpacking of
+// k_decrypt_round are done here too (Z, M non-null; U unused): q' = p_0, so
+// m = floor((2 t u + p_0) / (2 p_0)) fits 64-bit arithmetic.
 __global__ void __launch_bounds__(256) k_decrypt_cl(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt,
-                                                   const uint32_t* cts, uint32_t* U) {
+                                                   const uint32_t* cts, uint32_t* U, uint32_t nct, uint32_t kq,
+                                                   uint32_t n, uint32_t* Z, uint32_t* M) {
     extern __shared__ uint32_t sa[];
     const uint32_t N = R.N, Q = N / kDecCl, logQ = R.logN - 2, Lo = R.L_out;
     const uint32_t r = cluster_ctarank(), tg = blockIdx.x / kDecCl, i = blockIdx.y, p = R.p[i];
@@ -290,6 +294,18 @@ __global__ void __launch_bounds__(256) k_decrypt_cl(Rns R, const uint32_t* d_tw,
         }
     }
     cluster_sync();
+    if (Z) {                                  // L_out = 1: round and unpack here
+        const uint32_t ell = R.ell, Rr = N / n, theta = tg % nct, query = tg / nct;
+        const uint32_t rows = min(Rr, kq - theta * Rr);
+        const uint64_t tmask = (1ULL << ell) - 1;
+        for (uint32_t j = threadIdx.x; j < Q; j += blockDim.x) {
+            const uint32_t J = r * Q + j, u = submod(b[j], sa[j], p);
+            const uint32_t m = (uint32_t)(((((uint64_t)u << (ell + 1)) + p) / (2ULL * p)) & tmask);
+            if (M) M[(size_t)tg * N + J] = m;
+            if (J < rows * n) Z[((size_t)query * kq + theta * Rr) * n + J] = m;
+        }
+        return;
+    }
     uint32_t* u = U + ((size_t)tg * Lo + i) * N + r * Q;
     for (uint32_t j = threadIdx.x; j < Q; j += blockDim.x) u[j] = submod(b[j], sa[j], p);
 }
@@ -411,11 +427,15 @@ cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        // L_out = 1 (ell <= 32): round and unpack inside the cluster kernel
+        const bool fused = c->rns.L_out == 1 && elem_bytes(c->rns.ell) == 4;
         cudaError_t e0 = cudaLaunchKernelEx(&cfg, k_decrypt_cl, c->rns, (const uint32_t*)c->d_tw, d_s_ntt, cts,
-                                            d_u_tmp);
+                                            d_u_tmp, nct, kq, n, fused ? static_cast<uint32_t*>(d_Z) : nullptr,
+                                            fused ? static_cast<uint32_t*>(d_M) : nullptr);
         if (e0 != cudaSuccess) return e0;
+        c->launches++;
+        if (fused) return cudaGetLastError();
     }
-    c->launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // Garner constants
