@@ -352,9 +352,22 @@ static uint32_t mask_value(uint64_t seed, uint64_t theta_global, uint32_t N, uin
 /* Full client pipeline for n_queries queries of kq rows each, from the
  * unpacked C of step 2.  Output cts[query][theta][comp][limb < L_out][N]
  * and R[alpha][j] (alpha over all k = n_queries*kq rows, j < n) = Y_c. */
+void orc_pack_moddown_mask_rr(uint32_t N, uint32_t L, uint32_t L_out, const uint32_t* primes, uint32_t ell,
+                              const uint32_t* C, uint32_t kq, uint32_t n_queries, uint32_t n,
+                              uint64_t mask_seed, const uint32_t* Z0, uint32_t* cts, uint32_t* Rout);
 void orc_pack_moddown_mask(uint32_t N, uint32_t L, uint32_t L_out, const uint32_t* primes, uint32_t ell,
                            const uint32_t* C, uint32_t kq, uint32_t n_queries, uint32_t n,
                            uint64_t mask_seed, uint32_t* cts, uint32_t* Rout) {
+    orc_pack_moddown_mask_rr(N, L, L_out, primes, ell, C, kq, n_queries, n, mask_seed, NULL, cts, Rout);
+}
+
+/* Same, with circuit privacy (reading 26): when Z0 is not NULL the
+ * packed ciphertext tg first gets the public-key encryption of zero
+ * Z0[tg][comp][limb][J] (orc_rerand_zero) added at the full modulus q, then
+ * ModDown and mask as above. */
+void orc_pack_moddown_mask_rr(uint32_t N, uint32_t L, uint32_t L_out, const uint32_t* primes, uint32_t ell,
+                              const uint32_t* C, uint32_t kq, uint32_t n_queries, uint32_t n,
+                              uint64_t mask_seed, const uint32_t* Z0, uint32_t* cts, uint32_t* Rout) {
     uint32_t R = rows_per_ct(N, n), nct = orc_cts_per_query(N, n, kq);
     u128 qp = prod_q(primes, L_out);
     #pragma omp parallel for schedule(dynamic)
@@ -364,7 +377,11 @@ void orc_pack_moddown_mask(uint32_t N, uint32_t L, uint32_t L_out, const uint32_
         for (uint32_t J = 0; J < N; J++) {
             uint32_t r = mask_value(mask_seed, (uint64_t)tg, N, J, ell);
             for (uint32_t comp = 0; comp < 2; comp++) {
-                for (uint32_t i = 0; i < L; i++) res[i] = pack_coef(N, L, primes, C, n, kq, query, theta, comp, i, J);
+                for (uint32_t i = 0; i < L; i++) {
+                    res[i] = pack_coef(N, L, primes, C, n, kq, query, theta, comp, i, J);
+                    if (Z0)
+                        res[i] = (uint32_t)(((uint64_t)res[i] + Z0[(((uint64_t)tg * 2 + comp) * L + i) * N + J]) % primes[i]);
+                }
                 moddown_coef(res, L, L_out, primes);
                 for (uint32_t i = 0; i < L_out; i++) {
                     uint32_t v = res[i];
@@ -393,6 +410,78 @@ void orc_cop_matmul(uint32_t N, uint32_t L, uint32_t L_out, const uint32_t* prim
     orc_cop_accumulate(N, L, primes, encW, X, (uint32_t)k, m, C);
     orc_pack_moddown_mask(N, L, L_out, primes, ell, C, kq, n_queries, n, mask_seed, cts, Rout);
     free(C);
+}
+
+/* Steps 2-4 with the re-randomisation of reading 26 (Z0 from orc_rerand_zero). */
+void orc_cop_matmul_rr(uint32_t N, uint32_t L, uint32_t L_out, const uint32_t* primes, uint32_t ell,
+                       const uint32_t* encW, uint32_t m, uint32_t n, const uint32_t* X, uint32_t kq,
+                       uint32_t n_queries, uint64_t mask_seed, const uint32_t* Z0, uint32_t* cts, uint32_t* Rout) {
+    uint64_t k = (uint64_t)kq * n_queries;
+    uint32_t* C = (uint32_t*)malloc(4ULL * k * 2 * L * N);
+    orc_cop_accumulate(N, L, primes, encW, X, (uint32_t)k, m, C);
+    orc_pack_moddown_mask_rr(N, L, L_out, primes, ell, C, kq, n_queries, n, mask_seed, Z0, cts, Rout);
+    free(C);
+}
+
+/* Public key ("KeyGen. Generate the RLWE key pair (sk, pk)",
+ * PAPER.md:603 encryption "under a key pk"; reading 25):
+ *   a_pk[i] = uniform mod p_i (domain 7, index i N + j),  e_pk = CBD(21) (domain 8, index j),
+ *   b_pk[i] = a_pk[i] * s + e_pk  mod p_i   (negacyclic product, as in Encrypt).
+ * Output pk[comp b=0, a=1][limb][j]. */
+void orc_keygen_pk(uint32_t N, uint32_t L, const uint32_t* primes, const int8_t* s, uint64_t seed, uint32_t* pk) {
+    uint32_t* a = (uint32_t*)malloc(4ULL * N);
+    uint32_t* sp = (uint32_t*)malloc(4ULL * N);
+    uint32_t* as = (uint32_t*)malloc(4ULL * N);
+    for (uint32_t i = 0; i < L; i++) {
+        uint32_t p = primes[i];
+        for (uint32_t j = 0; j < N; j++) {
+            a[j] = uniform_mod(orc_word(seed, 7, (uint64_t)i * N + j), p);
+            sp[j] = smod(s[j], p);
+        }
+        orc_negacyclic_ntt(N, p, a, sp, as);
+        for (uint32_t j = 0; j < N; j++) {
+            int32_t e = cbd21(orc_word(seed, 8, j));
+            pk[(0 * (uint64_t)L + i) * N + j] = (uint32_t)(((uint64_t)as[j] + smod(e, p)) % p);
+            pk[(1 * (uint64_t)L + i) * N + j] = a[j];
+        }
+    }
+    free(a); free(sp); free(as);
+}
+
+/* Flooding noise f uniform in [-2^F, 2^F) from one PRG word (F = 0: no flooding). */
+static int64_t flood(uint64_t w, uint32_t F) {
+    if (F == 0) return 0;
+    return (int64_t)(w >> (63 - F)) - ((int64_t)1 << F);
+}
+
+/* Circuit privacy (the client's output ciphertext must not reveal
+ * X_c to the key owner; reading 26): a fresh public-key encryption of
+ * zero per packed ciphertext g, at the full modulus q:
+ *   v = ternary (domain 9, index g N + j), e1, e2 = CBD(21) (domains 10, 11, index g N + j),
+ *   f = flooding noise in [-2^F, 2^F) (domain 12, index g N + j),
+ *   z_b[i] = v * b_pk[i] + e1 + f,  z_a[i] = v * a_pk[i] + e2  mod p_i.
+ * It decrypts to v e_pk + e1 + f - e2 s (message 0).  Output z[g][comp][limb][j]. */
+void orc_rerand_zero(uint32_t N, uint32_t L, const uint32_t* primes, const uint32_t* pk, uint64_t seed,
+                     uint32_t n_cts, uint32_t F, uint32_t* z) {
+    #pragma omp parallel for schedule(dynamic)
+    for (int64_t g = 0; g < (int64_t)n_cts; g++) {
+        uint32_t* vp = (uint32_t*)malloc(4ULL * N);
+        uint32_t* prod = (uint32_t*)malloc(4ULL * N);
+        for (uint32_t i = 0; i < L; i++) {
+            uint32_t p = primes[i];
+            for (uint32_t j = 0; j < N; j++) vp[j] = smod(ternary(orc_word(seed, 9, (uint64_t)g * N + j)), p);
+            for (uint32_t comp = 0; comp < 2; comp++) {
+                orc_negacyclic_ntt(N, p, pk + ((uint64_t)comp * L + i) * N, vp, prod);
+                for (uint32_t j = 0; j < N; j++) {
+                    uint64_t idx = (uint64_t)g * N + j;
+                    int64_t e = comp == 0 ? (int64_t)cbd21(orc_word(seed, 10, idx)) + flood(orc_word(seed, 12, idx), F)
+                                          : (int64_t)cbd21(orc_word(seed, 11, idx));
+                    z[(((uint64_t)g * 2 + comp) * L + i) * N + j] = (uint32_t)(((uint64_t)prod[j] + smod(e, p)) % p);
+                }
+            }
+        }
+        free(vp); free(prod);
+    }
 }
 
 /* Sampled version for workloads too large for the full oracle: for each

@@ -74,6 +74,15 @@ def lib():
         L.orc_decrypt_unpack.argtypes = [C.c_uint32, C.c_uint32, u32p, C.c_uint32, i8p, u32p,
                                          C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_void_p,
                                          C.POINTER(C.c_double)]
+        L.orc_pack_moddown_mask_rr.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_uint32,
+                                               u32p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                               C.c_void_p, u32p, u32p]
+        L.orc_cop_matmul_rr.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_uint32, u32p,
+                                        C.c_uint32, C.c_uint32, u32p, C.c_uint32, C.c_uint32,
+                                        C.c_uint64, u32p, u32p, u32p]
+        L.orc_keygen_pk.argtypes = [C.c_uint32, C.c_uint32, u32p, i8p, C.c_uint64, u32p]
+        L.orc_rerand_zero.argtypes = [C.c_uint32, C.c_uint32, u32p, u32p, C.c_uint64, C.c_uint32,
+                                      C.c_uint32, u32p]
         L.orc_emb.argtypes = [u32p, C.c_uint32, C.c_uint32, C.c_uint64, u32p]
         L.orc_moddown.argtypes = [u32p, C.c_uint32, C.c_uint32, u32p]
         L.orc_sample_uniform_mod.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
@@ -172,6 +181,34 @@ def cop_matmul(N, L, L_out, pr, ell, encW, X, n, kq, n_queries, mask_seed):
     R = np.zeros((n_queries * kq, n), np.uint32)
     lib().orc_cop_matmul(N, L, L_out, _u32(pr), ell, encW, m, n, X, kq, n_queries, mask_seed,
                          cts, R)
+    return cts, R
+
+
+def keygen_pk(N, L, pr, s, seed) -> np.ndarray:
+    """Public key pk[comp b=0, a=1][limb][j] (reading 25)."""
+    pk = np.empty((2, L, N), np.uint32)
+    lib().orc_keygen_pk(N, L, _u32(pr), np.ascontiguousarray(s, np.int8), seed, pk)
+    return pk
+
+
+def rerand_zero(N, L, pr, pk, seed, n_cts, flood_bits) -> np.ndarray:
+    """Public-key encryptions of zero z[g][comp][limb][j] for circuit privacy
+    (reading 26)."""
+    z = np.empty((n_cts, 2, L, N), np.uint32)
+    lib().orc_rerand_zero(N, L, _u32(pr), _u32(pk), seed, n_cts, flood_bits, z)
+    return z
+
+
+def cop_matmul_rr(N, L, L_out, pr, ell, encW, X, n, kq, n_queries, mask_seed, Z0):
+    """Alg. 1 steps 2-4 with the zero encryptions Z0 added before ModDown."""
+    encW = _u32(encW)
+    X = _u32(X)
+    m = encW.shape[0]
+    nct = cts_per_query(N, n, kq)
+    cts = np.empty((n_queries, nct, 2, L_out, N), np.uint32)
+    R = np.zeros((n_queries * kq, n), np.uint32)
+    lib().orc_cop_matmul_rr(N, L, L_out, _u32(pr), ell, encW, m, n, X, kq, n_queries, mask_seed,
+                            _u32(Z0), cts, R)
     return cts, R
 
 

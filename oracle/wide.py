@@ -71,11 +71,13 @@ def _moddown(c: list, pr: list, L_out: int) -> list:
     return res
 
 
-def cop_matmul(N, L, L_out, pr, ell, E, X, n, kq, nq, seed):
+def cop_matmul(N, L, L_out, pr, ell, E, X, n, kq, nq, seed, Z0=None):
     """Alg. 1 steps 2-4: c[alpha] = sum_beta x (x) Enc(W_beta)
     per limb mod p_i; RShift packing with stride n; ModDown to
     L_out limbs; mask r_theta[J] = word(seed, 6, tg N + J) >> (64 - ell) subtracted
-    from b as Emb_q'(r).  Returns (cts [nq][nct][2][L_out][N] uint32, R [k][n] uint64)."""
+    from b as Emb_q'(r).  Z0 (optional, [nq*nct][2][L][N]): public-key encryptions of
+    zero added before ModDown (circuit privacy, reading 26).
+    Returns (cts [nq][nct][2][L_out][N] uint32, R [k][n] uint64)."""
     pr = [int(p) for p in pr]
     t = 1 << ell
     X = np.asarray(X, dtype=np.uint64)
@@ -108,6 +110,8 @@ def cop_matmul(N, L, L_out, pr, ell, E, X, n, kq, nq, seed):
                             sh = r * n
                             val = int(C[q_ * kq + th * R_ + r, comp, i, (J - sh) % N])
                             v += val if J >= sh else p - val
+                        if Z0 is not None:
+                            v += int(Z0[tg, comp, i, J])
                         c.append(v % p)
                     c = _moddown(c, pr, L_out)
                     if comp == 0:
