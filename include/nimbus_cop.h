@@ -70,6 +70,7 @@ typedef struct nimbus_ctx nimbus_ctx;
 typedef struct nimbus_sk nimbus_sk;
 typedef struct nimbus_encw nimbus_encw;
 typedef struct nimbus_plainw nimbus_plainw;
+typedef struct nimbus_pk nimbus_pk;
 
 /* Context: validates params, derives the primes (the L largest p < 2^31 with
  * p = 1 mod 2N), uploads NTT twiddles and RNS constants to
@@ -92,6 +93,18 @@ nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus
 void nimbus_sk_destroy(nimbus_sk* sk);
 /* Copies s (N int8 values in {-1,0,1}) to d_s. */
 nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream);
+
+/* Public key ("KeyGen. Generate the RLWE key pair (sk, pk)";
+ * DESIGN.md reading 25), for the client's re-randomisation below:
+ *   a_i = uniform mod p_i (PRG domain 7, index i N + j), e = CBD(21) (domain 8, index j),
+ *   b_i = a_i s + e mod p_i.
+ * The handle owns the key on the device (coefficients and NTT form).
+ * export: d_out 2 x L x N uint32 [comp b=0, a=1][limb][j] (what the server sends);
+ * import: the same layout, entries must be residues < p_i (not checked). */
+nimbus_status nimbus_keygen_pk(nimbus_ctx* ctx, const nimbus_sk* sk, uint64_t seed, void* stream, nimbus_pk** out);
+void nimbus_pk_destroy(nimbus_pk* pk);
+nimbus_status nimbus_pk_export(const nimbus_pk* pk, uint32_t* d_out, void* stream);
+nimbus_status nimbus_pk_import(nimbus_ctx* ctx, const uint32_t* d_in, void* stream, nimbus_pk** out);
 
 /* Alg. 1 step 1, server side: row-wise encode each weight row
  * (Eq. 2: w_hat[j] = W[beta][j] for j < n, 0 beyond) and
@@ -163,6 +176,37 @@ nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* encw, co
                                     uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
                                     uint32_t* d_cts, uint64_t* d_R, void* d_ws, size_t ws_bytes,
                                     void* stream);
+
+/* Circuit privacy of the client's output (the key owner must learn
+ * nothing about X_c from the ciphertexts it decrypts; reading 26).
+ * Offline, input-independent: nimbus_rerand_prepare writes one public-key
+ * encryption of zero per output ciphertext,
+ *   z_b = v b_pk + e1 + f,  z_a = v a_pk + e2  (mod each of the L primes),
+ *   v ternary (domain 9), e1, e2 CBD(21) (domains 10, 11), f uniform in
+ *   [-2^F, 2^F) (domain 12, F = flood_bits, 0 = none); PRG index g N + j for
+ *   output ciphertext g (query-major, as d_cts).
+ * Online, nimbus_cop_matmul_rr is nimbus_cop_matmul with z[g] added to packed
+ * ciphertext g at the full modulus, before the mod-switch: the output's a
+ * component is re-randomised, its noise grows by at most 2 eta N + eta + 2^F
+ * before the limb drops, and it decrypts to the same (X.W - R) mod t.
+ *  d_zero   n_cts x 2 x L x N uint32 [g][comp][limb][j] (n_cts of nimbus_cop_out_count);
+ *           prepare it with the same encw, k_per_query, n_queries, and a fresh seed per call.
+ * nimbus_rerand_flood_max: the largest F (<= 62) that keeps decryption exact for
+ * this encw and k_per_query (NIMBUS_ENOISE if none); prepare returns NIMBUS_ENOISE
+ * for a larger F. */
+nimbus_status nimbus_rerand_flood_max(const nimbus_ctx* ctx, const nimbus_encw* encw, uint32_t k_per_query,
+                                      uint32_t* flood_bits);
+nimbus_status nimbus_rerand_prepare(nimbus_ctx* ctx, const nimbus_pk* pk, const nimbus_encw* encw,
+                                    uint32_t k_per_query, uint32_t n_queries, uint64_t seed, uint32_t flood_bits,
+                                    uint32_t* d_zero, void* stream);
+nimbus_status nimbus_cop_matmul_rr(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* d_X,
+                                   uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
+                                   const uint32_t* d_zero, uint32_t* d_cts, uint32_t* d_R, void* d_ws,
+                                   size_t ws_bytes, void* stream);
+nimbus_status nimbus_cop_matmul_rr_u64(nimbus_ctx* ctx, const nimbus_encw* encw, const uint64_t* d_X,
+                                       uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
+                                       const uint32_t* d_zero, uint32_t* d_cts, uint64_t* d_R, void* d_ws,
+                                       size_t ws_bytes, void* stream);
 
 /* A sequence of COP matmuls (e.g. all linear layers of a model pass, SURVEY.md
  * config C5): equivalent to nimbus_cop_matmul for jobs[0..count-1] in order,

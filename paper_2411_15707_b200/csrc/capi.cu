@@ -86,11 +86,14 @@ static int big_cmp(const Big& a, const Big& b) {
 // Worst-case decryption bound (SURVEY.md §8(c) "Worst-case noise guarantee"),
 // in integer upper bounds on 2|v|:  fresh+COP+packing 2v <= R m (t-1)(2 eta + 1);
 // each limb drop v -> v/p + (1+N)/2; the mask adds 1/2.  Requires 2|v| t < q.
-static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff) {
+// extra2: a further bound on 2|v| added before the mod-switch (the public-key zero
+// encryption of reading 26: 2 |v e_pk + e1 + f - e2 s| <= 4 eta N + 2 eta + 2^(F+1)).
+static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff, uint64_t extra2 = 0) {
     const uint32_t ell = c->rns.ell, N = c->rns.N;
     const uint64_t tm1 = ell >= 64 ? ~0ULL : (1ULL << ell) - 1;
     Big B = big_of((u128)R_eff * m * 43u);      // 2 eta + 1 = 43 for CBD(21)
     big_mul(B, tm1);
+    big_add(B, extra2);
     Big Bt = B;
     big_shl(Bt, ell);
     if (big_cmp(Bt, c->q) >= 0) return false;
@@ -276,6 +279,60 @@ nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream) {
     if (!sk || !d_s) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = sk->ctx;
     CK(cudaMemcpyAsync(d_s, sk->d_s, ctx->rns.N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "sk export");
+    return NIMBUS_OK;
+}
+
+// ---------------------------------------------------------------- public key (reading 25)
+nimbus_status nimbus_keygen_pk(nimbus_ctx* ctx, const nimbus_sk* sk, uint64_t seed, void* stream, nimbus_pk** out) {
+    DevGuard dg_(ctx);
+    if (!ctx || !sk || !out || sk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    *out = nullptr;
+    nimbus_pk* pk = new (std::nothrow) nimbus_pk();
+    if (!pk) return NIMBUS_ENOMEM;
+    pk->ctx = ctx;
+    const size_t words = 2ull * ctx->rns.L * ctx->rns.N;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMalloc(&pk->d_pk, words * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&pk->d_pk_ntt, words * 4);
+    if (e == cudaSuccess) e = launch_keygen_pk(ctx, sk->d_s_ntt, seed, pk->d_pk, st);
+    if (e == cudaSuccess) e = launch_ntt_rows(ctx, pk->d_pk, 2, pk->d_pk_ntt, st);
+    if (e != cudaSuccess) { nimbus_pk_destroy(pk); return cuda_err(ctx, e, "keygen_pk"); }
+    *out = pk;
+    return NIMBUS_OK;
+}
+
+void nimbus_pk_destroy(nimbus_pk* pk) {
+    DevGuard dg_(pk ? pk->ctx : nullptr);
+    if (!pk) return;
+    if (pk->d_pk) cudaFree(pk->d_pk);
+    if (pk->d_pk_ntt) cudaFree(pk->d_pk_ntt);
+    delete pk;
+}
+
+nimbus_status nimbus_pk_export(const nimbus_pk* pk, uint32_t* d_out, void* stream) {
+    DevGuard dg_(pk ? pk->ctx : nullptr);
+    if (!pk || !d_out) return NIMBUS_EINVAL;
+    nimbus_ctx* ctx = pk->ctx;
+    CK(cudaMemcpyAsync(d_out, pk->d_pk, 2ull * ctx->rns.L * ctx->rns.N * 4, cudaMemcpyDeviceToDevice,
+                       (cudaStream_t)stream), "pk export");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_pk_import(nimbus_ctx* ctx, const uint32_t* d_in, void* stream, nimbus_pk** out) {
+    DevGuard dg_(ctx);
+    if (!ctx || !d_in || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    *out = nullptr;
+    nimbus_pk* pk = new (std::nothrow) nimbus_pk();
+    if (!pk) return NIMBUS_ENOMEM;
+    pk->ctx = ctx;
+    const size_t words = 2ull * ctx->rns.L * ctx->rns.N;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMalloc(&pk->d_pk, words * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&pk->d_pk_ntt, words * 4);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pk->d_pk, d_in, words * 4, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = launch_ntt_rows(ctx, pk->d_pk, 2, pk->d_pk_ntt, st);
+    if (e != cudaSuccess) { nimbus_pk_destroy(pk); return cuda_err(ctx, e, "pk import"); }
+    *out = pk;
     return NIMBUS_OK;
 }
 
@@ -586,7 +643,8 @@ nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq,
 // allow_no_R: d_R may be null (the host-buffer call produces R separately)
 static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const void* d_X, uint32_t kq,
                                 uint32_t nq, uint64_t seed, uint32_t* d_cts, void* d_R, void* d_ws,
-                                size_t ws_bytes, void* stream, bool allow_no_R = false) {
+                                size_t ws_bytes, void* stream, bool allow_no_R = false,
+                                const uint32_t* d_zero = nullptr) {
     nimbus_status st = check_online(ctx, w, kq, nq);
     if (st != NIMBUS_OK) return st;
     if (!d_X || !d_cts || (!d_R && !allow_no_R) || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
@@ -600,7 +658,7 @@ static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const voi
     if (st != NIMBUS_OK) return st;
     prof_mark(ctx, s);
     prof_mark(ctx, s);
-    CK(launch_pack(ctx, C, kq, nq, w->n, seed, d_cts, d_R, s, true), "pack");
+    CK(launch_pack(ctx, C, kq, nq, w->n, seed, d_cts, d_R, s, true, d_zero), "pack");
     prof_mark(ctx, s);
     return NIMBUS_OK;
 }
@@ -619,6 +677,56 @@ nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* w, const
     DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream);
+}
+
+// ---------------------------------------------------------------- circuit privacy (reading 26)
+static uint64_t rerand_extra2(const nimbus_ctx* ctx, uint32_t F) {
+    return 84ull * ctx->rns.N + 42 + (F ? (2ull << F) : 0);
+}
+
+nimbus_status nimbus_rerand_flood_max(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t kq, uint32_t* bits) {
+    if (!ctx || !w || !bits || w->ctx != ctx || kq == 0) return NIMBUS_EINVAL;
+    const uint32_t R = ctx->rns.N / w->n, Reff = kq < R ? kq : R;
+    for (uint32_t F = 62; F >= 1; F--)
+        if (noise_ok(ctx, w->m, Reff, rerand_extra2(ctx, F))) { *bits = F; return NIMBUS_OK; }
+    if (noise_ok(ctx, w->m, Reff, rerand_extra2(ctx, 0))) { *bits = 0; return NIMBUS_OK; }
+    return NIMBUS_ENOISE;
+}
+
+nimbus_status nimbus_rerand_prepare(nimbus_ctx* ctx, const nimbus_pk* pk, const nimbus_encw* w, uint32_t kq,
+                                    uint32_t nq, uint64_t seed, uint32_t flood_bits, uint32_t* d_zero,
+                                    void* stream) {
+    DevGuard dg_(ctx);
+    if (!ctx || !pk || !w || !d_zero || pk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    nimbus_status st = check_shape(ctx, w, kq, nq);
+    if (st != NIMBUS_OK) return st;
+    if (flood_bits > 62) return set_err(ctx, NIMBUS_EINVAL, "flood_bits > 62");
+    const uint32_t R = ctx->rns.N / w->n, Reff = kq < R ? kq : R;
+    if (!noise_ok(ctx, w->m, Reff, rerand_extra2(ctx, flood_bits)))
+        return set_err(ctx, NIMBUS_ENOISE, "flooding noise exceeds the decryption bound (see nimbus_rerand_flood_max)");
+    const uint32_t n_cts = nq * cts_per_query(ctx, kq, w->n);
+    CK(launch_rerand(ctx, pk->d_pk_ntt, seed, n_cts, flood_bits, d_zero, (cudaStream_t)stream), "rerand");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul_rr(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t kq,
+                                   uint32_t nq, uint64_t seed, const uint32_t* d_zero, uint32_t* d_cts,
+                                   uint32_t* d_R, void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
+    if (!d_zero) return set_err(ctx, NIMBUS_EINVAL, "null zero encryptions");
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st
+                           : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream, false, d_zero);
+}
+
+nimbus_status nimbus_cop_matmul_rr_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* d_X, uint32_t kq,
+                                       uint32_t nq, uint64_t seed, const uint32_t* d_zero, uint32_t* d_cts,
+                                       uint64_t* d_R, void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
+    if (!d_zero) return set_err(ctx, NIMBUS_EINVAL, "null zero encryptions");
+    nimbus_status st = want_width(ctx, 8);
+    return st != NIMBUS_OK ? st
+                           : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream, false, d_zero);
 }
 
 // ---------------------------------------------------------------- batched online path

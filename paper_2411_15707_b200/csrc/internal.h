@@ -59,6 +59,13 @@ struct nimbus_sk {
     uint32_t* d_s_ntt = nullptr;   // L x N, NTT domain (bit-reversed order)
 };
 
+// public key pk = (b, a) (reading 25)
+struct nimbus_pk {
+    nimbus_ctx* ctx = nullptr;
+    uint32_t* d_pk = nullptr;      // [comp b=0, a=1][limb][N] coefficients (the exported form)
+    uint32_t* d_pk_ntt = nullptr;  // same, NTT domain (bit-reversed), for the zero encryptions
+};
+
 struct nimbus_encw {
     nimbus_ctx* ctx = nullptr;
     uint32_t m = 0, n = 0, KB = 0; // KB = ceil(m / 128) k-blocks
@@ -94,6 +101,13 @@ cudaError_t launch_negacyclic_mul(nimbus_ctx* c, const uint32_t* a, const uint32
 cudaError_t launch_decrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const uint32_t* cts, uint32_t nct_total,
                            uint32_t nct, uint32_t kq, uint32_t n, uint32_t* d_u_tmp, void* d_Z,
                            void* d_M, cudaStream_t st);
+// public key (coefficients, [comp][limb][N]) from sk; then launch_ntt_rows for its NTT form
+cudaError_t launch_keygen_pk(nimbus_ctx* c, const uint32_t* d_s_ntt, uint64_t seed, uint32_t* d_pk, cudaStream_t st);
+// forward NTT of `count` x L polynomials [count][L][N] (limb i mod p_i)
+cudaError_t launch_ntt_rows(nimbus_ctx* c, const uint32_t* in, uint32_t count, uint32_t* out, cudaStream_t st);
+// n_cts public-key encryptions of zero [g][comp][limb][N] with F flooding bits (reading 26)
+cudaError_t launch_rerand(nimbus_ctx* c, const uint32_t* d_pk_ntt, uint64_t seed, uint32_t n_cts, uint32_t F,
+                          uint32_t* d_zero, cudaStream_t st);
 cudaError_t launch_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* out,
                              cudaStream_t st);
 // layout.cu
@@ -103,9 +117,11 @@ cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, u
                                uint32_t* d_canon, cudaStream_t st);
 cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st);
-// d_R may be null: then the pack writes only the ciphertexts (R comes from launch_mask_R)
+// d_R may be null: then the pack writes only the ciphertexts (R comes from launch_mask_R).
+// d_zero (nullable): public-key encryptions of zero [tg][comp][L][N] added before ModDown.
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
-                        uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl);
+                        uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl,
+                        const uint32_t* d_zero = nullptr);
 cudaError_t launch_mask_R(nimbus_ctx* c, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed, void* d_R,
                           cudaStream_t st);
 // cop_cc.cu

@@ -169,6 +169,94 @@ __global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, co
     }
 }
 
+// ---------------------------------------------------------------- public key (reading 25)
+// PAPER.md:602 KeyGen "(sk, pk)": limb i = blockIdx.x,
+//   a = uniform mod p_i (domain 7, index i N + j), e = CBD(21) (domain 8, index j),
+//   b = a*s + e mod p_i.  Writes pk[comp b=0, a=1][limb][j] (coefficients).
+__global__ void k_keygen_pk(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, uint64_t seed, uint32_t* pk) {
+    extern __shared__ uint32_t sa[];
+    const uint32_t N = R.N, L = R.L, i = blockIdx.x, p = R.p[i];
+    const uint64_t ka = prg_key(seed, 7), ke = prg_key(seed, 8);
+    uint32_t* bo = pk + (size_t)i * N;
+    uint32_t* ao = pk + ((size_t)L + i) * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+        const uint32_t a = samp_uniform_mod(prg_word(ka, (uint64_t)i * N + j), p);
+        sa[j] = a;
+        ao[j] = a;
+    }
+    TwLimb tw = tw_limb(d_tw, N, i);
+    __syncthreads();
+    ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
+    const uint32_t* sn = s_ntt + (size_t)i * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sn[j], p, R.mu[i]);
+    __syncthreads();
+    ntt_inv_smem(sa, tw.iv, tw.iv_sh, N, R.logN, p, R.ninv[i], R.ninv_sh[i]);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+        const int32_t e = samp_cbd21(prg_word(ke, j));
+        bo[j] = addmod(sa[j], e < 0 ? p - (uint32_t)(-e) : (uint32_t)e, p);
+    }
+}
+
+// forward NTT of polynomial blockIdx.x, limb blockIdx.y of a [count][L][N] array
+__global__ void k_ntt_rows(Rns R, const uint32_t* d_tw, const uint32_t* in, uint32_t* out) {
+    extern __shared__ uint32_t sa[];
+    const uint32_t N = R.N, i = blockIdx.y, p = R.p[i];
+    const size_t off = ((size_t)blockIdx.x * R.L + i) * N;
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = in[off + j];
+    TwLimb tw = tw_limb(d_tw, N, i);
+    __syncthreads();
+    ntt_fwd_smem(sa, tw.fw, tw.fw_sh, N, R.logN, p);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) out[off + j] = sa[j];
+}
+
+// signed 64-bit value mod p
+__device__ __forceinline__ uint32_t smod64(int64_t e, uint32_t p) {
+    const uint64_t mag = e < 0 ? (uint64_t)(-(e + 1)) + 1 : (uint64_t)e;
+    const uint32_t r = (uint32_t)(mag % p);
+    return (e < 0 && r) ? p - r : r;
+}
+
+// ---------------------------------------------------------------- circuit privacy (reading 26)
+// the client's output must not reveal X_c to the key owner.  One
+// public-key encryption of zero per packed ciphertext g = blockIdx.x, limb i = blockIdx.y:
+//   v ternary (domain 9, index g N + j), e1, e2 CBD(21) (domains 10, 11, index g N + j),
+//   f flooding noise (w >> (63 - F)) - 2^F (domain 12; none when F = 0),
+//   z_b = v b_pk + e1 + f,  z_a = v a_pk + e2  mod p_i   ->  z[g][comp][limb][j].
+// Offline (input-independent) work: the online pack only adds z before its ModDown.
+__global__ void k_rerand(Rns R, const uint32_t* d_tw, const uint32_t* pk_ntt, uint64_t seed, uint32_t F,
+                         uint32_t* z) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t N = R.N, L = R.L, g = blockIdx.x, i = blockIdx.y, p = R.p[i];
+    uint32_t *sv = sm, *sp = sm + N;
+    const uint64_t kv = prg_key(seed, 9), k1 = prg_key(seed, 10), k2 = prg_key(seed, 11), kf = prg_key(seed, 12);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+        const int32_t v = samp_ternary(prg_word(kv, (uint64_t)g * N + j));
+        sv[j] = v < 0 ? p - 1 : (uint32_t)v;
+    }
+    TwLimb tw = tw_limb(d_tw, N, i);
+    __syncthreads();
+    ntt_fwd_smem(sv, tw.fw, tw.fw_sh, N, R.logN, p);
+    for (uint32_t comp = 0; comp < 2; comp++) {
+        const uint32_t* pn = pk_ntt + ((size_t)comp * L + i) * N;
+        for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sp[j] = mulmod(sv[j], pn[j], p, R.mu[i]);
+        __syncthreads();
+        ntt_inv_smem(sp, tw.iv, tw.iv_sh, N, R.logN, p, R.ninv[i], R.ninv_sh[i]);
+        uint32_t* zo = z + (((size_t)g * 2 + comp) * L + i) * N;
+        for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+            const uint64_t idx = (uint64_t)g * N + j;
+            int64_t e;
+            if (comp == 0) {
+                e = samp_cbd21(prg_word(k1, idx));
+                if (F) e += (int64_t)(prg_word(kf, idx) >> (63 - F)) - ((int64_t)1 << F);
+            } else {
+                e = samp_cbd21(prg_word(k2, idx));
+            }
+            zo[j] = addmod(sp[j], smod64(e, p), p);
+        }
+        __syncthreads();   // sp is reused by the next component
+    }
+}
+
 // ---------------------------------------------------------------- test helper
 __global__ void k_negacyclic_mul(Rns R, const uint32_t* d_tw, const uint32_t* A, const uint32_t* B,
                                  uint32_t* Cout) {
@@ -394,6 +482,34 @@ cudaError_t launch_encrypt(nimbus_ctx* c, const uint32_t* d_s_ntt, const void* d
     else
         k_encrypt<uint32_t><<<dim3(m, c->rns.L), ntt_threads(N), N * 4, st>>>(
             c->rns, c->d_tw, d_s_ntt, static_cast<const uint32_t*>(d_W), n, seed, d_encW);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_keygen_pk(nimbus_ctx* c, const uint32_t* d_s_ntt, uint64_t seed, uint32_t* d_pk, cudaStream_t st) {
+    const uint32_t N = c->rns.N;
+    cudaError_t e = ntt_smem(k_keygen_pk, N);
+    if (e != cudaSuccess) return e;
+    k_keygen_pk<<<c->rns.L, ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, d_s_ntt, seed, d_pk);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ntt_rows(nimbus_ctx* c, const uint32_t* in, uint32_t count, uint32_t* out, cudaStream_t st) {
+    const uint32_t N = c->rns.N;
+    cudaError_t e = ntt_smem(k_ntt_rows, N);
+    if (e != cudaSuccess) return e;
+    k_ntt_rows<<<dim3(count, c->rns.L), ntt_threads(N), N * 4, st>>>(c->rns, c->d_tw, in, out);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rerand(nimbus_ctx* c, const uint32_t* d_pk_ntt, uint64_t seed, uint32_t n_cts, uint32_t F,
+                          uint32_t* d_zero, cudaStream_t st) {
+    const uint32_t N = c->rns.N;
+    cudaError_t e = ntt_smem(k_rerand, 2 * N);
+    if (e != cudaSuccess) return e;
+    k_rerand<<<dim3(n_cts, c->rns.L), ntt_threads(N), 2 * N * 4, st>>>(c->rns, c->d_tw, d_pk_ntt, seed, F, d_zero);
     c->launches++;
     return cudaGetLastError();
 }

@@ -22,12 +22,13 @@ namespace nimbus {
 template <int V, int L, int RB, typename MT = uint32_t>
 __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                               uint32_t Rr, uint32_t nct, uint64_t key_mask,
-                                              uint32_t* __restrict__ cts, MT* __restrict__ Rout) {
+                                              uint32_t* __restrict__ cts, MT* __restrict__ Rout,
+                                              const uint32_t* __restrict__ Z0) {
     pdl_trigger();
     const uint32_t J = (blockIdx.x * blockDim.x + threadIdx.x) * V;
     if (J >= Rn.N) return;
     pdl_wait();  // C is produced by the contraction kernel
-    pack_item<V, L, RB, MT>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, blockIdx.y, blockIdx.z, J);
+    pack_item<V, L, RB, MT>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, Z0, blockIdx.y, blockIdx.z, J);
 }
 
 template <typename K, typename... Args>
@@ -39,34 +40,34 @@ static cudaError_t launch_maybe_pdl(bool pdl, K kernel, dim3 grid, dim3 block, c
 
 template <int V, int RB>
 static cudaError_t launch_vr(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                             uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl) {
+                             uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl, const uint32_t* Z0) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     const uint32_t per_block = 128 * V;
     dim3 grid((N + per_block - 1) / per_block, nq * nct, 2);
     const uint64_t key = prg_key(seed, 6);
     uint32_t* d_R = static_cast<uint32_t*>(d_Rv);
     switch (c->rns.L) {
-        case 1: return launch_maybe_pdl(pdl, k_pack<V, 1, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 2: return launch_maybe_pdl(pdl, k_pack<V, 2, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 3: return launch_maybe_pdl(pdl, k_pack<V, 3, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 4: return launch_maybe_pdl(pdl, k_pack<V, 4, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 5: return launch_maybe_pdl(pdl, k_pack<V, 5, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        default: return launch_maybe_pdl(pdl, k_pack<V, 6, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 1: return launch_maybe_pdl(pdl, k_pack<V, 1, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 2: return launch_maybe_pdl(pdl, k_pack<V, 2, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 3: return launch_maybe_pdl(pdl, k_pack<V, 3, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 4: return launch_maybe_pdl(pdl, k_pack<V, 4, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 5: return launch_maybe_pdl(pdl, k_pack<V, 5, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        default: return launch_maybe_pdl(pdl, k_pack<V, 6, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
     }
 }
 
 // ell > 32: 64-bit masks and R, one coefficient per thread, L in {4, 5, 6}
 template <int RB>
 static cudaError_t launch_r64(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                              uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl) {
+                              uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl, const uint32_t* Z0) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     dim3 grid((N + 127) / 128, nq * nct, 2);
     const uint64_t key = prg_key(seed, 6);
     uint64_t* d_R = static_cast<uint64_t*>(d_Rv);
     switch (c->rns.L) {
-        case 4: return launch_maybe_pdl(pdl, k_pack<1, 4, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 5: return launch_maybe_pdl(pdl, k_pack<1, 5, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
-        case 6: return launch_maybe_pdl(pdl, k_pack<1, 6, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R);
+        case 4: return launch_maybe_pdl(pdl, k_pack<1, 4, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 5: return launch_maybe_pdl(pdl, k_pack<1, 5, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 6: return launch_maybe_pdl(pdl, k_pack<1, 6, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -81,25 +82,25 @@ static uint32_t rows_per_batch(uint32_t Rr, uint32_t kq) {
 }
 
 static cudaError_t launch_64(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                             uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl) {
+                             uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl, const uint32_t* Z0) {
     switch (rows_per_batch(c->rns.N / n, kq)) {
-        case 1: return launch_r64<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        case 2: return launch_r64<2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        case 4: return launch_r64<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        case 5: return launch_r64<5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        default: return launch_r64<8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 1: return launch_r64<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 2: return launch_r64<2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 4: return launch_r64<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 5: return launch_r64<5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        default: return launch_r64<8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
     }
 }
 
 template <int V>
 static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                            uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl) {
+                            uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl, const uint32_t* Z0) {
     switch (rows_per_batch(c->rns.N / n, kq)) {
-        case 1: return launch_vr<V, 1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        case 2: return launch_vr<V, 2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        case 4: return launch_vr<V, 4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        case 5: return launch_vr<V, 5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
-        default: return launch_vr<V, 8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        case 1: return launch_vr<V, 1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 2: return launch_vr<V, 2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 4: return launch_vr<V, 4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 5: return launch_vr<V, 5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        default: return launch_vr<V, 8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
     }
 }
 
@@ -135,9 +136,9 @@ cudaError_t launch_mask_R(nimbus_ctx* c, uint32_t kq, uint32_t nq, uint32_t n, u
 }
 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
-                        uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl) {
+                        uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl, const uint32_t* Z0) {
     if (elem_bytes(c->rns.ell) == 8) {
-        cudaError_t e = launch_64(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+        cudaError_t e = launch_64(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
         c->launches++;
         return e;
     }
@@ -148,8 +149,8 @@ cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_
     // (C2: V = 1 26.1 us/step vs V = 4 28.2; C3: V = 4)
     const uint64_t threads_v1 = 2ull * nq * nct * N;      // one thread per (comp, J)
     const bool vec = (n % 4 == 0) && threads_v1 / 4 >= 8ull * 128 * (uint64_t)c->num_sms;
-    cudaError_t e = vec ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl)
-                        : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl);
+    cudaError_t e = vec ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0)
+                        : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
     c->launches++;
     return e;
 }

@@ -66,7 +66,8 @@ struct VecU32<4> {
 template <int V, int L, int RB, typename MT = uint32_t>
 __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                           uint32_t Rr, uint32_t nct, uint64_t key_mask, uint32_t* __restrict__ cts,
-                                          MT* __restrict__ Rout, uint32_t tg, uint32_t comp, uint32_t J) {
+                                          MT* __restrict__ Rout, const uint32_t* __restrict__ Z0, uint32_t tg,
+                                          uint32_t comp, uint32_t J) {
     static_assert(sizeof(MT) == 4 || V == 1, "64-bit masks: one coefficient per thread");
     const uint32_t N = Rn.N, Lo = Rn.L_out;
     const uint32_t query = tg / nct, theta = tg - query * nct;
@@ -109,6 +110,16 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
             }
         }
     }
+    if (Z0) {
+        // circuit privacy: + Enc_pk(0) at the full modulus, before the mod-switch (reading 26)
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            uint32_t z[V];
+            VecU32<V>::load(Z0 + (((size_t)tg * 2 + comp) * L + i) * N + J, z);
+#pragma unroll
+            for (int u = 0; u < V; u++) acc[i][u] += z[u];
+        }
+    }
     MT rmask[V];
     if (comp == 0) {
         // word(seed, 6, i) = mix64(key + golden (i + 1)) for i = tg N + J + u: one multiply, then steps;
@@ -126,9 +137,13 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
         uint32_t res[L];
 #pragma unroll
         for (int i = 0; i < L; i++) {
-            // RB == 1: a single unwrapped row (R = 1), already a residue
-            if (RB == 1) res[i] = (uint32_t)acc[i][u];
-            else res[i] = reduce44_pm(acc[i][u], Rn.p[i], Rn.c32[i]);
+            // RB == 1: a single unwrapped row (R = 1) plus at most one zero-encryption residue (< 2 p)
+            if (RB == 1) {
+                const uint32_t r = (uint32_t)acc[i][u];
+                res[i] = r >= Rn.p[i] ? r - Rn.p[i] : r;
+            } else {
+                res[i] = reduce44_pm(acc[i][u], Rn.p[i], Rn.c32[i]);
+            }
         }
 #pragma unroll
         for (int l = L - 1; l >= 1; l--) {

@@ -85,6 +85,14 @@ _SIGS = {
     "nimbus_server_workspace_size": (C.c_int, [_vp, _vp, _u32, _u32, C.POINTER(_sz)]),
     "nimbus_plain_matmul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _sz, _vp]),
     "nimbus_server_output": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _sz, _vp]),
+    "nimbus_keygen_pk": (C.c_int, [_vp, _vp, _u64, _vp, C.POINTER(_vp)]),
+    "nimbus_pk_destroy": (None, [_vp]),
+    "nimbus_pk_export": (C.c_int, [_vp, _vp, _vp]),
+    "nimbus_pk_import": (C.c_int, [_vp, _vp, _vp, C.POINTER(_vp)]),
+    "nimbus_rerand_flood_max": (C.c_int, [_vp, _vp, _u32, C.POINTER(_u32)]),
+    "nimbus_rerand_prepare": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _u32, _vp, _vp]),
+    "nimbus_cop_matmul_rr": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_cop_matmul_rr_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -170,6 +178,10 @@ class Context(_Handle):
 
 class SecretKey(_Handle):
     _destroy = "nimbus_sk_destroy"
+
+
+class PublicKey(_Handle):
+    _destroy = "nimbus_pk_destroy"
 
 
 class EncW(_Handle):
@@ -313,6 +325,64 @@ def nimbus_cop_matmul_u64(ctx: Context, w: EncW, X: torch.Tensor, k_per_query: i
     _check(lib().nimbus_cop_matmul_u64(ctx.ptr, w.ptr, _ptr(X, torch.int64, "X"), k_per_query, n_queries,
                                        mask_seed, _ptr(cts, torch.int32, "cts"), _ptr(R, torch.int64, "R"),
                                        _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return cts, R
+
+
+def nimbus_keygen_pk(ctx: Context, sk: SecretKey, seed: int, stream=None) -> PublicKey:
+    out = C.c_void_p()
+    _check(lib().nimbus_keygen_pk(ctx.ptr, sk.ptr, seed, _stream(stream), C.byref(out)), ctx)
+    return PublicKey(out, ctx)
+
+
+def nimbus_pk_export(pk: PublicKey, stream=None) -> torch.Tensor:
+    ctx = pk.owner
+    out = torch.empty((2, ctx.L, ctx.N), dtype=torch.int32, device=f"cuda:{ctx.device}")
+    _check(lib().nimbus_pk_export(pk.ptr, _ptr(out), _stream(stream)), ctx)
+    return out
+
+
+def nimbus_pk_import(ctx: Context, pk: torch.Tensor, stream=None) -> PublicKey:
+    out = C.c_void_p()
+    _check(lib().nimbus_pk_import(ctx.ptr, _ptr(pk, torch.int32, "pk"), _stream(stream), C.byref(out)), ctx)
+    return PublicKey(out, ctx)
+
+
+def nimbus_rerand_flood_max(ctx: Context, w: EncW, k_per_query: int) -> int:
+    out = _u32()
+    _check(lib().nimbus_rerand_flood_max(ctx.ptr, w.ptr, k_per_query, C.byref(out)), ctx)
+    return int(out.value)
+
+
+def alloc_zero(ctx: Context, w: EncW, k_per_query: int, n_queries: int) -> torch.Tensor:
+    nct = nimbus_cop_out_count(ctx, k_per_query, w.n, n_queries)
+    return torch.empty((nct, 2, ctx.L, ctx.N), dtype=torch.int32, device=f"cuda:{ctx.device}")
+
+
+def nimbus_rerand_prepare(ctx: Context, pk: PublicKey, w: EncW, k_per_query: int, n_queries: int, seed: int,
+                          flood_bits: int, zero: torch.Tensor = None, stream=None) -> torch.Tensor:
+    if zero is None:
+        zero = alloc_zero(ctx, w, k_per_query, n_queries)
+    _check(lib().nimbus_rerand_prepare(ctx.ptr, pk.ptr, w.ptr, k_per_query, n_queries, seed, flood_bits,
+                                       _ptr(zero, torch.int32, "zero"), _stream(stream)), ctx)
+    return zero
+
+
+def nimbus_cop_matmul_rr(ctx: Context, w: EncW, X: torch.Tensor, k_per_query: int, n_queries: int,
+                         mask_seed: int, zero: torch.Tensor, cts: torch.Tensor, R: torch.Tensor, ws: torch.Tensor,
+                         stream=None):
+    _check(lib().nimbus_cop_matmul_rr(ctx.ptr, w.ptr, _ptr(X, torch.int32, "X"), k_per_query, n_queries,
+                                      mask_seed, _ptr(zero, torch.int32, "zero"), _ptr(cts, torch.int32, "cts"),
+                                      _ptr(R, torch.int32, "R"), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return cts, R
+
+
+def nimbus_cop_matmul_rr_u64(ctx: Context, w: EncW, X: torch.Tensor, k_per_query: int, n_queries: int,
+                             mask_seed: int, zero: torch.Tensor, cts: torch.Tensor, R: torch.Tensor,
+                             ws: torch.Tensor, stream=None):
+    _check(lib().nimbus_cop_matmul_rr_u64(ctx.ptr, w.ptr, _ptr(X, torch.int64, "X"), k_per_query, n_queries,
+                                          mask_seed, _ptr(zero, torch.int32, "zero"),
+                                          _ptr(cts, torch.int32, "cts"), _ptr(R, torch.int64, "R"), _ptr(ws),
+                                          ws.numel(), _stream(stream)), ctx)
     return cts, R
 
 

@@ -48,6 +48,48 @@ __global__ void __launch_bounds__(128) k_tiles(const uint8_t* src, uint32_t ntil
     sink[blockIdx.x] = acc;
 }
 
+// contiguous variant: CTA c streams bytes [c*chunk, (c+1)*chunk) in `bytes` copies
+__global__ void __launch_bounds__(128) k_contig(const uint8_t* src, size_t total, uint32_t stages, uint32_t bytes,
+                                               unsigned long long* sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bars[16];
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < stages; s++) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const uint64_t pol = policy_evict_first();
+    const size_t ncopies = total / bytes;
+    const size_t per = (ncopies + gridDim.x - 1) / gridDim.x;
+    const size_t c0 = blockIdx.x * per, c1 = c0 + per < ncopies ? c0 + per : ncopies;
+    const uint32_t n = c1 > c0 ? (uint32_t)(c1 - c0) : 0;
+    unsigned long long acc = 0;
+    for (uint32_t i = 0; i < n + stages; i++) {
+        if (i >= stages) {
+            const uint32_t j = i - stages, s = j % stages;
+            mbar_wait(&bars[s], (j / stages) & 1);
+            acc += smem[s * bytes];
+        }
+        if (i < n) {
+            const uint32_t s = i % stages;
+            mbar_arrive_expect_tx(&bars[s], bytes);
+            bulk_g2s(smem + s * bytes, src + (c0 + i) * bytes, bytes, &bars[s], pol);
+        }
+    }
+    sink[blockIdx.x] = acc;
+}
+
+// touch one 16-byte word every `stride` bytes (TLB warm-up; brings < 0.1 % of the lines into L2)
+__global__ void k_touch(const uint8_t* p, size_t total, size_t stride, unsigned long long* sink) {
+    unsigned long long acc = 0;
+    for (size_t o = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * stride; o < total;
+         o += (size_t)gridDim.x * blockDim.x * stride)
+        acc += *reinterpret_cast<const unsigned long long*>(p + o);
+    if (acc == 7) sink[0] = acc;
+}
+
 __global__ void k_read(const uint4* p, size_t n, unsigned long long* sink) {
     unsigned long long acc = 0;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -96,6 +138,35 @@ int main() {
         printf("%5u B x %2u stages x %u CTA/SM (%4u KB in flight/SM): best %6.2f us (%5.0f GB/s), mean %6.2f us  %s\n",
                v.bytes, v.stages, v.ctas_per_sm, v.bytes * v.stages * v.ctas_per_sm / 1024, best * 1e3,
                (double)ntiles * tile / (best * 1e-3) / 1e9, sum / reps * 1e3, cudaGetErrorString(cudaGetLastError()));
+    }
+    // TLB / pattern experiments at 32 KB x 3 (the resident kernel's ring)
+    cudaFuncSetAttribute(k_contig, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32768 + 1024);
+    cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32768 + 1024);
+    for (int mode = 0; mode < 6; mode++) {
+        // 0 tiles, 1 tiles + touch/2MB, 2 tiles + touch/64KB, 3 contiguous, 4 contiguous + touch/2MB, 5 tiles after a warm run
+        float best = 1e9, sum = 0;
+        const int reps = 8;
+        for (int rep = 0; rep < reps; rep++) {
+            const uint8_t* s = src + (size_t)(rep % 8) * (mb << 20);
+            k_read<<<sms * 4, 256>>>(reinterpret_cast<const uint4*>(fl), ((size_t)512 << 20) / 16, sink);
+            if (mode == 1 || mode == 4) k_touch<<<sms, 128>>>(s, mb << 20, (size_t)2 << 20, sink);
+            if (mode == 2) k_touch<<<sms, 128>>>(s, mb << 20, (size_t)64 << 10, sink);
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0); cudaEventCreate(&e1);
+            cudaEventRecord(e0);
+            if (mode >= 3 && mode <= 4) k_contig<<<sms, 128, 3 * 32768 + 1024>>>(s, ntiles * tile, 3, 32768, sink);
+            else k_tiles<<<sms, 128, 3 * 32768 + 1024>>>(s, (uint32_t)ntiles, (uint32_t)tile, 3, 32768, sink);
+            cudaEventRecord(e1);
+            cudaDeviceSynchronize();
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = ms < best ? ms : best;
+            sum += ms;
+        }
+        static const char* names[] = {"tiles", "tiles+touch2MB", "tiles+touch64KB", "contig", "contig+touch2MB", "-"};
+        if (mode < 5)
+            printf("%-18s best %6.2f us mean %6.2f us  %s\n", names[mode], best * 1e3, sum / reps * 1e3,
+                   cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
 }
