@@ -82,12 +82,15 @@ __device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c)
 
 // x mod p for any 64-bit x when c32 = 2^32 mod p < 2^21 (true for the primes
 // within 2^20 of 2^31 that the context derives): fold x = hi 2^32 + lo ->
-// hi c32 + lo five times (64 -> 54 -> 44 -> 34 -> 33 -> 32 bits), then at most
-// two conditional subtractions (2^32 < 3p).
+// hi c32 + lo three times (< 2^53 + 2^32, < 2^42 + 2^33, < 2^32 + 2^31 + 2^21),
+// then the last carry h in {0, 1} as h c32 on the low word (l < 2^31 + 2^21 when
+// h = 1, so the sum stays below 2^32 < 3p), then at most two conditional
+// subtractions.  Three IMAD.WIDE instead of five: the epilogue that calls it per
+// output is bound by the FMA pipe.
 __device__ __forceinline__ uint32_t reduce64_pm(uint64_t x, uint32_t p, uint32_t c32) {
 #pragma unroll
-    for (int f = 0; f < 5; f++) x = mad_wide((uint32_t)(x >> 32), c32, (uint32_t)x);
-    uint32_t r = (uint32_t)x;
+    for (int f = 0; f < 3; f++) x = mad_wide((uint32_t)(x >> 32), c32, (uint32_t)x);
+    uint32_t r = (uint32_t)x + ((uint32_t)(x >> 32) ? c32 : 0u);
     r = r >= p ? r - p : r;
     r = r >= p ? r - p : r;
     return r;
