@@ -56,6 +56,15 @@ def parse():
     return ap.parse_args()
 
 
+def step_dist(step_ms):
+    """median and p10 / p90 of the per-step times (nearest-rank percentiles)."""
+    v = sorted(step_ms)
+    if not v:
+        return None
+    pick = lambda q: v[min(len(v) - 1, max(0, int(round(q * (len(v) - 1)))))]
+    return {"runs": len(v), "median": statistics.median(v), "p10": pick(0.10), "p90": pick(0.90)}
+
+
 def get_config(key: str):
     if key.endswith("l16"):
         return ni.CONFIGS_L16[int(key[0])]
@@ -541,6 +550,8 @@ def main():
         "stages_ms_per_step_profiled": {"slice_x": res["stage_ms"][0] / args.steps,
                                         "contraction": res["stage_ms"][1] / args.steps,
                                         "pack_moddown_mask": res["stage_ms"][2] / args.steps},
+        # per-step spread of the timed pass (CUDA events around each step, rank 0)
+        "step_ms_dist": step_dist(res["step_ms"]),
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
         "setup_encrypt_s": res["t_setup"],
