@@ -229,20 +229,22 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 mt["encw"].append(encrypt(ctx, sk, mt["W"], mt["seed"]))
                 mt["X"].append(mt["X"][0].clone())
     # setup on the device, steady state (allocations excluded): re-encrypt the first
-    # matrix into a fresh handle, CUDA events around the kernels' stream work
+    # matrix into its existing handle (nimbus_encrypt_weights_into: the encrypt and tile
+    # kernels and a stream-ordered temporary), CUDA events around the stream work
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     mt0 = mats[0]
-    tmp = encrypt(ctx, sk, mt0["W"], mt0["seed"])       # allocate once, then time a second pass
+    tmp = encrypt(ctx, sk, mt0["W"], mt0["seed"])       # allocate once
+    nb.nimbus_encrypt_weights_into(ctx, sk, mt0["W"], mt0["seed"], tmp)   # warm the temporary pool
     torch.cuda.synchronize()
     t_h0 = time.perf_counter()
     e0.record()
-    tmp2 = encrypt(ctx, sk, mt0["W"], mt0["seed"])
+    nb.nimbus_encrypt_weights_into(ctx, sk, mt0["W"], mt0["seed"], tmp)
     e1.record()
     torch.cuda.synchronize()
     setup_host_s = time.perf_counter() - t_h0
     setup_gpu_ms = e0.elapsed_time(e1)
-    setup_bytes = nb.nimbus_encw_bytes(tmp2)
-    del tmp, tmp2
+    setup_bytes = nb.nimbus_encw_bytes(tmp)
+    del tmp
     for mt in mats:
         del mt["W"]
     torch.cuda.synchronize()

@@ -127,6 +127,14 @@ nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const
 nimbus_status nimbus_encrypt_weights_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W,
                                          uint32_t m, uint32_t n, uint64_t seed, void* stream,
                                          nimbus_encw** out);
+/* Re-encrypt new weights (same m x n, same layout) into an existing resident handle,
+ * e.g. a weight update or a new key: nothing is allocated beyond a stream-ordered
+ * temporary for the canonical rows.  Same semantics and PRG indices as
+ * nimbus_encrypt_weights with this seed.  NIMBUS_EINVAL for an offloaded handle. */
+nimbus_status nimbus_encrypt_weights_into(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint64_t seed,
+                                          void* stream, nimbus_encw* encw);
+nimbus_status nimbus_encrypt_weights_into_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W,
+                                              uint64_t seed, void* stream, nimbus_encw* encw);
 void nimbus_encw_destroy(nimbus_encw* encw);
 /* Bytes of device memory held by the handle. */
 size_t nimbus_encw_bytes(const nimbus_encw* encw);

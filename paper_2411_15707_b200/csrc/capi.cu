@@ -216,6 +216,7 @@ void nimbus_ctx_destroy(nimbus_ctx* ctx) {
     DevGuard dg_(ctx);
     if (!ctx) return;
     if (ctx->d_tw) cudaFree(ctx->d_tw);
+    if (ctx->d_scratch) cudaFree(ctx->d_scratch);
     if (ctx->d_flag) cudaFree(ctx->d_flag);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->ev_pending) cudaEventDestroy(e);
@@ -366,24 +367,6 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     return NIMBUS_OK;
 }
 
-static nimbus_status encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const void* d_W, uint32_t m,
-                                     uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
-    if (!ctx || !sk || !d_W || !out || sk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
-    *out = nullptr;
-    nimbus_encw* w = nullptr;
-    nimbus_status st = new_encw(ctx, m, n, &w);
-    if (st != NIMBUS_OK) return st;
-    cudaStream_t s = (cudaStream_t)stream;
-    uint32_t* canon = nullptr;
-    cudaError_t e = cudaMallocAsync(&canon, (size_t)m * ncols(ctx) * 4, s);
-    if (e == cudaSuccess) e = launch_encrypt(ctx, sk->d_s_ntt, d_W, m, n, seed, canon, s);
-    if (e == cudaSuccess) e = launch_tile_encw(ctx, canon, m, w->KB, w->bn, w->d_Et, s);
-    if (canon) cudaFreeAsync(canon, s);
-    if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encrypt_weights"); }
-    *out = w;
-    return NIMBUS_OK;
-}
-
 // the element width at the boundary follows ell: uint32 up to 32 bits, uint64 beyond
 static nimbus_status want_width(nimbus_ctx* ctx, uint32_t bytes) {
     if (!ctx) return NIMBUS_EINVAL;
@@ -392,6 +375,64 @@ static nimbus_status want_width(nimbus_ctx* ctx, uint32_t bytes) {
                                                       : "ell <= 32: use the 32-bit entry point");
     return NIMBUS_OK;
 }
+
+// encrypt (canonical rows, stream-ordered temporary) and tile into w's resident planes
+// (the canonical rows go to the context's grow-only scratch: a fresh 50-600 MB
+// allocation per call costs more than the kernels; calls on a context are serialised)
+static cudaError_t encrypt_into(nimbus_ctx* ctx, const nimbus_sk* sk, const void* d_W, uint64_t seed,
+                                cudaStream_t s, nimbus_encw* w) {
+    const size_t need = (size_t)w->m * ncols(ctx) * 4;
+    if (ctx->scratch_bytes < need) {
+        cudaError_t e = cudaStreamSynchronize(s);         // earlier work may still use the old scratch
+        if (e != cudaSuccess) return e;
+        if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+        ctx->d_scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        e = cudaMalloc(&ctx->d_scratch, need);
+        if (e != cudaSuccess) return e;
+        ctx->scratch_bytes = need;
+    }
+    uint32_t* canon = static_cast<uint32_t*>(ctx->d_scratch);
+    cudaError_t e = launch_encrypt(ctx, sk->d_s_ntt, d_W, w->m, w->n, seed, canon, s);
+    if (e == cudaSuccess) e = launch_tile_encw(ctx, canon, w->m, w->KB, w->bn, w->d_Et, s);
+    return e;
+}
+
+static nimbus_status encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const void* d_W, uint32_t m,
+                                     uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
+    if (!ctx || !sk || !d_W || !out || sk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    *out = nullptr;
+    nimbus_encw* w = nullptr;
+    nimbus_status st = new_encw(ctx, m, n, &w);
+    if (st != NIMBUS_OK) return st;
+    cudaError_t e = encrypt_into(ctx, sk, d_W, seed, (cudaStream_t)stream, w);
+    if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encrypt_weights"); }
+    *out = w;
+    return NIMBUS_OK;
+}
+
+static nimbus_status reencrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const void* d_W, uint64_t seed,
+                                       void* stream, nimbus_encw* w) {
+    if (!ctx || !sk || !d_W || !w || sk->ctx != ctx || w->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    if (!w->d_Et) return set_err(ctx, NIMBUS_EINVAL, "Enc(W) is host-resident: nimbus_encw_reload first");
+    CK(encrypt_into(ctx, sk, d_W, seed, (cudaStream_t)stream, w), "encrypt_weights_into");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_encrypt_weights_into(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint64_t seed,
+                                          void* stream, nimbus_encw* encw) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : reencrypt_weights(ctx, sk, d_W, seed, stream, encw);
+}
+
+nimbus_status nimbus_encrypt_weights_into_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W,
+                                              uint64_t seed, void* stream, nimbus_encw* encw) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 8);
+    return st != NIMBUS_OK ? st : reencrypt_weights(ctx, sk, d_W, seed, stream, encw);
+}
+
 
 nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint32_t m,
                                      uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {

@@ -110,6 +110,29 @@ __device__ __forceinline__ uint32_t emb_mod(uint64_t w, uint64_t qmodt, uint32_t
     return mulmod(dr, tinv, p, mu);
 }
 
+// Emb_{Q}(w) mod p with 32-bit Shoup multiplication:
+// (t/2 - f) * t^-1 mod p,  f = (Q w + t/2) mod t,  |t/2 - f| <= t/2 < 2p.
+__device__ __forceinline__ uint32_t emb_fast(uint32_t w, uint32_t qmodt, uint32_t ell, uint32_t p, uint32_t tinv,
+                                             uint32_t tinv_sh) {
+    const uint64_t t = 1ULL << ell;
+    const uint64_t f = ((uint64_t)qmodt * w + (t >> 1)) & (t - 1);
+    int64_t d = (int64_t)(t >> 1) - (int64_t)f;
+    if (d < 0) d += p;
+    if (d < 0) d += p;
+    if (d >= (int64_t)p) d -= p;
+    return mulmod_shoup((uint32_t)d, tinv, tinv_sh, p);
+}
+
+// Emb_{Q}(w) mod p for ell <= 16, all in 32 bits: Q w + t/2 < 2^32 when Q < t = 2^ell.
+__device__ __forceinline__ uint32_t emb_fast16(uint32_t w, uint32_t qmodt, uint32_t ell, uint32_t p, uint32_t tinv,
+                                               uint32_t tinv_sh) {
+    const uint32_t t = 1u << ell;
+    const uint32_t f = (qmodt * w + (t >> 1)) & (t - 1);
+    const uint32_t h = t >> 1;
+    const uint32_t d = h >= f ? h - f : p - (f - h);     // (t/2 - f) mod p, |t/2 - f| <= t/2 < p
+    return mulmod_shoup(d, tinv, tinv_sh, p);
+}
+
 // ------------------------------------------------------------------ PTX: mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

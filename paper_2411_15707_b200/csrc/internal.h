@@ -49,6 +49,9 @@ struct nimbus_ctx {
     // streamed path (nimbus_cop_matmul_streamed): host -> device copy stream + events
     cudaStream_t copy = nullptr;
     std::vector<cudaEvent_t> stream_ev;
+    // grow-only device scratch for the canonical rows of Enc(W) during (re-)encryption
+    void* d_scratch = nullptr;
+    size_t scratch_bytes = 0;
     // kernels already opted into their dynamic shared memory on this context's device
     std::vector<const void*> smem_ok;
 };

@@ -146,8 +146,12 @@ __global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, co
     const uint64_t ka = prg_key(seed, 2), ke = prg_key(seed, 3);
     uint32_t* bo = encW + (((size_t)beta * 2 + 0) * L + i) * N;
     uint32_t* ao = encW + (((size_t)beta * 2 + 1) * L + i) * N;
-    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
-        uint32_t a = samp_uniform_mod(prg_word(ka, ((uint64_t)beta * L + i) * N + j), p);
+    // PRG counters stepped per thread: word(key, idx) = mix64(key + golden (idx + 1))
+    constexpr uint64_t G = 0x9E3779B97F4A7C15ULL;
+    const uint64_t dz = G * blockDim.x;
+    uint64_t za = ka + G * (((uint64_t)beta * L + i) * N + threadIdx.x + 1);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x, za += dz) {
+        uint32_t a = samp_uniform_mod(mix64(za), p);
         sa[j] = a;
         ao[j] = a;
     }
@@ -160,10 +164,14 @@ __global__ void k_encrypt(Rns R, const uint32_t* d_tw, const uint32_t* s_ntt, co
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) sa[j] = mulmod(sa[j], sn[j], p, mu);
     __syncthreads();
     ntt_inv_smem(sa, tw.iv, tw.iv_sh, N, R.logN, p, R.ninv[i], R.ninv_sh[i]);
-    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
+    uint64_t ze = ke + G * ((uint64_t)beta * N + threadIdx.x + 1);
+    for (uint32_t j = threadIdx.x; j < N; j += blockDim.x, ze += dz) {
         const uint64_t w = j < n ? (uint64_t)W[(size_t)beta * n + j] : 0u;
-        int32_t e = samp_cbd21(prg_word(ke, (uint64_t)beta * N + j));
-        uint32_t em = emb_mod(w, R.q_mod_t, R.ell, p, mu, R.t_inv[i]);
+        int32_t e = samp_cbd21(mix64(ze));
+        // Emb_q(w) mod p: 32-bit Shoup forms up to ell = 32, the 64-bit one beyond
+        uint32_t em = R.ell > 32 ? emb_mod(w, R.q_mod_t, R.ell, p, mu, R.t_inv[i])
+                      : R.ell <= 16 ? emb_fast16((uint32_t)w, (uint32_t)R.q_mod_t, R.ell, p, R.t_inv[i], R.t_inv_sh[i])
+                                    : emb_fast((uint32_t)w, (uint32_t)R.q_mod_t, R.ell, p, R.t_inv[i], R.t_inv_sh[i]);
         uint32_t er = e < 0 ? p - (uint32_t)(-e) : (uint32_t)e;
         bo[j] = addmod(addmod(sa[j], em, p), er, p);
     }

@@ -5,29 +5,6 @@
 
 namespace nimbus {
 
-// Emb_{Q}(w) mod p with 32-bit Shoup multiplication:
-// (t/2 - f) * t^-1 mod p,  f = (Q w + t/2) mod t,  |t/2 - f| <= t/2 < 2p.
-__device__ __forceinline__ uint32_t emb_fast(uint32_t w, uint32_t qmodt, uint32_t ell, uint32_t p, uint32_t tinv,
-                                             uint32_t tinv_sh) {
-    const uint64_t t = 1ULL << ell;
-    const uint64_t f = ((uint64_t)qmodt * w + (t >> 1)) & (t - 1);
-    int64_t d = (int64_t)(t >> 1) - (int64_t)f;
-    if (d < 0) d += p;
-    if (d < 0) d += p;
-    if (d >= (int64_t)p) d -= p;
-    return mulmod_shoup((uint32_t)d, tinv, tinv_sh, p);
-}
-
-// Emb_{Q}(w) mod p for ell <= 16, all in 32 bits: Q w + t/2 < 2^32 when Q < t = 2^ell.
-__device__ __forceinline__ uint32_t emb_fast16(uint32_t w, uint32_t qmodt, uint32_t ell, uint32_t p, uint32_t tinv,
-                                               uint32_t tinv_sh) {
-    const uint32_t t = 1u << ell;
-    const uint32_t f = (qmodt * w + (t >> 1)) & (t - 1);
-    const uint32_t h = t >> 1;
-    const uint32_t d = h >= f ? h - f : p - (f - h);     // (t/2 - f) mod p, |t/2 - f| <= t/2 < p
-    return mulmod_shoup(d, tinv, tinv_sh, p);
-}
-
 // x mod p for a sum of at most 2^13 residues (x < 2^44, rows <= N <= 8192) when c32 = 2^32 mod p < 2^21:
 // three folds x = hi 2^32 + lo -> hi c32 + lo (< 3*2^32, < 2^32 + 2^22, < 2^32),
 // then two conditional subtractions (2^32 < 3p).

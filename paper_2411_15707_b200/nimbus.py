@@ -85,6 +85,8 @@ _SIGS = {
     "nimbus_server_workspace_size": (C.c_int, [_vp, _vp, _u32, _u32, C.POINTER(_sz)]),
     "nimbus_plain_matmul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _sz, _vp]),
     "nimbus_server_output": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _sz, _vp]),
+    "nimbus_encrypt_weights_into": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
+    "nimbus_encrypt_weights_into_u64": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
     "nimbus_keygen_pk": (C.c_int, [_vp, _vp, _u64, _vp, C.POINTER(_vp)]),
     "nimbus_pk_destroy": (None, [_vp]),
     "nimbus_pk_export": (C.c_int, [_vp, _vp, _vp]),
@@ -252,6 +254,16 @@ def nimbus_encrypt_weights_u64(ctx: Context, sk: SecretKey, W: torch.Tensor, see
     _check(lib().nimbus_encrypt_weights_u64(ctx.ptr, sk.ptr, _ptr(W, torch.int64, "W"), m, n, seed,
                                             _stream(stream), C.byref(out)), ctx)
     return EncW(out, ctx, m, n)
+
+
+def nimbus_encrypt_weights_into(ctx: Context, sk: SecretKey, W: torch.Tensor, seed: int, w: EncW, stream=None):
+    """Re-encrypt W (same shape as the handle's) into the existing handle w."""
+    if tuple(W.shape) != (w.m, w.n):
+        raise ValueError(f"W shape {tuple(W.shape)} != handle ({w.m}, {w.n})")
+    wide = ctx.ell > 32
+    fn = lib().nimbus_encrypt_weights_into_u64 if wide else lib().nimbus_encrypt_weights_into
+    _check(fn(ctx.ptr, sk.ptr, _ptr(W, torch.int64 if wide else torch.int32, "W"), seed, _stream(stream), w.ptr), ctx)
+    return w
 
 
 def nimbus_encw_bytes(w: EncW) -> int:

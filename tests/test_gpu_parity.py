@@ -148,6 +148,21 @@ def test_encrypt_weights_parity(nb, oracle, N, L, ell, m, n):
     assert (u32(nb.nimbus_encw_export(w2)) == E).all()
 
 
+@pytest.mark.parametrize("N,L,ell,m,n", [(4096, 2, 16, 200, 700), (8192, 3, 32, 130, 768), (1024, 2, 8, 3, 5)])
+def test_encrypt_weights_into(nb, oracle, N, L, ell, m, n):
+    """Re-encryption into an existing handle (new weights and seed) equals a fresh
+    encryption with that seed, bit for bit against the oracle; offloaded handles
+    are refused."""
+    c = Case(nb, oracle, N, L, ell, 2 if ell == 32 else 1, m, n, kq=1)
+    W2 = ni.gen_W(c.seed + 9, m, n, ell)
+    nb.nimbus_encrypt_weights_into(c.ctx, c.sk, dev_u32(W2), c.seed + 9, c.encw)
+    E2 = oracle.encrypt_rows(N, L, c.pr, ell, c.s_oracle, W2, c.seed + 9)
+    assert (u32(nb.nimbus_encw_export(c.encw)) == E2).all()
+    nb.nimbus_encw_offload(c.encw)
+    with pytest.raises(nb.NimbusError):
+        nb.nimbus_encrypt_weights_into(c.ctx, c.sk, dev_u32(W2), 1, c.encw)
+
+
 # ------------------------------------------------------------------ contraction (step 2)
 @pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("N,L,ell,k,m,n", [
