@@ -71,7 +71,24 @@ def main():
     def empty_sync():
         s.synchronize()
 
-    out = {"config": cfg.name, "host_call_us": wall(host_call), "device_call_sync_us": wall(dev_call),
+    # GPU-side timeline of the same sequence on one stream (events between the stages)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    seg = [[], [], []]
+    for _ in range(55):
+        torch.cuda.synchronize()
+        ev[0].record(s)
+        X.copy_(Xh, non_blocking=True)
+        ev[1].record(s)
+        nb.nimbus_cop_matmul(ctx, w, X, kq, nq, seed, cts, R, ws)
+        ev[2].record(s)
+        ch.copy_(cts, non_blocking=True)
+        Rh.copy_(R, non_blocking=True)
+        ev[3].record(s)
+        s.synchronize()
+        for i in range(3):
+            seg[i].append(ev[i].elapsed_time(ev[i + 1]) * 1e3)
+    gpu = {k: statistics.median(v[5:]) for k, v in zip(("h2d_X", "cop_matmul", "d2h_cts_R"), seg)}
+    out = {"config": cfg.name, "gpu_timeline_us": gpu, "host_call_us": wall(host_call), "device_call_sync_us": wall(dev_call),
            "h2d_X_us": wall(h2d), "d2h_cts_us": wall(d2h_cts), "d2h_R_us": wall(d2h_R),
            "sync_only_us": wall(empty_sync),
            "bytes": {"X": Xh.numel() * 4, "cts": ch.numel() * 4, "R": Rh.numel() * 4}}
