@@ -243,6 +243,15 @@ def test_host_buffer_api_matches_device(nb, oracle):
     Xh = torch.from_numpy(c.X.view(np.int32)).pin_memory()
     nb.nimbus_cop_matmul_host(c.ctx, c.encw, Xh, c.kq, c.nq, c.seed, cts_h, R_h, ws)
     assert torch.equal(cts_h, cts_d.cpu()) and torch.equal(R_h, R_d.cpu())
+    # pageable host buffers (staged copies from / to pageable memory): same bytes, and mixed
+    Xp = torch.from_numpy(c.X.view(np.int32).copy())
+    cts_p, R_p = torch.zeros_like(cts_h, device="cpu"), torch.zeros_like(R_h, device="cpu")
+    assert not Xp.is_pinned() and not cts_p.is_pinned()
+    nb.nimbus_cop_matmul_host(c.ctx, c.encw, Xp, c.kq, c.nq, c.seed, cts_p, R_p, ws)
+    assert torch.equal(cts_p, cts_h) and torch.equal(R_p, R_h)
+    cts_h.zero_()
+    nb.nimbus_cop_matmul_host(c.ctx, c.encw, Xp, c.kq, c.nq, c.seed, cts_h, R_p, ws)
+    assert torch.equal(cts_h, cts_p)
 
 
 # ------------------------------------------------------------------ full-size configs (sampled)
