@@ -644,7 +644,7 @@ static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
     if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
         uint8_t* xt = ws + ws_layout(ctx, w, k).xt;
         // X rows per tile: 128, or 256 / S_x in the transposed orientation
-        const uint32_t rt = w->bn == kBNW ? 256 / sx_of(ctx->rns.ell) : kBM;
+        const uint32_t rt = w->bn == kBNW ? transposed_rows(ctx) : kBM;
         CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, rt, xt, s), "slice X");
         prof_mark(ctx, s);
         CK(launch_cop_tcgen05(ctx, w, xt, k, d_C, s), "cop tcgen05");

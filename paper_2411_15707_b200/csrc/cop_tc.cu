@@ -443,43 +443,52 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
 // outputs, against 64 KB of X + 24 KB of E for 6144 in the streaming kernel:
 // the L2->SM delivery rate is what bounds ell = 32.  The epilogue thread owns
 // one coefficient column and writes rows, so stores are coalesced across lanes.
-template <int SX_>
+// RT_ X rows per tile: 256 / S_x fills N = 256 (one accumulator set: 7 x 64 or
+// 11 x 32 TMEM columns); RT_ = 32 at S_x = 4 (N = 128, 7 x 32 = 224 columns) leaves
+// room for two accumulator sets, so the epilogue of one tile overlaps the MMAs of
+// the next -- with one set, the short m = 768 matmuls of C5 (6 k-blocks a tile)
+// idle the tensor pipe for every epilogue -- at the price of more shared-memory
+// fill per MAC (80 KB per 1024 MMA cycles instead of 96 KB per 2048).
+template <int SX_, int RT_ = 256 / SX_>
 struct TCfgT {
-    static constexpr uint32_t BM = kBNW, RT = 256 / SX_, BK = kBK, SX = SX_;   // ell = 32: 64 rows; ell = 64: 32
+    static constexpr uint32_t BM = kBNW, RT = RT_, BK = kBK, SX = SX_;
     static constexpr uint32_t A_BYTES = kSW * BM * BK;     // 64 KB: 4 planes x 128 columns x 128 B
-    static constexpr uint32_t B_BYTES = SX * RT * BK;      // 32 KB: 4 slices x 64 rows x 128 B
+    static constexpr uint32_t B_BYTES = SX * RT * BK;      // S_x slices x RT rows x 128 B
     static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
     static constexpr uint32_t STAGES = 2;
-    static constexpr uint32_t NACC = SX + kSW - 1;         // 7 x 64 or 11 x 32 TMEM columns
+    static constexpr uint32_t NACC = SX + kSW - 1;         // 7 or 11 shifted accumulators
+    static constexpr uint32_t ACC_COLS = NACC * RT;
+    static constexpr uint32_t ACC_BUFS = 2 * ACC_COLS <= 512 ? 2 : 1;
+    static constexpr uint32_t BUF_STRIDE = 256;            // TMEM column offset of accumulator set 1
     static constexpr uint32_t EPI_BATCH = NACC <= 7 ? 2 : 1;   // 8-row chunks per tcgen05.ld wait (registers)
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr uint32_t EPI_WARPS = 8;
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
     static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
-    static_assert(NACC * RT <= TMEM_COLS, "TMEM");
+    static_assert(ACC_COLS <= TMEM_COLS && (ACC_BUFS == 1 || ACC_COLS <= BUF_STRIDE), "TMEM");
+    static_assert(RT % 16 == 0 && (RT / 2) % 8 == 0, "epilogue halves of whole 8-row chunks");
     static_assert(SMEM <= 232448, "shared memory");
 };
 
-template <int SX>
-__global__ void __launch_bounds__(TCfgT<SX>::THREADS, 1)
+template <int SX, int RT>
+__global__ void __launch_bounds__(TCfgT<SX, RT>::THREADS, 1)
 k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t RTt,
            uint32_t CT, uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
-    using Cfg = TCfgT<SX>;
+    using Cfg = TCfgT<SX, RT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
     uint64_t* empty = full + Cfg::STAGES;
-    uint64_t* tfull = empty + Cfg::STAGES;
-    uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint64_t* tfull = empty + Cfg::STAGES;        // [ACC_BUFS]
+    uint64_t* tempty = tfull + 2;                 // [ACC_BUFS]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nunits = RTt * CT;
     if (threadIdx.x == 0) TRACE(0);
     if (warp == 0 && lane == 0) {
         for (uint32_t s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, Cfg::EPI_WARPS);
+        for (uint32_t b = 0; b < 2; b++) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -519,9 +528,12 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
             constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::RT);                    // N = 64
             uint32_t it = 0, ti = 0;
             for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
-                if (ti >= 1) mbar_wait(tempty, (ti - 1) & 1);
+                const uint32_t buf = Cfg::ACC_BUFS == 2 ? (ti & 1) : 0;
+                const uint32_t use = Cfg::ACC_BUFS == 2 ? (ti >> 1) : ti;
+                if (use >= 1) mbar_wait(&tempty[buf], (use - 1) & 1);
                 TRACE(4 + 4 * ti);
                 tc_fence_after();
+                const uint32_t dacc = tmem + buf * Cfg::BUF_STRIDE;
                 for (uint32_t kb = 0; kb < KB; kb++, it++) {
                     const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
                     mbar_wait(&full[s], ph);
@@ -535,18 +547,18 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
                         for (uint32_t j = 0; j < kSW; j++) {
                             const uint64_t ad = sdesc_kmajor_sw128(a0 + j * Cfg::BM * Cfg::BK + kk * 32);
                             if ((kb | kk) != 0 || j == 0) {
-                                mma_i8_ss(tmem + j * Cfg::RT, ad, bd, idesc_full, (kb | kk) != 0);
+                                mma_i8_ss(dacc + j * Cfg::RT, ad, bd, idesc_full, (kb | kk) != 0);
                             } else {
                                 // first k-step, j >= 1: acc_j..acc_{j+SX-2} exist, acc_{j+SX-1} is new
-                                mma_i8_ss(tmem + j * Cfg::RT, ad, bd, idesc_lo, 1u);
+                                mma_i8_ss(dacc + j * Cfg::RT, ad, bd, idesc_lo, 1u);
                                 const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (Cfg::SX - 1) * Cfg::RT * Cfg::BK + kk * 32);
-                                mma_i8_ss(tmem + (j + Cfg::SX - 1) * Cfg::RT, ad, bd3, idesc_one, 0u);
+                                mma_i8_ss(dacc + (j + Cfg::SX - 1) * Cfg::RT, ad, bd3, idesc_one, 0u);
                             }
                         }
                     }
                     mma_commit(&empty[s]);
                 }
-                mma_commit(tfull);
+                mma_commit(&tfull[buf]);
                 TRACE(5 + 4 * ti);
             }
         }
@@ -558,13 +570,15 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
         uint32_t ti = 0;
         for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
             const uint32_t rt = u % RTt, ct = u / RTt;
-            mbar_wait(tfull, ti & 1);
+            const uint32_t buf = Cfg::ACC_BUFS == 2 ? (ti & 1) : 0;
+            const uint32_t use = Cfg::ACC_BUFS == 2 ? (ti >> 1) : ti;
+            mbar_wait(&tfull[buf], use & 1);
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
             tc_fence_after();
             const uint32_t col = ct * Cfg::BM + sub * 32 + lane;
             const uint32_t limb = (col / R.N) % R.L;
             const uint32_t p = R.p[limb], c32 = R.c32[limb];
-            const uint32_t tbase = tmem + ((sub * 32) << 16) + half * HR;
+            const uint32_t tbase = tmem + ((sub * 32) << 16) + buf * Cfg::BUF_STRIDE + half * HR;
 #pragma unroll 1
             for (uint32_t c0 = 0; c0 < CH; c0 += B) {
                 uint32_t v[B][Cfg::NACC][8];
@@ -590,7 +604,7 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty);
+            if (lane == 0) mbar_arrive(&tempty[buf]);
             if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
         }
     }
@@ -652,19 +666,19 @@ static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t
     return e;
 }
 
-template <int SX>
+template <int SX, int RT>
 static cudaError_t launch_t(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                             cudaStream_t st) {
-    using Cfg = TCfgT<SX>;
+    using Cfg = TCfgT<SX, RT>;
     {
-        cudaError_t e = ensure_smem(c, k_cop_tc_t<SX>, Cfg::SMEM);
+        cudaError_t e = ensure_smem(c, k_cop_tc_t<SX, RT>, Cfg::SMEM);
         if (e != cudaSuccess) return e;
     }
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
     const uint32_t CT = col_tiles(c, kBNW), RTt = (k + Cfg::RT - 1) / Cfg::RT;
     const uint32_t nunits = CT * RTt;
     const uint32_t grid = nunits < (uint32_t)c->num_sms ? nunits : (uint32_t)c->num_sms;
-    cudaError_t e = launch_pdl(k_cop_tc_t<SX>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, c->rns, d_Xt,
+    cudaError_t e = launch_pdl(k_cop_tc_t<SX, RT>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, c->rns, d_Xt,
                                (const uint8_t*)w->d_Et, k, RTt, CT, w->KB, ncol, d_C);
     c->launches++;
     return e;
@@ -676,12 +690,22 @@ static cudaError_t launch_cl(nimbus_ctx* c, const nimbus_encw* w, const uint8_t*
     return c->cluster == 2 ? launch_sx<SX, 2, BN>(c, w, d_Xt, k, d_C, st) : launch_sx<SX, 1, BN>(c, w, d_Xt, k, d_C, st);
 }
 
+// X rows per tile of the transposed kernel (the slice layout follows it): 32 at S_x = 8;
+// at S_x = 4, 64 (one accumulator set, N = 256) unless NIMBUS_T_RT=32 (two sets, the
+// epilogue overlapped: C5 115.5 vs 108.3 ms -- the extra fill per MAC costs more)
+uint32_t transposed_rows(const nimbus_ctx* c) {
+    if (sx_of(c->rns.ell) == 8) return 32;
+    const char* env = getenv("NIMBUS_T_RT");     // read per call: the slice and the kernel agree
+    return env && atoi(env) == 32 ? 32 : 64;
+}
+
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st) {
     const uint32_t SX = sx_of(c->rns.ell);
     if (w->bn == kBNW) {
-        if (SX == 4) return launch_t<4>(c, w, d_Xt, k, d_C, st);
-        if (SX == 8) return launch_t<8>(c, w, d_Xt, k, d_C, st);
+        if (SX == 4) return transposed_rows(c) == 32 ? launch_t<4, 32>(c, w, d_Xt, k, d_C, st)
+                                                     : launch_t<4, 64>(c, w, d_Xt, k, d_C, st);
+        if (SX == 8) return launch_t<8, 32>(c, w, d_Xt, k, d_C, st);
         return cudaErrorInvalidValue;
     }
     if (SX == 8) return cudaErrorInvalidValue;    // 8 slices only in the transposed orientation

@@ -16,7 +16,6 @@ constexpr uint32_t kBK = 128;      // beta (contraction) bytes per k-block = one
 constexpr uint32_t kBNT = 48;      // coefficient columns per Enc(W) tile, streaming kernel (4 planes -> MMA N = 192)
 constexpr uint32_t kBNR = 32;      // tile width of the resident-X kernel (ell <= 16, m <= 768; MMA N = 128)
 constexpr uint32_t kBNW = 128;     // tile width of the transposed ell = 32 kernel (E planes are the MMA A operand)
-constexpr uint32_t kRTT = 64;      // X rows per tile of the transposed kernel (4 slices x 64 rows -> MMA N = 256)
 constexpr uint32_t kResMaxKB = 6;  // resident-X kernel: at most 6 k-blocks (m <= 768) of X in TMEM + smem
 constexpr uint32_t kBM = 128;      // rows (alpha) per X tile = tcgen05 M
 constexpr uint32_t kSW = 4;        // 8-bit slices of a 31-bit residue (S_w)
@@ -137,6 +136,7 @@ cudaError_t launch_tile_plainw(nimbus_ctx* c, const uint32_t* d_W, uint32_t m, u
 cudaError_t launch_plain_matmul(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_t* d_Wt, uint32_t k, uint32_t n,
                                 uint32_t KB, const uint32_t* d_add, uint32_t* d_Y, cudaStream_t st);
 // cop_tc.cu
+uint32_t transposed_rows(const nimbus_ctx* c);
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st);
 }  // namespace nimbus

@@ -374,7 +374,7 @@ def test_batch_matches_sequential_and_oracle(nb, oracle):
     assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all()
 
 
-@pytest.mark.parametrize("env", [{"NIMBUS_TRANSPOSED": "1"},
+@pytest.mark.parametrize("env", [{"NIMBUS_TRANSPOSED": "1"}, {"NIMBUS_TRANSPOSED": "1", "NIMBUS_T_RT": "32"},
                                  {"NIMBUS_NO_RESIDENT": "1"}, {"NIMBUS_CLUSTER": "2"},
                                  {"NIMBUS_NO_RESIDENT": "1", "NIMBUS_CLUSTER": "2"}])
 @pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [(4096, 2, 16, 1, 768, 768, 128, 1),
