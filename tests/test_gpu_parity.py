@@ -562,11 +562,17 @@ def test_width_guards(nb):
 
 
 # ------------------------------------------------------------------ seeded random shapes
-def _fuzz_cases(count=24, seed=2024):
+def _fuzz_cases(count=None, seed=None):
+    """24 seeded cases by default; NIMBUS_FUZZ_CASES=<count> (and NIMBUS_FUZZ_SEED) for a
+    longer soak, which also draws N = 2048 / 4096."""
+    import os
+    count = int(os.environ.get("NIMBUS_FUZZ_CASES", "24")) if count is None else count
+    seed = int(os.environ.get("NIMBUS_FUZZ_SEED", "2024")) if seed is None else seed
+    Ns = [64, 128, 256, 512, 1024] + ([2048, 4096] if count > 24 else [])
     rng = np.random.default_rng(seed)
     out = []
     for _ in range(count):
-        N = int(rng.choice([64, 128, 256, 512, 1024]))
+        N = int(rng.choice(Ns))
         ell = int(rng.choice([4, 8, 12, 16, 24, 32]))
         L = 2 if ell <= 16 else 3
         L_out = 1 if ell <= 16 else 2
