@@ -288,6 +288,42 @@ nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* enc
                                          uint32_t* h_cts, uint64_t* h_R, void* d_ws, size_t ws_bytes,
                                          void* stream);
 
+/* A list of independent matmuls with HOST buffers (e.g. many queries, or every
+ * layer of many queries' passes), pipelined: job i+1's X upload (copy stream) and
+ * job i-1's ciphertext/R download (a second copy stream) run while job i computes
+ * on `stream`, through kHostSlots = 3 device staging slots.  Each job's outputs
+ * are identical to nimbus_cop_matmul_host's for it; jobs must be independent (no
+ * job's h_X is another job's output).  Host buffers should be pinned (pageable
+ * memory works but the copies then do not overlap).  Synchronises `stream` before
+ * returning, so all h_cts / h_R are filled.  Workspace (device):
+ * nimbus_cop_workspace_size_host_batch.  Errors are checked for all jobs before
+ * any copy or launch. */
+typedef struct {
+    const nimbus_encw* encw;
+    const uint32_t* h_X;          /* host, k x m, k = n_queries * k_per_query */
+    uint32_t k_per_query, n_queries;
+    uint64_t mask_seed;
+    uint32_t* h_cts;              /* host, n_queries x n_cts x 2 x L_out x N */
+    uint32_t* h_R;                /* host, k x n */
+} nimbus_cop_host_job;
+nimbus_status nimbus_cop_workspace_size_host_batch(const nimbus_ctx* ctx, const nimbus_cop_host_job* jobs,
+                                                   uint32_t count, size_t* bytes);
+nimbus_status nimbus_cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_host_job* jobs, uint32_t count,
+                                           void* d_ws, size_t ws_bytes, void* stream);
+/* ell > 32: the same with uint64 X and R (same struct layout). */
+typedef struct {
+    const nimbus_encw* encw;
+    const uint64_t* h_X;
+    uint32_t k_per_query, n_queries;
+    uint64_t mask_seed;
+    uint32_t* h_cts;
+    uint64_t* h_R;
+} nimbus_cop_host_job_u64;
+nimbus_status nimbus_cop_workspace_size_host_batch_u64(const nimbus_ctx* ctx, const nimbus_cop_host_job_u64* jobs,
+                                                       uint32_t count, size_t* bytes);
+nimbus_status nimbus_cop_matmul_host_batch_u64(nimbus_ctx* ctx, const nimbus_cop_host_job_u64* jobs, uint32_t count,
+                                               void* d_ws, size_t ws_bytes, void* stream);
+
 /* Step 2 alone (verification of the contraction): d_C is k x 2 x L x N uint32,
  * [alpha][comp][limb][j], the unpacked ciphertexts c[alpha] reduced mod p_i. */
 nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* d_X,

@@ -142,6 +142,7 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
     ctx->device = device;
     ctx->num_sms = prop.multiProcessorCount;
     if (const char* cl = getenv("NIMBUS_CLUSTER")) ctx->cluster = atoi(cl) == 2 ? 2 : 1;
+    if (const char* rr = getenv("NIMBUS_RES")) ctx->res_ring = atoi(rr) == 2 ? 2 : 1;
     Rns& R = ctx->rns;
     R.N = N; R.L = L; R.L_out = Lo; R.ell = ell;
     R.logN = 0; while ((1u << R.logN) < N) R.logN++;
@@ -223,6 +224,7 @@ void nimbus_ctx_destroy(nimbus_ctx* ctx) {
     for (cudaEvent_t e : ctx->sync_ev) cudaEventDestroy(e);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     for (cudaEvent_t e : ctx->stream_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->host_ev) cudaEventDestroy(e);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     delete ctx;
 }
@@ -1077,6 +1079,126 @@ nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* w, 
     DevGuard dg_(ctx);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
+}
+
+// ---------------------------------------------------------------- host-buffer job list, pipelined
+// Workspace: the matmul workspace of the largest job (nimbus_cop_workspace_size),
+// then kHostSlots staging slots (X | cts | R) sized for the largest job.
+static constexpr uint32_t kHostSlots = 3;
+struct HostBatchLayout {
+    size_t mm = 0, slot = 0, x = 0, cts = 0, r = 0, total = 0;   // x / cts / r: offsets inside a slot
+};
+static HostBatchLayout host_batch_layout(const nimbus_ctx* ctx, const nimbus_cop_host_job* jobs, uint32_t count) {
+    auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+    HostBatchLayout H;
+    const size_t es = elem_bytes(ctx->rns.ell);
+    size_t xb = 0, cb = 0, rb = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        const nimbus_cop_host_job& J = jobs[i];
+        const uint32_t k = J.k_per_query * J.n_queries;
+        const WsLayout L = ws_layout(ctx, J.encw, k);
+        H.mm = H.mm > L.total ? H.mm : L.total;                     // what nimbus_cop_matmul checks for
+        xb = std::max(xb, al((size_t)k * J.encw->m * es));
+        cb = std::max(cb, al((size_t)J.n_queries * cts_per_query(ctx, J.k_per_query, J.encw->n) * 2 *
+                             ctx->rns.L_out * ctx->rns.N * 4));
+        rb = std::max(rb, al((size_t)k * J.encw->n * es));
+    }
+    H.x = 0;
+    H.cts = xb;
+    H.r = xb + cb;
+    H.slot = xb + cb + rb;
+    H.total = H.mm + kHostSlots * H.slot;
+    return H;
+}
+
+nimbus_status nimbus_cop_workspace_size_host_batch(const nimbus_ctx* ctx, const nimbus_cop_host_job* jobs,
+                                                   uint32_t count, size_t* bytes) {
+    if (!ctx || !jobs || !bytes || count == 0) return NIMBUS_EINVAL;
+    for (uint32_t i = 0; i < count; i++)
+        if (!jobs[i].encw || jobs[i].encw->ctx != ctx || jobs[i].k_per_query == 0 || jobs[i].n_queries == 0)
+            return NIMBUS_EINVAL;
+    *bytes = host_batch_layout(ctx, jobs, count).total;
+    return NIMBUS_OK;
+}
+
+static nimbus_status cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_host_job* jobs, uint32_t count,
+                                           void* d_ws, size_t ws_bytes, void* stream) {
+    if (!ctx || !jobs || count == 0 || !d_ws) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    for (uint32_t i = 0; i < count; i++) {
+        nimbus_status st = check_online(ctx, jobs[i].encw, jobs[i].k_per_query, jobs[i].n_queries);
+        if (st != NIMBUS_OK) return st;
+        if (!jobs[i].h_X || !jobs[i].h_cts || !jobs[i].h_R) return set_err(ctx, NIMBUS_EINVAL, "null buffer");
+    }
+    const HostBatchLayout H = host_batch_layout(ctx, jobs, count);
+    if (ws_bytes < H.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    const size_t es = elem_bytes(ctx->rns.ell);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!ctx->copy) CK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "copy stream");
+    if (!ctx->side) CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
+    cudaStream_t up = ctx->copy, down = ctx->side;
+    while (ctx->host_ev.size() < 3 * kHostSlots + 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        ctx->host_ev.push_back(e);
+    }
+    cudaEvent_t* ev_x = ctx->host_ev.data();                    // slot's X uploaded
+    cudaEvent_t* ev_c = ev_x + kHostSlots;                      // slot's matmul done
+    cudaEvent_t* ev_o = ev_c + kHostSlots;                      // slot's outputs downloaded (slot free)
+    cudaEvent_t start = ev_o[kHostSlots];
+    // neither copy stream may touch the workspace before earlier work on `stream`
+    CK(cudaEventRecord(start, s), "record");
+    CK(cudaStreamWaitEvent(up, start, 0), "wait");
+    CK(cudaStreamWaitEvent(down, start, 0), "wait");
+    uint8_t* ws = (uint8_t*)d_ws;
+    for (uint32_t i = 0; i < count; i++) {
+        const nimbus_cop_host_job& J = jobs[i];
+        const uint32_t sl = i % kHostSlots, k = J.k_per_query * J.n_queries;
+        uint8_t* slot = ws + H.mm + sl * H.slot;
+        void* dX = slot + H.x;
+        uint32_t* dcts = reinterpret_cast<uint32_t*>(slot + H.cts);
+        const size_t cts_bytes = (size_t)J.n_queries * cts_per_query(ctx, J.k_per_query, J.encw->n) * 2 *
+                                 ctx->rns.L_out * ctx->rns.N * 4;
+        void* dR = slot + H.r;
+        // upload job i's X once the slot's previous outputs are out (job i - kHostSlots)
+        if (i >= kHostSlots) CK(cudaStreamWaitEvent(up, ev_o[sl], 0), "wait slot");
+        CK(cudaMemcpyAsync(dX, J.h_X, (size_t)k * J.encw->m * es, cudaMemcpyHostToDevice, up), "h2d X");
+        CK(cudaEventRecord(ev_x[sl], up), "record");
+        CK(cudaStreamWaitEvent(s, ev_x[sl], 0), "wait X");
+        nimbus_status st = cop_matmul(ctx, J.encw, dX, J.k_per_query, J.n_queries, J.mask_seed, dcts, dR, ws,
+                                      H.mm, stream);
+        if (st != NIMBUS_OK) return st;
+        CK(cudaEventRecord(ev_c[sl], s), "record");
+        // download job i's outputs while job i+1 computes
+        CK(cudaStreamWaitEvent(down, ev_c[sl], 0), "wait matmul");
+        CK(cudaMemcpyAsync(J.h_cts, dcts, cts_bytes, cudaMemcpyDeviceToHost, down), "d2h cts");
+        CK(cudaMemcpyAsync(J.h_R, dR, (size_t)k * J.encw->n * es, cudaMemcpyDeviceToHost, down), "d2h R");
+        CK(cudaEventRecord(ev_o[sl], down), "record");
+    }
+    CK(cudaStreamWaitEvent(s, ev_o[(count - 1) % kHostSlots], 0), "join");
+    CK(cudaStreamSynchronize(s), "host batch sync");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_host_job* jobs, uint32_t count,
+                                           void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 4);
+    return st != NIMBUS_OK ? st : cop_matmul_host_batch(ctx, jobs, count, d_ws, ws_bytes, stream);
+}
+
+nimbus_status nimbus_cop_workspace_size_host_batch_u64(const nimbus_ctx* ctx, const nimbus_cop_host_job_u64* jobs,
+                                                       uint32_t count, size_t* bytes) {
+    return nimbus_cop_workspace_size_host_batch(ctx, reinterpret_cast<const nimbus_cop_host_job*>(jobs), count,
+                                                bytes);
+}
+
+nimbus_status nimbus_cop_matmul_host_batch_u64(nimbus_ctx* ctx, const nimbus_cop_host_job_u64* jobs, uint32_t count,
+                                               void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx);
+    nimbus_status st = want_width(ctx, 8);
+    return st != NIMBUS_OK ? st
+                           : cop_matmul_host_batch(ctx, reinterpret_cast<const nimbus_cop_host_job*>(jobs), count,
+                                                   d_ws, ws_bytes, stream);
 }
 
 static nimbus_status decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t n,

@@ -339,7 +339,17 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                     bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES,
                              &full[s], pol_b);
                     if (first) {
-                        if (kp == 0) { pdl_wait(); TRACE(2); }
+                        if (kp == 0) {
+#ifdef NIMBUS_PF
+                            // while the predecessors (previous pack, this slice) finish, pull the rest of
+                            // this CTA's Enc(W) tiles towards L2: DRAM is otherwise idle until X is ready
+                            const uint32_t tb = KB * Cfg::B_BYTES;
+                            if (KB > Cfg::KPS) prefetch_l2_bulk(b_src + Cfg::SLOT, tb - Cfg::SLOT);
+                            for (uint32_t c2 = ct + gridDim.x; c2 < CT; c2 += gridDim.x)
+                                prefetch_l2_bulk(Et + (size_t)c2 * tb, tb);
+#endif
+                            pdl_wait(); TRACE(2);
+                        }
                         else mbar_wait(&sfree[0], (kp - 1) & 1);       // staging copied into TMEM
                         for (uint32_t q = 0; q < nkb; q++) {
                             const uint8_t* xsrc = Xt + (size_t)(kb0 + q) * 2 * Cfg::SLICE;   // Xt[0][kb][slice]
@@ -422,6 +432,236 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) TRACE(3);
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, Cfg::TMEM_COLS);
+    }
+}
+
+// ------------------------------------------------------------------ resident-X kernel, deep E ring
+// Same contraction as k_cop_tc_res, with the shared memory given to the Enc(W)
+// stream instead: slice 0 (all k-blocks) AND slice 1 of k-blocks 0..3 live in
+// TMEM (both read by `kind::i8` MMAs as A from TMEM), only slice 1 of k-blocks
+// 4..5 stays in shared memory, and one accumulator set (5 x 32 columns) is
+// released by the epilogue as soon as it has been loaded into registers (the
+// recombination and the stores then overlap the next tile's MMAs).  TMEM:
+// 192 + 128 + 160 = 480 columns.  Shared memory: 32 KB of slice 1 + a 6-slot
+// ring of 32 KB (192 KB; k_cop_tc_res: 96 KB).  Why: at k = 128 the MMAs of a
+// 32 KB slot (~0.53 us) hold it out of the stream, so with 3 slots only ~2 are
+// in flight and the per-SM Enc(W) rate stays at ~30 GB/s; a short cold stream
+// needs more bytes in flight per SM than that (tools/stream_prefetch.cu).
+// Ring messages, in the order producer and MMA issuer both follow: every
+// (tile, k-block pair) kp is one E message; in the first tile it is followed by
+// an X0 message (slice 0 of the pair -> TMEM) and, for pairs below k-block 4, an
+// X1 message (slice 1 -> TMEM); slice 1 of pairs from k-block 4 on is copied
+// straight into its resident place on the X0 message's barrier.
+struct ResCfg2 {
+    static constexpr uint32_t BM = kBM, BN = kBNR, BK = kBK, SX = 2;
+    static constexpr uint32_t SLICE = BM * BK;                 // one X slice, one k-block: 16 KB
+    static constexpr uint32_t B_BYTES = kSW * BN * BK;         // Enc(W) per k-block: 16 KB
+    static constexpr uint32_t KPS = 2;                         // k-blocks per message: 32 KB
+    static constexpr uint32_t SLOT = KPS * B_BYTES;
+    static constexpr uint32_t STAGES = 6;
+    static constexpr uint32_t T1 = 4;                          // slice-1 k-blocks in TMEM
+    static constexpr uint32_t NACC = SX + kSW - 1;             // 5
+    static constexpr uint32_t ACC_COLS = NACC * BN;            // 160
+    static constexpr uint32_t A0_COL = 0, A1_COL = kResMaxKB * (BK / 4), ACC_COL = A1_COL + T1 * (BK / 4);
+    static constexpr uint32_t TMEM_COLS = 512;
+    static constexpr uint32_t EPI_WARPS = 8;
+    static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
+    // smem: slice 1 k-blocks T1.. [KB - T1][16 KB] | ring [STAGES][32 KB]
+    static constexpr uint32_t OFF_A1 = 0, OFF_B = (kResMaxKB - T1) * SLICE;
+    static constexpr size_t SMEM = (size_t)OFF_B + STAGES * SLOT + 1024 + 256;
+    static_assert(ACC_COL + ACC_COLS <= TMEM_COLS, "TMEM budget");
+    static_assert(SMEM <= 232448, "shared memory");
+    static_assert(T1 % KPS == 0, "a k-block pair is either in TMEM or in smem");
+    static_assert(SLOT == KPS * SLICE, "an X message fills one slot");
+};
+
+__global__ void __launch_bounds__(ResCfg2::THREADS, 1)
+k_cop_tc_res2(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t CT,
+              uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
+    using Cfg = ResCfg2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::SLOT);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) TRACE(0);
+    if (warp == 0 && lane == 0) {
+        for (uint32_t s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, Cfg::EPI_WARPS);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) TRACE(1);
+    pdl_trigger();
+    const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- producer
+            const uint64_t pol_a = policy_evict_last();
+            const uint64_t pol_b = policy_evict_first();
+            uint32_t it = 0, ti = 0;
+            auto acquire = [&](uint32_t bytes) {
+                const uint32_t s = it % Cfg::STAGES;
+                if (it >= Cfg::STAGES) mbar_wait(&empty[s], ((it / Cfg::STAGES) & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[s], bytes);
+                it++;
+                return s;
+            };
+            for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+                const uint8_t* b_src = Et + (size_t)ct * KB * Cfg::B_BYTES;
+                for (uint32_t kp = 0; kp < KP; kp++) {
+                    const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
+                    uint32_t s = acquire(nkb * Cfg::B_BYTES);
+                    bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES,
+                             nkb * Cfg::B_BYTES, &full[s], pol_b);
+                    if (ti == 0) {
+                        if (kp == 0) { pdl_wait(); TRACE(2); }
+                        const bool res1 = kb0 >= Cfg::T1;          // slice 1 of this pair resident in smem
+                        s = acquire(nkb * Cfg::SLICE * (res1 ? 2 : 1));
+                        for (uint32_t q = 0; q < nkb; q++) {
+                            const uint8_t* xsrc = Xt + (size_t)(kb0 + q) * 2 * Cfg::SLICE;   // Xt[kb][slice]
+                            bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT + q * Cfg::SLICE, xsrc, Cfg::SLICE, &full[s],
+                                     pol_a);
+                            if (res1)
+                                bulk_g2s(smem + Cfg::OFF_A1 + (kb0 + q - Cfg::T1) * Cfg::SLICE, xsrc + Cfg::SLICE,
+                                         Cfg::SLICE, &full[s], pol_a);
+                        }
+                        if (!res1) {
+                            s = acquire(nkb * Cfg::SLICE);
+                            for (uint32_t q = 0; q < nkb; q++)
+                                bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT + q * Cfg::SLICE,
+                                         Xt + (size_t)(kb0 + q) * 2 * Cfg::SLICE + Cfg::SLICE, Cfg::SLICE, &full[s],
+                                         pol_a);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer
+            constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 128
+            constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 96
+            constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = 32
+            const uint32_t dacc = tmem + Cfg::ACC_COL;
+            uint32_t it = 0, ti = 0;
+            auto take = [&]() {
+                const uint32_t s = it % Cfg::STAGES;
+                mbar_wait(&full[s], (it / Cfg::STAGES) & 1);
+                it++;
+                tc_fence_after();
+                return s;
+            };
+            // X message in slot s: k-blocks kb0.. of one slice -> TMEM columns col0 + 32 kb
+            auto x_to_tmem = [&](uint32_t s, uint32_t kb0, uint32_t nkb, uint32_t col0) {
+                for (uint32_t q = 0; q < nkb; q++) {
+                    const uint32_t stg = smem_u32(smem + Cfg::OFF_B + s * Cfg::SLOT + q * Cfg::SLICE);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
+                        tmem_cp_128x256b(tmem + col0 + (kb0 + q) * (Cfg::BK / 4) + kk * 8,
+                                         sdesc_kmajor_sw128(stg + kk * 32));
+                }
+                mma_commit(&empty[s]);
+            };
+            for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+                if (ti >= 1) mbar_wait(tempty, (ti - 1) & 1);     // previous tile's accumulators are in registers
+                TRACE(4 + 4 * ti);
+                tc_fence_after();
+                for (uint32_t kp = 0; kp < KP; kp++) {
+                    const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
+                    const uint32_t sE = take();
+                    if (ti == 0) {
+                        x_to_tmem(take(), kb0, nkb, Cfg::A0_COL);
+                        if (kb0 < Cfg::T1) x_to_tmem(take(), kb0, nkb, Cfg::A1_COL);
+                    }
+                    for (uint32_t q = 0; q < nkb; q++) {
+                        const uint32_t kb = kb0 + q;
+                        const uint32_t b0 = smem_u32(smem + Cfg::OFF_B + sE * Cfg::SLOT + q * Cfg::B_BYTES);
+                        const bool t1 = kb < Cfg::T1;
+                        const uint32_t a1s = t1 ? 0u : smem_u32(smem + Cfg::OFF_A1 + (kb - Cfg::T1) * Cfg::SLICE);
+#pragma unroll
+                        for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
+                            const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
+                            const uint32_t first = (kb | kk) == 0;
+                            mma_i8_ts(dacc, tmem + Cfg::A0_COL + kb * (Cfg::BK / 4) + kk * 8, bd, idesc_full, !first);
+                            const uint32_t a1t = tmem + Cfg::A1_COL + kb * (Cfg::BK / 4) + kk * 8;
+                            if (!first) {
+                                if (t1) mma_i8_ts(dacc + Cfg::BN, a1t, bd, idesc_full, 1u);
+                                else mma_i8_ss(dacc + Cfg::BN, sdesc_kmajor_sw128(a1s + kk * 32), bd, idesc_full, 1u);
+                            } else {
+                                // acc_1..3 accumulate onto x_0's first products, acc_4 starts here (kb 0 is in TMEM)
+                                const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (kSW - 1) * Cfg::BN * Cfg::BK + kk * 32);
+                                mma_i8_ts(dacc + Cfg::BN, a1t, bd, idesc_lo, 1u);
+                                mma_i8_ts(dacc + kSW * Cfg::BN, a1t, bd3, idesc_one, 0u);
+                            }
+                        }
+                    }
+                    mma_commit(&empty[sE]);
+                }
+                mma_commit(tfull);
+                TRACE(5 + 4 * ti);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: load the whole set, release it, then recombine and store
+        const uint32_t ew = warp - 4;
+        const uint32_t sub = ew & 3, half = ew >> 2;
+        const uint32_t row = sub * 32 + lane;
+        constexpr uint32_t CPW = Cfg::BN / 8 / 2;                 // 2 chunks of 8 columns per warp
+        const uint32_t tacc = tmem + ((sub * 32) << 16) + Cfg::ACC_COL;
+        uint32_t ti = 0;
+        for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+            mbar_wait(tfull, ti & 1);
+            if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
+            tc_fence_after();
+            uint32_t v[CPW][Cfg::NACC][8];
+#pragma unroll
+            for (uint32_t b = 0; b < CPW; b++)
+#pragma unroll
+                for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld8(tacc + s * Cfg::BN + (half * CPW + b) * 8, v[b][s]);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+#pragma unroll
+            for (uint32_t b = 0; b < CPW; b++) {
+                const uint32_t col0 = ct * Cfg::BN + (half * CPW + b) * 8;
+                if (col0 >= ncol || row >= k) continue;
+                const uint32_t limb = (col0 / R.N) % R.L;
+                const uint32_t p = R.p[limb], c32 = R.c32[limb];
+                uint32_t out[8];
+#pragma unroll
+                for (uint32_t u = 0; u < 8; u++) {
+                    uint64_t x = v[b][0][u];
+                    x = mad_wide(v[b][1][u], 1u << 8, x);
+                    x = mad_wide(v[b][2][u], 1u << 16, x);
+                    x = mad_wide(v[b][3][u], 1u << 24, x);
+                    x = mad_wide(v[b][4][u], R.pow8[limb][4], x);
+                    out[u] = reduce64_pm(x, p, c32);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ncol + col0);
+                dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+                dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+            }
             if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
         }
     }
@@ -653,6 +893,17 @@ static cudaError_t launch_sx(nimbus_ctx* c, const nimbus_encw* w, const uint8_t*
 
 static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint32_t* d_C,
                               cudaStream_t st) {
+    if (c->res_ring == 2) {
+        cudaError_t e = ensure_smem(c, k_cop_tc_res2, ResCfg2::SMEM);
+        if (e != cudaSuccess) return e;
+        const uint32_t ncol = 2 * c->rns.L * c->rns.N;
+        const uint32_t CT = col_tiles(c, kBNR);
+        const uint32_t grid = CT < (uint32_t)c->num_sms ? CT : (uint32_t)c->num_sms;
+        e = launch_pdl(k_cop_tc_res2, dim3(grid), dim3(ResCfg2::THREADS), ResCfg2::SMEM, st, c->rns, d_Xt,
+                       (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, d_C);
+        c->launches++;
+        return e;
+    }
     {
         cudaError_t e = ensure_smem(c, k_cop_tc_res, ResCfg::SMEM);
         if (e != cudaSuccess) return e;

@@ -36,6 +36,7 @@ struct nimbus_ctx {
     std::string err;
     uint64_t launches = 0;
     int num_sms = 148;
+    int res_ring = 1;              // resident-X contraction: 1 = 3-slot ring + slice 1 in smem, 2 = deep ring (k_cop_tc_res2); env NIMBUS_RES
     int cluster = 1;               // CTAs per cluster of the streaming contraction (2 = X multicast); env NIMBUS_CLUSTER
     // stage profiling (nimbus_profile_*): pending event quadruples, accumulated ms
     bool profile = false;
@@ -48,6 +49,8 @@ struct nimbus_ctx {
     // streamed path (nimbus_cop_matmul_streamed): host -> device copy stream + events
     cudaStream_t copy = nullptr;
     std::vector<cudaEvent_t> stream_ev;
+    // host-buffer job list (nimbus_cop_matmul_host_batch): per staging slot X-up / matmul / outputs-down events
+    std::vector<cudaEvent_t> host_ev;
     // grow-only device scratch for the canonical rows of Enc(W) during (re-)encryption
     void* d_scratch = nullptr;
     size_t scratch_bytes = 0;

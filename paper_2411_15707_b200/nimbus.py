@@ -69,6 +69,10 @@ _SIGS = {
     "nimbus_cop_matmul_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
     "nimbus_decrypt_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _vp]),
     "nimbus_cop_matmul_host_u64": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_cop_workspace_size_host_batch": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
+    "nimbus_cop_matmul_host_batch": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
+    "nimbus_cop_workspace_size_host_batch_u64": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
+    "nimbus_cop_matmul_host_batch_u64": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_cop_workspace_size_batch_u64": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
     "nimbus_cop_matmul_batch_u64": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_cop_stage_size_u64": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
@@ -512,6 +516,40 @@ def nimbus_cop_matmul_host_u64(ctx: Context, w: EncW, X_host: torch.Tensor, k_pe
                                             _ptr(R_host, torch.int64, "R"), _ptr(ws), ws.numel(),
                                             _stream(stream)), ctx)
     return cts_host, R_host
+
+
+class nimbus_cop_host_job(C.Structure):
+    _fields_ = [("encw", _vp), ("h_X", _vp), ("k_per_query", _u32), ("n_queries", _u32),
+                ("mask_seed", _u64), ("h_cts", _vp), ("h_R", _vp)]
+
+
+def _host_jobs(jobs, wide=False):
+    """jobs: sequence of dicts with encw, X, k_per_query, n_queries, mask_seed, cts, R -- all HOST
+    tensors (pinned for overlap); X and R int64 holding uint64 when wide (ell > 32)."""
+    dt = torch.int64 if wide else torch.int32
+    arr = (nimbus_cop_host_job * len(jobs))()
+    for i, j in enumerate(jobs):
+        for nm in ("X", "cts", "R"):
+            if j[nm].is_cuda:
+                raise ValueError(f"job {i}: {nm} must be a host tensor")
+        arr[i] = nimbus_cop_host_job(j["encw"].ptr, _ptr(j["X"], dt, "X"), j["k_per_query"], j["n_queries"],
+                                     j["mask_seed"], _ptr(j["cts"], torch.int32, "cts"), _ptr(j["R"], dt, "R"))
+    return arr
+
+
+def nimbus_cop_workspace_size_host_batch(ctx: Context, jobs, wide=False) -> int:
+    out = _sz()
+    fn = lib().nimbus_cop_workspace_size_host_batch_u64 if wide else lib().nimbus_cop_workspace_size_host_batch
+    _check(fn(ctx.ptr, _host_jobs(jobs, wide), len(jobs), C.byref(out)), ctx)
+    return int(out.value)
+
+
+def nimbus_cop_matmul_host_batch(ctx: Context, jobs, ws: torch.Tensor, stream=None, wide=False):
+    """Pipelined host-buffer job list (uploads / downloads overlap the compute); returns
+    when every job's cts and R are in host memory."""
+    arr = _host_jobs(jobs, wide)
+    fn = lib().nimbus_cop_matmul_host_batch_u64 if wide else lib().nimbus_cop_matmul_host_batch
+    _check(fn(ctx.ptr, arr, len(jobs), _ptr(ws), ws.numel(), _stream(stream)), ctx)
 
 
 def nimbus_cop_accumulate(ctx: Context, w: EncW, X: torch.Tensor, ws: torch.Tensor, C_out=None,

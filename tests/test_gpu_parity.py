@@ -254,6 +254,74 @@ def test_host_buffer_api_matches_device(nb, oracle):
     assert torch.equal(cts_h, cts_p)
 
 
+def test_host_batch_matches_single_calls(nb, oracle):
+    """nimbus_cop_matmul_host_batch (uploads / downloads pipelined over 3 staging
+    slots) gives, for every job of a mixed list longer than the slot count, the
+    bytes nimbus_cop_matmul gives for it; one job checked against the oracle; a
+    job list with a device tensor or a bad shape is refused before any work."""
+    N, L, ell, L_out = 4096, 2, 16, 1
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, 21)
+    shapes = [(128, 768, 768, 1), (64, 300, 700, 2), (128, 768, 3072, 1), (100, 1000, 500, 1), (16, 64, 64, 1),
+              (128, 768, 768, 1), (33, 129, 5, 3)]
+    encs = {}
+    jobs, ref = [], []
+    for i, (kq, m, n, nq) in enumerate(shapes):
+        if (m, n) not in encs:
+            W = ni.gen_W(140 + i, m, n, ell)
+            encs[(m, n)] = (W, nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W), 140 + i))
+        W, w = encs[(m, n)]
+        Xn = ni.gen_X(150 + i, kq * nq, m, ell)
+        ws = nb.alloc_workspace(ctx, w, kq * nq)
+        c0, R0 = nb.alloc_outputs(ctx, w, kq, nq)
+        nb.nimbus_cop_matmul(ctx, w, dev_u32(Xn), kq, nq, 160 + i, c0, R0, ws)
+        ref.append((c0.cpu(), R0.cpu()))
+        cts, R = nb.alloc_outputs(ctx, w, kq, nq, pin=True, device="cpu")
+        jobs.append(dict(encw=w, X=torch.from_numpy(Xn.view(np.int32)).pin_memory(), k_per_query=kq,
+                         n_queries=nq, mask_seed=160 + i, cts=cts, R=R, Xn=Xn, W=W))
+    nb.nimbus_sync(ctx)
+    wsb = torch.empty(nb.nimbus_cop_workspace_size_host_batch(ctx, jobs), dtype=torch.uint8, device=DEV)
+    nb.nimbus_cop_matmul_host_batch(ctx, jobs, wsb)
+    for j, (c0, R0) in zip(jobs, ref):
+        assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+    j = jobs[3]
+    pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
+    E = oracle.encrypt_rows(N, L, pr, ell, oracle.keygen(N, 21), j["W"], 143)
+    cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E, j["Xn"], j["W"].shape[1], j["k_per_query"],
+                                   j["n_queries"], j["mask_seed"])
+    assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all()
+    # refused before any work: a device tensor, a workspace too small
+    bad = dict(jobs[0], X=jobs[0]["X"].cuda())
+    with pytest.raises(ValueError):
+        nb.nimbus_cop_matmul_host_batch(ctx, [jobs[1], bad], wsb)
+    with pytest.raises(nb.NimbusError):
+        nb.nimbus_cop_matmul_host_batch(ctx, jobs, wsb[:1024])
+
+
+def test_host_batch_u64(nb, oracle):
+    """The same pipelined host-buffer list at ell = 64 (uint64 X / R)."""
+    N, L, ell, L_out = 256, 5, 64, 3
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, 9)
+    shapes = [(33, 130, 100, 2), (7, 300, 128, 1), (64, 64, 256, 1), (20, 50, 60, 1)]
+    jobs, ref = [], []
+    for i, (kq, m, n, nq) in enumerate(shapes):
+        w = nb.nimbus_encrypt_weights_u64(ctx, sk, _dev_u64(ni.gen_W(70 + i, m, n, ell)), 70 + i)
+        X = _dev_u64(ni.gen_X(80 + i, kq * nq, m, ell))
+        ws = nb.alloc_workspace(ctx, w, kq * nq)
+        c0, R0 = nb.alloc_outputs_u64(ctx, w, kq, nq)
+        nb.nimbus_cop_matmul_u64(ctx, w, X, kq, nq, 90 + i, c0, R0, ws)
+        ref.append((c0.cpu(), R0.cpu()))
+        jobs.append(dict(encw=w, X=X.cpu().pin_memory(), k_per_query=kq, n_queries=nq, mask_seed=90 + i,
+                         cts=torch.zeros_like(c0, device="cpu").pin_memory(),
+                         R=torch.zeros_like(R0, device="cpu").pin_memory()))
+    nb.nimbus_sync(ctx)
+    wsb = torch.empty(nb.nimbus_cop_workspace_size_host_batch(ctx, jobs, wide=True), dtype=torch.uint8, device=DEV)
+    nb.nimbus_cop_matmul_host_batch(ctx, jobs, wsb, wide=True)
+    for j, (c0, R0) in zip(jobs, ref):
+        assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+
+
 # ------------------------------------------------------------------ full-size configs (sampled)
 def _sampled_check(c, cts, n_samples=600, rng_seed=0):
     nct = cts.shape[1]
@@ -376,7 +444,8 @@ def test_batch_matches_sequential_and_oracle(nb, oracle):
 
 @pytest.mark.parametrize("env", [{"NIMBUS_TRANSPOSED": "1"}, {"NIMBUS_TRANSPOSED": "1", "NIMBUS_T_RT": "32"},
                                  {"NIMBUS_NO_RESIDENT": "1"}, {"NIMBUS_CLUSTER": "2"},
-                                 {"NIMBUS_NO_RESIDENT": "1", "NIMBUS_CLUSTER": "2"}])
+                                 {"NIMBUS_NO_RESIDENT": "1", "NIMBUS_CLUSTER": "2"}, {"NIMBUS_RES": "1"},
+                                 {"NIMBUS_RES": "2"}])
 @pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [(4096, 2, 16, 1, 768, 768, 128, 1),
                                                      (8192, 3, 32, 2, 300, 1000, 70, 3)])
 def test_kernel_variants_parity(nb, oracle, monkeypatch, env, N, L, ell, L_out, m, n, kq, nq):
@@ -386,6 +455,20 @@ def test_kernel_variants_parity(nb, oracle, monkeypatch, env, N, L, ell, L_out, 
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=777 + m)
+    cts, R = c.run()
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+
+
+@pytest.mark.parametrize("res", ["1", "2"])
+@pytest.mark.parametrize("m,n,kq,nq", [(64, 64, 16, 1), (129, 200, 128, 1), (300, 1000, 70, 1), (520, 768, 33, 2),
+                                       (640, 3072, 128, 1), (768, 5, 128, 1)])
+def test_resident_kernels_parity(nb, oracle, monkeypatch, res, m, n, kq, nq):
+    """Both resident-X contraction kernels (ell = 16, k <= 128, m <= 768): k-block
+    counts 1..6 (odd counts leave a half k-block pair; from k-block 4 on slice 1
+    sits in shared memory in the deep-ring kernel), ragged rows and columns."""
+    monkeypatch.setenv("NIMBUS_RES", res)
+    c = Case(nb, oracle, 4096, 2, 16, 1, m, n, kq, nq, seed=4242 + m + n)
     cts, R = c.run()
     cts_o, R_o = c.oracle_out()
     assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
