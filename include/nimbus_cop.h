@@ -291,7 +291,7 @@ nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* enc
 /* A list of independent matmuls with HOST buffers (e.g. many queries, or every
  * layer of many queries' passes), pipelined: job i+1's X upload (copy stream) and
  * job i-1's ciphertext/R download (a second copy stream) run while job i computes
- * on `stream`, through kHostSlots = 3 device staging slots.  Each job's outputs
+ * on `stream`, through 4 device staging slots.  Each job's outputs
  * are identical to nimbus_cop_matmul_host's for it; jobs must be independent (no
  * job's h_X is another job's output).  Host buffers should be pinned (pageable
  * memory works but the copies then do not overlap).  Synchronises `stream` before

@@ -1084,7 +1084,7 @@ nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* w, 
 // ---------------------------------------------------------------- host-buffer job list, pipelined
 // Workspace: the matmul workspace of the largest job (nimbus_cop_workspace_size),
 // then kHostSlots staging slots (X | cts | R) sized for the largest job.
-static constexpr uint32_t kHostSlots = 3;
+static constexpr uint32_t kHostSlots = 4;
 struct HostBatchLayout {
     size_t mm = 0, slot = 0, x = 0, cts = 0, r = 0, total = 0;   // x / cts / r: offsets inside a slot
 };
@@ -1150,29 +1150,55 @@ static nimbus_status cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_hos
     CK(cudaStreamWaitEvent(up, start, 0), "wait");
     CK(cudaStreamWaitEvent(down, start, 0), "wait");
     uint8_t* ws = (uint8_t*)d_ws;
-    for (uint32_t i = 0; i < count; i++) {
+    auto slot_of = [&](uint32_t i) { return ws + H.mm + (i % kHostSlots) * H.slot; };
+    auto cts_bytes = [&](const nimbus_cop_host_job& J) {
+        return (size_t)J.n_queries * cts_per_query(ctx, J.k_per_query, J.encw->n) * 2 * ctx->rns.L_out *
+               ctx->rns.N * 4;
+    };
+    // upload job i's X into its slot once the matmul that last used the slot (job i - S) is done
+    auto upload = [&](uint32_t i) -> nimbus_status {
         const nimbus_cop_host_job& J = jobs[i];
-        const uint32_t sl = i % kHostSlots, k = J.k_per_query * J.n_queries;
-        uint8_t* slot = ws + H.mm + sl * H.slot;
-        void* dX = slot + H.x;
+        if (i >= kHostSlots) CK(cudaStreamWaitEvent(up, ev_c[i % kHostSlots], 0), "wait slot X");
+        CK(cudaMemcpyAsync(slot_of(i) + H.x, J.h_X, (size_t)J.k_per_query * J.n_queries * J.encw->m * es,
+                           cudaMemcpyHostToDevice, up), "h2d X");
+        CK(cudaEventRecord(ev_x[i % kHostSlots], up), "record");
+        return NIMBUS_OK;
+    };
+    // `stream` may start job i once its X is up and its output buffers were read out (job i - S)
+    auto admit = [&](uint32_t i) -> nimbus_status {
+        CK(cudaStreamWaitEvent(s, ev_x[i % kHostSlots], 0), "wait X");
+        if (i >= kHostSlots) CK(cudaStreamWaitEvent(s, ev_o[i % kHostSlots], 0), "wait slot out");
+        return NIMBUS_OK;
+    };
+    nimbus_status st = upload(0);
+    if (st == NIMBUS_OK) st = admit(0);
+    for (uint32_t i = 0; i < count && st == NIMBUS_OK; i++) {
+        const nimbus_cop_host_job& J = jobs[i];
+        const uint32_t k = J.k_per_query * J.n_queries;
+        uint8_t* slot = slot_of(i);
         uint32_t* dcts = reinterpret_cast<uint32_t*>(slot + H.cts);
-        const size_t cts_bytes = (size_t)J.n_queries * cts_per_query(ctx, J.k_per_query, J.encw->n) * 2 *
-                                 ctx->rns.L_out * ctx->rns.N * 4;
         void* dR = slot + H.r;
-        // upload job i's X once the slot's previous outputs are out (job i - kHostSlots)
-        if (i >= kHostSlots) CK(cudaStreamWaitEvent(up, ev_o[sl], 0), "wait slot");
-        CK(cudaMemcpyAsync(dX, J.h_X, (size_t)k * J.encw->m * es, cudaMemcpyHostToDevice, up), "h2d X");
-        CK(cudaEventRecord(ev_x[sl], up), "record");
-        CK(cudaStreamWaitEvent(s, ev_x[sl], 0), "wait X");
-        nimbus_status st = cop_matmul(ctx, J.encw, dX, J.k_per_query, J.n_queries, J.mask_seed, dcts, dR, ws,
-                                      H.mm, stream);
-        if (st != NIMBUS_OK) return st;
-        CK(cudaEventRecord(ev_c[sl], s), "record");
-        // download job i's outputs while job i+1 computes
-        CK(cudaStreamWaitEvent(down, ev_c[sl], 0), "wait matmul");
-        CK(cudaMemcpyAsync(J.h_cts, dcts, cts_bytes, cudaMemcpyDeviceToHost, down), "d2h cts");
+        // job i+1's prerequisites go into `stream` BEFORE job i's kernels, so that job i's pack and
+        // job i+1's slice stay adjacent (programmatic dependent launch across jobs)
+        if (i + 1 < count) {
+            st = upload(i + 1);
+            if (st == NIMBUS_OK) st = admit(i + 1);
+            if (st != NIMBUS_OK) break;
+        }
+        st = cop_matmul(ctx, J.encw, slot + H.x, J.k_per_query, J.n_queries, J.mask_seed, dcts, dR, ws, H.mm,
+                        stream);
+        if (st != NIMBUS_OK) break;
+        CK(cudaEventRecord(ev_c[i % kHostSlots], s), "record");
+        // download job i's outputs while the next jobs compute
+        CK(cudaStreamWaitEvent(down, ev_c[i % kHostSlots], 0), "wait matmul");
+        CK(cudaMemcpyAsync(J.h_cts, dcts, cts_bytes(J), cudaMemcpyDeviceToHost, down), "d2h cts");
         CK(cudaMemcpyAsync(J.h_R, dR, (size_t)k * J.encw->n * es, cudaMemcpyDeviceToHost, down), "d2h R");
-        CK(cudaEventRecord(ev_o[sl], down), "record");
+        CK(cudaEventRecord(ev_o[i % kHostSlots], down), "record");
+    }
+    if (st != NIMBUS_OK) {
+        cudaStreamSynchronize(up);          // no copy may outlive the call into a buffer the caller frees
+        cudaStreamSynchronize(down);
+        return st;
     }
     CK(cudaStreamWaitEvent(s, ev_o[(count - 1) % kHostSlots], 0), "join");
     CK(cudaStreamSynchronize(s), "host batch sync");

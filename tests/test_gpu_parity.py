@@ -255,7 +255,7 @@ def test_host_buffer_api_matches_device(nb, oracle):
 
 
 def test_host_batch_matches_single_calls(nb, oracle):
-    """nimbus_cop_matmul_host_batch (uploads / downloads pipelined over 3 staging
+    """nimbus_cop_matmul_host_batch (uploads / downloads pipelined over 4 staging
     slots) gives, for every job of a mixed list longer than the slot count, the
     bytes nimbus_cop_matmul gives for it; one job checked against the oracle; a
     job list with a device tensor or a bad shape is refused before any work."""
