@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--impl", default="tcgen05", choices=["tcgen05", "cudacore", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="skip the secondary timing of the steps replayed from a CUDA graph")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-stage-profile", action="store_true", help="no per-stage events inside the step")
     ap.add_argument("--l2", default="rotate", choices=["rotate", "write"],
@@ -272,15 +274,18 @@ def run_gpu(args, cfg, rank, world, local_rank):
             flush.zero_()
         step_no[0] += 1
 
-    def step():
+    def step_on(st):
         c = step_no[0] % n_copies
         if ws_batch is not None:
-            batch(ctx, jobs[c], ws_batch)
+            batch(ctx, jobs[c], ws_batch, stream=st)
             return
         for mt in mats:
             lay = mt["lay"]
             matmul(ctx, mt["encw"][c], mt["X"][c], lay.k_per_query, lay.n_queries, mt["seed"],
-                   mt["cts"], mt["R"], mt["ws"])
+                   mt["cts"], mt["R"], mt["ws"], stream=st)
+
+    def step():
+        step_on(stream)
 
     for _ in range(max(args.warmup, n_copies)):
         cold()
@@ -297,21 +302,31 @@ def run_gpu(args, cfg, rank, world, local_rank):
             step()
         torch.cuda.synchronize()
 
-    def timed(profile: bool):
-        """K steps, each preceded (outside the timed window) by an L2 flush."""
+    def timed(profile: bool, per_step: bool):
+        """K steps.  per_step: CUDA events around every step (and, with --l2 write, the flush
+        between steps outside them); otherwise one event pair around the K back-to-back steps,
+        so the PDL chain runs on from one step's pack into the next step's slice and
+        contraction (with --l2 rotate every step already reads inputs not in L2)."""
         nb.nimbus_profile_enable(ctx, profile)
         nb.nimbus_profile_read(ctx, reset=True)
         launches0 = nb.nimbus_launch_count(ctx)
-        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        n_ev = args.steps if per_step else 1
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        if not per_step:
+            starts[0].record(stream)
         for i in range(args.steps):
             cold()                              # Enc(W), X of this step are not in L2
-            starts[i].record(stream)
+            if per_step:
+                starts[i].record(stream)
             step()
-            ends[i].record(stream)
+            if per_step:
+                ends[i].record(stream)
+        if not per_step:
+            ends[0].record(stream)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -322,6 +337,33 @@ def run_gpu(args, cfg, rank, world, local_rank):
         total = sum(step_ms)
         total = max_over_ranks(total, world, dev)
         return total, step_ms, stage_ms, calls, launches
+
+    def timed_graph():
+        """K steps replayed from a CUDA graph holding n_copies consecutive steps (one per
+        input copy, so the rotation is the same as in pass A)."""
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        g = torch.cuda.CUDAGraph()
+        nonlocal_step = step_no[0]
+        with torch.cuda.graph(g, stream=gs, capture_error_mode="thread_local"):
+            for c in range(n_copies):
+                step_no[0] = c
+                step_on(gs)
+        step_no[0] = nonlocal_step
+        reps = -(-args.steps // n_copies)
+        g.replay()
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a_.record(stream)
+        for _ in range(reps):
+            g.replay()
+        b_.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(a_.elapsed_time(b_), world, dev)
+        return ms / (reps * n_copies)
 
     # pass A (the reported number): the step exactly as a user runs it, no events inside
     # clocks: the sampler is already polling when the timed region starts; a region
@@ -338,7 +380,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     clocks.wait_samples(1, busy=busy)
     n0 = len(clocks.lines)
-    total_ms, step_ms, _, _, launches = timed(profile=False)
+    total_ms, _, _, _, launches = timed(profile=False, per_step=args.l2 == "write")
     clocks.wait_samples(n0 + 2, busy=busy)
     clk = clocks.stop()
     # pass B (roofline evidence): same K steps with CUDA events around each kernel of the
@@ -347,7 +389,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     calls = 0
     stage_ms = [0.0, 0.0, 0.0]
     if not args.no_stage_profile:
-        _, _, stage_ms, calls, _ = timed(profile=True)
+        _, _, stage_ms, calls, _ = timed(profile=True, per_step=False)
+    # per-step distribution (events around every step: no PDL overlap across steps)
+    _, step_ms, _, _, _ = timed(profile=False, per_step=True)
+    graph_ms = timed_graph() if args.graph and args.l2 == "rotate" else None
     # secondary: warm L2 -- the same copy every step, when the step's
     # Enc(W) fits in half the L2; rank-local, no barrier
     warm_ms = None
@@ -429,7 +474,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     l2_desc = (f"cold: {n_copies} rotating copies of Enc(W)+X ({n_copies * enc_bytes >> 20} MiB >= 3x the "
                f"{l2_bytes >> 20} MiB L2), step i reads copy i mod {n_copies}" if args.l2 == "rotate" else
                f"flushed by a {L2_FLUSH_BYTES >> 20} MiB write before every timed step")
-    return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=stage_ms, calls=calls, launches=launches,
+    return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=stage_ms, calls=calls, launches=launches, graph_ms=graph_ms,
                 clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e, l2_desc=l2_desc, warm_ms=warm_ms,
                 setup=dict(gpu_ms=setup_gpu_ms, host_s=setup_host_s, bytes=setup_bytes))
 
@@ -592,11 +637,16 @@ def main():
                                         "contraction": res["stage_ms"][1] / args.steps,
                                         "pack_moddown_mask": res["stage_ms"][2] / args.steps},
         # per-step spread of the timed pass (CUDA events around each step, rank 0)
-        "step_ms_dist": step_dist(res["step_ms"]),
+        "step_ms_dist": dict(step_dist(res["step_ms"]),
+                             note="separate pass, CUDA events around every step (no PDL overlap across steps)"),
         # secondary: Enc(W) L2-resident (same copy every step); null when it does not fit
         "warm_l2": (None if res["warm_ms"] is None else
                     {"ms_per_step": res["warm_ms"], "value": weak_value(macs_step, 1, res["warm_ms"]),
                      "unit": UNIT}),
+        "graph": (None if res["graph_ms"] is None else
+                  {"ms_per_step": res["graph_ms"], "value": weak_value(macs_step, world, res["graph_ms"]),
+                   "unit": UNIT, "note": "secondary: the same steps replayed from a CUDA graph capturing n_copies "
+                           "consecutive steps (one per input copy)"}),
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
         "setup_encrypt_s": res["t_setup"],

@@ -174,7 +174,10 @@ nimbus_status nimbus_cop_workspace_size(const nimbus_ctx* ctx, const nimbus_encw
  *  d_cts   n_queries x n_cts x 2 x L_out x N uint32  [query][theta][comp][limb][J]
  *  d_R     k x n uint32: the client's output share Y_c = R
  *  d_ws    workspace of at least nimbus_cop_workspace_size bytes (16-byte aligned)
- * No allocation, no host synchronisation. */
+ * No allocation, no host synchronisation: the call (like nimbus_cop_matmul_batch)
+ * may be captured into a CUDA graph and replayed; a replay reads the captured
+ * buffers as they are at replay time (tests/test_gpu_graph.py).  Do one call
+ * per context and kernel variant before capturing (it sets kernel attributes). */
 nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* encw, const uint32_t* d_X,
                                 uint32_t k_per_query, uint32_t n_queries, uint64_t mask_seed,
                                 uint32_t* d_cts, uint32_t* d_R, void* d_ws, size_t ws_bytes,
