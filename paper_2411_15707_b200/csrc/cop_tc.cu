@@ -327,6 +327,19 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             const uint64_t pol_b = policy_evict_first();
             const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
             uint32_t it = 0, ti = 0;
+#ifdef NIMBUS_E3
+            // every ring slot of the first tile gets its Enc(W) copy before the PDL wait: in a
+            // chain of calls this runs while the previous call's pack and this call's slice finish
+            const uint32_t pre = min(KP, Cfg::STAGES);
+            for (uint32_t kp = 0; kp < pre; kp++) {
+                const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
+                mbar_arrive_expect_tx(&full[kp], nkb * Cfg::B_BYTES + nkb * 2 * Cfg::SLICE);
+                bulk_g2s(smem + Cfg::OFF_B + kp * Cfg::SLOT, Et + (size_t)blockIdx.x * KB * Cfg::B_BYTES +
+                         (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[kp], pol_b);
+            }
+#else
+            const uint32_t pre = 0;
+#endif
             for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
                 const uint8_t* b_src = Et + (size_t)ct * KB * Cfg::B_BYTES;
                 for (uint32_t kp = 0; kp < KP; kp++, it++) {
@@ -335,9 +348,11 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                     if (it >= Cfg::STAGES) mbar_wait(&empty[s], ph ^ 1);
                     if (ti == 1 && kp < 8) TRACE(52 + kp);
                     const bool first = ti == 0;
-                    mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES + (first ? nkb * 2 * Cfg::SLICE : 0));
-                    bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES,
-                             &full[s], pol_b);
+                    if (it >= pre) {
+                        mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES + (first ? nkb * 2 * Cfg::SLICE : 0));
+                        bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES,
+                                 nkb * Cfg::B_BYTES, &full[s], pol_b);
+                    }
                     if (first) {
                         if (kp == 0) {
 #ifdef NIMBUS_PF
@@ -347,6 +362,11 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                             if (KB > Cfg::KPS) prefetch_l2_bulk(b_src + Cfg::SLOT, tb - Cfg::SLOT);
                             for (uint32_t c2 = ct + gridDim.x; c2 < CT; c2 += gridDim.x)
                                 prefetch_l2_bulk(Et + (size_t)c2 * tb, tb);
+#endif
+#ifdef NIMBUS_PF1
+                            // lighter: only the next tile of this CTA
+                            if (ct + gridDim.x < CT)
+                                prefetch_l2_bulk(Et + (size_t)(ct + gridDim.x) * KB * Cfg::B_BYTES, KB * Cfg::B_BYTES);
 #endif
                             pdl_wait(); TRACE(2);
                         }
