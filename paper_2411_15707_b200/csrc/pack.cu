@@ -12,9 +12,11 @@
 //            rho = centered c_l  (= round(c / p_l));
 //   step 4:  b_i -= Emb_{q'}(r_theta[J]),  r_theta[J] = word(seed, 6, tg*N + J) >> (64-ell)
 //            (SURVEY.md §8(c) #13); R[alpha][j] = r_theta[(alpha mod R) n + j].
-// V = 4 (uint4 loads/stores) when n % 4 == 0 and the grid stays large; a group
-// of 4 J never straddles a wrap point because J and r n are multiples of 4.
+// V = 2 or 4 coefficients per thread (uint2 / uint4 loads and stores) when V
+// divides n and the grid stays large; a group of V J never straddles a wrap
+// point because J and r n are multiples of V.
 #include <algorithm>
+#include <cstdlib>
 #include "pack_dev.cuh"
 
 namespace nimbus {
@@ -143,14 +145,22 @@ cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_
         return e;
     }
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
-    // 4 coefficients per thread when the RShift stride allows it and the grid stays
-    // at >= 8 blocks of 128 per SM: in the PDL chain the pack runs alone after the
-    // contraction and is latency-bound, so thread count beats per-thread efficiency
-    // (C2: V = 1 26.1 us/step vs V = 4 28.2; C3: V = 4)
+    // V coefficients per thread (vector loads/stores; J and r n stay multiples of V): the
+    // widest V whose grid still has >= 16 blocks of 128 per SM.  In the PDL chain the pack
+    // runs alone after the contraction and is latency-bound, so thread count beats per-thread
+    // efficiency until the grid is well over one wave (block timing, B200: C2 V=1 22.3 us/step
+    // vs V=2 23.9 / V=4 23.0; C3 V=2 23.5 vs V=4 24.2 / V=1 25.9)
     const uint64_t threads_v1 = 2ull * nq * nct * N;      // one thread per (comp, J)
-    const bool vec = (n % 4 == 0) && threads_v1 / 4 >= 8ull * 128 * (uint64_t)c->num_sms;
-    cudaError_t e = vec ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0)
-                        : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+    const uint64_t min_threads = 16ull * 128 * (uint64_t)c->num_sms;
+    uint32_t V = (n % 4 == 0 && threads_v1 / 4 >= min_threads) ? 4
+               : (n % 2 == 0 && threads_v1 / 2 >= min_threads) ? 2 : 1;
+    if (const char* ev = getenv("NIMBUS_PACK_V")) {        // experiment switch: 1, 2 or 4
+        const uint32_t v = (uint32_t)atoi(ev);
+        if ((v == 1 || v == 2 || v == 4) && n % v == 0) V = v;
+    }
+    cudaError_t e = V == 4 ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0)
+                  : V == 2 ? launch_v<2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0)
+                           : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
     c->launches++;
     return e;
 }

@@ -25,6 +25,16 @@ struct VecU32<1> {
     __device__ static void store(uint32_t* p, const uint32_t (&v)[1]) { p[0] = v[0]; }
 };
 template <>
+struct VecU32<2> {
+    __device__ static void load(const uint32_t* p, uint32_t (&v)[2]) {
+        const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+        v[0] = x.x; v[1] = x.y;
+    }
+    __device__ static void store(uint32_t* p, const uint32_t (&v)[2]) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[1]);
+    }
+};
+template <>
 struct VecU32<4> {
     __device__ static void load(const uint32_t* p, uint32_t (&v)[4]) {
         const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));

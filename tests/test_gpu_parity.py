@@ -445,7 +445,8 @@ def test_batch_matches_sequential_and_oracle(nb, oracle):
 @pytest.mark.parametrize("env", [{"NIMBUS_TRANSPOSED": "1"}, {"NIMBUS_TRANSPOSED": "1", "NIMBUS_T_RT": "32"},
                                  {"NIMBUS_NO_RESIDENT": "1"}, {"NIMBUS_CLUSTER": "2"},
                                  {"NIMBUS_NO_RESIDENT": "1", "NIMBUS_CLUSTER": "2"}, {"NIMBUS_RES": "1"},
-                                 {"NIMBUS_RES": "2"}])
+                                 {"NIMBUS_RES": "2"}, {"NIMBUS_PACK_V": "1"}, {"NIMBUS_PACK_V": "2"},
+                                 {"NIMBUS_PACK_V": "4"}])
 @pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [(4096, 2, 16, 1, 768, 768, 128, 1),
                                                      (8192, 3, 32, 2, 300, 1000, 70, 3)])
 def test_kernel_variants_parity(nb, oracle, monkeypatch, env, N, L, ell, L_out, m, n, kq, nq):
