@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI of libnimbus_cop.so (include/nimbus_cop.h): parameter
 // validation, RNS constant / twiddle derivation, handle management, and the
 // launch sequence of each entry point.  All arithmetic runs in the kernels.
+#include <nvtx3/nvToolsExt.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -110,14 +111,21 @@ static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff, uint64_t e
 
 // Every entry point that touches the GPU runs on its context's device and restores the
 // caller's current device on return (a process may drive several devices).
+// Every public call: run on the context's device (restoring the caller's), inside an
+// NVTX range named after the call (visible to ncu --nvtx / Nsight Systems; a no-op
+// without a tool attached).
 struct DevGuard {
     int prev = -1;
-    explicit DevGuard(int dev) {
+    DevGuard(int dev, const char* name) {
+        nvtxRangePushA(name);
         if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
         else prev = -1;
     }
-    explicit DevGuard(const nimbus_ctx* c) : DevGuard(c ? c->device : -1) {}
-    ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+    DevGuard(const nimbus_ctx* c, const char* name) : DevGuard(c ? c->device : -1, name) {}
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+        nvtxRangePop();
+    }
 };
 
 extern "C" {
@@ -203,7 +211,7 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
             b[3 * N + kk] = (uint32_t)(((uint64_t)iw << 32) / p);
         }
     }
-    DevGuard dg_(device);
+    DevGuard dg_(device, __func__);
     cudaError_t e = cudaMalloc(&ctx->d_tw, tw.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_flag, 16);
@@ -214,7 +222,7 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
 }
 
 void nimbus_ctx_destroy(nimbus_ctx* ctx) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx) return;
     if (ctx->d_tw) cudaFree(ctx->d_tw);
     if (ctx->d_scratch) cudaFree(ctx->d_scratch);
@@ -240,7 +248,7 @@ const char* nimbus_last_error(const nimbus_ctx* ctx) { return ctx ? ctx->err.c_s
 uint64_t nimbus_launch_count(const nimbus_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx) return NIMBUS_EINVAL;
     CK(cudaStreamSynchronize((cudaStream_t)stream), "sync");
     uint32_t flag = 0;
@@ -254,7 +262,7 @@ nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
 
 // ---------------------------------------------------------------- keys
 nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus_sk** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !out) return NIMBUS_EINVAL;
     *out = nullptr;
     nimbus_sk* sk = new (std::nothrow) nimbus_sk();
@@ -270,7 +278,7 @@ nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus
 }
 
 void nimbus_sk_destroy(nimbus_sk* sk) {
-    DevGuard dg_(sk ? sk->ctx : nullptr);
+    DevGuard dg_(sk ? sk->ctx : nullptr, __func__);
     if (!sk) return;
     if (sk->d_s) cudaFree(sk->d_s);
     if (sk->d_s_ntt) cudaFree(sk->d_s_ntt);
@@ -278,7 +286,7 @@ void nimbus_sk_destroy(nimbus_sk* sk) {
 }
 
 nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream) {
-    DevGuard dg_(sk ? sk->ctx : nullptr);
+    DevGuard dg_(sk ? sk->ctx : nullptr, __func__);
     if (!sk || !d_s) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = sk->ctx;
     CK(cudaMemcpyAsync(d_s, sk->d_s, ctx->rns.N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "sk export");
@@ -287,7 +295,7 @@ nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream) {
 
 // ---------------------------------------------------------------- public key (reading 25)
 nimbus_status nimbus_keygen_pk(nimbus_ctx* ctx, const nimbus_sk* sk, uint64_t seed, void* stream, nimbus_pk** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !sk || !out || sk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     *out = nullptr;
     nimbus_pk* pk = new (std::nothrow) nimbus_pk();
@@ -305,7 +313,7 @@ nimbus_status nimbus_keygen_pk(nimbus_ctx* ctx, const nimbus_sk* sk, uint64_t se
 }
 
 void nimbus_pk_destroy(nimbus_pk* pk) {
-    DevGuard dg_(pk ? pk->ctx : nullptr);
+    DevGuard dg_(pk ? pk->ctx : nullptr, __func__);
     if (!pk) return;
     if (pk->d_pk) cudaFree(pk->d_pk);
     if (pk->d_pk_ntt) cudaFree(pk->d_pk_ntt);
@@ -313,7 +321,7 @@ void nimbus_pk_destroy(nimbus_pk* pk) {
 }
 
 nimbus_status nimbus_pk_export(const nimbus_pk* pk, uint32_t* d_out, void* stream) {
-    DevGuard dg_(pk ? pk->ctx : nullptr);
+    DevGuard dg_(pk ? pk->ctx : nullptr, __func__);
     if (!pk || !d_out) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = pk->ctx;
     CK(cudaMemcpyAsync(d_out, pk->d_pk, 2ull * ctx->rns.L * ctx->rns.N * 4, cudaMemcpyDeviceToDevice,
@@ -322,7 +330,7 @@ nimbus_status nimbus_pk_export(const nimbus_pk* pk, uint32_t* d_out, void* strea
 }
 
 nimbus_status nimbus_pk_import(nimbus_ctx* ctx, const uint32_t* d_in, void* stream, nimbus_pk** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !d_in || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     *out = nullptr;
     nimbus_pk* pk = new (std::nothrow) nimbus_pk();
@@ -423,14 +431,14 @@ static nimbus_status reencrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, con
 
 nimbus_status nimbus_encrypt_weights_into(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint64_t seed,
                                           void* stream, nimbus_encw* encw) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : reencrypt_weights(ctx, sk, d_W, seed, stream, encw);
 }
 
 nimbus_status nimbus_encrypt_weights_into_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W,
                                               uint64_t seed, void* stream, nimbus_encw* encw) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : reencrypt_weights(ctx, sk, d_W, seed, stream, encw);
 }
@@ -438,20 +446,20 @@ nimbus_status nimbus_encrypt_weights_into_u64(nimbus_ctx* ctx, const nimbus_sk* 
 
 nimbus_status nimbus_encrypt_weights(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_W, uint32_t m,
                                      uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : encrypt_weights(ctx, sk, d_W, m, n, seed, stream, out);
 }
 
 nimbus_status nimbus_encrypt_weights_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint64_t* d_W, uint32_t m,
                                          uint32_t n, uint64_t seed, void* stream, nimbus_encw** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : encrypt_weights(ctx, sk, d_W, m, n, seed, stream, out);
 }
 
 void nimbus_encw_destroy(nimbus_encw* w) {
-    DevGuard dg_(w ? w->ctx : nullptr);
+    DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w) return;
     if (w->d_Et) cudaFree(w->d_Et);
     if (w->h_Et) cudaFreeHost(w->h_Et);
@@ -459,7 +467,7 @@ void nimbus_encw_destroy(nimbus_encw* w) {
 }
 
 nimbus_status nimbus_encw_offload(nimbus_encw* w, void* stream) {
-    DevGuard dg_(w ? w->ctx : nullptr);
+    DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
     if (!w->d_Et) return NIMBUS_OK;                       // already host-resident
@@ -473,7 +481,7 @@ nimbus_status nimbus_encw_offload(nimbus_encw* w, void* stream) {
 }
 
 nimbus_status nimbus_encw_reload(nimbus_encw* w, void* stream) {
-    DevGuard dg_(w ? w->ctx : nullptr);
+    DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
     if (w->d_Et) return NIMBUS_OK;
@@ -487,7 +495,7 @@ int nimbus_encw_is_resident(const nimbus_encw* w) { return w && w->d_Et ? 1 : 0;
 size_t nimbus_encw_bytes(const nimbus_encw* w) { return w ? w->bytes : 0; }
 
 nimbus_status nimbus_encw_export(const nimbus_encw* w, uint32_t* d_out, void* stream) {
-    DevGuard dg_(w ? w->ctx : nullptr);
+    DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w || !d_out) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
     if (!w->d_Et) return set_err(ctx, NIMBUS_EINVAL, "Enc(W) is host-resident (nimbus_encw_reload first)");
@@ -497,7 +505,7 @@ nimbus_status nimbus_encw_export(const nimbus_encw* w, uint32_t* d_out, void* st
 
 nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t m, uint32_t n, void* stream,
                                  nimbus_encw** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !d_in || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     *out = nullptr;
     nimbus_encw* w = nullptr;
@@ -518,7 +526,7 @@ static uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h = 0xcbf29ce48422232
 nimbus_status nimbus_encw_save(const nimbus_encw* w, const char* path) {
     if (!w || !path) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!w->d_Et) return set_err(ctx, NIMBUS_EINVAL, "Enc(W) is host-resident (nimbus_encw_reload first)");
     const size_t bytes = (size_t)w->m * ncols(ctx) * 4;
     uint32_t* d_canon = nullptr;
@@ -540,7 +548,7 @@ nimbus_status nimbus_encw_save(const nimbus_encw* w, const char* path) {
 }
 
 nimbus_status nimbus_encw_load(nimbus_ctx* ctx, const char* path, nimbus_encw** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !path || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     *out = nullptr;
     FILE* f = fopen(path, "rb");
@@ -659,7 +667,7 @@ static nimbus_status run_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
 
 nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t k,
                                     uint32_t* d_C, void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     if (st != NIMBUS_OK) return st;
     st = check_online(ctx, w, k, 1);
@@ -675,7 +683,7 @@ nimbus_status nimbus_cop_accumulate(nimbus_ctx* ctx, const nimbus_encw* w, const
 
 nimbus_status nimbus_cop_pack(nimbus_ctx* ctx, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                               uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;
     if (!ctx || !d_C || !d_cts || !d_R || kq == 0 || nq == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
@@ -709,7 +717,7 @@ static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const voi
 nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t kq,
                                 uint32_t nq, uint64_t seed, uint32_t* d_cts, uint32_t* d_R, void* d_ws,
                                 size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream);
 }
@@ -717,7 +725,7 @@ nimbus_status nimbus_cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const uin
 nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* d_X, uint32_t kq,
                                     uint32_t nq, uint64_t seed, uint32_t* d_cts, uint64_t* d_R, void* d_ws,
                                     size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : cop_matmul(ctx, w, d_X, kq, nq, seed, d_cts, d_R, d_ws, ws_bytes, stream);
 }
@@ -739,7 +747,7 @@ nimbus_status nimbus_rerand_flood_max(const nimbus_ctx* ctx, const nimbus_encw* 
 nimbus_status nimbus_rerand_prepare(nimbus_ctx* ctx, const nimbus_pk* pk, const nimbus_encw* w, uint32_t kq,
                                     uint32_t nq, uint64_t seed, uint32_t flood_bits, uint32_t* d_zero,
                                     void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !pk || !w || !d_zero || pk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     nimbus_status st = check_shape(ctx, w, kq, nq);
     if (st != NIMBUS_OK) return st;
@@ -755,7 +763,7 @@ nimbus_status nimbus_rerand_prepare(nimbus_ctx* ctx, const nimbus_pk* pk, const 
 nimbus_status nimbus_cop_matmul_rr(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* d_X, uint32_t kq,
                                    uint32_t nq, uint64_t seed, const uint32_t* d_zero, uint32_t* d_cts,
                                    uint32_t* d_R, void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!d_zero) return set_err(ctx, NIMBUS_EINVAL, "null zero encryptions");
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st
@@ -765,7 +773,7 @@ nimbus_status nimbus_cop_matmul_rr(nimbus_ctx* ctx, const nimbus_encw* w, const 
 nimbus_status nimbus_cop_matmul_rr_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* d_X, uint32_t kq,
                                        uint32_t nq, uint64_t seed, const uint32_t* d_zero, uint32_t* d_cts,
                                        uint64_t* d_R, void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!d_zero) return set_err(ctx, NIMBUS_EINVAL, "null zero encryptions");
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st
@@ -859,7 +867,7 @@ static std::vector<nimbus_cop_job> jobs_of(const nimbus_cop_job_u64* jobs, uint3
 
 nimbus_status nimbus_cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                       size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : cop_matmul_batch(ctx, jobs, count, d_ws, ws_bytes, stream);
 }
@@ -873,7 +881,7 @@ nimbus_status nimbus_cop_workspace_size_batch_u64(const nimbus_ctx* ctx, const n
 
 nimbus_status nimbus_cop_matmul_batch_u64(nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
                                           void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     if (st != NIMBUS_OK) return st;
     if (!jobs || count == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
@@ -973,7 +981,7 @@ static nimbus_status cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* 
 
 nimbus_status nimbus_cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
                                          size_t ws_bytes, void* d_stage, size_t stage_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : cop_matmul_streamed(ctx, jobs, count, d_ws, ws_bytes, d_stage, stage_bytes, stream);
 }
@@ -988,7 +996,7 @@ nimbus_status nimbus_cop_stage_size_u64(const nimbus_ctx* ctx, const nimbus_cop_
 nimbus_status nimbus_cop_matmul_streamed_u64(nimbus_ctx* ctx, const nimbus_cop_job_u64* jobs, uint32_t count,
                                              void* d_ws, size_t ws_bytes, void* d_stage, size_t stage_bytes,
                                              void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     if (st != NIMBUS_OK) return st;
     if (!jobs || count == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
@@ -1003,7 +1011,7 @@ nimbus_status nimbus_profile_enable(nimbus_ctx* ctx, int on) {
 }
 
 nimbus_status nimbus_profile_read(nimbus_ctx* ctx, double* ms, uint64_t* calls, int reset) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx) return NIMBUS_EINVAL;
     auto& P = ctx->ev_pending;
     // groups of 5: before slice, after slice, after contraction, before pack, after pack
@@ -1068,7 +1076,7 @@ static nimbus_status cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, cons
 nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, const uint32_t* h_X, uint32_t kq,
                                      uint32_t nq, uint64_t seed, uint32_t* h_cts, uint32_t* h_R, void* d_ws,
                                      size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
 }
@@ -1076,7 +1084,7 @@ nimbus_status nimbus_cop_matmul_host(nimbus_ctx* ctx, const nimbus_encw* w, cons
 nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* w, const uint64_t* h_X, uint32_t kq,
                                          uint32_t nq, uint64_t seed, uint32_t* h_cts, uint64_t* h_R, void* d_ws,
                                          size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : cop_matmul_host(ctx, w, h_X, kq, nq, seed, h_cts, h_R, d_ws, ws_bytes, stream);
 }
@@ -1207,7 +1215,7 @@ static nimbus_status cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_hos
 
 nimbus_status nimbus_cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_host_job* jobs, uint32_t count,
                                            void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : cop_matmul_host_batch(ctx, jobs, count, d_ws, ws_bytes, stream);
 }
@@ -1220,7 +1228,7 @@ nimbus_status nimbus_cop_workspace_size_host_batch_u64(const nimbus_ctx* ctx, co
 
 nimbus_status nimbus_cop_matmul_host_batch_u64(nimbus_ctx* ctx, const nimbus_cop_host_job_u64* jobs, uint32_t count,
                                                void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st
                            : cop_matmul_host_batch(ctx, reinterpret_cast<const nimbus_cop_host_job*>(jobs), count,
@@ -1243,14 +1251,14 @@ static nimbus_status decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_
 
 nimbus_status nimbus_decrypt(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq, uint32_t n,
                              uint32_t nq, uint32_t* d_Z, uint32_t* d_M, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 4);
     return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, n, nq, d_Z, d_M, stream);
 }
 
 nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uint32_t* d_cts, uint32_t kq,
                                  uint32_t n, uint32_t nq, uint64_t* d_Z, uint64_t* d_M, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     nimbus_status st = want_width(ctx, 8);
     return st != NIMBUS_OK ? st : decrypt(ctx, sk, d_cts, kq, n, nq, d_Z, d_M, stream);
 }
@@ -1258,7 +1266,7 @@ nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uin
 // ---------------------------------------------------------------- server, step 5
 nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_t m, uint32_t n, void* stream,
                                    nimbus_plainw** out) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;          // server GEMM: ell <= 32
     if (!ctx || !d_W || !out || m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     nimbus_plainw* w = new (std::nothrow) nimbus_plainw();
@@ -1277,7 +1285,7 @@ nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_
 }
 
 void nimbus_plainw_destroy(nimbus_plainw* w) {
-    DevGuard dg_(w ? w->ctx : nullptr);
+    DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w) return;
     if (w->d_Wt) cudaFree(w->d_Wt);
     delete w;
@@ -1313,7 +1321,7 @@ nimbus_status nimbus_server_workspace_size(const nimbus_ctx* ctx, const nimbus_p
 
 nimbus_status nimbus_plain_matmul(nimbus_ctx* ctx, const nimbus_plainw* w, const uint32_t* d_X, uint32_t k,
                                   const uint32_t* d_add, uint32_t* d_Y, void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !w || w->ctx != ctx || !d_X || !d_Y || !d_ws || k == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (k > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
     const ServerWs L = server_ws(ctx, w, k, 0);
@@ -1328,7 +1336,7 @@ nimbus_status nimbus_plain_matmul(nimbus_ctx* ctx, const nimbus_plainw* w, const
 nimbus_status nimbus_server_output(nimbus_ctx* ctx, const nimbus_sk* sk, const nimbus_plainw* w,
                                    const uint32_t* d_Xs, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
                                    uint32_t* d_Ys, void* d_ws, size_t ws_bytes, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !sk || !w || w->ctx != ctx || !d_Xs || !d_cts || !d_Ys || !d_ws || kq == 0 || nq == 0)
         return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     if (w->n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
@@ -1355,7 +1363,7 @@ nimbus_status nimbus_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint
 
 nimbus_status nimbus_negacyclic_mul(nimbus_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t count,
                                     uint32_t* c, void* stream) {
-    DevGuard dg_(ctx);
+    DevGuard dg_(ctx, __func__);
     if (!ctx || !a || !b || !c || count == 0) return NIMBUS_EINVAL;
     CK(launch_negacyclic_mul(ctx, a, b, count, c, (cudaStream_t)stream), "negacyclic_mul");
     return NIMBUS_OK;
