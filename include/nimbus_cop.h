@@ -261,12 +261,24 @@ nimbus_status nimbus_cop_matmul_batch_u64(nimbus_ctx* ctx, const nimbus_cop_job_
  *                       then returns EINVAL for it;
  *  nimbus_encw_reload   copies it back into a fresh device allocation (async on `stream`);
  *  nimbus_cop_stage_size  bytes of the device staging buffer for a job list
- *                       (2 x the largest host-resident Enc(W); 0 if none);
+ *                       (2 x the largest non-resident tiled Enc(W), plus the largest
+ *                       file-backed canonical payload; 0 if all are resident);
  *  nimbus_cop_matmul_streamed  runs the jobs in order on `stream` exactly as
  *                       nimbus_cop_matmul would (same outputs, bit for bit); the
  *                       host-resident ones are copied into alternating halves of
  *                       d_stage on the context's copy stream, job j+2's copy
  *                       overlapping job j+1's compute.  d_ws as for the largest job. */
+/*  nimbus_encw_open     a FILE-backed handle on a store file written by nimbus_encw_save
+ *                       (header, parameters and file size checked; verify != 0 also checks the
+ *                       payload checksum in one streaming pass; NIMBUS_EIO otherwise).  Nothing is
+ *                       read into memory: nimbus_cop_matmul_streamed reads the payload for each job
+ *                       on its copy stream (a stream-ordered host callback into one of two pinned
+ *                       buffers), uploads and tiles it while earlier jobs compute -- the paper's
+ *                       Enc(W) kept on the client's disk and loaded for the next layer
+ *                       (PAPER.md:300, 312-317).  A read failure during streaming is reported as
+ *                       NIMBUS_EIO by nimbus_sync or the next streamed call.  nimbus_cop_matmul
+ *                       refuses the handle; nimbus_encw_reload reads it into HBM. */
+nimbus_status nimbus_encw_open(nimbus_ctx* ctx, const char* path, int verify, nimbus_encw** out);
 nimbus_status nimbus_encw_offload(nimbus_encw* encw, void* stream);
 nimbus_status nimbus_encw_reload(nimbus_encw* encw, void* stream);
 int nimbus_encw_is_resident(const nimbus_encw* encw);

@@ -2,10 +2,15 @@
 // validation, RNS constant / twiddle derivation, handle management, and the
 // launch sequence of each entry point.  All arithmetic runs in the kernels.
 #include <nvtx3/nvToolsExt.h>
+#include <fcntl.h>
+#include <unistd.h>
+#include <cerrno>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -233,6 +238,7 @@ void nimbus_ctx_destroy(nimbus_ctx* ctx) {
     if (ctx->side) cudaStreamDestroy(ctx->side);
     for (cudaEvent_t e : ctx->stream_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->host_ev) cudaEventDestroy(e);
+    for (uint8_t* h : ctx->h_read) if (h) cudaFreeHost(h);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     delete ctx;
 }
@@ -251,6 +257,7 @@ nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
     DevGuard dg_(ctx, __func__);
     if (!ctx) return NIMBUS_EINVAL;
     CK(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+    if (ctx->io_error.exchange(0)) return set_err(ctx, NIMBUS_EIO, "reading a file-backed Enc(W) failed");
     uint32_t flag = 0;
     CK(cudaMemcpy(&flag, ctx->d_flag, 4, cudaMemcpyDeviceToHost), "sync flag");
     if (flag) {
@@ -348,7 +355,7 @@ nimbus_status nimbus_pk_import(nimbus_ctx* ctx, const uint32_t* d_in, void* stre
 }
 
 // ---------------------------------------------------------------- Enc(W)
-static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_encw** out) {
+static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_encw** out, bool alloc = true) {
     if (m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "m and n must be positive");
     if (n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N (PAPER.md:232 needs n < N)");
     if (m > 8192) return set_err(ctx, NIMBUS_ESHAPE, "m > 8192 exceeds the int32 slice-accumulator bound");
@@ -371,8 +378,10 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
         else if (sx_of(ctx->rns.ell) == 8) w->bn = kBNW;      // 8 X slices: transposed kernel only
     }
     w->bytes = (size_t)w->KB * kBK * col_tiles(ctx, w->bn) * w->bn * 4;
-    cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
-    if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "encw alloc"); }
+    if (alloc) {
+        cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
+        if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "encw alloc"); }
+    }
     *out = w;
     return NIMBUS_OK;
 }
@@ -466,6 +475,9 @@ void nimbus_encw_destroy(nimbus_encw* w) {
     delete w;
 }
 
+static bool read_at(const char* path, uint64_t off, uint8_t* dst, uint64_t bytes);
+static nimbus_status payload_to_device(nimbus_ctx* ctx, nimbus_encw* w, const uint8_t* host, uint64_t nbytes);
+
 nimbus_status nimbus_encw_offload(nimbus_encw* w, void* stream) {
     DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w) return NIMBUS_EINVAL;
@@ -485,6 +497,12 @@ nimbus_status nimbus_encw_reload(nimbus_encw* w, void* stream) {
     if (!w) return NIMBUS_EINVAL;
     nimbus_ctx* ctx = w->ctx;
     if (w->d_Et) return NIMBUS_OK;
+    if (!w->h_Et && !w->file.empty()) {                   // file-backed: read, upload, tile
+        std::vector<uint8_t> host(w->canon_bytes);
+        if (!read_at(w->file.c_str(), w->file_off, host.data(), w->canon_bytes))
+            return set_err(ctx, NIMBUS_EIO, "cannot read the store file");
+        return payload_to_device(ctx, w, host.data(), w->canon_bytes);
+    }
     CK(cudaMalloc(&w->d_Et, w->bytes), "reload alloc");
     CK(cudaMemcpyAsync(w->d_Et, w->h_Et, w->bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream), "reload copy");
     return NIMBUS_OK;
@@ -547,20 +565,82 @@ nimbus_status nimbus_encw_save(const nimbus_encw* w, const char* path) {
     return ok ? NIMBUS_OK : set_err(ctx, NIMBUS_EIO, "store file write failed");
 }
 
+// Store-file header (written by nimbus_encw_save): checks magic, version and that the file
+// was made for this context's N, L, ell and primes; returns m, n, payload offset and bytes.
+static bool read_store_header(const nimbus_ctx* ctx, FILE* f, uint32_t* m, uint32_t* n, uint64_t* off,
+                              uint64_t* nbytes) {
+    char magic[8];
+    uint32_t hdr[6], pr[NIMBUS_MAXL];
+    const bool ok = fread(magic, 1, 8, f) == 8 && memcmp(magic, "NIMBUSEW", 8) == 0 && fread(hdr, 4, 6, f) == 6 &&
+                    hdr[0] == 1u && hdr[1] == ctx->rns.N && hdr[2] == ctx->rns.L && hdr[3] == ctx->rns.ell &&
+                    fread(pr, 4, ctx->rns.L, f) == ctx->rns.L && memcmp(pr, ctx->rns.p, 4 * ctx->rns.L) == 0 &&
+                    fread(nbytes, 8, 1, f) == 1 && hdr[4] > 0 && hdr[5] > 0 &&
+                    *nbytes == (uint64_t)hdr[4] * ncols(ctx) * 4;
+    *m = hdr[4];
+    *n = hdr[5];
+    *off = 8 + 24 + 4ull * ctx->rns.L + 8;
+    return ok;
+}
+
+// read exactly `bytes` at `off` of `path` into `dst` (large reads, EINTR-safe); payloads over
+// 64 MB are split over up to 8 threads (one pread stream per thread: from the page cache a
+// single thread copies at ~6 GB/s)
+static bool read_range(int fd, uint64_t off, uint8_t* dst, uint64_t bytes) {
+    uint64_t done = 0;
+    while (done < bytes) {
+        const size_t chunk = (size_t)std::min<uint64_t>(bytes - done, 1ull << 30);
+        const ssize_t r = pread(fd, dst + done, chunk, (off_t)(off + done));
+        if (r < 0 && errno == EINTR) continue;
+        if (r <= 0) return false;
+        done += (uint64_t)r;
+    }
+    return true;
+}
+
+static bool read_at(const char* path, uint64_t off, uint8_t* dst, uint64_t bytes) {
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return false;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = bytes > (64ull << 20) ? std::min(8u, hw) : 1u;
+    bool ok = true;
+    if (nt == 1) {
+        ok = read_range(fd, off, dst, bytes);
+    } else {
+        const uint64_t per = ((bytes + nt - 1) / nt + 4095) & ~uint64_t(4095);
+        std::vector<std::thread> th;
+        std::vector<char> res(nt, 1);
+        for (unsigned t = 0; t < nt; t++) {
+            const uint64_t b0 = std::min<uint64_t>(bytes, t * per), b1 = std::min<uint64_t>(bytes, b0 + per);
+            if (b1 > b0) th.emplace_back([&, t, b0, b1] { res[t] = read_range(fd, off + b0, dst + b0, b1 - b0); });
+        }
+        for (auto& x : th) x.join();
+        for (char r : res) ok = ok && r;
+    }
+    close(fd);
+    return ok;
+}
+
+// canonical payload (host) -> a fresh tiled device copy in w->d_Et
+static nimbus_status payload_to_device(nimbus_ctx* ctx, nimbus_encw* w, const uint8_t* host, uint64_t nbytes) {
+    uint32_t* d_canon = nullptr;
+    CK(cudaMalloc(&d_canon, nbytes), "load alloc");
+    cudaError_t e = w->d_Et ? cudaSuccess : cudaMalloc(&w->d_Et, w->bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(d_canon, host, nbytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_tile_encw(ctx, d_canon, w->m, w->KB, w->bn, w->d_Et, nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(d_canon);
+    return e == cudaSuccess ? NIMBUS_OK : cuda_err(ctx, e, "load import");
+}
+
 nimbus_status nimbus_encw_load(nimbus_ctx* ctx, const char* path, nimbus_encw** out) {
     DevGuard dg_(ctx, __func__);
     if (!ctx || !path || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     *out = nullptr;
     FILE* f = fopen(path, "rb");
     if (!f) return set_err(ctx, NIMBUS_EIO, "cannot open store file");
-    char magic[8];
-    uint32_t hdr[6], pr[NIMBUS_MAXL];
-    uint64_t nbytes = 0, sum = 0;
-    bool ok = fread(magic, 1, 8, f) == 8 && memcmp(magic, "NIMBUSEW", 8) == 0 && fread(hdr, 4, 6, f) == 6 &&
-              hdr[0] == 1u && hdr[1] == ctx->rns.N && hdr[2] == ctx->rns.L && hdr[3] == ctx->rns.ell &&
-              fread(pr, 4, ctx->rns.L, f) == ctx->rns.L && memcmp(pr, ctx->rns.p, 4 * ctx->rns.L) == 0 &&
-              fread(&nbytes, 8, 1, f) == 1 && hdr[4] > 0 && hdr[5] > 0 &&
-              nbytes == (uint64_t)hdr[4] * ncols(ctx) * 4;
+    uint32_t m = 0, n = 0;
+    uint64_t off = 0, nbytes = 0, sum = 0;
+    bool ok = read_store_header(ctx, f, &m, &n, &off, &nbytes);
     std::vector<uint8_t> host;
     if (ok) {
         host.resize(nbytes);
@@ -569,18 +649,48 @@ nimbus_status nimbus_encw_load(nimbus_ctx* ctx, const char* path, nimbus_encw** 
     }
     fclose(f);
     if (!ok) return set_err(ctx, NIMBUS_EIO, "store file corrupt or made for other parameters");
-    uint32_t* d_canon = nullptr;
-    CK(cudaMalloc(&d_canon, nbytes), "load alloc");
-    cudaError_t e = cudaMemcpy(d_canon, host.data(), nbytes, cudaMemcpyHostToDevice);
-    nimbus_status st = NIMBUS_OK;
-    if (e == cudaSuccess) st = nimbus_encw_import(ctx, d_canon, hdr[4], hdr[5], nullptr, out);
-    if (e == cudaSuccess && st == NIMBUS_OK) e = cudaDeviceSynchronize();
-    cudaFree(d_canon);
-    if (e != cudaSuccess) {
-        if (*out) { nimbus_encw_destroy(*out); *out = nullptr; }
-        return cuda_err(ctx, e, "load import");
+    nimbus_encw* w = nullptr;
+    nimbus_status st = new_encw(ctx, m, n, &w);
+    if (st != NIMBUS_OK) return st;
+    st = payload_to_device(ctx, w, host.data(), nbytes);
+    if (st != NIMBUS_OK) { nimbus_encw_destroy(w); return st; }
+    *out = w;
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_encw_open(nimbus_ctx* ctx, const char* path, int verify, nimbus_encw** out) {
+    DevGuard dg_(ctx, __func__);
+    if (!ctx || !path || !out) return set_err(ctx, NIMBUS_EINVAL, "null argument");
+    *out = nullptr;
+    FILE* f = fopen(path, "rb");
+    if (!f) return set_err(ctx, NIMBUS_EIO, "cannot open store file");
+    uint32_t m = 0, n = 0;
+    uint64_t off = 0, nbytes = 0, sum = 0;
+    bool ok = read_store_header(ctx, f, &m, &n, &off, &nbytes);
+    // whole file present: payload + trailing checksum
+    ok = ok && fseeko(f, 0, SEEK_END) == 0 && (uint64_t)ftello(f) == off + nbytes + 8;
+    if (ok && verify) {                  // one streaming pass over the payload
+        ok = fseeko(f, (off_t)off, SEEK_SET) == 0;
+        std::vector<uint8_t> buf(64u << 20);
+        uint64_t h = 0xcbf29ce484222325ULL, left = nbytes;
+        while (ok && left) {
+            const size_t c = (size_t)std::min<uint64_t>(left, buf.size());
+            ok = fread(buf.data(), 1, c, f) == c;
+            h = fnv1a(buf.data(), c, h);
+            left -= c;
+        }
+        ok = ok && fread(&sum, 8, 1, f) == 1 && sum == h;
     }
-    return st;
+    fclose(f);
+    if (!ok) return set_err(ctx, NIMBUS_EIO, "store file corrupt, truncated or made for other parameters");
+    nimbus_encw* w = nullptr;
+    nimbus_status st = new_encw(ctx, m, n, &w, /*alloc=*/false);
+    if (st != NIMBUS_OK) return st;
+    w->file = path;
+    w->file_off = off;
+    w->canon_bytes = nbytes;
+    *out = w;
+    return NIMBUS_OK;
 }
 
 // ---------------------------------------------------------------- online path
@@ -893,13 +1003,28 @@ nimbus_status nimbus_cop_matmul_batch_u64(nimbus_ctx* ctx, const nimbus_cop_job_
 nimbus_status nimbus_cop_stage_size(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
                                     size_t* bytes) {
     if (!ctx || !jobs || !bytes || count == 0) return NIMBUS_EINVAL;
-    size_t mx = 0;
+    size_t mx = 0, mc = 0;
     for (uint32_t i = 0; i < count; i++) {
         if (!jobs[i].encw) return NIMBUS_EINVAL;
-        if (!jobs[i].encw->d_Et) mx = mx > jobs[i].encw->bytes ? mx : jobs[i].encw->bytes;
+        const nimbus_encw* w = jobs[i].encw;
+        if (!w->d_Et) mx = mx > w->bytes ? mx : w->bytes;
+        if (!w->d_Et && !w->h_Et) mc = mc > w->canon_bytes ? mc : w->canon_bytes;   // file-backed
     }
-    *bytes = 2 * al1k(mx);
+    *bytes = 2 * al1k(mx) + al1k(mc);     // two tiled slots + one canonical buffer for file reads
     return NIMBUS_OK;
+}
+
+// stream-ordered read of a file-backed Enc(W) payload into a pinned buffer (cudaLaunchHostFunc)
+struct FileRead {
+    nimbus_ctx* ctx;
+    std::string path;
+    uint64_t off, bytes;
+    uint8_t* dst;
+};
+static void CUDART_CB file_read_cb(void* p) {
+    FileRead* r = static_cast<FileRead*>(p);
+    if (!read_at(r->path.c_str(), r->off, r->dst, r->bytes)) r->ctx->io_error.store(1);
+    delete r;
 }
 
 static nimbus_status cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, void* d_ws,
@@ -914,10 +1039,26 @@ static nimbus_status cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* 
         need = need > w ? need : w;
     }
     if (ws_bytes < need) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    if (ctx->io_error.exchange(0)) return set_err(ctx, NIMBUS_EIO, "an earlier file-backed Enc(W) read failed");
     size_t stage_need = 0;
     nimbus_cop_stage_size(ctx, jobs, count, &stage_need);
     if (stage_need && (!d_stage || stage_bytes < stage_need)) return set_err(ctx, NIMBUS_ESHAPE, "stage too small");
-    const size_t slot = stage_need / 2;
+    size_t mx = 0, mc = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        const nimbus_encw* w = jobs[i].encw;
+        if (!w->d_Et) mx = std::max(mx, w->bytes);
+        if (!w->d_Et && !w->h_Et) mc = std::max<size_t>(mc, w->canon_bytes);
+    }
+    const size_t slot = al1k(mx);
+    uint32_t* d_canon = reinterpret_cast<uint32_t*>((uint8_t*)d_stage + 2 * slot);
+    if (mc > ctx->h_read_bytes) {         // pinned read buffers (grow-only; none may be in flight)
+        if (ctx->copy) CK(cudaStreamSynchronize(ctx->copy), "read buffers idle");
+        for (uint8_t*& h : ctx->h_read) { if (h) cudaFreeHost(h); h = nullptr; }
+        ctx->h_read_bytes = 0;
+        for (uint8_t*& h : ctx->h_read) CK(cudaMallocHost(&h, mc), "pinned read buffer");
+        ctx->h_read_bytes = mc;
+    }
+    uint32_t n_file = 0;
     cudaStream_t a = (cudaStream_t)stream;
     if (!ctx->copy) CK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking), "copy stream");
     cudaStream_t b = ctx->copy;
@@ -944,9 +1085,22 @@ static nimbus_status cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* 
     }
     uint8_t* stage = (uint8_t*)d_stage;
     auto issue_copy = [&](uint32_t j) -> nimbus_status {
+        const nimbus_encw* w = jobs[j].encw;
         if (prev_user[j] >= 0) CK(cudaStreamWaitEvent(b, used[prev_user[j]], 0), "wait slot");
-        CK(cudaMemcpyAsync(stage + (size_t)slot_of[j] * slot, jobs[j].encw->h_Et, jobs[j].encw->bytes,
-                           cudaMemcpyHostToDevice, b), "stage copy");
+        if (w->h_Et) {
+            CK(cudaMemcpyAsync(stage + (size_t)slot_of[j] * slot, w->h_Et, w->bytes, cudaMemcpyHostToDevice, b),
+               "stage copy");
+        } else {
+            // file-backed: read the canonical payload on the copy stream's host
+            // callback into pinned buffer n_file % 2 (free again: its previous upload precedes this
+            // callback on the same stream), upload it, and tile it into the slot
+            uint8_t* hb = ctx->h_read[n_file++ & 1];
+            FileRead* rd = new (std::nothrow) FileRead{ctx, w->file, w->file_off, w->canon_bytes, hb};
+            if (!rd) return set_err(ctx, NIMBUS_ENOMEM, "host alloc");
+            CK(cudaLaunchHostFunc(b, file_read_cb, rd), "file read");
+            CK(cudaMemcpyAsync(d_canon, hb, w->canon_bytes, cudaMemcpyHostToDevice, b), "stage upload");
+            CK(launch_tile_encw(ctx, d_canon, w->m, w->KB, w->bn, stage + (size_t)slot_of[j] * slot, b), "stage tile");
+        }
         CK(cudaEventRecord(loaded[j], b), "record");
         return NIMBUS_OK;
     };

@@ -2,6 +2,7 @@
 // libnimbus_cop.so.  Not part of the public ABI (see include/nimbus_cop.h).
 #pragma once
 #include <cstdint>
+#include <atomic>
 #include <string>
 #include <vector>
 #include <cuda_runtime.h>
@@ -51,6 +52,11 @@ struct nimbus_ctx {
     std::vector<cudaEvent_t> stream_ev;
     // host-buffer job list (nimbus_cop_matmul_host_batch): per staging slot X-up / matmul / outputs-down events
     std::vector<cudaEvent_t> host_ev;
+    // file-backed Enc(W) streaming: two pinned read buffers (grow-only) and the first read error of a
+    // stream-ordered host callback (reported by nimbus_sync / the next streamed call)
+    uint8_t* h_read[2] = {nullptr, nullptr};
+    size_t h_read_bytes = 0;
+    std::atomic<int> io_error{0};
     // grow-only device scratch for the canonical rows of Enc(W) during (re-)encryption
     void* d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -78,6 +84,9 @@ struct nimbus_encw {
     uint8_t* d_Et = nullptr;       // tiled byte planes [ct][kb][s][bn][128 swizzled]; null when offloaded
     uint8_t* h_Et = nullptr;       // pinned host copy of the same bytes (nimbus_encw_offload)
     size_t bytes = 0;
+    // file-backed (nimbus_encw_open): canonical payload of a store file, read per streamed matmul
+    std::string file;
+    uint64_t file_off = 0, canon_bytes = 0;
 };
 
 struct nimbus_plainw {

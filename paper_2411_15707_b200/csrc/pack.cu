@@ -21,16 +21,38 @@
 
 namespace nimbus {
 
+#ifdef NIMBUS_TRACE
+// Debug-only pack timeline (globaltimer ns): [0] first block start, [1] first block past the
+// PDL wait, [2] last block past the wait, [3] last block end (tools/trace_tc.py).
+__device__ unsigned long long* g_trace_pack = nullptr;
+extern "C" int nimbus_trace_pack_set(void* p) { return (int)cudaMemcpyToSymbol(g_trace_pack, &p, sizeof(p)); }
+__device__ __forceinline__ unsigned long long gtimer_pack() {
+    unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
+}
+#define PTRACE_MIN(i) do { if (g_trace_pack && threadIdx.x == 0) atomicMin(&g_trace_pack[i], gtimer_pack()); } while (0)
+#define PTRACE_MAX(i) do { if (g_trace_pack) { __syncthreads(); if (threadIdx.x == 0) atomicMax(&g_trace_pack[i], gtimer_pack()); } } while (0)
+#else
+#define PTRACE_MIN(i) do { } while (0)
+#define PTRACE_MAX(i) do { } while (0)
+#endif
+
 template <int V, int L, int RB, typename MT = uint32_t>
 __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                               uint32_t Rr, uint32_t nct, uint64_t key_mask,
                                               uint32_t* __restrict__ cts, MT* __restrict__ Rout,
                                               const uint32_t* __restrict__ Z0) {
     pdl_trigger();
+    PTRACE_MIN(0);
     const uint32_t J = (blockIdx.x * blockDim.x + threadIdx.x) * V;
+#ifndef NIMBUS_TRACE
     if (J >= Rn.N) return;
+#endif
     pdl_wait();  // C is produced by the contraction kernel
-    pack_item<V, L, RB, MT>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, Z0, blockIdx.y, blockIdx.z, J);
+    PTRACE_MIN(1);
+    PTRACE_MAX(2);
+    if (J < Rn.N)
+        pack_item<V, L, RB, MT>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, Z0, blockIdx.y, blockIdx.z, J);
+    PTRACE_MAX(3);
 }
 
 template <typename K, typename... Args>

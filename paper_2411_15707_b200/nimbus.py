@@ -79,6 +79,7 @@ _SIGS = {
     "nimbus_cop_matmul_streamed_u64": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp, _sz, _vp]),
     "nimbus_encw_save": (C.c_int, [_vp, C.c_char_p]),
     "nimbus_encw_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "nimbus_encw_open": (C.c_int, [_vp, C.c_char_p, C.c_int, C.POINTER(_vp)]),
     "nimbus_encw_offload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_reload": (C.c_int, [_vp, _vp]),
     "nimbus_encw_is_resident": (C.c_int, [_vp]),
@@ -437,6 +438,17 @@ def nimbus_encw_load(ctx: Context, path: str, m: int = None, n: int = None) -> E
     """Enc(W) from a store file; m, n are read from the file (the arguments only label the handle)."""
     out = C.c_void_p()
     _check(lib().nimbus_encw_load(ctx.ptr, path.encode(), C.byref(out)), ctx)
+    import struct
+    with open(path, "rb") as f:
+        hdr = struct.unpack("<8s6I", f.read(32))
+    return EncW(out, ctx, hdr[5], hdr[6])
+
+
+def nimbus_encw_open(ctx: Context, path: str, verify: bool = False) -> EncW:
+    """File-backed Enc(W) handle on a store file: its payload is read from disk per
+    nimbus_cop_matmul_streamed job; m, n come from the file header."""
+    out = C.c_void_p()
+    _check(lib().nimbus_encw_open(ctx.ptr, path.encode(), 1 if verify else 0, C.byref(out)), ctx)
     import struct
     with open(path, "rb") as f:
         hdr = struct.unpack("<8s6I", f.read(32))

@@ -558,6 +558,87 @@ def test_streamed_matches_resident(nb, oracle):
     assert torch.equal(c1, ref[0][0]) and torch.equal(R1, ref[0][1])
 
 
+def test_streamed_from_files(nb, oracle, tmp_path):
+    """Enc(W) kept on disk: store files opened as file-backed
+    handles are read, uploaded and tiled per job by nimbus_cop_matmul_streamed; a job
+    list mixing resident, host-offloaded and file-backed matrices (more file jobs than
+    read buffers) gives the bytes of resident calls.  Opening a truncated or corrupt
+    file fails with NIMBUS_EIO (the corrupt one only with verify); a file that vanishes
+    after opening makes nimbus_sync report NIMBUS_EIO; nimbus_encw_reload reads a
+    file-backed handle into HBM."""
+    N, L, ell, L_out = 4096, 2, 16, 1
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, 6)
+    shapes = [(128, 768, 768, 1), (64, 300, 700, 2), (128, 768, 3072, 1), (100, 1000, 500, 1), (33, 129, 64, 1),
+              (128, 768, 768, 1)]
+    kinds = ["file", "resident", "file", "host", "file", "file"]
+    jobs, ref, paths = [], [], []
+    ws = torch.empty(max(nb.nimbus_cop_workspace_size(ctx, nb.nimbus_encrypt_weights(ctx, sk, dev_u32(
+        ni.gen_W(1, m, n, ell)), 1), kq * nq) for kq, m, n, nq in shapes), dtype=torch.uint8, device=DEV)
+    for i, ((kq, m, n, nq), kind) in enumerate(zip(shapes, kinds)):
+        w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(ni.gen_W(40 + i, m, n, ell)), 40 + i)
+        X = dev_u32(ni.gen_X(50 + i, kq * nq, m, ell))
+        c0, R0 = nb.alloc_outputs(ctx, w, kq, nq)
+        nb.nimbus_cop_matmul(ctx, w, X, kq, nq, 60 + i, c0, R0, ws)
+        ref.append((c0, R0))
+        if kind == "file":
+            path = str(tmp_path / f"w{i}.nimbus")
+            nb.nimbus_encw_save(w, path)
+            paths.append(path)
+            w = nb.nimbus_encw_open(ctx, path, verify=(i == 0))
+            assert not nb.nimbus_encw_is_resident(w)
+        elif kind == "host":
+            nb.nimbus_encw_offload(w)
+        cts, R = nb.alloc_outputs(ctx, w, kq, nq)
+        jobs.append(dict(encw=w, X=X, k_per_query=kq, n_queries=nq, mask_seed=60 + i, cts=cts, R=R))
+    nb.nimbus_sync(ctx)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_cop_matmul(ctx, jobs[0]["encw"], jobs[0]["X"], 128, 1, 60, jobs[0]["cts"], jobs[0]["R"], ws)
+    assert e.value.status == -1
+    stage = torch.empty(nb.nimbus_cop_stage_size(ctx, jobs), dtype=torch.uint8, device=DEV)
+    for rep in range(2):
+        for j in jobs:
+            j["cts"].zero_()
+            j["R"].zero_()
+        nb.nimbus_cop_matmul_streamed(ctx, jobs, ws, stage)
+        nb.nimbus_sync(ctx)
+        for j, (c0, R0) in zip(jobs, ref):
+            assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+    # reload a file-backed handle into HBM: plain calls work again
+    nb.nimbus_encw_reload(jobs[0]["encw"])
+    c1, R1 = nb.alloc_outputs(ctx, jobs[0]["encw"], 128, 1)
+    nb.nimbus_cop_matmul(ctx, jobs[0]["encw"], jobs[0]["X"], 128, 1, 60, c1, R1, ws)
+    nb.nimbus_sync(ctx)
+    assert torch.equal(c1, ref[0][0]) and torch.equal(R1, ref[0][1])
+    # truncated / corrupt files
+    data = open(paths[1], "rb").read()
+    trunc = str(tmp_path / "trunc.nimbus")
+    open(trunc, "wb").write(data[:-100])
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_encw_open(ctx, trunc)
+    assert e.value.status == -7
+    bad = bytearray(data)
+    bad[len(bad) // 2] ^= 0x40
+    corrupt = str(tmp_path / "corrupt.nimbus")
+    open(corrupt, "wb").write(bytes(bad))
+    nb.nimbus_encw_open(ctx, corrupt)                      # header and size are fine
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_encw_open(ctx, corrupt, verify=True)
+    assert e.value.status == -7
+    # a file removed after opening: the streamed call's read fails, nimbus_sync reports it
+    gone = str(tmp_path / "gone.nimbus")
+    open(gone, "wb").write(data)
+    wg = nb.nimbus_encw_open(ctx, gone)
+    import os
+    os.remove(gone)
+    jg = dict(jobs[2], encw=wg)
+    stage2 = torch.empty(nb.nimbus_cop_stage_size(ctx, [jg]), dtype=torch.uint8, device=DEV)
+    nb.nimbus_cop_matmul_streamed(ctx, [jg], ws, stage2)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_sync(ctx)
+    assert e.value.status == -7
+
+
 # ------------------------------------------------------------------ ell = 64 (the paper's t, 5 limbs)
 def _u64(t):
     from paper_2411_15707_b200 import nimbus

@@ -1,8 +1,12 @@
 """Asynchronous weight loading on the
 GPU: the first `--layers` BERT-base layers of config 5 (6 matmuls each) with
 every Enc(W) offloaded to pinned host memory, run through
-nimbus_cop_matmul_streamed; compared with the same pass resident in HBM and
-with the bare host->device copy time of all Enc(W).  Prints one JSON line.
+nimbus_cop_matmul_streamed; compared with the same pass resident in HBM, with
+the bare host->device copy time of all Enc(W), and with every Enc(W) read from
+its store file on disk (file-backed handles, nimbus_encw_open; `--dir` for the
+files, default /tmp; the files were just written, so they are likely in the
+page cache -- the number is a page-cache read + upload + tile rate, not a cold
+disk rate).  Prints one JSON line.
 
   python tools/bench_stream.py --config 5 --layers 1
 """
@@ -34,6 +38,7 @@ def ev_time(fn, reps=3):
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="5")
 ap.add_argument("--layers", type=int, default=1)
+ap.add_argument("--dir", default="/tmp")
 args = ap.parse_args()
 cfg = ni.CONFIGS[int(args.config)]
 lays = [x for x in cfg.layers if x[0] < args.layers]
@@ -56,6 +61,21 @@ for j in jobs:
     nb.nimbus_encw_offload(j["encw"])
 stage = torch.empty(nb.nimbus_cop_stage_size(ctx, jobs), dtype=torch.uint8, device=dev)
 t_str = ev_time(lambda: nb.nimbus_cop_matmul_streamed(ctx, jobs, ws, stage))
+# Enc(W) on disk: store files -> file-backed handles -> streamed (read + upload + tile per job)
+fjobs, paths = [], []
+for i, j in enumerate(jobs):
+    nb.nimbus_encw_reload(j["encw"])
+    path = os.path.join(args.dir, f"nimbus_stream_{os.getpid()}_{i}.nimbus")
+    nb.nimbus_encw_save(j["encw"], path)
+    nb.nimbus_encw_offload(j["encw"])
+    paths.append(path)
+    fjobs.append(dict(j, encw=nb.nimbus_encw_open(ctx, path)))
+fstage = torch.empty(nb.nimbus_cop_stage_size(ctx, fjobs), dtype=torch.uint8, device=dev)
+t_file = ev_time(lambda: nb.nimbus_cop_matmul_streamed(ctx, fjobs, ws, fstage))
+nb.nimbus_sync(ctx)
+file_bytes = sum(os.path.getsize(p) for p in paths)
+for p in paths:
+    os.remove(p)
 # bare H2D of the same bytes (pinned host -> device) for the copy-bound floor
 host = torch.empty(enc_bytes, dtype=torch.uint8).pin_memory()
 devbuf = torch.empty(enc_bytes, dtype=torch.uint8, device=dev)
@@ -63,5 +83,6 @@ t_copy = ev_time(lambda: devbuf.copy_(host, non_blocking=True))
 print(json.dumps({"workload": f"{cfg.name} first {args.layers} layer(s): {len(jobs)} matmuls, "
                               f"{enc_bytes / 1e9:.2f} GB Enc(W)",
                   "resident_ms": t_res, "streamed_ms": t_str, "h2d_only_ms": t_copy,
+                  "from_files_ms": t_file, "file_gb_per_s": file_bytes / (t_file * 1e-3) / 1e9,
                   "h2d_gb_per_s": enc_bytes / (t_copy * 1e-3) / 1e9,
                   "overlap": "streamed ~ max(resident, h2d) means copy and compute overlap"}))

@@ -37,6 +37,8 @@ if MODE == "rotate":   # as bench --l2 rotate: other copies' inputs fill the L2 
     for wo, Xo in others:
         nb.nimbus_cop_matmul(ctx, wo, Xo, k, 1, 3, cts, R, ws)
 lib.nimbus_trace_set(ctypes.c_void_p(tr.data_ptr()))
+trp = torch.tensor([2**62, 2**62, 0, 0], dtype=torch.int64, device="cuda")
+lib.nimbus_trace_pack_set(ctypes.c_void_p(trp.data_ptr()))
 if MODE in ("write", "writeread"):
     flush.zero_()
 if MODE == "writeread":
@@ -45,6 +47,7 @@ torch.cuda.synchronize()
 nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
 torch.cuda.synchronize()
 lib.nimbus_trace_set(ctypes.c_void_p(0))
+lib.nimbus_trace_pack_set(ctypes.c_void_p(0))
 t = tr.cpu().numpy().reshape(148, 64).astype(np.int64)
 t0 = t[:, 0][t[:, 0] > 0].min()
 us = lambda x: (x - t0) / 1e3 if x > 0 else float("nan")
@@ -71,3 +74,6 @@ e = np.array([us(x) for x in t[:, 3] if x > 0])
 print(f"CTA end: min {e.min():.2f} median {np.median(e):.2f} max {e.max():.2f} us")
 st = np.array([us(x) for x in t[:, 0] if x > 0])
 print(f"CTA start: min {st.min():.2f} max {st.max():.2f}")
+tp = trp.cpu().numpy().astype(np.int64)
+print(f"pack: first block start {us(tp[0]):.2f}  first past PDL wait {us(tp[1]):.2f}  last past wait {us(tp[2]):.2f}  "
+      f"last block end {us(tp[3]):.2f} us (contraction CTAs end max {e.max():.2f})")
