@@ -1097,7 +1097,8 @@ static nimbus_status cop_matmul_streamed(nimbus_ctx* ctx, const nimbus_cop_job* 
             uint8_t* hb = ctx->h_read[n_file++ & 1];
             FileRead* rd = new (std::nothrow) FileRead{ctx, w->file, w->file_off, w->canon_bytes, hb};
             if (!rd) return set_err(ctx, NIMBUS_ENOMEM, "host alloc");
-            CK(cudaLaunchHostFunc(b, file_read_cb, rd), "file read");
+            const cudaError_t e = cudaLaunchHostFunc(b, file_read_cb, rd);
+            if (e != cudaSuccess) { delete rd; return cuda_err(ctx, e, "file read"); }
             CK(cudaMemcpyAsync(d_canon, hb, w->canon_bytes, cudaMemcpyHostToDevice, b), "stage upload");
             CK(launch_tile_encw(ctx, d_canon, w->m, w->KB, w->bn, stage + (size_t)slot_of[j] * slot, b), "stage tile");
         }
