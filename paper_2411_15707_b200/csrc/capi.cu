@@ -156,6 +156,7 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
     ctx->num_sms = prop.multiProcessorCount;
     if (const char* cl = getenv("NIMBUS_CLUSTER")) ctx->cluster = atoi(cl) == 2 ? 2 : 1;
     if (const char* rr = getenv("NIMBUS_RES")) ctx->res_ring = atoi(rr) == 2 ? 2 : 1;
+    if (const char* nf = getenv("NIMBUS_NO_FUSE")) ctx->fuse_r1 = atoi(nf) == 0;
     Rns& R = ctx->rns;
     R.N = N; R.L = L; R.L_out = Lo; R.ell = ell;
     R.logN = 0; while ((1u << R.logN) < N) R.logN++;
@@ -815,6 +816,18 @@ static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const voi
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t* C = reinterpret_cast<uint32_t*>((uint8_t*)d_ws + L.c);
     prof_mark(ctx, s);
+    if (!d_zero && ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && fused_r1_ok(ctx, w, k)) {
+        // R = 1 (n > N/2): packing is the identity, the contraction's epilogue does the
+        // mod-switch and the mask; no C round trip, no pack launch (the pack stage times 0)
+        CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, kBM, (uint8_t*)d_ws + L.xt, s), "slice X");
+        prof_mark(ctx, s);
+        CK(launch_cop_fused_r1(ctx, w, (uint8_t*)d_ws + L.xt, k, seed, d_cts, static_cast<uint32_t*>(d_R), s),
+           "cop fused");
+        prof_mark(ctx, s);
+        prof_mark(ctx, s);
+        prof_mark(ctx, s);
+        return NIMBUS_OK;
+    }
     st = run_accumulate(ctx, w, d_X, k, C, (uint8_t*)d_ws, s);
     if (st != NIMBUS_OK) return st;
     prof_mark(ctx, s);

@@ -108,6 +108,102 @@ __device__ __forceinline__ void epilogue_tile(const Rns& R, uint32_t tacc, uint3
     }
 }
 
+// ------------------------------------------------------------------ R = 1 fused epilogue
+// Output of an R = 1 layer (n > N/2, L = 2 -> L_out = 1): packing is the identity
+// (c~[theta] = c[theta], PAPER.md:672-679 with one row), so the epilogue itself does
+// the mod-switch c_0 <- (c_0 - [c_1]_centered) p_1^-1 mod p_0
+// and the mask b -= Emb_{q'}(r), r = word(seed, 6, theta N + J) >> (64 - ell)
+// (§8(c) #13) -- the arithmetic of pack_item (pack_dev.cuh) for one
+// unwrapped row.  The CTA takes the limb-0 and the limb-1 tile of the same
+// (component, J) range back to back; on the limb-0 tile the thread keeps its
+// reduced residues in `hold`, on the limb-1 tile it combines and stores the output
+// ciphertext (and R for component 0) -- no C round trip and no pack launch.
+struct FuseOut {
+    uint32_t* cts;      // [row][comp][N] (L_out = 1)
+    uint32_t* Rout;     // [row][n], or null (R produced elsewhere)
+    uint64_t key;       // prg_key(seed, 6)
+    uint32_t n;
+};
+
+template <uint32_t NACC, uint32_t BN>
+__device__ __forceinline__ void epilogue_fused(const Rns& R, uint32_t tacc, uint32_t half, uint32_t row, uint32_t k,
+                                               uint32_t col_base, bool second, uint32_t (&hold)[BN / 16][8],
+                                               const FuseOut& fo) {
+    constexpr uint32_t CPW = BN / 8 / 2;
+    uint32_t v[CPW][NACC][8];
+#pragma unroll
+    for (uint32_t b = 0; b < CPW; b++)
+#pragma unroll
+        for (uint32_t s = 0; s < NACC; s++) tmem_ld8(tacc + s * BN + (half * CPW + b) * 8, v[b][s]);
+    tmem_ld_wait();
+    if (row >= k) return;
+    const uint32_t N = R.N, limb = second ? 1 : 0;
+    const uint32_t p = R.p[limb], c32 = R.c32[limb];
+#pragma unroll
+    for (uint32_t b = 0; b < CPW; b++) {
+        uint32_t res[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; u++) {
+            uint64_t x = v[b][0][u];
+            if (NACC > 1) x = mad_wide(v[b][1][u], 1u << 8, x);
+            if (NACC > 2) x = mad_wide(v[b][2][u], 1u << 16, x);
+            if (NACC > 3) x = mad_wide(v[b][3][u], 1u << 24, x);
+#pragma unroll
+            for (uint32_t s = 4; s < NACC; s++) x = mad_wide(v[b][s][u], R.pow8[limb][s], x);
+            res[u] = reduce64_pm(x, p, c32);
+        }
+        if (!second) {
+#pragma unroll
+            for (uint32_t u = 0; u < 8; u++) hold[b][u] = res[u];
+            continue;
+        }
+        const uint32_t col0 = col_base + (half * CPW + b) * 8;
+        const uint32_t comp = col0 / (2 * N), J = col0 % N;
+        const uint32_t p0 = R.p[0], p1 = R.p[1];
+        uint64_t z = fo.key + 0x9E3779B97F4A7C15ULL * ((uint64_t)row * N + J + 1);
+        uint32_t out[8], rm[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; u++, z += 0x9E3779B97F4A7C15ULL) {
+            const uint32_t c = res[u];
+            const bool neg = c > (p1 >> 1);                 // centered rho = c - p_1 < 0
+            const uint32_t mag = neg ? p1 - c : c;
+            const uint32_t d = neg ? addmod(hold[b][u], mag, p0) : submod(hold[b][u], mag, p0);
+            uint32_t o = mulmod_shoup(d, R.inv_p[1][0], R.inv_p_sh[1][0], p0);
+            if (comp == 0) {
+                rm[u] = (uint32_t)(mix64(z) >> (64 - R.ell));
+                o = submod(o, emb_fast16(rm[u], (uint32_t)R.qout_mod_t, R.ell, p0, R.t_inv[0], R.t_inv_sh[0]), p0);
+            }
+            out[u] = o;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(fo.cts + ((size_t)row * 2 + comp) * N + J);
+        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+        if (comp == 0 && fo.Rout) {
+            uint32_t* rdst = fo.Rout + (size_t)row * fo.n + J;
+#pragma unroll
+            for (uint32_t u = 0; u < 8; u++)
+                if (J + u < fo.n) rdst[u] = rm[u];
+        }
+    }
+}
+
+// The i-th column tile of this CTA: round-robin over the grid, or (FUSE) round-robin
+// over (component, J-tile) pairs, each pair's limb-0 and limb-1 tiles back to back.
+template <bool FUSE>
+struct TileSeq {
+    uint32_t count, NT;
+    __device__ TileSeq(uint32_t CT, uint32_t N, uint32_t BN) : NT(N / BN) {
+        const uint32_t units = FUSE ? CT / 2 : CT;
+        const uint32_t mine = blockIdx.x < units ? (units - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+        count = FUSE ? 2 * mine : mine;
+    }
+    __device__ uint32_t at(uint32_t ti) const {
+        if (!FUSE) return blockIdx.x + ti * gridDim.x;
+        const uint32_t pair = blockIdx.x + (ti >> 1) * gridDim.x;
+        return (pair / NT) * 2 * NT + (ti & 1) * NT + pair % NT;
+    }
+};
+
 // ------------------------------------------------------------------ streaming kernel
 template <int SX, int BN_>
 struct TcCfg {
@@ -288,10 +384,12 @@ struct ResCfg {
     static_assert(SMEM <= 232448, "shared memory");
 };
 
+template <bool FUSE>
 __global__ void __launch_bounds__(ResCfg::THREADS, 1)
 k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t CT,
-             uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C) {
+             uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C, FuseOut fo) {
     using Cfg = ResCfg;
+    const TileSeq<FUSE> tiles(CT, R.N, Cfg::BN);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::SLOT);
@@ -326,7 +424,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             const uint64_t pol_a = policy_evict_last();
             const uint64_t pol_b = policy_evict_first();
             const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
-            uint32_t it = 0, ti = 0;
+            uint32_t it = 0;
 #ifdef NIMBUS_E3
             // every ring slot of the first tile gets its Enc(W) copy before the PDL wait: in a
             // chain of calls this runs while the previous call's pack and this call's slice finish
@@ -340,7 +438,8 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
 #else
             const uint32_t pre = 0;
 #endif
-            for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+            for (uint32_t ti = 0; ti < tiles.count; ti++) {
+                const uint32_t ct = tiles.at(ti);
                 const uint8_t* b_src = Et + (size_t)ct * KB * Cfg::B_BYTES;
                 for (uint32_t kp = 0; kp < KP; kp++, it++) {
                     const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
@@ -388,8 +487,8 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 96
             constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = 32
             const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
-            uint32_t it = 0, ti = 0;
-            for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+            uint32_t it = 0;
+            for (uint32_t ti = 0; ti < tiles.count; ti++) {
                 const uint32_t buf = ti & 1, use = ti >> 1;
                 if (ti >= 2) mbar_wait(&tempty[buf], (use & 1) ^ 1);
                 TRACE(4 + 4 * ti);
@@ -441,14 +540,19 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
         // ---------------- epilogue
         const uint32_t ew = warp - 4;
         const uint32_t sub = ew & 3, half = ew >> 2;
-        uint32_t ti = 0;
-        for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
+        uint32_t hold[Cfg::BN / 16][8];
+        for (uint32_t ti = 0; ti < tiles.count; ti++) {
+            const uint32_t ct = tiles.at(ti);
             const uint32_t buf = ti & 1, use = ti >> 1;
             mbar_wait(&tfull[buf], use & 1);
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
             tc_fence_after();
-            epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS, half,
-                                             sub * 32 + lane, k, ct * Cfg::BN, ncol, C);
+            if (FUSE)
+                epilogue_fused<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
+                                                   half, sub * 32 + lane, k, ct * Cfg::BN, ti & 1, hold, fo);
+            else
+                epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
+                                                  half, sub * 32 + lane, k, ct * Cfg::BN, ncol, C);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -925,14 +1029,38 @@ static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t
         return e;
     }
     {
-        cudaError_t e = ensure_smem(c, k_cop_tc_res, ResCfg::SMEM);
+        cudaError_t e = ensure_smem(c, k_cop_tc_res<false>, ResCfg::SMEM);
         if (e != cudaSuccess) return e;
     }
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
     const uint32_t CT = col_tiles(c, kBNR);
     const uint32_t grid = CT < (uint32_t)c->num_sms ? CT : (uint32_t)c->num_sms;
-    cudaError_t e = launch_pdl(k_cop_tc_res, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt,
-                               (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, d_C);
+    cudaError_t e = launch_pdl(k_cop_tc_res<false>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt,
+                               (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, d_C, FuseOut{});
+    c->launches++;
+    return e;
+}
+
+static bool resident_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t k) {
+    return w->bn == kBNR && sx_of(c->rns.ell) == 2 && k <= kBM && w->KB <= kResMaxKB;
+}
+
+bool fused_r1_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t k) {
+    return c->fuse_r1 && c->res_ring == 1 && resident_ok(c, w, k) && c->rns.L == 2 && c->rns.L_out == 1 &&
+           2 * w->n > c->rns.N && c->rns.N % (2 * kBNR) == 0;
+}
+
+cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint64_t seed,
+                                uint32_t* d_cts, uint32_t* d_R, cudaStream_t st) {
+    if (!fused_r1_ok(c, w, k)) return cudaErrorInvalidValue;
+    cudaError_t e = ensure_smem(c, k_cop_tc_res<true>, ResCfg::SMEM);
+    if (e != cudaSuccess) return e;
+    const uint32_t ncol = 2 * c->rns.L * c->rns.N;
+    const uint32_t CT = col_tiles(c, kBNR), P = CT / 2;       // (component, J-tile) pairs
+    const uint32_t grid = P < (uint32_t)c->num_sms ? P : (uint32_t)c->num_sms;
+    const FuseOut fo{d_cts, d_R, prg_key(seed, 6), w->n};
+    e = launch_pdl(k_cop_tc_res<true>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt,
+                   (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, (uint32_t*)nullptr, fo);
     c->launches++;
     return e;
 }
@@ -981,7 +1109,7 @@ cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_
     }
     if (SX == 8) return cudaErrorInvalidValue;    // 8 slices only in the transposed orientation
     if (w->bn == kBNR) {
-        if (SX == 2 && k <= kBM && w->KB <= kResMaxKB) return launch_res(c, w, d_Xt, k, d_C, st);
+        if (resident_ok(c, w, k)) return launch_res(c, w, d_Xt, k, d_C, st);
         switch (SX) {
             case 1: return launch_cl<1, kBNR>(c, w, d_Xt, k, d_C, st);
             case 2: return launch_cl<2, kBNR>(c, w, d_Xt, k, d_C, st);

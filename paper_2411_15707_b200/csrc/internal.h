@@ -39,6 +39,7 @@ struct nimbus_ctx {
     int num_sms = 148;
     int res_ring = 1;              // resident-X contraction: 1 = 3-slot ring + slice 1 in smem, 2 = deep ring (k_cop_tc_res2); env NIMBUS_RES
     int cluster = 1;               // CTAs per cluster of the streaming contraction (2 = X multicast); env NIMBUS_CLUSTER
+    bool fuse_r1 = true;           // R = 1 layers: mod-switch + mask in the resident kernel's epilogue; env NIMBUS_NO_FUSE=1 off
     // stage profiling (nimbus_profile_*): pending event quadruples, accumulated ms
     bool profile = false;
     std::vector<cudaEvent_t> ev_pool, ev_pending;
@@ -151,6 +152,11 @@ cudaError_t launch_plain_matmul(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_
 uint32_t transposed_rows(const nimbus_ctx* c);
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st);
+// R = 1 fast path of cop_matmul: the resident-X contraction writes the output ciphertexts
+// and R itself (mod-switch + mask fused in its epilogue); fused_r1_ok says when it applies
+bool fused_r1_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t k);
+cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint64_t seed,
+                                uint32_t* d_cts, uint32_t* d_R, cudaStream_t st);
 }  // namespace nimbus
 
 // Opt `kernel` into `bytes` of dynamic shared memory on the context's device, once

@@ -475,6 +475,33 @@ def test_resident_kernels_parity(nb, oracle, monkeypatch, res, m, n, kq, nq):
     assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
 
 
+@pytest.mark.parametrize("fuse", ["1", "0"])
+@pytest.mark.parametrize("N,m,n,kq,nq", [(4096, 768, 3072, 128, 1), (4096, 129, 2049, 100, 1),
+                                         (4096, 520, 4096, 33, 2), (256, 64, 129, 128, 1), (64, 300, 37, 17, 3)])
+def test_fused_r1_parity(nb, oracle, monkeypatch, fuse, N, m, n, kq, nq):
+    """R = 1 layers (n > N/2, L = 2 -> L_out = 1, ell = 16, k <= 128): the resident
+    contraction's epilogue does the mod-switch and the mask and writes the output
+    ciphertexts and R itself (2 launches: slice + contraction; NIMBUS_NO_FUSE=1 keeps
+    the separate pack, 3 launches).  Both are bit-exact vs the oracle: C3, ragged
+    n (R tail not a multiple of 8), ragged rows and k-blocks, n = N with two
+    queries, and grids smaller than the SM count (N = 256, 64)."""
+    monkeypatch.setenv("NIMBUS_NO_FUSE", "0" if fuse == "1" else "1")
+    c = Case(nb, oracle, N, 2, 16, 1, m, n, kq, nq, seed=9090 + m + n)
+    before = nb.nimbus_launch_count(c.ctx)
+    cts, R = c.run()
+    assert nb.nimbus_launch_count(c.ctx) - before == (2 if fuse == "1" else 3)
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all(), "output ciphertexts differ"
+    assert (u32(R) == R_o).all(), "client share R differs"
+    c.check_decrypt(cts, R)
+    # host-buffer call (R produced by its own kernel, the fused epilogue skips it): same bytes
+    ws = nb.alloc_workspace(c.ctx, c.encw, c.k)
+    cts_h, R_h = nb.alloc_outputs(c.ctx, c.encw, c.kq, c.nq, pin=True, device="cpu")
+    Xh = torch.from_numpy(c.X.view(np.int32)).pin_memory()
+    nb.nimbus_cop_matmul_host(c.ctx, c.encw, Xh, c.kq, c.nq, c.seed, cts_h, R_h, ws)
+    assert torch.equal(cts_h, cts.cpu()) and torch.equal(R_h, R.cpu())
+
+
 # ------------------------------------------------------------------ server, Alg. 1 step 5
 @pytest.mark.parametrize("ell", [8, 12, 16, 32])
 @pytest.mark.parametrize("k,m,n", [(1, 1, 1), (200, 300, 100), (128, 768, 768), (130, 129, 65)])
