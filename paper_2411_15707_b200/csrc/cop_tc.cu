@@ -180,9 +180,14 @@ __device__ __forceinline__ void epilogue_fused(const Rns& R, uint32_t tacc, uint
         dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
         if (comp == 0 && fo.Rout) {
             uint32_t* rdst = fo.Rout + (size_t)row * fo.n + J;
+            if (fo.n % 4 == 0 && J + 8 <= fo.n) {          // 16-byte aligned: J % 8 == 0, n % 4 == 0
+                reinterpret_cast<uint4*>(rdst)[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
+                reinterpret_cast<uint4*>(rdst)[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
+            } else {
 #pragma unroll
-            for (uint32_t u = 0; u < 8; u++)
-                if (J + u < fo.n) rdst[u] = rm[u];
+                for (uint32_t u = 0; u < 8; u++)
+                    if (J + u < fo.n) rdst[u] = rm[u];
+            }
         }
     }
 }
