@@ -816,7 +816,9 @@ static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const voi
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t* C = reinterpret_cast<uint32_t*>((uint8_t*)d_ws + L.c);
     prof_mark(ctx, s);
-    if (!d_zero && ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && fused_r1_ok(ctx, w, k)) {
+    // the fused epilogue stores cts and R with 16-byte vector stores: 16-byte aligned buffers only
+    const bool aligned16 = (((uintptr_t)d_cts | (uintptr_t)d_R) & 15) == 0;
+    if (!d_zero && aligned16 && ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && fused_r1_ok(ctx, w, k)) {
         // R = 1 (n > N/2): packing is the identity, the contraction's epilogue does the
         // mod-switch and the mask; no C round trip, no pack launch (the pack stage times 0)
         CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, kBM, (uint8_t*)d_ws + L.xt, s), "slice X");

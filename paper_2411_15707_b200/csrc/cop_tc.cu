@@ -437,7 +437,8 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             for (uint32_t kp = 0; kp < pre; kp++) {
                 const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
                 mbar_arrive_expect_tx(&full[kp], nkb * Cfg::B_BYTES + nkb * 2 * Cfg::SLICE);
-                bulk_g2s(smem + Cfg::OFF_B + kp * Cfg::SLOT, Et + (size_t)blockIdx.x * KB * Cfg::B_BYTES +
+                // the CTA's first tile is tiles.at(0) (not blockIdx.x: the FUSE pair order differs)
+                bulk_g2s(smem + Cfg::OFF_B + kp * Cfg::SLOT, Et + (size_t)tiles.at(0) * KB * Cfg::B_BYTES +
                          (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[kp], pol_b);
             }
 #else
@@ -464,13 +465,13 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                             // this CTA's Enc(W) tiles towards L2: DRAM is otherwise idle until X is ready
                             const uint32_t tb = KB * Cfg::B_BYTES;
                             if (KB > Cfg::KPS) prefetch_l2_bulk(b_src + Cfg::SLOT, tb - Cfg::SLOT);
-                            for (uint32_t c2 = ct + gridDim.x; c2 < CT; c2 += gridDim.x)
-                                prefetch_l2_bulk(Et + (size_t)c2 * tb, tb);
+                            for (uint32_t t2 = 1; t2 < tiles.count; t2++)
+                                prefetch_l2_bulk(Et + (size_t)tiles.at(t2) * tb, tb);
 #endif
 #ifdef NIMBUS_PF1
                             // lighter: only the next tile of this CTA
-                            if (ct + gridDim.x < CT)
-                                prefetch_l2_bulk(Et + (size_t)(ct + gridDim.x) * KB * Cfg::B_BYTES, KB * Cfg::B_BYTES);
+                            if (tiles.count > 1)
+                                prefetch_l2_bulk(Et + (size_t)tiles.at(1) * KB * Cfg::B_BYTES, KB * Cfg::B_BYTES);
 #endif
                             pdl_wait(); TRACE(2);
                         }

@@ -85,6 +85,8 @@ def _matmul_guarded(nb, ctx, w, X, kq, nq, seed, wide=False):
     ({"NIMBUS_TRANSPOSED": "1"}, 8192, 3, 32, 2, 257, 129, 65, 2, 0),   # transposed, ell = 32
     ({"NIMBUS_CLUSTER": "2", "NIMBUS_NO_RESIDENT": "1"}, 4096, 2, 16, 1, 200, 100, 130, 1, 0),
     ({}, 4096, 2, 16, 1, 300, 1000, 70, 1, 1),                      # CUDA-core ablation
+    ({}, 4096, 2, 16, 1, 300, 2051, 60, 2, 0),                      # fused R = 1 epilogue, ragged R tail
+    ({}, 4096, 2, 16, 1, 300, 3072, 128, 1, 0),                     # fused R = 1 epilogue, uint4 R stores
 ])
 def test_cop_matmul_no_oob(nb, monkeypatch, env, N, L, ell, L_out, m, n, kq, nq, impl):
     for k, v in env.items():
@@ -197,3 +199,23 @@ def test_server_no_oob(nb):
     Xsum = ni.gen_X(22, kq * nq, m, ell).astype(np.uint64) + ni.gen_X(23, kq * nq, m, ell).astype(np.uint64)
     ref = _xw_minus(Xsum, Wn, np.zeros((kq * nq, n), np.uint64), ell)
     assert ((u32(Ys).astype(np.uint64) + u32(R).astype(np.uint64)) % np.uint64(1 << ell) == ref).all()
+
+
+def test_fused_r1_misaligned_outputs(nb):
+    """The fused R = 1 epilogue stores with 16-byte vectors; output buffers that are
+    only 4-byte aligned must take the unfused path (same bytes), not fault."""
+    N, L, ell, L_out, m, n, kq, nq = 4096, 2, 16, 1, 300, 3072, 100, 1
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, 31)
+    w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(ni.gen_W(31, m, n, ell)), 31)
+    X = dev_u32(ni.gen_X(32, kq * nq, m, ell))
+    ref_c, ref_R = nb.alloc_outputs(ctx, w, kq, nq)
+    ws = nb.alloc_workspace(ctx, w, kq * nq)
+    nb.nimbus_cop_matmul(ctx, w, X, kq, nq, 33, ref_c, ref_R, ws)
+    bc = torch.zeros(ref_c.numel() + 1, dtype=torch.int32, device=DEV)
+    br = torch.zeros(ref_R.numel() + 1, dtype=torch.int32, device=DEV)
+    c4, r4 = bc[1:].view(ref_c.shape), br[1:].view(ref_R.shape)      # 4 bytes past a 16-byte boundary
+    assert c4.data_ptr() % 16 == 4 and r4.data_ptr() % 16 == 4
+    nb.nimbus_cop_matmul(ctx, w, X, kq, nq, 33, c4, r4, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(c4, ref_c) and torch.equal(r4, ref_R)
