@@ -1,13 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the Nimbus COP hot path (Alg. 1 steps 2-4)
-on B200: one `step` = one nimbus_cop_matmul (slice X -> tcgen05 contraction ->
-RShift packing + mod-switch + mask) over one batch of synthetic inputs with
-Enc(W) resident in HBM.
+on B200: one `step` = one pass of the client's COP matmuls (slice X -> tcgen05
+contraction -> RShift packing + mod-switch + mask) over one batch of synthetic
+inputs with Enc(W) resident in HBM.
 
-Default workload = BASELINE.json configs[1] (C2, BERT-base attention
-projection X 128x768 . W 768x768, N=4096, 2 limbs, ell=16).  `--config`
-selects another BASELINE config (1..5; 4l16 / 5l16 = the ell=16 secondary
-lines).  For C5 a step is the full 12-layer x 6-matmul pass.
+Default line = BASELINE.json configs[4] (C5): the full BERT-base linear stack,
+12 layers x (Q, K, V, O 768x768, FFN-up 768x3072, FFN-down 3072x768) = 72
+matmuls of k = 2048 rows (seq 512 x 4 queries), N=8192, 3 limbs, ell=32 -- the
+north star's "BERT-base FFN layers" in their full-model setting.  The same line
+carries `per_config`: C2 (attention projection), C3 (FFN up), C4 (FFN down),
+each with its own ms_per_step, roofline, cpu_baseline and e2e, plus the paper's
+ell = 64 (C4@l64, C5@l64) as secondary entries.  `--config K` times one config
+alone (1..5; 4l16 / 5l16 / 4l64 / 5l64 the secondary parameter sets).
 
 Prints ONE JSON line (rank 0).  Multi-GPU (torchrun): every rank runs its own
 independent queries against its own copy of Enc(W) (weak scaling, no
@@ -42,15 +46,17 @@ L2_FLUSH_BYTES = 512 << 20     # > 126 MB L2, written between timed steps
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="2")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=None, help="one config alone (default: C5 with per_config entries)")
+    ap.add_argument("--no-per-config", dest="per_config", action="store_false")
     ap.add_argument("--impl", default="tcgen05", choices=["tcgen05", "cudacore", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="skip the secondary timing of the steps replayed from a CUDA graph")
-    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=8.0,
+                    help="oracle seconds per cpu_baseline leg (all cores, then one thread)")
     ap.add_argument("--no-stage-profile", action="store_true", help="no per-stage events inside the step")
     ap.add_argument("--l2", default="rotate", choices=["rotate", "write"],
                     help="cold-L2 method: rotate through input copies totalling >= 3x L2 (default), "
@@ -164,7 +170,7 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -175,11 +181,16 @@ class ClockSampler:
                 mx = float(f[2])
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[3]))
+            except ValueError:
+                pass
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -381,6 +392,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     clocks.wait_samples(1, busy=busy)
     n0 = len(clocks.lines)
     total_ms, _, _, _, launches = timed(profile=False, per_step=args.l2 == "write")
+    kernel = nb.nimbus_last_contraction(ctx)
     clocks.wait_samples(n0 + 2, busy=busy)
     clk = clocks.stop()
     # pass B (roofline evidence): same K steps with CUDA events around each kernel of the
@@ -475,15 +487,26 @@ def run_gpu(args, cfg, rank, world, local_rank):
                f"{l2_bytes >> 20} MiB L2), step i reads copy i mod {n_copies}" if args.l2 == "rotate" else
                f"flushed by a {L2_FLUSH_BYTES >> 20} MiB write before every timed step")
     return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=stage_ms, calls=calls, launches=launches, graph_ms=graph_ms,
+                kernel=kernel,
                 clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e, l2_desc=l2_desc, warm_ms=warm_ms,
                 setup=dict(gpu_ms=setup_gpu_ms, host_s=setup_host_s, bytes=setup_bytes))
 
 
 # ----------------------------------------------------------------- CPU oracle
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(cfg, budget_s, rows_cap=None):
     """Time the oracle (as it stands) on a bounded row sample of the workload:
     the first matrix of the config, steps 2-4 on `rows` rows (whole packed
-    groups), grown until ~budget_s of CPU work.  Returns (modMAC/s, desc, cores)."""
+    groups), grown until ~budget_s of CPU work.  Returns (modMAC/s, desc)."""
     from oracle import oracle as O
     li, pj, lay = cfg.layers[0]
     seed = ni.seed_mm(cfg.cid, li, pj)
@@ -508,10 +531,34 @@ def oracle_sample(cfg, budget_s, rows_cap=None):
             break
         if rows < lay.k_per_query:
             rows = min(lay.k_per_query, rows * 2)
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     desc = (f"{cfg.name} matrix {lay.name} (m={lay.m}, n={lay.n}): oracle steps 2-4 on up to {rows} rows "
             f"x {reps} runs, {done_t:.1f} s CPU wall; Enc(W) setup {t_enc:.1f} s untimed")
-    return done_macs / done_t, desc, cores
+    return done_macs / done_t, desc
+
+
+def cpu_baseline(cfg, budget_s):
+    """The oracle as it stands, on the host's cores (all of them, then one thread;
+    BASELINE.md §3): a reported baseline, not the target."""
+    if cfg.ell > 32:
+        # q > 2^128: only the Python-integer oracle (oracle/wide.py) covers ell = 64, far too slow
+        # to time on a workload-sized sample
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "cpu_model": cpu_model(),
+                "sample": "not timed: the ell > 32 oracle is Python integers (oracle/wide.py)"}
+    from oracle import oracle as O
+    all_threads = O.set_threads(os.cpu_count() or 1)
+    v, desc = oracle_sample(cfg, budget_s)
+    O.set_threads(1)
+    v1, desc1 = oracle_sample(cfg, budget_s / 2)
+    O.set_threads(all_threads)
+    return {"value": v, "unit": UNIT, "cores": all_threads, "kind": "oracle", "sample": desc,
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": desc1}}
+
+
+def workload_config(cfg):
+    """The workload keys both arms print identically (the driver compares them)."""
+    lays = [l for _, _, l in cfg.layers]
+    return {"workload": workload_name(cfg), "config": cfg.name, "k": lays[0].k, "matmuls_per_step": len(lays)}
 
 
 def run_reference(args, cfg, rank, world):
@@ -521,6 +568,7 @@ def run_reference(args, cfg, rank, world):
         return {"impl": "reference", "unavailable": "ell > 32 needs the Python-integer oracle (oracle/wide.py), "
                                                     "not timed as a reference arm"}
     from oracle import oracle as O
+    cores = O.set_threads(os.cpu_count() or 1)
     li, pj, lay = cfg.layers[0]
     seed = ni.seed_mm(cfg.cid, li, pj)
     pr = O.primes(cfg.N, cfg.L)
@@ -547,95 +595,105 @@ def run_reference(args, cfg, rank, world):
         times.append(time.perf_counter() - t0)
     macs = ni.modmacs(rows, lay.m, cfg.N, cfg.L)
     value = macs * len(times) / sum(times)
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     sample = (f"{rows} of {lay.k} rows of {cfg.name} matrix {lay.name} per step (oracle steps 2-4: "
-              f"contraction + packing + mod-switch + mask)")
+              f"contraction + packing + mod-switch + mask), {cores} OpenMP threads")
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u128", "data": "synthetic",
-            "config": {"workload": workload_name(cfg), "config": cfg.name, "k": lay.k,
-                       "matmuls_per_step": 1, "impl": "reference (oracle/, CPU)", "sample_rows": rows,
-                       "l2": "n/a (host)"},
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "config": workload_config(cfg),
+            "impl": "reference", "impl_detail": "reference (oracle/, CPU)", "sample_rows": rows,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-# ----------------------------------------------------------------- main
-def main():
-    args = parse()
-    cfg = get_config(args.config)
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
-    local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    if args.impl == "reference":
-        out = run_reference(args, cfg, rank, world)
-        if out is not None:
-            print(json.dumps(out), flush=True)
-        return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    res = run_gpu(args, cfg, rank, world, local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
+# ----------------------------------------------------------------- roofline
+def algorithmic_bytes(cfg, lay):
+    """SURVEY.md §8(d) bytes of one matmul: Enc(W) + X in + compact output ciphertexts + R out."""
+    es = 4 if cfg.ell <= 32 else 8
+    nct = lay.n_queries * -(-lay.k_per_query // (cfg.N // lay.n))
+    return (lay.m * 2 * cfg.L * cfg.N * 4 + lay.k * lay.m * es + nct * 2 * cfg.L_out * cfg.N * 4
+            + lay.k * lay.n * es)
 
+
+def i8_floor():
+    """The measured tcgen05 kind::i8 rate (tools/mma_bench.cu, profiles/mma_bench.json), if captured."""
+    path = os.path.join(ROOT, "profiles", "mma_bench.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        if d.get("tops_n256"):
+            return float(d["tops_n256"]), d.get("src", "profiles/mma_bench.json")
+    return None, None
+
+
+def ncu_traffic(cfg, kernel):
+    """DRAM read+write bytes per launch from profiles/ncu_<config>.json, when its captured kernel
+    is the kernel this line ran."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{cfg.name.replace('@', '')}.json")
+    if not os.path.exists(path):
+        return None, None
+    cap = json.load(open(path)).get("kernel_capture", {})
+    name = (cap.get("kernel") or "").replace("void ", "").split("(")[0].replace("(int)", "").replace(" ", "")
+    if cap.get("dram_traffic_bytes") is None or name != kernel.replace(" ", ""):
+        return None, f"profiles/ncu_{cfg.name}.json captured {name or '?'}, not {kernel}"
+    return cap["dram_traffic_bytes"], f"profiles/ncu_{cfg.name.replace('@', '')}.json ({name})"
+
+
+def make_line(args, cfg, res, world, steps, warmup, cpu):
+    """The JSON record of one config: the contract keys plus roofline, e2e, cpu_baseline."""
     peaks = measured_peaks()
     lays = [l for _, _, l in cfg.layers]
     macs_step = sum(ni.modmacs(l.k, l.m, cfg.N, cfg.L) for l in lays)
-    ms_step = res["total_ms"] / args.steps
+    ms_step = res["total_ms"] / steps
     value = weak_value(macs_step, world, ms_step)
-    # roofline of the dominant kernel (the contraction, stage 1)
+    # roofline of the dominant kernel (the contraction, stage 1), per launch: the per-step units
+    # (modMACs -> int8 ops, §8(d) bytes) over the contraction launches of a step
     SX, SW = sx_of(cfg.ell), 4
-    contract_ms = res["stage_ms"][1] / max(1, res["calls"])           # per launch
+    launches_step = max(1.0, res["calls"] / steps) if res["calls"] else float(len(lays))
+    contract_ms = res["stage_ms"][1] / res["calls"] if res["calls"] else 0.0
     if contract_ms <= 0:   # stage events off: bound the kernel by the whole step (conservative)
-        contract_ms = ms_step / len(lays)
-    per_launch_macs = macs_step / len(lays)
-    ops = 2 * per_launch_macs * SX * SW                                  # int8 tensor ops
-    hbm_bytes = sum(4 * l.m * 2 * cfg.L * cfg.N + SX * l.k * l.m + 4 * l.k * 2 * cfg.L * cfg.N
-                    for l in lays) / len(lays)                           # Enc(W) + X slices + C
+        contract_ms = ms_step / launches_step
+    ops = 2 * macs_step * SX * SW / launches_step                          # int8 tensor ops per launch
+    hbm_bytes = sum(algorithmic_bytes(cfg, l) for l in lays) / launches_step
     long_step = ms_step > 5.0   # a kernel timed inside a long (multi-matmul) step: sustained peak
     i8_peak = 2.0 * (peaks["bf16_tflops_sustained"] if long_step else peaks["bf16_tflops"])
-    t_i8 = ops / (i8_peak * 1e12)
+    floor, fsrc = i8_floor()
+    # which ceiling binds: the tensor time at the kernel's real int8 rate (the measured kind::i8
+    # floor when captured, else the 2 x bf16 figure) against the HBM time of the §8(d) bytes
+    t_i8 = ops / ((floor or i8_peak) * 1e12)
     t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
-    tens = {"bound": "tensor", "achieved": ops / (contract_ms / 1e3) / 1e12, "peak": i8_peak,
-            "unit": "TFLOP/s"}
+    tens = {"bound": "tensor", "achieved": ops / (contract_ms / 1e3) / 1e12, "peak": i8_peak, "unit": "TFLOP/s"}
     tens["frac"] = tens["achieved"] / tens["peak"]
     hbm = {"bound": "hbm", "achieved": hbm_bytes / (contract_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"],
            "unit": "GB/s"}
     hbm["frac"] = hbm["achieved"] / hbm["peak"]
     prim, alt = (tens, hbm) if t_i8 >= t_hbm else (hbm, tens)
     prim = dict(prim)
-    prim["traffic"] = None
-    ncu_json = os.path.join(ROOT, "profiles", f"ncu_{cfg.name.replace('@', '')}.json")
-    if args.impl == "tcgen05" and os.path.exists(ncu_json):   # dram bytes read + written of one captured launch
-        cap = json.load(open(ncu_json)).get("kernel_capture", {})
-        if cap.get("dram_traffic_bytes") is not None:
-            prim["traffic"] = cap["dram_traffic_bytes"]
-            prim["traffic_src"] = f"profiles/ncu_{cfg.name}.json ({cap.get('kernel', '')[:40]})"
-    prim["kernel"] = "k_cop_tc (tcgen05 kind::i8 contraction)" if args.impl == "tcgen05" else "k_cop_cc"
-    prim["peak_src"] = (f"{peaks['src']}: int8 = 2 x bf16 {'sustained' if long_step else 'burst'}"
+    kernel = res.get("kernel") or "?"
+    prim["traffic"], src = (ncu_traffic(cfg, kernel) if args.impl == "tcgen05" else (None, None))
+    if src:
+        prim["traffic_src"] = src
+    prim["kernel"] = kernel
+    prim["launch_ms"] = contract_ms
+    prim["launches_per_step"] = launches_step
+    prim["peak_src"] = (f"{peaks['src']}: int8 = 2 x bf16 {'sustained' if long_step else 'burst'} (guide's nominal ratio)"
                         if prim["bound"] == "tensor" else f"{peaks['src']} hbm_gbs")
-    prim["ops_per_launch"] = ops if prim["bound"] == "tensor" else hbm_bytes
+    prim["units_per_launch"] = ({"int8_ops": ops} if prim["bound"] == "tensor" else
+                                {"bytes": hbm_bytes, "bytes_def": "|Enc(W)| + |X| + |compact cts| + |R| (SURVEY.md §8(d))"})
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": workload_name(cfg), "config": cfg.name, "k": lays[0].k, "matmuls_per_step": len(lays),
-                   "impl": args.impl, "l2": res["l2_desc"],
-                   "enc_w_bytes_resident": res["enc_bytes"]},
+        "config": workload_config(cfg),
+        "impl": args.impl, "l2": res["l2_desc"], "enc_w_bytes_resident": res["enc_bytes"],
         "roofline": prim,
         "roofline_other": alt,
-        "stages_ms_per_step_profiled": {"slice_x": res["stage_ms"][0] / args.steps,
-                                        "contraction": res["stage_ms"][1] / args.steps,
-                                        "pack_moddown_mask": res["stage_ms"][2] / args.steps},
+        "roofline_i8_floor": (None if floor is None else
+                              {"achieved": tens["achieved"], "peak": floor, "unit": "TFLOP/s",
+                               "frac": tens["achieved"] / floor, "peak_src": fsrc}),
+        "stages_ms_per_step_profiled": {"slice_x": res["stage_ms"][0] / steps,
+                                        "contraction": res["stage_ms"][1] / steps,
+                                        "pack_moddown_mask": res["stage_ms"][2] / steps},
         # per-step spread of the timed pass (CUDA events around each step, rank 0; SURVEY.md §8(d))
         "step_ms_dist": dict(step_dist(res["step_ms"]),
                              note="separate pass, CUDA events around every step (no PDL overlap across steps)"),
@@ -665,16 +723,69 @@ def main():
                       "single_call": {"ms_per_step": e["single_ms"],
                                       "value": weak_value(macs_step, world, e["single_ms"]),
                                       "call": "one synchronous nimbus_cop_matmul_host per matmul, L2 cold before"}}
-    if world == 1 and not args.no_cpu_baseline:
-        if cfg.ell > 32:
-            # q > 2^128: only the Python-integer oracle (oracle/wide.py) covers ell = 64, far too slow
-            # to time on a workload-sized sample
-            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
-                                   "sample": "not timed: the ell > 32 oracle is Python integers (oracle/wide.py)"}
-        else:
-            v, desc, cores = oracle_sample(cfg, args.cpu_budget_s)
-            out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
-    print(json.dumps(out), flush=True)
+    if cpu:
+        out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_budget_s)
+    return out
+
+
+def bench_config(args, key, rank, world, local_rank, steps=None, warmup=None, e2e=True, cpu=True):
+    """Run and describe one config; frees its device memory before returning."""
+    import copy
+    import gc
+    import torch
+    cfg = get_config(key)
+    a = copy.copy(args)
+    a.steps = args.steps if steps is None else steps
+    a.warmup = args.warmup if warmup is None else warmup
+    a.no_e2e = args.no_e2e or not e2e
+    res = run_gpu(a, cfg, rank, world, local_rank)
+    gc.collect()
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+    return make_line(a, cfg, res, world, a.steps, a.warmup, cpu and world == 1 and not args.no_cpu_baseline)
+
+
+# ----------------------------------------------------------------- main
+MAIN_CONFIG = "5"
+# (config, steps cap) of the per_config block: C2 / C3 / C4 at the bench's steps, the paper's ell = 64
+# pass at <= 5 steps (a 27 GB Enc(W), ~0.3 s per pass)
+PER_CONFIG = (("2", None), ("3", None), ("4", None), ("4l64", None), ("5l64", 5))
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    key = args.config or MAIN_CONFIG
+    cfg = get_config(key)
+    if args.impl == "reference":
+        out = run_reference(args, cfg, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    line = bench_config(args, key, rank, world, local_rank)
+    if args.config is None and args.per_config:
+        per = {}
+        for k2, cap in PER_CONFIG:
+            st = args.steps if cap is None else min(args.steps, cap)
+            wu = args.warmup if cap is None else min(args.warmup, 3)
+            d = bench_config(args, k2, rank, world, local_rank, steps=st, warmup=wu)
+            if d is not None:
+                per[get_config(k2).name] = d
+        if line is not None:
+            line["per_config"] = per
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -403,6 +403,10 @@ nimbus_status nimbus_negacyclic_mul(nimbus_ctx* ctx, const uint32_t* d_a, const 
                                     uint32_t count, uint32_t* d_c, void* stream);
 /* Number of library kernels launched through this context since creation. */
 uint64_t nimbus_launch_count(const nimbus_ctx* ctx);
+/* Name of the last contraction kernel the context launched ("k_cop_pk<4, 52>", "k_cop_tc_res<true>",
+ * ...; "" before the first), owned by the context and valid until its next call.  Measurement
+ * support: bench.py matches it against the kernel of the ncu capture it takes `traffic` from. */
+const char* nimbus_last_contraction(const nimbus_ctx* ctx);
 
 /* Per-stage CUDA-event timing of nimbus_cop_matmul (for the bench's live
  * roofline numbers).  When enabled, each stage -- [0] slice X (K4),

@@ -36,6 +36,22 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's parallel loops (execution only, no arithmetic change);
+    returns the thread count now in effect (for the bench's cpu_baseline `cores`)."""
+    lib()
+    gomp = C.CDLL("libgomp.so.1")
+    gomp.omp_set_num_threads(int(n))
+    return max_threads()
+
+
+def max_threads() -> int:
+    lib()
+    gomp = C.CDLL("libgomp.so.1")
+    gomp.omp_get_max_threads.restype = C.c_int
+    return int(gomp.omp_get_max_threads())
+
+
 def lib():
     global _lib
     if _lib is None:

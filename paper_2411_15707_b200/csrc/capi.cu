@@ -254,6 +254,8 @@ const char* nimbus_last_error(const nimbus_ctx* ctx) { return ctx ? ctx->err.c_s
 
 uint64_t nimbus_launch_count(const nimbus_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+const char* nimbus_last_contraction(const nimbus_ctx* ctx) { return ctx ? ctx->last_contraction : ""; }
+
 nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
     DevGuard dg_(ctx, __func__);
     if (!ctx) return NIMBUS_EINVAL;
@@ -383,6 +385,11 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
         cudaError_t e = cudaMalloc(&w->d_Et, w->bytes);
         if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "encw alloc"); }
     }
+    if (packed_layout_ok(ctx, w)) {
+        // the packed contraction's complement correction (cop_pk.cu): corr + ColSum, 2 x 2LN residues
+        cudaError_t e = cudaMalloc(&w->d_corr, 2 * ncols(ctx) * 4);
+        if (e != cudaSuccess) { if (w->d_Et) cudaFree(w->d_Et); delete w; return cuda_err(ctx, e, "encw corr alloc"); }
+    }
     *out = w;
     return NIMBUS_OK;
 }
@@ -415,6 +422,7 @@ static cudaError_t encrypt_into(nimbus_ctx* ctx, const nimbus_sk* sk, const void
     uint32_t* canon = static_cast<uint32_t*>(ctx->d_scratch);
     cudaError_t e = launch_encrypt(ctx, sk->d_s_ntt, d_W, w->m, w->n, seed, canon, s);
     if (e == cudaSuccess) e = launch_tile_encw(ctx, canon, w->m, w->KB, w->bn, w->d_Et, s);
+    if (e == cudaSuccess) e = launch_pk_corr(ctx, w, s);
     return e;
 }
 
@@ -472,6 +480,7 @@ void nimbus_encw_destroy(nimbus_encw* w) {
     DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w) return;
     if (w->d_Et) cudaFree(w->d_Et);
+    if (w->d_corr) cudaFree(w->d_corr);
     if (w->h_Et) cudaFreeHost(w->h_Et);
     delete w;
 }
@@ -531,6 +540,7 @@ nimbus_status nimbus_encw_import(nimbus_ctx* ctx, const uint32_t* d_in, uint32_t
     nimbus_status st = new_encw(ctx, m, n, &w);
     if (st != NIMBUS_OK) return st;
     cudaError_t e = launch_tile_encw(ctx, d_in, m, w->KB, w->bn, w->d_Et, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = launch_pk_corr(ctx, w, (cudaStream_t)stream);
     if (e != cudaSuccess) { nimbus_encw_destroy(w); return cuda_err(ctx, e, "encw import"); }
     *out = w;
     return NIMBUS_OK;
@@ -628,6 +638,7 @@ static nimbus_status payload_to_device(nimbus_ctx* ctx, nimbus_encw* w, const ui
     cudaError_t e = w->d_Et ? cudaSuccess : cudaMalloc(&w->d_Et, w->bytes);
     if (e == cudaSuccess) e = cudaMemcpy(d_canon, host, nbytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = launch_tile_encw(ctx, d_canon, w->m, w->KB, w->bn, w->d_Et, nullptr);
+    if (e == cudaSuccess) e = launch_pk_corr(ctx, w, nullptr);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaFree(d_canon);
     return e == cudaSuccess ? NIMBUS_OK : cuda_err(ctx, e, "load import");
@@ -724,6 +735,15 @@ static WsLayout ws_layout(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t 
     L.stage_cts = L.stage_x + al((size_t)k * w->m * es);
     L.stage_r = L.stage_cts + al((size_t)k * 2 * ctx->rns.L_out * ctx->rns.N * 4);
     L.total = L.stage_r + al((size_t)k * w->n * es);
+    if (packed_layout_ok(ctx, w)) {
+        // packed X slices (cop_pk.cu) at offset 0: room for ceil(k / R) packed ciphertexts plus one
+        // per query boundary for up to 64 queries; cop_matmul falls back when a call needs more
+        const uint64_t Rr = ctx->rns.N / w->n;
+        size_t pk = 0;
+        for (uint32_t rt : {48u, 52u, 56u, 64u})
+            pk = std::max(pk, 1024 + packed_xp_bytes(ctx, w, (k + Rr - 1) / Rr + 64, rt));
+        L.total = std::max(L.total, al(pk));
+    }
     return L;
 }
 
@@ -818,6 +838,22 @@ static nimbus_status cop_matmul(nimbus_ctx* ctx, const nimbus_encw* w, const voi
     prof_mark(ctx, s);
     // the fused epilogue stores cts and R with 16-byte vector stores: 16-byte aligned buffers only
     const bool aligned16 = (((uintptr_t)d_cts | (uintptr_t)d_R) & 15) == 0;
+    if (!d_zero && packed_ok(ctx, w, kq, nq)) {
+        // packed contraction: slice into the packed layout, then one kernel that writes the compact
+        // output ciphertexts (mod-switch + mask in its epilogue) -- no C round trip, no pack launch
+        PkHostJob J;
+        J.w = w; J.d_X = static_cast<const uint32_t*>(d_X); J.kq = kq; J.nq = nq; J.seed = seed;
+        J.d_cts = d_cts; J.d_R = static_cast<uint32_t*>(d_R); J.d_Xp = (const uint8_t*)d_ws + 1024;
+        const uint32_t rt = packed_rt(ctx, &J, 1);
+        if (1024 + packed_job_bytes(ctx, J, rt) <= ws_bytes) {
+            // workspace: [dispatch counter | packed X slices | dropped-limb residues | flags]
+            CK(launch_cop_packed(ctx, &J, 1, rt, static_cast<uint32_t*>(d_ws), s, prof_mark), "cop packed");
+            prof_mark(ctx, s);      // after the contraction; the (empty) pack stage: two more marks
+            prof_mark(ctx, s);
+            prof_mark(ctx, s);
+            return NIMBUS_OK;
+        }
+    }
     if (!d_zero && aligned16 && ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && fused_r1_ok(ctx, w, k)) {
         // R = 1 (n > N/2): packing is the identity, the contraction's epilogue does the
         // mod-switch and the mask; no C round trip, no pack launch (the pack stage times 0)
@@ -908,6 +944,50 @@ nimbus_status nimbus_cop_matmul_rr_u64(nimbus_ctx* ctx, const nimbus_encw* w, co
 // ---------------------------------------------------------------- batched online path
 static size_t al1k(size_t x) { return (x + 1023) & ~size_t(1023); }
 
+// the batch as one packed job list (cop_pk.cu) when every job qualifies: the packed X slices of
+// all jobs side by side in the workspace, one slice launch and one contraction launch in total
+static bool batch_packed(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
+                         std::vector<PkHostJob>* out, uint32_t* rt, size_t* bytes) {
+    std::vector<PkHostJob> v(count);
+    for (uint32_t i = 0; i < count; i++) {
+        const nimbus_cop_job& J = jobs[i];
+        if (!J.encw || !packed_ok(ctx, J.encw, J.k_per_query, J.n_queries)) return false;
+        v[i].w = J.encw; v[i].d_X = J.d_X; v[i].kq = J.k_per_query; v[i].nq = J.n_queries;
+        v[i].seed = J.mask_seed; v[i].d_cts = J.d_cts; v[i].d_R = J.d_R;
+    }
+    *rt = packed_rt(ctx, v.data(), count);
+    size_t off = 1024;                                              // [0, 1024): dispatch counter
+    for (uint32_t i = 0; i < count; i++) {
+        v[i].d_Xp = reinterpret_cast<const uint8_t*>(off);          // offset; rebased by the caller
+        off += al1k(packed_job_bytes(ctx, v[i], *rt));
+    }
+    *bytes = off;
+    if (out) out->swap(v);
+    return true;
+}
+
+// Same-X groups (Q, K, V of a layer share their input): consecutive jobs with the
+// same X pointer and shape whose contraction is the resident-X kernel run as ONE contraction
+// launch over their Enc(W)s and one pack launch.  Returns the group length at job i (1 = alone).
+static uint32_t same_x_group(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, uint32_t i) {
+    const nimbus_cop_job& A = jobs[i];
+    const uint32_t k = A.k_per_query * A.n_queries;
+    auto ok = [&](const nimbus_cop_job& J) {
+        return J.encw && J.encw->d_Et && ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && ctx->res_ring == 1 &&
+               resident_ok(ctx, J.encw, k) && !fused_r1_ok(ctx, J.encw, k);
+    };
+    if (!ok(A) || getenv("NIMBUS_NO_GROUP")) return 1;
+    uint32_t g = 1;
+    while (g < 4 && i + g < count) {
+        const nimbus_cop_job& B = jobs[i + g];
+        if (B.d_X != A.d_X || B.k_per_query != A.k_per_query || B.n_queries != A.n_queries || !B.encw ||
+            B.encw->m != A.encw->m || B.encw->n != A.encw->n || !ok(B))
+            break;
+        g++;
+    }
+    return g;
+}
+
 nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
                                               size_t* bytes) {
     if (!ctx || !jobs || !bytes || count == 0) return NIMBUS_EINVAL;
@@ -920,7 +1000,16 @@ nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbu
         const size_t cb = al1k((size_t)k * ncols(ctx) * 4);
         c = c > cb ? c : cb;
     }
-    *bytes = xt + 2 * c;
+    uint32_t nbuf = 2;                                              // C buffers: 2, or the largest group
+    for (uint32_t i = 0; i < count;) {
+        const uint32_t g = same_x_group(ctx, jobs, count, i);
+        nbuf = std::max(nbuf, g);
+        i += g;
+    }
+    *bytes = xt + nbuf * c;
+    uint32_t rt = 0;
+    size_t pk = 0;
+    if (batch_packed(ctx, jobs, count, nullptr, &rt, &pk)) *bytes = std::max(*bytes, pk);
     return NIMBUS_OK;
 }
 
@@ -936,14 +1025,34 @@ static nimbus_status cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* job
     size_t need = 0;
     nimbus_cop_workspace_size_batch(ctx, jobs, count, &need);
     if (ws_bytes < need) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    {
+        std::vector<PkHostJob> pj;
+        uint32_t rt = 0;
+        size_t pk = 0;
+        if (batch_packed(ctx, jobs, count, &pj, &rt, &pk)) {
+            cudaStream_t a = (cudaStream_t)stream;
+            for (auto& j : pj) j.d_Xp = (const uint8_t*)d_ws + reinterpret_cast<uintptr_t>(j.d_Xp);
+            prof_mark(ctx, a);
+            CK(launch_cop_packed(ctx, pj.data(), count, rt, static_cast<uint32_t*>(d_ws), a,
+                                 count <= 128 ? prof_mark : nullptr), "cop packed batch");
+            if (count > 128) prof_mark(ctx, a);
+            prof_mark(ctx, a);
+            prof_mark(ctx, a);
+            prof_mark(ctx, a);
+            return NIMBUS_OK;
+        }
+    }
     size_t xt = 0;
     for (uint32_t i = 0; i < count; i++) {
         const WsLayout L = ws_layout(ctx, jobs[i].encw, jobs[i].k_per_query * jobs[i].n_queries);
         xt = xt > L.c ? xt : L.c;
     }
-    const size_t cbytes = (need - xt) / 2;
+    size_t cbytes = 0;
+    for (uint32_t i = 0; i < count; i++)
+        cbytes = std::max(cbytes, al1k((size_t)jobs[i].k_per_query * jobs[i].n_queries * ncols(ctx) * 4));
     uint8_t* ws = (uint8_t*)d_ws;
-    uint32_t* Cbuf[2] = {reinterpret_cast<uint32_t*>(ws + xt), reinterpret_cast<uint32_t*>(ws + xt + cbytes)};
+    uint32_t* Cbuf[4];
+    for (uint32_t b = 0; b < 4; b++) Cbuf[b] = reinterpret_cast<uint32_t*>(ws + xt + b * cbytes);
     cudaStream_t a = (cudaStream_t)stream;
     if (!ctx->side) CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
     cudaStream_t b = ctx->side;
@@ -961,6 +1070,39 @@ static nimbus_status cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* job
     for (uint32_t i = 0; i < count; i++) {
         const nimbus_cop_job& J = jobs[i];
         const uint32_t k = J.k_per_query * J.n_queries;
+        const uint32_t g = same_x_group(ctx, jobs, count, i);
+        if (g > 1) {
+            // one slice of the shared X, one contraction over the group's Enc(W)s into C buffers
+            // 0..g-1, one pack launch, all on `stream` (PDL-chained); earlier packs on the side
+            // stream may still read buffers 0 / 1
+            if (i >= 1) CK(cudaStreamWaitEvent(a, done_p[i - 1], 0), "wait pack");
+            if (i >= 2) CK(cudaStreamWaitEvent(a, done_p[i - 2], 0), "wait pack");
+            prof_mark(ctx, a);
+            CK(launch_slice_x(ctx, J.d_X, k, J.encw->m, J.encw->KB, kBM, ws, a), "slice X");
+            prof_mark(ctx, a);
+            ResJobs RJ;
+            PackJobs PJ;
+            RJ.nj = PJ.nj = g;
+            for (uint32_t q = 0; q < g; q++) {
+                RJ.Et[q] = jobs[i + q].encw->d_Et;
+                RJ.C[q] = Cbuf[q];
+                PJ.C[q] = Cbuf[q];
+                PJ.cts[q] = jobs[i + q].d_cts;
+                PJ.R[q] = jobs[i + q].d_R;
+                PJ.key[q] = prg_key(jobs[i + q].mask_seed, 6);
+            }
+            CK(launch_res_jobs(ctx, RJ, J.encw->KB, ws, k, a), "cop group");
+            prof_mark(ctx, a);
+            prof_mark(ctx, a);
+            CK(launch_pack_jobs(ctx, PJ, J.k_per_query, J.n_queries, J.encw->n, a, true), "pack group");
+            prof_mark(ctx, a);
+            for (uint32_t q = 0; q < g; q++) {
+                CK(cudaEventRecord(done_c[i + q], a), "record");
+                CK(cudaEventRecord(done_p[i + q], a), "record");
+            }
+            i += g - 1;
+            continue;
+        }
         uint32_t* C = Cbuf[i & 1];
         // C[i%2] is free once the pack of job i-2 has read it
         if (i >= 2) CK(cudaStreamWaitEvent(a, done_p[i - 2], 0), "wait pack");

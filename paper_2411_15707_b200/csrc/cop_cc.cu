@@ -1,3 +1,4 @@
+#include <cstdio>
 // cop_cc.cu -- K6: the COP contraction on CUDA cores (ablation; first parity
 // kernel).  Alg. 1 step 2:
 //     C[alpha][col] = sum_beta X[alpha][beta] * E[beta][col]  mod p(col)
@@ -90,6 +91,7 @@ cudaError_t launch_cop_cudacore(nimbus_ctx* c, const nimbus_encw* w, const uint3
     else
         k_cop_cc<true><<<g, kCcCols, 0, st>>>(c->rns, w->d_Et, d_X, k, w->m, w->KB, w->bn, ncol, d_C);
     c->launches++;
+    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_cc");
     return cudaGetLastError();
 }
 

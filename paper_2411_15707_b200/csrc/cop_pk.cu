@@ -1,0 +1,664 @@
+// cop_pk.cu -- K5 + K7 fused: the COP contraction computed directly in the PACKED
+// output layout, with the mod-switch and the mask in its epilogue (ell in (16, 32],
+// n a multiple of 128, Enc(W) in the 128-column "transposed" layout).
+//
+// RShift packing (stride n: PAPER.md:243) is linear in the rows:
+//     c~[theta] = sum_{r<R} X^{r n} c[theta R + r]
+//               = sum_{r<R} sum_beta x[theta R + r, beta] X^{r n} Enc(W_beta)
+// so, per (component, limb) and output coefficient J,
+//     c~[theta][J] = sum_{r<R} sgn(r, J) sum_beta x[theta R + r, beta] E[beta][(J - r n) mod N]
+// with sgn = -1 exactly when J < r n (the negacyclic wrap, X^N = -1).  That is a GEMM
+// with K = (r, beta) (R m terms) and M = the packed ciphertexts theta -- the same MACs
+// as the row-wise contraction (k m 2 L N), but the unpacked C (k x 2LN, 403 MB per C5
+// matmul) is never written and no pack kernel reads it back.
+//
+// When n % 128 == 0 every shift r n is a whole number of 128-coefficient tiles, so the
+// operand of term r for output tile T is simply Enc(W) tile (T - r n / 128) mod (N/128),
+// and the sign is constant over the tile (wrapped iff 128 T < r n).  The sign cannot be
+// applied inside an unsigned int8 MMA; instead a wrapped term multiplies the bitwise
+// complement ~x = (2^(8 S_x) - 1) - x, and the epilogue subtracts the precomputed
+//     corr[J] = (2^(8 S_x) - 1) * sum_{r: J < r n} ColSum[(J - r n) mod N]   (mod p),
+// ColSum[col] = sum_beta E[beta][col]: sum_beta ~x E = (2^(8S_x)-1) ColSum - sum_beta x E.
+// Rows theta R + r >= k_q ("pad with zeros") are x = 0, i.e. ~x = all ones
+// in the complemented copy, so corr is the same for every theta.
+//
+// Exactness: 8-bit slices as in cop_tc.cu (acc_s = sum_{i+j=s} x_i e_j in int32 TMEM);
+// the K loop runs in chunks of at most 64 k-blocks (8192 terms: acc_s < 4 * 8192 * 255^2
+// < 2^31, and the recombination sum_s acc_s (2^(8s) mod p) < 2^63), each chunk drained
+// by the epilogue into a running residue mod p.
+//
+// Work unit = (matmul, limb pass, component, theta tile of RT packed ciphertexts,
+// 128-coefficient J tile).  The limb passes of a matmul run in the order L-1 .. L_out
+// (the limbs ModDown drops) then 0 .. L_out-1, so that the Enc(W) blocks in use at any
+// time belong to one (component, limb) slab (25 MB at m = 768, 100 MB at m = 3072) and
+// stay in L2 while the R shifted output tiles and the theta tiles that read each block
+// come by.  A dropped-limb pass leaves its centred residues rho in an L2-resident
+// scratch and raises a per-tile flag; the output passes wait for the flag and apply
+// ModDown (c_i <- (c_i - [c_l]) p_l^-1) and the mask
+// b -= Emb_{q'}(r) (§8(c) #13) in the epilogue, which writes the compact
+// output ciphertexts and R.  Units are handed out in order by an atomic counter (the
+// CTAs in flight always work on neighbouring units); one persistent launch serves a
+// whole job list (the 72 matmuls of the C5 pass), so there is one tail per pass.
+#include <memory>
+#include <cstdio>
+#include <cstring>
+#include "internal.h"
+#include "slice_dev.cuh"
+
+namespace nimbus {
+
+constexpr uint32_t kPkMaxJobs = 128;
+constexpr uint32_t kPkMaxChunkKB = 64;     // k-blocks (x 128 terms) per accumulator drain at S_x <= 4
+constexpr uint32_t kPkQ = 4;               // unit-id queue depth (producer -> MMA issuer, epilogue)
+
+struct PkJob {
+    const uint8_t* Et;        // Enc(W) tiles [ct][kb][4 planes][128][128 B]
+    const uint8_t* Xp;        // packed X slices [(r, cmp)][theta tile][kb][S_x][RT][128 B]
+    const uint32_t* corr;     // [comp][limb][N]
+    uint32_t* cts;            // [theta_global][comp][L_out][N]
+    uint32_t* Rout;           // [alpha_global][n], or null
+    const uint32_t* X;        // slice kernel input [k][m]
+    int32_t* rho;             // [drop][theta tile row][comp][N]: centred residues of the dropped limbs
+    uint32_t* flags;          // [drop][comp][theta tile][J tile]: rho written
+    uint64_t key;             // prg_key(mask_seed, 6)
+    uint32_t m, KB, Rr, n, kq, nct, ntheta, TT, CKB, NCH, nflags;
+    uint32_t unit_end;        // contraction: prefix end of this job's units
+    uint32_t blk_end;         // slice kernel: prefix end of this job's blocks
+};
+struct PkParams {
+    uint32_t njobs;
+    uint32_t* ctr;            // unit dispatch counter (zeroed by the slice kernel)
+    PkJob job[kPkMaxJobs];
+};
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+                    "r"(v[7]) : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                 :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]) : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }   // the 8 epilogue warps
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// Shared memory: two rings with their own barriers, so a freed slot is refilled after a
+// quarter (E) / one (X) k-step of MMAs instead of a whole one: an Enc(W) ring of ESLOTS
+// slots holding ONE byte plane (128 columns x 128 B = 16 KB) each, and an X ring of XSLOTS
+// slots holding the S_x slices of one (term r, k-block).  A 2-slot ring of whole
+// (E + X) k-steps left the MMA issuer waiting for data ~25% of the time (L2 latency).
+template <int SX, int RT>
+struct PkCfg {
+    static constexpr uint32_t BM = kBNW, BK = kBK;
+    static constexpr uint32_t A_BYTES = kSW * BM * BK;     // 64 KB: 4 planes x 128 columns x 128 B
+    static constexpr uint32_t P_BYTES = BM * BK;           // one plane: 16 KB
+    static constexpr uint32_t B_BYTES = SX * RT * BK;      // S_x slices x RT rows x 128 B
+    static constexpr uint32_t ESLOTS = 8, XSLOTS = 3;
+    static constexpr uint32_t OFF_X = ESLOTS * P_BYTES;
+    static constexpr uint32_t RING = OFF_X + XSLOTS * B_BYTES;
+    static constexpr uint32_t NACC = SX + kSW - 1;
+    static constexpr uint32_t NCHK = (RT + 7) / 8;         // 8-row chunks of an accumulator (the last may hold 4)
+    static constexpr uint32_t TAIL = RT - 8 * (NCHK - 1);  // rows of the last chunk: 8, or 4 (RT = 52)
+    static constexpr uint32_t CPT0 = (NCHK + 1) / 2;       // chunks of the first epilogue half
+    static constexpr uint32_t EPI_WARPS = 8;
+    static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
+    static constexpr size_t SMEM = (size_t)RING + 1024 + 512;     // alignment slack + barriers, queue
+    static_assert(RT % 4 == 0 && (TAIL == 8 || TAIL == 4), "8-row chunks, a 4-row tail at most");
+    static_assert((SX * RT) % 16 == 0 && SX * RT <= 256, "MMA N");
+    static_assert(NACC * RT <= 512, "TMEM");
+    static_assert(B_BYTES % 1024 == 0, "swizzle atoms");
+    static_assert(SMEM <= 232448, "shared memory");
+};
+
+// unit u -> (job, limb pass, component, theta tile, J tile); T fastest so that the CTAs
+// in flight read neighbouring Enc(W) tiles of one (component, limb) slab
+struct PkUnit {
+    uint32_t j, pass, comp, tt, T;
+};
+__device__ __forceinline__ PkUnit pk_decode(const PkParams& P, uint32_t u, uint32_t NT) {
+    PkUnit x;
+    uint32_t j = 0;
+    while (u >= P.job[j].unit_end) j++;
+    uint32_t v = u - (j ? P.job[j - 1].unit_end : 0u);
+    const uint32_t TT = P.job[j].TT;
+    x.j = j;
+    x.T = v % NT; v /= NT;
+    x.tt = v % TT; v /= TT;
+    x.comp = v & 1;
+    x.pass = v >> 1;
+    return x;
+}
+// limb of pass `pass`: dropped limbs L-1 .. L_out first, then 0 .. L_out-1
+__device__ __forceinline__ uint32_t pk_limb(const Rns& R, uint32_t pass) {
+    const uint32_t nd = R.L - R.L_out;
+    return pass < nd ? R.L - 1 - pass : pass - nd;
+}
+
+template <int SX, int RT>
+__global__ void __launch_bounds__(PkCfg<SX, RT>::THREADS, 1)
+k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint32_t total_units) {
+    using Cfg = PkCfg<SX, RT>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* efull = reinterpret_cast<uint64_t*>(smem + Cfg::RING);
+    uint64_t* eempty = efull + Cfg::ESLOTS;
+    uint64_t* xfull = eempty + Cfg::ESLOTS;
+    uint64_t* xempty = xfull + Cfg::XSLOTS;
+    uint64_t* tfull = xempty + Cfg::XSLOTS;
+    uint64_t* tempty = tfull + 1;
+    uint64_t* qfull = tempty + 1;                 // [kPkQ]
+    uint64_t* qempty = qfull + kPkQ;              // [kPkQ]
+    uint32_t* unit_q = reinterpret_cast<uint32_t*>(qempty + kPkQ);
+    uint32_t* tmem_slot = unit_q + kPkQ;
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t N = R.N, NT = N / Cfg::BM, L = R.L, ND = R.L - R.L_out;
+    if (warp == 0 && lane == 0) {
+        for (uint32_t s = 0; s < Cfg::ESLOTS; s++) { mbar_init(&efull[s], 1); mbar_init(&eempty[s], 1); }
+        for (uint32_t s = 0; s < Cfg::XSLOTS; s++) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, Cfg::EPI_WARPS);
+        for (uint32_t q = 0; q < kPkQ; q++) { mbar_init(&qfull[q], 1); mbar_init(&qempty[q], 1 + Cfg::EPI_WARPS); }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- producer: fetches units in order; per (kb, r) one Enc(W) block + one X block
+            const uint64_t pol_e = policy_evict_last();    // an Enc(W) block serves R output tiles x theta tiles
+            const uint64_t pol_x = policy_evict_last();    // X blocks serve every J tile
+            pdl_wait();                                    // X slices, counter and flags: the slice kernel's
+            // every unit, the first included, comes from the counter: a unit is only ever held by a
+            // running CTA, so a flag wait never depends on a CTA that has not been scheduled
+            uint32_t ie = 0, ix = 0, u = atomicAdd(P.ctr, 1u);
+            for (uint32_t i = 0;; i++) {
+                const uint32_t q = i % kPkQ;
+                if (i >= kPkQ) mbar_wait(&qempty[q], ((i / kPkQ) & 1) ^ 1);
+                unit_q[q] = u;
+                mbar_arrive(&qfull[q]);
+                if (u >= total_units) break;
+                const PkUnit U = pk_decode(P, u, NT);
+                const PkJob& J = P.job[U.j];
+                const uint32_t limb = pk_limb(R, U.pass);
+                const size_t slab = ((size_t)U.comp * L + limb) * NT;
+                const uint32_t shift_t = J.n / Cfg::BM;               // tiles per shift step
+                for (uint32_t kb = 0; kb < J.KB; kb++) {
+                    for (uint32_t r = 0; r < J.Rr; r++) {
+                        const uint32_t sh = r * shift_t;
+                        const bool wrap = U.T < sh;
+                        const uint32_t srcT = wrap ? U.T + NT - sh : U.T - sh;
+                        {   // X slices of (r, kb)
+                            const uint32_t s = ix % Cfg::XSLOTS, ph = (ix / Cfg::XSLOTS) & 1;
+                            if (ix >= Cfg::XSLOTS) mbar_wait(&xempty[s], ph ^ 1);
+                            ix++;
+                            mbar_arrive_expect_tx(&xfull[s], Cfg::B_BYTES);
+                            bulk_g2s(smem + Cfg::OFF_X + s * Cfg::B_BYTES,
+                                     J.Xp + ((((size_t)(2 * r + (wrap ? 1 : 0)) * J.TT + U.tt) * J.KB + kb) *
+                                             Cfg::B_BYTES),
+                                     Cfg::B_BYTES, &xfull[s], pol_x);
+                        }
+                        const uint8_t* eb = J.Et + ((slab + srcT) * J.KB + kb) * Cfg::A_BYTES;
+                        for (uint32_t jp = 0; jp < kSW; jp++, ie++) {   // the 4 byte planes of the Enc(W) block
+                            const uint32_t s = ie % Cfg::ESLOTS, ph = (ie / Cfg::ESLOTS) & 1;
+                            if (ie >= Cfg::ESLOTS) mbar_wait(&eempty[s], ph ^ 1);
+                            mbar_arrive_expect_tx(&efull[s], Cfg::P_BYTES);
+                            bulk_g2s(smem + s * Cfg::P_BYTES, eb + jp * Cfg::P_BYTES, Cfg::P_BYTES, &efull[s], pol_e);
+                        }
+                    }
+                }
+                u = atomicAdd(P.ctr, 1u);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (the whole warp, converged; one elected lane issues):
+        // D[coefficient][theta] += E_j^T . [x_0 | x_1 | .. ] per plane j.  Descriptors are the slot
+        // base descriptors plus (kk * 32 B) >> 4 in the start-address field.
+        constexpr uint32_t idesc = idesc_i8(Cfg::BM, SX * RT);
+        const uint64_t e_desc0 = sdesc_kmajor_sw128(smem_u32(smem));
+        const uint64_t x_desc0 = sdesc_kmajor_sw128(smem_u32(smem + Cfg::OFF_X));
+        constexpr uint64_t EP = Cfg::P_BYTES >> 4, XP = Cfg::B_BYTES >> 4;
+        uint32_t ie = 0, ix = 0, gc = 0;
+        for (uint32_t i = 0;; i++) {
+            const uint32_t q = i % kPkQ;
+            mbar_wait(&qfull[q], (i / kPkQ) & 1);
+            const uint32_t u = unit_q[q];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&qempty[q]);
+            if (u >= total_units) break;
+            const PkUnit U = pk_decode(P, u, NT);
+            const uint32_t KB = P.job[U.j].KB, Rr = P.job[U.j].Rr, CKB = P.job[U.j].CKB, NCH = P.job[U.j].NCH;
+            for (uint32_t c = 0; c < NCH; c++, gc++) {
+                mbar_wait(tempty, gc & 1);           // accumulators drained (and zeroed)
+                tc_fence_after();
+                const uint32_t kb1 = min(KB, (c + 1) * CKB);
+                for (uint32_t kb = c * CKB; kb < kb1; kb++) {
+                    for (uint32_t r = 0; r < Rr; r++, ix++) {
+                        const uint32_t xs = ix % Cfg::XSLOTS;
+                        mbar_wait(&xfull[xs], (ix / Cfg::XSLOTS) & 1);
+                        const uint64_t bd = x_desc0 + xs * XP;
+#pragma unroll
+                        for (uint32_t jp = 0; jp < kSW; jp++, ie++) {
+                            const uint32_t es = ie % Cfg::ESLOTS;
+                            mbar_wait(&efull[es], (ie / Cfg::ESLOTS) & 1);
+                            tc_fence_after();
+                            const uint64_t ad = e_desc0 + es * EP;
+#pragma unroll
+                            for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
+                                mma_i8_ss_w(tmem + jp * RT, ad + 2 * kk, bd + 2 * kk, idesc, 1u);
+                            mma_commit_w(&eempty[es]);      // this plane's slot is free once its MMAs retire
+                        }
+                        mma_commit_w(&xempty[xs]);
+                    }
+                }
+                mma_commit_w(tfull);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: lane = coefficient column, 8-row chunks of the theta tile
+        const uint32_t ew = warp - 4;
+        const uint32_t sub = ew & 3, half = ew >> 2;
+        constexpr uint32_t CPT = Cfg::CPT0;
+        const uint32_t ch0 = half * Cfg::CPT0;
+        const uint32_t nch = half ? Cfg::NCHK - Cfg::CPT0 : Cfg::CPT0;     // chunks of this thread
+        const uint32_t tl = tmem + ((sub * 32) << 16);
+        const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        pdl_wait();          // flags / rho / outputs: after the slice kernel (and the stream's earlier work)
+        // zero the accumulators once; afterwards every drain re-zeroes what it read
+#pragma unroll
+        for (uint32_t ci = 0; ci < CPT; ci++)
+            if (ci < nch) {
+                const bool t4 = Cfg::TAIL == 4 && ch0 + ci == Cfg::NCHK - 1;   // 4 columns: the next acc starts
+#pragma unroll
+                for (uint32_t s = 0; s < Cfg::NACC; s++) {
+                    if (t4) tmem_st4(tl + s * RT + (ch0 + ci) * 8, zero8);
+                    else tmem_st8(tl + s * RT + (ch0 + ci) * 8, zero8);
+                }
+            }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+
+        uint32_t acc[CPT][8];        // running residue of the unit's limb (mod p_limb)
+        uint32_t gc = 0;
+        for (uint32_t i = 0;; i++) {
+            const uint32_t q = i % kPkQ;
+            mbar_wait(&qfull[q], (i / kPkQ) & 1);
+            const uint32_t u = unit_q[q];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&qempty[q]);
+            if (u >= total_units) break;
+            const PkUnit U = pk_decode(P, u, NT);
+            const PkJob& J = P.job[U.j];
+            const uint32_t Jc = U.T * Cfg::BM + sub * 32 + lane;         // output coefficient
+            const uint32_t limb = pk_limb(R, U.pass);
+            const uint32_t p = R.p[limb], c32 = R.c32[limb];
+            for (uint32_t c = 0; c < J.NCH; c++, gc++) {
+                mbar_wait(tfull, gc & 1);
+                tc_fence_after();
+#pragma unroll
+                for (uint32_t ci = 0; ci < CPT; ci++) {
+                    if (ci >= nch) continue;
+                    uint32_t v[Cfg::NACC][8];
+                    const uint32_t col = (ch0 + ci) * 8;
+                    const bool t4 = Cfg::TAIL == 4 && ch0 + ci == Cfg::NCHK - 1;
+                    if (t4) {
+#pragma unroll
+                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld4(tl + s * RT + col, v[s]);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_st4(tl + s * RT + col, zero8);
+                    } else {
+#pragma unroll
+                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld8(tl + s * RT + col, v[s]);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_st8(tl + s * RT + col, zero8);
+                    }
+#pragma unroll
+                    for (uint32_t qq = 0; qq < 8; qq++) {
+                        uint64_t x = mad_wide(v[1][qq], 1u << 8, v[0][qq]);
+                        x = mad_wide(v[2][qq], 1u << 16, x);
+                        x = mad_wide(v[3][qq], 1u << 24, x);
+#pragma unroll
+                        for (uint32_t s = 4; s < Cfg::NACC; s++) x = mad_wide(v[s][qq], R.pow8[limb][s], x);
+                        const uint32_t red = reduce64_pm(x, p, c32);
+                        acc[ci][qq] = c == 0 ? red : addmod(acc[ci][qq], red, p);
+                    }
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty);     // the MMA issuer may start the next chunk
+            }
+            // ---- the unit's limb is complete: remove the complement offset, then ModDown / mask / store
+            const uint32_t ndep = U.pass < ND ? U.pass : ND;          // dropped limbs this pass depends on
+            const size_t fl_tile = ((size_t)U.comp * J.TT + U.tt) * NT + U.T;
+            const size_t fl_stride = (size_t)2 * J.TT * NT;
+            if (ndep) {
+                if (ew == 0 && lane == 0) {
+                    for (uint32_t d = 0; d < ndep; d++)
+                        while (ld_acquire(J.flags + d * fl_stride + fl_tile) == 0) __nanosleep(200);
+                }
+                epi_bar();
+            }
+            const uint32_t cr = J.corr[((size_t)U.comp * L + limb) * N + Jc];
+            const size_t rho_stride = (size_t)J.TT * RT * 2 * N;
+#pragma unroll
+            for (uint32_t ci = 0; ci < CPT; ci++) {
+                if (ci >= nch) continue;
+#pragma unroll
+                for (uint32_t qq = 0; qq < 8; qq++) {
+                    const uint32_t row = (ch0 + ci) * 8 + qq;
+                    if (row >= (uint32_t)RT) continue;                            // past a 4-row tail
+                    const uint32_t tg = U.tt * RT + row;                          // packed ciphertext (global)
+                    const size_t ridx = ((size_t)tg * 2 + U.comp) * N + Jc;
+                    uint32_t v = submod(acc[ci][qq], cr, p);
+                    // earlier dropped limbs: v <- (v - rho_d) p_{L-1-d}^-1 mod p   (|rho| < p_l / 2 < p)
+                    for (uint32_t d = 0; d < ndep; d++) {
+                        const uint32_t ld = L - 1 - d;
+                        const int32_t rh = __ldcg(J.rho + d * rho_stride + ridx);
+                        const uint32_t t = rh < 0 ? addmod(v, (uint32_t)(-rh), p) : submod(v, (uint32_t)rh, p);
+                        v = mulmod_shoup(t, R.inv_p[ld][limb], R.inv_p_sh[ld][limb], p);
+                    }
+                    if (U.pass < ND) {
+                        // a dropped limb: keep its centred residue for the later passes
+                        __stcg(J.rho + U.pass * rho_stride + ridx, v > (p >> 1) ? (int32_t)v - (int32_t)p : (int32_t)v);
+                        continue;
+                    }
+                    if (tg >= J.ntheta) continue;
+                    if (U.comp == 0) {
+                        const uint32_t rm = (uint32_t)(prg_word(J.key, (uint64_t)tg * N + Jc) >> (64 - R.ell));
+                        v = submod(v, emb_fast(rm, (uint32_t)R.qout_mod_t, R.ell, p, R.t_inv[limb], R.t_inv_sh[limb]), p);
+                        if (limb == 0 && J.Rout) {
+                            const uint32_t qy = tg / J.nct, th = tg - qy * J.nct;
+                            const uint32_t ri = Jc / J.n, jj = Jc - ri * J.n;
+                            if (ri < J.Rr && th * J.Rr + ri < J.kq)
+                                J.Rout[((size_t)qy * J.kq + th * J.Rr + ri) * J.n + jj] = rm;
+                        }
+                    }
+                    J.cts[(((size_t)tg * 2 + U.comp) * R.L_out + limb) * N + Jc] = v;
+                }
+            }
+            if (U.pass < ND) {
+                __threadfence();
+                epi_bar();
+                if (ew == 0 && lane == 0) st_release(J.flags + U.pass * fl_stride + fl_tile, 1u);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ------------------------------------------------------------------ packed X slices
+// Item (rc = 2 r + cmp, theta row, kb, 16-byte chunk): row theta_global of theta tile tt
+// holds x[q kq + theta R + r] (zero when theta R + r >= kq or theta_global >= ntheta),
+// bitwise complemented (S_x bytes) when cmp = 1.
+template <int SX, int RT>
+__global__ void __launch_bounds__(256) k_slice_pk(const __grid_constant__ PkParams P, uint32_t ell, uint32_t* flag,
+                                                  int check) {
+    pdl_trigger();
+    pdl_wait();          // the packed slices may still be read by the previous contraction in the stream
+    uint32_t j = 0;
+    while (blockIdx.x >= P.job[j].blk_end) j++;
+    const PkJob& J = P.job[j];
+    const uint32_t idx = (blockIdx.x - (j ? P.job[j - 1].blk_end : 0u)) * blockDim.x + threadIdx.x;
+    // the contraction's dispatch counter and this job's rho flags start at zero
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctr = 0;
+    if (idx < J.nflags) J.flags[idx] = 0;
+    const uint32_t rows = J.TT * RT;
+    const uint32_t per_rc = rows * J.KB * 8;
+    const uint32_t rc = idx / per_rc;
+    if (rc >= 2 * J.Rr) return;
+    const uint32_t r = rc >> 1, cmp = rc & 1;
+    if (r == 0 && cmp) return;                 // term 0 never wraps
+    const uint32_t rem = idx - rc * per_rc;
+    const uint32_t tgl = rem / (J.KB * 8), ch = rem % (J.KB * 8);
+    const uint32_t kb = ch >> 3, c16 = ch & 7;
+    const uint32_t beta0 = kb * kBK + c16 * 16;
+    const uint32_t qy = tgl / J.nct, th = tgl - qy * J.nct;
+    const bool present = tgl < J.ntheta && th * J.Rr + r < J.kq;
+    const size_t arow = (size_t)qy * J.kq + th * J.Rr + r;
+    uint32_t v[16];
+    if (present && beta0 + 16 <= J.m && (J.m & 3) == 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(J.X + arow * J.m + beta0);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint4 w = __ldg(src + q);
+            v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 16; u++) v[u] = (present && beta0 + u < J.m) ? J.X[arow * J.m + beta0 + u] : 0u;
+    }
+    if (check && present && ell < 32) {
+        uint32_t bad = 0;
+#pragma unroll
+        for (int u = 0; u < 16; u++) bad |= v[u] >> ell;
+        if (bad) atomicOr(flag, 1u);
+    }
+    if (cmp) {
+        const uint32_t ones = SX >= 4 ? 0xFFFFFFFFu : (1u << (8 * SX)) - 1u;
+#pragma unroll
+        for (int u = 0; u < 16; u++) v[u] ^= ones;
+    }
+    const uint32_t tt = tgl / RT, rr = tgl % RT;
+#pragma unroll
+    for (int i = 0; i < SX; i++) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            w[q] = ((v[4 * q] >> (8 * i)) & 0xFF) | (((v[4 * q + 1] >> (8 * i)) & 0xFF) << 8) |
+                   (((v[4 * q + 2] >> (8 * i)) & 0xFF) << 16) | (((v[4 * q + 3] >> (8 * i)) & 0xFF) << 24);
+        // the 128-B swizzle follows the row's position in the whole (S_x x RT)-row operand block:
+        // slice i starts at row i RT, which is not a multiple of 8 when RT = 52
+        uint8_t* dst = const_cast<uint8_t*>(J.Xp) + ((((size_t)rc * J.TT + tt) * J.KB + kb) * SX * RT) * kBK +
+                       swz_off(i * RT + rr, c16);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// ------------------------------------------------------------------ setup: column sums and corr
+// ColSum[col] = sum_{beta < m} E[beta][col] mod p(col), read from the tiled byte planes
+// (thread = one coefficient column = one 128-B row of each plane).
+__global__ void __launch_bounds__(128) k_colsum(Rns R, const uint8_t* __restrict__ Et, uint32_t KB, uint32_t ncol,
+                                                uint32_t* __restrict__ colsum) {
+    const uint32_t ct = blockIdx.x, row = threadIdx.x;
+    const uint32_t col = ct * kBNW + row;
+    if (col >= ncol) return;
+    uint32_t sum[kSW] = {0, 0, 0, 0};
+    for (uint32_t kb = 0; kb < KB; kb++) {
+        const uint8_t* base = Et + ((size_t)ct * KB + kb) * kSW * kBNW * kBK;
+#pragma unroll
+        for (uint32_t s = 0; s < kSW; s++) {
+            const uint4* rp = reinterpret_cast<const uint4*>(base + (size_t)s * kBNW * kBK + row * kBK);
+#pragma unroll
+            for (int c = 0; c < 8; c++) {          // the 8 chunks of the row, in any (swizzled) order
+                const uint4 w = __ldg(rp + c);
+                const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    sum[s] += (ws[q] & 0xFF) + ((ws[q] >> 8) & 0xFF) + ((ws[q] >> 16) & 0xFF) + (ws[q] >> 24);
+            }
+        }
+    }
+    const uint32_t limb = (col / R.N) % R.L, p = R.p[limb];
+    uint64_t x = 0;
+#pragma unroll
+    for (uint32_t s = 0; s < kSW; s++) x += (uint64_t)sum[s] << (8 * s);       // < 2^45
+    colsum[col] = reduce64_pm(x, p, R.c32[limb]);
+}
+
+// corr[comp][limb][J] = (2^(8 S_x) - 1) sum_{1 <= r < R, J < r n} ColSum[comp][limb][J - r n + N]  mod p
+__global__ void k_corr(Rns R, const uint32_t* __restrict__ colsum, uint32_t n, uint32_t SX,
+                       uint32_t* __restrict__ corr) {
+    const uint32_t col = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t N = R.N, ncol = 2 * R.L * N;
+    if (col >= ncol) return;
+    const uint32_t slab = col / N, J = col % N, limb = slab % R.L, p = R.p[limb];
+    const uint32_t Rr = N / n;
+    uint64_t s = 0;
+    for (uint32_t r = 1; r < Rr; r++)
+        if (J < r * n) s += colsum[slab * N + J + N - r * n];
+    const uint32_t c = reduce64_pm(s, p, R.c32[limb]);
+    // (2^(8 S_x) - 1) mod p: 2^32 - 1 = c32 - 1 (mod p) at S_x = 4
+    const uint64_t ones = SX >= 4 ? (uint64_t)R.c32[limb] + p - 1 : (1ull << (8 * SX)) - 1;
+    corr[col] = reduce64_pm((uint64_t)c * (ones % p), p, R.c32[limb]);
+}
+
+// ------------------------------------------------------------------ host
+static uint32_t pk_sx(const nimbus_ctx* c) { return sx_of(c->rns.ell); }
+
+bool packed_layout_ok(const nimbus_ctx* c, const nimbus_encw* w) {
+    const char* off = getenv("NIMBUS_NO_PACKED");
+    return c->prm.impl == NIMBUS_IMPL_TCGEN05 && w->bn == kBNW && pk_sx(c) == 4 && w->n % kBNW == 0 &&
+           c->rns.N % kBNW == 0 && c->rns.L - c->rns.L_out >= 1 && c->rns.L - c->rns.L_out <= 2 &&
+           !(off && atoi(off) != 0);
+}
+
+static uint32_t pk_nct(const nimbus_ctx* c, const nimbus_encw* w, uint32_t kq) {
+    const uint32_t Rr = c->rns.N / w->n;
+    return (kq + Rr - 1) / Rr;
+}
+
+// the packed path pays off once a matmul has enough packed ciphertexts to fill MMA tiles
+bool packed_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t kq, uint32_t nq) {
+    return w->d_corr && w->d_Et && packed_layout_ok(c, w) && nq * pk_nct(c, w, kq) >= 48;
+}
+
+static const uint32_t kPkRT[4] = {48, 52, 56, 64};
+
+// RT minimising the padded MMA work of the job list (ties: the larger RT)
+uint32_t packed_rt(const nimbus_ctx* c, const PkHostJob* jobs, uint32_t count) {
+    uint64_t best = ~0ull;
+    uint32_t brt = 64;
+    for (int i = 3; i >= 0; i--) {
+        const uint32_t rt = kPkRT[i];
+        uint64_t work = 0;
+        for (uint32_t j = 0; j < count; j++) {
+            const nimbus_encw* w = jobs[j].w;
+            const uint64_t nth = (uint64_t)jobs[j].nq * pk_nct(c, w, jobs[j].kq);
+            work += ((nth + rt - 1) / rt) * rt * (c->rns.N / w->n) * w->KB;
+        }
+        if (work < best) { best = work; brt = rt; }
+    }
+    return brt;
+}
+
+// per job: packed X slices | rho of the dropped limbs | their flags (each 1 KB aligned)
+struct PkBytes {
+    size_t xp, rho, flags, total;
+};
+static PkBytes pk_bytes(const nimbus_ctx* c, const nimbus_encw* w, uint64_t ntheta, uint32_t rt) {
+    auto al = [](size_t x) { return (x + 1023) & ~size_t(1023); };
+    const uint64_t Rr = c->rns.N / w->n, TT = (ntheta + rt - 1) / rt, ND = c->rns.L - c->rns.L_out;
+    PkBytes b;
+    b.xp = al((size_t)(2 * Rr * TT * w->KB * pk_sx(c) * rt * kBK));
+    b.rho = al((size_t)(ND * TT * rt * 2 * c->rns.N * 4));
+    b.flags = al((size_t)(ND * 2 * TT * (c->rns.N / kBNW) * 4));
+    b.total = b.xp + b.rho + b.flags;
+    return b;
+}
+size_t packed_xp_bytes(const nimbus_ctx* c, const nimbus_encw* w, uint64_t ntheta, uint32_t rt) {
+    return pk_bytes(c, w, ntheta, rt).total;
+}
+size_t packed_job_bytes(const nimbus_ctx* c, const PkHostJob& j, uint32_t rt) {
+    return pk_bytes(c, j.w, (uint64_t)j.nq * pk_nct(c, j.w, j.kq), rt).total;
+}
+
+template <int RT>
+static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
+                                void (*mark)(nimbus_ctx*, cudaStream_t)) {
+    using Cfg = PkCfg<4, RT>;
+    std::unique_ptr<PkParams> Pp(new PkParams());     // kernel parameters (copied at launch)
+    PkParams& P = *Pp;
+    cudaError_t e = ensure_smem(c, k_cop_pk<4, RT>, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    const uint32_t NT = c->rns.N / kBNW, ND = c->rns.L - c->rns.L_out;
+    for (uint32_t base = 0; base < count; base += kPkMaxJobs) {
+        const uint32_t nj = count - base < kPkMaxJobs ? count - base : kPkMaxJobs;
+        memset(&P, 0, sizeof(P));
+        P.njobs = nj;
+        P.ctr = d_ctr;
+        uint32_t units = 0, blocks = 0;
+        for (uint32_t i = 0; i < nj; i++) {
+            const PkHostJob& h = jobs[base + i];
+            PkJob& J = P.job[i];
+            const nimbus_encw* w = h.w;
+            J.Et = w->d_Et; J.Xp = h.d_Xp; J.corr = w->d_corr; J.cts = h.d_cts; J.Rout = h.d_R; J.X = h.d_X;
+            J.key = prg_key(h.seed, 6);
+            J.m = w->m; J.KB = w->KB; J.Rr = c->rns.N / w->n; J.n = w->n; J.kq = h.kq;
+            J.nct = pk_nct(c, w, h.kq);
+            J.ntheta = h.nq * J.nct;
+            J.TT = (J.ntheta + RT - 1) / RT;
+            J.CKB = kPkMaxChunkKB / J.Rr;
+            J.NCH = (J.KB + J.CKB - 1) / J.CKB;
+            const PkBytes b = pk_bytes(c, w, J.ntheta, RT);
+            J.rho = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp);
+            J.flags = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp + b.rho);
+            J.nflags = ND * 2 * J.TT * NT;
+            units += c->rns.L * 2 * J.TT * NT;
+            J.unit_end = units;
+            const uint32_t items = 2 * J.Rr * J.TT * RT * J.KB * 8;
+            blocks += ((items > J.nflags ? items : J.nflags) + 255) / 256;
+            J.blk_end = blocks;
+        }
+        const int check = (c->prm.flags & NIMBUS_FLAG_CHECK_RANGE) && c->rns.ell < 32;
+        e = launch_pdl(k_slice_pk<4, RT>, dim3(blocks), dim3(256), 0, st, P, c->rns.ell, c->d_flag, check);
+        c->launches++;
+        if (e != cudaSuccess) return e;
+        if (mark) mark(c, st);
+        const uint32_t grid = units < (uint32_t)c->num_sms ? units : (uint32_t)c->num_sms;
+        e = launch_pdl(k_cop_pk<4, RT>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, c->rns, P, units);
+        c->launches++;
+        snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_pk<4, %d>", RT);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_cop_packed(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t rt, uint32_t* d_ctr,
+                              cudaStream_t st, void (*mark)(nimbus_ctx*, cudaStream_t)) {
+    if (rt == 48) return launch_pk_rt<48>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 52) return launch_pk_rt<52>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 56) return launch_pk_rt<56>(c, jobs, count, d_ctr, st, mark);
+    return launch_pk_rt<64>(c, jobs, count, d_ctr, st, mark);
+}
+
+// ColSum -> corr for a freshly tiled Enc(W) (every path that fills w->d_Et)
+cudaError_t launch_pk_corr(nimbus_ctx* c, nimbus_encw* w, cudaStream_t st) {
+    if (!w->d_corr) return cudaSuccess;
+    const uint32_t ncol = 2 * c->rns.L * c->rns.N;
+    uint32_t* colsum = w->d_corr + ncol;
+    k_colsum<<<col_tiles(c, kBNW), 128, 0, st>>>(c->rns, w->d_Et, w->KB, ncol, colsum);
+    c->launches++;
+    k_corr<<<(ncol + 255) / 256, 256, 0, st>>>(c->rns, colsum, w->n, pk_sx(c), w->d_corr);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+}  // namespace nimbus

@@ -26,6 +26,7 @@
 // Roles: warp 0 producer, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-11
 // epilogue (tcgen05.ld -> recombination -> mod p -> C), double-buffered TMEM
 // accumulators when two sets fit so the epilogue overlaps the next tile.
+#include <cstdio>
 #include "internal.h"
 
 namespace nimbus {
@@ -38,6 +39,23 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
         :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// warp-converged: the whole warp calls with uniform operands, one elected lane issues (common.cuh)
+__device__ __forceinline__ void mma_i8_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+        :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void tmem_cp_128x256b_w(uint32_t taddr, uint64_t sdesc) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}"
+        :: "r"(taddr), "l"(sdesc) : "memory");
 }
 // smem (SWIZZLE_128B K-major, 128 rows x 32 B) -> TMEM 128 lanes x 8 columns
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
@@ -295,7 +313,7 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // the whole warp, converged: one elected lane issues (warp-uniform operands)
             // ---------------- MMA issuer
             constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 4 BN
             constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 3 BN
@@ -321,21 +339,21 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
                         for (uint32_t i = 0; i < (uint32_t)SX; i++) {
                             const uint64_t ad = sdesc_kmajor_sw128(a0 + i * Cfg::BM * Cfg::BK + kk * 32);
                             if ((kb | kk) != 0 || i == 0) {
-                                mma_i8_ss(dacc + i * Cfg::BN, ad, bd, idesc_full, (kb | kk) != 0);
+                                mma_i8_ss_w(dacc + i * Cfg::BN, ad, bd, idesc_full, (kb | kk) != 0);
                             } else {
                                 // first k-step, i >= 1: acc_i..acc_{i+2} exist, acc_{i+3} is new
-                                mma_i8_ss(dacc + i * Cfg::BN, ad, bd, idesc_lo, 1u);
+                                mma_i8_ss_w(dacc + i * Cfg::BN, ad, bd, idesc_lo, 1u);
                                 const uint64_t bd3 =
                                     sdesc_kmajor_sw128(b0 + (kSW - 1) * Cfg::BN * Cfg::BK + kk * 32);
-                                mma_i8_ss(dacc + (i + kSW - 1) * Cfg::BN, ad, bd3, idesc_one, 0u);
+                                mma_i8_ss_w(dacc + (i + kSW - 1) * Cfg::BN, ad, bd3, idesc_one, 0u);
                             }
                         }
                     }
                     // frees the stage (in every CTA of the cluster) when these MMAs retire
-                    if (CL > 1) mma_commit_mc(&empty[s], (1u << CL) - 1);
-                    else mma_commit(&empty[s]);
+                    if (CL > 1) mma_commit_mc_w(&empty[s], (1u << CL) - 1);
+                    else mma_commit_w(&empty[s]);
                 }
-                mma_commit(&tfull[buf]);       // accumulator set complete
+                mma_commit_w(&tfull[buf]);       // accumulator set complete
                 TRACE(5 + 4 * ti);
             }
         }
@@ -389,12 +407,15 @@ struct ResCfg {
     static_assert(SMEM <= 232448, "shared memory");
 };
 
+// Several matmuls that share X (Q, K, V of a layer) run as one launch: the
+// column tiles of their Enc(W)s are one tile sequence (tile t = job t / CT, tile t % CT), so X is
+// fetched once per CTA and the launch streams all of their Enc(W) bytes with one ramp and one tail.
 template <bool FUSE>
 __global__ void __launch_bounds__(ResCfg::THREADS, 1)
-k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, uint32_t k, uint32_t CT,
-             uint32_t KB, uint32_t ncol, uint32_t* __restrict__ C, FuseOut fo) {
+k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, uint32_t CT,
+             uint32_t KB, uint32_t ncol, FuseOut fo) {
     using Cfg = ResCfg;
-    const TileSeq<FUSE> tiles(CT, R.N, Cfg::BN);
+    const TileSeq<FUSE> tiles(FUSE ? CT : CT * jobs.nj, R.N, Cfg::BN);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::SLOT);
@@ -438,15 +459,16 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                 const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
                 mbar_arrive_expect_tx(&full[kp], nkb * Cfg::B_BYTES + nkb * 2 * Cfg::SLICE);
                 // the CTA's first tile is tiles.at(0) (not blockIdx.x: the FUSE pair order differs)
-                bulk_g2s(smem + Cfg::OFF_B + kp * Cfg::SLOT, Et + (size_t)tiles.at(0) * KB * Cfg::B_BYTES +
+                const uint32_t t0 = tiles.at(0);
+                bulk_g2s(smem + Cfg::OFF_B + kp * Cfg::SLOT, jobs.Et[t0 / CT] + (size_t)(t0 % CT) * KB * Cfg::B_BYTES +
                          (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[kp], pol_b);
             }
 #else
             const uint32_t pre = 0;
 #endif
             for (uint32_t ti = 0; ti < tiles.count; ti++) {
-                const uint32_t ct = tiles.at(ti);
-                const uint8_t* b_src = Et + (size_t)ct * KB * Cfg::B_BYTES;
+                const uint32_t tg = tiles.at(ti), ct = tg % CT;
+                const uint8_t* b_src = jobs.Et[tg / CT] + (size_t)ct * KB * Cfg::B_BYTES;
                 for (uint32_t kp = 0; kp < KP; kp++, it++) {
                     const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
                     const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
@@ -466,12 +488,13 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                             const uint32_t tb = KB * Cfg::B_BYTES;
                             if (KB > Cfg::KPS) prefetch_l2_bulk(b_src + Cfg::SLOT, tb - Cfg::SLOT);
                             for (uint32_t t2 = 1; t2 < tiles.count; t2++)
-                                prefetch_l2_bulk(Et + (size_t)tiles.at(t2) * tb, tb);
+                                prefetch_l2_bulk(jobs.Et[tiles.at(t2) / CT] + (size_t)(tiles.at(t2) % CT) * tb, tb);
 #endif
 #ifdef NIMBUS_PF1
                             // lighter: only the next tile of this CTA
                             if (tiles.count > 1)
-                                prefetch_l2_bulk(Et + (size_t)tiles.at(1) * KB * Cfg::B_BYTES, KB * Cfg::B_BYTES);
+                                prefetch_l2_bulk(jobs.Et[tiles.at(1) / CT] + (size_t)(tiles.at(1) % CT) * KB * Cfg::B_BYTES,
+                                                 KB * Cfg::B_BYTES);
 #endif
                             pdl_wait(); TRACE(2);
                         }
@@ -487,7 +510,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // the whole warp, converged: one elected lane issues (warp-uniform operands)
             // ---------------- MMA issuer
             constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 128
             constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 96
@@ -512,9 +535,9 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                             const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + q * Cfg::SLICE);
 #pragma unroll
                             for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
-                                tmem_cp_128x256b(tmem + (kb0 + q) * (Cfg::BK / 4) + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
+                                tmem_cp_128x256b_w(tmem + (kb0 + q) * (Cfg::BK / 4) + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
                         }
-                        mma_commit(&sfree[0]);
+                        mma_commit_w(&sfree[0]);
                     }
                     for (uint32_t q = 0; q < nkb; q++) {
                         const uint32_t kb = kb0 + q;
@@ -525,20 +548,20 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                         for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
                             const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
                             const uint32_t first = (kb | kk) == 0;
-                            mma_i8_ts(dacc, a0t + kk * 8, bd, idesc_full, !first);          // x_0 e_j -> acc_j
+                            mma_i8_ts_w(dacc, a0t + kk * 8, bd, idesc_full, !first);          // x_0 e_j -> acc_j
                             const uint64_t ad1 = sdesc_kmajor_sw128(a1 + kk * 32);
                             if (!first) {
-                                mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_full, 1u);          // x_1 e_j -> acc_{j+1}
+                                mma_i8_ss_w(dacc + Cfg::BN, ad1, bd, idesc_full, 1u);          // x_1 e_j -> acc_{j+1}
                             } else {
-                                mma_i8_ss(dacc + Cfg::BN, ad1, bd, idesc_lo, 1u);
+                                mma_i8_ss_w(dacc + Cfg::BN, ad1, bd, idesc_lo, 1u);
                                 const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (kSW - 1) * Cfg::BN * Cfg::BK + kk * 32);
-                                mma_i8_ss(dacc + kSW * Cfg::BN, ad1, bd3, idesc_one, 0u);
+                                mma_i8_ss_w(dacc + kSW * Cfg::BN, ad1, bd3, idesc_one, 0u);
                             }
                         }
                     }
-                    mma_commit(&empty[s]);
+                    mma_commit_w(&empty[s]);
                 }
-                mma_commit(&tfull[buf]);
+                mma_commit_w(&tfull[buf]);
                 TRACE(5 + 4 * ti);
             }
         }
@@ -548,7 +571,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
         const uint32_t sub = ew & 3, half = ew >> 2;
         uint32_t hold[Cfg::BN / 16][8];
         for (uint32_t ti = 0; ti < tiles.count; ti++) {
-            const uint32_t ct = tiles.at(ti);
+            const uint32_t tg = tiles.at(ti), ct = tg % CT;
             const uint32_t buf = ti & 1, use = ti >> 1;
             mbar_wait(&tfull[buf], use & 1);
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
@@ -558,7 +581,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ 
                                                    half, sub * 32 + lane, k, ct * Cfg::BN, ti & 1, hold, fo);
             else
                 epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
-                                                  half, sub * 32 + lane, k, ct * Cfg::BN, ncol, C);
+                                                  half, sub * 32 + lane, k, ct * Cfg::BN, ncol, jobs.C[tg / CT]);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -687,7 +710,7 @@ k_cop_tc_res2(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // the whole warp, converged: one elected lane issues (warp-uniform operands)
             // ---------------- MMA issuer
             constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 128
             constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 96
@@ -707,10 +730,10 @@ k_cop_tc_res2(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__
                     const uint32_t stg = smem_u32(smem + Cfg::OFF_B + s * Cfg::SLOT + q * Cfg::SLICE);
 #pragma unroll
                     for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
-                        tmem_cp_128x256b(tmem + col0 + (kb0 + q) * (Cfg::BK / 4) + kk * 8,
+                        tmem_cp_128x256b_w(tmem + col0 + (kb0 + q) * (Cfg::BK / 4) + kk * 8,
                                          sdesc_kmajor_sw128(stg + kk * 32));
                 }
-                mma_commit(&empty[s]);
+                mma_commit_w(&empty[s]);
             };
             for (uint32_t ct = blockIdx.x; ct < CT; ct += gridDim.x, ti++) {
                 if (ti >= 1) mbar_wait(tempty, (ti - 1) & 1);     // previous tile's accumulators are in registers
@@ -732,22 +755,22 @@ k_cop_tc_res2(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__
                         for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
                             const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
                             const uint32_t first = (kb | kk) == 0;
-                            mma_i8_ts(dacc, tmem + Cfg::A0_COL + kb * (Cfg::BK / 4) + kk * 8, bd, idesc_full, !first);
+                            mma_i8_ts_w(dacc, tmem + Cfg::A0_COL + kb * (Cfg::BK / 4) + kk * 8, bd, idesc_full, !first);
                             const uint32_t a1t = tmem + Cfg::A1_COL + kb * (Cfg::BK / 4) + kk * 8;
                             if (!first) {
-                                if (t1) mma_i8_ts(dacc + Cfg::BN, a1t, bd, idesc_full, 1u);
-                                else mma_i8_ss(dacc + Cfg::BN, sdesc_kmajor_sw128(a1s + kk * 32), bd, idesc_full, 1u);
+                                if (t1) mma_i8_ts_w(dacc + Cfg::BN, a1t, bd, idesc_full, 1u);
+                                else mma_i8_ss_w(dacc + Cfg::BN, sdesc_kmajor_sw128(a1s + kk * 32), bd, idesc_full, 1u);
                             } else {
                                 // acc_1..3 accumulate onto x_0's first products, acc_4 starts here (kb 0 is in TMEM)
                                 const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (kSW - 1) * Cfg::BN * Cfg::BK + kk * 32);
-                                mma_i8_ts(dacc + Cfg::BN, a1t, bd, idesc_lo, 1u);
-                                mma_i8_ts(dacc + kSW * Cfg::BN, a1t, bd3, idesc_one, 0u);
+                                mma_i8_ts_w(dacc + Cfg::BN, a1t, bd, idesc_lo, 1u);
+                                mma_i8_ts_w(dacc + kSW * Cfg::BN, a1t, bd3, idesc_one, 0u);
                             }
                         }
                     }
-                    mma_commit(&empty[sE]);
+                    mma_commit_w(&empty[sE]);
                 }
-                mma_commit(tfull);
+                mma_commit_w(tfull);
                 TRACE(5 + 4 * ti);
             }
         }
@@ -891,7 +914,7 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // the whole warp, converged: one elected lane issues (warp-uniform operands)
             // ---------------- MMA issuer
             constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, Cfg::SX * Cfg::RT);         // N = 256
             constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (Cfg::SX - 1) * Cfg::RT);     // N = 192
@@ -917,18 +940,18 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
                         for (uint32_t j = 0; j < kSW; j++) {
                             const uint64_t ad = sdesc_kmajor_sw128(a0 + j * Cfg::BM * Cfg::BK + kk * 32);
                             if ((kb | kk) != 0 || j == 0) {
-                                mma_i8_ss(dacc + j * Cfg::RT, ad, bd, idesc_full, (kb | kk) != 0);
+                                mma_i8_ss_w(dacc + j * Cfg::RT, ad, bd, idesc_full, (kb | kk) != 0);
                             } else {
                                 // first k-step, j >= 1: acc_j..acc_{j+SX-2} exist, acc_{j+SX-1} is new
-                                mma_i8_ss(dacc + j * Cfg::RT, ad, bd, idesc_lo, 1u);
+                                mma_i8_ss_w(dacc + j * Cfg::RT, ad, bd, idesc_lo, 1u);
                                 const uint64_t bd3 = sdesc_kmajor_sw128(b0 + (Cfg::SX - 1) * Cfg::RT * Cfg::BK + kk * 32);
-                                mma_i8_ss(dacc + (j + Cfg::SX - 1) * Cfg::RT, ad, bd3, idesc_one, 0u);
+                                mma_i8_ss_w(dacc + (j + Cfg::SX - 1) * Cfg::RT, ad, bd3, idesc_one, 0u);
                             }
                         }
                     }
-                    mma_commit(&empty[s]);
+                    mma_commit_w(&empty[s]);
                 }
-                mma_commit(&tfull[buf]);
+                mma_commit_w(&tfull[buf]);
                 TRACE(5 + 4 * ti);
             }
         }
@@ -1018,6 +1041,7 @@ static cudaError_t launch_sx(nimbus_ctx* c, const nimbus_encw* w, const uint8_t*
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_cop_tc<SX, CL, BN>, c->rns, d_Xt, (const uint8_t*)w->d_Et, k, Mt,
                                        CT, w->KB, ncol, d_C);
     c->launches++;
+    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc<%d, %d, %d>", SX, CL, BN);
     return e;
 }
 
@@ -1032,22 +1056,32 @@ static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t
         e = launch_pdl(k_cop_tc_res2, dim3(grid), dim3(ResCfg2::THREADS), ResCfg2::SMEM, st, c->rns, d_Xt,
                        (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, d_C);
         c->launches++;
+        snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res2");
         return e;
     }
-    {
-        cudaError_t e = ensure_smem(c, k_cop_tc_res<false>, ResCfg::SMEM);
-        if (e != cudaSuccess) return e;
-    }
+    ResJobs J;
+    J.nj = 1;
+    J.Et[0] = w->d_Et;
+    J.C[0] = d_C;
+    return launch_res_jobs(c, J, w->KB, d_Xt, k, st);
+}
+
+// the resident-X contraction over up to 4 matmuls sharing X (same m, ell <= 16, k <= 128)
+cudaError_t launch_res_jobs(nimbus_ctx* c, const ResJobs& J, uint32_t KB, const uint8_t* d_Xt, uint32_t k,
+                            cudaStream_t st) {
+    cudaError_t e = ensure_smem(c, k_cop_tc_res<false>, ResCfg::SMEM);
+    if (e != cudaSuccess) return e;
     const uint32_t ncol = 2 * c->rns.L * c->rns.N;
-    const uint32_t CT = col_tiles(c, kBNR);
-    const uint32_t grid = CT < (uint32_t)c->num_sms ? CT : (uint32_t)c->num_sms;
-    cudaError_t e = launch_pdl(k_cop_tc_res<false>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt,
-                               (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, d_C, FuseOut{});
+    const uint32_t CT = col_tiles(c, kBNR), tiles = CT * J.nj;
+    const uint32_t grid = tiles < (uint32_t)c->num_sms ? tiles : (uint32_t)c->num_sms;
+    e = launch_pdl(k_cop_tc_res<false>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt, J, k, CT, KB,
+                   ncol, FuseOut{});
     c->launches++;
+    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<false>");
     return e;
 }
 
-static bool resident_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t k) {
+bool resident_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t k) {
     return w->bn == kBNR && sx_of(c->rns.ell) == 2 && k <= kBM && w->KB <= kResMaxKB;
 }
 
@@ -1065,9 +1099,13 @@ cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8
     const uint32_t CT = col_tiles(c, kBNR), P = CT / 2;       // (component, J-tile) pairs
     const uint32_t grid = P < (uint32_t)c->num_sms ? P : (uint32_t)c->num_sms;
     const FuseOut fo{d_cts, d_R, prg_key(seed, 6), w->n};
-    e = launch_pdl(k_cop_tc_res<true>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt,
-                   (const uint8_t*)w->d_Et, k, CT, w->KB, ncol, (uint32_t*)nullptr, fo);
+    ResJobs J;
+    J.nj = 1;
+    J.Et[0] = w->d_Et;
+    e = launch_pdl(k_cop_tc_res<true>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt, J, k, CT,
+                   w->KB, ncol, fo);
     c->launches++;
+    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<true>");
     return e;
 }
 
@@ -1086,6 +1124,7 @@ static cudaError_t launch_t(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* 
     cudaError_t e = launch_pdl(k_cop_tc_t<SX, RT>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, c->rns, d_Xt,
                                (const uint8_t*)w->d_Et, k, RTt, CT, w->KB, ncol, d_C);
     c->launches++;
+    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_t<%d, %d>", SX, RT);
     return e;
 }
 

@@ -36,6 +36,7 @@ struct nimbus_ctx {
     uint32_t* d_flag = nullptr;    // device error flags (bit 0: input >= t)
     std::string err;
     uint64_t launches = 0;
+    char last_contraction[48] = "";  // name of the last contraction kernel launched (nimbus_last_contraction)
     int num_sms = 148;
     int res_ring = 1;              // resident-X contraction: 1 = 3-slot ring + slice 1 in smem, 2 = deep ring (k_cop_tc_res2); env NIMBUS_RES
     int cluster = 1;               // CTAs per cluster of the streaming contraction (2 = X multicast); env NIMBUS_CLUSTER
@@ -83,6 +84,7 @@ struct nimbus_encw {
     uint32_t m = 0, n = 0, KB = 0; // KB = ceil(m / 128) k-blocks
     uint32_t bn = kBNT;            // tile width (columns) of the resident layout
     uint8_t* d_Et = nullptr;       // tiled byte planes [ct][kb][s][bn][128 swizzled]; null when offloaded
+    uint32_t* d_corr = nullptr;    // packed contraction (cop_pk.cu): corr [2LN] then ColSum [2LN]; stays resident
     uint8_t* h_Et = nullptr;       // pinned host copy of the same bytes (nimbus_encw_offload)
     size_t bytes = 0;
     // file-backed (nimbus_encw_open): canonical payload of a store file, read per streamed matmul
@@ -104,6 +106,32 @@ inline uint32_t elem_bytes(uint32_t ell) { return ell <= 32 ? 4u : 8u; }
 // number of 48-column Enc(W) tiles covering the 2 L N coefficient columns (last one zero padded)
 // (rounded up to an even count so column tiles pair up in 2-CTA clusters)
 inline uint32_t col_tiles(const nimbus_ctx* c, uint32_t bn) { return (((2 * c->rns.L * c->rns.N + bn - 1) / bn) + 1) & ~1u; }
+
+// one matmul of the packed contraction (cop_pk.cu); d_Xp: its packed X slices in the workspace
+struct PkHostJob {
+    const nimbus_encw* w = nullptr;
+    const uint32_t* d_X = nullptr;
+    uint32_t kq = 0, nq = 0;
+    uint64_t seed = 0;
+    uint32_t* d_cts = nullptr;
+    uint32_t* d_R = nullptr;       // null: R not written (the host-buffer call makes it separately)
+    const uint8_t* d_Xp = nullptr;
+};
+
+// the matmuls of one pack launch (same shape; blockIdx.z = comp + 2 job)
+struct PackJobs {
+    const uint32_t* C[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t* cts[4] = {nullptr, nullptr, nullptr, nullptr};
+    void* R[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint64_t key[4] = {0, 0, 0, 0};      // prg_key(mask_seed, 6)
+    uint32_t nj = 0;
+};
+// the matmuls of one resident-X contraction launch (same X, same m: Q / K / V of a layer)
+struct ResJobs {
+    const uint8_t* Et[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t* C[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint32_t nj = 0;
+};
 
 // ---------------------------------------------------------------- launchers
 namespace nimbus {
@@ -137,6 +165,8 @@ cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_X, uint32_t k, uint32_t 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                         uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl,
                         const uint32_t* d_zero = nullptr);
+cudaError_t launch_pack_jobs(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint32_t nq, uint32_t n, cudaStream_t st,
+                             bool pdl, const uint32_t* Z0 = nullptr);
 cudaError_t launch_mask_R(nimbus_ctx* c, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed, void* d_R,
                           cudaStream_t st);
 // cop_cc.cu
@@ -155,8 +185,24 @@ cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_
 // R = 1 fast path of cop_matmul: the resident-X contraction writes the output ciphertexts
 // and R itself (mod-switch + mask fused in its epilogue); fused_r1_ok says when it applies
 bool fused_r1_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t k);
+// the resident-X contraction (ell <= 16, k <= 128, m <= 768) applies to w: resident_ok; several
+// such matmuls sharing X run as one launch (launch_res_jobs)
+bool resident_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t k);
+cudaError_t launch_res_jobs(nimbus_ctx* c, const ResJobs& J, uint32_t KB, const uint8_t* d_Xt, uint32_t k,
+                            cudaStream_t st);
 cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k, uint64_t seed,
                                 uint32_t* d_cts, uint32_t* d_R, cudaStream_t st);
+// cop_pk.cu: the contraction in the packed output layout with ModDown + mask in its epilogue
+bool packed_layout_ok(const nimbus_ctx* c, const nimbus_encw* w);
+bool packed_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t kq, uint32_t nq);
+uint32_t packed_rt(const nimbus_ctx* c, const PkHostJob* jobs, uint32_t count);
+// workspace bytes of one packed job (packed X slices, dropped-limb residues, flags)
+size_t packed_xp_bytes(const nimbus_ctx* c, const nimbus_encw* w, uint64_t ntheta, uint32_t rt);
+size_t packed_job_bytes(const nimbus_ctx* c, const PkHostJob& j, uint32_t rt);
+// d_ctr: a 4-byte device word for the unit dispatch counter (zeroed by the launch itself)
+cudaError_t launch_cop_packed(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t rt, uint32_t* d_ctr,
+                              cudaStream_t st, void (*mark)(nimbus_ctx*, cudaStream_t));
+cudaError_t launch_pk_corr(nimbus_ctx* c, nimbus_encw* w, cudaStream_t st);
 }  // namespace nimbus
 
 // Opt `kernel` into `bytes` of dynamic shared memory on the context's device, once

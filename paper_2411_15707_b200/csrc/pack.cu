@@ -36,10 +36,10 @@ __device__ __forceinline__ unsigned long long gtimer_pack() {
 #define PTRACE_MAX(i) do { } while (0)
 #endif
 
+// blockIdx.z = comp + 2 * job: one launch packs the matmuls of a same-X group (PackJobs, all
+// of one shape) whose contractions ran as one launch (k_cop_tc_res over a job list)
 template <int V, int L, int RB, typename MT = uint32_t>
-__global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
-                                              uint32_t Rr, uint32_t nct, uint64_t key_mask,
-                                              uint32_t* __restrict__ cts, MT* __restrict__ Rout,
+__global__ void __launch_bounds__(128) k_pack(Rns Rn, PackJobs P, uint32_t kq, uint32_t n, uint32_t Rr, uint32_t nct,
                                               const uint32_t* __restrict__ Z0) {
     pdl_trigger();
     PTRACE_MIN(0);
@@ -50,8 +50,10 @@ __global__ void __launch_bounds__(128) k_pack(Rns Rn, const uint32_t* __restrict
     pdl_wait();  // C is produced by the contraction kernel
     PTRACE_MIN(1);
     PTRACE_MAX(2);
+    const uint32_t job = blockIdx.z >> 1;
     if (J < Rn.N)
-        pack_item<V, L, RB, MT>(Rn, C, kq, n, Rr, nct, key_mask, cts, Rout, Z0, blockIdx.y, blockIdx.z, J);
+        pack_item<V, L, RB, MT>(Rn, P.C[job], kq, n, Rr, nct, P.key[job], P.cts[job], static_cast<MT*>(P.R[job]), Z0,
+                                blockIdx.y, blockIdx.z & 1, J);
     PTRACE_MAX(3);
 }
 
@@ -63,35 +65,31 @@ static cudaError_t launch_maybe_pdl(bool pdl, K kernel, dim3 grid, dim3 block, c
 }
 
 template <int V, int RB>
-static cudaError_t launch_vr(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                             uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl, const uint32_t* Z0) {
+static cudaError_t launch_vr(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint32_t nq, uint32_t n, cudaStream_t st,
+                             bool pdl, const uint32_t* Z0) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     const uint32_t per_block = 128 * V;
-    dim3 grid((N + per_block - 1) / per_block, nq * nct, 2);
-    const uint64_t key = prg_key(seed, 6);
-    uint32_t* d_R = static_cast<uint32_t*>(d_Rv);
+    dim3 grid((N + per_block - 1) / per_block, nq * nct, 2 * P.nj);
     switch (c->rns.L) {
-        case 1: return launch_maybe_pdl(pdl, k_pack<V, 1, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
-        case 2: return launch_maybe_pdl(pdl, k_pack<V, 2, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
-        case 3: return launch_maybe_pdl(pdl, k_pack<V, 3, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
-        case 4: return launch_maybe_pdl(pdl, k_pack<V, 4, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
-        case 5: return launch_maybe_pdl(pdl, k_pack<V, 5, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
-        default: return launch_maybe_pdl(pdl, k_pack<V, 6, RB>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 1: return launch_maybe_pdl(pdl, k_pack<V, 1, RB>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
+        case 2: return launch_maybe_pdl(pdl, k_pack<V, 2, RB>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
+        case 3: return launch_maybe_pdl(pdl, k_pack<V, 3, RB>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
+        case 4: return launch_maybe_pdl(pdl, k_pack<V, 4, RB>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
+        case 5: return launch_maybe_pdl(pdl, k_pack<V, 5, RB>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
+        default: return launch_maybe_pdl(pdl, k_pack<V, 6, RB>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
     }
 }
 
 // ell > 32: 64-bit masks and R, one coefficient per thread, L in {4, 5, 6}
 template <int RB>
-static cudaError_t launch_r64(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                              uint32_t* d_cts, void* d_Rv, cudaStream_t st, bool pdl, const uint32_t* Z0) {
+static cudaError_t launch_r64(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint32_t nq, uint32_t n, cudaStream_t st,
+                              bool pdl, const uint32_t* Z0) {
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
-    dim3 grid((N + 127) / 128, nq * nct, 2);
-    const uint64_t key = prg_key(seed, 6);
-    uint64_t* d_R = static_cast<uint64_t*>(d_Rv);
+    dim3 grid((N + 127) / 128, nq * nct, 2 * P.nj);
     switch (c->rns.L) {
-        case 4: return launch_maybe_pdl(pdl, k_pack<1, 4, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
-        case 5: return launch_maybe_pdl(pdl, k_pack<1, 5, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
-        case 6: return launch_maybe_pdl(pdl, k_pack<1, 6, RB, uint64_t>, grid, dim3(128), st, c->rns, d_C, kq, n, Rr, nct, key, d_cts, d_R, Z0);
+        case 4: return launch_maybe_pdl(pdl, k_pack<1, 4, RB, uint64_t>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
+        case 5: return launch_maybe_pdl(pdl, k_pack<1, 5, RB, uint64_t>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
+        case 6: return launch_maybe_pdl(pdl, k_pack<1, 6, RB, uint64_t>, grid, dim3(128), st, c->rns, P, kq, n, Rr, nct, Z0);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -105,26 +103,26 @@ static uint32_t rows_per_batch(uint32_t Rr, uint32_t kq) {
     return 8;
 }
 
-static cudaError_t launch_64(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                             uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl, const uint32_t* Z0) {
+static cudaError_t launch_64(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint32_t nq, uint32_t n, cudaStream_t st,
+                             bool pdl, const uint32_t* Z0) {
     switch (rows_per_batch(c->rns.N / n, kq)) {
-        case 1: return launch_r64<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        case 2: return launch_r64<2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        case 4: return launch_r64<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        case 5: return launch_r64<5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        default: return launch_r64<8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 1: return launch_r64<1>(c, P, kq, nq, n, st, pdl, Z0);
+        case 2: return launch_r64<2>(c, P, kq, nq, n, st, pdl, Z0);
+        case 4: return launch_r64<4>(c, P, kq, nq, n, st, pdl, Z0);
+        case 5: return launch_r64<5>(c, P, kq, nq, n, st, pdl, Z0);
+        default: return launch_r64<8>(c, P, kq, nq, n, st, pdl, Z0);
     }
 }
 
 template <int V>
-static cudaError_t launch_v(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n, uint64_t seed,
-                            uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl, const uint32_t* Z0) {
+static cudaError_t launch_v(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint32_t nq, uint32_t n, cudaStream_t st,
+                            bool pdl, const uint32_t* Z0) {
     switch (rows_per_batch(c->rns.N / n, kq)) {
-        case 1: return launch_vr<V, 1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        case 2: return launch_vr<V, 2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        case 4: return launch_vr<V, 4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        case 5: return launch_vr<V, 5>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
-        default: return launch_vr<V, 8>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        case 1: return launch_vr<V, 1>(c, P, kq, nq, n, st, pdl, Z0);
+        case 2: return launch_vr<V, 2>(c, P, kq, nq, n, st, pdl, Z0);
+        case 4: return launch_vr<V, 4>(c, P, kq, nq, n, st, pdl, Z0);
+        case 5: return launch_vr<V, 5>(c, P, kq, nq, n, st, pdl, Z0);
+        default: return launch_vr<V, 8>(c, P, kq, nq, n, st, pdl, Z0);
     }
 }
 
@@ -161,8 +159,16 @@ cudaError_t launch_mask_R(nimbus_ctx* c, uint32_t kq, uint32_t nq, uint32_t n, u
 
 cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_t nq, uint32_t n,
                         uint64_t seed, uint32_t* d_cts, void* d_R, cudaStream_t st, bool pdl, const uint32_t* Z0) {
+    PackJobs P;
+    P.nj = 1;
+    P.C[0] = d_C; P.cts[0] = d_cts; P.R[0] = d_R; P.key[0] = prg_key(seed, 6);
+    return launch_pack_jobs(c, P, kq, nq, n, st, pdl, Z0);
+}
+
+cudaError_t launch_pack_jobs(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint32_t nq, uint32_t n, cudaStream_t st,
+                             bool pdl, const uint32_t* Z0) {
     if (elem_bytes(c->rns.ell) == 8) {
-        cudaError_t e = launch_64(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+        cudaError_t e = launch_64(c, P, kq, nq, n, st, pdl, Z0);
         c->launches++;
         return e;
     }
@@ -180,9 +186,14 @@ cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_
         const uint32_t v = (uint32_t)atoi(ev);
         if ((v == 1 || v == 2 || v == 4) && n % v == 0) V = v;
     }
-    cudaError_t e = V == 4 ? launch_v<4>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0)
-                  : V == 2 ? launch_v<2>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0)
-                           : launch_v<1>(c, d_C, kq, nq, n, seed, d_cts, d_R, st, pdl, Z0);
+    // vector stores need V * 4-byte aligned outputs: a caller's 4- or 8-byte aligned buffers get V = 1 / 2
+    uintptr_t al = 0;
+    for (uint32_t j = 0; j < P.nj; j++) al |= (uintptr_t)P.cts[j] | (uintptr_t)P.R[j];
+    if (V == 4 && (al & 15)) V = 2;
+    if (V == 2 && (al & 7)) V = 1;
+    cudaError_t e = V == 4 ? launch_v<4>(c, P, kq, nq, n, st, pdl, Z0)
+                  : V == 2 ? launch_v<2>(c, P, kq, nq, n, st, pdl, Z0)
+                           : launch_v<1>(c, P, kq, nq, n, st, pdl, Z0);
     c->launches++;
     return e;
 }

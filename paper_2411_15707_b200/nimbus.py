@@ -61,6 +61,7 @@ _SIGS = {
     "nimbus_prg_words": (C.c_int, [_u64, _u32, _u64, _u64, _vp, _vp]),
     "nimbus_negacyclic_mul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp]),
     "nimbus_launch_count": (_u64, [_vp]),
+    "nimbus_last_contraction": (C.c_char_p, [_vp]),
     "nimbus_cop_workspace_size_batch": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
     "nimbus_cop_matmul_batch": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_profile_enable": (C.c_int, [_vp, C.c_int]),
@@ -637,6 +638,10 @@ def nimbus_negacyclic_mul(ctx: Context, a: torch.Tensor, b: torch.Tensor, stream
 
 def nimbus_launch_count(ctx: Context) -> int:
     return int(lib().nimbus_launch_count(ctx.ptr))
+
+
+def nimbus_last_contraction(ctx: Context) -> str:
+    return lib().nimbus_last_contraction(ctx.ptr).decode()
 
 
 def nimbus_profile_enable(ctx: Context, on: bool = True):

@@ -369,6 +369,103 @@ def test_c5_layer_matmuls(nb, oracle, proj):
     c.check_decrypt(cts, R)
 
 
+# ------------------------------------------------------------------ packed contraction (cop_pk.cu)
+PACKED_CASES = [
+    # N, L, ell, L_out, m, n, kq, nq            R = N/n; theta = nq * ceil(kq/R)
+    (1024, 3, 32, 2, 200, 128, 300, 2),        # R = 8, 76 theta: two theta tiles of 48 (last ragged), ragged m
+    (2048, 3, 32, 2, 600, 256, 190, 3),        # R = 8, 72 theta over 3 queries (tiles cross queries)
+    (2048, 3, 32, 2, 600, 128, 100, 8),        # R = 16: 4 k-blocks per accumulator drain, KB = 5 -> 2 chunks
+    (1024, 4, 32, 2, 300, 384, 100, 1),        # two dropped limbs (L - L_out = 2), R = 2
+    (1024, 3, 32, 2, 129, 1024, 60, 1),        # n = N: R = 1, no wrapped term at all
+    (1024, 3, 32, 2, 200, 128, 416, 2),        # 104 theta = 2 tiles of RT = 52 (4-row accumulator tail chunk)
+    (8192, 3, 32, 2, 257, 768, 500, 1),        # C5 geometry (R = 10, 50 theta, the last one holding 0 of 10 rows... ragged)
+]
+
+
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", PACKED_CASES)
+def test_packed_parity(nb, oracle, monkeypatch, N, L, ell, L_out, m, n, kq, nq):
+    """The packed contraction (the GEMM over K = (shift r, beta) that writes the packed,
+    mod-switched, masked ciphertexts directly; the wrapped terms through the bitwise
+    complement of x and the ColSum correction) is bit-exact vs the oracle, takes 2
+    launches (slice + contraction), and equals the unpacked two-pass path."""
+    c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=7000 + N + m + n, flags=nb.FLAG_LARGE_K)
+    before = nb.nimbus_launch_count(c.ctx)
+    cts, R = c.run()
+    assert nb.nimbus_launch_count(c.ctx) - before == 2, "packed path not taken"
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all(), "output ciphertexts differ"
+    assert (u32(R) == R_o).all(), "client share R differs"
+    c.check_decrypt(cts, R)
+    monkeypatch.setenv("NIMBUS_NO_PACKED", "1")
+    c2 = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=7000 + N + m + n, flags=nb.FLAG_LARGE_K,
+              oracle_full=False)
+    before = nb.nimbus_launch_count(c2.ctx)
+    cts2, R2 = c2.run()
+    assert nb.nimbus_launch_count(c2.ctx) - before == 3
+    assert torch.equal(cts, cts2) and torch.equal(R, R2)
+
+
+def test_packed_batch_parity(nb, oracle):
+    """A C5-like job list (Q/up/down shapes at a small N) as ONE packed slice launch
+    and ONE packed contraction launch: every job bit-exact vs the oracle."""
+    N, L, ell, L_out = 2048, 3, 32, 2
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out, flags=nb.FLAG_LARGE_K)
+    pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
+    sk = nb.nimbus_keygen(ctx, 77)
+    s = oracle.keygen(N, 77)
+    shapes = [(200, 256, 256, 2), (160, 256, 1024, 2), (200, 700, 256, 2), (130, 256, 256, 3)]   # >= 48 theta each
+    jobs = []
+    for i, (kq, m, n, nq) in enumerate(shapes):
+        W = ni.gen_W(500 + i, m, n, ell)
+        X = ni.gen_X(600 + i, kq * nq, m, ell)
+        w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W), 500 + i)
+        cts, R = nb.alloc_outputs(ctx, w, kq, nq)
+        jobs.append(dict(encw=w, X=dev_u32(X), k_per_query=kq, n_queries=nq, mask_seed=900 + i, cts=cts, R=R,
+                         W=W, Xh=X))
+    ws = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs), dtype=torch.uint8, device=DEV)
+    before = nb.nimbus_launch_count(ctx)
+    nb.nimbus_cop_matmul_batch(ctx, jobs, ws)
+    nb.nimbus_sync(ctx)
+    assert nb.nimbus_launch_count(ctx) - before == 2
+    for i, j in enumerate(jobs):
+        E = oracle.encrypt_rows(N, L, pr, ell, s, j["W"], 500 + i)
+        cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E, j["Xh"], j["W"].shape[1], j["k_per_query"],
+                                       j["n_queries"], j["mask_seed"])
+        assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all(), f"job {i}"
+
+
+def test_same_x_group_batch_parity(nb, oracle):
+    """Q, K, V of a layer share their input X: in a batch, consecutive jobs with
+    the same X and shape run as ONE slice + ONE resident-X contraction over their three Enc(W)s
+    + ONE pack launch; the output ciphertexts and R of every job are bit-exact vs the oracle,
+    and a following job with its own X (O) takes the per-job path."""
+    N, L, ell, L_out = 4096, 2, 16, 1
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
+    sk = nb.nimbus_keygen(ctx, 55)
+    s = oracle.keygen(N, 55)
+    kq, nq, m, n = 70, 1, 300, 700
+    Xq = ni.gen_X(56, kq * nq, m, ell)
+    Xo = ni.gen_X(57, kq * nq, m, ell)
+    dXq, dXo = dev_u32(Xq), dev_u32(Xo)
+    jobs = []
+    for i in range(4):
+        W = ni.gen_W(560 + i, m, n, ell)
+        w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W), 560 + i)
+        cts, R = nb.alloc_outputs(ctx, w, kq, nq)
+        jobs.append(dict(encw=w, X=dXq if i < 3 else dXo, k_per_query=kq, n_queries=nq, mask_seed=570 + i,
+                         cts=cts, R=R, W=W, Xh=Xq if i < 3 else Xo))
+    ws = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs), dtype=torch.uint8, device=DEV)
+    before = nb.nimbus_launch_count(ctx)
+    nb.nimbus_cop_matmul_batch(ctx, jobs, ws)
+    nb.nimbus_sync(ctx)
+    assert nb.nimbus_launch_count(ctx) - before == 3 + 3, "group (3 launches) + O (3 launches)"
+    for i, j in enumerate(jobs):
+        E = oracle.encrypt_rows(N, L, pr, ell, s, j["W"], 560 + i)
+        cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E, j["Xh"], n, kq, nq, j["mask_seed"])
+        assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all(), f"job {i}"
+
+
 # ------------------------------------------------------------------ errors
 def test_error_codes(nb, oracle):
     ctx = nb.nimbus_ctx_create(1024, 2, 16, 1)
