@@ -74,6 +74,8 @@ def step_dist(step_ms):
 
 
 def get_config(key: str):
+    if key == "2qkv":
+        return ni.CONFIG_QKV
     if key.endswith("l16"):
         return ni.CONFIGS_L16[int(key[0])]
     if key.endswith("l64"):
@@ -87,6 +89,10 @@ def workload_name(cfg):
         l = lays[0]
         return (f"{cfg.name} {l.name}: X {l.k}x{l.m} . W {l.m}x{l.n}, N={cfg.N}, L={cfg.L}, "
                 f"ell={cfg.ell}, L_out={cfg.L_out}")
+    if cfg.shared_x:
+        l = lays[0]
+        return (f"{cfg.name}: {len(lays)} matmuls sharing X ({', '.join(x.name for x in lays)}), each X {l.k}x{l.m} . "
+                f"W {l.m}x{l.n}, N={cfg.N}, L={cfg.L}, ell={cfg.ell}, L_out={cfg.L_out}")
     return (f"{cfg.name} BERT-base linear stack: 12 layers x (4x768x768 + 768x3072 + 3072x768), "
             f"k={lays[0].k} (seq {lays[0].k_per_query} x {lays[0].n_queries} queries), N={cfg.N}, "
             f"L={cfg.L}, ell={cfg.ell}, L_out={cfg.L_out}")
@@ -223,9 +229,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         t_setup += time.perf_counter() - t0
         enc_bytes += nb.nimbus_encw_bytes(encw)
-        # per-rank independent queries (weak scaling): X seeded by rank
+        # per-rank independent queries (weak scaling): X seeded by rank; one X for a shared-X step
         xseed = rank_x_seed(seed, rank)
-        X = to_dev(ni.gen_X(xseed, lay.k, lay.m, cfg.ell), dev)
+        X = mats[0]["X"][0] if (cfg.shared_x and mats) else to_dev(ni.gen_X(xseed, lay.k, lay.m, cfg.ell), dev)
         cts, R = outputs(ctx, encw, lay.k_per_query, lay.n_queries)
         mats.append(dict(lay=lay, seed=seed, encw=[encw], X=[X], W=W, cts=cts, R=R,
                          ws_bytes=nb.nimbus_cop_workspace_size(ctx, encw, lay.k)))
@@ -238,9 +244,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
         n_copies = max(1, -(-3 * l2_bytes // enc_bytes))
         for mt in mats:
             lay = mt["lay"]
-            for _ in range(n_copies - 1):
+            for c in range(n_copies - 1):
                 mt["encw"].append(encrypt(ctx, sk, mt["W"], mt["seed"]))
-                mt["X"].append(mt["X"][0].clone())
+                # a shared-X step keeps one X per copy for all of its matmuls
+                mt["X"].append(mats[0]["X"][c + 1] if (cfg.shared_x and mt is not mats[0]) else mt["X"][0].clone())
     # setup on the device, steady state (allocations excluded): re-encrypt the first
     # matrix into its existing handle (nimbus_encrypt_weights_into: the encrypt and tile
     # kernels and a stream-ordered temporary), CUDA events around the stream work
@@ -750,7 +757,7 @@ def bench_config(args, key, rank, world, local_rank, steps=None, warmup=None, e2
 MAIN_CONFIG = "5"
 # (config, steps cap) of the per_config block: C2 / C3 / C4 at the bench's steps, the paper's ell = 64
 # pass at <= 5 steps (a 27 GB Enc(W), ~0.3 s per pass)
-PER_CONFIG = (("2", None), ("3", None), ("4", None), ("4l64", None), ("5l64", 5))
+PER_CONFIG = (("2", None), ("2qkv", None), ("3", None), ("4", None), ("4l64", None), ("5l64", 5))
 
 
 def main():

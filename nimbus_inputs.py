@@ -80,7 +80,8 @@ class Layer:
 @dataclasses.dataclass(frozen=True)
 class Config:
     """RLWE parameters + workload.  N ring degree, L limbs of 31-bit NTT primes,
-    ell plaintext bits (t = 2^ell), L_out limbs after the mod-switch."""
+    ell plaintext bits (t = 2^ell), L_out limbs after the mod-switch.  shared_x: every
+    matmul of the step multiplies the SAME client share X (Q, K, V of one layer)."""
     cid: int
     name: str
     N: int
@@ -88,6 +89,7 @@ class Config:
     ell: int
     L_out: int
     layers: tuple  # tuple[(layer_idx, proj, Layer)]
+    shared_x: bool = False
 
     @property
     def seed_cfg(self) -> int:
@@ -128,6 +130,11 @@ CONFIGS = {
     4: Config(4, "C4", 8192, 3, 32, 2, _single("ffn_down", 128, 3072, 768)),
     5: Config(5, "C5", 8192, 3, 32, 2, _bert_layer_stack(12, 512, 4)),
 }
+# The three same-X attention projections of one layer at C2's shape (Q, K, V: X 128x768 . W 768x768
+# each), one batched call per step -- the k = 128 stream as the model issues it.
+CONFIG_QKV = Config(2, "C2-QKV", 4096, 2, 16, 1,
+                    tuple((0, p, Layer(f"L0.{_PROJ[p]}", 128, 1, 768, 768)) for p in range(3)), shared_x=True)
+
 # Secondary lines named by SURVEY.md §8(d): C4/C5 at ell=16 (L_out=1).
 CONFIGS_L16 = {
     4: dataclasses.replace(CONFIGS[4], ell=16, L_out=1, name="C4@l16"),

@@ -71,6 +71,27 @@ struct PkParams {
     PkJob job[kPkMaxJobs];
 };
 
+#ifdef NIMBUS_TRACE
+// Debug-only cycle accounting per CTA (tools/pk_stats.py): [0] MMA warp waiting for drained
+// accumulators, [1] waiting for X, [2] waiting for Enc(W), [3] MMA warp total, [4] epilogue in
+// drains, [5] epilogue in finalize, [6] epilogue waiting for accumulators, [7] units,
+// [8] epilogue waiting for flags/rho prefetch, [9] producer waiting for free slots.
+__device__ unsigned long long* g_pk_stats = nullptr;
+extern "C" int nimbus_pk_stats_set(void* p) { return (int)cudaMemcpyToSymbol(g_pk_stats, &p, sizeof(p)); }
+#define PKS_T0(v) const long long v = clock64()
+#define PKS_ADD(i, t0) do { pks[i] += (unsigned long long)(clock64() - (t0)); } while (0)
+#define PKS_INC(i) do { pks[i] += 1ull; } while (0)
+#define PKS_DECL unsigned long long pks[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
+#define PKS_FLUSH do { if (g_pk_stats && lane == 0) for (int i_ = 0; i_ < 12; i_++) if (pks[i_]) \
+        atomicAdd(&g_pk_stats[blockIdx.x * 16 + i_], pks[i_]); } while (0)
+#else
+#define PKS_DECL do { } while (0)
+#define PKS_FLUSH do { } while (0)
+#define PKS_T0(v) do { } while (0)
+#define PKS_ADD(i, t0) do { } while (0)
+#define PKS_INC(i) do { } while (0)
+#endif
+
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                  :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
@@ -106,10 +127,15 @@ struct PkCfg {
     static constexpr uint32_t A_BYTES = kSW * BM * BK;     // 64 KB: 4 planes x 128 columns x 128 B
     static constexpr uint32_t P_BYTES = BM * BK;           // one plane: 16 KB
     static constexpr uint32_t B_BYTES = SX * RT * BK;      // S_x slices x RT rows x 128 B
+#ifdef NIMBUS_PK_E9
+    static constexpr uint32_t ESLOTS = (SX * RT * BK * 3 + 9 * BM * BK + 1024 + 512 <= 232448) ? 9 : 8, XSLOTS = 3;
+#else
     static constexpr uint32_t ESLOTS = 8, XSLOTS = 3;
+#endif
     static constexpr uint32_t OFF_X = ESLOTS * P_BYTES;
     static constexpr uint32_t RING = OFF_X + XSLOTS * B_BYTES;
     static constexpr uint32_t NACC = SX + kSW - 1;
+    static constexpr uint32_t ZCOL = 480;                  // TMEM columns [480, 488): a zero A operand
     static constexpr uint32_t NCHK = (RT + 7) / 8;         // 8-row chunks of an accumulator (the last may hold 4)
     static constexpr uint32_t TAIL = RT - 8 * (NCHK - 1);  // rows of the last chunk: 8, or 4 (RT = 52)
     static constexpr uint32_t CPT0 = (NCHK + 1) / 2;       // chunks of the first epilogue half
@@ -118,25 +144,27 @@ struct PkCfg {
     static constexpr size_t SMEM = (size_t)RING + 1024 + 512;     // alignment slack + barriers, queue
     static_assert(RT % 4 == 0 && (TAIL == 8 || TAIL == 4), "8-row chunks, a 4-row tail at most");
     static_assert((SX * RT) % 16 == 0 && SX * RT <= 256, "MMA N");
-    static_assert(NACC * RT <= 512, "TMEM");
+    static_assert(NACC * RT <= ZCOL && 3 * RT + SX * RT <= ZCOL, "TMEM: accumulators below the zero operand");
     static_assert(B_BYTES % 1024 == 0, "swizzle atoms");
     static_assert(SMEM <= 232448, "shared memory");
 };
 
-// unit u -> (job, limb pass, component, theta tile, J tile); T fastest so that the CTAs
-// in flight read neighbouring Enc(W) tiles of one (component, limb) slab
+// cluster-unit u -> (job, limb pass, component, group of CL theta tiles, J tile); T fastest so
+// that the clusters in flight read neighbouring Enc(W) tiles of one (component, limb) slab.
+// The CL CTAs of a cluster take theta tiles g CL + rank of the same (job, pass, comp, T): they
+// consume the same Enc(W) planes in lockstep, each plane fetched once and multicast to all.
 struct PkUnit {
     uint32_t j, pass, comp, tt, T;
 };
-__device__ __forceinline__ PkUnit pk_decode(const PkParams& P, uint32_t u, uint32_t NT) {
+__device__ __forceinline__ PkUnit pk_decode(const PkParams& P, uint32_t u, uint32_t NT, uint32_t CL, uint32_t rank) {
     PkUnit x;
     uint32_t j = 0;
     while (u >= P.job[j].unit_end) j++;
     uint32_t v = u - (j ? P.job[j - 1].unit_end : 0u);
-    const uint32_t TT = P.job[j].TT;
+    const uint32_t G = (P.job[j].TT + CL - 1) / CL;
     x.j = j;
     x.T = v % NT; v /= NT;
-    x.tt = v % TT; v /= TT;
+    x.tt = (v % G) * CL + rank; v /= G;
     x.comp = v & 1;
     x.pass = v >> 1;
     return x;
@@ -147,7 +175,32 @@ __device__ __forceinline__ uint32_t pk_limb(const Rns& R, uint32_t pass) {
     return pass < nd ? R.L - 1 - pass : pass - nd;
 }
 
-template <int SX, int RT>
+// mbarrier wait with cluster-scope acquire (the phase may be completed by the peer CTA)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONEC_%=;\n\t"
+        "bra WAITC_%=;\n\t"
+        "DONEC_%=:\n\t}"
+        :: "r"(smem_u32(bar)), "r"(parity), "r"(0x989680) : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_cl(uint32_t saddr, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(cta));
+    return r;
+}
+// arrive on the mbarrier at the same offset in CTA `cta` of the cluster (release, cluster scope)
+__device__ __forceinline__ void mbar_arrive_cl(uint64_t* bar, uint32_t cta) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(mapa_cl(smem_u32(bar), cta))
+                 : "memory");
+}
+__device__ __forceinline__ void st_cl_u32(uint32_t* p, uint32_t cta, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(mapa_cl(smem_u32(p), cta)), "r"(v) : "memory");
+}
+
+template <int SX, int RT, int CL>
 __global__ void __launch_bounds__(PkCfg<SX, RT>::THREADS, 1)
 k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint32_t total_units) {
     using Cfg = PkCfg<SX, RT>;
@@ -165,39 +218,67 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
     uint32_t* tmem_slot = unit_q + kPkQ;
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CL > 1 ? cluster_ctarank() : 0;
+    PKS_DECL;
     const uint32_t N = R.N, NT = N / Cfg::BM, L = R.L, ND = R.L - R.L_out;
+    constexpr uint32_t MASK = (1u << CL) - 1;
     if (warp == 0 && lane == 0) {
-        for (uint32_t s = 0; s < Cfg::ESLOTS; s++) { mbar_init(&efull[s], 1); mbar_init(&eempty[s], 1); }
+        for (uint32_t s = 0; s < Cfg::ESLOTS; s++) { mbar_init(&efull[s], 1); mbar_init(&eempty[s], CL); }
         for (uint32_t s = 0; s < Cfg::XSLOTS; s++) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], 1); }
         mbar_init(tfull, 1);
         mbar_init(tempty, Cfg::EPI_WARPS);
-        for (uint32_t q = 0; q < kPkQ; q++) { mbar_init(&qfull[q], 1); mbar_init(&qempty[q], 1 + Cfg::EPI_WARPS); }
+        // unit ids come from the cluster's leader; its queue slot is free once every consumer of
+        // every CTA has read it (MMA warp + epilogue warps, and the peers' producers)
+        for (uint32_t q = 0; q < kPkQ; q++) {
+            mbar_init(&qfull[q], 1);
+            mbar_init(&qempty[q], CL * (1 + Cfg::EPI_WARPS) + (CL - 1));
+        }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
-    __syncthreads();
+    if (CL > 1) cluster_sync(); else __syncthreads();   // the peers' barriers exist before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_trigger();
+    // a consumer takes unit id i: wait, read, release the leader's queue slot
+    auto take_unit = [&](uint32_t i, bool arrive_one) -> uint32_t {
+        const uint32_t q = i % kPkQ;
+        if (CL > 1) mbar_wait_cl(&qfull[q], (i / kPkQ) & 1); else mbar_wait(&qfull[q], (i / kPkQ) & 1);
+        const uint32_t u = unit_q[q];
+        if (arrive_one) {
+            if (CL > 1 && rank != 0) mbar_arrive_cl(&qempty[q], 0); else mbar_arrive(&qempty[q]);
+        }
+        return u;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- producer: fetches units in order; per (kb, r) one Enc(W) block + one X block
+            // ---------------- producer: per (kb, r) the X slices of this CTA's theta tile and the 4 byte
+            // planes of one Enc(W) block (plane jp fetched by CTA jp % CL, multicast to the cluster)
             const uint64_t pol_e = policy_evict_last();    // an Enc(W) block serves R output tiles x theta tiles
             const uint64_t pol_x = policy_evict_last();    // X blocks serve every J tile
             pdl_wait();                                    // X slices, counter and flags: the slice kernel's
-            // every unit, the first included, comes from the counter: a unit is only ever held by a
-            // running CTA, so a flag wait never depends on a CTA that has not been scheduled
-            uint32_t ie = 0, ix = 0, u = atomicAdd(P.ctr, 1u);
+            uint32_t ie = 0, ix = 0;
             for (uint32_t i = 0;; i++) {
-                const uint32_t q = i % kPkQ;
-                if (i >= kPkQ) mbar_wait(&qempty[q], ((i / kPkQ) & 1) ^ 1);
-                unit_q[q] = u;
-                mbar_arrive(&qfull[q]);
+                uint32_t u;
+                if (rank == 0) {
+                    // every unit, the first included, comes from the counter: a unit is only ever held by
+                    // a running cluster, so a flag wait never depends on one that has not been scheduled
+                    u = atomicAdd(P.ctr, 1u);
+                    const uint32_t q = i % kPkQ;
+                    if (i >= kPkQ) mbar_wait(&qempty[q], ((i / kPkQ) & 1) ^ 1);
+                    unit_q[q] = u;
+                    for (uint32_t c = 1; c < (uint32_t)CL; c++) st_cl_u32(&unit_q[q], c, u);
+                    mbar_arrive(&qfull[q]);
+                    for (uint32_t c = 1; c < (uint32_t)CL; c++) mbar_arrive_cl(&qfull[q], c);
+                } else {
+                    u = take_unit(i, true);
+                }
                 if (u >= total_units) break;
-                const PkUnit U = pk_decode(P, u, NT);
+                const PkUnit U = pk_decode(P, u, NT, CL, rank);
                 const PkJob& J = P.job[U.j];
+                const bool ghost = U.tt >= J.TT;                      // a cluster's spare theta tile
                 const uint32_t limb = pk_limb(R, U.pass);
                 const size_t slab = ((size_t)U.comp * L + limb) * NT;
                 const uint32_t shift_t = J.n / Cfg::BM;               // tiles per shift step
@@ -208,24 +289,36 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                         const uint32_t srcT = wrap ? U.T + NT - sh : U.T - sh;
                         {   // X slices of (r, kb)
                             const uint32_t s = ix % Cfg::XSLOTS, ph = (ix / Cfg::XSLOTS) & 1;
-                            if (ix >= Cfg::XSLOTS) mbar_wait(&xempty[s], ph ^ 1);
+                            if (ix >= Cfg::XSLOTS) { PKS_T0(t0); mbar_wait(&xempty[s], ph ^ 1); PKS_ADD(10, t0); }
                             ix++;
-                            mbar_arrive_expect_tx(&xfull[s], Cfg::B_BYTES);
-                            bulk_g2s(smem + Cfg::OFF_X + s * Cfg::B_BYTES,
-                                     J.Xp + ((((size_t)(2 * r + (wrap ? 1 : 0)) * J.TT + U.tt) * J.KB + kb) *
-                                             Cfg::B_BYTES),
-                                     Cfg::B_BYTES, &xfull[s], pol_x);
+                            if (ghost) {
+                                mbar_arrive(&xfull[s]);
+                            } else {
+                                mbar_arrive_expect_tx(&xfull[s], Cfg::B_BYTES);
+                                bulk_g2s(smem + Cfg::OFF_X + s * Cfg::B_BYTES,
+                                         J.Xp + ((((size_t)(2 * r + (wrap ? 1 : 0)) * J.TT + U.tt) * J.KB + kb) *
+                                                 Cfg::B_BYTES),
+                                         Cfg::B_BYTES, &xfull[s], pol_x);
+                            }
                         }
                         const uint8_t* eb = J.Et + ((slab + srcT) * J.KB + kb) * Cfg::A_BYTES;
                         for (uint32_t jp = 0; jp < kSW; jp++, ie++) {   // the 4 byte planes of the Enc(W) block
                             const uint32_t s = ie % Cfg::ESLOTS, ph = (ie / Cfg::ESLOTS) & 1;
-                            if (ie >= Cfg::ESLOTS) mbar_wait(&eempty[s], ph ^ 1);
+                            // the slot is free in every CTA of the cluster (CL commits)
+                            if (ie >= Cfg::ESLOTS) {
+                                PKS_T0(t0);
+                                if (CL > 1) mbar_wait_cl(&eempty[s], ph ^ 1); else mbar_wait(&eempty[s], ph ^ 1);
+                                PKS_ADD(9, t0);
+                            }
                             mbar_arrive_expect_tx(&efull[s], Cfg::P_BYTES);
-                            bulk_g2s(smem + s * Cfg::P_BYTES, eb + jp * Cfg::P_BYTES, Cfg::P_BYTES, &efull[s], pol_e);
+                            if (CL == 1)
+                                bulk_g2s(smem + s * Cfg::P_BYTES, eb + jp * Cfg::P_BYTES, Cfg::P_BYTES, &efull[s], pol_e);
+                            else if (jp % CL == rank)
+                                bulk_g2s_mc(smem + s * Cfg::P_BYTES, eb + jp * Cfg::P_BYTES, Cfg::P_BYTES, &efull[s],
+                                            MASK, pol_e);
                         }
                     }
                 }
-                u = atomicAdd(P.ctr, 1u);
             }
         }
     } else if (warp == 1) {
@@ -237,34 +330,50 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         const uint64_t x_desc0 = sdesc_kmajor_sw128(smem_u32(smem + Cfg::OFF_X));
         constexpr uint64_t EP = Cfg::P_BYTES >> 4, XP = Cfg::B_BYTES >> 4;
         uint32_t ie = 0, ix = 0, gc = 0;
+        PKS_T0(t_mma0);
         for (uint32_t i = 0;; i++) {
-            const uint32_t q = i % kPkQ;
-            mbar_wait(&qfull[q], (i / kPkQ) & 1);
-            const uint32_t u = unit_q[q];
+            const uint32_t u = take_unit(i, false);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&qempty[q]);
-            if (u >= total_units) break;
-            const PkUnit U = pk_decode(P, u, NT);
+            if (lane == 0) {
+                if (CL > 1 && rank != 0) mbar_arrive_cl(&qempty[i % kPkQ], 0); else mbar_arrive(&qempty[i % kPkQ]);
+            }
+            if (u >= total_units) { PKS_ADD(3, t_mma0); break; }
+            PKS_INC(7);
+            const PkUnit U = pk_decode(P, u, NT, CL, rank);
             const uint32_t KB = P.job[U.j].KB, Rr = P.job[U.j].Rr, CKB = P.job[U.j].CKB, NCH = P.job[U.j].NCH;
+            const bool ghost = U.tt >= P.job[U.j].TT;
             for (uint32_t c = 0; c < NCH; c++, gc++) {
-                mbar_wait(tempty, gc & 1);           // accumulators drained (and zeroed)
+                { PKS_T0(t0); mbar_wait(tempty, gc & 1); PKS_ADD(0, t0); }   // accumulators drained (and zeroed)
                 tc_fence_after();
                 const uint32_t kb1 = min(KB, (c + 1) * CKB);
                 for (uint32_t kb = c * CKB; kb < kb1; kb++) {
                     for (uint32_t r = 0; r < Rr; r++, ix++) {
                         const uint32_t xs = ix % Cfg::XSLOTS;
-                        mbar_wait(&xfull[xs], (ix / Cfg::XSLOTS) & 1);
+                        { PKS_T0(t0); mbar_wait(&xfull[xs], (ix / Cfg::XSLOTS) & 1); PKS_ADD(1, t0); }
                         const uint64_t bd = x_desc0 + xs * XP;
+                        // a chunk starts from zero accumulators without a TMEM clear: 0 . X (A = the zero
+                        // operand in TMEM) sets acc_3..acc_6, plane 0's first MMA (no accumulate) sets acc_0..3
+                        const bool first = kb == c * CKB && r == 0;
+                        if (first && !ghost) mma_i8_ts_w(tmem + 3 * RT, tmem + Cfg::ZCOL, bd, idesc, 0u);
 #pragma unroll
                         for (uint32_t jp = 0; jp < kSW; jp++, ie++) {
                             const uint32_t es = ie % Cfg::ESLOTS;
-                            mbar_wait(&efull[es], (ie / Cfg::ESLOTS) & 1);
+                            {
+                                PKS_T0(t0);
+                                if (CL > 1) mbar_wait_cl(&efull[es], (ie / Cfg::ESLOTS) & 1);
+                                else mbar_wait(&efull[es], (ie / Cfg::ESLOTS) & 1);
+                                PKS_ADD(2, t0);
+                            }
                             tc_fence_after();
                             const uint64_t ad = e_desc0 + es * EP;
+                            if (!ghost) {
 #pragma unroll
-                            for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
-                                mma_i8_ss_w(tmem + jp * RT, ad + 2 * kk, bd + 2 * kk, idesc, 1u);
-                            mma_commit_w(&eempty[es]);      // this plane's slot is free once its MMAs retire
+                                for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
+                                    mma_i8_ss_w(tmem + jp * RT, ad + 2 * kk, bd + 2 * kk, idesc,
+                                                (first && jp == 0 && kk == 0) ? 0u : 1u);
+                            }
+                            // this plane's slot is free (in every CTA of the cluster) once its MMAs retire
+                            if (CL > 1) mma_commit_mc_w(&eempty[es], MASK); else mma_commit_w(&eempty[es]);
                         }
                         mma_commit_w(&xempty[xs]);
                     }
@@ -282,17 +391,8 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         const uint32_t tl = tmem + ((sub * 32) << 16);
         const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         pdl_wait();          // flags / rho / outputs: after the slice kernel (and the stream's earlier work)
-        // zero the accumulators once; afterwards every drain re-zeroes what it read
-#pragma unroll
-        for (uint32_t ci = 0; ci < CPT; ci++)
-            if (ci < nch) {
-                const bool t4 = Cfg::TAIL == 4 && ch0 + ci == Cfg::NCHK - 1;   // 4 columns: the next acc starts
-#pragma unroll
-                for (uint32_t s = 0; s < Cfg::NACC; s++) {
-                    if (t4) tmem_st4(tl + s * RT + (ch0 + ci) * 8, zero8);
-                    else tmem_st8(tl + s * RT + (ch0 + ci) * 8, zero8);
-                }
-            }
+        // the zero A operand (8 columns x 128 lanes) the MMA issuer starts every chunk with
+        if (half == 0) tmem_st8(tl + Cfg::ZCOL, zero8);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -301,19 +401,47 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         uint32_t acc[CPT][8];        // running residue of the unit's limb (mod p_limb)
         uint32_t gc = 0;
         for (uint32_t i = 0;; i++) {
-            const uint32_t q = i % kPkQ;
-            mbar_wait(&qfull[q], (i / kPkQ) & 1);
-            const uint32_t u = unit_q[q];
+            const uint32_t u = take_unit(i, false);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&qempty[q]);
+            if (lane == 0) {
+                if (CL > 1 && rank != 0) mbar_arrive_cl(&qempty[i % kPkQ], 0); else mbar_arrive(&qempty[i % kPkQ]);
+            }
             if (u >= total_units) break;
-            const PkUnit U = pk_decode(P, u, NT);
+            const PkUnit U = pk_decode(P, u, NT, CL, rank);
             const PkJob& J = P.job[U.j];
+            const bool ghost = U.tt >= J.TT;
             const uint32_t Jc = U.T * Cfg::BM + sub * 32 + lane;         // output coefficient
             const uint32_t limb = pk_limb(R, U.pass);
             const uint32_t p = R.p[limb], c32 = R.c32[limb];
+            // the finalize's operands are fetched before the drains, so their L2 latency hides under
+            // the MMAs: the complement correction, and -- for a pass after a dropped limb -- its flag
+            // and centred residues
+            const uint32_t ndep = (U.pass < ND ? U.pass : ND) * (ghost ? 0 : 1);   // dropped limbs it depends on
+            const size_t fl_tile = ((size_t)U.comp * J.TT + U.tt) * NT + U.T;
+            const size_t fl_stride = (size_t)2 * J.TT * NT;
+            const size_t rho_stride = (size_t)J.TT * RT * 2 * N;
+            PKS_T0(t_pre);
+            const uint32_t cr = __ldg(J.corr + ((size_t)U.comp * L + limb) * N + Jc);
+            int32_t rh0[CPT][8];
+            if (ndep) {
+                if (ew == 0 && lane == 0) {
+                    for (uint32_t d = 0; d < ndep; d++)
+                        while (ld_acquire(J.flags + d * fl_stride + fl_tile) == 0) __nanosleep(64);
+                }
+                epi_bar();
+#pragma unroll
+                for (uint32_t ci = 0; ci < CPT; ci++)
+#pragma unroll
+                    for (uint32_t qq = 0; qq < 8; qq++) {
+                        const uint32_t row = (ch0 + ci) * 8 + qq;
+                        rh0[ci][qq] = (ci < nch && row < (uint32_t)RT)
+                                          ? __ldcg(J.rho + ((size_t)(U.tt * RT + row) * 2 + U.comp) * N + Jc) : 0;
+                    }
+            }
+            PKS_ADD(8, t_pre);
             for (uint32_t c = 0; c < J.NCH; c++, gc++) {
-                mbar_wait(tfull, gc & 1);
+                { PKS_T0(t0); mbar_wait(tfull, gc & 1); PKS_ADD(6, t0); }
+                PKS_T0(t_dr);
                 tc_fence_after();
 #pragma unroll
                 for (uint32_t ci = 0; ci < CPT; ci++) {
@@ -323,80 +451,84 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                     const bool t4 = Cfg::TAIL == 4 && ch0 + ci == Cfg::NCHK - 1;
                     if (t4) {
 #pragma unroll
-                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld4(tl + s * RT + col, v[s]);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_st4(tl + s * RT + col, zero8);
+                        for (uint32_t s2 = 0; s2 < Cfg::NACC; s2++) tmem_ld4(tl + s2 * RT + col, v[s2]);
                     } else {
 #pragma unroll
-                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld8(tl + s * RT + col, v[s]);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_st8(tl + s * RT + col, zero8);
+                        for (uint32_t s2 = 0; s2 < Cfg::NACC; s2++) tmem_ld8(tl + s2 * RT + col, v[s2]);
                     }
+                    tmem_ld_wait();
 #pragma unroll
                     for (uint32_t qq = 0; qq < 8; qq++) {
                         uint64_t x = mad_wide(v[1][qq], 1u << 8, v[0][qq]);
                         x = mad_wide(v[2][qq], 1u << 16, x);
                         x = mad_wide(v[3][qq], 1u << 24, x);
 #pragma unroll
-                        for (uint32_t s = 4; s < Cfg::NACC; s++) x = mad_wide(v[s][qq], R.pow8[limb][s], x);
+                        for (uint32_t s2 = 4; s2 < Cfg::NACC; s2++) x = mad_wide(v[s2][qq], R.pow8[limb][s2], x);
                         const uint32_t red = reduce64_pm(x, p, c32);
                         acc[ci][qq] = c == 0 ? red : addmod(acc[ci][qq], red, p);
                     }
                 }
-                tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(tempty);     // the MMA issuer may start the next chunk
+                PKS_ADD(4, t_dr);
             }
-            // ---- the unit's limb is complete: remove the complement offset, then ModDown / mask / store
-            const uint32_t ndep = U.pass < ND ? U.pass : ND;          // dropped limbs this pass depends on
-            const size_t fl_tile = ((size_t)U.comp * J.TT + U.tt) * NT + U.T;
-            const size_t fl_stride = (size_t)2 * J.TT * NT;
-            if (ndep) {
-                if (ew == 0 && lane == 0) {
-                    for (uint32_t d = 0; d < ndep; d++)
-                        while (ld_acquire(J.flags + d * fl_stride + fl_tile) == 0) __nanosleep(200);
-                }
-                epi_bar();
-            }
-            const uint32_t cr = J.corr[((size_t)U.comp * L + limb) * N + Jc];
-            const size_t rho_stride = (size_t)J.TT * RT * 2 * N;
+            if (ghost) continue;
+            PKS_T0(t_fin);
+            // ---- the unit's limb is complete: remove the complement offset, then ModDown / mask / store.
+            // Everything per row is incremental (this thread's rows are consecutive packed ciphertexts
+            // tg of one column J): the mask PRG counter steps by gamma N.
+            const uint32_t tg0 = U.tt * RT + ch0 * 8;
+            const bool out_pass = U.pass >= ND, masked = out_pass && U.comp == 0;
+            const uint64_t gN = 0x9E3779B97F4A7C15ULL * (uint64_t)N;
+            uint64_t z = J.key + 0x9E3779B97F4A7C15ULL * ((uint64_t)tg0 * N + Jc + 1);
+            const uint32_t ri = Jc / J.n, jj = Jc - ri * J.n;             // R column of this J (valid if ri < R)
+            const bool r_col = masked && limb == 0 && J.Rout && ri < J.Rr;
+            const uint32_t qy = tg0 / J.nct, th = tg0 - qy * J.nct;
+            const uint32_t inv0 = ND ? R.inv_p[L - 1][limb] : 0, inv0_sh = ND ? R.inv_p_sh[L - 1][limb] : 0;
+            uint32_t* ctsp = J.cts + (((size_t)tg0 * 2 + U.comp) * R.L_out + limb) * N + Jc;
+            const size_t cts_row = (size_t)2 * R.L_out * N;
 #pragma unroll
             for (uint32_t ci = 0; ci < CPT; ci++) {
                 if (ci >= nch) continue;
 #pragma unroll
-                for (uint32_t qq = 0; qq < 8; qq++) {
+                for (uint32_t qq = 0; qq < 8; qq++, z += gN) {
                     const uint32_t row = (ch0 + ci) * 8 + qq;
                     if (row >= (uint32_t)RT) continue;                            // past a 4-row tail
-                    const uint32_t tg = U.tt * RT + row;                          // packed ciphertext (global)
-                    const size_t ridx = ((size_t)tg * 2 + U.comp) * N + Jc;
+                    const uint32_t k_row = ci * 8 + qq;                          // row within this thread's rows
+                    const uint32_t tg = tg0 + k_row;                              // packed ciphertext (global)
                     uint32_t v = submod(acc[ci][qq], cr, p);
                     // earlier dropped limbs: v <- (v - rho_d) p_{L-1-d}^-1 mod p   (|rho| < p_l / 2 < p)
-                    for (uint32_t d = 0; d < ndep; d++) {
-                        const uint32_t ld = L - 1 - d;
-                        const int32_t rh = __ldcg(J.rho + d * rho_stride + ridx);
+                    if (ndep) {
+                        const int32_t rh = rh0[ci][qq];
                         const uint32_t t = rh < 0 ? addmod(v, (uint32_t)(-rh), p) : submod(v, (uint32_t)rh, p);
-                        v = mulmod_shoup(t, R.inv_p[ld][limb], R.inv_p_sh[ld][limb], p);
+                        v = mulmod_shoup(t, inv0, inv0_sh, p);
+                        for (uint32_t d = 1; d < ndep; d++) {
+                            const uint32_t ld = L - 1 - d;
+                            const int32_t rh1 = __ldcg(J.rho + d * rho_stride + ((size_t)tg * 2 + U.comp) * N + Jc);
+                            const uint32_t t1 = rh1 < 0 ? addmod(v, (uint32_t)(-rh1), p) : submod(v, (uint32_t)rh1, p);
+                            v = mulmod_shoup(t1, R.inv_p[ld][limb], R.inv_p_sh[ld][limb], p);
+                        }
                     }
-                    if (U.pass < ND) {
+                    if (!out_pass) {
                         // a dropped limb: keep its centred residue for the later passes
-                        __stcg(J.rho + U.pass * rho_stride + ridx, v > (p >> 1) ? (int32_t)v - (int32_t)p : (int32_t)v);
+                        __stcg(J.rho + U.pass * rho_stride + ((size_t)tg * 2 + U.comp) * N + Jc,
+                               v > (p >> 1) ? (int32_t)v - (int32_t)p : (int32_t)v);
                         continue;
                     }
                     if (tg >= J.ntheta) continue;
-                    if (U.comp == 0) {
-                        const uint32_t rm = (uint32_t)(prg_word(J.key, (uint64_t)tg * N + Jc) >> (64 - R.ell));
+                    if (masked) {
+                        const uint32_t rm = (uint32_t)(mix64(z) >> (64 - R.ell));       // word(seed, 6, tg N + J)
                         v = submod(v, emb_fast(rm, (uint32_t)R.qout_mod_t, R.ell, p, R.t_inv[limb], R.t_inv_sh[limb]), p);
-                        if (limb == 0 && J.Rout) {
-                            const uint32_t qy = tg / J.nct, th = tg - qy * J.nct;
-                            const uint32_t ri = Jc / J.n, jj = Jc - ri * J.n;
-                            if (ri < J.Rr && th * J.Rr + ri < J.kq)
-                                J.Rout[((size_t)qy * J.kq + th * J.Rr + ri) * J.n + jj] = rm;
+                        if (r_col) {
+                            // theta of query qy: row theta R + ri of that query, if it exists
+                            const uint32_t thr = th + k_row, qd = thr / J.nct;        // k_row < 32: one division
+                            const uint32_t th2 = thr - qd * J.nct;
+                            if (th2 * J.Rr + ri < J.kq)
+                                J.Rout[((size_t)(qy + qd) * J.kq + th2 * J.Rr + ri) * J.n + jj] = rm;
                         }
                     }
-                    J.cts[(((size_t)tg * 2 + U.comp) * R.L_out + limb) * N + Jc] = v;
+                    ctsp[(size_t)k_row * cts_row] = v;
                 }
             }
             if (U.pass < ND) {
@@ -404,10 +536,12 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                 epi_bar();
                 if (ew == 0 && lane == 0) st_release(J.flags + U.pass * fl_stride + fl_tile, 1u);
             }
+            PKS_ADD(5, t_fin);
         }
     }
+    PKS_FLUSH;
     tc_fence_before();
-    __syncthreads();
+    if (CL > 1) cluster_sync(); else __syncthreads();   // no CTA leaves while a peer may still multicast into it
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -590,14 +724,47 @@ size_t packed_job_bytes(const nimbus_ctx* c, const PkHostJob& j, uint32_t rt) {
     return pk_bytes(c, j.w, (uint64_t)j.nq * pk_nct(c, j.w, j.kq), rt).total;
 }
 
-template <int RT>
+// clusters of CL CTAs that can be co-resident (one CTA per SM), cached per kernel
+template <typename K>
+static uint32_t max_clusters(nimbus_ctx* c, K kernel, uint32_t CL, size_t smem, uint32_t threads) {
+    if (CL == 1) return (uint32_t)c->num_sms;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * (c->num_sms / CL));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        return (uint32_t)c->num_sms / CL;
+    }
+    return (uint32_t)n;
+}
+
+// CTAs per cluster of the packed contraction: 2 (Enc(W) planes multicast to a theta-tile pair)
+// unless NIMBUS_PK_CL=1
+static uint32_t pk_cluster() {
+    const char* e = getenv("NIMBUS_PK_CL");
+    return e && atoi(e) == 1 ? 1 : 2;
+}
+
+template <int RT, int CL>
 static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
                                 void (*mark)(nimbus_ctx*, cudaStream_t)) {
     using Cfg = PkCfg<4, RT>;
     std::unique_ptr<PkParams> Pp(new PkParams());     // kernel parameters (copied at launch)
     PkParams& P = *Pp;
-    cudaError_t e = ensure_smem(c, k_cop_pk<4, RT>, Cfg::SMEM);
+    cudaError_t e = ensure_smem(c, k_cop_pk<4, RT, CL>, Cfg::SMEM);
     if (e != cudaSuccess) return e;
+    static uint32_t ncl_cache[2][4] = {{0}};
+    uint32_t& ncl = ncl_cache[CL - 1][RT == 48 ? 0 : RT == 52 ? 1 : RT == 56 ? 2 : 3];
+    if (!ncl) ncl = max_clusters(c, k_cop_pk<4, RT, CL>, CL, Cfg::SMEM, Cfg::THREADS);
     const uint32_t NT = c->rns.N / kBNW, ND = c->rns.L - c->rns.L_out;
     for (uint32_t base = 0; base < count; base += kPkMaxJobs) {
         const uint32_t nj = count - base < kPkMaxJobs ? count - base : kPkMaxJobs;
@@ -621,7 +788,7 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
             J.rho = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp);
             J.flags = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp + b.rho);
             J.nflags = ND * 2 * J.TT * NT;
-            units += c->rns.L * 2 * J.TT * NT;
+            units += c->rns.L * 2 * ((J.TT + CL - 1) / CL) * NT;    // cluster units
             J.unit_end = units;
             const uint32_t items = 2 * J.Rr * J.TT * RT * J.KB * 8;
             blocks += ((items > J.nflags ? items : J.nflags) + 255) / 256;
@@ -632,21 +799,42 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
         c->launches++;
         if (e != cudaSuccess) return e;
         if (mark) mark(c, st);
-        const uint32_t grid = units < (uint32_t)c->num_sms ? units : (uint32_t)c->num_sms;
-        e = launch_pdl(k_cop_pk<4, RT>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, c->rns, P, units);
+        const uint32_t clusters = units < ncl ? units : ncl;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(clusters * CL);
+        cfg.blockDim = dim3(Cfg::THREADS);
+        cfg.dynamicSmemBytes = Cfg::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = CL;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        e = cudaLaunchKernelEx(&cfg, k_cop_pk<4, RT, CL>, c->rns, P, units);
         c->launches++;
-        snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_pk<4, %d>", RT);
+        snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_pk<4, %d, %d>", RT, CL);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }
 
+template <int RT>
+static cudaError_t launch_pk_cl(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
+                                void (*mark)(nimbus_ctx*, cudaStream_t)) {
+    return pk_cluster() == 2 ? launch_pk_rt<RT, 2>(c, jobs, count, d_ctr, st, mark)
+                             : launch_pk_rt<RT, 1>(c, jobs, count, d_ctr, st, mark);
+}
+
 cudaError_t launch_cop_packed(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t rt, uint32_t* d_ctr,
                               cudaStream_t st, void (*mark)(nimbus_ctx*, cudaStream_t)) {
-    if (rt == 48) return launch_pk_rt<48>(c, jobs, count, d_ctr, st, mark);
-    if (rt == 52) return launch_pk_rt<52>(c, jobs, count, d_ctr, st, mark);
-    if (rt == 56) return launch_pk_rt<56>(c, jobs, count, d_ctr, st, mark);
-    return launch_pk_rt<64>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 48) return launch_pk_cl<48>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 52) return launch_pk_cl<52>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 56) return launch_pk_cl<56>(c, jobs, count, d_ctr, st, mark);
+    return launch_pk_cl<64>(c, jobs, count, d_ctr, st, mark);
 }
 
 // ColSum -> corr for a freshly tiled Enc(W) (every path that fills w->d_Et)

@@ -4,6 +4,7 @@
 // on resident operands; reports cycles per MMA and the implied int8 TOPS.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mma_bench tools/mma_bench.cu
 #include <cstdio>
+#include <string>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../paper_2411_15707_b200/csrc/common.cuh"
@@ -188,16 +189,225 @@ void run(int sms) {
     const double ops = 2.0 * 128 * N * 32 * mmas * sms;
     printf("N=%3u  %6.1f cycles/MMA (floor %5.1f)  %7.1f TOPS over %.3f ms  %s\n", N, cyc / mmas, 128.0 * N / 256.0,
            ops / (ms * 1e-3) / 1e12, ms, cudaGetErrorString(err));
+    printf("JSON {\"n\": %u, \"cycles_per_mma\": %.2f, \"tops\": %.1f}\n", N, cyc / mmas, ops / (ms * 1e-3) / 1e12);
     cudaFree(d);
 }
 
-int main() {
+
+// The packed contraction's MMA pattern: per "k-step", for each of 4 planes (A = 16 KB plane
+// buffer), 4 MMAs (kk) into D at column plane * STRIDE with N columns -- consecutive planes'
+// accumulator ranges overlap when STRIDE < N -- and, if COMMIT, a tcgen05.commit per plane.
+// Issued by one converged warp (elect.sync), like k_cop_pk.
+template <uint32_t N, uint32_t STRIDE, bool COMMIT>
+__global__ void __launch_bounds__(128, 1) k_mma3(uint32_t iters, unsigned long long* cycles) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* A = smem;                 // 4 planes x 128 rows x 128 B
+    uint8_t* B = smem + 65536;         // N rows x 128 B (<= 32 KB)
+    __shared__ uint64_t bar, pbar[4];
+    __shared__ uint32_t tslot;
+    for (uint32_t i = threadIdx.x; i < (65536 + 32768) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(smem)[i] = i * 2654435761u;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int p = 0; p < 4; p++) mbar_init(&pbar[p], 1); fence_mbar_init(); }
+    if (threadIdx.x < 32) tmem_alloc(&tslot, 512);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (threadIdx.x < 32) {
+        constexpr uint32_t idesc = idesc_i8(128, N);
+        const uint64_t ad0 = sdesc_kmajor_sw128(smem_u32(A)), bd0 = sdesc_kmajor_sw128(smem_u32(B));
+        long long t0 = clock64();
+        for (uint32_t it = 0; it < iters; it++) {
+#pragma unroll
+            for (uint32_t p = 0; p < 4; p++) {
+#pragma unroll
+                for (uint32_t kk = 0; kk < 4; kk++)
+                    mma_i8_ss_w(tmem + (STRIDE >= 256 ? (p & 1) * 256 : p * STRIDE), ad0 + p * 1024 + 2 * kk, bd0 + 2 * kk, idesc, 1u);
+                if (COMMIT) mma_commit_w(&pbar[p]);
+            }
+        }
+        mma_commit_w(&bar);
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (threadIdx.x == 0) cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+template <uint32_t N, uint32_t STRIDE, bool COMMIT>
+void run3(int sms) {
+    unsigned long long* d;
+    cudaMalloc(&d, sizeof(unsigned long long) * sms);
+    const size_t smem = 65536 + 32768 + 1024;
+    cudaFuncSetAttribute(k_mma3<N, STRIDE, COMMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_mma3<N, STRIDE, COMMIT><<<sms, 128, smem>>>(16, d);
+    const uint32_t iters = 1024;
+    k_mma3<N, STRIDE, COMMIT><<<sms, 128, smem>>>(iters, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long h[256];
+    cudaMemcpy(h, d, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+    double cyc = 0;
+    for (int i = 0; i < sms; i++) cyc += h[i];
+    cyc /= sms;
+    const double mmas = 16.0 * iters;
+    printf("planes N=%3u stride=%3u commit/plane=%d: %6.1f cycles/MMA (floor %5.1f)  %s\n", N, STRIDE, (int)COMMIT,
+           cyc / mmas, 128.0 * N / 256.0, cudaGetErrorString(err));
+    printf("JSON {\"pattern\": \"planes\", \"n\": %u, \"stride\": %u, \"commit\": %d, \"cycles_per_mma\": %.2f}\n", N,
+           STRIDE, (int)COMMIT, cyc / mmas);
+    cudaFree(d);
+}
+
+
+// k_mma3's pattern (N = 208, 4 planes, stride 52) with warp 1 streaming bulk copies of an
+// L2-resident 1 MB buffer into a separate 96 KB of shared memory for as long as the MMA
+// warp runs: does TMA fill traffic into shared memory slow the MMA stream?  CHUNK bytes per
+// copy, DEPTH copies in flight.  Reports cycles per MMA and the fill bandwidth (B/clk).
+template <uint32_t CHUNK, uint32_t DEPTH>
+__global__ void __launch_bounds__(128, 1) k_mma4(uint32_t iters, const uint8_t* gsrc, unsigned long long* cycles,
+                                                 unsigned long long* filled) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* A = smem;                 // 4 planes x 128 rows x 128 B
+    uint8_t* B = smem + 65536;         // 208 rows x 128 B
+    uint8_t* F = smem + 65536 + 32768; // fill target 96 KB
+    __shared__ uint64_t bar, fbar[8];
+    __shared__ uint32_t tslot;
+    __shared__ volatile uint32_t stop;
+    for (uint32_t i = threadIdx.x; i < (65536 + 32768) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(smem)[i] = i * 2654435761u;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int q = 0; q < 8; q++) mbar_init(&fbar[q], 1); stop = 0; fence_mbar_init(); }
+    if (threadIdx.x < 32) tmem_alloc(&tslot, 512);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    if (threadIdx.x < 32) {
+        constexpr uint32_t idesc = idesc_i8(128, 208);
+        const uint64_t ad0 = sdesc_kmajor_sw128(smem_u32(A)), bd0 = sdesc_kmajor_sw128(smem_u32(B));
+        long long t0 = clock64();
+        for (uint32_t it = 0; it < iters; it++) {
+#pragma unroll
+            for (uint32_t p = 0; p < 4; p++)
+#pragma unroll
+                for (uint32_t kk = 0; kk < 4; kk++)
+                    mma_i8_ss_w(tmem + p * 52, ad0 + p * 1024 + 2 * kk, bd0 + 2 * kk, idesc, 1u);
+        }
+        mma_commit_w(&bar);
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (threadIdx.x == 0) { cycles[blockIdx.x] = (unsigned long long)(t1 - t0); stop = 1; }
+    } else if (threadIdx.x == 32) {
+        const uint64_t pol = policy_evict_last();
+        unsigned long long n = 0;
+        uint32_t i = 0;
+        const uint32_t slots = (96u * 1024u) / CHUNK;
+        while (!stop) {
+            const uint32_t q = i % DEPTH;
+            if (i >= DEPTH) mbar_wait(&fbar[q], ((i / DEPTH) - 1) & 1);
+            mbar_arrive_expect_tx(&fbar[q], CHUNK);
+            bulk_g2s(F + (i % slots) * CHUNK, gsrc + ((size_t)(i * 7919u) % (1024u * 1024u / CHUNK)) * CHUNK, CHUNK, &fbar[q], pol);
+            i++;
+            n += CHUNK;
+        }
+        for (uint32_t j = (i > DEPTH ? i - DEPTH : 0); j < i; j++) mbar_wait(&fbar[j % DEPTH], (j / DEPTH) & 1);
+        filled[blockIdx.x] = n;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+template <uint32_t CHUNK, uint32_t DEPTH>
+void run4(int sms, const uint8_t* g) {
+    unsigned long long *d, *f;
+    cudaMalloc(&d, sizeof(unsigned long long) * sms);
+    cudaMalloc(&f, sizeof(unsigned long long) * sms);
+    const size_t smem = 65536 + 32768 + 98304 + 1024;
+    cudaFuncSetAttribute(k_mma4<CHUNK, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_mma4<CHUNK, DEPTH><<<sms, 128, smem>>>(16, g, d, f);
+    const uint32_t iters = 1024;
+    k_mma4<CHUNK, DEPTH><<<sms, 128, smem>>>(iters, g, d, f);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long h[256], hf[256];
+    cudaMemcpy(h, d, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hf, f, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+    double cyc = 0, fb = 0;
+    for (int i = 0; i < sms; i++) { cyc += h[i]; fb += hf[i]; }
+    cyc /= sms; fb /= sms;
+    const double mmas = 16.0 * iters;
+    printf("planes N=208 + fill %5u B x %u in flight: %6.1f cycles/MMA (floor 104.0), fill %.1f B/clk  %s\n", CHUNK,
+           DEPTH, cyc / mmas, fb / cyc, cudaGetErrorString(err));
+    printf("JSON {\"pattern\": \"planes+fill\", \"chunk\": %u, \"depth\": %u, \"cycles_per_mma\": %.2f, \"fill_b_per_clk\": %.2f}\n",
+           CHUNK, DEPTH, cyc / mmas, fb / cyc);
+    cudaFree(d);
+    cudaFree(f);
+}
+
+// back-to-back launches of the N = 256 stream for ~4 s: the kind::i8 rate a long tensor-bound
+// pass sees under the board power limit (the burst figure above is a ~1 ms launch)
+static double sustained_tops(int sms) {
+    unsigned long long* d;
+    cudaMalloc(&d, sizeof(unsigned long long) * sms);
+    const size_t smem = 16384 + 32768 + 1024;
+    const uint32_t iters = 65536;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    k_mma<256><<<sms, 128, smem>>>(64, d);
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    int launches = 0;
+    float ms = 0;
+    do {
+        for (int i = 0; i < 8; i++, launches++) k_mma<256><<<sms, 128, smem>>>(iters, d);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+    } while (ms < 4000.0f);
+    cudaFree(d);
+    const double ops = 2.0 * 128 * 256 * 32 * 4.0 * iters * sms * launches;
+    return ops / (ms * 1e-3) / 1e12;
+}
+
+int main(int argc, char** argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     run<64>(sms);
     run<128>(sms);
     run<192>(sms);
     run<256>(sms);
+    if (argc > 1 && std::string(argv[1]) == "planes") {
+        run3<208, 52, true>(sms);
+        run3<208, 52, false>(sms);
+        run3<208, 0, true>(sms);
+        run3<208, 0, false>(sms);
+        run3<256, 64, false>(sms);
+        run3<256, 0, false>(sms);
+        run3<128, 256, false>(sms);
+        run3<208, 256, false>(sms);
+        uint8_t* g;
+        cudaMalloc(&g, 1 << 20);
+        cudaMemset(g, 3, 1 << 20);
+        run4<4096, 4>(sms, g);
+        run4<8192, 4>(sms, g);
+        run4<16384, 2>(sms, g);
+        run4<16384, 4>(sms, g);
+        run4<16384, 6>(sms, g);
+        run4<32768, 2>(sms, g);
+        run4<32768, 3>(sms, g);
+        run4<49152, 2>(sms, g);
+        run4<65536, 1>(sms, g);
+        return 0;
+    }
+    if (argc > 1) {                 // mma_bench json: burst + sustained N = 256 rates, machine-readable
+        const double sus = sustained_tops(sms);
+        printf("JSON {\"sustained_tops_n256\": %.1f}\n", sus);
+        return 0;
+    }
     uint8_t* g;
     cudaMalloc(&g, 1 << 20);
     cudaMemset(g, 1, 1 << 20);
