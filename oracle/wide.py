@@ -156,3 +156,22 @@ def decrypt_unpack(N, L_out, pr, ell, s, cts, kq, nq, n):
             for rho in range(rows):
                 Z[q_ * kq + th * R_ + rho] = full[q_ * nct + th][rho * n:(rho + 1) * n]
     return Z, full
+
+
+def plain_matmul64(X, W) -> np.ndarray:
+    """The server's W<X>_s at the paper's t = 2^64 (Alg. 1 step 5; ell = 64,
+    PAPER.md:402): the textbook product of the uint64 matrices, whose wrap-around IS the
+    reduction mod 2^64 (Y = X.W, SURVEY.md §8(c) #10 orientation)."""
+    X = np.ascontiguousarray(X, dtype=np.uint64)
+    W = np.ascontiguousarray(W, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return X @ W
+
+
+def server_output(N, L_out, pr, ell, s, cts, Xs, W, kq, nq) -> np.ndarray:
+    """Alg. 1 step 5 at ell = 64: <Y>_s = W<X>_s + (W<X>_c - R) mod 2^64, the
+    second term the server's decryption + unpack of the client's ciphertexts (decrypt_unpack)."""
+    assert ell == 64
+    Z, _ = decrypt_unpack(N, L_out, pr, ell, s, cts, kq, nq, np.asarray(W).shape[1])
+    with np.errstate(over="ignore"):
+        return plain_matmul64(Xs, W) + Z

@@ -567,3 +567,42 @@ def test_wide_e2e_ell64(oracle, case):
         mask = oracle.words(seed, 6, tg * N, N)
         for J in range(rows * c["n"], N):
             assert int(full[tg, J]) == (t - int(mask[J])) % t
+
+
+# ----------------------------------------------------------------- server step 5 at ell = 64
+def test_plain_matmul64_bruteforce(oracle):
+    """The server's W<X>_s mod 2^64 (PAPER.md:681 at the paper's t) against Python
+    integers: random full-width entries and all-(2^64 - 1) entries (every carry)."""
+    from oracle import wide
+    t = 1 << 64
+    for k, m, n, seed in ((3, 5, 4, 1), (6, 37, 9, 2)):
+        X = ni.gen_X(seed, k, m, 64)
+        W = ni.gen_W(seed, m, n, 64)
+        got = wide.plain_matmul64(X, W)
+        want = py_matmul_mod(X, W, t)
+        assert all(int(got[a, j]) == int(want[a, j]) for a in range(k) for j in range(n))
+    X = np.full((2, 40), t - 1, np.uint64)
+    W = np.full((40, 3), t - 1, np.uint64)
+    assert all(int(v) == (40 * (t - 1) ** 2) % t for v in wide.plain_matmul64(X, W).ravel())
+
+
+def test_server_output_ell64_reconstructs(oracle):
+    """Alg. 1 end to end at t = 2^64: with X = <X>_s + <X>_c mod 2^64 the
+    server's <Y>_s (wide oracle: decrypt + unpack + its own product) and the client's R satisfy
+    <Y>_s + R = X.W mod 2^64 by Python integers, and <Y>_s alone is not the product."""
+    from oracle import wide
+    N, L, L_out, ell, k, m, n, nq = 64, 5, 3, 64, 6, 7, 20, 1
+    t = 1 << ell
+    pr = [int(p) for p in oracle.primes(N, L)]
+    seed = 0x5E64
+    s = oracle.keygen(N, seed)
+    W = ni.gen_W(seed, m, n, ell)
+    Xc = ni.gen_X(seed, k, m, ell)
+    Xs = ni.gen_X(seed + 1, k, m, ell)
+    E = wide.encrypt_rows(N, L, pr, ell, s, W, seed)
+    cts, R = wide.cop_matmul(N, L, L_out, pr, ell, E, Xc, n, k, nq, seed)
+    Ys = wide.server_output(N, L_out, pr, ell, s, cts, Xs, W, k, nq)
+    X = [[(int(Xc[a, b]) + int(Xs[a, b])) % t for b in range(m)] for a in range(k)]
+    want = [[sum(X[a][b] * int(W[b, j]) for b in range(m)) % t for j in range(n)] for a in range(k)]
+    assert all((int(Ys[a, j]) + int(R[a, j])) % t == want[a][j] for a in range(k) for j in range(n))
+    assert any(int(Ys[a, j]) != want[a][j] for a in range(k) for j in range(n))
