@@ -448,17 +448,28 @@ void orc_keygen_pk(uint32_t N, uint32_t L, const uint32_t* primes, const int8_t*
     free(a); free(sp); free(as);
 }
 
-/* Flooding noise f uniform in [-2^F, 2^F) from one PRG word (F = 0: no flooding). */
-static int64_t flood(uint64_t w, uint32_t F) {
+/* Flooding noise f uniform in [-2^F, 2^F) (F = 0: no flooding; reading 26):
+ * F <= 62: the top F + 1 bits of w0 = word(seed, 12, idx), f = (w0 >> (63 - F)) - 2^F;
+ * 62 < F <= 126: the top F + 1 bits of the 128-bit V = w1 2^64 + w0 with
+ * w1 = word(seed, 13, idx), f = (V >> (127 - F)) - 2^F. */
+static __int128 flood(uint64_t seed, uint64_t idx, uint32_t F) {
     if (F == 0) return 0;
-    return (int64_t)(w >> (63 - F)) - ((int64_t)1 << F);
+    uint64_t w0 = orc_word(seed, 12, idx);
+    if (F <= 62) return (__int128)(w0 >> (63 - F)) - ((__int128)1 << F);
+    u128 V = ((u128)orc_word(seed, 13, idx) << 64) | w0;
+    return (__int128)(V >> (127 - F)) - ((__int128)1 << F);
+}
+static uint32_t smod128(__int128 v, uint32_t p) {
+    __int128 r = v % (__int128)p;
+    if (r < 0) r += p;
+    return (uint32_t)r;
 }
 
 /* Circuit privacy (the client's output ciphertext must not reveal
  * X_c to the key owner; reading 26): a fresh public-key encryption of
  * zero per packed ciphertext g, at the full modulus q:
  *   v = ternary (domain 9, index g N + j), e1, e2 = CBD(21) (domains 10, 11, index g N + j),
- *   f = flooding noise in [-2^F, 2^F) (domain 12, index g N + j),
+ *   f = flooding noise in [-2^F, 2^F) (domain 12, and 13 for F > 62, index g N + j; flood()),
  *   z_b[i] = v * b_pk[i] + e1 + f,  z_a[i] = v * a_pk[i] + e2  mod p_i.
  * It decrypts to v e_pk + e1 + f - e2 s (message 0).  Output z[g][comp][limb][j]. */
 void orc_rerand_zero(uint32_t N, uint32_t L, const uint32_t* primes, const uint32_t* pk, uint64_t seed,
@@ -474,9 +485,9 @@ void orc_rerand_zero(uint32_t N, uint32_t L, const uint32_t* primes, const uint3
                 orc_negacyclic_ntt(N, p, pk + ((uint64_t)comp * L + i) * N, vp, prod);
                 for (uint32_t j = 0; j < N; j++) {
                     uint64_t idx = (uint64_t)g * N + j;
-                    int64_t e = comp == 0 ? (int64_t)cbd21(orc_word(seed, 10, idx)) + flood(orc_word(seed, 12, idx), F)
-                                          : (int64_t)cbd21(orc_word(seed, 11, idx));
-                    z[(((uint64_t)g * 2 + comp) * L + i) * N + j] = (uint32_t)(((uint64_t)prod[j] + smod(e, p)) % p);
+                    __int128 e = comp == 0 ? (__int128)cbd21(orc_word(seed, 10, idx)) + flood(seed, idx, F)
+                                           : (__int128)cbd21(orc_word(seed, 11, idx));
+                    z[(((uint64_t)g * 2 + comp) * L + i) * N + j] = (uint32_t)(((uint64_t)prod[j] + smod128(e, p)) % p);
                 }
             }
         }

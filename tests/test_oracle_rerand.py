@@ -38,10 +38,15 @@ def ternary_words(O, seed, dom, start, N):
 
 
 def flood_words(O, seed, start, N, F):
-    """Reading 26: f = (w >> (63 - F)) - 2^F, uniform in [-2^F, 2^F); none when F = 0."""
+    """Reading 26: f uniform in [-2^F, 2^F), the top F + 1 bits of w0 = word(seed, 12, i) (F <= 62)
+    or of the 128-bit w1 2^64 + w0 with w1 = word(seed, 13, i) (62 < F <= 126); none when F = 0."""
     if F == 0:
         return [0] * N
-    return [(int(w) >> (63 - F)) - (1 << F) for w in O.words(seed, 12, start, N)]
+    w0 = [int(w) for w in O.words(seed, 12, start, N)]
+    if F <= 62:
+        return [(w >> (63 - F)) - (1 << F) for w in w0]
+    w1 = [int(w) for w in O.words(seed, 13, start, N)]
+    return [(((hi << 64) | lo) >> (127 - F)) - (1 << F) for hi, lo in zip(w1, w0)]
 
 
 @pytest.mark.parametrize("N,pr", [(64, P4096), (64, P8192), (128, P8192)])
@@ -65,7 +70,7 @@ def test_public_key_decrypts_to_cbd_noise(oracle, N, pr):
     assert (pk[1, 0] != pk[1, 1] % pr[0]).any()
 
 
-@pytest.mark.parametrize("F", [0, 20])
+@pytest.mark.parametrize("F", [0, 20, 80])
 def test_zero_encryption_noise_is_exact(oracle, F):
     """z = (v b_pk + e1 + f, v a_pk + e2) decrypts to exactly
     v e_pk + e1 + f - e2 s over Z (reading 26), the same integer in every limb,
@@ -87,13 +92,22 @@ def test_zero_encryption_noise_is_exact(oracle, F):
         e2s = negacyclic_Z(e2, [int(x) for x in s])
         want = [ve[j] + e1[j] + f[j] - e2s[j] for j in range(N)]
         assert max(abs(w) for w in want) <= 42 * N + 21 + (1 << F)
+        res = []
         for i, p in enumerate(pr):
             b, a = z[g, 0, i], z[g, 1, i]
             as_ = py_negacyclic(a, [int(x) % p for x in s], p)
-            got = [centered(int(b[j]) - as_[j], p) for j in range(N)]
-            assert got == want
-        m = oracle.decrypt_ct(N, L, np.array(pr, np.uint32), ell, s, z[g])[0]
-        assert not np.asarray(m).any()
+            res.append([(int(b[j]) - as_[j]) % p for j in range(N)])
+            assert [centered(r, p) for r in res[-1]] == [centered(w, p) for w in want]
+        # one integer in every limb: CRT over q = prod p_i (> 2^92 > 2 |noise|) recovers it exactly
+        q = 1
+        for p in pr:
+            q *= p
+        crt = [centered(sum(res[i][j] * (q // p) * pow(q // p, -1, p) for i, p in enumerate(pr)), q)
+               for j in range(N)]
+        assert crt == want
+        if F <= 62:     # the C oracle's decryption needs |noise| < q / (2 t) (q ~ 2^93, t = 2^32)
+            m = oracle.decrypt_ct(N, L, np.array(pr, np.uint32), ell, s, z[g])[0]
+            assert not np.asarray(m).any()
     if F:
         assert any(abs(x) > 42 * N + 21 for x in want)  # the flooding term is really there
 
@@ -114,7 +128,7 @@ def max_flood_bits(N, pr, ell, L_out, m, R_eff):
     for p in pr[:L_out]:
         q_out *= p
     best = 0
-    for F in range(1, 63):
+    for F in range(1, 127):
         if noise_bound_rr(N, pr, ell, L_out, m, R_eff, F) < q_out / (2 * (1 << ell)):
             best = F
     return best
@@ -157,15 +171,43 @@ def test_rerandomised_output_decrypts_to_the_same_shares(oracle, case):
     assert tv / t <= noise_bound_rr(N, pr, ell, L_out, c["m"], R_eff, F)
     a0, a1 = cts0[:, :, 1], cts[:, :, 1]
     assert (a0 != a1).mean() > 0.99
-    # 4 bits past the bound (when that fits the 62-bit flooding range): wrong plaintexts
-    if F + 4 > 62:
-        return
+    # 4 bits past the bound: wrong plaintexts
     zbig = oracle.rerand_zero(N, L, np.array(pr, np.uint32), pk, seed ^ 0xABC, nct, F + 4)
     cbig, _ = oracle.cop_matmul_rr(N, L, L_out, np.array(pr, np.uint32), ell, E, X, c["n"], c["k"], c["nq"],
                                    seed, zbig)
     Zb, _, _ = oracle.decrypt_unpack(N, L_out, np.array(pr[:L_out], np.uint32), ell, s, cbig, c["k"], c["nq"],
                                      c["n"])
     assert (Zb.astype(np.uint64) != (Y + t - R) % t).mean() > 0.5
+
+
+def test_statistical_flooding_parameter_set(oracle):
+    """The shipped circuit-privacy parameter set (reading 26): one more limb (L = 3,
+    L_out = 1, ell = 16) lets the flooding noise exceed the worst-case COP noise
+    R m (t-1)(eta + 1/2) by >= 40 bits -- statistical smudging -- and the output
+    still decrypts exactly to X.W - R mod t (brute force)."""
+    N, ell, L_out, L = 256, 16, 1, 3
+    pr = [int(p) for p in oracle.primes(N, L)]
+    k, m, n = 12, 64, 100
+    t = 1 << ell
+    seed = 0xF10D
+    R_eff = min(N // n, k)
+    F = max_flood_bits(N, pr, ell, L_out, m, R_eff)
+    cop = R_eff * m * (t - 1) * 21.5
+    assert F - np.log2(cop) >= 40, (F, np.log2(cop))
+    s = oracle.keygen(N, seed)
+    W = ni.gen_W(seed, m, n, ell)
+    X = ni.gen_X(seed, k, m, ell)
+    E = oracle.encrypt_rows(N, L, np.array(pr, np.uint32), ell, s, W, seed)
+    pk = oracle.keygen_pk(N, L, np.array(pr, np.uint32), s, seed + 1)
+    nct = oracle.cts_per_query(N, n, k)
+    z = oracle.rerand_zero(N, L, np.array(pr, np.uint32), pk, seed + 2, nct, F)
+    cts, R = oracle.cop_matmul_rr(N, L, L_out, np.array(pr, np.uint32), ell, E, X, n, k, 1, seed, z)
+    Z, _, tv = oracle.decrypt_unpack(N, L_out, np.array(pr[:L_out], np.uint32), ell, s, cts, k, 1, n)
+    Y = py_matmul_mod(X, W, t)
+    assert (Z.astype(np.uint64) == (Y + t - R) % t).all()
+    # the flooding term dominates the zero encryptions' noise (|f| up to 2^F)
+    f = flood_words(oracle, seed + 2, 0, N, F)
+    assert max(abs(x) for x in f) > 2 ** (F - 2)
 
 
 def test_rerandomised_ell64_wide_oracle(oracle):
