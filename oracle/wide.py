@@ -40,16 +40,17 @@ def encrypt_rows(N, L, pr, ell, s, W, seed) -> np.ndarray:
     W = np.asarray(W, dtype=np.uint64)
     m, n = W.shape
     out = np.empty((m, 2, L, N), np.uint32)
+    sps = [np.array([int(x) % p for x in s], np.uint32) for p in pr]
     for beta in range(m):
         e = O.sample_cbd21(seed, 3, beta * N, N).astype(np.int64)
-        what = [int(W[beta, j]) if j < n else 0 for j in range(N)]
-        embs = [emb(q, w, ell) for w in what]
+        # w_hat[j] = W[beta][j] for j < n, else 0 (Emb_q(0) = 0): only the first n slots need Emb
+        embs = [emb(q, int(W[beta, j]), ell) for j in range(n)]
         for i, p in enumerate(pr):
             a = O.sample_uniform_mod(seed, 2, (beta * L + i) * N, N, p)
-            sp = np.array([int(x) % p for x in s], np.uint32)
-            a_s = O.negacyclic_ntt(N, p, a, sp).astype(np.int64)
-            b = [(int(a_s[j]) + embs[j] + int(e[j])) % p for j in range(N)]
-            out[beta, 0, i] = np.array(b, np.uint32)
+            a_s = O.negacyclic_ntt(N, p, a, sps[i]).astype(np.int64)
+            em = np.zeros(N, np.int64)
+            em[:n] = np.array([x % p for x in embs], np.int64)
+            out[beta, 0, i] = ((a_s + em + e) % p).astype(np.uint32)
             out[beta, 1, i] = a
     return out
 
@@ -175,3 +176,42 @@ def server_output(N, L_out, pr, ell, s, cts, Xs, W, kq, nq) -> np.ndarray:
     Z, _ = decrypt_unpack(N, L_out, pr, ell, s, cts, kq, nq, np.asarray(W).shape[1])
     with np.errstate(over="ignore"):
         return plain_matmul64(Xs, W) + Z
+
+
+def cop_matmul_sampled(N, L, L_out, pr, ell, E, X, n, kq, nq, seed, s_query, s_theta, s_J) -> np.ndarray:
+    """cop_matmul restricted to sampled output coefficients (query, theta, J), for sizes the full
+    oracle cannot run: the same steps (per-limb contraction mod p_i of the rows theta R + r and the
+    columns (J - r n) mod N RShift packing reads, ModDown on the CRT integer, the mask Emb_q'(r)).
+    Returns out[sample][comp][limb < L_out] uint32."""
+    pr = [int(p) for p in pr]
+    t = 1 << ell
+    X = np.asarray(X, dtype=np.uint64)
+    E = np.asarray(E)
+    R_ = N // n
+    nct = -(-kq // R_)
+    qo = _q(pr[:L_out])
+    out = np.zeros((len(s_query), 2, L_out), np.uint32)
+    for si, (q_, th, J) in enumerate(zip(s_query, s_theta, s_J)):
+        q_, th, J = int(q_), int(th), int(J)
+        tg = q_ * nct + th
+        rows = min(R_, kq - th * R_)
+        w = int(O.words(seed, 6, tg * N + J, 1)[0])
+        r_mask = w >> (64 - ell) if ell < 64 else w
+        for comp in range(2):
+            c = []
+            for i, p in enumerate(pr):
+                v = 0
+                for r in range(rows):            # RShift: X^(r n) c[theta R + r]
+                    sh = r * n
+                    col = (J - sh) % N
+                    xs = np.array([int(x) % p for x in X[q_ * kq + th * R_ + r]], dtype=object)
+                    es = E[:, comp, i, col].astype(object)
+                    val = int((xs * es).sum()) % p
+                    v += val if J >= sh else p - val
+                c.append(v % p)
+            c = _moddown(c, pr, L_out)
+            if comp == 0:
+                em = emb(qo, r_mask, ell)
+                c = [(c[i] - em) % pr[i] for i in range(L_out)]
+            out[si, comp] = c
+    return out

@@ -606,3 +606,22 @@ def test_server_output_ell64_reconstructs(oracle):
     want = [[sum(X[a][b] * int(W[b, j]) for b in range(m)) % t for j in range(n)] for a in range(k)]
     assert all((int(Ys[a, j]) + int(R[a, j])) % t == want[a][j] for a in range(k) for j in range(n))
     assert any(int(Ys[a, j]) != want[a][j] for a in range(k) for j in range(n))
+
+
+def test_wide_sampled_equals_full(oracle):
+    """wide.cop_matmul_sampled (the full-size check of the ell = 64 bytes) returns exactly the
+    coefficients wide.cop_matmul computes, on every slot of a small two-query case (incl. wrapped
+    shifts, the ragged last packed ciphertext and invalid slots)."""
+    from oracle import wide
+    N, L, L_out, ell, k, m, n, nq = 64, 5, 3, 64, 7, 5, 20, 2
+    pr = [int(p) for p in oracle.primes(N, L)]
+    seed = 0x5A3
+    s = oracle.keygen(N, seed)
+    W = ni.gen_W(seed, m, n, ell)
+    X = ni.gen_X(seed, k * nq, m, ell)
+    E = wide.encrypt_rows(N, L, pr, ell, s, W, seed)
+    cts, _ = wide.cop_matmul(N, L, L_out, pr, ell, E, X, n, k, nq, seed)
+    nct = cts.shape[1]
+    sq, st, sJ = np.meshgrid(np.arange(nq), np.arange(nct), np.arange(N), indexing="ij")
+    got = wide.cop_matmul_sampled(N, L, L_out, pr, ell, E, X, n, k, nq, seed, sq.ravel(), st.ravel(), sJ.ravel())
+    assert (got == cts.transpose(0, 1, 4, 2, 3).reshape(-1, 2, L_out)).all()
