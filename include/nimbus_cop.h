@@ -194,17 +194,20 @@ nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* encw, co
  * encryption of zero per output ciphertext,
  *   z_b = v b_pk + e1 + f,  z_a = v a_pk + e2  (mod each of the L primes),
  *   v ternary (domain 9), e1, e2 CBD(21) (domains 10, 11), f uniform in
- *   [-2^F, 2^F) (domain 12, F = flood_bits, 0 = none); PRG index g N + j for
- *   output ciphertext g (query-major, as d_cts).
+ *   [-2^F, 2^F) (F = flood_bits <= 126, 0 = none): the top F + 1 bits of the word
+ *   of domain 12 (F <= 62) or of the 128-bit (domain 13 word) 2^64 + (domain 12 word);
+ *   PRG index g N + j for output ciphertext g (query-major, as d_cts).
  * Online, nimbus_cop_matmul_rr is nimbus_cop_matmul with z[g] added to packed
  * ciphertext g at the full modulus, before the mod-switch: the output's a
  * component is re-randomised, its noise grows by at most 2 eta N + eta + 2^F
  * before the limb drops, and it decrypts to the same (X.W - R) mod t.
  *  d_zero   n_cts x 2 x L x N uint32 [g][comp][limb][j] (n_cts of nimbus_cop_out_count);
  *           prepare it with the same encw, k_per_query, n_queries, and a fresh seed per call.
- * nimbus_rerand_flood_max: the largest F (<= 62) that keeps decryption exact for
+ * nimbus_rerand_flood_max: the largest F (<= 126) that keeps decryption exact for
  * this encw and k_per_query (NIMBUS_ENOISE if none); prepare returns NIMBUS_ENOISE
- * for a larger F. */
+ * for a larger F.  Statistical smudging (F >= 40 bits above the worst-case COP noise
+ * R m (t-1)(eta + 1/2)) needs headroom in q: e.g. N = 4096, L = 3, ell = 16, L_out = 1
+ * gives F = 73 at the C2 shape (41 bits over 2^32.3); L = 2 allows only F = 44. */
 nimbus_status nimbus_rerand_flood_max(const nimbus_ctx* ctx, const nimbus_encw* encw, uint32_t k_per_query,
                                       uint32_t* flood_bits);
 nimbus_status nimbus_rerand_prepare(nimbus_ctx* ctx, const nimbus_pk* pk, const nimbus_encw* encw,
@@ -392,6 +395,22 @@ nimbus_status nimbus_server_output(nimbus_ctx* ctx, const nimbus_sk* sk, const n
                                    const uint32_t* d_Xs, const uint32_t* d_cts, uint32_t k_per_query,
                                    uint32_t n_queries, uint32_t* d_Ys, void* d_ws, size_t ws_bytes,
                                    void* stream);
+
+/* The paper's t = 2^64, ell > 32 contexts: W, X, Y,
+ * the added term and the shares are uint64 (k x m, m x n, k x n row-major).  Products are
+ * exact mod 2^64: 8 byte slices of each operand on the int8 tensor cores, the 36 slice
+ * pairs with shift < 64 (m <= 4096, NIMBUS_ESHAPE beyond).  Workspace:
+ * nimbus_server_workspace_size as for the 32-bit calls. */
+nimbus_status nimbus_plain_weights_u64(nimbus_ctx* ctx, const uint64_t* d_W, uint32_t m, uint32_t n,
+                                       void* stream, nimbus_plainw** out);
+nimbus_status nimbus_plain_matmul_u64(nimbus_ctx* ctx, const nimbus_plainw* w, const uint64_t* d_X, uint32_t k,
+                                      const uint64_t* d_add, uint64_t* d_Y, void* d_ws, size_t ws_bytes,
+                                      void* stream);
+/* d_Ys = (d_Xs . W + unpack(Dec(d_cts))) mod 2^64 (Alg. 1 step 5 at the paper's t). */
+nimbus_status nimbus_server_output_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const nimbus_plainw* w,
+                                       const uint64_t* d_Xs, const uint32_t* d_cts, uint32_t k_per_query,
+                                       uint32_t n_queries, uint64_t* d_Ys, void* d_ws, size_t ws_bytes,
+                                       void* stream);
 
 /* ---------------------------------------------------------- test helpers --- */
 /* PRG words word(seed, dom, start + i), i < count. */

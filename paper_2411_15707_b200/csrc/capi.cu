@@ -94,12 +94,22 @@ static int big_cmp(const Big& a, const Big& b) {
 // each limb drop v -> v/p + (1+N)/2; the mask adds 1/2.  Requires 2|v| t < q.
 // extra2: a further bound on 2|v| added before the mod-switch (the public-key zero
 // encryption of reading 26: 2 |v e_pk + e1 + f - e2 s| <= 4 eta N + 2 eta + 2^(F+1)).
-static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff, uint64_t extra2 = 0) {
+static bool noise_ok(const nimbus_ctx* c, uint32_t m, uint32_t R_eff, uint64_t extra2 = 0, uint32_t flood2 = 0) {
     const uint32_t ell = c->rns.ell, N = c->rns.N;
     const uint64_t tm1 = ell >= 64 ? ~0ULL : (1ULL << ell) - 1;
     Big B = big_of((u128)R_eff * m * 43u);      // 2 eta + 1 = 43 for CBD(21)
     big_mul(B, tm1);
     big_add(B, extra2);
+    if (flood2) {                               // + 2^flood2 (twice the flooding bound 2^F, F up to 126)
+        Big F2;
+        F2.w[flood2 / 64] = 1ull << (flood2 % 64);
+        uint64_t carry = 0;
+        for (int i = 0; i < 6; i++) {
+            const u128 sum = (u128)B.w[i] + F2.w[i] + carry;
+            B.w[i] = (uint64_t)sum;
+            carry = (uint64_t)(sum >> 64);
+        }
+    }
     Big Bt = B;
     big_shl(Bt, ell);
     if (big_cmp(Bt, c->q) >= 0) return false;
@@ -892,16 +902,17 @@ nimbus_status nimbus_cop_matmul_u64(nimbus_ctx* ctx, const nimbus_encw* w, const
 }
 
 // ---------------------------------------------------------------- circuit privacy (reading 26)
-static uint64_t rerand_extra2(const nimbus_ctx* ctx, uint32_t F) {
-    return 84ull * ctx->rns.N + 42 + (F ? (2ull << F) : 0);
-}
+static constexpr uint32_t kMaxFlood = 126;      // flooding noise in [-2^F, 2^F), F <= 126 (two PRG words)
+// the zero encryption's noise bound, doubled: 2 |v e_pk + e1 + f - e2 s| <= 4 eta N + 2 eta + 2^(F+1)
+static uint64_t rerand_extra2(const nimbus_ctx* ctx) { return 84ull * ctx->rns.N + 42; }
+static uint32_t rerand_flood2(uint32_t F) { return F ? F + 1 : 0; }
 
 nimbus_status nimbus_rerand_flood_max(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t kq, uint32_t* bits) {
     if (!ctx || !w || !bits || w->ctx != ctx || kq == 0) return NIMBUS_EINVAL;
     const uint32_t R = ctx->rns.N / w->n, Reff = kq < R ? kq : R;
-    for (uint32_t F = 62; F >= 1; F--)
-        if (noise_ok(ctx, w->m, Reff, rerand_extra2(ctx, F))) { *bits = F; return NIMBUS_OK; }
-    if (noise_ok(ctx, w->m, Reff, rerand_extra2(ctx, 0))) { *bits = 0; return NIMBUS_OK; }
+    for (uint32_t F = kMaxFlood; F >= 1; F--)
+        if (noise_ok(ctx, w->m, Reff, rerand_extra2(ctx), rerand_flood2(F))) { *bits = F; return NIMBUS_OK; }
+    if (noise_ok(ctx, w->m, Reff, rerand_extra2(ctx), 0)) { *bits = 0; return NIMBUS_OK; }
     return NIMBUS_ENOISE;
 }
 
@@ -912,9 +923,9 @@ nimbus_status nimbus_rerand_prepare(nimbus_ctx* ctx, const nimbus_pk* pk, const 
     if (!ctx || !pk || !w || !d_zero || pk->ctx != ctx) return set_err(ctx, NIMBUS_EINVAL, "null argument");
     nimbus_status st = check_shape(ctx, w, kq, nq);
     if (st != NIMBUS_OK) return st;
-    if (flood_bits > 62) return set_err(ctx, NIMBUS_EINVAL, "flood_bits > 62");
+    if (flood_bits > kMaxFlood) return set_err(ctx, NIMBUS_EINVAL, "flood_bits > 126");
     const uint32_t R = ctx->rns.N / w->n, Reff = kq < R ? kq : R;
-    if (!noise_ok(ctx, w->m, Reff, rerand_extra2(ctx, flood_bits)))
+    if (!noise_ok(ctx, w->m, Reff, rerand_extra2(ctx), rerand_flood2(flood_bits)))
         return set_err(ctx, NIMBUS_ENOISE, "flooding noise exceeds the decryption bound (see nimbus_rerand_flood_max)");
     const uint32_t n_cts = nq * cts_per_query(ctx, kq, w->n);
     CK(launch_rerand(ctx, pk->d_pk_ntt, seed, n_cts, flood_bits, d_zero, (cudaStream_t)stream), "rerand");
@@ -1576,10 +1587,31 @@ nimbus_status nimbus_decrypt_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const uin
 }
 
 // ---------------------------------------------------------------- server, step 5
+nimbus_status nimbus_plain_weights_u64(nimbus_ctx* ctx, const uint64_t* d_W, uint32_t m, uint32_t n, void* stream,
+                                       nimbus_plainw** out) {
+    DevGuard dg_(ctx, __func__);
+    if (want_width(ctx, 8) != NIMBUS_OK) return NIMBUS_EINVAL;          // ell > 32: t = 2^64 products
+    if (!ctx || !d_W || !out || m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (m > 4096) return set_err(ctx, NIMBUS_ESHAPE, "m > 4096 at ell = 64 (int32 slice accumulators)");
+    nimbus_plainw* w = new (std::nothrow) nimbus_plainw();
+    if (!w) return set_err(ctx, NIMBUS_ENOMEM, "host alloc");
+    w->ctx = ctx;
+    w->m = m;
+    w->n = n;
+    w->KB = (m + kBK - 1) / kBK;
+    w->bytes = (size_t)plain_col_tiles64(n) * w->KB * 8 * 128 * kBK;
+    cudaError_t e = cudaMalloc(&w->d_Wt, w->bytes);
+    if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "plain weights alloc"); }
+    e = launch_tile_plainw64(ctx, d_W, m, n, w->KB, w->d_Wt, (cudaStream_t)stream);
+    if (e != cudaSuccess) { cudaFree(w->d_Wt); delete w; return cuda_err(ctx, e, "tile plain weights"); }
+    *out = w;
+    return NIMBUS_OK;
+}
+
 nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_t m, uint32_t n, void* stream,
                                    nimbus_plainw** out) {
     DevGuard dg_(ctx, __func__);
-    if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;          // server GEMM: ell <= 32
+    if (want_width(ctx, 4) != NIMBUS_OK) return NIMBUS_EINVAL;          // ell <= 32 (ell = 64: _u64)
     if (!ctx || !d_W || !out || m == 0 || n == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
     nimbus_plainw* w = new (std::nothrow) nimbus_plainw();
     if (!w) return set_err(ctx, NIMBUS_ENOMEM, "host alloc");
@@ -1611,9 +1643,12 @@ static ServerWs server_ws(const nimbus_ctx* ctx, const nimbus_plainw* w, uint32_
     ServerWs L;
     const size_t k = (size_t)kq * (nq ? nq : 1);
     const size_t Mt = (k + kBM - 1) / kBM;
+    const size_t es = elem_bytes(ctx->rns.ell);
     L.xt = 0;
-    L.z = al(sx_of(ctx->rns.ell) * Mt * kBM * (size_t)w->KB * kBK);
-    L.u = L.z + (nq ? al(k * w->n * 4) : 0);
+    // X slices: 128-row tiles, or 32-row tiles for the ell = 64 kernel (k_plain_t64)
+    const size_t xrows = es == 8 ? ((k + 31) / 32) * 32 : Mt * kBM;
+    L.z = al(sx_of(ctx->rns.ell) * xrows * (size_t)w->KB * kBK);
+    L.u = L.z + (nq ? al(k * w->n * es) : 0);
     size_t ubytes = 0;
     if (nq) {
         const uint32_t R = ctx->rns.N / w->n, nct = (kq + R - 1) / R;
@@ -1663,6 +1698,43 @@ nimbus_status nimbus_server_output(nimbus_ctx* ctx, const nimbus_sk* sk, const n
     CK(launch_decrypt(ctx, sk->d_s_ntt, d_cts, nq * nct, nct, kq, w->n, U, Z, nullptr, s), "decrypt");
     CK(launch_slice_x(ctx, d_Xs, k, w->m, w->KB, kBM, ws + L.xt, s), "slice X_s");
     CK(launch_plain_matmul(ctx, ws + L.xt, w->d_Wt, k, w->n, w->KB, Z, d_Ys, s), "plain matmul");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_plain_matmul_u64(nimbus_ctx* ctx, const nimbus_plainw* w, const uint64_t* d_X, uint32_t k,
+                                      const uint64_t* d_add, uint64_t* d_Y, void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx, __func__);
+    if (want_width(ctx, 8) != NIMBUS_OK) return NIMBUS_EINVAL;
+    if (!ctx || !w || w->ctx != ctx || !d_X || !d_Y || !d_ws || k == 0) return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (k > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
+    const ServerWs L = server_ws(ctx, w, k, 0);
+    if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* xt = (uint8_t*)d_ws + L.xt;
+    CK(launch_slice_x(ctx, d_X, k, w->m, w->KB, 32, xt, s), "slice X");
+    CK(launch_plain_matmul64(ctx, xt, w->d_Wt, k, w->n, w->KB, d_add, d_Y, s), "plain matmul 64");
+    return NIMBUS_OK;
+}
+
+nimbus_status nimbus_server_output_u64(nimbus_ctx* ctx, const nimbus_sk* sk, const nimbus_plainw* w,
+                                       const uint64_t* d_Xs, const uint32_t* d_cts, uint32_t kq, uint32_t nq,
+                                       uint64_t* d_Ys, void* d_ws, size_t ws_bytes, void* stream) {
+    DevGuard dg_(ctx, __func__);
+    if (want_width(ctx, 8) != NIMBUS_OK) return NIMBUS_EINVAL;
+    if (!ctx || !sk || !w || w->ctx != ctx || !d_Xs || !d_cts || !d_Ys || !d_ws || kq == 0 || nq == 0)
+        return set_err(ctx, NIMBUS_EINVAL, "bad argument");
+    if (w->n > ctx->rns.N) return set_err(ctx, NIMBUS_ESHAPE, "n > N");
+    if ((uint64_t)kq * nq > (1u << 24)) return set_err(ctx, NIMBUS_ESHAPE, "k too large");
+    const ServerWs L = server_ws(ctx, w, kq, nq);
+    if (ws_bytes < L.total) return set_err(ctx, NIMBUS_ESHAPE, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t k = kq * nq, R = ctx->rns.N / w->n, nct = (kq + R - 1) / R;
+    uint8_t* ws = (uint8_t*)d_ws;
+    uint64_t* Z = reinterpret_cast<uint64_t*>(ws + L.z);
+    uint32_t* U = reinterpret_cast<uint32_t*>(ws + L.u);
+    CK(launch_decrypt(ctx, sk->d_s_ntt, d_cts, nq * nct, nct, kq, w->n, U, Z, nullptr, s), "decrypt");
+    CK(launch_slice_x(ctx, d_Xs, k, w->m, w->KB, 32, ws + L.xt, s), "slice X_s");
+    CK(launch_plain_matmul64(ctx, ws + L.xt, w->d_Wt, k, w->n, w->KB, Z, d_Ys, s), "plain matmul 64");
     return NIMBUS_OK;
 }
 

@@ -1068,7 +1068,7 @@ cudaError_t launch_res_jobs(nimbus_ctx* c, const ResJobs& J, uint32_t KB, const 
     e = launch_pdl(k_cop_tc_res<false>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt, J, k, CT, KB,
                    ncol, FuseOut{});
     c->launches++;
-    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<false>");
+    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<0>");
     return e;
 }
 
@@ -1096,7 +1096,7 @@ cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8
     e = launch_pdl(k_cop_tc_res<true>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt, J, k, CT,
                    w->KB, ncol, fo);
     c->launches++;
-    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<true>");
+    snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<1>");
     return e;
 }
 

@@ -178,6 +178,12 @@ cudaError_t launch_tile_plainw(nimbus_ctx* c, const uint32_t* d_W, uint32_t m, u
                                uint8_t* d_Wt, cudaStream_t st);
 cudaError_t launch_plain_matmul(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_t* d_Wt, uint32_t k, uint32_t n,
                                 uint32_t KB, const uint32_t* d_add, uint32_t* d_Y, cudaStream_t st);
+// ell = 64: 8-plane W tiles of 128 columns, X slices of 32-row tiles (k_slice_x<8, 32>), uint64 Y / add
+uint32_t plain_col_tiles64(uint32_t n);
+cudaError_t launch_tile_plainw64(nimbus_ctx* c, const uint64_t* d_W, uint32_t m, uint32_t n, uint32_t KB,
+                                 uint8_t* d_Wt, cudaStream_t st);
+cudaError_t launch_plain_matmul64(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_t* d_Wt, uint32_t k, uint32_t n,
+                                  uint32_t KB, const uint64_t* d_add, uint64_t* d_Y, cudaStream_t st);
 // cop_tc.cu
 uint32_t transposed_rows(const nimbus_ctx* c);
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,

@@ -236,7 +236,8 @@ __global__ void k_rerand(Rns R, const uint32_t* d_tw, const uint32_t* pk_ntt, ui
     extern __shared__ uint32_t sm[];
     const uint32_t N = R.N, L = R.L, g = blockIdx.x, i = blockIdx.y, p = R.p[i];
     uint32_t *sv = sm, *sp = sm + N;
-    const uint64_t kv = prg_key(seed, 9), k1 = prg_key(seed, 10), k2 = prg_key(seed, 11), kf = prg_key(seed, 12);
+    const uint64_t kv = prg_key(seed, 9), k1 = prg_key(seed, 10), k2 = prg_key(seed, 11), kf = prg_key(seed, 12),
+                   kf2 = prg_key(seed, 13);
     for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
         const int32_t v = samp_ternary(prg_word(kv, (uint64_t)g * N + j));
         sv[j] = v < 0 ? p - 1 : (uint32_t)v;
@@ -253,13 +254,22 @@ __global__ void k_rerand(Rns R, const uint32_t* d_tw, const uint32_t* pk_ntt, ui
         for (uint32_t j = threadIdx.x; j < N; j += blockDim.x) {
             const uint64_t idx = (uint64_t)g * N + j;
             int64_t e;
+            uint32_t fm = 0;                          // flooding noise mod p (reading 26)
             if (comp == 0) {
                 e = samp_cbd21(prg_word(k1, idx));
-                if (F) e += (int64_t)(prg_word(kf, idx) >> (63 - F)) - ((int64_t)1 << F);
+                if (F && F <= 62) {
+                    e += (int64_t)(prg_word(kf, idx) >> (63 - F)) - ((int64_t)1 << F);
+                } else if (F > 62) {
+                    // f = (V >> (127 - F)) - 2^F, V = w1 2^64 + w0 (domains 13, 12): f mod p from 128 bits
+                    const unsigned __int128 V = ((unsigned __int128)prg_word(kf2, idx) << 64) | prg_word(kf, idx);
+                    const unsigned __int128 top = V >> (127 - F);
+                    const uint32_t tm = (uint32_t)(top % p), pw = (uint32_t)((((unsigned __int128)1) << F) % p);
+                    fm = submod(tm, pw, p);
+                }
             } else {
                 e = samp_cbd21(prg_word(k2, idx));
             }
-            zo[j] = addmod(sp[j], smod64(e, p), p);
+            zo[j] = addmod(addmod(sp[j], smod64(e, p), p), fm, p);
         }
         __syncthreads();   // sp is reused by the next component
     }

@@ -206,6 +206,218 @@ k_plain_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Wt, uint3
     }
 }
 
+// ---------------------------------------------------------------- ell = 64 (the paper's t)
+// X.W mod 2^64 with 8 slices of each operand: acc_s = sum_{i+j=s} x_i w_j for s < 8 only
+// (shifts 8s >= 64 vanish mod 2^64): 36 of the 64 slice products.  acc_s < 8 m 255^2 < 2^31
+// for m <= 4096 (host-checked), so Y = sum_s acc_s 2^(8s) in 64-bit wrap-around is exact mod 2^64.
+// Transposed orientation (as the COP kernel k_cop_tc_t<8>): A = the 8 byte planes of a
+// 128-column W tile (M = 128 output columns), B = the 8 X slices of a 32-row tile stacked along
+// N; plane j multiplies only slices 0 .. 7-j (N = 32 (8 - j)), D at TMEM column 32 j, so it
+// writes exactly acc_j .. acc_7.  Plane 0's first MMA (N = 256) initialises all 8 accumulators.
+// Shared memory: 2 X slots (32 KB) + 4 plane-quad slots (64 KB) = 192 KB; TMEM: 2 sets x 256.
+constexpr uint32_t kBNP64 = 128;   // output columns per W tile at ell = 64
+
+// CTA (ct, kb): W[beta][col] uint64 -> 8 byte planes Wt[ct][kb][j][128 rows = columns][128 B swizzled].
+// Thread item (16-byte chunk c16, column r; r fastest: coalesced W reads) reads 16 entries once and
+// writes the chunk of every plane.
+__global__ void __launch_bounds__(256) k_tile_plainw64(const uint64_t* __restrict__ W, uint32_t m, uint32_t n,
+                                                       uint32_t KB, uint8_t* __restrict__ Wt) {
+    const uint32_t ct = blockIdx.x, kb = blockIdx.y;
+    uint8_t* base = Wt + ((size_t)ct * KB + kb) * 8 * kBNP64 * kBK;
+    for (uint32_t idx = threadIdx.x; idx < 8 * kBNP64; idx += blockDim.x) {
+        const uint32_t r = idx % kBNP64, c16 = idx / kBNP64, col = ct * kBNP64 + r;
+        uint64_t v[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            const uint32_t beta = kb * kBK + c16 * 16 + u;
+            v[u] = (beta < m && col < n) ? W[(size_t)beta * n + col] : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int u = 0; u < 4; u++) acc |= (uint32_t)((v[4 * q + u] >> (8 * j)) & 0xFF) << (8 * u);
+                w[q] = acc;
+            }
+            *reinterpret_cast<uint4*>(base + (size_t)j * kBNP64 * kBK + swz_off(r, c16)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
+struct Plain64Cfg {
+    static constexpr uint32_t BM = kBNP64, RT = 32, BK = kBK;
+    static constexpr uint32_t X_BYTES = 8 * RT * BK;        // 32 KB: 8 slices x 32 rows
+    static constexpr uint32_t Q_BYTES = 4 * BM * BK;        // 64 KB: 4 planes
+    static constexpr uint32_t OFF_Q = 2 * X_BYTES;
+    static constexpr uint32_t RING = OFF_Q + 2 * Q_BYTES;
+    static constexpr uint32_t EPI_WARPS = 8;
+    static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
+    static constexpr size_t SMEM = (size_t)RING + 1024 + 256;
+    static_assert(SMEM <= 232448, "shared memory");
+};
+
+// Y[row][col] = (sum_{s<8} acc_s 2^(8s) + add[row][col]) mod 2^64 for row < k, col < n
+__global__ void __launch_bounds__(Plain64Cfg::THREADS, 1)
+k_plain_t64(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Wt, uint32_t k, uint32_t n, uint32_t Mt,
+            uint32_t CT, uint32_t KB, const uint64_t* __restrict__ add, uint64_t* __restrict__ Y) {
+    using Cfg = Plain64Cfg;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* xfull = reinterpret_cast<uint64_t*>(smem + Cfg::RING);
+    uint64_t* xempty = xfull + 2;
+    uint64_t* qfull = xempty + 2;
+    uint64_t* qempty = qfull + 2;
+    uint64_t* tfull = qempty + 2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nunits = Mt * CT;
+    if (warp == 0 && lane == 0) {
+        for (uint32_t b = 0; b < 2; b++) {
+            mbar_init(&xfull[b], 1); mbar_init(&xempty[b], 1); mbar_init(&qfull[b], 1); mbar_init(&qempty[b], 1);
+            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- producer: per k-block the X block, then the two plane quads
+            const uint64_t pol = policy_evict_last();
+            pdl_wait();
+            uint32_t ix = 0, iq = 0;
+            for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const uint32_t mt = u % Mt, ct = u / Mt;
+                for (uint32_t kb = 0; kb < KB; kb++) {
+                    {
+                        const uint32_t s = ix & 1;
+                        if (ix >= 2) mbar_wait(&xempty[s], ((ix >> 1) & 1) ^ 1);
+                        ix++;
+                        mbar_arrive_expect_tx(&xfull[s], Cfg::X_BYTES);
+                        bulk_g2s(smem + s * Cfg::X_BYTES, Xt + ((size_t)mt * KB + kb) * Cfg::X_BYTES, Cfg::X_BYTES,
+                                 &xfull[s], pol);
+                    }
+                    for (uint32_t qd = 0; qd < 2; qd++, iq++) {
+                        const uint32_t s = iq & 1;
+                        if (iq >= 2) mbar_wait(&qempty[s], ((iq >> 1) & 1) ^ 1);
+                        mbar_arrive_expect_tx(&qfull[s], Cfg::Q_BYTES);
+                        bulk_g2s(smem + Cfg::OFF_Q + s * Cfg::Q_BYTES,
+                                 Wt + ((size_t)ct * KB + kb) * 8 * Cfg::BM * Cfg::BK + qd * Cfg::Q_BYTES, Cfg::Q_BYTES,
+                                 &qfull[s], pol);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (converged warp): plane j x slices 0..7-j -> acc_j .. acc_7
+        const uint64_t x_desc0 = sdesc_kmajor_sw128(smem_u32(smem));
+        const uint64_t q_desc0 = sdesc_kmajor_sw128(smem_u32(smem + Cfg::OFF_Q));
+        uint32_t ix = 0, iq = 0, ti = 0;
+        for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
+            const uint32_t buf = ti & 1, use = ti >> 1;
+            if (ti >= 2) mbar_wait(&tempty[buf], (use & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dacc = tmem + buf * 256;
+            for (uint32_t kb = 0; kb < KB; kb++, ix++) {
+                const uint32_t xs = ix & 1;
+                mbar_wait(&xfull[xs], (ix >> 1) & 1);
+                const uint64_t bd = x_desc0 + xs * (Cfg::X_BYTES >> 4);
+                for (uint32_t qd = 0; qd < 2; qd++, iq++) {
+                    const uint32_t qs = iq & 1;
+                    mbar_wait(&qfull[qs], (iq >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (uint32_t jl = 0; jl < 4; jl++) {
+                        const uint32_t j = qd * 4 + jl;
+                        const uint64_t ad = q_desc0 + qs * (Cfg::Q_BYTES >> 4) + jl * ((Cfg::BM * Cfg::BK) >> 4);
+                        const uint32_t idesc = idesc_i8(Cfg::BM, (8 - j) * Cfg::RT);
+#pragma unroll
+                        for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
+                            mma_i8_ss_w(dacc + j * Cfg::RT, ad + 2 * kk, bd + 2 * kk, idesc,
+                                        (kb == 0 && kk == 0 && j == 0) ? 0u : 1u);
+                    }
+                    mma_commit_w(&qempty[qs]);
+                }
+                mma_commit_w(&xempty[xs]);
+            }
+            mma_commit_w(&tfull[buf]);
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: lane = output column, 8 rows per tcgen05.ld, 16 rows per warp
+        const uint32_t ew = warp - 4;
+        const uint32_t sub = ew & 3, half = ew >> 2;
+        pdl_wait();
+        uint32_t ti = 0;
+        for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
+            const uint32_t mt = u % Mt, ct = u / Mt;
+            const uint32_t buf = ti & 1, use = ti >> 1;
+            mbar_wait(&tfull[buf], use & 1);
+            tc_fence_after();
+            const uint32_t col = ct * Cfg::BM + sub * 32 + lane;
+            const uint32_t tb = tmem + ((sub * 32) << 16) + buf * 256;
+#pragma unroll 1
+            for (uint32_t ch = 0; ch < 2; ch++) {
+                const uint32_t r0 = half * 16 + ch * 8;
+                uint32_t v[8][8];
+#pragma unroll
+                for (uint32_t s2 = 0; s2 < 8; s2++) tmem_ld8(tb + s2 * Cfg::RT + r0, v[s2]);
+                tmem_ld_wait();
+#pragma unroll
+                for (uint32_t q = 0; q < 8; q++) {
+                    const uint32_t row = mt * Cfg::RT + r0 + q;
+                    uint64_t y = 0;
+#pragma unroll
+                    for (uint32_t s2 = 0; s2 < 8; s2++) y += (uint64_t)v[s2][q] << (8 * s2);   // mod 2^64
+                    if (row < k && col < n) {
+                        const size_t o = (size_t)row * n + col;
+                        Y[o] = y + (add ? add[o] : 0ull);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+uint32_t plain_col_tiles64(uint32_t n) { return (n + kBNP64 - 1) / kBNP64; }
+
+cudaError_t launch_tile_plainw64(nimbus_ctx* c, const uint64_t* d_W, uint32_t m, uint32_t n, uint32_t KB,
+                                 uint8_t* d_Wt, cudaStream_t st) {
+    k_tile_plainw64<<<dim3(plain_col_tiles64(n), KB), 256, 0, st>>>(d_W, m, n, KB, d_Wt);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plain_matmul64(nimbus_ctx* c, const uint8_t* d_Xt, const uint8_t* d_Wt, uint32_t k, uint32_t n,
+                                  uint32_t KB, const uint64_t* d_add, uint64_t* d_Y, cudaStream_t st) {
+    using Cfg = Plain64Cfg;
+    cudaError_t e = ensure_smem(c, k_plain_t64, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    const uint32_t Mt = (k + Cfg::RT - 1) / Cfg::RT, CT = plain_col_tiles64(n);
+    const uint32_t units = Mt * CT;
+    const uint32_t grid = units < (uint32_t)c->num_sms ? units : (uint32_t)c->num_sms;
+    e = launch_pdl(k_plain_t64, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, d_Xt, d_Wt, k, n, Mt, CT, KB, d_add, d_Y);
+    c->launches++;
+    return e;
+}
+
 // ---------------------------------------------------------------- launchers
 uint32_t plain_col_tiles(uint32_t n) { return (n + kBNP - 1) / kBNP; }
 

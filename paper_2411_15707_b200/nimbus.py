@@ -91,6 +91,9 @@ _SIGS = {
     "nimbus_server_workspace_size": (C.c_int, [_vp, _vp, _u32, _u32, C.POINTER(_sz)]),
     "nimbus_plain_matmul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _sz, _vp]),
     "nimbus_server_output": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _sz, _vp]),
+    "nimbus_plain_weights_u64": (C.c_int, [_vp, _vp, _u32, _u32, _vp, C.POINTER(_vp)]),
+    "nimbus_plain_matmul_u64": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp, _vp, _sz, _vp]),
+    "nimbus_server_output_u64": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u32, _u32, _vp, _vp, _sz, _vp]),
     "nimbus_encrypt_weights_into": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
     "nimbus_encrypt_weights_into_u64": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp]),
     "nimbus_keygen_pk": (C.c_int, [_vp, _vp, _u64, _vp, C.POINTER(_vp)]),
@@ -694,6 +697,42 @@ def nimbus_server_output(ctx: Context, sk: SecretKey, w: PlainW, Xs: torch.Tenso
     _check(lib().nimbus_server_output(ctx.ptr, sk.ptr, w.ptr, _ptr(Xs, torch.int32, "Xs"),
                                       _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
                                       _ptr(Ys, torch.int32, "Ys"), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return Ys
+
+
+def nimbus_plain_weights_u64(ctx: Context, W: torch.Tensor, stream=None) -> PlainW:
+    """ell > 32 (the paper's t = 2^64): W is an int64 tensor holding uint64 values."""
+    m, n = W.shape
+    out = C.c_void_p()
+    _check(lib().nimbus_plain_weights_u64(ctx.ptr, _ptr(W, torch.int64, "W"), m, n, _stream(stream), C.byref(out)),
+           ctx)
+    return PlainW(out, ctx, m, n)
+
+
+def nimbus_plain_matmul_u64(ctx: Context, w: PlainW, X: torch.Tensor, add: torch.Tensor = None, Y=None, ws=None,
+                            stream=None) -> torch.Tensor:
+    k = X.shape[0]
+    if Y is None:
+        Y = torch.empty((k, w.n), dtype=torch.int64, device=X.device)
+    if ws is None:
+        ws = torch.empty(nimbus_server_workspace_size(ctx, w, k, 0), dtype=torch.uint8, device=X.device)
+    _check(lib().nimbus_plain_matmul_u64(ctx.ptr, w.ptr, _ptr(X, torch.int64, "X"), k,
+                                         _ptr(add, torch.int64, "add") if add is not None else None,
+                                         _ptr(Y, torch.int64, "Y"), _ptr(ws), ws.numel(), _stream(stream)), ctx)
+    return Y
+
+
+def nimbus_server_output_u64(ctx: Context, sk: SecretKey, w: PlainW, Xs: torch.Tensor, cts: torch.Tensor,
+                             k_per_query: int, n_queries: int, Ys=None, ws=None, stream=None) -> torch.Tensor:
+    k = k_per_query * n_queries
+    if Ys is None:
+        Ys = torch.empty((k, w.n), dtype=torch.int64, device=Xs.device)
+    if ws is None:
+        ws = torch.empty(nimbus_server_workspace_size(ctx, w, k_per_query, n_queries), dtype=torch.uint8,
+                         device=Xs.device)
+    _check(lib().nimbus_server_output_u64(ctx.ptr, sk.ptr, w.ptr, _ptr(Xs, torch.int64, "Xs"),
+                                          _ptr(cts, torch.int32, "cts"), k_per_query, n_queries,
+                                          _ptr(Ys, torch.int64, "Ys"), _ptr(ws), ws.numel(), _stream(stream)), ctx)
     return Ys
 
 

@@ -642,6 +642,16 @@ def test_server_output_parity_and_shares(nb, oracle, N, L, ell, L_out, m, n, kq,
 
 
 # ------------------------------------------------------------------ streamed Enc(W) (host-resident)
+def _oracle_job(oracle, N, L, L_out, ell, sk_seed, w_seed, x_seed, shape, mask_seed):
+    """The oracle's (cts, R) for one job of the streamed-path tests (W, X from their seeds)."""
+    kq, m, n, nq = shape
+    pr = oracle.primes(N, L)
+    s = oracle.keygen(N, sk_seed)
+    W = ni.gen_W(w_seed, m, n, ell)
+    E = oracle.encrypt_rows(N, L, pr, ell, s, W, w_seed)
+    return oracle.cop_matmul(N, L, L_out, pr, ell, E, ni.gen_X(x_seed, kq * nq, m, ell), n, kq, nq, mask_seed)
+
+
 def test_streamed_matches_resident(nb, oracle):
     """nimbus_cop_matmul_streamed (Enc(W) offloaded to pinned host memory and
     staged into alternating device slots, copy j+2 overlapping compute j+1) gives
@@ -673,8 +683,11 @@ def test_streamed_matches_resident(nb, oracle):
     stage = torch.empty(nb.nimbus_cop_stage_size(ctx, jobs), dtype=torch.uint8, device=DEV)
     nb.nimbus_cop_matmul_streamed(ctx, jobs, ws, stage)
     nb.nimbus_sync(ctx)
-    for j, (c0, R0) in zip(jobs, ref):
+    for i, (j, (c0, R0)) in enumerate(zip(jobs, ref)):
         assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+        # and the oracle's bytes, independently of the resident path
+        cts_o, R_o = _oracle_job(oracle, N, L, L_out, ell, 5, 40 + i, 50 + i, shapes[i], 60 + i)
+        assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all(), f"job {i}"
     nb.nimbus_encw_reload(jobs[0]["encw"])
     c1, R1 = nb.alloc_outputs(ctx, jobs[0]["encw"], 128, 1)
     nb.nimbus_cop_matmul(ctx, jobs[0]["encw"], jobs[0]["X"], 128, 1, 60, c1, R1, ws)
@@ -726,8 +739,11 @@ def test_streamed_from_files(nb, oracle, tmp_path):
             j["R"].zero_()
         nb.nimbus_cop_matmul_streamed(ctx, jobs, ws, stage)
         nb.nimbus_sync(ctx)
-        for j, (c0, R0) in zip(jobs, ref):
+        for i, (j, (c0, R0)) in enumerate(zip(jobs, ref)):
             assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0)
+            if rep == 0:      # the oracle's bytes, independently of the resident path
+                cts_o, R_o = _oracle_job(oracle, N, L, L_out, ell, 6, 40 + i, 50 + i, shapes[i], 60 + i)
+                assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all(), f"job {i} ({kinds[i]})"
     # reload a file-backed handle into HBM: plain calls work again
     nb.nimbus_encw_reload(jobs[0]["encw"])
     c1, R1 = nb.alloc_outputs(ctx, jobs[0]["encw"], 128, 1)
@@ -805,6 +821,58 @@ def test_ell64_parity(nb, oracle, N, m, n, kq, nq):
         assert (_u64(Z) == Y - R_o).all()
 
 
+@pytest.mark.parametrize("k,m,n", [(1, 1, 1), (33, 130, 100), (128, 768, 768), (70, 3072, 129), (200, 300, 260)])
+def test_plain_matmul_u64_parity(nb, oracle, k, m, n):
+    """Server step 5's W<X>_s at the paper's t = 2^64: nimbus_plain_matmul_u64
+    (8 byte slices, the 36 slice pairs with shift < 64 on the int8 tensor cores) equals the oracle's
+    uint64 product bit for bit, with and without the added term; ragged k / m / n tiles, m up to 3072."""
+    from oracle import wide
+    ctx = nb.nimbus_ctx_create(8192, 5, 64, 3)
+    W = ni.gen_W(31 + m, m, n, 64)
+    X = ni.gen_X(32 + k, k, m, 64)
+    w = nb.nimbus_plain_weights_u64(ctx, _dev_u64(W))
+    Y = nb.nimbus_plain_matmul_u64(ctx, w, _dev_u64(X))
+    want = wide.plain_matmul64(X, W)
+    assert (_u64(Y) == want).all()
+    A = ni.gen_X(33, k, n, 64)
+    Y2 = nb.nimbus_plain_matmul_u64(ctx, w, _dev_u64(X), add=_dev_u64(A))
+    with np.errstate(over="ignore"):
+        assert (_u64(Y2) == want + A).all()
+    # all-ones operands: every carry of every slice product
+    Xf = np.full((5, m), (1 << 64) - 1, np.uint64)
+    Wf = np.full((m, n), (1 << 64) - 1, np.uint64)
+    wf = nb.nimbus_plain_weights_u64(ctx, _dev_u64(Wf))
+    assert (_u64(nb.nimbus_plain_matmul_u64(ctx, wf, _dev_u64(Xf))) == wide.plain_matmul64(Xf, Wf)).all()
+
+
+@pytest.mark.parametrize("N,m,n,kq,nq", [(64, 16, 20, 12, 1), (256, 130, 100, 33, 2)])
+def test_server_output_u64_parity_and_shares(nb, oracle, N, m, n, kq, nq):
+    """Alg. 1 end to end at t = 2^64 on the GPU: client COP (nimbus_cop_matmul_u64) + server
+    step 5 (nimbus_server_output_u64).  <Y>_s equals the wide oracle's bit for bit, and
+    <Y>_s + R = (X_s + X_c).W mod 2^64."""
+    from oracle import wide
+    L, ell, L_out = 5, 64, 3
+    seed = 0x5E64 + N + m
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    pr = [int(p) for p in nb.nimbus_ctx_primes(ctx)]
+    sk = nb.nimbus_keygen(ctx, seed)
+    s = oracle.keygen(N, seed)
+    W = ni.gen_W(seed, m, n, ell)
+    Xc = ni.gen_X(seed ^ 0xA5, kq * nq, m, ell)
+    Xs = ni.gen_X(seed ^ 0x5A, kq * nq, m, ell)
+    w = nb.nimbus_encrypt_weights_u64(ctx, sk, _dev_u64(W), seed)
+    ws = nb.alloc_workspace(ctx, w, kq * nq)
+    cts, R = nb.alloc_outputs_u64(ctx, w, kq, nq)
+    nb.nimbus_cop_matmul_u64(ctx, w, _dev_u64(Xc), kq, nq, seed, cts, R, ws)
+    pw = nb.nimbus_plain_weights_u64(ctx, _dev_u64(W))
+    Ys = nb.nimbus_server_output_u64(ctx, sk, pw, _dev_u64(Xs), cts, kq, nq)
+    nb.nimbus_sync(ctx)
+    want = wide.server_output(N, L_out, pr, ell, s, u32(cts), Xs, W, kq, nq)
+    assert (_u64(Ys) == want).all()
+    with np.errstate(over="ignore"):
+        assert (_u64(Ys) + _u64(R) == wide.plain_matmul64(Xc + Xs, W)).all()
+
+
 def test_ell64_full_size_decrypts(nb, oracle):
     """C4's FFN-down shape at the paper's ell = 64 (N = 8192, 5 limbs, m = 3072,
     k = 128): every output slot decrypts to X.W - R mod 2^64 (valid slots) or
@@ -831,6 +899,20 @@ def test_ell64_full_size_decrypts(nb, oracle):
         mask = ni.prg_words(seed, 6, tg * N, N)
         with np.errstate(over="ignore"):
             assert (Mn[tg][rows * n:] == (np.uint64(0) - mask[rows * n:])).all()
+    # the ciphertext bytes themselves, at the full shape: Enc(W) in full and 64 sampled output
+    # coefficients (both components, all 3 output limbs) against the wide (Python-integer) oracle
+    from oracle import wide
+    pr = [int(p) for p in nb.nimbus_ctx_primes(ctx)]
+    E = wide.encrypt_rows(N, L, pr, ell, oracle.keygen(N, seed), W, seed)
+    assert (u32(nb.nimbus_encw_export(w)) == E).all()
+    rng = np.random.default_rng(64)
+    nct = cts.shape[1]
+    st = rng.integers(0, nct, 64)
+    sJ = rng.integers(0, N, 64)
+    st[:4], sJ[:4] = [0, nct - 1, nct - 1, 5], [0, N - 1, (kq - (nct - 1) * Rr) * n, n - 1]
+    want = wide.cop_matmul_sampled(N, L, L_out, pr, ell, E, X, n, kq, 1, seed, np.zeros(64, int), st, sJ)
+    g = u32(cts)
+    assert (np.stack([g[0, st[i], :, :, sJ[i]] for i in range(64)]) == want).all()
 
 
 def test_width_guards(nb):

@@ -30,6 +30,7 @@ CASES = [
     (4096, 2, 16, 1, 128, 3072, 20, 1),      # R = 1 (C3 packing: single-row path of the pack)
     (8192, 3, 32, 2, 256, 768, 30, 1),       # ell = 32, 3 -> 2 limbs
     (8192, 3, 16, 1, 300, 1000, 17, 1),      # ell = 16 on the 3-prime ring (two limb drops)
+    (4096, 3, 16, 1, 768, 768, 128, 1),      # C2 with one more limb: statistical flooding (F > 62, two words)
 ]
 
 
@@ -50,6 +51,10 @@ def test_rerand_parity(nb, oracle, N, L, ell, L_out, m, n, kq, nq):
     w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W), seed)
     F = nb.nimbus_rerand_flood_max(ctx, w, kq)
     assert F >= 8
+    if L == 3 and ell == 16 and N == 4096:
+        # the shipped circuit-privacy parameter set: >= 40 bits of smudging over the worst-case noise
+        cop = min(N // n, kq) * m * ((1 << ell) - 1) * 21.5
+        assert F - np.log2(cop) >= 40, (F, np.log2(cop))
     # zero encryptions (reading 26), with the largest flooding the bound allows
     rseed = seed ^ 0xABC
     zero = nb.nimbus_rerand_prepare(ctx, pk, w, kq, nq, rseed, F)
@@ -77,7 +82,7 @@ def test_rerand_parity(nb, oracle, N, L, ell, L_out, m, n, kq, nq):
     nb.nimbus_sync(ctx)
     assert (u32(cts0)[:, :, 1] != u32(cts)[:, :, 1]).mean() > 0.99
     # flooding past the bound is refused before any launch
-    if F < 62:
+    if F < 126:
         with pytest.raises(nb.NimbusError) as ei:
             nb.nimbus_rerand_prepare(ctx, pk, w, kq, nq, rseed, F + 1, zero)
         assert ei.value.status == -4

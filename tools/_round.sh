@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
+timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/full_pytest.log 2>&1; tail -2 gpurun_out/full_pytest.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench rc $?
+bash tools/profile_round.sh r02 5 2 2qkv 3 4 4l64 > gpurun_out/profile.log 2>&1; tail -8 gpurun_out/profile.log
