@@ -110,6 +110,9 @@ __device__ __forceinline__ void epilogue_tile(const Rns& R, uint32_t tacc, uint3
                 out[u] = reduce64_pm(x, p, c32);
             }
 #endif
+#ifdef NIMBUS_RES_NOSTORE
+            if (out[0] != 0xFFFFFFFFu) continue;     // diagnostic (wrong results): practically no C stores
+#endif
             uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ncol + col0);
             dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
             dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
@@ -382,9 +385,16 @@ struct ResCfg {
     static constexpr uint32_t BM = kBM, BN = kBNR, BK = kBK, SX = 2;
     static constexpr uint32_t SLICE = BM * BK;                 // one X slice, one k-block: 16 KB
     static constexpr uint32_t B_BYTES = kSW * BN * BK;         // Enc(W) per k-block: 16 KB
+#ifdef NIMBUS_RES_KPS1
+    // experiment: one k-block (16 KB) per slot, 7 slots, a 16 KB slice-0 staging buffer
+    static constexpr uint32_t KPS = 1;
+    static constexpr uint32_t SLOT = KPS * B_BYTES;
+    static constexpr uint32_t STAGES = 7;
+#else
     static constexpr uint32_t KPS = 2;                         // k-blocks per ring slot: one 32 KB bulk copy
     static constexpr uint32_t SLOT = KPS * B_BYTES;
     static constexpr uint32_t STAGES = 96 * 1024 / SLOT;       // 96 KB ring
+#endif
     static constexpr uint32_t NACC = SX + kSW - 1;             // 5
     static constexpr uint32_t ACC_COLS = NACC * BN;            // 160
     static constexpr uint32_t A0_COLS = kResMaxKB * (BK / 4);  // slice 0 in TMEM: 32 columns per k-block
@@ -393,6 +403,13 @@ struct ResCfg {
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
     // smem: slice 1 resident [KB][16 KB] | slice 0 staging [KPS][16 KB] | E ring [STAGES][32 KB]
     static constexpr uint32_t OFF_A1 = 0, OFF_STG = kResMaxKB * SLICE, OFF_B = OFF_STG + KPS * SLICE;
+#ifdef NIMBUS_RES_X0UP
+    // X up front (see the producer): the Enc(W) ring is the staging buffer plus the 3 slots, 4 x 32 KB,
+    // slice 0 occupying its first 3 slots until it is copied into TMEM; message it -> slot (it + 3) % 4
+    static constexpr uint32_t RING_BASE = OFF_STG, NSLOT = STAGES + 1, OFS = STAGES;
+#else
+    static constexpr uint32_t RING_BASE = OFF_B, NSLOT = STAGES, OFS = 0;
+#endif
     static constexpr size_t SMEM = (size_t)OFF_B + STAGES * SLOT + 1024 + 256;
     static_assert(A0_COLS + 2 * ACC_COLS <= TMEM_COLS, "TMEM budget");
     static_assert(SMEM <= 232448, "shared memory");
@@ -410,8 +427,8 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::SLOT);
-    uint64_t* empty = full + Cfg::STAGES;
-    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* empty = full + Cfg::NSLOT;
+    uint64_t* tfull = empty + Cfg::NSLOT;
     uint64_t* tempty = tfull + 2;
     uint64_t* sfree = tempty + 2;                 // slice-0 staging slot free (tcgen05.cp done)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
@@ -419,7 +436,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) TRACE(0);
     if (warp == 0 && lane == 0) {
-        for (uint32_t s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (uint32_t s = 0; s < Cfg::NSLOT; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (uint32_t b = 0; b < 2; b++) {
             mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); mbar_init(&sfree[b], 1);
         }
@@ -456,6 +473,42 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
             }
 #else
             const uint32_t pre = 0;
+#endif
+#ifdef NIMBUS_RES_X0UP
+            // X up front: all of the X slices in one round trip -- slice 0 into the staging buffer and
+            // ring slots 0-1 (contiguous, 96 KB), slice 1 into its resident place, on full[0]'s phase 0
+            // (full[1]'s phase 0 is a plain arrive); the MMA issuer copies slice 0 into TMEM and frees
+            // slots 0-1 (empty[0], empty[1] phase 0).  Enc(W) message `it` then uses ring slot
+            // (it + 2) % STAGES, its first copy (slot 2) issued before the PDL wait.
+            {
+                const uint32_t t0 = tiles.at(0);
+                mbar_arrive_expect_tx(&full[Cfg::OFS], min(Cfg::KPS, KB) * Cfg::B_BYTES);
+                bulk_g2s(smem + Cfg::RING_BASE + Cfg::OFS * Cfg::SLOT,
+                         jobs.Et[t0 / CT] + (size_t)(t0 % CT) * KB * Cfg::B_BYTES, min(Cfg::KPS, KB) * Cfg::B_BYTES,
+                         &full[Cfg::OFS], pol_b);
+                pdl_wait(); TRACE(2);
+                mbar_arrive_expect_tx(&full[0], KB * 2 * Cfg::SLICE);
+                for (uint32_t kb = 0; kb < KB; kb++) {
+                    const uint8_t* xsrc = Xt + (size_t)kb * 2 * Cfg::SLICE;      // Xt[0][kb][slice]
+                    bulk_g2s(smem + Cfg::OFF_STG + kb * Cfg::SLICE, xsrc, Cfg::SLICE, &full[0], pol_a);
+                    bulk_g2s(smem + Cfg::OFF_A1 + kb * Cfg::SLICE, xsrc + Cfg::SLICE, Cfg::SLICE, &full[0], pol_a);
+                }
+                for (uint32_t s2 = 1; s2 < Cfg::OFS; s2++) mbar_arrive(&full[s2]);
+            }
+            for (uint32_t ti = 0; ti < tiles.count; ti++) {
+                const uint32_t tg = tiles.at(ti), ct = tg % CT;
+                const uint8_t* b_src = jobs.Et[tg / CT] + (size_t)ct * KB * Cfg::B_BYTES;
+                for (uint32_t kp = 0; kp < KP; kp++, it++) {
+                    if (it == 0) continue;                          // issued above
+                    const uint32_t u = it + Cfg::OFS, s = u % Cfg::NSLOT, ph = (u / Cfg::NSLOT) & 1;
+                    const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES);
+                    bulk_g2s(smem + Cfg::RING_BASE + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES,
+                             nkb * Cfg::B_BYTES, &full[s], pol_b);
+                }
+            }
+            if (false)
 #endif
             for (uint32_t ti = 0; ti < tiles.count; ti++) {
                 const uint32_t tg = tiles.at(ti), ct = tg % CT;
@@ -508,6 +561,20 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
             constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = 32
             const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
             uint32_t it = 0;
+            constexpr uint32_t OFS = Cfg::OFS;   // Enc(W) message it -> ring slot (it + OFS) % NSLOT
+#ifdef NIMBUS_RES_X0UP
+            {
+                for (uint32_t s2 = 0; s2 < OFS; s2++) mbar_wait(&full[s2], 0);
+                tc_fence_after();
+                for (uint32_t kb = 0; kb < KB; kb++) {
+                    const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + kb * Cfg::SLICE);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
+                        tmem_cp_128x256b_w(tmem + kb * (Cfg::BK / 4) + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
+                }
+                for (uint32_t s2 = 0; s2 < OFS; s2++) mma_commit_w(&empty[s2]);
+            }
+#endif
             for (uint32_t ti = 0; ti < tiles.count; ti++) {
                 const uint32_t buf = ti & 1, use = ti >> 1;
                 if (ti >= 2) mbar_wait(&tempty[buf], (use & 1) ^ 1);
@@ -515,12 +582,12 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
                 tc_fence_after();
                 const uint32_t dacc = tmem + Cfg::A0_COLS + buf * Cfg::ACC_COLS;
                 for (uint32_t kp = 0; kp < KP; kp++, it++) {
-                    const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
+                    const uint32_t s = (it + OFS) % Cfg::NSLOT, ph = ((it + OFS) / Cfg::NSLOT) & 1;
                     const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
                     mbar_wait(&full[s], ph);
                     if (ti == 1 && kp < 8) TRACE(40 + kp);
                     tc_fence_after();
-                    if (ti == 0) {
+                    if (ti == 0 && OFS == 0) {
                         // first tile: move these k-blocks of slice 0 into TMEM (in issue order with the MMAs)
                         for (uint32_t q = 0; q < nkb; q++) {
                             const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + q * Cfg::SLICE);
@@ -530,11 +597,14 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
                         }
                         mma_commit_w(&sfree[0]);
                     }
+#ifdef NIMBUS_RES_NOMMA
+                    if (ti > 0) { mma_commit_w(&empty[s]); continue; }   // diagnostic (wrong results): stream only
+#endif
                     for (uint32_t q = 0; q < nkb; q++) {
                         const uint32_t kb = kb0 + q;
                         const uint32_t a0t = tmem + kb * (Cfg::BK / 4);                      // slice 0, TMEM
                         const uint32_t a1 = smem_u32(smem + Cfg::OFF_A1 + kb * Cfg::SLICE);  // slice 1, smem
-                        const uint32_t b0 = smem_u32(smem + Cfg::OFF_B + s * Cfg::SLOT + q * Cfg::B_BYTES);
+                        const uint32_t b0 = smem_u32(smem + Cfg::RING_BASE + s * Cfg::SLOT + q * Cfg::B_BYTES);
 #pragma unroll
                         for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
                             const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);

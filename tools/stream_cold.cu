@@ -100,7 +100,7 @@ __global__ void k_read(const uint4* p, size_t n, unsigned long long* sink) {
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const size_t mb = 50;
+    const size_t mb = getenv("MB") ? (size_t)atoi(getenv("MB")) : 50;
     const size_t tile = getenv("TILE_KB") ? (size_t)atoi(getenv("TILE_KB")) * 1024 : 96 * 1024;
     const size_t ntiles = (mb << 20) / tile;
     printf("tile %zu KB\n", tile / 1024);
@@ -112,8 +112,9 @@ int main() {
     unsigned long long* sink;
     cudaMalloc(&sink, 64 * 1024);
     struct V { uint32_t bytes, stages, ctas_per_sm; };
-    const V vs[] = {{32768, 3, 1}, {32768, 4, 1}, {65536, 1, 1}, {65536, 2, 1}, {65536, 3, 1}, {65536, 1, 2},
-                    {131072, 1, 1}, {49152, 2, 1}, {49152, 4, 1}, {98304, 1, 1}, {98304, 2, 1}, {16384, 12, 1}};
+    const V vs[] = {{32768, 3, 1}, {32768, 4, 1}, {32768, 5, 1}, {32768, 6, 1}, {16384, 8, 1}, {16384, 12, 1},
+                    {65536, 1, 1}, {65536, 2, 1}, {65536, 3, 1}, {65536, 1, 2}, {49152, 2, 1}, {49152, 4, 1},
+                    {98304, 1, 1}, {98304, 2, 1}};
     for (const V& v : vs) {
         const size_t smem = (size_t)v.stages * v.bytes + 1024;
         if (smem * v.ctas_per_sm > 228 * 1024 || tile % v.bytes) continue;   // copies must tile the tile
