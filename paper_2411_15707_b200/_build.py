@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 TRACE = os.environ.get("NIMBUS_TRACE") == "1"   # debug timeline build (tools/trace_tc.py)
-VARIANT = os.environ.get("NIMBUS_VARIANT", "")   # experiment macro: -DNIMBUS_<VARIANT>, own .so name
+VARIANT = os.environ.get("NIMBUS_VARIANT", "")   # experiment macros: -DNIMBUS_<V> per "+"-separated V, own .so name
 _SUFFIX = ("_trace" if TRACE else "") + (f"_{VARIANT}" if VARIANT else "")
 LIB = os.path.join(PKG, f"libnimbus_cop{_SUFFIX}.so")
 OBJ = os.path.join(ROOT, "build", f"obj{_SUFFIX}")
@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")] + (["-DNIMBUS_TRACE"] if TRACE else []) \
-    + ([f"-DNIMBUS_{VARIANT.upper()}"] if VARIANT else [])
+    + [f"-DNIMBUS_{v.upper()}" for v in VARIANT.split("+") if v]
 
 
 def _sources():

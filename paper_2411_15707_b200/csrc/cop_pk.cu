@@ -156,9 +156,11 @@ struct PkCfg {
 struct PkUnit {
     uint32_t j, pass, comp, tt, T;
 };
-__device__ __forceinline__ PkUnit pk_decode(const PkParams& P, uint32_t u, uint32_t NT, uint32_t CL, uint32_t rank) {
+// j: the caller's job cursor -- a CTA receives its units in increasing order, so the job search
+// resumes where the previous unit's ended (a scan from job 0 per unit cost ~8% of the pass)
+__device__ __forceinline__ PkUnit pk_decode(const PkParams& P, uint32_t u, uint32_t NT, uint32_t CL, uint32_t rank,
+                                            uint32_t& j) {
     PkUnit x;
-    uint32_t j = 0;
     while (u >= P.job[j].unit_end) j++;
     uint32_t v = u - (j ? P.job[j - 1].unit_end : 0u);
     const uint32_t G = (P.job[j].TT + CL - 1) / CL;
@@ -259,7 +261,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
             const uint64_t pol_e = policy_evict_last();    // an Enc(W) block serves R output tiles x theta tiles
             const uint64_t pol_x = policy_evict_last();    // X blocks serve every J tile
             pdl_wait();                                    // X slices, counter and flags: the slice kernel's
-            uint32_t ie = 0, ix = 0;
+            uint32_t ie = 0, ix = 0, jcur = 0;
             for (uint32_t i = 0;; i++) {
                 uint32_t u;
                 if (rank == 0) {
@@ -276,7 +278,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                     u = take_unit(i, true);
                 }
                 if (u >= total_units) break;
-                const PkUnit U = pk_decode(P, u, NT, CL, rank);
+                const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur);
                 const PkJob& J = P.job[U.j];
                 const bool ghost = U.tt >= J.TT;                      // a cluster's spare theta tile
                 const uint32_t limb = pk_limb(R, U.pass);
@@ -329,7 +331,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         const uint64_t e_desc0 = sdesc_kmajor_sw128(smem_u32(smem));
         const uint64_t x_desc0 = sdesc_kmajor_sw128(smem_u32(smem + Cfg::OFF_X));
         constexpr uint64_t EP = Cfg::P_BYTES >> 4, XP = Cfg::B_BYTES >> 4;
-        uint32_t ie = 0, ix = 0, gc = 0;
+        uint32_t ie = 0, ix = 0, gc = 0, jcur = 0;
         PKS_T0(t_mma0);
         for (uint32_t i = 0;; i++) {
             const uint32_t u = take_unit(i, false);
@@ -339,7 +341,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
             }
             if (u >= total_units) { PKS_ADD(3, t_mma0); break; }
             PKS_INC(7);
-            const PkUnit U = pk_decode(P, u, NT, CL, rank);
+            const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur);
             const uint32_t KB = P.job[U.j].KB, Rr = P.job[U.j].Rr, CKB = P.job[U.j].CKB, NCH = P.job[U.j].NCH;
             const bool ghost = U.tt >= P.job[U.j].TT;
             for (uint32_t c = 0; c < NCH; c++, gc++) {
@@ -399,7 +401,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         if (lane == 0) mbar_arrive(tempty);
 
         uint32_t acc[CPT][8];        // running residue of the unit's limb (mod p_limb)
-        uint32_t gc = 0;
+        uint32_t gc = 0, jcur = 0;
         for (uint32_t i = 0;; i++) {
             const uint32_t u = take_unit(i, false);
             __syncwarp();
@@ -407,7 +409,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                 if (CL > 1 && rank != 0) mbar_arrive_cl(&qempty[i % kPkQ], 0); else mbar_arrive(&qempty[i % kPkQ]);
             }
             if (u >= total_units) break;
-            const PkUnit U = pk_decode(P, u, NT, CL, rank);
+            const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur);
             const PkJob& J = P.job[U.j];
             const bool ghost = U.tt >= J.TT;
             const uint32_t Jc = U.T * Cfg::BM + sub * 32 + lane;         // output coefficient
@@ -434,8 +436,12 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
 #pragma unroll
                     for (uint32_t qq = 0; qq < 8; qq++) {
                         const uint32_t row = (ch0 + ci) * 8 + qq;
-                        rh0[ci][qq] = (ci < nch && row < (uint32_t)RT)
-                                          ? __ldcg(J.rho + ((size_t)(U.tt * RT + row) * 2 + U.comp) * N + Jc) : 0;
+                        rh0[ci][qq] = 0;
+                        // issued here, consumed after the drains (asm volatile: the compiler may not sink the
+                        // load to its use, where its L2 latency would stall the finalize)
+                        if (ci < nch && row < (uint32_t)RT)
+                            asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(rh0[ci][qq])
+                                         : "l"(J.rho + ((size_t)(U.tt * RT + row) * 2 + U.comp) * N + Jc));
                     }
             }
             PKS_ADD(8, t_pre);
@@ -449,6 +455,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                     uint32_t v[Cfg::NACC][8];
                     const uint32_t col = (ch0 + ci) * 8;
                     const bool t4 = Cfg::TAIL == 4 && ch0 + ci == Cfg::NCHK - 1;
+                    PKS_T0(t_ld);
                     if (t4) {
 #pragma unroll
                         for (uint32_t s2 = 0; s2 < Cfg::NACC; s2++) tmem_ld4(tl + s2 * RT + col, v[s2]);
@@ -457,6 +464,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                         for (uint32_t s2 = 0; s2 < Cfg::NACC; s2++) tmem_ld8(tl + s2 * RT + col, v[s2]);
                     }
                     tmem_ld_wait();
+                    PKS_ADD(11, t_ld);
 #pragma unroll
                     for (uint32_t qq = 0; qq < 8; qq++) {
                         uint64_t x = mad_wide(v[1][qq], 1u << 8, v[0][qq]);

@@ -399,7 +399,11 @@ struct ResCfg {
     static constexpr uint32_t ACC_COLS = NACC * BN;            // 160
     static constexpr uint32_t A0_COLS = kResMaxKB * (BK / 4);  // slice 0 in TMEM: 32 columns per k-block
     static constexpr uint32_t TMEM_COLS = 512;
+#ifdef NIMBUS_RES_EPI4
+    static constexpr uint32_t EPI_WARPS = 4;      // experiment: one epilogue warp per sub-partition
+#else
     static constexpr uint32_t EPI_WARPS = 8;
+#endif
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
     // smem: slice 1 resident [KB][16 KB] | slice 0 staging [KPS][16 KB] | E ring [STAGES][32 KB]
     static constexpr uint32_t OFF_A1 = 0, OFF_STG = kResMaxKB * SLICE, OFF_B = OFF_STG + KPS * SLICE;
@@ -637,12 +641,16 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
             mbar_wait(&tfull[buf], use & 1);
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
             tc_fence_after();
+#ifdef NIMBUS_RES_NOEPI
+            if (false)        // diagnostic (wrong results): no epilogue work at all
+#endif
             if (FUSE)
                 epilogue_fused<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
                                                    half, sub * 32 + lane, k, ct * Cfg::BN, ti & 1, hold, fo);
             else
-                epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
-                                                  half, sub * 32 + lane, k, ct * Cfg::BN, ncol, jobs.C[tg / CT]);
+                for (uint32_t hh = 0; hh < 8 / Cfg::EPI_WARPS; hh++)
+                    epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
+                                                      half + hh, sub * 32 + lane, k, ct * Cfg::BN, ncol, jobs.C[tg / CT]);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);

@@ -46,6 +46,9 @@ tot = s[3]
 print(f"kernel {nb.nimbus_last_contraction(ctx)}  pass {e0.elapsed_time(e1):.2f} ms (trace build)  units/CTA {s[7]:.1f}")
 print(f"MMA warp: total {tot/1e6:.1f} Mcyc | wait accum {s[0]/tot:.1%} | wait X {s[1]/tot:.1%} | wait E {s[2]/tot:.1%} | "
       f"issuing {(tot - s[0] - s[1] - s[2])/tot:.1%}")
-print(f"epilogue (per warp): drains {s[4]/8/tot:.1%} | finalize {s[5]/8/tot:.1%} | wait accum {s[6]/8/tot:.1%} | "
-      f"prefetch/flags {s[8]/8/tot:.1%}")
+print(f"epilogue (per warp): drains {s[4]/8/tot:.1%} (of which TMEM loads {s[11]/8/tot:.1%}) | finalize {s[5]/8/tot:.1%} | "
+      f"wait accum {s[6]/8/tot:.1%} | prefetch/flags {s[8]/8/tot:.1%}")
+u = s[7]
+print(f"per unit (avg over {u:.0f}): MMA wait accum {s[0]/u:.0f} cyc, drain {s[4]/8/u:.0f} cyc (loads {s[11]/8/u:.0f}), "
+      f"finalize {s[5]/8/u:.0f} cyc, MMA total {tot/u:.0f} cyc")
 print(f"producer: waiting for free E slots {s[9]/tot:.1%} | X slots {s[10]/tot:.1%}")
