@@ -74,6 +74,14 @@ def step_dist(step_ms):
 
 
 def get_config(key: str):
+    if ":" in key:
+        # diagnostic subset of a stack: "5:down" = C5's FFN-down matmuls only (projections Q K V O up down)
+        import dataclasses
+        base, projs = key.split(":")
+        cfg = get_config(base)
+        keep = [ni._PROJ.index(p) for p in projs.split(",")]
+        return dataclasses.replace(cfg, name=f"{cfg.name}:{projs}",
+                                   layers=tuple(x for x in cfg.layers if x[1] in keep))
     if key == "2qkv":
         return ni.CONFIG_QKV
     if key.endswith("l16"):

@@ -81,8 +81,8 @@ extern "C" int nimbus_pk_stats_set(void* p) { return (int)cudaMemcpyToSymbol(g_p
 #define PKS_T0(v) const long long v = clock64()
 #define PKS_ADD(i, t0) do { pks[i] += (unsigned long long)(clock64() - (t0)); } while (0)
 #define PKS_INC(i) do { pks[i] += 1ull; } while (0)
-#define PKS_DECL unsigned long long pks[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
-#define PKS_FLUSH do { if (g_pk_stats && lane == 0) for (int i_ = 0; i_ < 12; i_++) if (pks[i_]) \
+#define PKS_DECL unsigned long long pks[16] = {0}
+#define PKS_FLUSH do { if (g_pk_stats && lane == 0) for (int i_ = 0; i_ < 16; i_++) if (pks[i_]) \
         atomicAdd(&g_pk_stats[blockIdx.x * 16 + i_], pks[i_]); } while (0)
 #else
 #define PKS_DECL do { } while (0)
@@ -496,19 +496,31 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
             const uint32_t inv0 = ND ? R.inv_p[L - 1][limb] : 0, inv0_sh = ND ? R.inv_p_sh[L - 1][limb] : 0;
             uint32_t* ctsp = J.cts + (((size_t)tg0 * 2 + U.comp) * R.L_out + limb) * N + Jc;
             const size_t cts_row = (size_t)2 * R.L_out * N;
+            // chunk loop NOT unrolled (the chunk's residues are selected out of the register arrays):
+            // one copy of the row body instead of CPT keeps the kernel's hot code inside the
+            // instruction cache (unrolled, ~13% of all warp stalls were instruction fetch)
+#pragma unroll 1
+            for (uint32_t ci = 0; ci < nch; ci++) {
+                uint32_t a8[8];
+                int32_t r8[8];
 #pragma unroll
-            for (uint32_t ci = 0; ci < CPT; ci++) {
-                if (ci >= nch) continue;
+                for (uint32_t qq = 0; qq < 8; qq++) {
+                    a8[qq] = acc[0][qq];
+                    r8[qq] = rh0[0][qq];
+#pragma unroll
+                    for (uint32_t k = 1; k < CPT; k++)
+                        if (ci == k) { a8[qq] = acc[k][qq]; r8[qq] = rh0[k][qq]; }
+                }
 #pragma unroll
                 for (uint32_t qq = 0; qq < 8; qq++, z += gN) {
                     const uint32_t row = (ch0 + ci) * 8 + qq;
                     if (row >= (uint32_t)RT) continue;                            // past a 4-row tail
                     const uint32_t k_row = ci * 8 + qq;                          // row within this thread's rows
                     const uint32_t tg = tg0 + k_row;                              // packed ciphertext (global)
-                    uint32_t v = submod(acc[ci][qq], cr, p);
+                    uint32_t v = submod(a8[qq], cr, p);
                     // earlier dropped limbs: v <- (v - rho_d) p_{L-1-d}^-1 mod p   (|rho| < p_l / 2 < p)
                     if (ndep) {
-                        const int32_t rh = rh0[ci][qq];
+                        const int32_t rh = r8[qq];
                         const uint32_t t = rh < 0 ? addmod(v, (uint32_t)(-rh), p) : submod(v, (uint32_t)rh, p);
                         v = mulmod_shoup(t, inv0, inv0_sh, p);
                         for (uint32_t d = 1; d < ndep; d++) {
@@ -539,12 +551,14 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                     ctsp[(size_t)k_row * cts_row] = v;
                 }
             }
+            PKS_ADD(U.pass < ND ? 13 : 12, t_fin);
             if (U.pass < ND) {
                 __threadfence();
                 epi_bar();
                 if (ew == 0 && lane == 0) st_release(J.flags + U.pass * fl_stride + fl_tile, 1u);
             }
             PKS_ADD(5, t_fin);
+            if (U.pass >= ND) PKS_INC(14);
         }
     }
     PKS_FLUSH;

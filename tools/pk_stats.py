@@ -17,12 +17,16 @@ from paper_2411_15707_b200 import nimbus as nb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=12)
 ap.add_argument("--config", default="5")
+ap.add_argument("--projs", default="Q,K,V,O,up,down", help="projections of each layer to include")
 args = ap.parse_args()
 cfg = ni.CONFIGS[int(args.config)]
+keep = [ni._PROJ.index(p) for p in args.projs.split(",")]
 ctx = nb.nimbus_ctx_create(cfg.N, cfg.L, cfg.ell, cfg.L_out, flags=nb.FLAG_LARGE_K)
 sk = nb.nimbus_keygen(ctx, 1)
 jobs = []
 for li, pj, lay in cfg.layers[: 6 * args.layers]:
+    if pj not in keep:
+        continue
     seed = ni.seed_mm(cfg.cid, li, pj)
     w = nb.nimbus_encrypt_weights(ctx, sk, nb.from_numpy_u32(ni.gen_W(seed, lay.m, lay.n, cfg.ell), "cuda"), seed)
     cts, R = nb.alloc_outputs(ctx, w, lay.k_per_query, lay.n_queries)
@@ -51,4 +55,7 @@ print(f"epilogue (per warp): drains {s[4]/8/tot:.1%} (of which TMEM loads {s[11]
 u = s[7]
 print(f"per unit (avg over {u:.0f}): MMA wait accum {s[0]/u:.0f} cyc, drain {s[4]/8/u:.0f} cyc (loads {s[11]/8/u:.0f}), "
       f"finalize {s[5]/8/u:.0f} cyc, MMA total {tot/u:.0f} cyc")
+uo = max(s[14], 1.0)
+print(f"finalize split (per warp): output passes {s[12]/8/uo:.0f} cyc/unit over {uo:.0f} units, dropped-limb passes "
+      f"{s[13]/8/max(u - uo, 1):.0f} cyc/unit + fence/flag {(s[5] - s[12] - s[13])/8/max(u - uo, 1):.0f}")
 print(f"producer: waiting for free E slots {s[9]/tot:.1%} | X slots {s[10]/tot:.1%}")
