@@ -489,67 +489,93 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
             const uint32_t tg0 = U.tt * RT + ch0 * 8;
             const bool out_pass = U.pass >= ND, masked = out_pass && U.comp == 0;
             const uint64_t gN = 0x9E3779B97F4A7C15ULL * (uint64_t)N;
-            uint64_t z = J.key + 0x9E3779B97F4A7C15ULL * ((uint64_t)tg0 * N + Jc + 1);
+            const uint64_t z = J.key + 0x9E3779B97F4A7C15ULL * ((uint64_t)tg0 * N + Jc + 1);
             const uint32_t ri = Jc / J.n, jj = Jc - ri * J.n;             // R column of this J (valid if ri < R)
             const bool r_col = masked && limb == 0 && J.Rout && ri < J.Rr;
             const uint32_t qy = tg0 / J.nct, th = tg0 - qy * J.nct;
-            const uint32_t inv0 = ND ? R.inv_p[L - 1][limb] : 0, inv0_sh = ND ? R.inv_p_sh[L - 1][limb] : 0;
             uint32_t* ctsp = J.cts + (((size_t)tg0 * 2 + U.comp) * R.L_out + limb) * N + Jc;
             const size_t cts_row = (size_t)2 * R.L_out * N;
             // chunk loop NOT unrolled (the chunk's residues are selected out of the register arrays):
             // one copy of the row body instead of CPT keeps the kernel's hot code inside the
-            // instruction cache (unrolled, ~13% of all warp stalls were instruction fetch)
+            // instruction cache (unrolled, ~13% of all warp stalls were instruction fetch).  Within a
+            // chunk the 8 rows go stage by stage, each stage branch-free (stores predicated): the unit-
+            // uniform decisions sit between stages, so the scheduler interleaves the 8 rows' dependency
+            // chains instead of running one row's ~90 dependent instructions at a time
+            const uint32_t iv_w = ND ? R.inv_p[L - 1][limb] : 0, iv_sh = ND ? R.inv_p_sh[L - 1][limb] : 0;
 #pragma unroll 1
             for (uint32_t ci = 0; ci < nch; ci++) {
-                uint32_t a8[8];
+                uint32_t v8[8];
                 int32_t r8[8];
 #pragma unroll
                 for (uint32_t qq = 0; qq < 8; qq++) {
-                    a8[qq] = acc[0][qq];
-                    r8[qq] = rh0[0][qq];
+                    uint32_t a = acc[0][qq];
+                    int32_t r = rh0[0][qq];
 #pragma unroll
-                    for (uint32_t k = 1; k < CPT; k++)
-                        if (ci == k) { a8[qq] = acc[k][qq]; r8[qq] = rh0[k][qq]; }
+                    for (uint32_t k = 1; k < CPT; k++) {
+                        a = ci == k ? acc[k][qq] : a;
+                        r = ci == k ? rh0[k][qq] : r;
+                    }
+                    v8[qq] = submod(a, cr, p);
+                    r8[qq] = r;
                 }
+                const uint32_t kr0 = ci * 8;                              // first row within this thread's rows
+                const uint32_t nrow = (ch0 + ci) * 8 + 8 <= (uint32_t)RT ? 8u : (uint32_t)RT - (ch0 + ci) * 8;
+                // earlier dropped limbs: v <- (v - rho_d) p_{L-1-d}^-1 mod p   (|rho| < p_l / 2 < p)
+                if (ndep) {
 #pragma unroll
-                for (uint32_t qq = 0; qq < 8; qq++, z += gN) {
-                    const uint32_t row = (ch0 + ci) * 8 + qq;
-                    if (row >= (uint32_t)RT) continue;                            // past a 4-row tail
-                    const uint32_t k_row = ci * 8 + qq;                          // row within this thread's rows
-                    const uint32_t tg = tg0 + k_row;                              // packed ciphertext (global)
-                    uint32_t v = submod(a8[qq], cr, p);
-                    // earlier dropped limbs: v <- (v - rho_d) p_{L-1-d}^-1 mod p   (|rho| < p_l / 2 < p)
-                    if (ndep) {
+                    for (uint32_t qq = 0; qq < 8; qq++) {
                         const int32_t rh = r8[qq];
-                        const uint32_t t = rh < 0 ? addmod(v, (uint32_t)(-rh), p) : submod(v, (uint32_t)rh, p);
-                        v = mulmod_shoup(t, inv0, inv0_sh, p);
-                        for (uint32_t d = 1; d < ndep; d++) {
-                            const uint32_t ld = L - 1 - d;
-                            const int32_t rh1 = __ldcg(J.rho + d * rho_stride + ((size_t)tg * 2 + U.comp) * N + Jc);
-                            const uint32_t t1 = rh1 < 0 ? addmod(v, (uint32_t)(-rh1), p) : submod(v, (uint32_t)rh1, p);
-                            v = mulmod_shoup(t1, R.inv_p[ld][limb], R.inv_p_sh[ld][limb], p);
+                        const uint32_t t = rh < 0 ? addmod(v8[qq], (uint32_t)(-rh), p) : submod(v8[qq], (uint32_t)rh, p);
+                        v8[qq] = mulmod_shoup(t, iv_w, iv_sh, p);
+                    }
+                    for (uint32_t d = 1; d < ndep; d++) {
+                        const uint32_t ld = L - 1 - d;
+                        const uint32_t w = R.inv_p[ld][limb], wsh = R.inv_p_sh[ld][limb];
+                        int32_t rh1[8];
+#pragma unroll
+                        for (uint32_t qq = 0; qq < 8; qq++)
+                            rh1[qq] = qq < nrow ? __ldcg(J.rho + d * rho_stride + ((size_t)(tg0 + kr0 + qq) * 2 + U.comp) * N + Jc)
+                                                : 0;
+#pragma unroll
+                        for (uint32_t qq = 0; qq < 8; qq++) {
+                            const int32_t rh = rh1[qq];
+                            const uint32_t t = rh < 0 ? addmod(v8[qq], (uint32_t)(-rh), p) : submod(v8[qq], (uint32_t)rh, p);
+                            v8[qq] = mulmod_shoup(t, w, wsh, p);
                         }
                     }
-                    if (!out_pass) {
-                        // a dropped limb: keep its centred residue for the later passes
-                        __stcg(J.rho + U.pass * rho_stride + ((size_t)tg * 2 + U.comp) * N + Jc,
-                               v > (p >> 1) ? (int32_t)v - (int32_t)p : (int32_t)v);
-                        continue;
-                    }
-                    if (tg >= J.ntheta) continue;
-                    if (masked) {
-                        const uint32_t rm = (uint32_t)(mix64(z) >> (64 - R.ell));       // word(seed, 6, tg N + J)
-                        v = submod(v, emb_fast(rm, (uint32_t)R.qout_mod_t, R.ell, p, R.t_inv[limb], R.t_inv_sh[limb]), p);
-                        if (r_col) {
-                            // theta of query qy: row theta R + ri of that query, if it exists
-                            const uint32_t thr = th + k_row, qd = thr / J.nct;        // k_row < 32: one division
-                            const uint32_t th2 = thr - qd * J.nct;
-                            if (th2 * J.Rr + ri < J.kq)
-                                J.Rout[((size_t)(qy + qd) * J.kq + th2 * J.Rr + ri) * J.n + jj] = rm;
-                        }
-                    }
-                    ctsp[(size_t)k_row * cts_row] = v;
                 }
+                if (!out_pass) {
+                    // a dropped limb: keep its centred residues for the later passes
+#pragma unroll
+                    for (uint32_t qq = 0; qq < 8; qq++)
+                        if (qq < nrow)
+                            __stcg(J.rho + U.pass * rho_stride + ((size_t)(tg0 + kr0 + qq) * 2 + U.comp) * N + Jc,
+                                   v8[qq] > (p >> 1) ? (int32_t)v8[qq] - (int32_t)p : (int32_t)v8[qq]);
+                    continue;
+                }
+                if (masked) {
+                    uint32_t rm8[8];
+                    const uint64_t zc = z + (uint64_t)kr0 * gN;
+#pragma unroll
+                    for (uint32_t qq = 0; qq < 8; qq++) {
+                        rm8[qq] = (uint32_t)(mix64(zc + qq * gN) >> (64 - R.ell));      // word(seed, 6, tg N + J)
+                        v8[qq] = submod(v8[qq], emb_fast(rm8[qq], (uint32_t)R.qout_mod_t, R.ell, p, R.t_inv[limb],
+                                                          R.t_inv_sh[limb]), p);
+                    }
+                    if (r_col) {
+#pragma unroll
+                        for (uint32_t qq = 0; qq < 8; qq++) {
+                            // theta of query qy: row theta R + ri of that query, if it exists
+                            const uint32_t thr = th + kr0 + qq, qd = thr / J.nct;
+                            const uint32_t th2 = thr - qd * J.nct;
+                            if (qq < nrow && tg0 + kr0 + qq < J.ntheta && th2 * J.Rr + ri < J.kq)
+                                J.Rout[((size_t)(qy + qd) * J.kq + th2 * J.Rr + ri) * J.n + jj] = rm8[qq];
+                        }
+                    }
+                }
+#pragma unroll
+                for (uint32_t qq = 0; qq < 8; qq++)
+                    if (qq < nrow && tg0 + kr0 + qq < J.ntheta) ctsp[(size_t)(kr0 + qq) * cts_row] = v8[qq];
             }
             PKS_ADD(U.pass < ND ? 13 : 12, t_fin);
             if (U.pass < ND) {
