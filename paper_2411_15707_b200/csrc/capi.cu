@@ -292,6 +292,11 @@ nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus
     cudaError_t e = cudaMalloc(&sk->d_s, N);
     if (e == cudaSuccess) e = cudaMalloc(&sk->d_s_ntt, (size_t)L * N * 4);
     if (e == cudaSuccess) e = launch_keygen(ctx, seed, sk->d_s, sk->d_s_ntt, (cudaStream_t)stream);
+    if (e == cudaSuccess && (N == 4096 || N == 8192)) {
+        // s_hat in the fused encrypt kernel's thread order, with Shoup companions (encrypt.cu)
+        e = cudaMalloc(&sk->d_s_enc, (size_t)2 * L * N * 4);
+        if (e == cudaSuccess) e = launch_perm_s(ctx, sk->d_s_ntt, sk->d_s_enc, (cudaStream_t)stream);
+    }
     if (e != cudaSuccess) { nimbus_sk_destroy(sk); return cuda_err(ctx, e, "keygen"); }
     *out = sk;
     return NIMBUS_OK;
@@ -302,6 +307,7 @@ void nimbus_sk_destroy(nimbus_sk* sk) {
     if (!sk) return;
     if (sk->d_s) cudaFree(sk->d_s);
     if (sk->d_s_ntt) cudaFree(sk->d_s_ntt);
+    if (sk->d_s_enc) cudaFree(sk->d_s_enc);
     delete sk;
 }
 
@@ -413,11 +419,17 @@ static nimbus_status want_width(nimbus_ctx* ctx, uint32_t bytes) {
     return NIMBUS_OK;
 }
 
-// encrypt (canonical rows, stream-ordered temporary) and tile into w's resident planes
-// (the canonical rows go to the context's grow-only scratch: a fresh 50-600 MB
-// allocation per call costs more than the kernels; calls on a context are serialised)
+// encrypt straight into w's resident planes (encrypt.cu, N = 4096 / 8192); other ring degrees:
+// canonical rows (stream-ordered temporary) then tile (the canonical rows go to the context's
+// grow-only scratch: a fresh 50-600 MB allocation per call costs more than the kernels; calls on
+// a context are serialised)
 static cudaError_t encrypt_into(nimbus_ctx* ctx, const nimbus_sk* sk, const void* d_W, uint64_t seed,
                                 cudaStream_t s, nimbus_encw* w) {
+    if (sk->d_s_enc && encrypt_planes_ok(ctx)) {
+        cudaError_t e = launch_encrypt_planes(ctx, sk->d_s_enc, d_W, w->m, w->n, seed, w->KB, w->bn, w->d_Et, s);
+        if (e == cudaSuccess) e = launch_pk_corr(ctx, w, s);
+        return e;
+    }
     const size_t need = (size_t)w->m * ncols(ctx) * 4;
     if (ctx->scratch_bytes < need) {
         cudaError_t e = cudaStreamSynchronize(s);         // earlier work may still use the old scratch

@@ -70,6 +70,7 @@ struct nimbus_sk {
     nimbus_ctx* ctx = nullptr;
     int8_t* d_s = nullptr;         // N ternary coefficients
     uint32_t* d_s_ntt = nullptr;   // L x N, NTT domain (bit-reversed order)
+    uint32_t* d_s_enc = nullptr;   // 2 x L x N: s_hat in the fused encrypt's thread order + Shoup (N = 4096 / 8192)
 };
 
 // public key pk = (b, a) (reading 25)
@@ -154,6 +155,11 @@ cudaError_t launch_rerand(nimbus_ctx* c, const uint32_t* d_pk_ntt, uint64_t seed
 cudaError_t launch_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint64_t count, uint64_t* out,
                              cudaStream_t st);
 // layout.cu
+// fused Encrypt rows -> resident planes (encrypt.cu; N = 4096 / 8192)
+bool encrypt_planes_ok(const nimbus_ctx* c);
+cudaError_t launch_perm_s(nimbus_ctx* c, const uint32_t* d_s_ntt, uint32_t* d_s_enc, cudaStream_t st);
+cudaError_t launch_encrypt_planes(nimbus_ctx* c, const uint32_t* d_s_enc, const void* d_W, uint32_t m, uint32_t n,
+                                  uint64_t seed, uint32_t KB, uint32_t bn, uint8_t* d_Et, cudaStream_t st);
 cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m, uint32_t KB, uint32_t bn,
                              uint8_t* d_Et, cudaStream_t st);
 cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t bn,

@@ -7,24 +7,9 @@
 // and transformed in place: Cooley-Tukey forward (natural -> bit-reversed) and
 // Gentleman-Sande inverse (bit-reversed -> natural) with the negacyclic twist
 // psi^i folded into the twiddles, Shoup modular multiplication.
-#include "internal.h"
+#include "ntt_dev.cuh"
 
 namespace nimbus {
-
-// psi_rev[k] = psi^bitrev(k), k in [1, N) used by stage (m, i) as psi_rev[m + i].
-// Two butterfly stages per pass (radix 4 in registers): a thread loads the four
-// elements a pair of consecutive stages couples, so a transform takes
-// ceil(log N / 2) barriers instead of log N.
-__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t S, uint32_t Ssh, uint32_t p) {
-    const uint32_t V = mulmod_shoup(y, S, Ssh, p);
-    y = submod(x, V, p);
-    x = addmod(x, V, p);
-}
-__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint32_t S, uint32_t Ssh, uint32_t p) {
-    const uint32_t U = x;
-    x = addmod(U, y, p);
-    y = mulmod_shoup(submod(U, y, p), S, Ssh, p);
-}
 
 // Cooley-Tukey forward, natural -> bit-reversed order
 __device__ void ntt_fwd_smem(uint32_t* a, const uint32_t* tw, const uint32_t* tw_sh, uint32_t N,
@@ -319,20 +304,6 @@ __global__ void k_decrypt_phase(Rns R, const uint32_t* d_tw, const uint32_t* s_n
 // other stage is CTA-local.  4x the SMs per polynomial: a few dozen packed
 // ciphertexts (C2: 26) no longer leave most of the GPU idle.
 constexpr uint32_t kDecCl = 4;
-
-__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t cta) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
-    return r;
-}
-__device__ __forceinline__ uint32_t ld_dsmem(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_dsmem(uint32_t a, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
-}
 
 // With one output limb (L_out = 1, ell <= 32) the rounding and unpacking of
 // k_decrypt_round are done here too (Z, M non-null; U unused): q' = p_0, so
