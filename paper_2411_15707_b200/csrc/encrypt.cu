@@ -272,7 +272,9 @@ k_encrypt_planes(Rns R, const uint32_t* __restrict__ d_tw, const uint32_t* __res
             }
         }
     }
-    cluster_sync();     // no CTA leaves while a peer may still read its shared memory
+    // no CTA leaves while a peer may still read its shared memory.  Relaxed arrive: the gathered
+    // values were consumed (stored) before it, and a release would wait for those global stores
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
 // s_hat (bit-reversed NTT order, KeyGen) -> the order of the last forward pass's threads:

@@ -29,6 +29,12 @@ WANT = {
     "sm__pipe_tensor_cycles_active.avg": "tensor_active_cycles",
     "lts__t_sectors_srcunit_tex_op_read.sum": "l2_read_sectors_from_sm",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed": "fmaheavy_pct",
+    "sm__inst_executed.avg.per_cycle_active": "ipc",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
+    "sm__inst_executed.sum": "warp_instructions",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "us": 1e-6, "ns": 1e-9,
          "msecond": 1e-3, "ms": 1e-3, "nsecond": 1e-9, "Ghz": 1e9, "GHz": 1e9, "Mhz": 1e6}
