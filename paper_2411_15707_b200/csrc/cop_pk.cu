@@ -796,10 +796,11 @@ static uint32_t max_clusters(nimbus_ctx* c, K kernel, uint32_t CL, size_t smem, 
 }
 
 // CTAs per cluster of the packed contraction: 2 (Enc(W) planes multicast to a theta-tile pair)
-// unless NIMBUS_PK_CL=1
+// unless NIMBUS_PK_CL=1 or 4
 static uint32_t pk_cluster() {
     const char* e = getenv("NIMBUS_PK_CL");
-    return e && atoi(e) == 1 ? 1 : 2;
+    const int v = e ? atoi(e) : 2;
+    return v == 1 || v == 4 ? (uint32_t)v : 2u;
 }
 
 template <int RT, int CL>
@@ -810,8 +811,8 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
     PkParams& P = *Pp;
     cudaError_t e = ensure_smem(c, k_cop_pk<4, RT, CL>, Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    static uint32_t ncl_cache[2][4] = {{0}};
-    uint32_t& ncl = ncl_cache[CL - 1][RT == 48 ? 0 : RT == 52 ? 1 : RT == 56 ? 2 : 3];
+    static uint32_t ncl_cache[3][4] = {{0}};
+    uint32_t& ncl = ncl_cache[CL == 4 ? 2 : CL - 1][RT == 48 ? 0 : RT == 52 ? 1 : RT == 56 ? 2 : 3];
     if (!ncl) ncl = max_clusters(c, k_cop_pk<4, RT, CL>, CL, Cfg::SMEM, Cfg::THREADS);
     const uint32_t NT = c->rns.N / kBNW, ND = c->rns.L - c->rns.L_out;
     for (uint32_t base = 0; base < count; base += kPkMaxJobs) {
@@ -873,8 +874,10 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
 template <int RT>
 static cudaError_t launch_pk_cl(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
                                 void (*mark)(nimbus_ctx*, cudaStream_t)) {
-    return pk_cluster() == 2 ? launch_pk_rt<RT, 2>(c, jobs, count, d_ctr, st, mark)
-                             : launch_pk_rt<RT, 1>(c, jobs, count, d_ctr, st, mark);
+    const uint32_t cl = pk_cluster();
+    return cl == 2 ? launch_pk_rt<RT, 2>(c, jobs, count, d_ctr, st, mark)
+           : cl == 4 ? launch_pk_rt<RT, 4>(c, jobs, count, d_ctr, st, mark)
+                     : launch_pk_rt<RT, 1>(c, jobs, count, d_ctr, st, mark);
 }
 
 cudaError_t launch_cop_packed(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t rt, uint32_t* d_ctr,
