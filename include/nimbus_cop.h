@@ -76,6 +76,9 @@ typedef struct nimbus_pk nimbus_pk;
  * p = 1 mod 2N), uploads NTT twiddles and RNS constants to
  * `device`.  Fails with NIMBUS_EARCH off sm_100. */
 nimbus_status nimbus_ctx_create(const nimbus_params* params, int device, nimbus_ctx** out);
+/* Drops the caller's reference.  Every handle made from the context (sk, pk, encw,
+ * plainw) holds one too, so handles may be destroyed before or after the context, in
+ * any order; the device memory of the context goes with the last reference. */
 void nimbus_ctx_destroy(nimbus_ctx* ctx);
 /* Writes the L primes to out_primes[L] (host). */
 nimbus_status nimbus_ctx_primes(const nimbus_ctx* ctx, uint32_t* out_primes);

@@ -237,9 +237,17 @@ nimbus_status nimbus_ctx_create(const nimbus_params* prm, int device, nimbus_ctx
     return NIMBUS_OK;
 }
 
-void nimbus_ctx_destroy(nimbus_ctx* ctx) {
-    DevGuard dg_(ctx, __func__);
-    if (!ctx) return;
+static void ctx_retain(nimbus_ctx* ctx) { ctx->refs.fetch_add(1, std::memory_order_relaxed); }
+
+static void ctx_free(nimbus_ctx* ctx);
+static void ctx_release(nimbus_ctx* ctx) {
+    if (ctx && ctx->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) ctx_free(ctx);
+}
+
+void nimbus_ctx_destroy(nimbus_ctx* ctx) { ctx_release(ctx); }
+
+static void ctx_free(nimbus_ctx* ctx) {
+    DevGuard dg_(ctx, "nimbus_ctx_destroy");
     if (ctx->d_tw) cudaFree(ctx->d_tw);
     if (ctx->d_scratch) cudaFree(ctx->d_scratch);
     if (ctx->d_flag) cudaFree(ctx->d_flag);
@@ -288,6 +296,7 @@ nimbus_status nimbus_keygen(nimbus_ctx* ctx, uint64_t seed, void* stream, nimbus
     nimbus_sk* sk = new (std::nothrow) nimbus_sk();
     if (!sk) return NIMBUS_ENOMEM;
     sk->ctx = ctx;
+    ctx_retain(ctx);
     const uint32_t N = ctx->rns.N, L = ctx->rns.L;
     cudaError_t e = cudaMalloc(&sk->d_s, N);
     if (e == cudaSuccess) e = cudaMalloc(&sk->d_s_ntt, (size_t)L * N * 4);
@@ -308,7 +317,9 @@ void nimbus_sk_destroy(nimbus_sk* sk) {
     if (sk->d_s) cudaFree(sk->d_s);
     if (sk->d_s_ntt) cudaFree(sk->d_s_ntt);
     if (sk->d_s_enc) cudaFree(sk->d_s_enc);
+    nimbus_ctx* ctx = sk->ctx;
     delete sk;
+    ctx_release(ctx);
 }
 
 nimbus_status nimbus_sk_export(const nimbus_sk* sk, int8_t* d_s, void* stream) {
@@ -327,6 +338,7 @@ nimbus_status nimbus_keygen_pk(nimbus_ctx* ctx, const nimbus_sk* sk, uint64_t se
     nimbus_pk* pk = new (std::nothrow) nimbus_pk();
     if (!pk) return NIMBUS_ENOMEM;
     pk->ctx = ctx;
+    ctx_retain(ctx);
     const size_t words = 2ull * ctx->rns.L * ctx->rns.N;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMalloc(&pk->d_pk, words * 4);
@@ -343,7 +355,9 @@ void nimbus_pk_destroy(nimbus_pk* pk) {
     if (!pk) return;
     if (pk->d_pk) cudaFree(pk->d_pk);
     if (pk->d_pk_ntt) cudaFree(pk->d_pk_ntt);
+    nimbus_ctx* ctx = pk->ctx;
     delete pk;
+    ctx_release(ctx);
 }
 
 nimbus_status nimbus_pk_export(const nimbus_pk* pk, uint32_t* d_out, void* stream) {
@@ -362,6 +376,7 @@ nimbus_status nimbus_pk_import(nimbus_ctx* ctx, const uint32_t* d_in, void* stre
     nimbus_pk* pk = new (std::nothrow) nimbus_pk();
     if (!pk) return NIMBUS_ENOMEM;
     pk->ctx = ctx;
+    ctx_retain(ctx);
     const size_t words = 2ull * ctx->rns.L * ctx->rns.N;
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaMalloc(&pk->d_pk, words * 4);
@@ -406,6 +421,7 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
         cudaError_t e = cudaMalloc(&w->d_corr, 2 * ncols(ctx) * 4);
         if (e != cudaSuccess) { if (w->d_Et) cudaFree(w->d_Et); delete w; return cuda_err(ctx, e, "encw corr alloc"); }
     }
+    ctx_retain(ctx);
     *out = w;
     return NIMBUS_OK;
 }
@@ -504,7 +520,9 @@ void nimbus_encw_destroy(nimbus_encw* w) {
     if (w->d_Et) cudaFree(w->d_Et);
     if (w->d_corr) cudaFree(w->d_corr);
     if (w->h_Et) cudaFreeHost(w->h_Et);
+    nimbus_ctx* ctx = w->ctx;
     delete w;
+    ctx_release(ctx);
 }
 
 static bool read_at(const char* path, uint64_t off, uint8_t* dst, uint64_t bytes);
@@ -1616,6 +1634,7 @@ nimbus_status nimbus_plain_weights_u64(nimbus_ctx* ctx, const uint64_t* d_W, uin
     if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "plain weights alloc"); }
     e = launch_tile_plainw64(ctx, d_W, m, n, w->KB, w->d_Wt, (cudaStream_t)stream);
     if (e != cudaSuccess) { cudaFree(w->d_Wt); delete w; return cuda_err(ctx, e, "tile plain weights"); }
+    ctx_retain(ctx);
     *out = w;
     return NIMBUS_OK;
 }
@@ -1636,6 +1655,7 @@ nimbus_status nimbus_plain_weights(nimbus_ctx* ctx, const uint32_t* d_W, uint32_
     if (e != cudaSuccess) { delete w; return cuda_err(ctx, e, "plain weights alloc"); }
     e = launch_tile_plainw(ctx, d_W, m, n, w->KB, w->d_Wt, (cudaStream_t)stream);
     if (e != cudaSuccess) { cudaFree(w->d_Wt); delete w; return cuda_err(ctx, e, "tile plain weights"); }
+    ctx_retain(ctx);
     *out = w;
     return NIMBUS_OK;
 }
@@ -1644,7 +1664,9 @@ void nimbus_plainw_destroy(nimbus_plainw* w) {
     DevGuard dg_(w ? w->ctx : nullptr, __func__);
     if (!w) return;
     if (w->d_Wt) cudaFree(w->d_Wt);
+    nimbus_ctx* ctx = w->ctx;
     delete w;
+    ctx_release(ctx);
 }
 
 struct ServerWs {

@@ -66,12 +66,23 @@ extern "C" int nimbus_trace_set(void* p) { return (int)cudaMemcpyToSymbol(g_trac
 #endif
 
 // ------------------------------------------------------------------ epilogue
+// The epilogue warp has its accumulators in registers: hand the TMEM set back to the MMA
+// issuer before the recombination / reduction / stores (warp-converged; one arrive per warp),
+// so the next tile's MMAs into this set overlap the epilogue's arithmetic.
+__device__ __forceinline__ void acc_release(uint64_t* bar) {
+    tc_fence_before();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
+// ------------------------------------------------------------------ epilogue
 // Warp (sub, half) drains rows [32 sub, 32 sub + 32) and half of the BN
 // columns of one accumulator set: CPW chunks of 8 columns, BATCH chunks of
 // tcgen05.ld per wait.  tacc = TMEM address of acc_0 for lane 32 sub.
 template <uint32_t NACC, uint32_t BN>
 __device__ __forceinline__ void epilogue_tile(const Rns& R, uint32_t tacc, uint32_t half, uint32_t row, uint32_t k,
-                                              uint32_t col_base, uint32_t ncol, uint32_t* __restrict__ C) {
+                                              uint32_t col_base, uint32_t ncol, uint32_t* __restrict__ C,
+                                              uint64_t* rel = nullptr) {
     constexpr uint32_t CPW = BN / 8 / 2;
     constexpr uint32_t BATCH = (NACC * 8 * CPW <= 128) ? CPW : 1;
 #pragma unroll 1
@@ -82,6 +93,7 @@ __device__ __forceinline__ void epilogue_tile(const Rns& R, uint32_t tacc, uint3
 #pragma unroll
             for (uint32_t s = 0; s < NACC; s++) tmem_ld8(tacc + s * BN + (half * CPW + c0 + b) * 8, v[b][s]);
         tmem_ld_wait();
+        if (rel && c0 + BATCH >= CPW) acc_release(rel);   // last load done: the MMA may reuse the set
 #pragma unroll
         for (uint32_t b = 0; b < BATCH; b++) {
             const uint32_t col0 = col_base + (half * CPW + c0 + b) * 8;
@@ -137,10 +149,36 @@ struct FuseOut {
     uint32_t n;
 };
 
+// The mask of 8 consecutive slots (row, J..J+7) of component 0: r = word(seed, 6, row N + J + 1 + u)
+// >> (64 - ell) is stored to R (the slots J + u < n), and Emb_{q'}(r) mod p_0 is returned in emb.
+__device__ __forceinline__ void fused_mask8(const Rns& R, const FuseOut& fo, uint32_t row, uint32_t J,
+                                            uint32_t (&emb)[8]) {
+    uint64_t z = fo.key + 0x9E3779B97F4A7C15ULL * ((uint64_t)row * R.N + J + 1);
+    uint32_t rm[8];
+#pragma unroll
+    for (uint32_t u = 0; u < 8; u++, z += 0x9E3779B97F4A7C15ULL) {
+        rm[u] = (uint32_t)(mix64(z) >> (64 - R.ell));
+        emb[u] = emb_fast16(rm[u], (uint32_t)R.qout_mod_t, R.ell, R.p[0], R.t_inv[0], R.t_inv_sh[0]);
+    }
+    if (!fo.Rout) return;
+    uint32_t* rdst = fo.Rout + (size_t)row * fo.n + J;
+    if (fo.n % 4 == 0 && J + 8 <= fo.n) {          // 16-byte aligned: J % 8 == 0, n % 4 == 0
+        reinterpret_cast<uint4*>(rdst)[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
+        reinterpret_cast<uint4*>(rdst)[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
+    } else {
+#pragma unroll
+        for (uint32_t u = 0; u < 8; u++)
+            if (J + u < fo.n) rdst[u] = rm[u];
+    }
+}
+
+// pre: the component-0 masks of this tile were computed (and R stored) ahead of time, while the
+// epilogue warps waited for their first accumulators (fused_mask8 into pre); else computed here.
 template <uint32_t NACC, uint32_t BN>
 __device__ __forceinline__ void epilogue_fused(const Rns& R, uint32_t tacc, uint32_t half, uint32_t row, uint32_t k,
                                                uint32_t col_base, bool second, uint32_t (&hold)[BN / 16][8],
-                                               const FuseOut& fo) {
+                                               const FuseOut& fo, uint64_t* rel, bool use_pre,
+                                               const uint32_t (&pre)[BN / 16][8]) {
     constexpr uint32_t CPW = BN / 8 / 2;
     uint32_t v[CPW][NACC][8];
 #pragma unroll
@@ -148,6 +186,7 @@ __device__ __forceinline__ void epilogue_fused(const Rns& R, uint32_t tacc, uint
 #pragma unroll
         for (uint32_t s = 0; s < NACC; s++) tmem_ld8(tacc + s * BN + (half * CPW + b) * 8, v[b][s]);
     tmem_ld_wait();
+    acc_release(rel);                                   // accumulators in registers: free the set
     if (row >= k) return;
     const uint32_t N = R.N, limb = second ? 1 : 0;
     const uint32_t p = R.p[limb], c32 = R.c32[limb];
@@ -172,35 +211,28 @@ __device__ __forceinline__ void epilogue_fused(const Rns& R, uint32_t tacc, uint
         const uint32_t col0 = col_base + (half * CPW + b) * 8;
         const uint32_t comp = col0 / (2 * N), J = col0 % N;
         const uint32_t p0 = R.p[0], p1 = R.p[1];
-        uint64_t z = fo.key + 0x9E3779B97F4A7C15ULL * ((uint64_t)row * N + J + 1);
-        uint32_t out[8], rm[8];
+        uint32_t out[8], emb[8];
+        if (comp == 0) {
+            if (use_pre) {
 #pragma unroll
-        for (uint32_t u = 0; u < 8; u++, z += 0x9E3779B97F4A7C15ULL) {
+                for (uint32_t u = 0; u < 8; u++) emb[u] = pre[b][u];
+            } else {
+                fused_mask8(R, fo, row, J, emb);
+            }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < 8; u++) {
             const uint32_t c = res[u];
             const bool neg = c > (p1 >> 1);                 // centered rho = c - p_1 < 0
             const uint32_t mag = neg ? p1 - c : c;
             const uint32_t d = neg ? addmod(hold[b][u], mag, p0) : submod(hold[b][u], mag, p0);
             uint32_t o = mulmod_shoup(d, R.inv_p[1][0], R.inv_p_sh[1][0], p0);
-            if (comp == 0) {
-                rm[u] = (uint32_t)(mix64(z) >> (64 - R.ell));
-                o = submod(o, emb_fast16(rm[u], (uint32_t)R.qout_mod_t, R.ell, p0, R.t_inv[0], R.t_inv_sh[0]), p0);
-            }
+            if (comp == 0) o = submod(o, emb[u], p0);
             out[u] = o;
         }
         uint4* dst = reinterpret_cast<uint4*>(fo.cts + ((size_t)row * 2 + comp) * N + J);
         dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
         dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
-        if (comp == 0 && fo.Rout) {
-            uint32_t* rdst = fo.Rout + (size_t)row * fo.n + J;
-            if (fo.n % 4 == 0 && J + 8 <= fo.n) {          // 16-byte aligned: J % 8 == 0, n % 4 == 0
-                reinterpret_cast<uint4*>(rdst)[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
-                reinterpret_cast<uint4*>(rdst)[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
-            } else {
-#pragma unroll
-                for (uint32_t u = 0; u < 8; u++)
-                    if (J + u < fo.n) rdst[u] = rm[u];
-            }
-        }
     }
 }
 
@@ -364,10 +396,7 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
             tc_fence_after();
             epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + buf * Cfg::BUF_STRIDE, half,
-                                             mt * Cfg::BM + sub * 32 + lane, k, ct * Cfg::BN, ncol, C);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
+                                             mt * Cfg::BM + sub * 32 + lane, k, ct * Cfg::BN, ncol, C, &tempty[buf]);
             if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
         }
     }
@@ -381,43 +410,40 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
 }
 
 // ------------------------------------------------------------------ resident-X kernel
+// Shared memory: slice 1 of X resident (96 KB) and four 32 KB slots.  In the first tile the
+// slots hold Enc(W) k-block pairs (slots 0, 1) and slice 0 of X on its way to TMEM (slots 2, 3),
+// so that both Enc(W) and X of the first two k-block pairs, and all of slice 1, are requested in
+// ONE round trip (the first tile used to wait for three: slice 0 went through one 32 KB staging
+// buffer, pair by pair).  From the second tile on all four slots carry Enc(W) (128 KB in flight).
 struct ResCfg {
     static constexpr uint32_t BM = kBM, BN = kBNR, BK = kBK, SX = 2;
     static constexpr uint32_t SLICE = BM * BK;                 // one X slice, one k-block: 16 KB
     static constexpr uint32_t B_BYTES = kSW * BN * BK;         // Enc(W) per k-block: 16 KB
-#ifdef NIMBUS_RES_KPS1
-    // experiment: one k-block (16 KB) per slot, 7 slots, a 16 KB slice-0 staging buffer
-    static constexpr uint32_t KPS = 1;
+    static constexpr uint32_t KPS = 2;                         // k-blocks per slot: one 32 KB bulk copy
     static constexpr uint32_t SLOT = KPS * B_BYTES;
-    static constexpr uint32_t STAGES = 7;
-#else
-    static constexpr uint32_t KPS = 2;                         // k-blocks per ring slot: one 32 KB bulk copy
-    static constexpr uint32_t SLOT = KPS * B_BYTES;
-    static constexpr uint32_t STAGES = 96 * 1024 / SLOT;       // 96 KB ring
-#endif
+    static constexpr uint32_t NSLOT = 4;
     static constexpr uint32_t NACC = SX + kSW - 1;             // 5
     static constexpr uint32_t ACC_COLS = NACC * BN;            // 160
     static constexpr uint32_t A0_COLS = kResMaxKB * (BK / 4);  // slice 0 in TMEM: 32 columns per k-block
     static constexpr uint32_t TMEM_COLS = 512;
-#ifdef NIMBUS_RES_EPI4
-    static constexpr uint32_t EPI_WARPS = 4;      // experiment: one epilogue warp per sub-partition
-#else
     static constexpr uint32_t EPI_WARPS = 8;
-#endif
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
-    // smem: slice 1 resident [KB][16 KB] | slice 0 staging [KPS][16 KB] | E ring [STAGES][32 KB]
-    static constexpr uint32_t OFF_A1 = 0, OFF_STG = kResMaxKB * SLICE, OFF_B = OFF_STG + KPS * SLICE;
-#ifdef NIMBUS_RES_X0UP
-    // X up front (see the producer): the Enc(W) ring is the staging buffer plus the 3 slots, 4 x 32 KB,
-    // slice 0 occupying its first 3 slots until it is copied into TMEM; message it -> slot (it + 3) % 4
-    static constexpr uint32_t RING_BASE = OFF_STG, NSLOT = STAGES + 1, OFS = STAGES;
-#else
-    static constexpr uint32_t RING_BASE = OFF_B, NSLOT = STAGES, OFS = 0;
-#endif
-    static constexpr size_t SMEM = (size_t)OFF_B + STAGES * SLOT + 1024 + 256;
+    // smem: slice 1 resident [KB][16 KB] | slots [4][32 KB] | barriers
+    static constexpr uint32_t OFF_A1 = 0, OFF_S = kResMaxKB * SLICE;
+    static constexpr uint32_t OFF_BAR = OFF_S + NSLOT * SLOT;
+    static constexpr size_t SMEM = (size_t)OFF_BAR + 1024 + 256;
     static_assert(A0_COLS + 2 * ACC_COLS <= TMEM_COLS, "TMEM budget");
     static_assert(SMEM <= 232448, "shared memory");
+    static_assert(KPS * SLICE == SLOT, "a slot holds one k-block pair of slice 0");
+    static_assert((kResMaxKB + KPS - 1) / KPS <= 3, "the first tile has at most 3 k-block pairs");
 };
+
+// Slot of Enc(W) message `it` >= KP (second tile on): the slots in the order the first tile
+// frees them (its pair kp uses Enc(W) slot kp & 1 and slice-0 slot 2 + (kp & 1)), 4 nibbles per KP.
+__device__ __forceinline__ uint32_t res_slot(uint32_t it, uint32_t KP) {
+    const uint32_t order = KP == 3 ? 0x0213u : KP == 2 ? 0x1302u : 0x0231u;
+    return (order >> (4 * ((it - KP) & 3))) & 0xFu;
+}
 
 // Several matmuls that share X (Q, K, V of a layer) run as one launch: the
 // column tiles of their Enc(W)s are one tile sequence (tile t = job t / CT, tile t % CT), so X is
@@ -430,20 +456,19 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
     const TileSeq<FUSE> tiles(FUSE ? CT : CT * jobs.nj, R.N, Cfg::BN);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_B + Cfg::STAGES * Cfg::SLOT);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
     uint64_t* empty = full + Cfg::NSLOT;
     uint64_t* tfull = empty + Cfg::NSLOT;
     uint64_t* tempty = tfull + 2;
-    uint64_t* sfree = tempty + 2;                 // slice-0 staging slot free (tcgen05.cp done)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
+    auto slot_ptr = [&](uint32_t s) { return smem + Cfg::OFF_S + s * Cfg::SLOT; };
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) TRACE(0);
     if (warp == 0 && lane == 0) {
         for (uint32_t s = 0; s < Cfg::NSLOT; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (uint32_t b = 0; b < 2; b++) {
-            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); mbar_init(&sfree[b], 1);
-        }
+        for (uint32_t b = 0; b < 2; b++) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -458,102 +483,71 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- producer: E every tile (32 KB copies = 2 k-blocks); X slices in the first tile
+            // ---------------- producer
             const uint64_t pol_a = policy_evict_last();
             const uint64_t pol_b = policy_evict_first();
-            const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
-            uint32_t it = 0;
-#ifdef NIMBUS_E3
-            // every ring slot of the first tile gets its Enc(W) copy before the PDL wait: in a
-            // chain of calls this runs while the previous call's pack and this call's slice finish
-            const uint32_t pre = min(KP, Cfg::STAGES);
-            for (uint32_t kp = 0; kp < pre; kp++) {
-                const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
-                mbar_arrive_expect_tx(&full[kp], nkb * Cfg::B_BYTES + nkb * 2 * Cfg::SLICE);
-                // the CTA's first tile is tiles.at(0) (not blockIdx.x: the FUSE pair order differs)
-                const uint32_t t0 = tiles.at(0);
-                bulk_g2s(smem + Cfg::OFF_B + kp * Cfg::SLOT, jobs.Et[t0 / CT] + (size_t)(t0 % CT) * KB * Cfg::B_BYTES +
-                         (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[kp], pol_b);
-            }
+            // every use of a slot is released by one commit of the MMA issuer on empty[slot]
+            uint32_t par = 0, seen = 0;
+            auto acquire = [&](uint32_t s) {
+                const uint32_t bit = 1u << s;
+                if (seen & bit) mbar_wait(&empty[s], ((par & bit) ? 1u : 0u) ^ 1u);
+                par ^= bit;
+                seen |= bit;
+            };
+            // first tile: pairs 0 and 1 -- Enc(W) (immutable: fetched before the PDL wait), slice 0 of
+            // X into slots 2, 3, all of slice 1 into its resident place -- in one round trip
+            const uint32_t t0 = tiles.at(0);
+            const uint8_t* e0 = jobs.Et[t0 / CT] + (size_t)(t0 % CT) * KB * Cfg::B_BYTES;
+            const uint32_t P0 = KP < 2 ? KP : 2;
+#ifdef NIMBUS_RES_XODD
+            const bool nox = blockIdx.x & 1;    // diagnostic (wrong results): odd CTAs skip X (half the L2 hot-line reads)
 #else
-            const uint32_t pre = 0;
+            constexpr bool nox = false;
 #endif
-#ifdef NIMBUS_RES_X0UP
-            // X up front: all of the X slices in one round trip -- slice 0 into the staging buffer and
-            // ring slots 0-1 (contiguous, 96 KB), slice 1 into its resident place, on full[0]'s phase 0
-            // (full[1]'s phase 0 is a plain arrive); the MMA issuer copies slice 0 into TMEM and frees
-            // slots 0-1 (empty[0], empty[1] phase 0).  Enc(W) message `it` then uses ring slot
-            // (it + 2) % STAGES, its first copy (slot 2) issued before the PDL wait.
-            {
-                const uint32_t t0 = tiles.at(0);
-                mbar_arrive_expect_tx(&full[Cfg::OFS], min(Cfg::KPS, KB) * Cfg::B_BYTES);
-                bulk_g2s(smem + Cfg::RING_BASE + Cfg::OFS * Cfg::SLOT,
-                         jobs.Et[t0 / CT] + (size_t)(t0 % CT) * KB * Cfg::B_BYTES, min(Cfg::KPS, KB) * Cfg::B_BYTES,
-                         &full[Cfg::OFS], pol_b);
-                pdl_wait(); TRACE(2);
-                mbar_arrive_expect_tx(&full[0], KB * 2 * Cfg::SLICE);
-                for (uint32_t kb = 0; kb < KB; kb++) {
-                    const uint8_t* xsrc = Xt + (size_t)kb * 2 * Cfg::SLICE;      // Xt[0][kb][slice]
-                    bulk_g2s(smem + Cfg::OFF_STG + kb * Cfg::SLICE, xsrc, Cfg::SLICE, &full[0], pol_a);
-                    bulk_g2s(smem + Cfg::OFF_A1 + kb * Cfg::SLICE, xsrc + Cfg::SLICE, Cfg::SLICE, &full[0], pol_a);
-                }
-                for (uint32_t s2 = 1; s2 < Cfg::OFS; s2++) mbar_arrive(&full[s2]);
+            for (uint32_t kp = 0; kp < P0; kp++) {
+                const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
+                acquire(kp);
+                acquire(2 + kp);
+                mbar_arrive_expect_tx(&full[kp], nkb * Cfg::B_BYTES +
+                                      (nox ? 0u : nkb * Cfg::SLICE + (kp == 0 ? KB * Cfg::SLICE : 0)));
+                bulk_g2s(slot_ptr(kp), e0 + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[kp], pol_b);
             }
-            for (uint32_t ti = 0; ti < tiles.count; ti++) {
+            pdl_wait();
+            TRACE(2);
+            if (!nox)
+            for (uint32_t kb = 0; kb < KB; kb++)        // Xt[0][kb][slice]
+                bulk_g2s(smem + Cfg::OFF_A1 + kb * Cfg::SLICE, Xt + ((size_t)kb * 2 + 1) * Cfg::SLICE, Cfg::SLICE,
+                         &full[0], pol_a);
+            for (uint32_t kp = 0; kp < P0; kp++) {
+                const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
+                if (!nox)
+                for (uint32_t q = 0; q < nkb; q++)
+                    bulk_g2s(slot_ptr(2 + kp) + q * Cfg::SLICE, Xt + (size_t)(kb0 + q) * 2 * Cfg::SLICE, Cfg::SLICE,
+                             &full[kp], pol_a);
+            }
+            if (KP == 3) {                              // pair 2 reuses pair 0's slots
+                const uint32_t kb0 = 2 * Cfg::KPS, nkb = KB - kb0;
+                acquire(0);
+                acquire(2);
+                mbar_arrive_expect_tx(&full[0], nkb * (Cfg::B_BYTES + (nox ? 0u : Cfg::SLICE)));
+                bulk_g2s(slot_ptr(0), e0 + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[0], pol_b);
+                if (!nox)
+                for (uint32_t q = 0; q < nkb; q++)
+                    bulk_g2s(slot_ptr(2) + q * Cfg::SLICE, Xt + (size_t)(kb0 + q) * 2 * Cfg::SLICE, Cfg::SLICE,
+                             &full[0], pol_a);
+            }
+            // later tiles: Enc(W) only, through all four slots
+            uint32_t it = KP;
+            for (uint32_t ti = 1; ti < tiles.count; ti++) {
                 const uint32_t tg = tiles.at(ti), ct = tg % CT;
                 const uint8_t* b_src = jobs.Et[tg / CT] + (size_t)ct * KB * Cfg::B_BYTES;
                 for (uint32_t kp = 0; kp < KP; kp++, it++) {
-                    if (it == 0) continue;                          // issued above
-                    const uint32_t u = it + Cfg::OFS, s = u % Cfg::NSLOT, ph = (u / Cfg::NSLOT) & 1;
+                    const uint32_t s = res_slot(it, KP);
                     const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
-                    mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES);
-                    bulk_g2s(smem + Cfg::RING_BASE + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES,
-                             nkb * Cfg::B_BYTES, &full[s], pol_b);
-                }
-            }
-            if (false)
-#endif
-            for (uint32_t ti = 0; ti < tiles.count; ti++) {
-                const uint32_t tg = tiles.at(ti), ct = tg % CT;
-                const uint8_t* b_src = jobs.Et[tg / CT] + (size_t)ct * KB * Cfg::B_BYTES;
-                for (uint32_t kp = 0; kp < KP; kp++, it++) {
-                    const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
-                    const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
-                    if (it >= Cfg::STAGES) mbar_wait(&empty[s], ph ^ 1);
+                    acquire(s);
                     if (ti == 1 && kp < 8) TRACE(52 + kp);
-                    const bool first = ti == 0;
-                    if (it >= pre) {
-                        mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES + (first ? nkb * 2 * Cfg::SLICE : 0));
-                        bulk_g2s(smem + Cfg::OFF_B + s * Cfg::SLOT, b_src + (size_t)kb0 * Cfg::B_BYTES,
-                                 nkb * Cfg::B_BYTES, &full[s], pol_b);
-                    }
-                    if (first) {
-                        if (kp == 0) {
-#ifdef NIMBUS_PF
-                            // while the predecessors (previous pack, this slice) finish, pull the rest of
-                            // this CTA's Enc(W) tiles towards L2: DRAM is otherwise idle until X is ready
-                            const uint32_t tb = KB * Cfg::B_BYTES;
-                            if (KB > Cfg::KPS) prefetch_l2_bulk(b_src + Cfg::SLOT, tb - Cfg::SLOT);
-                            for (uint32_t t2 = 1; t2 < tiles.count; t2++)
-                                prefetch_l2_bulk(jobs.Et[tiles.at(t2) / CT] + (size_t)(tiles.at(t2) % CT) * tb, tb);
-#endif
-#ifdef NIMBUS_PF1
-                            // lighter: only the next tile of this CTA
-                            if (tiles.count > 1)
-                                prefetch_l2_bulk(jobs.Et[tiles.at(1) / CT] + (size_t)(tiles.at(1) % CT) * KB * Cfg::B_BYTES,
-                                                 KB * Cfg::B_BYTES);
-#endif
-                            pdl_wait(); TRACE(2);
-                        }
-                        else mbar_wait(&sfree[0], (kp - 1) & 1);       // staging copied into TMEM
-                        for (uint32_t q = 0; q < nkb; q++) {
-                            const uint8_t* xsrc = Xt + (size_t)(kb0 + q) * 2 * Cfg::SLICE;   // Xt[0][kb][slice]
-                            bulk_g2s(smem + Cfg::OFF_STG + q * Cfg::SLICE, xsrc, Cfg::SLICE, &full[s], pol_a);
-                            bulk_g2s(smem + Cfg::OFF_A1 + (kb0 + q) * Cfg::SLICE, xsrc + Cfg::SLICE, Cfg::SLICE,
-                                     &full[s], pol_a);
-                        }
-                    }
+                    mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES);
+                    bulk_g2s(slot_ptr(s), b_src + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[s], pol_b);
                 }
             }
         }
@@ -563,22 +557,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
             constexpr uint32_t idesc_full = idesc_i8(Cfg::BM, kSW * Cfg::BN);        // N = 128
             constexpr uint32_t idesc_lo = idesc_i8(Cfg::BM, (kSW - 1) * Cfg::BN);    // N = 96
             constexpr uint32_t idesc_one = idesc_i8(Cfg::BM, Cfg::BN);               // N = 32
-            const uint32_t KP = (KB + Cfg::KPS - 1) / Cfg::KPS;
-            uint32_t it = 0;
-            constexpr uint32_t OFS = Cfg::OFS;   // Enc(W) message it -> ring slot (it + OFS) % NSLOT
-#ifdef NIMBUS_RES_X0UP
-            {
-                for (uint32_t s2 = 0; s2 < OFS; s2++) mbar_wait(&full[s2], 0);
-                tc_fence_after();
-                for (uint32_t kb = 0; kb < KB; kb++) {
-                    const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + kb * Cfg::SLICE);
-#pragma unroll
-                    for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
-                        tmem_cp_128x256b_w(tmem + kb * (Cfg::BK / 4) + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
-                }
-                for (uint32_t s2 = 0; s2 < OFS; s2++) mma_commit_w(&empty[s2]);
-            }
-#endif
+            uint32_t it = 0, fpar = 0;
             for (uint32_t ti = 0; ti < tiles.count; ti++) {
                 const uint32_t buf = ti & 1, use = ti >> 1;
                 if (ti >= 2) mbar_wait(&tempty[buf], (use & 1) ^ 1);
@@ -586,20 +565,22 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
                 tc_fence_after();
                 const uint32_t dacc = tmem + Cfg::A0_COLS + buf * Cfg::ACC_COLS;
                 for (uint32_t kp = 0; kp < KP; kp++, it++) {
-                    const uint32_t s = (it + OFS) % Cfg::NSLOT, ph = ((it + OFS) / Cfg::NSLOT) & 1;
+                    const uint32_t s = ti == 0 ? (kp & 1) : res_slot(it, KP), bit = 1u << s;
                     const uint32_t kb0 = kp * Cfg::KPS, nkb = min(Cfg::KPS, KB - kb0);
-                    mbar_wait(&full[s], ph);
+                    mbar_wait(&full[s], (fpar & bit) ? 1u : 0u);
+                    fpar ^= bit;
                     if (ti == 1 && kp < 8) TRACE(40 + kp);
                     tc_fence_after();
-                    if (ti == 0 && OFS == 0) {
-                        // first tile: move these k-blocks of slice 0 into TMEM (in issue order with the MMAs)
+                    if (ti == 0) {
+                        // first tile: this pair's slice 0 -> TMEM (in issue order with the MMAs), then its slot is free
+                        const uint32_t xs = 2 + (kp & 1);
                         for (uint32_t q = 0; q < nkb; q++) {
-                            const uint32_t stg = smem_u32(smem + Cfg::OFF_STG + q * Cfg::SLICE);
+                            const uint32_t stg = smem_u32(slot_ptr(xs) + q * Cfg::SLICE);
 #pragma unroll
                             for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
                                 tmem_cp_128x256b_w(tmem + (kb0 + q) * (Cfg::BK / 4) + kk * 8, sdesc_kmajor_sw128(stg + kk * 32));
                         }
-                        mma_commit_w(&sfree[0]);
+                        mma_commit_w(&empty[xs]);
                     }
 #ifdef NIMBUS_RES_NOMMA
                     if (ti > 0) { mma_commit_w(&empty[s]); continue; }   // diagnostic (wrong results): stream only
@@ -608,7 +589,7 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
                         const uint32_t kb = kb0 + q;
                         const uint32_t a0t = tmem + kb * (Cfg::BK / 4);                      // slice 0, TMEM
                         const uint32_t a1 = smem_u32(smem + Cfg::OFF_A1 + kb * Cfg::SLICE);  // slice 1, smem
-                        const uint32_t b0 = smem_u32(smem + Cfg::RING_BASE + s * Cfg::SLOT + q * Cfg::B_BYTES);
+                        const uint32_t b0 = smem_u32(slot_ptr(s) + q * Cfg::B_BYTES);
 #pragma unroll
                         for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
                             const uint64_t bd = sdesc_kmajor_sw128(b0 + kk * 32);
@@ -635,6 +616,23 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
         const uint32_t ew = warp - 4;
         const uint32_t sub = ew & 3, half = ew >> 2;
         uint32_t hold[Cfg::BN / 16][8];
+        // FUSE: the masks of the CTA's first component-0 output tile (a limb-1 tile, odd ti) are
+        // computed before its first accumulators are ready (the epilogue warps are idle then), and
+        // its R stored once the previous grid is done (pdl_wait: R may be its output too)
+        uint32_t pre[Cfg::BN / 16][8];
+        uint32_t pre_ti = ~0u;
+        if (FUSE) {
+            for (uint32_t ti = 1; ti < tiles.count; ti += 2)
+                if ((tiles.at(ti) % CT) * Cfg::BN < 2 * R.N) { pre_ti = ti; break; }
+            const uint32_t row = sub * 32 + lane;
+            if (pre_ti != ~0u && row < k) {
+                pdl_wait();
+                const uint32_t col_base = (tiles.at(pre_ti) % CT) * Cfg::BN;
+#pragma unroll
+                for (uint32_t b = 0; b < Cfg::BN / 16; b++)
+                    fused_mask8(R, fo, row, (col_base + (half * (Cfg::BN / 16) + b) * 8) % R.N, pre[b]);
+            }
+        }
         for (uint32_t ti = 0; ti < tiles.count; ti++) {
             const uint32_t tg = tiles.at(ti), ct = tg % CT;
             const uint32_t buf = ti & 1, use = ti >> 1;
@@ -642,18 +640,17 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
             tc_fence_after();
 #ifdef NIMBUS_RES_NOEPI
+            acc_release(&tempty[buf]);
             if (false)        // diagnostic (wrong results): no epilogue work at all
 #endif
             if (FUSE)
                 epilogue_fused<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
-                                                   half, sub * 32 + lane, k, ct * Cfg::BN, ti & 1, hold, fo);
+                                                   half, sub * 32 + lane, k, ct * Cfg::BN, ti & 1, hold, fo, &tempty[buf],
+                                                   ti == pre_ti, pre);
             else
-                for (uint32_t hh = 0; hh < 8 / Cfg::EPI_WARPS; hh++)
-                    epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
-                                                      half + hh, sub * 32 + lane, k, ct * Cfg::BN, ncol, jobs.C[tg / CT]);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
+                epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + Cfg::A0_COLS + buf * Cfg::ACC_COLS,
+                                                  half, sub * 32 + lane, k, ct * Cfg::BN, ncol, jobs.C[tg / CT],
+                                                  &tempty[buf]);
             if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
         }
     }
@@ -1049,6 +1046,7 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
 #pragma unroll
                     for (uint32_t s = 0; s < Cfg::NACC; s++) tmem_ld8(tbase + s * Cfg::RT + (c0 + b) * 8, v[b][s]);
                 tmem_ld_wait();
+                if (c0 + B >= CH) acc_release(&tempty[buf]);      // last chunk in registers
 #pragma unroll
                 for (uint32_t b = 0; b < B; b++) {
 #pragma unroll
@@ -1064,9 +1062,6 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
             if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
         }
     }

@@ -29,6 +29,9 @@ struct Big {
 struct nimbus_ctx {
     nimbus_params prm{};
     int device = 0;
+    // the caller's reference + one per live handle (sk, pk, encw, plainw): the context is freed
+    // when the last of them goes, so handles may be destroyed after it in any order
+    std::atomic<int> refs{1};
     nimbus::Rns rns{};
     Big q;                         // q = prod of all L primes (up to 6 x 31 bits)
     u128 qout = 0;                 // q' = prod of the first L_out primes (< 2^95)

@@ -17,10 +17,13 @@ template <int SX, int RT, typename T = uint32_t>
 __global__ void k_slice_x(const T* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB, uint32_t ell,
                           uint8_t* __restrict__ Xt, uint32_t total, uint32_t* flag, int check) {
     pdl_trigger();
-    pdl_wait();          // Xt may still be read by the previous contraction in the stream
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    slice_item<SX, RT, T>(X, k, m, KB, ell, Xt, idx, flag, check);
+    // X (the caller's input) is read and sliced while the previous kernel of the stream may
+    // still run; the planes are stored only after it is done (it may still read Xt)
+    SlicePlanes<SX> sp;
+    if (idx < total) sp = slice_load<SX, RT, T>(X, k, m, KB, ell, idx, check);
+    pdl_wait();
+    if (idx < total) slice_store<SX, RT>(sp, Xt, flag);
 }
 
 // ---------------------------------------------------------------- tile Enc(W)

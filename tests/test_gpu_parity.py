@@ -504,6 +504,25 @@ def test_error_codes(nb, oracle):
     assert e.value.status == -2
 
 
+def test_handles_outlive_context(nb, oracle):
+    """Handles hold a reference to their context (nimbus_ctx_destroy): destroying the context
+    first, then its handles in any order, leaves no CUDA error behind, and the next context's
+    calls run clean (cyclic garbage collection frees Python handles in arbitrary order)."""
+    for order in ("encw_first", "sk_first"):
+        ctx = nb.nimbus_ctx_create(256, 2, 16, 1)
+        sk = nb.nimbus_keygen(ctx, 1)
+        pk = nb.nimbus_keygen_pk(ctx, sk, 2)
+        w = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(ni.gen_W(1, 8, 8, 16)), 1)
+        ctx.close()
+        for h in ((w, pk, sk) if order == "encw_first" else (sk, pk, w)):
+            h.close()
+    torch.cuda.synchronize()
+    c = Case(nb, oracle, 256, 2, 16, 1, 40, 24, 9, 1, seed=77)
+    cts, R = c.run()
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+
+
 def test_batch_matches_sequential_and_oracle(nb, oracle):
     """nimbus_cop_matmul_batch (pack of job i overlapped with the contraction of
     job i+1 on a side stream) gives the same bytes as job-by-job calls, and the

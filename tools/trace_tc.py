@@ -44,7 +44,22 @@ if MODE in ("write", "writeread"):
 if MODE == "writeread":
     rflush.sum()
 torch.cuda.synchronize()
-nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
+if os.environ.get("QKV") == "1":
+    # Q, K, V sharing X: one batch call (one resident-X launch over the three Enc(W)s)
+    ws3 = [(nb.nimbus_encrypt_weights(ctx, sk, nb.from_numpy_u32(ni.gen_W(5 + i, m, n, ell), "cuda"), 5 + i),)
+           for i in range(3)]
+    outs = [nb.alloc_outputs(ctx, wq[0], k, 1) for wq in ws3]
+    jobs = [dict(encw=wq[0], X=X, k_per_query=k, n_queries=1, mask_seed=3, cts=o[0], R=o[1])
+            for wq, o in zip(ws3, outs)]
+    wsb = torch.empty(nb.nimbus_cop_workspace_size_batch(ctx, jobs), dtype=torch.uint8, device="cuda")
+    nb.nimbus_cop_matmul_batch(ctx, jobs, wsb)
+    torch.cuda.synchronize()
+    tr.zero_()
+    flush.zero_()
+    torch.cuda.synchronize()
+    nb.nimbus_cop_matmul_batch(ctx, jobs, wsb)
+else:
+    nb.nimbus_cop_matmul(ctx, w, X, k, 1, 3, cts, R, ws)
 torch.cuda.synchronize()
 lib.nimbus_trace_set(ctypes.c_void_p(0))
 lib.nimbus_trace_pack_set(ctypes.c_void_p(0))
@@ -77,3 +92,20 @@ print(f"CTA start: min {st.min():.2f} max {st.max():.2f}")
 tp = trp.cpu().numpy().astype(np.int64)
 print(f"pack: first block start {us(tp[0]):.2f}  first past PDL wait {us(tp[1]):.2f}  last past wait {us(tp[2]):.2f}  "
       f"last block end {us(tp[3]):.2f} us (contraction CTAs end max {e.max():.2f})")
+# aggregate over CTAs: first-tile MMA end, later tiles' MMA spans, the final epilogue (the tail)
+t0_end, spans, tails = [], [], []
+for c in range(148):
+    row = t[c]
+    if row[0] == 0 or row[4] == 0:
+        continue
+    nt = 0
+    while nt < 15 and row[4 + 4 * nt] > 0:
+        nt += 1
+    t0_end.append(us(row[5]))
+    for ti in range(1, nt):
+        spans.append((row[5 + 4 * ti] - row[5 + 4 * (ti - 1)]) / 1e3)
+    tails.append((row[7 + 4 * (nt - 1)] - row[5 + 4 * (nt - 1)]) / 1e3)
+if t0_end:
+    print(f"first tile MMA end: median {np.median(t0_end):.2f} max {np.max(t0_end):.2f} us; later tiles (MMA end to "
+          f"MMA end): median {np.median(spans) if spans else float('nan'):.2f} us; final epilogue after the last MMA: "
+          f"median {np.median(tails):.2f} max {np.max(tails):.2f} us")
