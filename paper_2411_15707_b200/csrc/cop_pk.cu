@@ -604,64 +604,76 @@ template <int SX, int RT>
 __global__ void __launch_bounds__(256) k_slice_pk(const __grid_constant__ PkParams P, uint32_t ell, uint32_t* flag,
                                                   int check) {
     pdl_trigger();
-    pdl_wait();          // the packed slices may still be read by the previous contraction in the stream
     uint32_t j = 0;
     while (blockIdx.x >= P.job[j].blk_end) j++;
     const PkJob& J = P.job[j];
     const uint32_t idx = (blockIdx.x - (j ? P.job[j - 1].blk_end : 0u)) * blockDim.x + threadIdx.x;
-    // the contraction's dispatch counter and this job's rho flags start at zero
-    if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctr = 0;
-    if (idx < J.nflags) J.flags[idx] = 0;
     const uint32_t rows = J.TT * RT;
     const uint32_t per_rc = rows * J.KB * 8;
     const uint32_t rc = idx / per_rc;
-    if (rc >= 2 * J.Rr) return;
     const uint32_t r = rc >> 1, cmp = rc & 1;
-    if (r == 0 && cmp) return;                 // term 0 never wraps
-    const uint32_t rem = idx - rc * per_rc;
-    const uint32_t tgl = rem / (J.KB * 8), ch = rem % (J.KB * 8);
-    const uint32_t kb = ch >> 3, c16 = ch & 7;
-    const uint32_t beta0 = kb * kBK + c16 * 16;
-    const uint32_t qy = tgl / J.nct, th = tgl - qy * J.nct;
-    const bool present = tgl < J.ntheta && th * J.Rr + r < J.kq;
-    const size_t arow = (size_t)qy * J.kq + th * J.Rr + r;
-    uint32_t v[16];
-    if (present && beta0 + 16 <= J.m && (J.m & 3) == 0) {
-        const uint4* src = reinterpret_cast<const uint4*>(J.X + arow * J.m + beta0);
+    const bool work = rc < 2 * J.Rr && !(r == 0 && cmp);      // term 0 never wraps
+    // X (the caller's input) is read and sliced before the PDL wait, while the previous kernel
+    // may still run; the counter, the flags and the slices are written after it (the previous
+    // contraction may still read them)
+    uint32_t w[SX][4];
+    size_t base = 0;                 // the operand block of (rc, theta tile, kb)
+    uint32_t brow = 0, bc16 = 0;     // the row in the theta tile, the 16-byte chunk
+    bool bad = false;
+    if (work) {
+        const uint32_t rem = idx - rc * per_rc;
+        const uint32_t tgl = rem / (J.KB * 8), ch = rem % (J.KB * 8);
+        const uint32_t kb = ch >> 3, c16 = ch & 7;
+        const uint32_t beta0 = kb * kBK + c16 * 16;
+        const uint32_t qy = tgl / J.nct, th = tgl - qy * J.nct;
+        const bool present = tgl < J.ntheta && th * J.Rr + r < J.kq;
+        const size_t arow = (size_t)qy * J.kq + th * J.Rr + r;
+        uint32_t v[16];
+        if (present && beta0 + 16 <= J.m && (J.m & 3) == 0) {
+            const uint4* src = reinterpret_cast<const uint4*>(J.X + arow * J.m + beta0);
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const uint4 w = __ldg(src + q);
-            v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+            for (int q = 0; q < 4; q++) {
+                const uint4 x4 = __ldg(src + q);
+                v[4 * q] = x4.x; v[4 * q + 1] = x4.y; v[4 * q + 2] = x4.z; v[4 * q + 3] = x4.w;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 16; u++) v[u] = (present && beta0 + u < J.m) ? J.X[arow * J.m + beta0 + u] : 0u;
         }
-    } else {
+        if (check && present && ell < 32) {
+            uint32_t any = 0;
 #pragma unroll
-        for (int u = 0; u < 16; u++) v[u] = (present && beta0 + u < J.m) ? J.X[arow * J.m + beta0 + u] : 0u;
-    }
-    if (check && present && ell < 32) {
-        uint32_t bad = 0;
+            for (int u = 0; u < 16; u++) any |= v[u] >> ell;
+            bad = any != 0;
+        }
+        if (cmp) {
+            const uint32_t ones = SX >= 4 ? 0xFFFFFFFFu : (1u << (8 * SX)) - 1u;
 #pragma unroll
-        for (int u = 0; u < 16; u++) bad |= v[u] >> ell;
-        if (bad) atomicOr(flag, 1u);
-    }
-    if (cmp) {
-        const uint32_t ones = SX >= 4 ? 0xFFFFFFFFu : (1u << (8 * SX)) - 1u;
+            for (int u = 0; u < 16; u++) v[u] ^= ones;
+        }
+        const uint32_t tt = tgl / RT, rr = tgl % RT;
 #pragma unroll
-        for (int u = 0; u < 16; u++) v[u] ^= ones;
-    }
-    const uint32_t tt = tgl / RT, rr = tgl % RT;
+        for (int i = 0; i < SX; i++)
 #pragma unroll
-    for (int i = 0; i < SX; i++) {
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-            w[q] = ((v[4 * q] >> (8 * i)) & 0xFF) | (((v[4 * q + 1] >> (8 * i)) & 0xFF) << 8) |
-                   (((v[4 * q + 2] >> (8 * i)) & 0xFF) << 16) | (((v[4 * q + 3] >> (8 * i)) & 0xFF) << 24);
+            for (int q = 0; q < 4; q++)
+                w[i][q] = ((v[4 * q] >> (8 * i)) & 0xFF) | (((v[4 * q + 1] >> (8 * i)) & 0xFF) << 8) |
+                          (((v[4 * q + 2] >> (8 * i)) & 0xFF) << 16) | (((v[4 * q + 3] >> (8 * i)) & 0xFF) << 24);
         // the 128-B swizzle follows the row's position in the whole (S_x x RT)-row operand block:
         // slice i starts at row i RT, which is not a multiple of 8 when RT = 52
-        uint8_t* dst = const_cast<uint8_t*>(J.Xp) + ((((size_t)rc * J.TT + tt) * J.KB + kb) * SX * RT) * kBK +
-                       swz_off(i * RT + rr, c16);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        base = ((((size_t)rc * J.TT + tt) * J.KB + kb) * SX * RT) * kBK;
+        brow = rr;
+        bc16 = c16;
     }
+    pdl_wait();
+    // the contraction's dispatch counter and this job's rho flags start at zero
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctr = 0;
+    if (idx < J.nflags) J.flags[idx] = 0;
+    if (!work) return;
+    if (bad) atomicOr(flag, 1u);
+#pragma unroll
+    for (int i = 0; i < SX; i++)
+        *reinterpret_cast<uint4*>(const_cast<uint8_t*>(J.Xp) + base + swz_off(i * RT + brow, bc16)) =
+            make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
 }
 
 // ------------------------------------------------------------------ setup: column sums and corr
