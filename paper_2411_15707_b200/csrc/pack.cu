@@ -47,13 +47,15 @@ __global__ void __launch_bounds__(128) k_pack(Rns Rn, PackJobs P, uint32_t kq, u
 #ifndef NIMBUS_TRACE
     if (J >= Rn.N) return;
 #endif
+    const uint32_t job = blockIdx.z >> 1, comp = blockIdx.z & 1;
+    PackMask<V, L, MT> mk;
+    if (comp == 0 && J < Rn.N) pack_mask<V, L, MT>(Rn, P.key[job], blockIdx.y, J, mk);
     pdl_wait();  // C is produced by the contraction kernel
     PTRACE_MIN(1);
     PTRACE_MAX(2);
-    const uint32_t job = blockIdx.z >> 1;
     if (J < Rn.N)
         pack_item<V, L, RB, MT>(Rn, P.C[job], kq, n, Rr, nct, P.key[job], P.cts[job], static_cast<MT*>(P.R[job]), Z0,
-                                blockIdx.y, blockIdx.z & 1, J);
+                                blockIdx.y, comp, J, mk);
     PTRACE_MAX(3);
 }
 

@@ -45,6 +45,37 @@ struct VecU32<4> {
     }
 };
 
+// The mask of the work item (component 0 only): r = word(seed, 6, tg N + J + u) >> (64 - ell)
+// and Emb_{q'}(r) mod p_i for the output limbs.  It depends on no kernel
+// input, so k_pack computes it before its PDL wait, while the contraction still runs.
+template <int V, int L, typename MT = uint32_t>
+struct PackMask {
+    MT r[V];
+    uint32_t emb[L][V];
+};
+
+template <int V, int L, typename MT = uint32_t>
+__device__ __forceinline__ void pack_mask(const Rns& Rn, uint64_t key_mask, uint32_t tg, uint32_t J,
+                                          PackMask<V, L, MT>& m) {
+    // word(seed, 6, i) = mix64(key + golden (i + 1)) for i = tg N + J + u: one multiply, then steps
+    uint64_t z = key_mask + 0x9E3779B97F4A7C15ULL * ((uint64_t)tg * Rn.N + J + 1);
+#pragma unroll
+    for (int u = 0; u < V; u++, z += 0x9E3779B97F4A7C15ULL) {
+        const uint64_t w = mix64(z);
+        m.r[u] = (MT)(Rn.ell >= 64 ? w : w >> (64 - Rn.ell));
+#pragma unroll
+        for (int i = 0; i < L; i++)
+            if ((uint32_t)i < Rn.L_out)
+                m.emb[i][u] = sizeof(MT) == 8
+                                  ? emb_mod(m.r[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.mu[i], Rn.t_inv[i])
+                                  : Rn.ell <= 16
+                                  ? emb_fast16((uint32_t)m.r[u], (uint32_t)Rn.qout_mod_t, Rn.ell, Rn.p[i],
+                                               Rn.t_inv[i], Rn.t_inv_sh[i])
+                                  : emb_fast((uint32_t)m.r[u], (uint32_t)Rn.qout_mod_t, Rn.ell, Rn.p[i],
+                                             Rn.t_inv[i], Rn.t_inv_sh[i]);
+    }
+}
+
 // One work item of K7: coefficients J..J+V-1 of component `comp` of packed
 // ciphertext tg (all limbs).  RB rows of loads are in flight per batch; the host
 // picks RB to fit R = floor(N/n) (1 for C3, 5 for C2, ...) so that few load slots
@@ -54,7 +85,7 @@ template <int V, int L, int RB, typename MT = uint32_t>
 __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restrict__ C, uint32_t kq, uint32_t n,
                                           uint32_t Rr, uint32_t nct, uint64_t key_mask, uint32_t* __restrict__ cts,
                                           MT* __restrict__ Rout, const uint32_t* __restrict__ Z0, uint32_t tg,
-                                          uint32_t comp, uint32_t J) {
+                                          uint32_t comp, uint32_t J, const PackMask<V, L, MT>& mk) {
     static_assert(sizeof(MT) == 4 || V == 1, "64-bit masks: one coefficient per thread");
     const uint32_t N = Rn.N, Lo = Rn.L_out;
     const uint32_t query = tg / nct, theta = tg - query * nct;
@@ -107,17 +138,6 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
             for (int u = 0; u < V; u++) acc[i][u] += z[u];
         }
     }
-    MT rmask[V];
-    if (comp == 0) {
-        // word(seed, 6, i) = mix64(key + golden (i + 1)) for i = tg N + J + u: one multiply, then steps;
-        // r = word >> (64 - ell)
-        uint64_t z = key_mask + 0x9E3779B97F4A7C15ULL * ((uint64_t)tg * N + J + 1);
-#pragma unroll
-        for (int u = 0; u < V; u++, z += 0x9E3779B97F4A7C15ULL) {
-            const uint64_t w = mix64(z);
-            rmask[u] = (MT)(Rn.ell >= 64 ? w : w >> (64 - Rn.ell));
-        }
-    }
     uint32_t out[L][V];
 #pragma unroll
     for (int u = 0; u < V; u++) {
@@ -149,15 +169,7 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
         if (comp == 0) {
 #pragma unroll
             for (int i = 0; i < L; i++)
-                if ((uint32_t)i < Lo)
-                    res[i] = submod(res[i], sizeof(MT) == 8
-                                                ? emb_mod(rmask[u], Rn.qout_mod_t, Rn.ell, Rn.p[i], Rn.mu[i],
-                                                          Rn.t_inv[i])
-                                                : Rn.ell <= 16
-                                                ? emb_fast16((uint32_t)rmask[u], (uint32_t)Rn.qout_mod_t, Rn.ell,
-                                                             Rn.p[i], Rn.t_inv[i], Rn.t_inv_sh[i])
-                                                : emb_fast((uint32_t)rmask[u], (uint32_t)Rn.qout_mod_t, Rn.ell,
-                                                           Rn.p[i], Rn.t_inv[i], Rn.t_inv_sh[i]), Rn.p[i]);
+                if ((uint32_t)i < Lo) res[i] = submod(res[i], mk.emb[i][u], Rn.p[i]);
         }
 #pragma unroll
         for (int i = 0; i < L; i++) out[i][u] = res[i];
@@ -166,9 +178,9 @@ __device__ __forceinline__ void pack_item(const Rns& Rn, const uint32_t* __restr
     for (int i = 0; i < L; i++)
         if ((uint32_t)i < Lo) VecU32<V>::store(cts + (((size_t)tg * 2 + comp) * Lo + i) * N + J, out[i]);
     if (comp == 0 && Rout && J < rows * n) {          // Rout null: R written by k_mask_R instead
-        if (sizeof(MT) == 8) Rout[row0 * n + J] = rmask[0];
+        if (sizeof(MT) == 8) Rout[row0 * n + J] = mk.r[0];
         else VecU32<V>::store(reinterpret_cast<uint32_t*>(Rout) + row0 * n + J,
-                              reinterpret_cast<const uint32_t(&)[V]>(rmask));
+                              reinterpret_cast<const uint32_t(&)[V]>(mk.r));
     }
 }
 
