@@ -284,20 +284,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                 const uint32_t limb = pk_limb(R, U.pass);
                 const size_t slab = ((size_t)U.comp * L + limb) * NT;
                 const uint32_t shift_t = J.n / Cfg::BM;               // tiles per shift step
-                // K runs kb-major from a per-unit start: the units of one (job, pass, component) are
-                // dispatched in order, ~gridDim/CL at a time, so unit g of the group starts at k-block
-                // g KB / (gridDim/CL) (mod KB) and the units in flight then read the same k-blocks at
-                // the same time -- a few MB of Enc(W) and X in use instead of the whole slab (100 MB
-                // + 51 MB of X at m = 3072), which stays in L2 (the sums are exact, so the order of
-                // the k-blocks within a unit is free; the MMA issuer only counts positions)
-                const uint32_t gidx = U.T + NT * (U.tt / CL);
-#ifdef NIMBUS_PK_NOSTAGGER
-                const uint32_t kb_off = 0 * gidx;     // A/B: every unit from k-block 0
-#else
-                const uint32_t kb_off = (uint32_t)(((uint64_t)gidx * J.KB) / (gridDim.x / CL)) % J.KB;
-#endif
-                for (uint32_t kq = 0; kq < J.KB; kq++) {
-                    const uint32_t kb = kq + kb_off < J.KB ? kq + kb_off : kq + kb_off - J.KB;
+                for (uint32_t kb = 0; kb < J.KB; kb++) {
                     for (uint32_t r = 0; r < J.Rr; r++) {
                         const uint32_t sh = r * shift_t;
                         const bool wrap = U.T < sh;
