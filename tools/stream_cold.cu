@@ -15,8 +15,13 @@
 
 using namespace nimbus;
 
+__device__ __forceinline__ unsigned long long gt_ns() {
+    unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
+}
+// hold: SM cycles a landed slot is kept before it is refilled (emulates the MMAs that consume it;
+// globaltimer ticks in ~1 us steps here, too coarse)
 __global__ void __launch_bounds__(128) k_tiles(const uint8_t* src, uint32_t ntiles, uint32_t tile, uint32_t stages,
-                                              uint32_t bytes, unsigned long long* sink) {
+                                              uint32_t bytes, unsigned long long* sink, uint32_t hold = 0) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bars[16];
@@ -37,6 +42,7 @@ __global__ void __launch_bounds__(128) k_tiles(const uint8_t* src, uint32_t ntil
             const uint32_t j = i - stages, s = j % stages;
             mbar_wait(&bars[s], (j / stages) & 1);
             acc += smem[s * bytes];
+            if (hold) { const long long t0 = clock64(); while (clock64() - t0 < (long long)hold) { } }
         }
         if (i < n) {
             const uint32_t s = i % stages;
@@ -139,6 +145,30 @@ int main() {
         printf("%5u B x %2u stages x %u CTA/SM (%4u KB in flight/SM): best %6.2f us (%5.0f GB/s), mean %6.2f us  %s\n",
                v.bytes, v.stages, v.ctas_per_sm, v.bytes * v.stages * v.ctas_per_sm / 1024, best * 1e3,
                (double)ntiles * tile / (best * 1e-3) / 1e9, sum / reps * 1e3, cudaGetErrorString(cudaGetLastError()));
+    }
+    if (getenv("HOLD_NS")) {
+        // the resident kernel's ring with its MMA hold per 32 KB slot: 3, 4, 6 slots
+        const uint32_t hold = (uint32_t)atoi(getenv("HOLD_NS"));
+        for (uint32_t st : {3u, 4u, 6u}) {
+            const size_t smem = (size_t)st * 32768 + 1024;
+            cudaFuncSetAttribute(k_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            float best = 1e9;
+            for (int rep = 0; rep < 8; rep++) {
+                k_read<<<sms * 4, 256>>>(reinterpret_cast<const uint4*>(fl), ((size_t)512 << 20) / 16, sink);
+                const uint8_t* s = src + (size_t)(rep % 8) * (mb << 20);
+                cudaEvent_t e0, e1;
+                cudaEventCreate(&e0); cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                k_tiles<<<sms, 128, smem>>>(s, (uint32_t)ntiles, (uint32_t)tile, st, 32768, sink, hold);
+                cudaEventRecord(e1);
+                cudaDeviceSynchronize();
+                float ms = 0;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            printf("hold %u cycles, %u x 32 KB: best %6.2f us (%5.0f GB/s)\n", hold, st, best * 1e3,
+                   (double)ntiles * tile / (best * 1e-3) / 1e9);
+        }
     }
     // TLB / pattern experiments at 32 KB x 3 (the resident kernel's ring)
     cudaFuncSetAttribute(k_contig, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 32768 + 1024);
