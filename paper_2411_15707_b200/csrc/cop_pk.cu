@@ -40,6 +40,7 @@
 // CTAs in flight always work on neighbouring units); one persistent launch serves a
 // whole job list (the 72 matmuls of the C5 pass), so there is one tail per pass.
 #include <memory>
+#include <vector>
 #include <cstdio>
 #include <cstring>
 #include "internal.h"
@@ -602,7 +603,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
 // bitwise complemented (S_x bytes) when cmp = 1.
 template <int SX, int RT>
 __global__ void __launch_bounds__(256) k_slice_pk(const __grid_constant__ PkParams P, uint32_t ell, uint32_t* flag,
-                                                  int check) {
+                                                  int check, int late) {
     pdl_trigger();
     uint32_t j = 0;
     while (blockIdx.x >= P.job[j].blk_end) j++;
@@ -613,6 +614,7 @@ __global__ void __launch_bounds__(256) k_slice_pk(const __grid_constant__ PkPara
     const uint32_t rc = idx / per_rc;
     const uint32_t r = rc >> 1, cmp = rc & 1;
     const bool work = rc < 2 * J.Rr && !(r == 0 && cmp);      // term 0 never wraps
+    if (late) pdl_wait();         // X is an output of the previous kernel (pdl_outputs_overlap)
     // X (the caller's input) is read and sliced before the PDL wait, while the previous kernel
     // may still run; the counter, the flags and the slices are written after it (the previous
     // contraction may still read them)
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(256) k_slice_pk(const __grid_constant__ PkPara
         brow = rr;
         bc16 = c16;
     }
-    pdl_wait();
+    if (!late) pdl_wait();
     // the contraction's dispatch counter and this job's rho flags start at zero
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctr = 0;
     if (idx < J.nflags) J.flags[idx] = 0;
@@ -856,7 +858,11 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
             J.blk_end = blocks;
         }
         const int check = (c->prm.flags & NIMBUS_FLAG_CHECK_RANGE) && c->rns.ell < 32;
-        e = launch_pdl(k_slice_pk<4, RT>, dim3(blocks), dim3(256), 0, st, P, c->rns.ell, c->d_flag, check);
+        int late = 0;
+        for (uint32_t i = 0; i < nj && !late; i++)
+            late = pdl_outputs_overlap(st, jobs[base + i].d_X,
+                                       (size_t)jobs[base + i].kq * jobs[base + i].nq * jobs[base + i].w->m * 4);
+        e = launch_pdl(k_slice_pk<4, RT>, dim3(blocks), dim3(256), 0, st, P, c->rns.ell, c->d_flag, check, late);
         c->launches++;
         if (e != cudaSuccess) return e;
         if (mark) mark(c, st);
@@ -877,6 +883,18 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
         cfg.numAttrs = 2;
         e = cudaLaunchKernelEx(&cfg, k_cop_pk<4, RT, CL>, c->rns, P, units);
         c->launches++;
+        {   // the contraction writes the jobs' ciphertexts and R, and triggers its dependents early
+            std::vector<const void*> op;
+            std::vector<size_t> ob;
+            for (uint32_t i = 0; i < nj; i++) {
+                const PkHostJob& h = jobs[base + i];
+                op.push_back(h.d_cts);
+                ob.push_back((size_t)h.nq * pk_nct(c, h.w, h.kq) * 2 * c->rns.L_out * c->rns.N * 4);
+                op.push_back(h.d_R);
+                ob.push_back((size_t)h.kq * h.nq * h.w->n * 4);
+            }
+            pdl_outputs_set(st, op.data(), ob.data(), (uint32_t)op.size());
+        }
         snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_pk<4, %d, %d>", RT, CL);
         if (e != cudaSuccess) return e;
     }

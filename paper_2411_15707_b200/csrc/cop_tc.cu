@@ -1169,6 +1169,11 @@ cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8
     e = launch_pdl(k_cop_tc_res<true>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt, J, k, CT,
                    w->KB, ncol, fo);
     c->launches++;
+    {   // writes the ciphertexts and R, and triggers its dependents early
+        const void* op[2] = {d_cts, d_R};
+        const size_t ob[2] = {(size_t)k * 2 * c->rns.N * 4, (size_t)k * w->n * 4};
+        pdl_outputs_set(st, op, ob, 2);
+    }
     snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<1>");
     return e;
 }

@@ -167,6 +167,13 @@ cudaError_t launch_tile_encw(nimbus_ctx* c, const uint32_t* d_canon, uint32_t m,
                              uint8_t* d_Et, cudaStream_t st);
 cudaError_t launch_untile_encw(nimbus_ctx* c, const uint8_t* d_Et, uint32_t m, uint32_t KB, uint32_t bn,
                                uint32_t* d_canon, cudaStream_t st);
+// Outputs of the last kernel we launched on a stream that triggers its dependents early
+// (griddepcontrol.launch_dependents at its start: k_pack, the fused R = 1 contraction,
+// k_cop_pk, the server GEMMs).  The next kernel on that stream may start before it is done;
+// the slice kernels read X before their PDL wait, which is only safe when X is not one of
+// these outputs -- otherwise they load X after the wait (pdl_outputs_overlap).
+void pdl_outputs_set(cudaStream_t st, const void* const* ptrs, const size_t* bytes, uint32_t n);
+bool pdl_outputs_overlap(cudaStream_t st, const void* p, size_t bytes);
 cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_X, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st);
 // d_R may be null: then the pack writes only the ciphertexts (R comes from launch_mask_R).

@@ -9,20 +9,25 @@
 // stored at chunk position c ^ (r & 7) -- the 128-byte swizzle that the
 // tcgen05 shared-memory descriptor (SWIZZLE_128B, K-major) expects, applied
 // once at rest so that one linear bulk copy lands a ready-to-use operand tile.
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 #include "slice_dev.cuh"
 
 namespace nimbus {
 
 template <int SX, int RT, typename T = uint32_t>
 __global__ void k_slice_x(const T* __restrict__ X, uint32_t k, uint32_t m, uint32_t KB, uint32_t ell,
-                          uint8_t* __restrict__ Xt, uint32_t total, uint32_t* flag, int check) {
+                          uint8_t* __restrict__ Xt, uint32_t total, uint32_t* flag, int check, int late) {
     pdl_trigger();
     const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
     // X (the caller's input) is read and sliced while the previous kernel of the stream may
-    // still run; the planes are stored only after it is done (it may still read Xt)
+    // still run; the planes are stored only after it is done (it may still read Xt).  late:
+    // X is an output of that kernel (pdl_outputs_overlap), so it is read after the wait too.
+    if (late) pdl_wait();
     SlicePlanes<SX> sp;
     if (idx < total) sp = slice_load<SX, RT, T>(X, k, m, KB, ell, idx, check);
-    pdl_wait();
+    if (!late) pdl_wait();
     if (idx < total) slice_store<SX, RT>(sp, Xt, flag);
 }
 
@@ -79,6 +84,46 @@ __global__ void __launch_bounds__(256) k_untile_encw(const uint8_t* __restrict__
     }
 }
 
+// ---------------------------------------------------------------- PDL output records
+namespace {
+struct PdlRecord {
+    cudaStream_t st;
+    std::vector<std::pair<uintptr_t, uintptr_t>> ranges;    // [lo, hi)
+};
+std::mutex g_pdl_mu;
+std::vector<PdlRecord> g_pdl;                                // one record per stream (a few streams)
+}  // namespace
+
+void pdl_outputs_set(cudaStream_t st, const void* const* ptrs, const size_t* bytes, uint32_t n) {
+    std::lock_guard<std::mutex> lk(g_pdl_mu);
+    PdlRecord* r = nullptr;
+    for (PdlRecord& x : g_pdl)
+        if (x.st == st) r = &x;
+    if (!r) {
+        if (g_pdl.size() >= 64) g_pdl.erase(g_pdl.begin());
+        g_pdl.push_back(PdlRecord{st, {}});
+        r = &g_pdl.back();
+    }
+    r->ranges.clear();
+    for (uint32_t i = 0; i < n; i++)
+        if (ptrs[i] && bytes[i]) {
+            const uintptr_t lo = reinterpret_cast<uintptr_t>(ptrs[i]);
+            r->ranges.emplace_back(lo, lo + bytes[i]);
+        }
+}
+
+bool pdl_outputs_overlap(cudaStream_t st, const void* p, size_t bytes) {
+    static const bool off = getenv("NIMBUS_NO_PDL_GUARD") != nullptr;    // test switch: show the hazard
+    if (off) return false;
+    std::lock_guard<std::mutex> lk(g_pdl_mu);
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(p), hi = lo + bytes;
+    for (const PdlRecord& x : g_pdl)
+        if (x.st == st)
+            for (const auto& r : x.ranges)
+                if (lo < r.second && r.first < hi) return true;
+    return false;
+}
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_Xv, uint32_t k, uint32_t m, uint32_t KB, uint32_t rt,
                            uint8_t* d_Xt, cudaStream_t st) {
@@ -90,15 +135,16 @@ cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_Xv, uint32_t k, uint32_t
     cudaError_t e;
     const uint32_t ell = c->rns.ell;
     const uint32_t* d_X = static_cast<const uint32_t*>(d_Xv);
+    const int late = pdl_outputs_overlap(st, d_Xv, (size_t)k * m * elem_bytes(ell)) ? 1 : 0;
     if (SX == 8) {
         const int check64 = (c->prm.flags & NIMBUS_FLAG_CHECK_RANGE) && ell < 64;
         e = launch_pdl(k_slice_x<8, 32, uint64_t>, g, 256, 0, st, static_cast<const uint64_t*>(d_Xv), k, m, KB, ell,
-                       d_Xt, total, c->d_flag, check64);
-    } else if (rt == 64) e = launch_pdl(k_slice_x<4, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
-    else if (rt == 32) e = launch_pdl(k_slice_x<4, 32>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
-    else if (SX == 1) e = launch_pdl(k_slice_x<1, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
-    else if (SX == 2) e = launch_pdl(k_slice_x<2, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
-    else e = launch_pdl(k_slice_x<4, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check);
+                       d_Xt, total, c->d_flag, check64, late);
+    } else if (rt == 64) e = launch_pdl(k_slice_x<4, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
+    else if (rt == 32) e = launch_pdl(k_slice_x<4, 32>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
+    else if (SX == 1) e = launch_pdl(k_slice_x<1, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
+    else if (SX == 2) e = launch_pdl(k_slice_x<2, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
+    else e = launch_pdl(k_slice_x<4, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
     c->launches++;
     return e;
 }

@@ -169,6 +169,19 @@ cudaError_t launch_pack(nimbus_ctx* c, const uint32_t* d_C, uint32_t kq, uint32_
 
 cudaError_t launch_pack_jobs(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint32_t nq, uint32_t n, cudaStream_t st,
                              bool pdl, const uint32_t* Z0) {
+    {   // the pack writes the ciphertexts and R and triggers its dependents early
+        const uint32_t Rr0 = c->rns.N / n, nct0 = (kq + Rr0 - 1) / Rr0;
+        const void* op[2 * 4];
+        size_t ob[2 * 4];
+        uint32_t no = 0;
+        for (uint32_t j = 0; j < P.nj && j < 4; j++) {
+            op[no] = P.cts[j];
+            ob[no++] = (size_t)nq * nct0 * 2 * c->rns.L_out * c->rns.N * 4;
+            op[no] = P.R[j];
+            ob[no++] = (size_t)kq * nq * n * elem_bytes(c->rns.ell);
+        }
+        pdl_outputs_set(st, op, ob, no);
+    }
     if (elem_bytes(c->rns.ell) == 8) {
         cudaError_t e = launch_64(c, P, kq, nq, n, st, pdl, Z0);
         c->launches++;
@@ -176,12 +189,14 @@ cudaError_t launch_pack_jobs(nimbus_ctx* c, const PackJobs& P, uint32_t kq, uint
     }
     const uint32_t N = c->rns.N, Rr = N / n, nct = (kq + Rr - 1) / Rr;
     // V coefficients per thread (vector loads/stores; J and r n stay multiples of V): the
-    // widest V whose grid still has >= 16 blocks of 128 per SM.  In the PDL chain the pack
-    // runs alone after the contraction and is latency-bound, so thread count beats per-thread
-    // efficiency until the grid is well over one wave (block timing, B200: C2 V=1 22.3 us/step
-    // vs V=2 23.9 / V=4 23.0; C3 V=2 23.5 vs V=4 24.2 / V=1 25.9)
-    const uint64_t threads_v1 = 2ull * nq * nct * N;      // one thread per (comp, J)
-    const uint64_t min_threads = 16ull * 128 * (uint64_t)c->num_sms;
+    // widest V whose grid (all jobs of the launch) still has >= 5 blocks of 128 per SM.  The
+    // pack runs alone after the contraction in the PDL chain; since its masks are computed
+    // before its PDL wait, what remains after it is the loads and the arithmetic, and fewer,
+    // wider threads win until the grid drops under ~5 blocks per SM (B200, block timing, this
+    // round: C2 V=2 20.05 us/step vs V=1 20.33 / V=4 20.57; C2-QKV V=2 40.3 vs V=1 42.2 /
+    // V=4 42.0; round 1, masks after the wait, 16 blocks per SM was the threshold)
+    const uint64_t threads_v1 = 2ull * nq * nct * N * P.nj;      // one thread per (job, comp, J)
+    const uint64_t min_threads = 5ull * 128 * (uint64_t)c->num_sms;
     uint32_t V = (n % 4 == 0 && threads_v1 / 4 >= min_threads) ? 4
                : (n % 2 == 0 && threads_v1 / 2 >= min_threads) ? 2 : 1;
     if (const char* ev = getenv("NIMBUS_PACK_V")) {        // experiment switch: 1, 2 or 4

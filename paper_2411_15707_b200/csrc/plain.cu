@@ -415,6 +415,11 @@ cudaError_t launch_plain_matmul64(nimbus_ctx* c, const uint8_t* d_Xt, const uint
     const uint32_t grid = units < (uint32_t)c->num_sms ? units : (uint32_t)c->num_sms;
     e = launch_pdl(k_plain_t64, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, d_Xt, d_Wt, k, n, Mt, CT, KB, d_add, d_Y);
     c->launches++;
+    {   // writes Y and triggers its dependents early
+        const void* op[1] = {d_Y};
+        const size_t ob[1] = {(size_t)k * n * 8};
+        pdl_outputs_set(st, op, ob, 1);
+    }
     return e;
 }
 
@@ -444,6 +449,11 @@ static cudaError_t launch_plain_s(nimbus_ctx* c, const uint8_t* d_Xt, const uint
     const uint32_t Mt = (k + kBM - 1) / kBM, CT = plain_col_tiles(n);
     const uint32_t units = Mt * CT;
     const uint32_t grid = units < (uint32_t)c->num_sms ? units : (uint32_t)c->num_sms;
+    {   // writes Y and triggers its dependents early
+        const void* op[1] = {d_Y};
+        const size_t ob[1] = {(size_t)k * n * 4};
+        pdl_outputs_set(st, op, ob, 1);
+    }
     return launch_pdl(k_plain_tc<S>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, d_Xt, d_Wt, k, n, Mt, CT, KB,
                       c->rns.ell, d_add, d_Y);
 }

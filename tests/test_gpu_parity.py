@@ -434,17 +434,20 @@ def test_packed_batch_parity(nb, oracle):
         assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all(), f"job {i}"
 
 
-def test_same_x_group_batch_parity(nb, oracle):
+@pytest.mark.parametrize("N,m,n,kq", [(4096, 300, 700, 70), (1024, 100, 200, 128), (2048, 768, 300, 33),
+                                      (256, 700, 100, 128)])
+def test_same_x_group_batch_parity(nb, oracle, N, m, n, kq):
     """Q, K, V of a layer share their input X: in a batch, consecutive jobs with
     the same X and shape run as ONE slice + ONE resident-X contraction over their three Enc(W)s
     + ONE pack launch; the output ciphertexts and R of every job are bit-exact vs the oracle,
-    and a following job with its own X (O) takes the per-job path."""
-    N, L, ell, L_out = 4096, 2, 16, 1
+    and a following job with its own X (O) takes the per-job path.  Shapes: 1, 2 and 3 k-block
+    pairs in the first tile, and fewer column tiles than SMs (N = 256)."""
+    L, ell, L_out = 2, 16, 1
     ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
     pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
     sk = nb.nimbus_keygen(ctx, 55)
     s = oracle.keygen(N, 55)
-    kq, nq, m, n = 70, 1, 300, 700
+    nq = 1
     Xq = ni.gen_X(56, kq * nq, m, ell)
     Xo = ni.gen_X(57, kq * nq, m, ell)
     dXq, dXo = dev_u32(Xq), dev_u32(Xo)
@@ -521,6 +524,43 @@ def test_handles_outlive_context(nb, oracle):
     cts, R = c.run()
     cts_o, R_o = c.oracle_out()
     assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+
+
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,n2,flags", [
+    (4096, 2, 16, 1, 300, 768, 128, 500, 0),      # pack (R = 5) -> resident-X slice
+    (4096, 2, 16, 1, 300, 3072, 128, 700, 0),     # fused R = 1 contraction -> slice
+    (1024, 3, 32, 2, 200, 128, 512, 256, 1),      # packed contraction (C5 path) -> packed slice
+])
+def test_output_feeds_next_input(nb, oracle, N, L, ell, L_out, m, n, kq, n2, flags):
+    """The client share R of one call used as X of the next call on the same stream, with no
+    synchronisation in between: the slice kernels normally read X before their PDL wait, but
+    X is an output of the kernel right before them (which triggers its dependents early), so
+    they must read it after the wait (pdl_outputs_overlap).  Both calls bit-exact vs the oracle."""
+    fl = nb.FLAG_LARGE_K if flags else 0
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out, flags=fl)
+    pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
+    sk = nb.nimbus_keygen(ctx, 91)
+    s = oracle.keygen(N, 91)
+    W1, W2 = ni.gen_W(92, m, n, ell), ni.gen_W(93, n, n2, ell)
+    X1 = ni.gen_X(94, kq, m, ell)
+    w1 = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W1), 92)
+    w2 = nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W2), 93)
+    ws1, ws2 = nb.alloc_workspace(ctx, w1, kq), nb.alloc_workspace(ctx, w2, kq)
+    c1, R1 = nb.alloc_outputs(ctx, w1, kq, 1)
+    c2, R2 = nb.alloc_outputs(ctx, w2, kq, 1)
+    nb.nimbus_sync(ctx)
+    for _ in range(3):                   # a few times: the race, if any, is timing-dependent
+        R1.fill_(-1)
+        torch.cuda.synchronize()
+        nb.nimbus_cop_matmul(ctx, w1, dev_u32(X1), kq, 1, 95, c1, R1, ws1)
+        nb.nimbus_cop_matmul(ctx, w2, R1, kq, 1, 96, c2, R2, ws2)     # X of call 2 = R of call 1
+        nb.nimbus_sync(ctx)
+        E1 = oracle.encrypt_rows(N, L, pr, ell, s, W1, 92)
+        cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E1, X1, n, kq, 1, 95)
+        assert (u32(c1) == cts_o).all() and (u32(R1) == R_o).all()
+        E2 = oracle.encrypt_rows(N, L, pr, ell, s, W2, 93)
+        cts2_o, R2_o = oracle.cop_matmul(N, L, L_out, pr, ell, E2, R_o, n2, kq, 1, 96)
+        assert (u32(c2) == cts2_o).all() and (u32(R2) == R2_o).all()
 
 
 def test_batch_matches_sequential_and_oracle(nb, oracle):
