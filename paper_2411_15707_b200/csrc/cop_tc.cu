@@ -132,6 +132,70 @@ __device__ __forceinline__ void epilogue_tile(const Rns& R, uint32_t tacc, uint3
     }
 }
 
+// Epilogue of the alternating-base single set (TcCfg::SPLIT): accumulators [F0, F1) first (the
+// ones the next tile overwrites), then the rest.  v = sum_s acc_s 2^(8s) is summed in the same
+// 64-bit terms as epilogue_tile (s < 4 shifted exactly, s >= 4 as acc_s (2^(8s) mod p); the sum
+// stays < 2^64 in any order), the first part kept as one uint64 per output.
+template <uint32_t NACC, uint32_t BN, uint32_t F0, uint32_t F1>
+__device__ __forceinline__ void epilogue_split(const Rns& R, uint32_t tacc, uint32_t half, uint32_t row, uint32_t k,
+                                               uint32_t col_base, uint32_t ncol, uint32_t* __restrict__ C,
+                                               uint64_t* rel_first, uint64_t* rel_all) {
+    constexpr uint32_t CPW = BN / 8 / 2;
+    uint64_t P[CPW][8];
+    auto term = [&](uint32_t s, uint32_t v, uint32_t limb) -> uint64_t {
+        return s < 4 ? (uint64_t)v << (8 * s) : (uint64_t)v * R.pow8[limb][s];
+    };
+    {
+        uint32_t v[CPW][F1 - F0][8];
+#pragma unroll
+        for (uint32_t b = 0; b < CPW; b++)
+#pragma unroll
+            for (uint32_t s = F0; s < F1; s++) tmem_ld8(tacc + s * BN + (half * CPW + b) * 8, v[b][s - F0]);
+        tmem_ld_wait();
+        acc_release(rel_first);
+#pragma unroll
+        for (uint32_t b = 0; b < CPW; b++) {
+            const uint32_t limb = ((col_base + (half * CPW + b) * 8) / R.N) % R.L;
+#pragma unroll
+            for (uint32_t u = 0; u < 8; u++) {
+                uint64_t x = 0;
+#pragma unroll
+                for (uint32_t s = F0; s < F1; s++) x += term(s, v[b][s - F0][u], limb);
+                P[b][u] = x;
+            }
+        }
+    }
+    uint32_t v[CPW][NACC - (F1 - F0)][8];
+#pragma unroll
+    for (uint32_t b = 0; b < CPW; b++) {
+        uint32_t q = 0;
+#pragma unroll
+        for (uint32_t s = 0; s < NACC; s++)
+            if (s < F0 || s >= F1) tmem_ld8(tacc + s * BN + (half * CPW + b) * 8, v[b][q++]);
+    }
+    tmem_ld_wait();
+    acc_release(rel_all);
+#pragma unroll
+    for (uint32_t b = 0; b < CPW; b++) {
+        const uint32_t col0 = col_base + (half * CPW + b) * 8;
+        if (col0 >= ncol || row >= k) continue;
+        const uint32_t limb = (col0 / R.N) % R.L;
+        uint32_t out[8];
+#pragma unroll
+        for (uint32_t u = 0; u < 8; u++) {
+            uint64_t x = P[b][u];
+            uint32_t q = 0;
+#pragma unroll
+            for (uint32_t s = 0; s < NACC; s++)
+                if (s < F0 || s >= F1) x += term(s, v[b][q++][u], limb);
+            out[u] = reduce64_pm(x, R.p[limb], R.c32[limb]);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ncol + col0);
+        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+    }
+}
+
 // ------------------------------------------------------------------ R = 1 fused epilogue
 // Output of an R = 1 layer (n > N/2, L = 2 -> L_out = 1): packing is the identity
 // (c~[theta] = c[theta], PAPER.md:672-679 with one row), so the epilogue itself does
@@ -266,10 +330,24 @@ struct TcCfg {
     static constexpr uint32_t ACC_BUFS = ACC_COLS <= 256 ? 2 : 1;
     static constexpr uint32_t BUF_STRIDE = 256;                // TMEM column offset of buffer 1
     static constexpr uint32_t TMEM_COLS = 512;
+    // One set does not fit twice (S_x = 4, BN = 48: 7 x 48 = 336 columns): consecutive tiles
+    // alternate between TMEM bases 0 and B1 = 512 - ACC_COLS, whose sets overlap in
+    // [B1, ACC_COLS).  The epilogue of a base-0 tile drains the accumulators in that overlap
+    // first (acc_LO_A..), of a base-B1 tile its acc_0..HI_B-1, and releases them before the
+    // rest: the next tile's MMAs then wait for half an epilogue instead of a whole one.
+#ifdef NIMBUS_NO_SPLIT
+    static constexpr bool SPLIT = false;
+#else
+    static constexpr bool SPLIT = ACC_BUFS == 1 && ACC_COLS < TMEM_COLS;
+#endif
+    static constexpr uint32_t B1 = TMEM_COLS - ACC_COLS;
+    static constexpr uint32_t LO_A = B1 / BN;                              // base 0: acc_LO_A.. overlap
+    static constexpr uint32_t HI_B = (ACC_COLS - B1 + BN - 1) / BN;        // base B1: acc_0..HI_B-1 overlap
     static constexpr uint32_t EPI_WARPS = 8;
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
     static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
     static_assert(ACC_COLS <= TMEM_COLS, "accumulators exceed TMEM");
+    static_assert(!SPLIT || (LO_A >= 1 && HI_B <= NACC - 1), "split: both phases non-empty");
     static_assert(SMEM <= 232448, "shared memory");
     static_assert((BN / 8) % 2 == 0, "epilogue split");
 };
@@ -289,7 +367,8 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* trel = tempty + 2;      // SPLIT: full release of a tile, by tile parity
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(trel + 2);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CL > 1 ? cluster_ctarank() : 0;
@@ -299,7 +378,9 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
 
     if (warp == 0 && lane == 0) {
         for (uint32_t s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL); }
-        for (uint32_t b = 0; b < 2; b++) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); }
+        for (uint32_t b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); mbar_init(&trel[b], Cfg::EPI_WARPS);
+        }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -348,10 +429,21 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
             for (uint32_t u = cid; u < nunits; u += ncl, ti++) {
                 const uint32_t buf = Cfg::ACC_BUFS == 2 ? (ti & 1) : 0;
                 const uint32_t use = Cfg::ACC_BUFS == 2 ? (ti >> 1) : ti;
-                if (ti >= Cfg::ACC_BUFS) mbar_wait(&tempty[buf], (use & 1) ^ 1);
+                uint32_t dacc;
+                if constexpr (Cfg::SPLIT) {
+                    // tile ti at base (ti & 1) B1: the previous tile's overlapping accumulators drained
+                    // (its first-part release on tempty[0]), and the tile before it (same base) drained
+                    // completely (trel[ti & 1]: only tiles of this parity arrive there, so the barrier
+                    // cannot run two phases ahead of this wait)
+                    if (ti >= 1) mbar_wait(&tempty[0], (ti - 1) & 1);
+                    if (ti >= 2) mbar_wait(&trel[ti & 1], ((ti - 2) >> 1) & 1);
+                    dacc = tmem + (ti & 1) * Cfg::B1;
+                } else {
+                    if (ti >= Cfg::ACC_BUFS) mbar_wait(&tempty[buf], (use & 1) ^ 1);
+                    dacc = tmem + buf * Cfg::BUF_STRIDE;
+                }
                 TRACE(4 + 4 * ti);
                 tc_fence_after();
-                const uint32_t dacc = tmem + buf * Cfg::BUF_STRIDE;
                 for (uint32_t kb = 0; kb < KB; kb++, it++) {
                     const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
                     mbar_wait(&full[s], ph);
@@ -395,8 +487,19 @@ k_cop_tc(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et, 
             mbar_wait(&tfull[buf], use & 1);
             if (ew == 0 && lane == 0) TRACE(6 + 4 * ti);
             tc_fence_after();
-            epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + buf * Cfg::BUF_STRIDE, half,
-                                             mt * Cfg::BM + sub * 32 + lane, k, ct * Cfg::BN, ncol, C, &tempty[buf]);
+            if constexpr (Cfg::SPLIT) {
+                const uint32_t tl = tmem + ((sub * 32) << 16) + (ti & 1) * Cfg::B1;
+                const uint32_t row = mt * Cfg::BM + sub * 32 + lane;
+                if ((ti & 1) == 0)
+                    epilogue_split<Cfg::NACC, Cfg::BN, Cfg::LO_A, Cfg::NACC>(R, tl, half, row, k, ct * Cfg::BN, ncol, C,
+                                                                           &tempty[0], &trel[0]);
+                else
+                    epilogue_split<Cfg::NACC, Cfg::BN, 0, Cfg::HI_B>(R, tl, half, row, k, ct * Cfg::BN, ncol, C,
+                                                                   &tempty[0], &trel[1]);
+            } else {
+                epilogue_tile<Cfg::NACC, Cfg::BN>(R, tmem + ((sub * 32) << 16) + buf * Cfg::BUF_STRIDE, half,
+                                                 mt * Cfg::BM + sub * 32 + lane, k, ct * Cfg::BN, ncol, C, &tempty[buf]);
+            }
             if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
         }
     }
