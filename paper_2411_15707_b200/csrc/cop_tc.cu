@@ -1011,6 +1011,60 @@ k_cop_tc_res2(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__
 // the next -- with one set, the short m = 768 matmuls of C5 (6 k-blocks a tile)
 // idle the tensor pipe for every epilogue -- at the price of more shared-memory
 // fill per MAC (80 KB per 1024 MMA cycles instead of 96 KB per 2048).
+// Transposed-kernel epilogue of the alternating-base single set (TCfgT::SPLIT): lane = one
+// coefficient column, CH chunks of 8 rows; accumulators [F0, F1) of every chunk first (released),
+// then the rest; the same 64-bit terms as the single-set epilogue, the first part kept per row.
+template <uint32_t NACC, uint32_t RT, uint32_t CH, uint32_t F0, uint32_t F1>
+__device__ __forceinline__ void epilogue_t_split(const Rns& R, uint32_t tb, uint32_t row0, uint32_t col, uint32_t limb,
+                                                 uint32_t k, uint32_t ncol, uint32_t* __restrict__ C,
+                                                 uint64_t* rel_first, uint64_t* rel_all) {
+    auto term = [&](uint32_t s, uint32_t v) -> uint64_t {
+        return s < 4 ? (uint64_t)v << (8 * s) : (uint64_t)v * R.pow8[limb][s];
+    };
+    uint64_t P[CH][8];
+    {
+        uint32_t v[CH][F1 - F0][8];
+#pragma unroll
+        for (uint32_t c = 0; c < CH; c++)
+#pragma unroll
+            for (uint32_t s = F0; s < F1; s++) tmem_ld8(tb + s * RT + c * 8, v[c][s - F0]);
+        tmem_ld_wait();
+        acc_release(rel_first);
+#pragma unroll
+        for (uint32_t c = 0; c < CH; c++)
+#pragma unroll
+            for (uint32_t q = 0; q < 8; q++) {
+                uint64_t x = 0;
+#pragma unroll
+                for (uint32_t s = F0; s < F1; s++) x += term(s, v[c][s - F0][q]);
+                P[c][q] = x;
+            }
+    }
+    uint32_t v[CH][NACC - (F1 - F0)][8];
+#pragma unroll
+    for (uint32_t c = 0; c < CH; c++) {
+        uint32_t i = 0;
+#pragma unroll
+        for (uint32_t s = 0; s < NACC; s++)
+            if (s < F0 || s >= F1) tmem_ld8(tb + s * RT + c * 8, v[c][i++]);
+    }
+    tmem_ld_wait();
+    acc_release(rel_all);
+    const uint32_t p = R.p[limb], c32 = R.c32[limb];
+#pragma unroll
+    for (uint32_t c = 0; c < CH; c++)
+#pragma unroll
+        for (uint32_t q = 0; q < 8; q++) {
+            uint64_t x = P[c][q];
+            uint32_t i = 0;
+#pragma unroll
+            for (uint32_t s = 0; s < NACC; s++)
+                if (s < F0 || s >= F1) x += term(s, v[c][i++][q]);
+            const uint32_t row = row0 + c * 8 + q;
+            if (row < k && col < ncol) C[(size_t)row * ncol + col] = reduce64_pm(x, p, c32);
+        }
+}
+
 template <int SX_, int RT_ = 256 / SX_>
 struct TCfgT {
     static constexpr uint32_t BM = kBNW, RT = RT_, BK = kBK, SX = SX_;
@@ -1024,6 +1078,16 @@ struct TCfgT {
     static constexpr uint32_t BUF_STRIDE = 256;            // TMEM column offset of accumulator set 1
     static constexpr uint32_t EPI_BATCH = NACC <= 7 ? 2 : 1;   // 8-row chunks per tcgen05.ld wait (registers)
     static constexpr uint32_t TMEM_COLS = 512;
+    // as TcCfg::SPLIT: one set (S_x = 8: 11 x 32 = 352 columns) at alternating bases 0 / B1 (not
+    // for S_x = 4, RT = 64: 7 x 64 = 448 columns overlap in 384, the first part would be 6 of 7)
+#ifdef NIMBUS_NO_SPLIT
+    static constexpr bool SPLIT = false;
+#else
+    static constexpr bool SPLIT = ACC_BUFS == 1 && ACC_COLS < TMEM_COLS && SX == 8;
+#endif
+    static constexpr uint32_t B1 = TMEM_COLS - ACC_COLS;
+    static constexpr uint32_t LO_A = B1 / RT;                              // base 0: acc_LO_A.. overlap
+    static constexpr uint32_t HI_B = (ACC_COLS - B1 + RT - 1) / RT;        // base B1: acc_0..HI_B-1 overlap
     static constexpr uint32_t EPI_WARPS = 8;
     static constexpr uint32_t THREADS = 128 + 32 * EPI_WARPS;
     static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 256;
@@ -1042,15 +1106,18 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;        // [ACC_BUFS]
-    uint64_t* tempty = tfull + 2;                 // [ACC_BUFS]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tempty = tfull + 2;                 // [ACC_BUFS]; SPLIT: [0] = a tile's first-part release
+    uint64_t* trel = tempty + 2;                  // SPLIT: full release of a tile, by tile parity
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(trel + 2);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nunits = RTt * CT;
     if (threadIdx.x == 0) TRACE(0);
     if (warp == 0 && lane == 0) {
         for (uint32_t s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (uint32_t b = 0; b < 2; b++) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); }
+        for (uint32_t b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1); mbar_init(&tempty[b], Cfg::EPI_WARPS); mbar_init(&trel[b], Cfg::EPI_WARPS);
+        }
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -1092,10 +1159,17 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
             for (uint32_t u = blockIdx.x; u < nunits; u += gridDim.x, ti++) {
                 const uint32_t buf = Cfg::ACC_BUFS == 2 ? (ti & 1) : 0;
                 const uint32_t use = Cfg::ACC_BUFS == 2 ? (ti >> 1) : ti;
-                if (use >= 1) mbar_wait(&tempty[buf], (use - 1) & 1);
+                uint32_t dacc;
+                if constexpr (Cfg::SPLIT) {
+                    if (ti >= 1) mbar_wait(&tempty[0], (ti - 1) & 1);            // previous tile's overlap drained
+                    if (ti >= 2) mbar_wait(&trel[ti & 1], ((ti - 2) >> 1) & 1);  // same-base tile fully drained
+                    dacc = tmem + (ti & 1) * Cfg::B1;
+                } else {
+                    if (use >= 1) mbar_wait(&tempty[buf], (use - 1) & 1);
+                    dacc = tmem + buf * Cfg::BUF_STRIDE;
+                }
                 TRACE(4 + 4 * ti);
                 tc_fence_after();
-                const uint32_t dacc = tmem + buf * Cfg::BUF_STRIDE;
                 for (uint32_t kb = 0; kb < KB; kb++, it++) {
                     const uint32_t s = it % Cfg::STAGES, ph = (it / Cfg::STAGES) & 1;
                     mbar_wait(&full[s], ph);
@@ -1140,6 +1214,18 @@ k_cop_tc_t(Rns R, const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Et
             const uint32_t col = ct * Cfg::BM + sub * 32 + lane;
             const uint32_t limb = (col / R.N) % R.L;
             const uint32_t p = R.p[limb], c32 = R.c32[limb];
+            if constexpr (Cfg::SPLIT) {
+                const uint32_t tb = tmem + ((sub * 32) << 16) + (ti & 1) * Cfg::B1 + half * HR;
+                const uint32_t row0 = rt * Cfg::RT + half * HR;
+                if ((ti & 1) == 0)
+                    epilogue_t_split<Cfg::NACC, Cfg::RT, CH, Cfg::LO_A, Cfg::NACC>(R, tb, row0, col, limb, k, ncol, C,
+                                                                                &tempty[0], &trel[0]);
+                else
+                    epilogue_t_split<Cfg::NACC, Cfg::RT, CH, 0, Cfg::HI_B>(R, tb, row0, col, limb, k, ncol, C,
+                                                                        &tempty[0], &trel[1]);
+                if (ew == 0 && lane == 0) TRACE(7 + 4 * ti);
+                continue;
+            }
             const uint32_t tbase = tmem + ((sub * 32) << 16) + buf * Cfg::BUF_STRIDE + half * HR;
 #pragma unroll 1
             for (uint32_t c0 = 0; c0 < CH; c0 += B) {
