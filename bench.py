@@ -439,9 +439,21 @@ def run_gpu(args, cfg, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         hosts = []
+        # consecutive matmuls with one input that the library runs as one resident-X group (Q, K, V
+        # at k <= 128, ell <= 16, m <= 768, R > 1) get ONE pinned copy, uploaded once per group;
+        # every other matmul gets its own copy (and its own upload)
+        pinned = []
+        prev = None
         for mt in mats:
             lay = mt["lay"]
-            Xh = mt["X"][0].cpu().pin_memory()
+            grp = cfg.ell <= 16 and lay.k <= 128 and lay.m <= 768 and 2 * lay.n <= cfg.N
+            key = mt["X"][0].data_ptr()
+            if grp and prev is not None and prev[0] == key:
+                Xh = prev[1]
+            else:
+                Xh = mt["X"][0].cpu().pin_memory()
+                pinned.append(Xh)
+            prev = (key, Xh) if grp else None
             if wide:
                 c_, R_ = nb.alloc_outputs_u64(ctx, mt["encw"][0], lay.k_per_query, lay.n_queries)
                 ch, Rh = c_.cpu().pin_memory(), R_.cpu().pin_memory()
@@ -449,7 +461,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 ch, Rh = nb.alloc_outputs(ctx, mt["encw"][0], lay.k_per_query, lay.n_queries, pin=True,
                                           device="cpu")
             hosts.append((Xh, ch, Rh))
-        h2d = sum(h[0].numel() * h[0].element_size() for h in hosts)
+        h2d = sum(x.numel() * x.element_size() for x in pinned)
         d2h = sum(h[1].numel() * h[1].element_size() + h[2].numel() * h[2].element_size() for h in hosts)
         host_matmul = nb.nimbus_cop_matmul_host_u64 if wide else nb.nimbus_cop_matmul_host
 

@@ -1010,23 +1010,72 @@ static bool batch_packed(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint
 // Same-X groups (Q, K, V of a layer share their input): consecutive jobs with the
 // same X pointer and shape whose contraction is the resident-X kernel run as ONE contraction
 // launch over their Enc(W)s and one pack launch.  Returns the group length at job i (1 = alone).
+static bool groupable(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t k) {
+    return w && w->d_Et && ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && ctx->res_ring == 1 && resident_ok(ctx, w, k) &&
+           !fused_r1_ok(ctx, w, k) && !getenv("NIMBUS_NO_GROUP");
+}
+
+// the group length at job i: consecutive jobs with the same X pointer (device X here, host X in
+// same_hx_group) and shape, at most 4
 static uint32_t same_x_group(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count, uint32_t i) {
     const nimbus_cop_job& A = jobs[i];
     const uint32_t k = A.k_per_query * A.n_queries;
-    auto ok = [&](const nimbus_cop_job& J) {
-        return J.encw && J.encw->d_Et && ctx->prm.impl == NIMBUS_IMPL_TCGEN05 && ctx->res_ring == 1 &&
-               resident_ok(ctx, J.encw, k) && !fused_r1_ok(ctx, J.encw, k);
-    };
-    if (!ok(A) || getenv("NIMBUS_NO_GROUP")) return 1;
+    if (!groupable(ctx, A.encw, k)) return 1;
     uint32_t g = 1;
     while (g < 4 && i + g < count) {
         const nimbus_cop_job& B = jobs[i + g];
         if (B.d_X != A.d_X || B.k_per_query != A.k_per_query || B.n_queries != A.n_queries || !B.encw ||
-            B.encw->m != A.encw->m || B.encw->n != A.encw->n || !ok(B))
+            B.encw->m != A.encw->m || B.encw->n != A.encw->n || !groupable(ctx, B.encw, k))
             break;
         g++;
     }
     return g;
+}
+
+static uint32_t same_hx_group(const nimbus_ctx* ctx, const nimbus_cop_host_job* jobs, uint32_t count, uint32_t i) {
+    const nimbus_cop_host_job& A = jobs[i];
+    const uint32_t k = A.k_per_query * A.n_queries;
+    if (!groupable(ctx, A.encw, k)) return 1;
+    uint32_t g = 1;
+    while (g < 4 && i + g < count) {
+        const nimbus_cop_host_job& B = jobs[i + g];
+        if (B.h_X != A.h_X || B.k_per_query != A.k_per_query || B.n_queries != A.n_queries || !B.encw ||
+            B.encw->m != A.encw->m || B.encw->n != A.encw->n || !groupable(ctx, B.encw, k))
+            break;
+        g++;
+    }
+    return g;
+}
+
+// one slice of the group's shared X, ONE resident-X contraction over their Enc(W)s into C buffers
+// 0..g-1, ONE pack launch, PDL-chained on stream a (ws: the X planes, then g C buffers of cbytes)
+static cudaError_t run_x_group(nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t g, uint8_t* ws, size_t xt,
+                               size_t cbytes, cudaStream_t a) {
+    const nimbus_cop_job& J = jobs[0];
+    const uint32_t k = J.k_per_query * J.n_queries;
+    prof_mark(ctx, a);
+    cudaError_t e = launch_slice_x(ctx, J.d_X, k, J.encw->m, J.encw->KB, kBM, ws, a);
+    if (e != cudaSuccess) return e;
+    prof_mark(ctx, a);
+    ResJobs RJ;
+    PackJobs PJ;
+    RJ.nj = PJ.nj = g;
+    for (uint32_t q = 0; q < g; q++) {
+        uint32_t* C = reinterpret_cast<uint32_t*>(ws + xt + q * cbytes);
+        RJ.Et[q] = jobs[q].encw->d_Et;
+        RJ.C[q] = C;
+        PJ.C[q] = C;
+        PJ.cts[q] = jobs[q].d_cts;
+        PJ.R[q] = jobs[q].d_R;
+        PJ.key[q] = prg_key(jobs[q].mask_seed, 6);
+    }
+    e = launch_res_jobs(ctx, RJ, J.encw->KB, ws, k, a);
+    if (e != cudaSuccess) return e;
+    prof_mark(ctx, a);
+    prof_mark(ctx, a);
+    e = launch_pack_jobs(ctx, PJ, J.k_per_query, J.n_queries, J.encw->n, a, true);
+    prof_mark(ctx, a);
+    return e;
 }
 
 nimbus_status nimbus_cop_workspace_size_batch(const nimbus_ctx* ctx, const nimbus_cop_job* jobs, uint32_t count,
@@ -1118,25 +1167,7 @@ static nimbus_status cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* job
             // stream may still read buffers 0 / 1
             if (i >= 1) CK(cudaStreamWaitEvent(a, done_p[i - 1], 0), "wait pack");
             if (i >= 2) CK(cudaStreamWaitEvent(a, done_p[i - 2], 0), "wait pack");
-            prof_mark(ctx, a);
-            CK(launch_slice_x(ctx, J.d_X, k, J.encw->m, J.encw->KB, kBM, ws, a), "slice X");
-            prof_mark(ctx, a);
-            ResJobs RJ;
-            PackJobs PJ;
-            RJ.nj = PJ.nj = g;
-            for (uint32_t q = 0; q < g; q++) {
-                RJ.Et[q] = jobs[i + q].encw->d_Et;
-                RJ.C[q] = Cbuf[q];
-                PJ.C[q] = Cbuf[q];
-                PJ.cts[q] = jobs[i + q].d_cts;
-                PJ.R[q] = jobs[i + q].d_R;
-                PJ.key[q] = prg_key(jobs[i + q].mask_seed, 6);
-            }
-            CK(launch_res_jobs(ctx, RJ, J.encw->KB, ws, k, a), "cop group");
-            prof_mark(ctx, a);
-            prof_mark(ctx, a);
-            CK(launch_pack_jobs(ctx, PJ, J.k_per_query, J.n_queries, J.encw->n, a, true), "pack group");
-            prof_mark(ctx, a);
+            CK(run_x_group(ctx, jobs + i, g, ws, xt, cbytes, a), "cop group");
             for (uint32_t q = 0; q < g; q++) {
                 CK(cudaEventRecord(done_c[i + q], a), "record");
                 CK(cudaEventRecord(done_p[i + q], a), "record");
@@ -1445,7 +1476,9 @@ nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* w, 
 // ---------------------------------------------------------------- host-buffer job list, pipelined
 // Workspace: the matmul workspace of the largest job (nimbus_cop_workspace_size),
 // then kHostSlots staging slots (X | cts | R) sized for the largest job.
-static constexpr uint32_t kHostSlots = 4;
+// staging slots of the host-buffer job list: a unit (one job, or a same-X group of up to 4) and
+// the next one are in flight together and must not share a slot, so 8
+static constexpr uint32_t kHostSlots = 8;
 struct HostBatchLayout {
     size_t mm = 0, slot = 0, x = 0, cts = 0, r = 0, total = 0;   // x / cts / r: offsets inside a slot
 };
@@ -1463,6 +1496,17 @@ static HostBatchLayout host_batch_layout(const nimbus_ctx* ctx, const nimbus_cop
         cb = std::max(cb, al((size_t)J.n_queries * cts_per_query(ctx, J.k_per_query, J.encw->n) * 2 *
                              ctx->rns.L_out * ctx->rns.N * 4));
         rb = std::max(rb, al((size_t)k * J.encw->n * es));
+    }
+    // a same-X group runs as one resident-X launch: X planes + one C buffer per job of the group
+    for (uint32_t i = 0; i < count;) {
+        const uint32_t g = same_hx_group(ctx, jobs, count, i);
+        if (g > 1) {
+            const nimbus_cop_host_job& J = jobs[i];
+            const uint32_t k = J.k_per_query * J.n_queries;
+            const WsLayout L = ws_layout(ctx, J.encw, k);
+            H.mm = std::max(H.mm, L.c + g * al((size_t)k * ncols(ctx) * 4));
+        }
+        i += g;
     }
     H.x = 0;
     H.cts = xb;
@@ -1531,30 +1575,55 @@ static nimbus_status cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_hos
         if (i >= kHostSlots) CK(cudaStreamWaitEvent(s, ev_o[i % kHostSlots], 0), "wait slot out");
         return NIMBUS_OK;
     };
-    nimbus_status st = upload(0);
-    if (st == NIMBUS_OK) st = admit(0);
-    for (uint32_t i = 0; i < count && st == NIMBUS_OK; i++) {
+    // a unit is one job, or a same-X group of g jobs (one X upload into the first job's slot, one
+    // resident-X launch; the group's outputs in the slots of its jobs)
+    auto prepare = [&](uint32_t i, uint32_t g) -> nimbus_status {
+        nimbus_status r = upload(i);
+        for (uint32_t q = 1; q < g && r == NIMBUS_OK; q++) {
+            // the other jobs' slots hold no X: their "X ready" is the group's
+            if (cudaEventRecord(ev_x[(i + q) % kHostSlots], up) != cudaSuccess) r = set_err(ctx, NIMBUS_ECUDA, "record");
+        }
+        for (uint32_t q = 0; q < g && r == NIMBUS_OK; q++) r = admit(i + q);
+        return r;
+    };
+    uint32_t g = same_hx_group(ctx, jobs, count, 0);
+    nimbus_status st = prepare(0, g);
+    for (uint32_t i = 0; i < count && st == NIMBUS_OK; i += g) {
+        g = same_hx_group(ctx, jobs, count, i);
         const nimbus_cop_host_job& J = jobs[i];
         const uint32_t k = J.k_per_query * J.n_queries;
         uint8_t* slot = slot_of(i);
-        uint32_t* dcts = reinterpret_cast<uint32_t*>(slot + H.cts);
-        void* dR = slot + H.r;
-        // job i+1's prerequisites go into `stream` BEFORE job i's kernels, so that job i's pack and
-        // job i+1's slice stay adjacent (programmatic dependent launch across jobs)
-        if (i + 1 < count) {
-            st = upload(i + 1);
-            if (st == NIMBUS_OK) st = admit(i + 1);
+        // the next unit's prerequisites go into `stream` BEFORE this unit's kernels, so that its
+        // pack and the next unit's slice stay adjacent (programmatic dependent launch across jobs)
+        if (i + g < count) {
+            st = prepare(i + g, same_hx_group(ctx, jobs, count, i + g));
             if (st != NIMBUS_OK) break;
         }
-        st = cop_matmul(ctx, J.encw, slot + H.x, J.k_per_query, J.n_queries, J.mask_seed, dcts, dR, ws, H.mm,
-                        stream);
-        if (st != NIMBUS_OK) break;
-        CK(cudaEventRecord(ev_c[i % kHostSlots], s), "record");
-        // download job i's outputs while the next jobs compute
-        CK(cudaStreamWaitEvent(down, ev_c[i % kHostSlots], 0), "wait matmul");
-        CK(cudaMemcpyAsync(J.h_cts, dcts, cts_bytes(J), cudaMemcpyDeviceToHost, down), "d2h cts");
-        CK(cudaMemcpyAsync(J.h_R, dR, (size_t)k * J.encw->n * es, cudaMemcpyDeviceToHost, down), "d2h R");
-        CK(cudaEventRecord(ev_o[i % kHostSlots], down), "record");
+        if (g > 1) {
+            nimbus_cop_job dj[4];
+            for (uint32_t q = 0; q < g; q++) {
+                const nimbus_cop_host_job& Jq = jobs[i + q];
+                dj[q] = {Jq.encw, reinterpret_cast<const uint32_t*>(slot + H.x), Jq.k_per_query, Jq.n_queries,
+                         Jq.mask_seed, reinterpret_cast<uint32_t*>(slot_of(i + q) + H.cts),
+                         reinterpret_cast<uint32_t*>(slot_of(i + q) + H.r)};
+            }
+            const WsLayout L = ws_layout(ctx, J.encw, k);
+            CK(run_x_group(ctx, dj, g, ws, L.c, al1k((size_t)k * ncols(ctx) * 4), s), "host batch group");
+        } else {
+            st = cop_matmul(ctx, J.encw, slot + H.x, J.k_per_query, J.n_queries, J.mask_seed,
+                            reinterpret_cast<uint32_t*>(slot + H.cts), slot + H.r, ws, H.mm, stream);
+            if (st != NIMBUS_OK) break;
+        }
+        for (uint32_t q = 0; q < g; q++) {
+            const nimbus_cop_host_job& Jq = jobs[i + q];
+            uint8_t* sq = slot_of(i + q);
+            CK(cudaEventRecord(ev_c[(i + q) % kHostSlots], s), "record");
+            // download the job's outputs while the next jobs compute
+            CK(cudaStreamWaitEvent(down, ev_c[(i + q) % kHostSlots], 0), "wait matmul");
+            CK(cudaMemcpyAsync(Jq.h_cts, sq + H.cts, cts_bytes(Jq), cudaMemcpyDeviceToHost, down), "d2h cts");
+            CK(cudaMemcpyAsync(Jq.h_R, sq + H.r, (size_t)k * Jq.encw->n * es, cudaMemcpyDeviceToHost, down), "d2h R");
+            CK(cudaEventRecord(ev_o[(i + q) % kHostSlots], down), "record");
+        }
     }
     if (st != NIMBUS_OK) {
         cudaStreamSynchronize(up);          // no copy may outlive the call into a buffer the caller frees

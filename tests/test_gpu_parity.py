@@ -255,7 +255,7 @@ def test_host_buffer_api_matches_device(nb, oracle):
 
 
 def test_host_batch_matches_single_calls(nb, oracle):
-    """nimbus_cop_matmul_host_batch (uploads / downloads pipelined over 4 staging
+    """nimbus_cop_matmul_host_batch (uploads / downloads pipelined over 8 staging
     slots) gives, for every job of a mixed list longer than the slot count, the
     bytes nimbus_cop_matmul gives for it; one job checked against the oracle; a
     job list with a device tensor or a bad shape is refused before any work."""
@@ -296,6 +296,49 @@ def test_host_batch_matches_single_calls(nb, oracle):
         nb.nimbus_cop_matmul_host_batch(ctx, [jobs[1], bad], wsb)
     with pytest.raises(nb.NimbusError):
         nb.nimbus_cop_matmul_host_batch(ctx, jobs, wsb[:1024])
+
+
+def test_host_batch_same_x_groups(nb, oracle):
+    """Host-buffer job list with same-X groups (Q, K, V of a layer share one pinned X):
+    the group is uploaded once and runs as one resident-X launch; over several layers (groups of 3
+    next to groups of 3 and single jobs, more jobs than staging slots) every job's ciphertexts and R
+    equal the single device calls; one job checked against the oracle."""
+    N, L, ell, L_out = 4096, 2, 16, 1
+    ctx = nb.nimbus_ctx_create(N, L, ell, L_out)
+    sk = nb.nimbus_keygen(ctx, 31)
+    kq, m, n = 128, 768, 768
+    Ws = [ni.gen_W(170 + i, m, n, ell) for i in range(4)]
+    ws_ = [nb.nimbus_encrypt_weights(ctx, sk, dev_u32(W), 170 + i) for i, W in enumerate(Ws)]
+    jobs, ref = [], []
+    for layer in range(4):
+        Xq = ni.gen_X(180 + layer, kq, m, ell)
+        Xo = ni.gen_X(190 + layer, kq, m, ell)
+        hq = torch.from_numpy(Xq.view(np.int32)).pin_memory()
+        ho = torch.from_numpy(Xo.view(np.int32)).pin_memory()
+        for p in range(4):                       # Q, K, V share hq; O has its own input
+            Xn, hx = (Xq, hq) if p < 3 else (Xo, ho)
+            seed = 200 + 4 * layer + p
+            wsd = nb.alloc_workspace(ctx, ws_[p], kq)
+            c0, R0 = nb.alloc_outputs(ctx, ws_[p], kq, 1)
+            nb.nimbus_cop_matmul(ctx, ws_[p], dev_u32(Xn), kq, 1, seed, c0, R0, wsd)
+            ref.append((c0.cpu(), R0.cpu()))
+            cts, R = nb.alloc_outputs(ctx, ws_[p], kq, 1, pin=True, device="cpu")
+            jobs.append(dict(encw=ws_[p], X=hx, k_per_query=kq, n_queries=1, mask_seed=seed, cts=cts, R=R,
+                             Xn=Xn, p=p))
+    nb.nimbus_sync(ctx)
+    wsb = torch.empty(nb.nimbus_cop_workspace_size_host_batch(ctx, jobs), dtype=torch.uint8, device=DEV)
+    for _ in range(2):
+        for j in jobs:
+            j["cts"].fill_(-1)
+            j["R"].fill_(-1)
+        nb.nimbus_cop_matmul_host_batch(ctx, jobs, wsb)
+        for i, (j, (c0, R0)) in enumerate(zip(jobs, ref)):
+            assert torch.equal(j["cts"], c0) and torch.equal(j["R"], R0), f"job {i}"
+    j = jobs[5]                                   # layer 1, K
+    pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
+    E = oracle.encrypt_rows(N, L, pr, ell, oracle.keygen(N, 31), Ws[1], 171)
+    cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E, j["Xn"], n, kq, 1, j["mask_seed"])
+    assert (u32(j["cts"]) == cts_o).all() and (u32(j["R"]) == R_o).all()
 
 
 def test_host_batch_u64(nb, oracle):
