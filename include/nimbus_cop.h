@@ -312,9 +312,11 @@ nimbus_status nimbus_cop_matmul_host_u64(nimbus_ctx* ctx, const nimbus_encw* enc
 /* A list of independent matmuls with HOST buffers (e.g. many queries, or every
  * layer of many queries' passes), pipelined: job i+1's X upload (copy stream) and
  * job i-1's ciphertext/R download (a second copy stream) run while job i computes
- * on `stream`, through 4 device staging slots.  Each job's outputs
- * are identical to nimbus_cop_matmul_host's for it; jobs must be independent (no
- * job's h_X is another job's output).  Host buffers should be pinned (pageable
+ * on `stream`, through 8 device staging slots.  Consecutive jobs with the same h_X
+ * pointer and shape that nimbus_cop_matmul_batch would run as a same-X group (Q, K,
+ * V of a layer) are uploaded once and run as one contraction launch.
+ * Each job's outputs are identical to nimbus_cop_matmul_host's for it; jobs must be
+ * independent (no job's h_X is another job's output).  Host buffers should be pinned (pageable
  * memory works but the copies then do not overlap).  Synchronises `stream` before
  * returning, so all h_cts / h_R are filled.  Workspace (device):
  * nimbus_cop_workspace_size_host_batch.  Errors are checked for all jobs before
