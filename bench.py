@@ -9,8 +9,9 @@ Default line = BASELINE.json configs[4] (C5): the full BERT-base linear stack,
 matmuls of k = 2048 rows (seq 512 x 4 queries), N=8192, 3 limbs, ell=32 -- the
 north star's "BERT-base FFN layers" in their full-model setting.  The same line
 carries `per_config`: C2 (attention projection), C3 (FFN up), C4 (FFN down),
-each with its own ms_per_step, roofline, cpu_baseline and e2e, plus the paper's
-ell = 64 (C4@l64, C5@l64) as secondary entries.  `--config K` times one config
+each with its own ms_per_step, roofline, cpu_baseline and e2e, plus C4 and C5 at
+ell = 16 (SURVEY.md 8(c) #2's secondary line) and the paper's ell = 64 (C4@l64,
+C5@l64) as secondary entries.  `--config K` times one config
 alone (1..5; 4l16 / 5l16 / 4l64 / 5l64 the secondary parameter sets).
 
 Prints ONE JSON line (rank 0).  Multi-GPU (torchrun): every rank runs its own
@@ -775,9 +776,10 @@ def bench_config(args, key, rank, world, local_rank, steps=None, warmup=None, e2
 
 # ----------------------------------------------------------------- main
 MAIN_CONFIG = "5"
-# (config, steps cap) of the per_config block: C2 / C3 / C4 at the bench's steps, the paper's ell = 64
-# pass at <= 5 steps (a 27 GB Enc(W), ~0.3 s per pass)
-PER_CONFIG = (("2", None), ("2qkv", None), ("3", None), ("4", None), ("4l64", None), ("5l64", 5))
+# (config, steps cap) of the per_config block: C2 / C2-QKV / C3 / C4 / C4@l16 at the bench's steps, the
+# C5@l16 pass and the paper's ell = 64 pass at <= 5 steps (a 27 GB Enc(W), ~0.3 s per pass)
+PER_CONFIG = (("2", None), ("2qkv", None), ("3", None), ("4", None), ("4l16", None), ("5l16", 5), ("4l64", None),
+              ("5l64", 5))
 
 
 def main():
