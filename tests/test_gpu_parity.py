@@ -434,7 +434,9 @@ def test_packed_parity(nb, oracle, monkeypatch, N, L, ell, L_out, m, n, kq, nq):
     c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=7000 + N + m + n, flags=nb.FLAG_LARGE_K)
     before = nb.nimbus_launch_count(c.ctx)
     cts, R = c.run()
-    assert nb.nimbus_launch_count(c.ctx) - before == 2, "packed path not taken"
+    import os
+    if not os.environ.get("NIMBUS_NO_PACKED"):                # switch soaks run the unpacked path here
+        assert nb.nimbus_launch_count(c.ctx) - before == 2, "packed path not taken"
     cts_o, R_o = c.oracle_out()
     assert (u32(cts) == cts_o).all(), "output ciphertexts differ"
     assert (u32(R) == R_o).all(), "client share R differs"
@@ -469,7 +471,9 @@ def test_packed_batch_parity(nb, oracle):
     before = nb.nimbus_launch_count(ctx)
     nb.nimbus_cop_matmul_batch(ctx, jobs, ws)
     nb.nimbus_sync(ctx)
-    assert nb.nimbus_launch_count(ctx) - before == 2
+    import os
+    if not os.environ.get("NIMBUS_NO_PACKED"):
+        assert nb.nimbus_launch_count(ctx) - before == 2
     for i, j in enumerate(jobs):
         E = oracle.encrypt_rows(N, L, pr, ell, s, j["W"], 500 + i)
         cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E, j["Xh"], j["W"].shape[1], j["k_per_query"],
@@ -505,7 +509,9 @@ def test_same_x_group_batch_parity(nb, oracle, N, m, n, kq):
     before = nb.nimbus_launch_count(ctx)
     nb.nimbus_cop_matmul_batch(ctx, jobs, ws)
     nb.nimbus_sync(ctx)
-    assert nb.nimbus_launch_count(ctx) - before == 3 + 3, "group (3 launches) + O (3 launches)"
+    import os
+    if not (os.environ.get("NIMBUS_NO_GROUP") or os.environ.get("NIMBUS_RES", "1") != "1"):   # switch soaks
+        assert nb.nimbus_launch_count(ctx) - before == 3 + 3, "group (3 launches) + O (3 launches)"
     for i, j in enumerate(jobs):
         E = oracle.encrypt_rows(N, L, pr, ell, s, j["W"], 560 + i)
         cts_o, R_o = oracle.cop_matmul(N, L, L_out, pr, ell, E, j["Xh"], n, kq, nq, j["mask_seed"])
