@@ -1608,7 +1608,8 @@ static nimbus_status cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_hos
                          reinterpret_cast<uint32_t*>(slot_of(i + q) + H.r)};
             }
             const WsLayout L = ws_layout(ctx, J.encw, k);
-            CK(run_x_group(ctx, dj, g, ws, L.c, al1k((size_t)k * ncols(ctx) * 4), s), "host batch group");
+            const cudaError_t e = run_x_group(ctx, dj, g, ws, L.c, al1k((size_t)k * ncols(ctx) * 4), s);
+            if (e != cudaSuccess) { st = cuda_err(ctx, e, "host batch group"); break; }
         } else {
             st = cop_matmul(ctx, J.encw, slot + H.x, J.k_per_query, J.n_queries, J.mask_seed,
                             reinterpret_cast<uint32_t*>(slot + H.cts), slot + H.r, ws, H.mm, stream);
