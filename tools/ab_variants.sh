@@ -1,3 +1,6 @@
+#!/bin/bash
+# A/B timing of library builds: VARS = NIMBUS_VARIANT names (built as libnimbus_cop_<v>.so), CFGS = bench
+# configs; one bench line per (config, build).  Run on the GPU box from the repo root.
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
 for v in $VARS; do NIMBUS_VARIANT=$v python -c "from paper_2411_15707_b200 import _build; _build.build()"; done
 for cfg in $CFGS; do

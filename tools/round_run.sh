@@ -1,3 +1,5 @@
+#!/bin/bash
+# A round-end validation run: build, GPU tests, smoke, the default bench line, ncu captures.
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
 timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/full_pytest.log 2>&1; tail -2 gpurun_out/full_pytest.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
