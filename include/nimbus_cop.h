@@ -48,9 +48,10 @@ typedef enum {
 
 enum { NIMBUS_IMPL_TCGEN05 = 0, NIMBUS_IMPL_CUDACORE = 1 };
 /* NIMBUS_FLAG_CHECK_RANGE: check X, W < t on the device (reported by nimbus_sync).
- * NIMBUS_FLAG_LARGE_K: 17 <= ell <= 32 only -- lay Enc(W) out for the transposed
- *   contraction (128-column tiles, Enc(W) planes as the MMA A operand), ~3% faster
- *   when the matmuls have k >= 512 rows (C5), ~7% slower at k = 128 (C4). */
+ * NIMBUS_FLAG_LARGE_K: 9 <= ell <= 32 only -- lay Enc(W) out for the transposed
+ *   contraction (128-column tiles, Enc(W) planes as the MMA A operand), which also feeds
+ *   the packed contraction (matmuls with >= 48 packed ciphertexts and n % 128 == 0: the
+ *   C5 pass); for matmuls with k >= 512 rows (C5), slower at k = 128 (C4). */
 enum { NIMBUS_FLAG_CHECK_RANGE = 1, NIMBUS_FLAG_LARGE_K = 2 };
 
 /* RLWE / workload parameters (App. B.1 {N, q, t}).

@@ -402,13 +402,16 @@ static nimbus_status new_encw(nimbus_ctx* ctx, uint32_t m, uint32_t n, nimbus_en
     // resident-X kernel (tcgen05, ell <= 16, m <= 768) uses 32-column tiles, the streaming kernel 48.
     // The transposed ell = 32 kernel (128-column tiles) is chosen by NIMBUS_FLAG_LARGE_K (or
     // NIMBUS_TRANSPOSED=1): 2.7% faster at C5 (k = 2048) but 7% slower at C4 (k = 128: 768 work
-    // units = 5.19 waves on 148 SMs), and the layout is fixed before k is known.
+    // units = 5.19 waves on 148 SMs), and the layout is fixed before k is known.  At ell <= 16 the
+    // same hint selects it too (ahead of the resident-X layout): there it feeds the packed
+    // contraction at S_x = 2 (the C5@l16 pass) and k_cop_tc_t<2, 64> otherwise.
     w->bn = kBNT;
     if (ctx->prm.impl == NIMBUS_IMPL_TCGEN05) {
         const char* tr = getenv("NIMBUS_TRANSPOSED");
         const bool large_k = (ctx->prm.flags & NIMBUS_FLAG_LARGE_K) || (tr && atoi(tr) == 1);
-        if (sx_of(ctx->rns.ell) == 2 && w->KB <= kResMaxKB && !getenv("NIMBUS_NO_RESIDENT")) w->bn = kBNR;
-        else if (sx_of(ctx->rns.ell) == 4 && ctx->rns.N >= kBNW && large_k) w->bn = kBNW;
+        const uint32_t sx = sx_of(ctx->rns.ell);
+        if ((sx == 4 || sx == 2) && ctx->rns.N >= kBNW && large_k) w->bn = kBNW;
+        else if (sx == 2 && w->KB <= kResMaxKB && !getenv("NIMBUS_NO_RESIDENT")) w->bn = kBNR;
         else if (sx_of(ctx->rns.ell) == 8) w->bn = kBNW;      // 8 X slices: transposed kernel only
     }
     w->bytes = (size_t)w->KB * kBK * col_tiles(ctx, w->bn) * w->bn * 4;
@@ -780,8 +783,11 @@ static WsLayout ws_layout(const nimbus_ctx* ctx, const nimbus_encw* w, uint32_t 
         // per query boundary for up to 64 queries; cop_matmul falls back when a call needs more
         const uint64_t Rr = ctx->rns.N / w->n;
         size_t pk = 0;
-        for (uint32_t rt : {48u, 52u, 56u, 64u})
-            pk = std::max(pk, 1024 + packed_xp_bytes(ctx, w, (k + Rr - 1) / Rr + 64, rt));
+        const uint32_t* cand;
+        uint32_t ncand;
+        packed_rt_candidates(ctx, &cand, &ncand);
+        for (uint32_t i = 0; i < ncand; i++)
+            pk = std::max(pk, 1024 + packed_xp_bytes(ctx, w, (k + Rr - 1) / Rr + 64, cand[i]));
         L.total = std::max(L.total, al(pk));
     }
     return L;

@@ -128,11 +128,9 @@ struct PkCfg {
     static constexpr uint32_t A_BYTES = kSW * BM * BK;     // 64 KB: 4 planes x 128 columns x 128 B
     static constexpr uint32_t P_BYTES = BM * BK;           // one plane: 16 KB
     static constexpr uint32_t B_BYTES = SX * RT * BK;      // S_x slices x RT rows x 128 B
-#ifdef NIMBUS_PK_E9
-    static constexpr uint32_t ESLOTS = (SX * RT * BK * 3 + 9 * BM * BK + 1024 + 512 <= 232448) ? 9 : 8, XSLOTS = 3;
-#else
-    static constexpr uint32_t ESLOTS = 8, XSLOTS = 3;
-#endif
+    // S_x = 2 (ell <= 16) issues half the MMA work per Enc(W) plane, so its planes are consumed twice
+    // as fast: two more slots in flight (the X slot is smaller)
+    static constexpr uint32_t ESLOTS = SX == 2 ? 10 : 8, XSLOTS = 3;
     static constexpr uint32_t OFF_X = ESLOTS * P_BYTES;
     static constexpr uint32_t RING = OFF_X + XSLOTS * B_BYTES;
     static constexpr uint32_t NACC = SX + kSW - 1;
@@ -145,7 +143,8 @@ struct PkCfg {
     static constexpr size_t SMEM = (size_t)RING + 1024 + 512;     // alignment slack + barriers, queue
     static_assert(RT % 4 == 0 && (TAIL == 8 || TAIL == 4), "8-row chunks, a 4-row tail at most");
     static_assert((SX * RT) % 16 == 0 && SX * RT <= 256, "MMA N");
-    static_assert(NACC * RT <= ZCOL && 3 * RT + SX * RT <= ZCOL, "TMEM: accumulators below the zero operand");
+    static_assert(NACC * RT <= ZCOL, "TMEM: accumulators below the zero operand");
+    static_assert(SX == 2 || SX == 4, "packed contraction: 2 or 4 X slices");
     static_assert(B_BYTES % 1024 == 0, "swizzle atoms");
     static_assert(SMEM <= 232448, "shared memory");
 };
@@ -355,9 +354,16 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                         { PKS_T0(t0); mbar_wait(&xfull[xs], (ix / Cfg::XSLOTS) & 1); PKS_ADD(1, t0); }
                         const uint64_t bd = x_desc0 + xs * XP;
                         // a chunk starts from zero accumulators without a TMEM clear: 0 . X (A = the zero
-                        // operand in TMEM) sets acc_3..acc_6, plane 0's first MMA (no accumulate) sets acc_0..3
+                        // operand in TMEM, N = S_x RT columns per MMA) sets acc_S_x..acc_{NACC-1} (S_x = 4: one
+                        // MMA at acc_3; S_x = 2: acc_2 and acc_3), plane 0's first MMA (no accumulate) then sets
+                        // acc_0..acc_{S_x-1}
                         const bool first = kb == c * CKB && r == 0;
-                        if (first && !ghost) mma_i8_ts_w(tmem + 3 * RT, tmem + Cfg::ZCOL, bd, idesc, 0u);
+                        if (first && !ghost) {
+#pragma unroll
+                            for (uint32_t z = SX; z < Cfg::NACC; z += SX)
+                                mma_i8_ts_w(tmem + (z < Cfg::NACC - SX ? z : Cfg::NACC - SX) * RT, tmem + Cfg::ZCOL, bd,
+                                            idesc, 0u);
+                        }
 #pragma unroll
                         for (uint32_t jp = 0; jp < kSW; jp++, ie++) {
                             const uint32_t es = ie % Cfg::ESLOTS;
@@ -731,7 +737,8 @@ static uint32_t pk_sx(const nimbus_ctx* c) { return sx_of(c->rns.ell); }
 
 bool packed_layout_ok(const nimbus_ctx* c, const nimbus_encw* w) {
     const char* off = getenv("NIMBUS_NO_PACKED");
-    return c->prm.impl == NIMBUS_IMPL_TCGEN05 && w->bn == kBNW && pk_sx(c) == 4 && w->n % kBNW == 0 &&
+    return c->prm.impl == NIMBUS_IMPL_TCGEN05 && w->bn == kBNW && (pk_sx(c) == 4 || pk_sx(c) == 2) &&
+           w->n % kBNW == 0 &&
            c->rns.N % kBNW == 0 && c->rns.L - c->rns.L_out >= 1 && c->rns.L - c->rns.L_out <= 2 &&
            !(off && atoi(off) != 0);
 }
@@ -746,14 +753,29 @@ bool packed_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t kq, uint32_t 
     return w->d_corr && w->d_Et && packed_layout_ok(c, w) && nq * pk_nct(c, w, kq) >= 48;
 }
 
-static const uint32_t kPkRT[4] = {48, 52, 56, 64};
+// theta-tile heights with an instantiated kernel: S_x = 4 (MMA N = 4 RT <= 256, 7 RT <= 480 TMEM
+// columns), S_x = 2 (N = 2 RT, 5 accumulators: RT = 72 fits C5's 208 packed ciphertexts per
+// n = 768 matmul in 3 tiles)
+static const uint32_t kPkRT4[4] = {48, 52, 56, 64};
+static const uint32_t kPkRT2[2] = {64, 72};
+
+void packed_rt_candidates(const nimbus_ctx* c, const uint32_t** rts, uint32_t* n) {
+    if (pk_sx(c) == 2) { *rts = kPkRT2; *n = 2; } else { *rts = kPkRT4; *n = 4; }
+}
 
 // RT minimising the padded MMA work of the job list (ties: the larger RT)
 uint32_t packed_rt(const nimbus_ctx* c, const PkHostJob* jobs, uint32_t count) {
+    const uint32_t* cand;
+    uint32_t ncand;
+    packed_rt_candidates(c, &cand, &ncand);
+    const char* force = getenv("NIMBUS_PK_RT");       // experiment switch: one of the candidates
+    if (force)
+        for (uint32_t i = 0; i < ncand; i++)
+            if ((uint32_t)atoi(force) == cand[i]) return cand[i];
     uint64_t best = ~0ull;
-    uint32_t brt = 64;
-    for (int i = 3; i >= 0; i--) {
-        const uint32_t rt = kPkRT[i];
+    uint32_t brt = cand[ncand - 1];
+    for (int i = (int)ncand - 1; i >= 0; i--) {
+        const uint32_t rt = cand[i];
         uint64_t work = 0;
         for (uint32_t j = 0; j < count; j++) {
             const nimbus_encw* w = jobs[j].w;
@@ -809,25 +831,26 @@ static uint32_t max_clusters(nimbus_ctx* c, K kernel, uint32_t CL, size_t smem, 
     return (uint32_t)n;
 }
 
-// CTAs per cluster of the packed contraction: 2 (Enc(W) planes multicast to a theta-tile pair)
-// unless NIMBUS_PK_CL=1 or 4
-static uint32_t pk_cluster() {
+// CTAs per cluster of the packed contraction (NIMBUS_PK_CL=1, 2 or 4 overrides): at S_x = 4, 2
+// (Enc(W) planes multicast to a theta-tile pair: C5 94.0 vs 95.9 ms single); at S_x = 2, 1 -- each
+// plane feeds half the MMA work, and the pair's lockstep costs more than the halved L2 reads (C5@l16:
+// 55.0 ms single vs 65.4 paired vs 68.7 in 4-CTA clusters; the MMA warp waited for Enc(W) 20% vs 29%)
+static uint32_t pk_cluster(uint32_t sx) {
     const char* e = getenv("NIMBUS_PK_CL");
-    const int v = e ? atoi(e) : 2;
+    const int v = e ? atoi(e) : (sx == 2 ? 1 : 2);
     return v == 1 || v == 4 ? (uint32_t)v : 2u;
 }
 
-template <int RT, int CL>
+template <int SX, int RT, int CL>
 static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
                                 void (*mark)(nimbus_ctx*, cudaStream_t)) {
-    using Cfg = PkCfg<4, RT>;
+    using Cfg = PkCfg<SX, RT>;
     std::unique_ptr<PkParams> Pp(new PkParams());     // kernel parameters (copied at launch)
     PkParams& P = *Pp;
-    cudaError_t e = ensure_smem(c, k_cop_pk<4, RT, CL>, Cfg::SMEM);
+    cudaError_t e = ensure_smem(c, k_cop_pk<SX, RT, CL>, Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    static uint32_t ncl_cache[3][4] = {{0}};
-    uint32_t& ncl = ncl_cache[CL == 4 ? 2 : CL - 1][RT == 48 ? 0 : RT == 52 ? 1 : RT == 56 ? 2 : 3];
-    if (!ncl) ncl = max_clusters(c, k_cop_pk<4, RT, CL>, CL, Cfg::SMEM, Cfg::THREADS);
+    static uint32_t ncl = 0;                          // one per instantiation
+    if (!ncl) ncl = max_clusters(c, k_cop_pk<SX, RT, CL>, CL, Cfg::SMEM, Cfg::THREADS);
     const uint32_t NT = c->rns.N / kBNW, ND = c->rns.L - c->rns.L_out;
     for (uint32_t base = 0; base < count; base += kPkMaxJobs) {
         const uint32_t nj = count - base < kPkMaxJobs ? count - base : kPkMaxJobs;
@@ -862,7 +885,7 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
         for (uint32_t i = 0; i < nj && !late; i++)
             late = pdl_outputs_overlap(st, jobs[base + i].d_X,
                                        (size_t)jobs[base + i].kq * jobs[base + i].nq * jobs[base + i].w->m * 4);
-        e = launch_pdl(k_slice_pk<4, RT>, dim3(blocks), dim3(256), 0, st, P, c->rns.ell, c->d_flag, check, late);
+        e = launch_pdl(k_slice_pk<SX, RT>, dim3(blocks), dim3(256), 0, st, P, c->rns.ell, c->d_flag, check, late);
         c->launches++;
         if (e != cudaSuccess) return e;
         if (mark) mark(c, st);
@@ -881,7 +904,7 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
         attr[1].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 2;
-        e = cudaLaunchKernelEx(&cfg, k_cop_pk<4, RT, CL>, c->rns, P, units);
+        e = cudaLaunchKernelEx(&cfg, k_cop_pk<SX, RT, CL>, c->rns, P, units);
         c->launches++;
         {   // the contraction writes the jobs' ciphertexts and R, and triggers its dependents early
             std::vector<const void*> op;
@@ -895,27 +918,33 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
             }
             pdl_outputs_set(st, op.data(), ob.data(), (uint32_t)op.size());
         }
-        snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_pk<4, %d, %d>", RT, CL);
+        snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_pk<%d, %d, %d>", SX, RT, CL);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }
 
-template <int RT>
+template <int SX, int RT>
 static cudaError_t launch_pk_cl(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
                                 void (*mark)(nimbus_ctx*, cudaStream_t)) {
-    const uint32_t cl = pk_cluster();
-    return cl == 2 ? launch_pk_rt<RT, 2>(c, jobs, count, d_ctr, st, mark)
-           : cl == 4 ? launch_pk_rt<RT, 4>(c, jobs, count, d_ctr, st, mark)
-                     : launch_pk_rt<RT, 1>(c, jobs, count, d_ctr, st, mark);
+    const uint32_t cl = pk_cluster(SX);
+    return cl == 2 ? launch_pk_rt<SX, RT, 2>(c, jobs, count, d_ctr, st, mark)
+           : cl == 4 ? launch_pk_rt<SX, RT, 4>(c, jobs, count, d_ctr, st, mark)
+                     : launch_pk_rt<SX, RT, 1>(c, jobs, count, d_ctr, st, mark);
 }
 
 cudaError_t launch_cop_packed(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t rt, uint32_t* d_ctr,
                               cudaStream_t st, void (*mark)(nimbus_ctx*, cudaStream_t)) {
-    if (rt == 48) return launch_pk_cl<48>(c, jobs, count, d_ctr, st, mark);
-    if (rt == 52) return launch_pk_cl<52>(c, jobs, count, d_ctr, st, mark);
-    if (rt == 56) return launch_pk_cl<56>(c, jobs, count, d_ctr, st, mark);
-    return launch_pk_cl<64>(c, jobs, count, d_ctr, st, mark);
+    if (pk_sx(c) == 2) {
+        if (rt == 72) return launch_pk_cl<2, 72>(c, jobs, count, d_ctr, st, mark);
+        if (rt == 64) return launch_pk_cl<2, 64>(c, jobs, count, d_ctr, st, mark);
+        return cudaErrorInvalidValue;
+    }
+    if (rt == 48) return launch_pk_cl<4, 48>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 52) return launch_pk_cl<4, 52>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 56) return launch_pk_cl<4, 56>(c, jobs, count, d_ctr, st, mark);
+    if (rt == 64) return launch_pk_cl<4, 64>(c, jobs, count, d_ctr, st, mark);
+    return cudaErrorInvalidValue;
 }
 
 // ColSum -> corr for a freshly tiled Enc(W) (every path that fills w->d_Et)

@@ -1397,6 +1397,7 @@ static cudaError_t launch_cl(nimbus_ctx* c, const nimbus_encw* w, const uint8_t*
 // epilogue overlapped: C5 115.5 vs 108.3 ms -- the extra fill per MAC costs more)
 uint32_t transposed_rows(const nimbus_ctx* c) {
     if (sx_of(c->rns.ell) == 8) return 32;
+    if (sx_of(c->rns.ell) == 2) return 64;       // 5 accumulators x 64 rows, N = 128
     const char* env = getenv("NIMBUS_T_RT");     // read per call: the slice and the kernel agree
     return env && atoi(env) == 32 ? 32 : 64;
 }
@@ -1408,6 +1409,7 @@ cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_
         if (SX == 4) return transposed_rows(c) == 32 ? launch_t<4, 32>(c, w, d_Xt, k, d_C, st)
                                                      : launch_t<4, 64>(c, w, d_Xt, k, d_C, st);
         if (SX == 8) return launch_t<8, 32>(c, w, d_Xt, k, d_C, st);
+        if (SX == 2) return launch_t<2, 64>(c, w, d_Xt, k, d_C, st);
         return cudaErrorInvalidValue;
     }
     if (SX == 8) return cudaErrorInvalidValue;    // 8 slices only in the transposed orientation

@@ -218,6 +218,8 @@ cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8
 bool packed_layout_ok(const nimbus_ctx* c, const nimbus_encw* w);
 bool packed_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t kq, uint32_t nq);
 uint32_t packed_rt(const nimbus_ctx* c, const PkHostJob* jobs, uint32_t count);
+// the theta-tile heights the packed contraction is instantiated for at this context's S_x
+void packed_rt_candidates(const nimbus_ctx* c, const uint32_t** rts, uint32_t* n);
 // workspace bytes of one packed job (packed X slices, dropped-limb residues, flags)
 size_t packed_xp_bytes(const nimbus_ctx* c, const nimbus_encw* w, uint64_t ntheta, uint32_t rt);
 size_t packed_job_bytes(const nimbus_ctx* c, const PkHostJob& j, uint32_t rt);

@@ -140,7 +140,8 @@ cudaError_t launch_slice_x(nimbus_ctx* c, const void* d_Xv, uint32_t k, uint32_t
         const int check64 = (c->prm.flags & NIMBUS_FLAG_CHECK_RANGE) && ell < 64;
         e = launch_pdl(k_slice_x<8, 32, uint64_t>, g, 256, 0, st, static_cast<const uint64_t*>(d_Xv), k, m, KB, ell,
                        d_Xt, total, c->d_flag, check64, late);
-    } else if (rt == 64) e = launch_pdl(k_slice_x<4, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
+    } else if (rt == 64 && SX == 2) e = launch_pdl(k_slice_x<2, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
+    else if (rt == 64) e = launch_pdl(k_slice_x<4, 64>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
     else if (rt == 32) e = launch_pdl(k_slice_x<4, 32>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
     else if (SX == 1) e = launch_pdl(k_slice_x<1, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);
     else if (SX == 2) e = launch_pdl(k_slice_x<2, 128>, g, 256, 0, st, d_X, k, m, KB, ell, d_Xt, total, c->d_flag, check, late);

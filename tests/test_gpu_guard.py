@@ -83,6 +83,9 @@ def _matmul_guarded(nb, ctx, w, X, kq, nq, seed, wide=False):
     ({}, 4096, 2, 16, 1, 1000, 300, 150, 2, 0),                     # streaming (k > 128, m > 768)
     ({}, 8192, 3, 32, 2, 300, 1000, 70, 3, 0),                      # streaming, ell = 32, 2 output limbs
     ({"NIMBUS_TRANSPOSED": "1"}, 8192, 3, 32, 2, 257, 129, 65, 2, 0),   # transposed, ell = 32
+    ({"NIMBUS_TRANSPOSED": "1"}, 1024, 3, 16, 1, 257, 129, 65, 2, 0),   # transposed, ell = 16 (S_x = 2)
+    ({"NIMBUS_TRANSPOSED": "1"}, 1024, 3, 32, 2, 200, 128, 300, 2, 0),  # packed contraction, S_x = 4
+    ({"NIMBUS_TRANSPOSED": "1"}, 1024, 3, 16, 1, 200, 128, 300, 2, 0),  # packed contraction, S_x = 2
     ({"NIMBUS_CLUSTER": "2", "NIMBUS_NO_RESIDENT": "1"}, 4096, 2, 16, 1, 200, 100, 130, 1, 0),
     ({}, 4096, 2, 16, 1, 300, 1000, 70, 1, 1),                      # CUDA-core ablation
     ({}, 4096, 2, 16, 1, 300, 2051, 60, 2, 0),                      # fused R = 1 epilogue, ragged R tail

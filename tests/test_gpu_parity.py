@@ -396,11 +396,12 @@ def test_c4_full_size(nb, oracle, ell, L_out):
     c.check_decrypt(cts, R)
 
 
-@pytest.mark.parametrize("proj", [0, 4, 5])
-def test_c5_layer_matmuls(nb, oracle, proj):
+@pytest.mark.parametrize("ell,proj", [(32, 0), (32, 4), (32, 5), (16, 0), (16, 4), (16, 5)])
+def test_c5_layer_matmuls(nb, oracle, ell, proj):
     """C5: seq 512 x 4 queries (k=2048) on the Q (768x768), FFN-up (768x3072) and
-    FFN-down (3072x768) shapes of layer 0, same launch as bench --config 5."""
-    cfg = ni.CONFIGS[5]
+    FFN-down (3072x768) shapes of layer 0, same launch as bench --config 5 (ell = 32: the
+    packed contraction at S_x = 4) and --config 5l16 (ell = 16: S_x = 2)."""
+    cfg = ni.CONFIGS[5] if ell == 32 else ni.CONFIGS_L16[5]
     li, pj, lay = cfg.layers[proj]
     seed = ni.seed_mm(5, li, pj)
     c = Case(nb, oracle, cfg.N, cfg.L, cfg.ell, cfg.L_out, lay.m, lay.n, lay.k_per_query, lay.n_queries,
@@ -422,6 +423,14 @@ PACKED_CASES = [
     (1024, 3, 32, 2, 129, 1024, 60, 1),        # n = N: R = 1, no wrapped term at all
     (1024, 3, 32, 2, 200, 128, 416, 2),        # 104 theta = 2 tiles of RT = 52 (4-row accumulator tail chunk)
     (8192, 3, 32, 2, 257, 768, 500, 1),        # C5 geometry (R = 10, 50 theta, the last one holding 0 of 10 rows... ragged)
+    # ell <= 16: S_x = 2 (5 accumulators, theta tiles of RT = 64 or 72)
+    (1024, 3, 16, 1, 200, 128, 300, 2),        # R = 8, 76 theta: RT = 64, two tiles (last ragged), ragged m
+    (2048, 3, 16, 1, 600, 256, 190, 3),        # R = 8, 72 theta = one RT = 72 tile over 3 queries
+    (2048, 3, 16, 1, 600, 128, 100, 8),        # R = 16: 4 k-blocks per accumulator drain, KB = 5 -> 2 chunks
+    (1024, 3, 16, 1, 300, 384, 100, 1),        # two dropped limbs, R = 2
+    (1024, 2, 16, 1, 129, 1024, 60, 1),        # n = N: R = 1, one dropped limb
+    (2048, 3, 12, 1, 300, 128, 100, 8),        # ell = 12 (t = 2^12, complement over 16 bits)
+    (8192, 3, 16, 1, 257, 768, 500, 1),        # C5@l16 geometry
 ]
 
 
@@ -450,10 +459,11 @@ def test_packed_parity(nb, oracle, monkeypatch, N, L, ell, L_out, m, n, kq, nq):
     assert torch.equal(cts, cts2) and torch.equal(R, R2)
 
 
-def test_packed_batch_parity(nb, oracle):
+@pytest.mark.parametrize("ell,L_out", [(32, 2), (16, 1)])
+def test_packed_batch_parity(nb, oracle, ell, L_out):
     """A C5-like job list (Q/up/down shapes at a small N) as ONE packed slice launch
-    and ONE packed contraction launch: every job bit-exact vs the oracle."""
-    N, L, ell, L_out = 2048, 3, 32, 2
+    and ONE packed contraction launch: every job bit-exact vs the oracle (S_x = 4 and 2)."""
+    N, L = 2048, 3
     ctx = nb.nimbus_ctx_create(N, L, ell, L_out, flags=nb.FLAG_LARGE_K)
     pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
     sk = nb.nimbus_keygen(ctx, 77)
@@ -579,6 +589,7 @@ def test_handles_outlive_context(nb, oracle):
     (4096, 2, 16, 1, 300, 768, 128, 500, 0),      # pack (R = 5) -> resident-X slice
     (4096, 2, 16, 1, 300, 3072, 128, 700, 0),     # fused R = 1 contraction -> slice
     (1024, 3, 32, 2, 200, 128, 512, 256, 1),      # packed contraction (C5 path) -> packed slice
+    (1024, 3, 16, 1, 200, 128, 512, 256, 1),      # the same at S_x = 2 (C5@l16 path)
 ])
 def test_output_feeds_next_input(nb, oracle, N, L, ell, L_out, m, n, kq, n2, flags):
     """The client share R of one call used as X of the next call on the same stream, with no
@@ -1061,6 +1072,45 @@ def _fuzz_cases(count=None, seed=None):
         nq = int(rng.integers(1, 3))
         out.append((N, L, ell, L_out, m, n, kq, nq))
     return out
+
+
+def _fuzz_cases_large_k(count=16, seed=31337):
+    """Seeded shapes for the NIMBUS_FLAG_LARGE_K layout (128-column tiles) at ell in (8, 32]:
+    half of them with n a multiple of 128 and enough rows for the packed contraction."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(count):
+        N = int(rng.choice([256, 512, 1024, 2048]))
+        ell = int(rng.choice([12, 16, 24, 32]))
+        L, L_out = (3, 1) if ell <= 16 else (3, 2)
+        if i % 2 == 0:
+            n = 128 * int(rng.integers(1, N // 128 + 1))
+            R = N // n
+            kq = int(rng.integers(48 * R // 2 + 1, 48 * R + 200))
+            nq = 2
+        else:
+            n = int(rng.integers(1, N + 1))
+            kq = int(rng.integers(1, 300))
+            nq = int(rng.integers(1, 3))
+        m = int(rng.integers(1, 700))
+        out.append((N, L, ell, L_out, m, n, kq, nq))
+    return out
+
+
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", _fuzz_cases_large_k())
+def test_random_shapes_large_k_parity(nb, oracle, N, L, ell, L_out, m, n, kq, nq):
+    """Seeded random shapes on the transposed layout (NIMBUS_FLAG_LARGE_K): the packed
+    contraction at S_x = 2 and 4 where it applies, the transposed row-wise kernel otherwise;
+    bit-exact vs the oracle and decrypting to X.W - R mod t."""
+    try:
+        c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=0xA00 + m * 7 + n, flags=nb.FLAG_LARGE_K)
+        cts, R = c.run()
+    except nb.NimbusError as e:
+        assert e.status == -4
+        return
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+    c.check_decrypt(cts, R)
 
 
 @pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", _fuzz_cases())

@@ -19,7 +19,7 @@ ap.add_argument("--layers", type=int, default=12)
 ap.add_argument("--config", default="5")
 ap.add_argument("--projs", default="Q,K,V,O,up,down", help="projections of each layer to include")
 args = ap.parse_args()
-cfg = ni.CONFIGS[int(args.config)]
+cfg = ni.CONFIGS_L16[int(args.config[0])] if args.config.endswith("l16") else ni.CONFIGS[int(args.config)]
 keep = [ni._PROJ.index(p) for p in args.projs.split(",")]
 ctx = nb.nimbus_ctx_create(cfg.N, cfg.L, cfg.ell, cfg.L_out, flags=nb.FLAG_LARGE_K)
 sk = nb.nimbus_keygen(ctx, 1)
