@@ -122,17 +122,25 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 // slots holding ONE byte plane (128 columns x 128 B = 16 KB) each, and an X ring of XSLOTS
 // slots holding the S_x slices of one (term r, k-block).  A 2-slot ring of whole
 // (E + X) k-steps left the MMA issuer waiting for data ~25% of the time (L2 latency).
-template <int SX, int RT>
+//
+// P2 (CTA pairs, tcgen05 cta_group::2): the pair's MMA is M = 256 -- two neighbouring J tiles, CTA
+// r holding the Enc(W) plane of tile 2P + r -- over ONE theta tile whose X block is split by rows
+// (the MMA's N): CTA r holds slices [r S_x/2, (r+1) S_x/2).  Each SM then reads its A half and its
+// B half per MMA instead of a whole B, and fills half the X: the single-CTA / multicast form reads
+// A 4 KB + B 6.5 KB per 104-cycle MMA and fills 54 B/cycle more, above the 128 B/cycle of shared
+// memory (smem-bound at ~0.82 of the tensor rate); the pair form needs ~110 B/cycle.
+template <int SX, int RT, bool P2 = false>
 struct PkCfg {
     static constexpr uint32_t BM = kBNW, BK = kBK;
     static constexpr uint32_t A_BYTES = kSW * BM * BK;     // 64 KB: 4 planes x 128 columns x 128 B
     static constexpr uint32_t P_BYTES = BM * BK;           // one plane: 16 KB
     static constexpr uint32_t B_BYTES = SX * RT * BK;      // S_x slices x RT rows x 128 B
+    static constexpr uint32_t XB = P2 ? B_BYTES / 2 : B_BYTES;   // this CTA's part of an X block
     // S_x = 2 (ell <= 16) issues half the MMA work per Enc(W) plane, so its planes are consumed twice
-    // as fast: two more slots in flight (the X slot is smaller)
-    static constexpr uint32_t ESLOTS = SX == 2 ? 10 : 8, XSLOTS = 3;
+    // as fast, and P2 halves the X slots: two more Enc(W) slots in flight
+    static constexpr uint32_t ESLOTS = (SX == 2 || P2) ? 10 : 8, XSLOTS = 3;
     static constexpr uint32_t OFF_X = ESLOTS * P_BYTES;
-    static constexpr uint32_t RING = OFF_X + XSLOTS * B_BYTES;
+    static constexpr uint32_t RING = OFF_X + XSLOTS * XB;
     static constexpr uint32_t NACC = SX + kSW - 1;
     static constexpr uint32_t ZCOL = 480;                  // TMEM columns [480, 488): a zero A operand
     static constexpr uint32_t NCHK = (RT + 7) / 8;         // 8-row chunks of an accumulator (the last may hold 4)
@@ -145,7 +153,9 @@ struct PkCfg {
     static_assert((SX * RT) % 16 == 0 && SX * RT <= 256, "MMA N");
     static_assert(NACC * RT <= ZCOL, "TMEM: accumulators below the zero operand");
     static_assert(SX == 2 || SX == 4, "packed contraction: 2 or 4 X slices");
-    static_assert(B_BYTES % 1024 == 0, "swizzle atoms");
+    static_assert(XB % 1024 == 0, "swizzle atoms");
+    // cta_group::2 kind::i8 takes N in steps of 16 (N = 208, RT = 52, checked bit-exact on B200)
+    static_assert(!P2 || (SX * RT) % 16 == 0, "cta_group::2 kind::i8: N a multiple of 16");
     static_assert(SMEM <= 232448, "shared memory");
 };
 
@@ -158,13 +168,22 @@ struct PkUnit {
 };
 // j: the caller's job cursor -- a CTA receives its units in increasing order, so the job search
 // resumes where the previous unit's ended (a scan from job 0 per unit cost ~8% of the pass)
+// P2: the pair takes J tiles 2 Tp + rank of one theta tile instead.
 __device__ __forceinline__ PkUnit pk_decode(const PkParams& P, uint32_t u, uint32_t NT, uint32_t CL, uint32_t rank,
-                                            uint32_t& j) {
+                                            uint32_t& j, bool p2 = false) {
     PkUnit x;
     while (u >= P.job[j].unit_end) j++;
     uint32_t v = u - (j ? P.job[j - 1].unit_end : 0u);
-    const uint32_t G = (P.job[j].TT + CL - 1) / CL;
     x.j = j;
+    if (p2) {
+        const uint32_t NTp = NT >> 1;
+        x.T = (v % NTp) * 2 + rank; v /= NTp;
+        x.tt = v % P.job[j].TT; v /= P.job[j].TT;
+        x.comp = v & 1;
+        x.pass = v >> 1;
+        return x;
+    }
+    const uint32_t G = (P.job[j].TT + CL - 1) / CL;
     x.T = v % NT; v /= NT;
     x.tt = (v % G) * CL + rank; v /= G;
     x.comp = v & 1;
@@ -198,14 +217,57 @@ __device__ __forceinline__ void mbar_arrive_cl(uint64_t* bar, uint32_t cta) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(mapa_cl(smem_u32(bar), cta))
                  : "memory");
 }
+// the same without release semantics: the P2 relay publishes no writes of its own (the bulk copies it
+// reports are complete at its local barrier), and a release per arrive serialises the relay thread
+__device__ __forceinline__ void mbar_arrive_cl_relaxed(uint64_t* bar, uint32_t cta) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" :: "r"(mapa_cl(smem_u32(bar), cta))
+                 : "memory");
+}
 __device__ __forceinline__ void st_cl_u32(uint32_t* p, uint32_t cta, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(mapa_cl(smem_u32(p), cta)), "r"(v) : "memory");
 }
 
-template <int SX, int RT, int CL>
-__global__ void __launch_bounds__(PkCfg<SX, RT>::THREADS, 1)
+// ---- tcgen05 with cta_group::2 (P2: every tcgen05 instruction of the kernel uses the pair form)
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(dst_smem)), "r"(ncols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void mma2_i8_ss_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void mma2_i8_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+        :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// arrive on the mbarrier at this offset in both CTAs of the pair when the pair's MMAs complete
+__device__ __forceinline__ void mma2_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+        :: "r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+
+template <int SX, int RT, int CL, bool P2 = false>
+__global__ void __launch_bounds__(PkCfg<SX, RT, P2>::THREADS, 1)
 k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint32_t total_units) {
-    using Cfg = PkCfg<SX, RT>;
+    using Cfg = PkCfg<SX, RT, P2>;
+    static_assert(!P2 || CL == 2, "P2: CTA pairs");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* efull = reinterpret_cast<uint64_t*>(smem + Cfg::RING);
@@ -224,11 +286,14 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
     PKS_DECL;
     const uint32_t N = R.N, NT = N / Cfg::BM, L = R.L, ND = R.L - R.L_out;
     constexpr uint32_t MASK = (1u << CL) - 1;
+    // P2: the leader's full barriers also wait for the peer's copies (relayed by the peer's warp 1),
+    // its tempty for both CTAs' epilogues; the pair's commits arrive on both CTAs' empty barriers
+    const uint32_t nfull = P2 && rank == 0 ? 2 : 1;
     if (warp == 0 && lane == 0) {
-        for (uint32_t s = 0; s < Cfg::ESLOTS; s++) { mbar_init(&efull[s], 1); mbar_init(&eempty[s], CL); }
-        for (uint32_t s = 0; s < Cfg::XSLOTS; s++) { mbar_init(&xfull[s], 1); mbar_init(&xempty[s], 1); }
+        for (uint32_t s = 0; s < Cfg::ESLOTS; s++) { mbar_init(&efull[s], nfull); mbar_init(&eempty[s], P2 ? 1 : CL); }
+        for (uint32_t s = 0; s < Cfg::XSLOTS; s++) { mbar_init(&xfull[s], nfull); mbar_init(&xempty[s], 1); }
         mbar_init(tfull, 1);
-        mbar_init(tempty, Cfg::EPI_WARPS);
+        mbar_init(tempty, Cfg::EPI_WARPS * nfull);
         // unit ids come from the cluster's leader; its queue slot is free once every consumer of
         // every CTA has read it (MMA warp + epilogue warps, and the peers' producers)
         for (uint32_t q = 0; q < kPkQ; q++) {
@@ -237,7 +302,12 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    if constexpr (P2) {
+        cluster_sync();                                 // both CTAs running before the pair allocation
+        if (warp == 2) tmem_alloc2(tmem_slot, 512);
+    } else {
+        if (warp == 2) tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
     if (CL > 1) cluster_sync(); else __syncthreads();   // the peers' barriers exist before any multicast
     tc_fence_after();
@@ -278,7 +348,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                     u = take_unit(i, true);
                 }
                 if (u >= total_units) break;
-                const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur);
+                const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur, P2);
                 const PkJob& J = P.job[U.j];
                 const bool ghost = U.tt >= J.TT;                      // a cluster's spare theta tile
                 const uint32_t limb = pk_limb(R, U.pass);
@@ -296,11 +366,12 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                             if (ghost) {
                                 mbar_arrive(&xfull[s]);
                             } else {
-                                mbar_arrive_expect_tx(&xfull[s], Cfg::B_BYTES);
-                                bulk_g2s(smem + Cfg::OFF_X + s * Cfg::B_BYTES,
+                                // (P2: this CTA's half of the block; the pair's wrap agrees, n / 128 even)
+                                mbar_arrive_expect_tx(&xfull[s], Cfg::XB);
+                                bulk_g2s(smem + Cfg::OFF_X + s * Cfg::XB,
                                          J.Xp + ((((size_t)(2 * r + (wrap ? 1 : 0)) * J.TT + U.tt) * J.KB + kb) *
-                                                 Cfg::B_BYTES),
-                                         Cfg::B_BYTES, &xfull[s], pol_x);
+                                                 Cfg::B_BYTES) + (P2 ? rank * Cfg::XB : 0u),
+                                         Cfg::XB, &xfull[s], pol_x);
                             }
                         }
                         const uint8_t* eb = J.Et + ((slab + srcT) * J.KB + kb) * Cfg::A_BYTES;
@@ -313,7 +384,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                                 PKS_ADD(9, t0);
                             }
                             mbar_arrive_expect_tx(&efull[s], Cfg::P_BYTES);
-                            if (CL == 1)
+                            if (CL == 1 || P2)      // P2: each CTA its own J tile's plane
                                 bulk_g2s(smem + s * Cfg::P_BYTES, eb + jp * Cfg::P_BYTES, Cfg::P_BYTES, &efull[s], pol_e);
                             else if (jp % CL == rank)
                                 bulk_g2s_mc(smem + s * Cfg::P_BYTES, eb + jp * Cfg::P_BYTES, Cfg::P_BYTES, &efull[s],
@@ -323,14 +394,42 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                 }
             }
         }
+    } else if (warp == 1 && P2 && rank != 0) {
+        // ---------------- P2 peer: relay.  The pair's MMAs read this CTA's Enc(W) planes and X half,
+        // so the leader's full barriers must also see this CTA's copies land: in the producer's order,
+        // wait for each local full barrier and arrive on the leader's (release, cluster scope)
+        uint32_t ie = 0, ix = 0, jcur = 0;
+        for (uint32_t i = 0;; i++) {
+            const uint32_t u = take_unit(i, false);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cl(&qempty[i % kPkQ], 0);
+            if (u >= total_units) break;
+            const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur, P2);
+            const uint32_t KB = P.job[U.j].KB, Rr = P.job[U.j].Rr;
+            if (lane == 0) {
+                for (uint32_t kb = 0; kb < KB; kb++) {
+                    for (uint32_t r = 0; r < Rr; r++, ix++) {
+                        mbar_wait(&xfull[ix % Cfg::XSLOTS], (ix / Cfg::XSLOTS) & 1);
+                        mbar_arrive_cl_relaxed(&xfull[ix % Cfg::XSLOTS], 0);
+                        for (uint32_t jp = 0; jp < kSW; jp++, ie++) {
+                            mbar_wait(&efull[ie % Cfg::ESLOTS], (ie / Cfg::ESLOTS) & 1);
+                            mbar_arrive_cl_relaxed(&efull[ie % Cfg::ESLOTS], 0);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
     } else if (warp == 1) {
         // ---------------- MMA issuer (the whole warp, converged; one elected lane issues):
         // D[coefficient][theta] += E_j^T . [x_0 | x_1 | .. ] per plane j.  Descriptors are the slot
-        // base descriptors plus (kk * 32 B) >> 4 in the start-address field.
-        constexpr uint32_t idesc = idesc_i8(Cfg::BM, SX * RT);
+        // base descriptors plus (kk * 32 B) >> 4 in the start-address field.  P2: the leader issues
+        // the pair's M = 256 MMAs (A: each CTA's plane, B: each CTA's half of the X block, D: each
+        // CTA's 128 coefficient lanes x all S_x RT columns -- the same accumulator layout).
+        constexpr uint32_t idesc = idesc_i8(P2 ? 2 * Cfg::BM : Cfg::BM, SX * RT);
         const uint64_t e_desc0 = sdesc_kmajor_sw128(smem_u32(smem));
         const uint64_t x_desc0 = sdesc_kmajor_sw128(smem_u32(smem + Cfg::OFF_X));
-        constexpr uint64_t EP = Cfg::P_BYTES >> 4, XP = Cfg::B_BYTES >> 4;
+        constexpr uint64_t EP = Cfg::P_BYTES >> 4, XP = Cfg::XB >> 4;
         uint32_t ie = 0, ix = 0, gc = 0, jcur = 0;
         PKS_T0(t_mma0);
         for (uint32_t i = 0;; i++) {
@@ -341,17 +440,26 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
             }
             if (u >= total_units) { PKS_ADD(3, t_mma0); break; }
             PKS_INC(7);
-            const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur);
+            const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur, P2);
             const uint32_t KB = P.job[U.j].KB, Rr = P.job[U.j].Rr, CKB = P.job[U.j].CKB, NCH = P.job[U.j].NCH;
             const bool ghost = U.tt >= P.job[U.j].TT;
             for (uint32_t c = 0; c < NCH; c++, gc++) {
-                { PKS_T0(t0); mbar_wait(tempty, gc & 1); PKS_ADD(0, t0); }   // accumulators drained (and zeroed)
+                {   // accumulators drained (and zeroed) -- P2: in both CTAs
+                    PKS_T0(t0);
+                    if (P2) mbar_wait_cl(tempty, gc & 1); else mbar_wait(tempty, gc & 1);
+                    PKS_ADD(0, t0);
+                }
                 tc_fence_after();
                 const uint32_t kb1 = min(KB, (c + 1) * CKB);
                 for (uint32_t kb = c * CKB; kb < kb1; kb++) {
                     for (uint32_t r = 0; r < Rr; r++, ix++) {
                         const uint32_t xs = ix % Cfg::XSLOTS;
-                        { PKS_T0(t0); mbar_wait(&xfull[xs], (ix / Cfg::XSLOTS) & 1); PKS_ADD(1, t0); }
+                        {
+                            PKS_T0(t0);
+                            if (P2) mbar_wait_cl(&xfull[xs], (ix / Cfg::XSLOTS) & 1);
+                            else mbar_wait(&xfull[xs], (ix / Cfg::XSLOTS) & 1);
+                            PKS_ADD(1, t0);
+                        }
                         const uint64_t bd = x_desc0 + xs * XP;
                         // a chunk starts from zero accumulators without a TMEM clear: 0 . X (A = the zero
                         // operand in TMEM, N = S_x RT columns per MMA) sets acc_S_x..acc_{NACC-1} (S_x = 4: one
@@ -360,9 +468,11 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                         const bool first = kb == c * CKB && r == 0;
                         if (first && !ghost) {
 #pragma unroll
-                            for (uint32_t z = SX; z < Cfg::NACC; z += SX)
-                                mma_i8_ts_w(tmem + (z < Cfg::NACC - SX ? z : Cfg::NACC - SX) * RT, tmem + Cfg::ZCOL, bd,
-                                            idesc, 0u);
+                            for (uint32_t z = SX; z < Cfg::NACC; z += SX) {
+                                const uint32_t d = tmem + (z < Cfg::NACC - SX ? z : Cfg::NACC - SX) * RT;
+                                if constexpr (P2) mma2_i8_ts_w(d, tmem + Cfg::ZCOL, bd, idesc, 0u);
+                                else mma_i8_ts_w(d, tmem + Cfg::ZCOL, bd, idesc, 0u);
+                            }
                         }
 #pragma unroll
                         for (uint32_t jp = 0; jp < kSW; jp++, ie++) {
@@ -377,17 +487,21 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                             const uint64_t ad = e_desc0 + es * EP;
                             if (!ghost) {
 #pragma unroll
-                                for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++)
-                                    mma_i8_ss_w(tmem + jp * RT, ad + 2 * kk, bd + 2 * kk, idesc,
-                                                (first && jp == 0 && kk == 0) ? 0u : 1u);
+                                for (uint32_t kk = 0; kk < Cfg::BK / 32; kk++) {
+                                    const uint32_t acc = (first && jp == 0 && kk == 0) ? 0u : 1u;
+                                    if constexpr (P2) mma2_i8_ss_w(tmem + jp * RT, ad + 2 * kk, bd + 2 * kk, idesc, acc);
+                                    else mma_i8_ss_w(tmem + jp * RT, ad + 2 * kk, bd + 2 * kk, idesc, acc);
+                                }
                             }
                             // this plane's slot is free (in every CTA of the cluster) once its MMAs retire
-                            if (CL > 1) mma_commit_mc_w(&eempty[es], MASK); else mma_commit_w(&eempty[es]);
+                            if constexpr (P2) mma2_commit_w(&eempty[es]);
+                            else if (CL > 1) mma_commit_mc_w(&eempty[es], MASK);
+                            else mma_commit_w(&eempty[es]);
                         }
-                        mma_commit_w(&xempty[xs]);
+                        if constexpr (P2) mma2_commit_w(&xempty[xs]); else mma_commit_w(&xempty[xs]);
                     }
                 }
-                mma_commit_w(tfull);
+                if constexpr (P2) mma2_commit_w(tfull); else mma_commit_w(tfull);
             }
         }
     } else if (warp >= 4) {
@@ -405,7 +519,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
+        if (lane == 0) { if (P2 && rank != 0) mbar_arrive_cl(tempty, 0); else mbar_arrive(tempty); }
 
         uint32_t acc[CPT][8];        // running residue of the unit's limb (mod p_limb)
         uint32_t gc = 0, jcur = 0;
@@ -416,7 +530,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                 if (CL > 1 && rank != 0) mbar_arrive_cl(&qempty[i % kPkQ], 0); else mbar_arrive(&qempty[i % kPkQ]);
             }
             if (u >= total_units) break;
-            const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur);
+            const PkUnit U = pk_decode(P, u, NT, CL, rank, jcur, P2);
             const PkJob& J = P.job[U.j];
             const bool ghost = U.tt >= J.TT;
             const uint32_t Jc = U.T * Cfg::BM + sub * 32 + lane;         // output coefficient
@@ -485,7 +599,9 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(tempty);     // the MMA issuer may start the next chunk
+                if (lane == 0) {                        // the MMA issuer may start the next chunk
+                    if (P2 && rank != 0) mbar_arrive_cl(tempty, 0); else mbar_arrive(tempty);
+                }
                 PKS_ADD(4, t_dr);
             }
             if (ghost) continue;
@@ -599,7 +715,7 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
     if (CL > 1) cluster_sync(); else __syncthreads();   // no CTA leaves while a peer may still multicast into it
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        if constexpr (P2) tmem_dealloc2(tmem, 512); else tmem_dealloc(tmem, 512);
     }
 }
 
@@ -759,6 +875,21 @@ bool packed_ok(const nimbus_ctx* c, const nimbus_encw* w, uint32_t kq, uint32_t 
 static const uint32_t kPkRT4[4] = {48, 52, 56, 64};
 static const uint32_t kPkRT2[2] = {64, 72};
 
+// CTA pairs with cta_group::2 MMAs (PkCfg, P2) for a job list -- opt-in, NIMBUS_PK_PAIR=1: S_x = 4,
+// every job's shift n / 128 even (the pair's two J tiles then agree on which shift terms wrap, so
+// they share the X operand), an even number of J tiles, no NIMBUS_PK_CL.  Measured at C5 (B200,
+// sw_power_cap, same box): 90.9-91.3 ms at 1410-1429 MHz vs 90.3 ms at 1444 MHz for the multicast
+// pairs (RT = 52 both) -- ~2% fewer cycles per pass, but the pair form reads every Enc(W) plane
+// from L2 once per CTA (no theta-tile multicast), and under the board's power cap that energy costs
+// the clock the halved smem operand reads win back.
+static bool pk_pair_ok(const nimbus_ctx* c, const PkHostJob* jobs, uint32_t count) {
+    const char* on = getenv("NIMBUS_PK_PAIR");
+    if (!(on && atoi(on) == 1) || getenv("NIMBUS_PK_CL") || pk_sx(c) != 4 || (c->rns.N / kBNW) % 2) return false;
+    for (uint32_t j = 0; j < count; j++)
+        if ((jobs[j].w->n / kBNW) % 2) return false;
+    return count > 0;
+}
+
 void packed_rt_candidates(const nimbus_ctx* c, const uint32_t** rts, uint32_t* n) {
     if (pk_sx(c) == 2) { *rts = kPkRT2; *n = 2; } else { *rts = kPkRT4; *n = 4; }
 }
@@ -841,16 +972,16 @@ static uint32_t pk_cluster(uint32_t sx) {
     return v == 1 || v == 4 ? (uint32_t)v : 2u;
 }
 
-template <int SX, int RT, int CL>
+template <int SX, int RT, int CL, bool P2 = false>
 static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
                                 void (*mark)(nimbus_ctx*, cudaStream_t)) {
-    using Cfg = PkCfg<SX, RT>;
+    using Cfg = PkCfg<SX, RT, P2>;
     std::unique_ptr<PkParams> Pp(new PkParams());     // kernel parameters (copied at launch)
     PkParams& P = *Pp;
-    cudaError_t e = ensure_smem(c, k_cop_pk<SX, RT, CL>, Cfg::SMEM);
+    cudaError_t e = ensure_smem(c, k_cop_pk<SX, RT, CL, P2>, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     static uint32_t ncl = 0;                          // one per instantiation
-    if (!ncl) ncl = max_clusters(c, k_cop_pk<SX, RT, CL>, CL, Cfg::SMEM, Cfg::THREADS);
+    if (!ncl) ncl = max_clusters(c, k_cop_pk<SX, RT, CL, P2>, CL, Cfg::SMEM, Cfg::THREADS);
     const uint32_t NT = c->rns.N / kBNW, ND = c->rns.L - c->rns.L_out;
     for (uint32_t base = 0; base < count; base += kPkMaxJobs) {
         const uint32_t nj = count - base < kPkMaxJobs ? count - base : kPkMaxJobs;
@@ -874,7 +1005,8 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
             J.rho = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp);
             J.flags = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp + b.rho);
             J.nflags = ND * 2 * J.TT * NT;
-            units += c->rns.L * 2 * ((J.TT + CL - 1) / CL) * NT;    // cluster units
+            units += P2 ? c->rns.L * 2 * J.TT * (NT / 2)               // pair units: J tile pairs
+                        : c->rns.L * 2 * ((J.TT + CL - 1) / CL) * NT;  // cluster units: theta tile groups
             J.unit_end = units;
             const uint32_t items = 2 * J.Rr * J.TT * RT * J.KB * 8;
             blocks += ((items > J.nflags ? items : J.nflags) + 255) / 256;
@@ -904,7 +1036,7 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
         attr[1].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 2;
-        e = cudaLaunchKernelEx(&cfg, k_cop_pk<SX, RT, CL>, c->rns, P, units);
+        e = cudaLaunchKernelEx(&cfg, k_cop_pk<SX, RT, CL, P2>, c->rns, P, units);
         c->launches++;
         {   // the contraction writes the jobs' ciphertexts and R, and triggers its dependents early
             std::vector<const void*> op;
@@ -918,7 +1050,8 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
             }
             pdl_outputs_set(st, op.data(), ob.data(), (uint32_t)op.size());
         }
-        snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_pk<%d, %d, %d>", SX, RT, CL);
+        snprintf(c->last_contraction, sizeof(c->last_contraction), P2 ? "k_cop_pk<%d, %d, %d, P2>" : "k_cop_pk<%d, %d, %d>",
+                 SX, RT, CL);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -938,6 +1071,13 @@ cudaError_t launch_cop_packed(nimbus_ctx* c, const PkHostJob* jobs, uint32_t cou
     if (pk_sx(c) == 2) {
         if (rt == 72) return launch_pk_cl<2, 72>(c, jobs, count, d_ctr, st, mark);
         if (rt == 64) return launch_pk_cl<2, 64>(c, jobs, count, d_ctr, st, mark);
+        return cudaErrorInvalidValue;
+    }
+    if (pk_pair_ok(c, jobs, count)) {
+        if (rt == 52) return launch_pk_rt<4, 52, 2, true>(c, jobs, count, d_ctr, st, mark);
+        if (rt == 56) return launch_pk_rt<4, 56, 2, true>(c, jobs, count, d_ctr, st, mark);
+        if (rt == 48) return launch_pk_rt<4, 48, 2, true>(c, jobs, count, d_ctr, st, mark);
+        if (rt == 64) return launch_pk_rt<4, 64, 2, true>(c, jobs, count, d_ctr, st, mark);
         return cudaErrorInvalidValue;
     }
     if (rt == 48) return launch_pk_cl<4, 48>(c, jobs, count, d_ctr, st, mark);

@@ -446,6 +446,9 @@ def test_packed_parity(nb, oracle, monkeypatch, N, L, ell, L_out, m, n, kq, nq):
     import os
     if not os.environ.get("NIMBUS_NO_PACKED"):                # switch soaks run the unpacked path here
         assert nb.nimbus_launch_count(c.ctx) - before == 2, "packed path not taken"
+        pair = ell > 16 and (n // 128) % 2 == 0 and (N // 128) % 2 == 0 and os.environ.get("NIMBUS_PK_PAIR") == "1"
+        if not os.environ.get("NIMBUS_PK_CL"):
+            assert ("P2" in nb.nimbus_last_contraction(c.ctx)) == pair, nb.nimbus_last_contraction(c.ctx)
     cts_o, R_o = c.oracle_out()
     assert (u32(cts) == cts_o).all(), "output ciphertexts differ"
     assert (u32(R) == R_o).all(), "client share R differs"
@@ -459,10 +462,29 @@ def test_packed_parity(nb, oracle, monkeypatch, N, L, ell, L_out, m, n, kq, nq):
     assert torch.equal(cts, cts2) and torch.equal(R, R2)
 
 
-@pytest.mark.parametrize("ell,L_out", [(32, 2), (16, 1)])
-def test_packed_batch_parity(nb, oracle, ell, L_out):
+@pytest.mark.parametrize("rt", ["48", "52", "56", "64"])
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [c for c in PACKED_CASES if c[2] > 16 and (c[5] // 128) % 2 == 0])
+def test_packed_pair_parity(nb, oracle, monkeypatch, rt, N, L, ell, L_out, m, n, kq, nq):
+    """The opt-in CTA-pair form of the packed contraction (NIMBUS_PK_PAIR=1: tcgen05 cta_group::2,
+    M = 256 over two J tiles, the X block split between the pair) is bit-exact vs the oracle, at
+    every theta-tile height (N = S_x RT = 192 / 208 / 224 / 256)."""
+    monkeypatch.setenv("NIMBUS_PK_PAIR", "1")
+    monkeypatch.setenv("NIMBUS_PK_RT", rt)
+    c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=7100 + N + m + n, flags=nb.FLAG_LARGE_K)
+    cts, R = c.run()
+    assert f"{rt}, 2, P2" in nb.nimbus_last_contraction(c.ctx)
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+    c.check_decrypt(cts, R)
+
+
+@pytest.mark.parametrize("ell,L_out,pair", [(32, 2, 0), (16, 1, 0), (32, 2, 1)])
+def test_packed_batch_parity(nb, oracle, monkeypatch, ell, L_out, pair):
     """A C5-like job list (Q/up/down shapes at a small N) as ONE packed slice launch
-    and ONE packed contraction launch: every job bit-exact vs the oracle (S_x = 4 and 2)."""
+    and ONE packed contraction launch: every job bit-exact vs the oracle (S_x = 4 and 2,
+    and the opt-in CTA-pair form)."""
+    if pair:
+        monkeypatch.setenv("NIMBUS_PK_PAIR", "1")
     N, L = 2048, 3
     ctx = nb.nimbus_ctx_create(N, L, ell, L_out, flags=nb.FLAG_LARGE_K)
     pr = np.array(nb.nimbus_ctx_primes(ctx), np.uint32)
