@@ -63,12 +63,14 @@ struct PkJob {
     uint32_t* flags;          // [drop][comp][theta tile][J tile]: rho written
     uint64_t key;             // prg_key(mask_seed, 6)
     uint32_t m, KB, Rr, n, kq, nct, ntheta, TT, CKB, NCH, nflags;
+    uint32_t ws, wc;          // unit order: shift in tiles (n / 128 mod NT) and its cycle length; wc = 0: T fastest
     uint32_t unit_end;        // contraction: prefix end of this job's units
     uint32_t blk_end;         // slice kernel: prefix end of this job's blocks
 };
 struct PkParams {
     uint32_t njobs;
     uint32_t* ctr;            // unit dispatch counter (zeroed by the slice kernel)
+    uint32_t epol;            // L2 policy of the Enc(W) copies: 0 evict_last, 1 evict_normal, 2 evict_first
     PkJob job[kPkMaxJobs];
 };
 
@@ -184,6 +186,17 @@ __device__ __forceinline__ PkUnit pk_decode(const PkParams& P, uint32_t u, uint3
         return x;
     }
     const uint32_t G = (P.job[j].TT + CL - 1) / CL;
+    if (const uint32_t wc = P.job[j].wc) {
+        // theta groups fastest, then the J tiles in shift order: position i of the walk is tile
+        // (i mod wc) ws + i / wc, so a unit's R shifted Enc(W) tiles (T - r ws) are the R walk positions
+        // before its own and the units in flight read a window of the slab instead of all of it
+        x.tt = (v % G) * CL + rank; v /= G;
+        const uint32_t i = v % NT; v /= NT;
+        x.T = ((i % wc) * P.job[j].ws + i / wc) % NT;
+        x.comp = v & 1;
+        x.pass = v >> 1;
+        return x;
+    }
     x.T = v % NT; v /= NT;
     x.tt = (v % G) * CL + rank; v /= G;
     x.comp = v & 1;
@@ -328,7 +341,9 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
         if (lane == 0) {
             // ---------------- producer: per (kb, r) the X slices of this CTA's theta tile and the 4 byte
             // planes of one Enc(W) block (plane jp fetched by CTA jp % CL, multicast to the cluster)
-            const uint64_t pol_e = policy_evict_last();    // an Enc(W) block serves R output tiles x theta tiles
+            // an Enc(W) block serves R output tiles x theta tiles: in the walk order (PkJob::wc) within a few
+            // k-steps of one another, so it needs no protection and leaves the evict_last lines to X
+            const uint64_t pol_e = P.epol == 0 ? policy_evict_last() : P.epol == 1 ? policy_evict_normal() : policy_evict_first();
             const uint64_t pol_x = policy_evict_last();    // X blocks serve every J tile
             pdl_wait();                                    // X slices, counter and flags: the slice kernel's
             uint32_t ie = 0, ix = 0, jcur = 0;
@@ -972,6 +987,14 @@ static uint32_t pk_cluster(uint32_t sx) {
     return v == 1 || v == 4 ? (uint32_t)v : 2u;
 }
 
+// unit order within a (pass, component) group: the J tiles walked in shift order with the theta groups
+// fastest (pk_decode).  C5 on B200: DRAM reads 39.9 -> 29.8 GB per pass (2.1x -> 1.65x the SURVEY 8(d)
+// bytes), 89.1-89.4 -> 88.5-88.7 ms.  NIMBUS_PK_ORDER=0 keeps T fastest (the order before).
+static bool pk_walk_order() {
+    const char* e = getenv("NIMBUS_PK_ORDER");
+    return !e || atoi(e) != 0;
+}
+
 template <int SX, int RT, int CL, bool P2 = false>
 static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t count, uint32_t* d_ctr, cudaStream_t st,
                                 void (*mark)(nimbus_ctx*, cudaStream_t)) {
@@ -988,6 +1011,10 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
         memset(&P, 0, sizeof(P));
         P.njobs = nj;
         P.ctr = d_ctr;
+        {
+            const char* ep = getenv("NIMBUS_PK_EPOL");
+            P.epol = ep ? (uint32_t)atoi(ep) : 0u;
+        }
         uint32_t units = 0, blocks = 0;
         for (uint32_t i = 0; i < nj; i++) {
             const PkHostJob& h = jobs[base + i];
@@ -1005,6 +1032,12 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
             J.rho = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp);
             J.flags = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(h.d_Xp) + b.xp + b.rho);
             J.nflags = ND * 2 * J.TT * NT;
+            if (!P2 && pk_walk_order()) {
+                J.ws = (w->n / kBNW) % NT;
+                uint32_t a = J.ws, b = NT;
+                while (a) { const uint32_t t = b % a; b = a; a = t; }     // b = gcd(ws, NT) (NT if ws = 0)
+                J.wc = NT / b;
+            }
             units += P2 ? c->rns.L * 2 * J.TT * (NT / 2)               // pair units: J tile pairs
                         : c->rns.L * 2 * ((J.TT + CL - 1) / CL) * NT;  // cluster units: theta tile groups
             J.unit_end = units;

@@ -462,6 +462,21 @@ def test_packed_parity(nb, oracle, monkeypatch, N, L, ell, L_out, m, n, kq, nq):
     assert torch.equal(cts, cts2) and torch.equal(R, R2)
 
 
+@pytest.mark.parametrize("order,epol", [("0", "0"), ("1", "1"), ("1", "2")])
+@pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [PACKED_CASES[i] for i in (1, 3, 4, 6, 9, 13)])
+def test_packed_unit_order_parity(nb, oracle, monkeypatch, order, epol, N, L, ell, L_out, m, n, kq, nq):
+    """The packed contraction's unit order (NIMBUS_PK_ORDER: 1 = theta groups fastest and the J tiles
+    walked in shift order, the default; 0 = J tiles fastest) and the L2 policy of its Enc(W) copies
+    (NIMBUS_PK_EPOL) change which CTA computes which tile and when, never a byte of the output."""
+    monkeypatch.setenv("NIMBUS_PK_ORDER", order)
+    monkeypatch.setenv("NIMBUS_PK_EPOL", epol)
+    c = Case(nb, oracle, N, L, ell, L_out, m, n, kq, nq, seed=7200 + N + m + n, flags=nb.FLAG_LARGE_K)
+    cts, R = c.run()
+    cts_o, R_o = c.oracle_out()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+    c.check_decrypt(cts, R)
+
+
 @pytest.mark.parametrize("rt", ["48", "52", "56", "64"])
 @pytest.mark.parametrize("N,L,ell,L_out,m,n,kq,nq", [c for c in PACKED_CASES if c[2] > 16 and (c[5] // 128) % 2 == 0])
 def test_packed_pair_parity(nb, oracle, monkeypatch, rt, N, L, ell, L_out, m, n, kq, nq):

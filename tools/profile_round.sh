@@ -7,7 +7,7 @@ set -u
 tag=$1; shift
 mkdir -p gpurun_out
 for c in "$@"; do
-  case $c in 5|5l64) args="--config $c --steps 1 --warmup 1";; *) args="--config $c --steps 5 --warmup 3";; esac
+  case $c in 5|5l64|5l16) args="--config $c --steps 1 --warmup 1";; *) args="--config $c --steps 5 --warmup 3";; esac
   name=C$c
   common="--no-cpu-baseline --no-e2e --no-graph"
   timeout 900 python bench.py $args $common --no-stage-profile > gpurun_out/${name}_plain.json 2> gpurun_out/${name}_plain.err \
