@@ -71,6 +71,10 @@ struct PkParams {
     uint32_t njobs;
     uint32_t* ctr;            // unit dispatch counter (zeroed by the slice kernel)
     uint32_t epol;            // L2 policy of the Enc(W) copies: 0 evict_last, 1 evict_normal, 2 evict_first
+#ifdef NIMBUS_PK_DIAG
+    uint32_t diag;            // diagnostic build only (wrong results): 1 every X copy reads the job's first block,
+                              // 2 every Enc(W) copy the slab's first tile -- what each stream costs in DRAM bytes
+#endif
     PkJob job[kPkMaxJobs];
 };
 
@@ -383,13 +387,18 @@ k_cop_pk(const __grid_constant__ Rns R, const __grid_constant__ PkParams P, uint
                             } else {
                                 // (P2: this CTA's half of the block; the pair's wrap agrees, n / 128 even)
                                 mbar_arrive_expect_tx(&xfull[s], Cfg::XB);
-                                bulk_g2s(smem + Cfg::OFF_X + s * Cfg::XB,
-                                         J.Xp + ((((size_t)(2 * r + (wrap ? 1 : 0)) * J.TT + U.tt) * J.KB + kb) *
-                                                 Cfg::B_BYTES) + (P2 ? rank * Cfg::XB : 0u),
-                                         Cfg::XB, &xfull[s], pol_x);
+                                size_t xo = ((((size_t)(2 * r + (wrap ? 1 : 0)) * J.TT + U.tt) * J.KB + kb) * Cfg::B_BYTES) +
+                                            (P2 ? rank * Cfg::XB : 0u);
+#ifdef NIMBUS_PK_DIAG
+                                if (P.diag == 1) xo = 0;
+#endif
+                                bulk_g2s(smem + Cfg::OFF_X + s * Cfg::XB, J.Xp + xo, Cfg::XB, &xfull[s], pol_x);
                             }
                         }
                         const uint8_t* eb = J.Et + ((slab + srcT) * J.KB + kb) * Cfg::A_BYTES;
+#ifdef NIMBUS_PK_DIAG
+                        if (P.diag == 2) eb = J.Et + (slab * J.KB + kb) * Cfg::A_BYTES;
+#endif
                         for (uint32_t jp = 0; jp < kSW; jp++, ie++) {   // the 4 byte planes of the Enc(W) block
                             const uint32_t s = ie % Cfg::ESLOTS, ph = (ie / Cfg::ESLOTS) & 1;
                             // the slot is free in every CTA of the cluster (CL commits)
@@ -1014,6 +1023,10 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
         {
             const char* ep = getenv("NIMBUS_PK_EPOL");
             P.epol = ep ? (uint32_t)atoi(ep) : 0u;
+#ifdef NIMBUS_PK_DIAG
+            const char* dg = getenv("NIMBUS_PK_DIAG");
+            P.diag = dg ? (uint32_t)atoi(dg) : 0u;
+#endif
         }
         uint32_t units = 0, blocks = 0;
         for (uint32_t i = 0; i < nj; i++) {
