@@ -708,6 +708,10 @@ def make_line(args, cfg, res, world, steps, warmup, cpu):
                         if prim["bound"] == "tensor" else f"{peaks['src']} hbm_gbs")
     prim["units_per_launch"] = ({"int8_ops": ops} if prim["bound"] == "tensor" else
                                 {"bytes": hbm_bytes, "bytes_def": "|Enc(W)| + |X| + |compact cts| + |R| (SURVEY.md §8(d))"})
+    step_units = (ops if prim["bound"] == "tensor" else hbm_bytes) * launches_step
+    step_ach = step_units / (ms_step / 1e3) / (1e12 if prim["bound"] == "tensor" else 1e9)
+    step_roof = {"bound": prim["bound"], "achieved": step_ach, "peak": prim["peak"], "unit": prim["unit"],
+                 "frac": step_ach / prim["peak"], "ms": ms_step}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -716,6 +720,9 @@ def make_line(args, cfg, res, world, steps, warmup, cpu):
         "impl": args.impl, "l2": res["l2_desc"], "enc_w_bytes_resident": res["enc_bytes"],
         "roofline": prim,
         "roofline_other": alt,
+        # the whole step against the same ceiling: the step's units over ms_per_step of the timed pass
+        # (all kernels of the step, PDL-chained, no event between them), not one bracketed launch
+        "roofline_step": step_roof,
         "roofline_i8_floor": (None if floor is None else
                               {"achieved": tens["achieved"], "peak": floor, "unit": "TFLOP/s",
                                "frac": tens["achieved"] / floor, "peak_src": fsrc}),

@@ -1111,13 +1111,18 @@ def _fuzz_cases(count=None, seed=None):
     return out
 
 
-def _fuzz_cases_large_k(count=16, seed=31337):
+def _fuzz_cases_large_k(count=None, seed=None):
     """Seeded shapes for the NIMBUS_FLAG_LARGE_K layout (128-column tiles) at ell in (8, 32]:
-    half of them with n a multiple of 128 and enough rows for the packed contraction."""
+    half of them with n a multiple of 128 and enough rows for the packed contraction.
+    16 cases by default; NIMBUS_FUZZ_LK_CASES=<count> (and NIMBUS_FUZZ_LK_SEED) for a soak,
+    which also draws N = 4096."""
+    import os
+    count = int(os.environ.get("NIMBUS_FUZZ_LK_CASES", "16")) if count is None else count
+    seed = int(os.environ.get("NIMBUS_FUZZ_LK_SEED", "31337")) if seed is None else seed
     rng = np.random.default_rng(seed)
     out = []
     for i in range(count):
-        N = int(rng.choice([256, 512, 1024, 2048]))
+        N = int(rng.choice([256, 512, 1024, 2048] + ([4096] if count > 16 else [])))
         ell = int(rng.choice([12, 16, 24, 32]))
         L, L_out = (3, 1) if ell <= 16 else (3, 2)
         if i % 2 == 0:
