@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--impl", default="tcgen05", choices=["tcgen05", "cudacore", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--prefetch-next", type=int, default=1, choices=[0, 1],
+                    help="k = 128 configs: hint the next step's Enc(W) to the library (nimbus_cop_prefetch_next)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="skip the secondary timing of the steps replayed from a CUDA graph")
     ap.add_argument("--cpu-budget-s", type=float, default=8.0,
@@ -303,6 +305,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     def step_on(st):
         c = step_no[0] % n_copies
+        if args.prefetch_next and cfg.ell <= 16 and max(l.k for _, _, l in cfg.layers) <= 128:
+            # the model's next matmul (here: the next step's copy) is known: its first Enc(W) tiles
+            # are prefetched towards L2 by this step's contraction once its own copies are issued
+            nb.nimbus_cop_prefetch_next(ctx, mats[0]["encw"][(c + 1) % n_copies])
         if ws_batch is not None:
             batch(ctx, jobs[c], ws_batch, stream=st)
             return
@@ -514,6 +520,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
     l2_desc = (f"cold: {n_copies} rotating copies of Enc(W)+X ({n_copies * enc_bytes >> 20} MiB >= 3x the "
                f"{l2_bytes >> 20} MiB L2), step i reads copy i mod {n_copies}" if args.l2 == "rotate" else
                f"flushed by a {L2_FLUSH_BYTES >> 20} MiB write before every timed step")
+    if args.prefetch_next and cfg.ell <= 16 and max(l.k for _, _, l in cfg.layers) <= 128:
+        l2_desc += ("; nimbus_cop_prefetch_next names the next step's Enc(W) copy: each contraction CTA prefetches the next "
+                    "launch's first two tiles (28 of 50 MB) into L2 after its own last copy is issued (--prefetch-next 0: off)")
     return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=stage_ms, calls=calls, launches=launches, graph_ms=graph_ms,
                 kernel=kernel,
                 clocks=clk, t_setup=t_setup, enc_bytes=enc_bytes, e2e=e2e, l2_desc=l2_desc, warm_ms=warm_ms,

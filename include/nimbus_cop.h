@@ -426,6 +426,19 @@ nimbus_status nimbus_prg_words(uint64_t seed, uint32_t dom, uint64_t start, uint
  * (PAPER.md:606, 180).  d_a, d_b, d_c: count x L x N uint32. */
 nimbus_status nimbus_negacyclic_mul(nimbus_ctx* ctx, const uint32_t* d_a, const uint32_t* d_b,
                                     uint32_t count, uint32_t* d_c, void* stream);
+/* Software pipelining across calls: names the Enc(W) of the matmul that will FOLLOW the next
+ * nimbus_cop_matmul / nimbus_cop_matmul_batch call on this context (a model's layer order is
+ * static; the weights are the asynchronously loaded operand of PAPER.md:312-317).  When that next
+ * call runs the resident-X contraction (k <= 128, ell <= 16), each of its CTAs, once its own last
+ * Enc(W) copy is issued, prefetches into L2 the first two tiles of the same CTA of the following
+ * contraction, so that launch does not start with a cold DRAM round trip.  The job-list calls
+ * (nimbus_cop_matmul_batch, nimbus_cop_matmul_host_batch) do this themselves between consecutive
+ * units of a list; a hint set before them names what follows the list's last unit.  A hint only:
+ * never changes a result, one-shot (consumed by the next contraction launch, ignored by the other
+ * kernels), `next` stays owned by the caller and must be resident and alive until that launch has
+ * run (destroying it first drops the hint).  next = NULL clears a pending hint.  Returns
+ * NIMBUS_EINVAL for a null ctx or an Enc(W) of another context. */
+nimbus_status nimbus_cop_prefetch_next(nimbus_ctx* ctx, const nimbus_encw* next);
 /* Number of library kernels launched through this context since creation. */
 uint64_t nimbus_launch_count(const nimbus_ctx* ctx);
 /* Name of the last contraction kernel the context launched ("k_cop_pk<4, 52>", "k_cop_tc_res<true>",

@@ -274,6 +274,12 @@ uint64_t nimbus_launch_count(const nimbus_ctx* ctx) { return ctx ? ctx->launches
 
 const char* nimbus_last_contraction(const nimbus_ctx* ctx) { return ctx ? ctx->last_contraction : ""; }
 
+nimbus_status nimbus_cop_prefetch_next(nimbus_ctx* ctx, const nimbus_encw* next) {
+    if (!ctx || (next && next->ctx != ctx)) return NIMBUS_EINVAL;
+    ctx->pf_next = next;
+    return NIMBUS_OK;
+}
+
 nimbus_status nimbus_sync(nimbus_ctx* ctx, void* stream) {
     DevGuard dg_(ctx, __func__);
     if (!ctx) return NIMBUS_EINVAL;
@@ -524,6 +530,7 @@ void nimbus_encw_destroy(nimbus_encw* w) {
     if (w->d_corr) cudaFree(w->d_corr);
     if (w->h_Et) cudaFreeHost(w->h_Et);
     nimbus_ctx* ctx = w->ctx;
+    if (ctx && ctx->pf_next == w) ctx->pf_next = nullptr;     // a pending prefetch hint must not outlive its Enc(W)
     delete w;
     ctx_release(ctx);
 }
@@ -1163,10 +1170,12 @@ static nimbus_status cop_matmul_batch(nimbus_ctx* ctx, const nimbus_cop_job* job
     // the side stream must not start before earlier work on `stream`
     CK(cudaEventRecord(start, a), "record");
     CK(cudaStreamWaitEvent(b, start, 0), "wait");
+    const nimbus_encw* after = ctx->pf_next;               // the caller's hint: what follows the list
     for (uint32_t i = 0; i < count; i++) {
         const nimbus_cop_job& J = jobs[i];
         const uint32_t k = J.k_per_query * J.n_queries;
         const uint32_t g = same_x_group(ctx, jobs, count, i);
+        ctx->pf_next = i + g < count ? jobs[i + g].encw : after;   // the list names each unit's successor
         if (g > 1) {
             // one slice of the shared X, one contraction over the group's Enc(W)s into C buffers
             // 0..g-1, one pack launch, all on `stream` (PDL-chained); earlier packs on the side
@@ -1594,11 +1603,13 @@ static nimbus_status cop_matmul_host_batch(nimbus_ctx* ctx, const nimbus_cop_hos
     };
     uint32_t g = same_hx_group(ctx, jobs, count, 0);
     nimbus_status st = prepare(0, g);
+    const nimbus_encw* after = ctx->pf_next;               // the caller's hint: what follows the list
     for (uint32_t i = 0; i < count && st == NIMBUS_OK; i += g) {
         g = same_hx_group(ctx, jobs, count, i);
         const nimbus_cop_host_job& J = jobs[i];
         const uint32_t k = J.k_per_query * J.n_queries;
         uint8_t* slot = slot_of(i);
+        ctx->pf_next = i + g < count ? jobs[i + g].encw : after;   // the list names each unit's successor
         // the next unit's prerequisites go into `stream` BEFORE this unit's kernels, so that its
         // pack and the next unit's slice stay adjacent (programmatic dependent launch across jobs)
         if (i + g < count) {

@@ -1010,6 +1010,7 @@ static cudaError_t launch_pk_rt(nimbus_ctx* c, const PkHostJob* jobs, uint32_t c
     using Cfg = PkCfg<SX, RT, P2>;
     std::unique_ptr<PkParams> Pp(new PkParams());     // kernel parameters (copied at launch)
     PkParams& P = *Pp;
+    c->pf_next = nullptr;                             // a prefetch hint is for a resident-X launch only
     cudaError_t e = ensure_smem(c, k_cop_pk<SX, RT, CL, P2>, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     static uint32_t ncl = 0;                          // one per instantiation

@@ -554,7 +554,7 @@ __device__ __forceinline__ uint32_t res_slot(uint32_t it, uint32_t KP) {
 template <bool FUSE>
 __global__ void __launch_bounds__(ResCfg::THREADS, 1)
 k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, uint32_t CT,
-             uint32_t KB, uint32_t ncol, FuseOut fo) {
+             uint32_t KB, uint32_t ncol, FuseOut fo, ResPf pf) {
     using Cfg = ResCfg;
     const TileSeq<FUSE> tiles(FUSE ? CT : CT * jobs.nj, R.N, Cfg::BN);
     extern __shared__ uint8_t smem_raw[];
@@ -651,6 +651,20 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
                     if (ti == 1 && kp < 8) TRACE(52 + kp);
                     mbar_arrive_expect_tx(&full[s], nkb * Cfg::B_BYTES);
                     bulk_g2s(slot_ptr(s), b_src + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[s], pol_b);
+                }
+            }
+            // all of this CTA's copies are issued: pull the tile that CTA blockIdx.x of the next
+            // contraction starts with towards L2 (nimbus_cop_prefetch_next; a hint, no completion)
+            if (pf.base != nullptr && blockIdx.x < pf.grid) {
+                const uint32_t b = blockIdx.x;
+                for (uint32_t ti = 0; ti < pf.count; ti++) {          // that CTA's tiles.at(ti)
+                    const uint32_t pair = b + (ti >> 1) * pf.grid;
+                    const uint32_t t = pf.fuse ? (pair / pf.NT) * 2 * pf.NT + (ti & 1) * pf.NT + pair % pf.NT
+                                               : b + ti * pf.grid;
+                    if (t >= pf.ntiles) break;
+                    const uint8_t* p = pf.base + (size_t)t * pf.tile_bytes;
+                    for (uint32_t off = 0; off < pf.tile_bytes; off += Cfg::SLOT)
+                        prefetch_l2_bulk(p + off, min(Cfg::SLOT, pf.tile_bytes - off));
                 }
             }
         }
@@ -1319,6 +1333,26 @@ static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t
     return launch_res_jobs(c, J, w->KB, d_Xt, k, st);
 }
 
+// The one-shot hint of nimbus_cop_prefetch_next as the kernel's ResPf: where the next resident-X
+// contraction's CTAs start (the same k assumed; a wrong guess only prefetches tiles that come later).
+static ResPf take_prefetch_hint(nimbus_ctx* c, uint32_t k) {
+    ResPf pf;
+    const nimbus_encw* w = c->pf_next;
+    c->pf_next = nullptr;
+    if (!w || !w->d_Et || !resident_ok(c, w, k)) return pf;
+    const uint32_t CT = col_tiles(c, kBNR);
+    pf.base = (const uint8_t*)w->d_Et;
+    pf.tile_bytes = w->KB * ResCfg::B_BYTES;
+    pf.ntiles = CT;
+    pf.NT = c->rns.N / kBNR;
+    pf.fuse = fused_r1_ok(c, w, k) ? 1u : 0u;
+    const uint32_t units = pf.fuse ? CT / 2 : CT;
+    pf.grid = units < (uint32_t)c->num_sms ? units : (uint32_t)c->num_sms;
+    const char* env = getenv("NIMBUS_PF_TILES");      // tiles per CTA to prefetch (measurement switch)
+    pf.count = env ? (uint32_t)atoi(env) : 2u;      // measured: C3 17.4 -> 17.2 (1) / 16.7 (2, 3) us, C2 20.1 -> 19.6 / 19.3 / 20.6
+    return pf;
+}
+
 // the resident-X contraction over up to 4 matmuls sharing X (same m, ell <= 16, k <= 128)
 cudaError_t launch_res_jobs(nimbus_ctx* c, const ResJobs& J, uint32_t KB, const uint8_t* d_Xt, uint32_t k,
                             cudaStream_t st) {
@@ -1328,7 +1362,7 @@ cudaError_t launch_res_jobs(nimbus_ctx* c, const ResJobs& J, uint32_t KB, const 
     const uint32_t CT = col_tiles(c, kBNR), tiles = CT * J.nj;
     const uint32_t grid = tiles < (uint32_t)c->num_sms ? tiles : (uint32_t)c->num_sms;
     e = launch_pdl(k_cop_tc_res<false>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt, J, k, CT, KB,
-                   ncol, FuseOut{});
+                   ncol, FuseOut{}, take_prefetch_hint(c, k));
     c->launches++;
     snprintf(c->last_contraction, sizeof(c->last_contraction), "k_cop_tc_res<0>");
     return e;
@@ -1356,7 +1390,7 @@ cudaError_t launch_cop_fused_r1(nimbus_ctx* c, const nimbus_encw* w, const uint8
     J.nj = 1;
     J.Et[0] = w->d_Et;
     e = launch_pdl(k_cop_tc_res<true>, dim3(grid), dim3(ResCfg::THREADS), ResCfg::SMEM, st, c->rns, d_Xt, J, k, CT,
-                   w->KB, ncol, fo);
+                   w->KB, ncol, fo, take_prefetch_hint(c, k));
     c->launches++;
     {   // writes the ciphertexts and R, and triggers its dependents early
         const void* op[2] = {d_cts, d_R};
@@ -1405,6 +1439,8 @@ uint32_t transposed_rows(const nimbus_ctx* c) {
 cudaError_t launch_cop_tcgen05(nimbus_ctx* c, const nimbus_encw* w, const uint8_t* d_Xt, uint32_t k,
                                uint32_t* d_C, cudaStream_t st) {
     const uint32_t SX = sx_of(c->rns.ell);
+    if (!(w->bn == kBNR && resident_ok(c, w, k) && c->res_ring != 2))
+        c->pf_next = nullptr;                     // a prefetch hint is for the next launch only
     if (w->bn == kBNW) {
         if (SX == 4) return transposed_rows(c) == 32 ? launch_t<4, 32>(c, w, d_Xt, k, d_C, st)
                                                      : launch_t<4, 64>(c, w, d_Xt, k, d_C, st);

@@ -44,6 +44,7 @@ struct nimbus_ctx {
     int res_ring = 1;              // resident-X contraction: 1 = 3-slot ring + slice 1 in smem, 2 = deep ring (k_cop_tc_res2); env NIMBUS_RES
     int cluster = 1;               // CTAs per cluster of the streaming contraction (2 = X multicast); env NIMBUS_CLUSTER
     bool fuse_r1 = true;           // R = 1 layers: mod-switch + mask in the resident kernel's epilogue; env NIMBUS_NO_FUSE=1 off
+    const nimbus_encw* pf_next = nullptr;   // nimbus_cop_prefetch_next: the Enc(W) of the call after the next one (one-shot hint)
     // stage profiling (nimbus_profile_*): pending event quadruples, accumulated ms
     bool profile = false;
     std::vector<cudaEvent_t> ev_pool, ev_pending;
@@ -135,6 +136,13 @@ struct ResJobs {
     const uint8_t* Et[4] = {nullptr, nullptr, nullptr, nullptr};
     uint32_t* C[4] = {nullptr, nullptr, nullptr, nullptr};
     uint32_t nj = 0;
+};
+
+// First tiles of the NEXT resident-X contraction (nimbus_cop_prefetch_next): CTA b of this launch
+// prefetches into L2 the Enc(W) tile CTA b of that launch starts with, once its own last copies are issued.
+struct ResPf {
+    const uint8_t* base = nullptr;
+    uint32_t tile_bytes = 0, ntiles = 0, NT = 0, fuse = 0, grid = 0, count = 1;
 };
 
 // ---------------------------------------------------------------- launchers

@@ -62,6 +62,7 @@ _SIGS = {
     "nimbus_negacyclic_mul": (C.c_int, [_vp, _vp, _vp, _u32, _vp, _vp]),
     "nimbus_launch_count": (_u64, [_vp]),
     "nimbus_last_contraction": (C.c_char_p, [_vp]),
+    "nimbus_cop_prefetch_next": (C.c_int, [_vp, _vp]),
     "nimbus_cop_workspace_size_batch": (C.c_int, [_vp, _vp, _u32, C.POINTER(_sz)]),
     "nimbus_cop_matmul_batch": (C.c_int, [_vp, _vp, _u32, _vp, _sz, _vp]),
     "nimbus_profile_enable": (C.c_int, [_vp, C.c_int]),
@@ -645,6 +646,11 @@ def nimbus_launch_count(ctx: Context) -> int:
 
 def nimbus_last_contraction(ctx: Context) -> str:
     return lib().nimbus_last_contraction(ctx.ptr).decode()
+
+
+def nimbus_cop_prefetch_next(ctx: Context, nxt=None):
+    """Hint: `nxt` is the Enc(W) of the matmul after the next call (see the header)."""
+    _check(lib().nimbus_cop_prefetch_next(ctx.ptr, nxt.ptr if nxt is not None else None), ctx)
 
 
 def nimbus_profile_enable(ctx: Context, on: bool = True):

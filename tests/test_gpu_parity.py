@@ -413,6 +413,31 @@ def test_c5_layer_matmuls(nb, oracle, ell, proj):
     c.check_decrypt(cts, R)
 
 
+@pytest.mark.parametrize("n,n_next", [(768, 768), (768, 3000), (3000, 768), (3000, 3000), (768, 100)])
+def test_prefetch_next_hint_parity(nb, oracle, n, n_next):
+    """nimbus_cop_prefetch_next (the next matmul's Enc(W), whose first tiles the resident-X
+    contraction prefetches towards L2) never changes a byte: plain and fused R = 1 kernels, the
+    hinted Enc(W) mapped either way, a hint left pending and one whose Enc(W) is destroyed."""
+    c = Case(nb, oracle, 4096, 2, 16, 1, 300, n, 100, seed=0x9F00 + n)
+    W2 = ni.gen_W(77, 300, n_next, 16)
+    nxt = nb.nimbus_encrypt_weights(c.ctx, c.sk, dev_u32(W2), 77)
+    cts_o, R_o = c.oracle_out()
+    for hint in (nxt, c.encw, None):
+        nb.nimbus_cop_prefetch_next(c.ctx, hint)
+        cts, R = c.run()
+        assert "k_cop_tc_res" in nb.nimbus_last_contraction(c.ctx)
+        assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+    c.check_decrypt(cts, R)
+    nb.nimbus_cop_prefetch_next(c.ctx, nxt)     # pending hint, its Enc(W) destroyed before the launch
+    del nxt
+    cts, R = c.run()
+    assert (u32(cts) == cts_o).all() and (u32(R) == R_o).all()
+    other = Case(nb, oracle, 4096, 2, 16, 1, 64, 64, 4, seed=5, oracle_full=False)
+    with pytest.raises(nb.NimbusError) as e:
+        nb.nimbus_cop_prefetch_next(c.ctx, other.encw)       # an Enc(W) of another context
+    assert e.value.status == -1
+
+
 # ------------------------------------------------------------------ packed contraction (cop_pk.cu)
 PACKED_CASES = [
     # N, L, ell, L_out, m, n, kq, nq            R = N/n; theta = nq * ceil(kq/R)
