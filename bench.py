@@ -54,7 +54,9 @@ def parse():
     ap.add_argument("--impl", default="tcgen05", choices=["tcgen05", "cudacore", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--prefetch-next", type=int, default=1, choices=[0, 1],
+    ap.add_argument("--profiler-range", action="store_true",
+                    help="cudaProfilerStart/Stop around the K block-timed steps (ncu --replay-mode range)")
+    ap.add_argument("--prefetch-next", type=int, default=1, choices=[0, 1, 2],
                     help="k = 128 configs: hint the next step's Enc(W) to the library (nimbus_cop_prefetch_next)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="skip the secondary timing of the steps replayed from a CUDA graph")
@@ -308,7 +310,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         if args.prefetch_next and cfg.ell <= 16 and max(l.k for _, _, l in cfg.layers) <= 128:
             # the model's next matmul (here: the next step's copy) is known: its first Enc(W) tiles
             # are prefetched towards L2 by this step's contraction once its own copies are issued
-            nb.nimbus_cop_prefetch_next(ctx, mats[0]["encw"][(c + 1) % n_copies])
+            # (2: a control -- the hint names a copy that is NOT read next, same prefetch traffic, no hits)
+            nxt = (c + 1) % n_copies if args.prefetch_next == 1 else (c + n_copies // 2) % n_copies
+            nb.nimbus_cop_prefetch_next(ctx, mats[0]["encw"][nxt])
         if ws_batch is not None:
             batch(ctx, jobs[c], ws_batch, stream=st)
             return
@@ -349,6 +353,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        ranged = args.profiler_range and not per_step and not profile
+        if ranged:                              # ncu --replay-mode range: the K chained steps as one range
+            torch.cuda.profiler.start()
         if not per_step:
             starts[0].record(stream)
         for i in range(args.steps):
@@ -361,6 +368,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         if not per_step:
             ends[0].record(stream)
         torch.cuda.synchronize()
+        if ranged:
+            torch.cuda.profiler.stop()
         if world > 1:
             torch.distributed.barrier()
         launches = nb.nimbus_launch_count(ctx) - launches0
@@ -710,6 +719,15 @@ def make_line(args, cfg, res, world, steps, warmup, cpu):
     prim["traffic"], src = (ncu_traffic(cfg, kernel) if args.impl == "tcgen05" else (None, None))
     if src:
         prim["traffic_src"] = src
+    # DRAM bytes per step of the chained pass itself (ncu range replay over K block-timed steps,
+    # profiles/range_traffic.json): what the steps move when they run as timed, PDL-overlapped and
+    # with the L2 as the previous step left it -- a --set full capture replays one serialised launch
+    rt_path = os.path.join(ROOT, "profiles", "range_traffic.json")
+    if args.impl == "tcgen05" and os.path.exists(rt_path):
+        ent = json.load(open(rt_path)).get(cfg.name, {}).get(f"prefetch_next={args.prefetch_next}")
+        if ent:
+            prim["traffic_chain"] = ent["dram_bytes_per_step"] / launches_step
+            prim["traffic_chain_src"] = "profiles/range_traffic.json (ncu --replay-mode range over the block-timed steps)"
     prim["kernel"] = kernel
     prim["launch_ms"] = contract_ms
     prim["launches_per_step"] = launches_step

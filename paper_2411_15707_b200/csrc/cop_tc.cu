@@ -615,6 +615,14 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
                                       (nox ? 0u : nkb * Cfg::SLICE + (kp == 0 ? KB * Cfg::SLICE : 0)));
                 bulk_g2s(slot_ptr(kp), e0 + (size_t)kb0 * Cfg::B_BYTES, nkb * Cfg::B_BYTES, &full[kp], pol_b);
             }
+            // own later tiles towards L2 while the kernels before this one finish (their tail and the
+            // pack leave DRAM idle); tiles 0 .. pf.from - 1 were prefetched by the previous contraction
+            for (uint32_t ti = pf.from; ti < pf.from + pf.self && ti < tiles.count; ti++) {
+                const uint32_t tg = tiles.at(ti);
+                const uint8_t* p = jobs.Et[tg / CT] + (size_t)(tg % CT) * KB * Cfg::B_BYTES;
+                for (uint32_t off = 0; off < KB * Cfg::B_BYTES; off += Cfg::SLOT)
+                    prefetch_l2_bulk(p + off, min(Cfg::SLOT, KB * Cfg::B_BYTES - off));
+            }
             pdl_wait();
             TRACE(2);
             if (!nox)
@@ -663,8 +671,12 @@ k_cop_tc_res(Rns R, const uint8_t* __restrict__ Xt, ResJobs jobs, uint32_t k, ui
                                                : b + ti * pf.grid;
                     if (t >= pf.ntiles) break;
                     const uint8_t* p = pf.base + (size_t)t * pf.tile_bytes;
-                    for (uint32_t off = 0; off < pf.tile_bytes; off += Cfg::SLOT)
-                        prefetch_l2_bulk(p + off, min(Cfg::SLOT, pf.tile_bytes - off));
+                    for (uint32_t off = 0; off < pf.tile_bytes; off += Cfg::SLOT) {
+                        const uint32_t nb = min(Cfg::SLOT, pf.tile_bytes - off);
+                        if (pf.pol == 1) prefetch_l2_bulk(p + off, nb, pol_a);                       // evict_last
+                        else if (pf.pol == 2) prefetch_l2_bulk(p + off, nb, policy_evict_normal());
+                        else prefetch_l2_bulk(p + off, nb);
+                    }
                 }
             }
         }
@@ -1337,6 +1349,14 @@ static cudaError_t launch_res(nimbus_ctx* c, const nimbus_encw* w, const uint8_t
 // contraction's CTAs start (the same k assumed; a wrong guess only prefetches tiles that come later).
 static ResPf take_prefetch_hint(nimbus_ctx* c, uint32_t k) {
     ResPf pf;
+    {   // measurement switch: own tiles [from, from + self) prefetched before the PDL wait
+        const char* es = getenv("NIMBUS_PF_SELF");
+        const char* ef = getenv("NIMBUS_PF_FROM");
+        pf.self = es ? (uint32_t)atoi(es) : 0u;
+        pf.from = ef ? (uint32_t)atoi(ef) : 2u;
+        const char* ep = getenv("NIMBUS_PF_POL");     // L2 policy of the next-launch prefetch: 0 none, 1 evict_last, 2 evict_normal
+        pf.pol = ep ? (uint32_t)atoi(ep) : 0u;
+    }
     const nimbus_encw* w = c->pf_next;
     c->pf_next = nullptr;
     if (!w || !w->d_Et || !resident_ok(c, w, k)) return pf;

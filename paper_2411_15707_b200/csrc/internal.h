@@ -143,6 +143,8 @@ struct ResJobs {
 struct ResPf {
     const uint8_t* base = nullptr;
     uint32_t tile_bytes = 0, ntiles = 0, NT = 0, fuse = 0, grid = 0, count = 1;
+    uint32_t self = 0, from = 2;     // own tiles [from, from + self) prefetched before the PDL wait
+    uint32_t pol = 0;                // L2 policy of the prefetch (measurement switch)
 };
 
 // ---------------------------------------------------------------- launchers
