@@ -680,6 +680,8 @@ def ncu_traffic(cfg, kernel):
         return None, None
     cap = json.load(open(path)).get("kernel_capture", {})
     name = (cap.get("kernel") or "").replace("void ", "").split("(")[0].replace("(int)", "").replace(" ", "")
+    if name.startswith("k_cop_pk<"):      # the library prints the CTA-pair flag (4th parameter) as "", ", P2"
+        name = name[:-3] + ">" if name.endswith(",0>") else name[:-3] + ",P2>" if name.endswith(",1>") else name
     if cap.get("dram_traffic_bytes") is None or name != kernel.replace(" ", ""):
         return None, f"profiles/ncu_{cfg.name}.json captured {name or '?'}, not {kernel}"
     return cap["dram_traffic_bytes"], f"profiles/ncu_{cfg.name.replace('@', '')}.json ({name})"
