@@ -9,6 +9,7 @@ C2, C3, ragged multi-tile shapes); at C4/C5 sizes, full Enc(W) comparison plus
 sampled output coefficients from the oracle, plus the exact decryption property
 over every output.
 """
+import os
 import numpy as np
 import pytest
 import torch
@@ -69,6 +70,8 @@ class Case:
         mask_seed = self.seed if mask_seed is None else mask_seed
         ws = nb.alloc_workspace(self.ctx, self.encw, self.k)
         cts, R = nb.alloc_outputs(self.ctx, self.encw, self.kq, self.nq)
+        if os.environ.get("NIMBUS_TEST_HINT"):      # soak switch: every call carries a next-matmul prefetch hint
+            nb.nimbus_cop_prefetch_next(self.ctx, self.encw)
         nb.nimbus_cop_matmul(self.ctx, self.encw, dev_u32(self.X), self.kq, self.nq, mask_seed, cts, R, ws)
         nb.nimbus_sync(self.ctx)
         return cts, R
