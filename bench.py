@@ -812,10 +812,12 @@ def bench_config(args, key, rank, world, local_rank, steps=None, warmup=None, e2
 
 # ----------------------------------------------------------------- main
 MAIN_CONFIG = "5"
-# (config, steps cap) of the per_config block: C2 / C2-QKV / C3 / C4 / C4@l16 at the bench's steps, the
-# C5@l16 pass and the paper's ell = 64 pass at <= 5 steps (a 27 GB Enc(W), ~0.3 s per pass)
-PER_CONFIG = (("2", None), ("2qkv", None), ("3", None), ("4", None), ("4l16", None), ("5l16", 5), ("4l64", None),
-              ("5l64", 5))
+# (config, steps cap, steps floor) of the per_config block: the single-matmul configs (20 us .. 0.6 ms per
+# step) at >= 200 steps -- 20 steps are a few ms, inside one swing of the power-capped clock right after
+# the C5 pass (C4 ran 198-238 us per step that way, 4 runs) -- the C5@l16 pass and the paper's ell = 64
+# pass at <= 5 steps (a 27 GB Enc(W), ~0.3 s per pass).  Each entry states its own steps / warmup.
+PER_CONFIG = (("2", None, 200), ("2qkv", None, 200), ("3", None, 200), ("4", None, 200), ("4l16", None, 200),
+              ("5l16", 5, 0), ("4l64", None, 200), ("5l64", 5, 0))
 
 
 def main():
@@ -838,8 +840,8 @@ def main():
     line = bench_config(args, key, rank, world, local_rank)
     if args.config is None and args.per_config:
         per = {}
-        for k2, cap in PER_CONFIG:
-            st = args.steps if cap is None else min(args.steps, cap)
+        for k2, cap, floor in PER_CONFIG:
+            st = max(args.steps, floor) if cap is None else min(args.steps, cap)
             wu = args.warmup if cap is None else min(args.warmup, 3)
             d = bench_config(args, k2, rank, world, local_rank, steps=st, warmup=wu)
             if d is not None:
